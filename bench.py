@@ -1,0 +1,324 @@
+"""bench.py — encrypted Z-score on B200 (BASELINE.json metric, config C2).
+
+Workload (configs[1]): one CKKS-emulated ciphertext of 2^15 slots holding
+32768 fp64 values ~ N(50, 10^2), seed-drawn; znorm with B = 100 and the
+reference's default inverse-root configuration (Chebyshev degree 511 seed, 6
+Newton iterations, 2 bootstraps), scale 2^-40 quantisation.  A step is one
+znorm of one ciphertext.
+
+  value  device time per ciphertext, inputs already resident in HBM, K steps
+         enqueued back to back through the public API; the inputs cycle through
+         a pool of distinct encrypted columns larger than L2 (config.l2).
+  e2e    the same metric through the public API with HOST buffers: every step
+         encodes from pinned host memory (H2D), runs znorm and decodes the result
+         (D2H), all inside the timed region.
+
+N > 1 (torchrun): replicas only — every rank runs its own ciphertexts, no
+collective on the data path; value = max-over-ranks time /
+ciphertexts processed by all ranks.
+
+--impl reference runs the reference's own CPU implementation (oracle/_ref, the
+unmodified reference headers compiled here; else the oracle port) on all host
+cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "encrypted Z-score ms per 2^15-slot ciphertext"
+UNIT = "ms/ciphertext"
+S = 32768
+B = 100.0
+SEED = 21
+POOL = 640  # 640 x 256 KiB = 160 MiB of distinct inputs > 126 MB L2
+
+
+def workload_config(extra=None):
+    cfg = {"workload": "C2 znorm: 32768 x N(50,10^2) in one 2^15-slot ciphertext, B=100, "
+                       "invsqrt degree 511 + 6 Newton, scale 2^-40",
+           "slots": S, "B": B, "cheb_degree": 511, "newton_iters": 6,
+           "l2": f"inputs > L2: {POOL} distinct resident columns ({POOL * S * 8 // (1 << 20)} MiB) cycled"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---- clocks ----------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.out = self.p.communicate(timeout=5)[0]
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (getattr(self, "out", "") or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---- CPU reference / oracle leg --------------------------------------------------------------------
+def cpu_lib():
+    from oracle_abi import oracle, reference
+    ref = reference()
+    if ref is not None:
+        return ref, "reference"
+    return oracle(), "port"
+
+
+def cpu_znorm_sample(x, threads: int, total: int):
+    """`total` independent znorm runs (one EvalContext each) over `threads` host
+    threads; returns (wall seconds, output of one run)."""
+    from oracle_abi import Params
+    lib, kind = cpu_lib()
+    p = Params(slot_count=S)
+    per = [total // threads + (1 if i < total % threads else 0) for i in range(threads)]
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        futs = [ex.submit(lib.znorm_reps, p, x, B, n) for n in per if n > 0]
+        outs = [f.result() for f in futs]
+    wall = time.perf_counter() - t0
+    assert all(o[0] == 0 for o in outs)
+    return wall, outs[0][1], kind
+
+
+def cpu_baseline(x):
+    threads = os.cpu_count() or 1
+    total = max(threads, 40)  # ~40 znorms x ~0.25 s = ~10 s of CPU work
+    wall, out, kind = cpu_znorm_sample(x, threads, total)
+    t1, _, _ = cpu_znorm_sample(x, 1, 1)
+    return {"value": 1e3 * wall / total, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{total} independent C2 znorm runs (one EvalContext each) on {threads} host threads",
+            "latency_1core_ms": 1e3 * t1}, out
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2508_12093_b200 import workloads as W
+    from oracle_abi import oracle
+    x = W.normal(oracle().synthetic_uniform, SEED, S, 50.0, 10.0)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_znorm_sample(x, threads, threads)
+    walls = []
+    for _ in range(args.steps):
+        w, _, kind = cpu_znorm_sample(x, threads, threads)
+        walls.append(w / threads)
+    v = 1e3 * float(np.mean(walls))
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": workload_config({"parallelism": f"{threads} host threads, independent contexts"}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"per step: {threads} independent C2 znorm runs on {threads} threads"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- GPU leg ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2508_12093_b200 import hestat as H
+    from paper_2508_12093_b200 import workloads as W
+    H.init(local)
+    stream = torch.cuda.ExternalStream(H.stream_handle())
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        H.sync()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # inputs: the seeded C2 column (identical on every rank) + a pool of distinct
+    # rolled copies so each step reads a column that is not L2-resident
+    x = W.normal(H.synthetic_uniform, SEED, S, 50.0, 10.0)
+    ctx = H.EvalContext(H.CkksParams(slot_count=S), rng_seed=rank)
+    pool = [H.encode_column(ctx, np.roll(x, 97 * i)) for i in range(POOL)]
+    H.sync()
+
+    # correctness gate: output of the bench path == oracle, bit for bit
+    from oracle_abi import Params, ST_ZNORM, bits, oracle
+    z = H.decode_column(ctx, H.znorm(ctx, pool[0], B))
+    ref = oracle().stat(Params(slot_count=S), ST_ZNORM, x, B)
+    parity = bool(np.array_equal(bits(z), bits(ref.out)))
+
+    # ---- value: device time, inputs resident --------------------------------------------
+    for i in range(args.warmup):
+        H.znorm(ctx, pool[i % POOL], B)
+    barrier_sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = H.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        keep = []
+        for i in range(args.steps):
+            keep.append(H.znorm(ctx, pool[i % POOL], B))
+            if len(keep) > 64:
+                keep.pop(0)
+        e1.record(stream)
+        barrier_sync()
+    launches = H.kernel_launches() - launches0
+    dev_ms = e0.elapsed_time(e1)
+    del keep
+
+    # ---- e2e: host buffers through the public API ----------------------------------------------
+    hx = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    hz = torch.empty(S, dtype=torch.float64).pin_memory()
+    xin = hx.numpy()
+    for _ in range(3):
+        H.decode_column(ctx, H.znorm(ctx, H.encode_column(ctx, xin), B))
+    barrier_sync()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(10, args.steps // 4)
+    t0 = time.perf_counter()
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        zc = H.znorm(ctx, H.encode_column(ctx, xin), B)
+        hz.numpy()[:] = H.decode_column(ctx, zc)
+    f1.record(stream)
+    barrier_sync()
+    e2e_wall_ms = 1e3 * (time.perf_counter() - t0)
+    e2e_ms = f0.elapsed_time(f1)
+
+    # ---- kernel roofline: the fused inverse-sqrt program (dominant kernel) -----------------------
+    m = H.moments(ctx, pool[0], B)
+    var = m.ct_var
+    for _ in range(5):
+        H.crypto_invsqrt(ctx, var, B * B)
+    barrier_sync()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    g0.record(stream)
+    for _ in range(reps):
+        H.crypto_invsqrt(ctx, var, B * B)
+    g1.record(stream)
+    barrier_sync()
+    prog_us = 1e3 * g0.elapsed_time(g1) / reps
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for i in range(reps):
+        H.moments(ctx, pool[i % POOL], B)
+    h1.record(stream)
+    barrier_sync()
+    mom_us = 1e3 * h0.elapsed_time(h1) / reps
+    # FP64 pipe instructions per slot of crypto_invsqrt (degree 511, 6 iterations) in the
+    # grid-unit formulation of quant.cuh: mul_ct 3, mul_pt 2, add_pt 2, add/sub 1
+    mul_ct, mul_pt, add_pt, add_ct = 263 + 18, 256 + 6 + 1, 256 + 8 + 1, 255 + 8 + 6
+    fp64_per_slot = 3 * mul_ct + 2 * mul_pt + 2 * add_pt + add_ct
+    achieved = fp64_per_slot * S / (prog_us * 1e-6) / 1e12
+    from paper_2508_12093_b200 import _abi
+    import ctypes
+    rate = ctypes.c_double(0)
+    _abi.lib().hs_diag_fp64_rate(0, ctypes.byref(rate))
+    peak = rate.value / 1e12
+
+    # ---- max over ranks ---------------------------------------------------------------------------
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank == 0:
+        value = dev_ms / (args.steps * ws)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded N(50,10^2) via mt19937_64 + Box-Muller (paper datasets absent)",
+            "config": workload_config({"parallelism": f"replicas x{ws} (no data-path collective)"}),
+            "parity_vs_oracle": parity,
+            "e2e": {"value": e2e_ms / (e2e_steps * ws), "unit": UNIT, "h2d_bytes_per_step": S * 8,
+                    "d2h_bytes_per_step": S * 8, "wall_ms_per_step": e2e_wall_ms / e2e_steps},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "fp64", "kernel": "k_prog (fused crypto_invsqrt, degree 511 + 6 Newton)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": None, "duration_us": prog_us,
+                         "work": f"{fp64_per_slot} fp64 ops/slot x {S} slots",
+                         "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
+                                        "MEASURED_PEAKS.json has no FP64 figure"},
+            "kernels_us": {"moments_slotsum": mom_us, "invsqrt_prog": prog_us},
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            cb, cout = cpu_baseline(x)
+            cb["parity_vs_gpu"] = bool(np.array_equal(bits(cout), bits(z)))
+            line["cpu_baseline"] = cb
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

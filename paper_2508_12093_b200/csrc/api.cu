@@ -1,0 +1,585 @@
+// api.cu — the extern "C" ABI of include/hestat_gpu.h.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "backends.h"
+#include "core.h"
+#include "pipelines.h"
+#include "series.h"
+
+using namespace hsg;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return HS_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::out_of_range& e) {  // map::at in the reference's BSGS
+    g_err = e.what();
+    return HS_E_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HS_E_ERROR;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) fail(HS_E_INVALID_ARG, std::string("null argument: ") + what);
+}
+
+const Ct& get(const hs_ct* h) {
+  need(h, "ciphertext");
+  return h->p;
+}
+
+hs_ct* wrap(Ct c) { return new hs_ct{std::move(c)}; }
+
+hs_ctx* ctxp(hs_ctx* c) {
+  need(c, "context");
+  return c;
+}
+const hs_ctx* ctxp(const hs_ctx* c) {
+  need(c, "context");
+  return c;
+}
+
+flow::InvCfg cfg_of(const hs_invroot_cfg* c) {
+  flow::InvCfg r;
+  if (c) {
+    r.n = c->n;
+    r.cheb_degree = c->cheb_degree;
+    r.newton_iters = c->newton_iters;
+    r.baseline_mode = c->baseline_mode != 0;
+    r.baseline_iters = c->baseline_iters;
+  }
+  return r;
+}
+
+flow::SignCfg sign_of(const hs_sign_cfg* c) {
+  flow::SignCfg r;
+  if (c) {
+    r.mode = c->mode;
+    r.folds = c->folds;
+    size_t off = 0;
+    for (uint64_t i = 0; i < c->npolys; ++i) {
+      r.custom_polys.emplace_back(c->polys + off, c->polys + off + c->poly_len[i]);
+      off += c->poly_len[i];
+    }
+  }
+  return r;
+}
+
+pipe::ColC col_of(const hs_column* c) {
+  need(c, "column");
+  pipe::ColC r;
+  r.n_valid = c->n_valid;
+  for (uint64_t i = 0; i < c->n_chunks; ++i) r.chunks.push_back(get(c->chunks[i]));
+  return r;
+}
+
+size_t nv_of(uint64_t n) { return n == HS_ALL_SLOTS ? flow::kAllSlots : static_cast<size_t>(n); }
+
+}  // namespace
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+const char* hs_version(void) { return "hestat-gpu 0.1 (sm_100a)"; }
+
+int hs_init(int device) {
+  return guard([&] {
+    Runtime::init(device);
+    Runtime::get();
+  });
+}
+
+int hs_sync(void) {
+  return guard([&] { Runtime::get().sync(); });
+}
+
+void* hs_stream(void) {
+  void* s = nullptr;
+  guard([&] { s = reinterpret_cast<void*>(Runtime::get().stream()); });
+  return s;
+}
+
+int hs_set_fused(int enabled) {
+  return guard([&] { Runtime::get().fused = enabled != 0; });
+}
+
+uint64_t hs_kernel_launches(void) {
+  uint64_t n = 0;
+  guard([&] { n = Runtime::get().launches(); });
+  return n;
+}
+
+// ---- EvalContext ----------------------------------------------------------------------
+int hs_params_validate(const hs_params* p) {
+  return guard([&] {
+    need(p, "params");
+    Params::from(*p).validate();
+  });
+}
+
+int hs_ctx_create(const hs_params* p, uint64_t seed, hs_ctx** out) {
+  return guard([&] {
+    need(p, "params");
+    need(out, "out");
+    Params q = Params::from(*p);
+    q.validate();  // EvalContext ctor, ckks.hpp:85-88
+    auto* c = new hs_ctx;
+    c->p = q;
+    c->seed = seed;
+    *out = c;
+  });
+}
+
+void hs_ctx_destroy(hs_ctx* c) { delete c; }
+
+int hs_ctx_params(const hs_ctx* c, hs_params* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = ctxp(c)->p.to();
+  });
+}
+
+int hs_ctx_meter(const hs_ctx* c, hs_meter* out) {
+  return guard([&] {
+    need(out, "out");
+    const Meter& m = ctxp(c)->m;
+    *out = hs_meter{m.mul_ct, m.mul_pt, m.add, m.rotate, m.bootstrap};
+  });
+}
+
+int hs_ctx_set_meter(hs_ctx* c, const hs_meter* m) {
+  return guard([&] {
+    need(m, "meter");
+    ctxp(c)->m = Meter{m->mul_ct, m->mul_pt, m->add, m->rotate, m->bootstrap};
+  });
+}
+
+uint64_t hs_ctx_rng_seed(const hs_ctx* c) { return c ? c->seed : 0; }
+
+// ---- Ciphertext -------------------------------------------------------------------------
+int hs_ct_new(const double* slots, uint64_t n, int32_t level, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    if (n) need(slots, "slots");
+    *out = wrap(ct_host(std::vector<double>(slots, slots + n), level));
+  });
+}
+
+hs_ct* hs_ct_retain(hs_ct* ct) { return ct ? new hs_ct{ct->p} : nullptr; }
+void hs_ct_release(hs_ct* ct) { delete ct; }
+int32_t hs_ct_level(const hs_ct* ct) { return ct && ct->p ? ct->p->level : 0; }
+uint64_t hs_ct_size(const hs_ct* ct) { return ct && ct->p ? ct->p->n : 0; }
+
+int hs_ct_read(const hs_ct* ct, double* out, uint64_t n) {
+  return guard([&] {
+    const Ct& c = get(ct);
+    if (n > c->n) fail(HS_E_TOO_MANY_VALUES, "hs_ct_read: n exceeds ciphertext size");
+    if (n) need(out, "out");
+    c->read(out, static_cast<size_t>(n));
+  });
+}
+
+// ---- EvalContext ops ------------------------------------------------------------------------
+int hs_encrypt(const hs_ctx* c, const double* v, uint64_t n, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    if (n) need(v, "values");
+    hs_ctx* cc = const_cast<hs_ctx*>(ctxp(c));
+    DevB db(cc->p, cc->m);  // encrypt is const: no meter update
+    *out = wrap(db.encrypt(v, static_cast<size_t>(n)));
+  });
+}
+
+int hs_decrypt(const hs_ctx* c, const hs_ct* ct, uint64_t n, double* out) {  // ckks.hpp:107-111
+  return guard([&] {
+    const hs_ctx* cc = ctxp(c);
+    if (n > cc->p.S) fail(HS_E_TOO_MANY_VALUES, "decrypt: n exceeds slot count");
+    const Ct& x = get(ct);
+    if (n > x->n) fail(HS_E_LENGTH_MISMATCH, "decrypt: ciphertext shorter than n");
+    if (n) need(out, "out");
+    x->read(out, static_cast<size_t>(n));
+  });
+}
+
+#define HS_OP(body)                       \
+  return guard([&] {                      \
+    need(out, "out");                     \
+    hs_ctx* cc = ctxp(c);                 \
+    DevB db(cc->p, cc->m);                \
+    body;                                 \
+  })
+
+int hs_add_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.add_ct(get(a), get(b)))); }
+int hs_sub_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.sub_ct(get(a), get(b)))); }
+int hs_add_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) { HS_OP(*out = wrap(db.add_pt(get(a), k))); }
+int hs_mul_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.mul_ct(get(a), get(b)))); }
+int hs_mul_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) { HS_OP(*out = wrap(db.mul_pt(get(a), k))); }
+int hs_mul_pt_vec(hs_ctx* c, const hs_ct* a, const double* p, uint64_t n, hs_ct** out) {
+  HS_OP({
+    if (n) need(p, "plaintext");
+    *out = wrap(db.mul_pt_vec(get(a), std::vector<double>(p, p + n)));
+  });
+}
+int hs_rotate(hs_ctx* c, const hs_ct* a, int64_t k, hs_ct** out) { HS_OP(*out = wrap(db.rotate(get(a), static_cast<long>(k)))); }
+int hs_bootstrap(hs_ctx* c, const hs_ct* a, hs_ct** out) { HS_OP(*out = wrap(db.bootstrap(get(a)))); }
+int hs_sum_all_slots(hs_ctx* c, const hs_ct* a, uint64_t n_valid, hs_ct** out) {
+  HS_OP(*out = wrap(db.sum_all_slots(get(a), static_cast<size_t>(n_valid))));
+}
+
+// ---- Chebyshev ------------------------------------------------------------------------------
+double hs_scaled_target(int kind, double S, double t) {
+  return scaled_target(kind == 1 ? TargetKind::SqrtShifted : TargetKind::InvSqrtShifted, S, t);
+}
+
+int32_t hs_cheb_eval_depth(int32_t degree) { return cheb_depth(degree); }
+
+int hs_fit(hs_target_fn f, void* user, int32_t degree, double lo, double hi, double* coeffs) {
+  return guard([&] {
+    need(reinterpret_cast<void*>(f), "target");
+    need(coeffs, "coeffs");
+    Series s = fit([f, user](double x) { return f(x, user); }, degree, lo, hi);
+    std::memcpy(coeffs, s.coeffs.data(), s.coeffs.size() * sizeof(double));
+  });
+}
+
+int hs_fit_target(int kind, double S, int32_t degree, double lo, double hi, double* coeffs) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    const TargetKind k = kind == 1 ? TargetKind::SqrtShifted : TargetKind::InvSqrtShifted;
+    Series s = (lo == -1.0 && hi == 1.0) ? fit_scaled(k, S, degree)
+                                         : fit([k, S](double t) { return scaled_target(k, S, t); }, degree, lo, hi);
+    std::memcpy(coeffs, s.coeffs.data(), s.coeffs.size() * sizeof(double));
+  });
+}
+
+double hs_eval_plain(const double* coeffs, uint64_t n, double lo, double hi, double x, int32_t* extrapolated) {
+  Series s;
+  s.coeffs.assign(coeffs, coeffs + n);
+  s.lo = lo;
+  s.hi = hi;
+  bool ex = false;
+  const double r = n ? eval_plain(s, x, &ex) : 0.0;
+  if (extrapolated) *extrapolated = ex ? 1 : 0;
+  return r;
+}
+
+int hs_eval_encrypted(hs_ctx* c, const double* coeffs, uint64_t n, double lo, double hi, const hs_ct* ct,
+                      hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    if (n) need(coeffs, "coeffs");
+    Series s;
+    s.coeffs.assign(coeffs, coeffs + n);
+    s.lo = lo;
+    s.hi = hi;
+    *out = wrap(pipe::eval_encrypted(ctxp(c), s, get(ct)));
+  });
+}
+
+// ---- primitives -----------------------------------------------------------------------------
+int hs_newton_loop(hs_ctx* c, const hs_ct* x_op, const hs_ct* y, int32_t n, int32_t iters, uint64_t n_valid,
+                   hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::newton_loop(ctxp(c), get(x_op), get(y), n, iters, nv_of(n_valid)));
+  });
+}
+
+int hs_newton_refine(hs_ctx* c, const hs_ct* x, const hs_ct* y0, int32_t n, int32_t iters, uint64_t n_valid,
+                     hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::newton_refine(ctxp(c), get(x), get(y0), n, iters, nv_of(n_valid)));
+  });
+}
+
+int hs_crypto_invsqrt(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg* cfg, uint64_t n_valid,
+                      hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::crypto_invsqrt(ctxp(c), get(ct), S, cfg_of(cfg), nv_of(n_valid)));
+  });
+}
+
+int hs_baseline_invsqrt(hs_ctx* c, const hs_ct* ct, double S, int32_t iters, uint64_t n_valid, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::baseline_invsqrt(ctxp(c), get(ct), S, iters, nv_of(n_valid)));
+  });
+}
+
+int hs_crypto_inv(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg* cfg, uint64_t n_valid,
+                  hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::crypto_inv(ctxp(c), get(ct), S, cfg_of(cfg), nv_of(n_valid)));
+  });
+}
+
+int hs_crypto_sqrt(hs_ctx* c, const hs_ct* ct, double S, int32_t degree, uint64_t n_valid, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::crypto_sqrt(ctxp(c), get(ct), S, degree, nv_of(n_valid)));
+  });
+}
+
+int hs_crypto_sign(hs_ctx* c, const hs_ct* ct, const hs_sign_cfg* cfg, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::crypto_sign(ctxp(c), get(ct), sign_of(cfg)));
+  });
+}
+
+// ---- columns ----------------------------------------------------------------------------------
+int hs_encode_column(hs_ctx* c, const double* v, uint64_t n, hs_ct** chunks_out, uint64_t* n_chunks) {
+  return guard([&] {  // column.hpp:25-39
+    hs_ctx* cc = ctxp(c);
+    need(n_chunks, "n_chunks");
+    if (n) {
+      need(v, "values");
+      need(chunks_out, "chunks_out");
+    }
+    for (uint64_t i = 0; i < n; ++i)
+      if (!std::isfinite(v[i])) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
+    DevB db(cc->p, cc->m);
+    const size_t S = cc->p.S;
+    std::vector<Ct> chunks;
+    for (size_t off = 0; off < n; off += S) chunks.push_back(db.encrypt(v + off, std::min<size_t>(S, n - off)));
+    for (size_t i = 0; i < chunks.size(); ++i) chunks_out[i] = wrap(chunks[i]);
+    *n_chunks = chunks.size();
+  });
+}
+
+int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
+  return guard([&] {  // column.hpp:41-56
+    const size_t S = ctxp(c)->p.S;
+    need(col, "column");
+    if (col->n_valid > col->n_chunks * S) fail(HS_E_LENGTH_MISMATCH, "decode_column: n_valid exceeds packed capacity");
+    if (col->n_valid) need(out, "out");
+    size_t remaining = col->n_valid, o = 0;
+    for (uint64_t i = 0; i < col->n_chunks; ++i) {
+      const size_t take = std::min(S, remaining);
+      const Ct& x = get(col->chunks[i]);
+      if (take > x->n) fail(HS_E_LENGTH_MISMATCH, "decode_column: chunk shorter than slot count");
+      x->read(out + o, take);
+      o += take;
+      remaining -= take;
+    }
+  });
+}
+
+// ---- statistics ---------------------------------------------------------------------------------
+int hs_mean_scaled(hs_ctx* c, const hs_column* col, double B, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::mean_scaled(ctxp(c), col_of(col), B));
+  });
+}
+
+int hs_variance_to_scale(hs_ctx* c, const hs_column* col, double S, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::variance_to_scale(ctxp(c), col_of(col), S));
+  });
+}
+
+int hs_variance_scaled(hs_ctx* c, const hs_column* col, double B, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::variance_scaled(ctxp(c), col_of(col), B));
+  });
+}
+
+int hs_moments(hs_ctx* c, const hs_column* col, double B, hs_ct** mu, hs_ct** var) {
+  return guard([&] {
+    need(mu, "mu");
+    need(var, "var");
+    auto m = pipe::moments(ctxp(c), col_of(col), B);
+    *mu = wrap(m.mu);
+    *var = wrap(m.var);
+  });
+}
+
+int hs_znorm(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out_chunks) {
+  return guard([&] {
+    auto z = pipe::znorm(ctxp(c), col_of(col), B, cfg_of(cfg));
+    if (!z.chunks.empty()) need(out_chunks, "out_chunks");
+    for (size_t i = 0; i < z.chunks.size(); ++i) out_chunks[i] = wrap(z.chunks[i]);
+  });
+}
+
+int hs_kurtosis(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::kurtosis(ctxp(c), col_of(col), B, cfg_of(cfg)));
+  });
+}
+
+int hs_skewness(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::skewness(ctxp(c), col_of(col), B, cfg_of(cfg)));
+  });
+}
+
+int hs_coeff_variation(hs_ctx* c, const hs_column* col, double B, const hs_sign_cfg* sc, const hs_invroot_cfg* cfg,
+                       hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::coeff_variation(ctxp(c), col_of(col), B, sign_of(sc), cfg_of(cfg)));
+  });
+}
+
+int hs_pearson(hs_ctx* c, const hs_column* x, const hs_column* y, double B, const hs_invroot_cfg* cfg,
+               hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(pipe::pearson(ctxp(c), col_of(x), col_of(y), B, cfg_of(cfg)));
+  });
+}
+
+// ---- host-side data helpers (data.hpp:148-208, plain.hpp:18-92) -------------------------------
+int hs_synthetic_uniform(uint64_t seed, uint64_t n, double lo, double hi, double* out) {
+  return guard([&] {
+    if (n < 1) fail(HS_E_ERROR, "synthetic_uniform: n must be >= 1");
+    if (!(lo < hi)) fail(HS_E_ERROR, "synthetic_uniform: lo must be < hi");
+    need(out, "out");
+    std::mt19937_64 rng(seed);
+    for (uint64_t i = 0; i < n; ++i) {
+      const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+      out[i] = lo + u * (hi - lo);
+    }
+  });
+}
+
+int hs_synthetic_grid(uint64_t n, double lo, double hi, double* out) {
+  return guard([&] {
+    if (n < 2) fail(HS_E_ERROR, "synthetic_grid: n must be >= 2");
+    if (!(lo < hi)) fail(HS_E_ERROR, "synthetic_grid: lo must be < hi");
+    need(out, "out");
+    const double step = (hi - lo) / static_cast<double>(n - 1);
+    for (uint64_t i = 0; i < n; ++i) out[i] = lo + step * static_cast<double>(i);
+    out[n - 1] = hi;
+  });
+}
+
+int hs_two_subrange_grid(uint64_t n, double lo, double hi, double* out) {
+  if (!(lo < 1.0 && 1.0 < hi)) return hs_synthetic_grid(n, lo, hi, out);
+  const int rc = hs_synthetic_grid(n / 2, lo, 1.0, out);
+  if (rc) return rc;
+  return hs_synthetic_grid(n - n / 2, 1.0, hi, out + n / 2);
+}
+
+int hs_mre(const double* a, const double* e, uint64_t n, double* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n == 0) fail(HS_E_ERROR, "mre: empty input");
+    double acc = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (e[i] == 0.0) fail(HS_E_ZERO_REFERENCE, "mre: exact value is zero at index " + std::to_string(i));
+      acc += std::abs(a[i] - e[i]) / std::abs(e[i]);
+    }
+    *out = acc / static_cast<double>(n);
+  });
+}
+
+int hs_relative_error(double a, double e, double* out) {
+  return guard([&] {
+    need(out, "out");
+    if (e == 0.0) fail(HS_E_ZERO_REFERENCE, "relative_error: zero reference");
+    *out = std::abs(a - e) / std::abs(e);
+  });
+}
+
+int hs_plain(int which, const double* x, uint64_t n, const double* y, double* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n == 0) fail(HS_E_EMPTY_COLUMN, "plain::mean: empty input");
+    const size_t N = static_cast<size_t>(n);
+    auto mean = [&](const double* v) {
+      double acc = 0.0;
+      for (size_t i = 0; i < N; ++i) acc += v[i];
+      return acc / static_cast<double>(N);
+    };
+    auto var = [&](const double* v) {
+      const double mu = mean(v);
+      double acc = 0.0;
+      for (size_t i = 0; i < N; ++i) acc += (v[i] - mu) * (v[i] - mu);
+      return acc / static_cast<double>(N);
+    };
+    switch (which) {
+      case 0: *out = mean(x); break;
+      case 1: *out = var(x); break;
+      case 2: {
+        const double mu = mean(x);
+        double m2 = 0.0, m3 = 0.0;
+        for (size_t i = 0; i < N; ++i) {
+          const double d = x[i] - mu;
+          m2 += d * d;
+          m3 += d * d * d;
+        }
+        m2 /= static_cast<double>(N);
+        m3 /= static_cast<double>(N);
+        *out = m3 / std::pow(m2, 1.5);
+        break;
+      }
+      case 3: {
+        const double mu = mean(x);
+        double m2 = 0.0, m4 = 0.0;
+        for (size_t i = 0; i < N; ++i) {
+          const double d = x[i] - mu;
+          m2 += d * d;
+          m4 += d * d * d * d;
+        }
+        m2 /= static_cast<double>(N);
+        m4 /= static_cast<double>(N);
+        *out = m4 / (m2 * m2);
+        break;
+      }
+      case 4: {
+        const double mu = mean(x);
+        if (mu == 0.0) fail(HS_E_NEAR_ZERO_MEAN, "plain::coeff_variation: zero mean");
+        *out = std::sqrt(var(x)) * (mu > 0 ? 1.0 : -1.0) / std::abs(mu);
+        break;
+      }
+      case 5: {
+        need(y, "y");
+        const double mx = mean(x), my = mean(y);
+        double cv = 0.0, vx = 0.0, vy = 0.0;
+        for (size_t i = 0; i < N; ++i) {
+          cv += (x[i] - mx) * (y[i] - my);
+          vx += (x[i] - mx) * (x[i] - mx);
+          vy += (y[i] - my) * (y[i] - my);
+        }
+        if (vx == 0.0 || vy == 0.0) fail(HS_E_DEGENERATE_VARIANCE, "plain::pearson: constant column");
+        *out = cv / std::sqrt(vx * vy);
+        break;
+      }
+      case 6: {
+        const double mu = mean(x), sd = std::sqrt(var(x));
+        if (sd == 0.0) fail(HS_E_DEGENERATE_VARIANCE, "plain::znorm: zero variance");
+        for (size_t i = 0; i < N; ++i) out[i] = (x[i] - mu) / sd;
+        break;
+      }
+      case 7: *out = std::sqrt(var(x)); break;
+      default: fail(HS_E_INVALID_ARG, "hs_plain: bad selector");
+    }
+  });
+}
+
+}  // extern "C"

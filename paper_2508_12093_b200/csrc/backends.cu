@@ -1,0 +1,179 @@
+// backends.cu — DevB: one CUDA kernel per EvalContext op (ckks.hpp:97-230).
+#include "backends.h"
+
+#include <cstring>
+#include <string>
+
+namespace hsg {
+
+DevB::DevB(const Params& p, Meter& m) : LedgerBase(p, m) {
+  qs_.mode = p.quantize ? QMode::Exact : QMode::None;
+  qs_.bits = p.scale_bits;
+}
+
+Ct DevB::encrypt(const double* v, size_t n) const {
+  if (n > p_.S) fail(HS_E_TOO_MANY_VALUES, "encrypt: more values than slots");
+  Runtime& rt = Runtime::get();
+  DevBuf d = rt.alloc(p_.S);
+  if (n) {
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    cuda_ok(cudaMemcpyAsync(d.get(), v, n * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
+            "encrypt upload");
+    if (pinned) rt.sync();  // the caller may reuse its pinned buffer on return
+  }
+  if (n < p_.S)
+    cuda_ok(cudaMemsetAsync(d.get() + n, 0, (p_.S - n) * sizeof(double), rt.stream()), "encrypt pad");
+  if (p_.quantize) k::requant(qs_, d.get(), d.get(), p_.S, rt.stream());
+  return ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::encrypt_const(double c) const {
+  std::vector<double> v(p_.S, c);
+  return encrypt(v.data(), v.size());
+}
+
+Ct DevB::addsub(const C& a, const C& b, k::BinOp op) {  // ckks.hpp:113-133
+  check_shape(sz(a));
+  check_shape(sz(b));
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::binary(qs_, op, a->device(), b->device(), o.get(), p_.S, Runtime::get().stream());
+  ++m_.add;
+  return ct_device(o, p_.S, std::min(a->level, b->level), p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::add_pt(const C& a, double c) {  // ckks.hpp:137-144
+  check_shape(sz(a));
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::scalar(qs_, k::S_ADD, a->device(), c, o.get(), p_.S, Runtime::get().stream());
+  ++m_.add;
+  return ct_device(o, p_.S, a->level, p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::bootstrap(const C& a) {  // ckks.hpp:207-213
+  check_shape(sz(a));
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::requant(qs_, a->device(), o.get(), p_.S, Runtime::get().stream());
+  ++m_.bootstrap;
+  return ct_device(o, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : a->grid);
+}
+
+Ct DevB::mul_ct(C a, C b) {  // ckks.hpp:149-164
+  check_shape(sz(a));
+  check_shape(sz(b));
+  if (std::min(a->level, b->level) < 1) {
+    if (!p_.auto_bootstrap) fail(HS_E_LEVEL_EXHAUSTED, "mul_ct: no multiplicative level left");
+    if (a->level < 1) a = bootstrap(a);
+    if (b->level < 1) b = bootstrap(b);
+  }
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::binary(qs_, k::B_MUL, a->device(), b->device(), o.get(), p_.S, Runtime::get().stream());
+  ++m_.mul_ct;
+  return ct_device(o, p_.S, std::min(a->level, b->level) - 1, p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::prepare_mul_pt(C a) {  // ckks.hpp:233-240
+  if (a->level < 1) {
+    if (!p_.auto_bootstrap) fail(HS_E_LEVEL_EXHAUSTED, "mul_pt: no multiplicative level left");
+    a = bootstrap(a);
+  }
+  return a;
+}
+
+Ct DevB::mul_pt(C a, double c) {  // ckks.hpp:168-176
+  check_shape(sz(a));
+  a = prepare_mul_pt(a);
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::scalar(qs_, k::S_MUL, a->device(), c, o.get(), p_.S, Runtime::get().stream());
+  ++m_.mul_pt;
+  return ct_device(o, p_.S, a->level - 1, p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::mul_pt_vec(C a, const std::vector<double>& v) {  // ckks.hpp:179-189
+  check_shape(sz(a));
+  if (v.size() != p_.S) fail(HS_E_LENGTH_MISMATCH, "mul_pt: plaintext vector length != slot count");
+  a = prepare_mul_pt(a);
+  Runtime& rt = Runtime::get();
+  DevBuf pv = rt.alloc(p_.S);
+  cuda_ok(cudaMemcpyAsync(pv.get(), v.data(), p_.S * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
+          "mul_pt plaintext upload");
+  DevBuf o = rt.alloc(p_.S);
+  k::binary(qs_, k::B_MUL, a->device(), pv.get(), o.get(), p_.S, rt.stream());
+  ++m_.mul_pt;
+  return ct_device(o, p_.S, a->level - 1, p_.quantize ? p_.scale_bits : 0);
+}
+
+Ct DevB::rotate(const C& a, long kk) {  // ckks.hpp:193-202
+  check_shape(sz(a));
+  const long n = static_cast<long>(p_.S);
+  const long shift = ((kk % n) + n) % n;
+  DevBuf o = Runtime::get().alloc(p_.S);
+  k::rotate(a->device(), o.get(), p_.S, static_cast<size_t>(shift), Runtime::get().stream());
+  ++m_.rotate;
+  return ct_device(o, p_.S, a->level, a->grid);
+}
+
+Ct DevB::sum_all_slots(const C& a, size_t n_valid) {  // ckks.hpp:218-230
+  check_shape(sz(a));
+  if (p_.debug && n_valid < p_.S) {
+    const double eps = std::ldexp(1.0, -(p_.scale_bits - 1));
+    const std::vector<double>& h = a->host_slots();
+    for (size_t i = n_valid; i < p_.S; ++i)
+      if (std::abs(h[i]) > eps) fail(HS_E_DIRTY_PADDING, "sum_all_slots: nonzero padding slot");
+  }
+  DevBuf o = Runtime::get().alloc(p_.S);
+  const double* src = a->device();
+  double* dst = o.get();
+  k::slot_sum(qs_, &src, &dst, 1, p_.S, Runtime::get().stream());
+  int steps = 0;
+  for (size_t s = 1; s < p_.S; s <<= 1) ++steps;
+  m_.rotate += steps;
+  m_.add += steps;
+  int grid = p_.quantize ? p_.scale_bits : 0;
+  if (steps == 0) grid = a->grid;  // S == 1: no add, value passes through untouched
+  return ct_device(o, p_.S, a->level, grid);
+}
+
+// ---- debug-mode value checks (host reads; debug is the diagnostics path) ----
+double DevB::first_slot(const C& c) {  // stats.hpp:89-91 (decrypt(ct, 1)[0])
+  double v = 0.0;
+  c->read(&v, 1);
+  return v;
+}
+
+void DevB::check_open_domain(const C& c, size_t n_valid, double lo, double hi, const char* who) {
+  const size_t n = std::min(n_valid, c->n);  // primitives.hpp:134-144
+  const std::vector<double>& h = c->host_slots();
+  for (size_t i = 0; i < n; ++i) {
+    const double t = h[i];
+    if (!(t > lo) || !(t <= hi)) fail(HS_E_DOMAIN_VIOLATION, std::string(who) + ": scaled slot outside domain");
+  }
+}
+
+void DevB::check_eval_domain(const C& c, double lo, double hi) {  // chebyshev.hpp:174-179
+  const double eps = 1e-9;
+  for (double v : c->host_slots())
+    if (v < lo - eps || v > hi + eps) fail(HS_E_DOMAIN_VIOLATION, "eval_encrypted: slot outside series domain");
+}
+
+void DevB::check_divergence(const C& c, size_t n_valid) {  // primitives.hpp:89-96
+  const size_t n = std::min(n_valid, c->n);
+  const std::vector<double>& h = c->host_slots();
+  for (size_t i = 0; i < n; ++i)
+    if (!(std::abs(h[i]) <= 1e6)) fail(HS_E_DIVERGENCE, "newton iterate exceeded the divergence guard");
+}
+
+void DevB::check_sqrt_domain(const C& c, size_t n_valid) {  // primitives.hpp:225-232
+  const size_t n = std::min(n_valid, c->n);
+  const std::vector<double>& h = c->host_slots();
+  for (size_t i = 0; i < n; ++i)
+    if (h[i] < -1e-9 || h[i] > 2.0 + 1e-9) fail(HS_E_DOMAIN_VIOLATION, "crypto_sqrt: scaled slot outside [0, 2]");
+}
+
+void DevB::check_sign_domain(const C& c) {  // primitives.hpp:282-286
+  for (double v : c->host_slots())
+    if (v < -1.0 - 1e-9 || v > 1.0 + 1e-9) fail(HS_E_DOMAIN_VIOLATION, "crypto_sign: slot outside [-1, 1]");
+}
+
+}  // namespace hsg

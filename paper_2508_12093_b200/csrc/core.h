@@ -1,0 +1,123 @@
+// core.h — host-side core of libhestat_gpu.so: errors, parameters, meter,
+// device runtime (stream + stream-ordered memory pool) and ciphertext storage.
+//
+// Reference counterparts: CkksParams / CostMeter / Ciphertext / EvalContext
+// (/root/reference/proj/include/hestat/ckks.hpp:19-93).  The reference keeps a
+// std::vector<double> per ciphertext; here a ciphertext is an immutable device
+// buffer in HBM plus a host-side level, with a lazily filled host mirror for
+// slots() reads.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "hestat_gpu.h"
+
+namespace hsg {
+
+// ---- errors: one C++ type carrying the ABI status code (errors.hpp:11-38) ----
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void cuda_ok(cudaError_t e, const char* what);
+
+// ---- CkksParams (ckks.hpp:19-42) ----
+struct Params {
+  size_t S = 32768;
+  int max_level = 11;
+  int scale_bits = 40;
+  bool quantize = true;
+  bool auto_bootstrap = true;
+  bool debug = false;
+
+  static Params from(const hs_params& p);
+  hs_params to() const;
+  void validate() const;  // ckks.hpp:34-39
+};
+
+// ---- CostMeter (ckks.hpp:46-60) ----
+struct Meter {
+  uint64_t mul_ct = 0, mul_pt = 0, add = 0, rotate = 0, bootstrap = 0;
+};
+
+// ---- device runtime --------------------------------------------------------
+using DevBuf = std::shared_ptr<double>;
+
+class Runtime {
+ public:
+  static Runtime& get();        // lazily initialised, never destroyed
+  static void init(int device); // optional explicit device choice (before first use)
+
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
+  int sm_count() const { return sms_; }
+  DevBuf alloc(size_t n_doubles);           // stream-ordered; freed stream-ordered
+  void sync();
+  void note_launch(uint64_t n = 1) { launches_ += n; }
+  uint64_t launches() const { return launches_.load(); }
+  bool fused = true;
+  int prog_lanes = 4;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
+
+  // Device copy of a host table, cached by content (coefficient tables).
+  const double* table(const std::vector<double>& host);
+
+ private:
+  Runtime(int device);
+  int device_ = 0;
+  int sms_ = 148;
+  cudaStream_t stream_ = nullptr;
+  std::atomic<uint64_t> launches_{0};
+  std::mutex tab_mu_;
+  std::unordered_map<std::string, DevBuf> tabs_;
+};
+
+// ---- Ciphertext storage ------------------------------------------------------
+// grid > 0 records that every slot is a multiple of 2^-grid (the output of a
+// quantising op under scale_bits == grid); fused kernels rely on it to carry
+// values in exact integer grid units.
+struct CtData {
+  size_t n = 0;
+  int level = 0;
+  int grid = 0;
+  DevBuf dev;  // null for host-constructed ciphertexts until first device use
+  mutable std::mutex mu;
+  mutable std::vector<double> host;
+  mutable bool host_ok = false;
+
+  const double* device() const;                 // uploads a host-only ciphertext once
+  void read(double* out, size_t count) const;   // synchronous D2H (cached)
+  const std::vector<double>& host_slots() const;
+};
+using Ct = std::shared_ptr<const CtData>;
+
+Ct ct_device(DevBuf buf, size_t n, int level, int grid);
+Ct ct_host(std::vector<double> v, int level);  // Ciphertext(std::vector<double>, int)
+Ct ct_empty();                                 // Ciphertext()
+
+// ---- EncryptedColumn (column.hpp:19-23) ----
+struct Column {
+  std::vector<Ct> chunks;
+  size_t n_valid = 0;
+};
+
+}  // namespace hsg
+
+// ABI handle types
+struct hs_ct {
+  hsg::Ct p;
+};
+struct hs_ctx {
+  hsg::Params p;
+  hsg::Meter m;
+  uint64_t seed = 0;
+};

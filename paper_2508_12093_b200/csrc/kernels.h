@@ -1,0 +1,116 @@
+// kernels.h — host-callable launchers for every CUDA kernel of libhestat_gpu.
+//
+//   ops.cu    E1-E5: slot-wise ops, rotation, requantisation, sum_all_slots
+//             (the log-step rotate-and-add reduction, in shared memory across a
+//             thread-block cluster via DSMEM).
+//   fused.cu  E6-E8: the per-slot program interpreter (Chebyshev BSGS, Newton,
+//             inverse roots, statistic epilogues) and the moment/central-moment
+//             slot-sum kernels of the statistics pipelines.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace hsg {
+
+// Arithmetic policy selector (quant.cuh)
+enum class QMode : int { None = 0, Exact = 1, Grid = 2 };
+struct QSpec {
+  QMode mode = QMode::None;
+  int bits = 40;
+};
+
+namespace k {
+
+// ---- ops.cu ------------------------------------------------------------------------
+enum BinOp : int { B_ADD = 0, B_SUB = 1, B_MUL = 2 };
+void binary(QSpec q, BinOp op, const double* a, const double* b, double* out, size_t n, cudaStream_t s);
+enum ScalOp : int { S_ADD = 0, S_MUL = 1 };
+void scalar(QSpec q, ScalOp op, const double* a, double c, double* out, size_t n, cudaStream_t s);
+void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s);
+void rotate(const double* a, double* out, size_t n, size_t shift, cudaStream_t s);
+// sum_all_slots over `batch` ciphertexts of S slots each (a[b], out[b]).
+void slot_sum(QSpec q, const double* const* a, double* const* out, int batch, size_t S, cudaStream_t s);
+// largest S the single-launch cluster kernel handles with `arrays` concurrent sums
+size_t slot_sum_max(int arrays);
+
+// ---- fused.cu: per-slot programs ------------------------------------------------------
+enum MOp : int {
+  M_LD = 0,   // r[dst] = in(arr[i0][slot])
+  M_ST,       // arr_out[i0][slot] = out(r[a])
+  M_CONST,    // r[dst] = c (already in the policy's units)
+  M_ADD,      // r[dst] = add(r[a], r[b])
+  M_SUB,      // r[dst] = sub(r[a], r[b])
+  M_MUL,      // r[dst] = mul(r[a], r[b])
+  M_ADDC,     // r[dst] = addc(r[a], c)
+  M_MULC,     // r[dst] = mulc(r[a], c)
+  M_CHEB,     // r[dst] = ChebEncryptedEval(table @ i0, degree i1) on r[a]
+  M_NEWTON,   // r[dst] = newton_loop(x_op = r[a], y = r[b], n = i0, iters = i1, (n+1)/n = c)
+  M_ZAPPLY    // for every chunk: zout[c][slot] = out(mul(sub(in(zin[c][slot]), r[a]), r[b]))
+};
+struct MInst {
+  int op, dst, a, b, i0, i1;
+  double c;
+};
+constexpr int kMaxInst = 40;
+constexpr int kMaxArr = 6;
+constexpr int kMaxChunks = 48;
+constexpr int kRegs = 24;
+constexpr int kMaxFusedDegree = 1023;
+constexpr int kMaxFusedNewtonN = 6;
+
+struct Prog {
+  int n = 0;
+  int nchunks = 0;
+  unsigned S = 0;
+  int ntab = 0;                  // doubles of coefficient tables, staged into shared memory
+  const double* tabs = nullptr;  // coefficient tables (device); M_CHEB i0 = offset, b = lane-split
+  MInst ins[kMaxInst];
+  const double* in[kMaxArr];
+  double* out[kMaxArr];
+  const double* zin[kMaxChunks];
+  double* zout[kMaxChunks];
+};
+
+// Launch one per-slot program over S slots.  lanes = 1, 2, 4 or 8 threads per slot.
+void run_prog(QSpec q, const Prog& p, int lanes, cudaStream_t s);
+
+// ---- fused.cu: statistics slot-sum kernels -------------------------------------------
+// Moments of one column (stats.hpp:41-51, 110-126): per slot over chunks
+//   mean term  t0 = sum_c mulc(X_c, cm)
+//   sq term    t1 = sum_c mul(mulc(X_c, ca), mulc(X_c, ca))
+//   mp term    t2 = sum_c mulc(X_c, cmp)
+// then sum_all_slots of each, then var = sub(t1, mul(t2, t2)).
+enum MomMode : int { MOM_MEAN = 1, MOM_VAR = 2, MOM_BOTH = 3 };
+struct MomArgs {
+  int mode = MOM_BOTH;
+  int nchunks = 0;
+  const double* x[kMaxChunks];
+  double cm = 0, ca = 0, cmp = 0;
+  double* mu = nullptr;   // MOM_MEAN / MOM_BOTH
+  double* var = nullptr;  // MOM_VAR / MOM_BOTH
+};
+void moments(QSpec q, const MomArgs* cols, int ncols, size_t S, cudaStream_t s);
+
+// Centered power sums (stats.hpp:56-87, 170-210, 239-265): per slot over chunks
+//   cx = sub(X_c, mask_c ? mulc(mux, slot < valid_c) : mux)
+//   p  = power 3: mul(mul(cx,cx), cx); power 4: mul(s,s) with s = mul(cx,cx);
+//        power 2 (pearson): mul(cx, sub(Y_c, muy))
+//   t  = sum_c mulc(p, inv_n);   out = sum_all_slots(t)
+struct CentArgs {
+  int power = 4;
+  int nchunks = 0;
+  const double* x[kMaxChunks];
+  const double* y[kMaxChunks];
+  uint64_t valid[kMaxChunks];  // valid slots per chunk (mask applied to x when < S)
+  const double* mux = nullptr;
+  const double* muy = nullptr;
+  double inv_n = 0;
+  double* out = nullptr;
+};
+void central(QSpec q, const CentArgs& a, size_t S, cudaStream_t s);
+
+}  // namespace k
+}  // namespace hsg

@@ -1,0 +1,659 @@
+// pipelines.cu — fused executors (see pipelines.h).
+#include "pipelines.h"
+
+#include <cmath>
+#include <type_traits>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+#include <string>
+#include <vector>
+
+#include "backends.h"
+#include "kernels.h"
+
+namespace hsg {
+namespace pipe {
+namespace {
+
+using flow::InvCfg;
+using flow::SignCfg;
+
+QSpec fused_q(const Params& p) { return QSpec{p.quantize ? QMode::Grid : QMode::None, p.scale_bits}; }
+int out_grid(const Params& p) { return p.quantize ? p.scale_bits : 0; }
+
+bool ct_ok(const Params& p, const Ct& c) {
+  return c && c->n == p.S && (!p.quantize || c->grid == p.scale_bits);
+}
+
+bool fusable(const hs_ctx* ctx, std::initializer_list<const Ct*> cts) {
+  const Params& p = ctx->p;
+  if (p.debug || !Runtime::get().fused) return false;
+  if (p.S > (1u << 30)) return false;
+  for (const Ct* c : cts)
+    if (!ct_ok(p, *c)) return false;
+  return true;
+}
+
+bool col_ok(const hs_ctx* ctx, const ColC& col, int arrays) {
+  const Params& p = ctx->p;
+  if (p.debug || !Runtime::get().fused) return false;
+  if (col.chunks.empty() || col.chunks.size() > static_cast<size_t>(k::kMaxChunks)) return false;
+  if (p.S > k::slot_sum_max(arrays)) return false;
+  for (const Ct& c : col.chunks)
+    if (!ct_ok(p, c)) return false;
+  return true;
+}
+
+bool degree_ok(int d) { return d <= k::kMaxFusedDegree; }
+bool cfg_ok(const InvCfg& c) {
+  return c.baseline_mode ? true : degree_ok(c.cheb_degree);
+}
+bool sign_ok(const SignCfg& s) {
+  if (s.mode == 0) return true;
+  for (const auto& p : s.custom_polys)
+    if (static_cast<int>(p.size()) - 1 > k::kMaxFusedDegree) return false;
+  return true;
+}
+
+SymCt sym(const Ct& c) { return SymCt{c ? c->n : 0, c ? c->level : 0}; }
+flow::Col<SymCt> sym(const ColC& c) {
+  flow::Col<SymCt> s;
+  s.n_valid = c.n_valid;
+  for (const Ct& x : c.chunks) s.chunks.push_back(sym(x));
+  return s;
+}
+
+// ---- ledger memo ----------------------------------------------------------------
+// The ledger (levels, meter, auto-bootstrap decisions) is a pure function of the
+// parameters, the input sizes/levels and the scalar arguments — never of slot
+// values — so a successful symbolic run is memoised under a key of exactly
+// those inputs: steady-state calls skip the host-side replay of ~1,200 ops.
+// Runs that throw are never memoised (errors re-raise from a fresh replay).
+class Key {
+ public:
+  explicit Key(const char* fn, const Params& p) : k_(fn) {
+    add(p.S);
+    add(p.max_level);
+    add(p.scale_bits);
+    add(static_cast<int>(p.quantize) | static_cast<int>(p.auto_bootstrap) << 1 | static_cast<int>(p.debug) << 2);
+  }
+  template <class T>
+  Key& add(const T& v) {
+    static_assert(std::is_trivially_copyable_v<T>);
+    k_.append(reinterpret_cast<const char*>(&v), sizeof v);
+    return *this;
+  }
+  Key& ct(const Ct& c) { return add(c ? c->n : size_t(0)).add(c ? c->level : 0); }
+  Key& col(const ColC& c) {
+    add(c.n_valid).add(c.chunks.size());
+    for (const Ct& x : c.chunks) ct(x);
+    return *this;
+  }
+  Key& cfg(const InvCfg& c) {
+    return add(c.n).add(c.cheb_degree).add(c.newton_iters).add(c.baseline_mode).add(c.baseline_iters);
+  }
+  Key& sign(const SignCfg& c) {
+    add(c.mode).add(c.folds).add(c.custom_polys.size());
+    for (const auto& p : c.custom_polys) {
+      add(p.size());
+      k_.append(reinterpret_cast<const char*>(p.data()), p.size() * sizeof(double));
+    }
+    return *this;
+  }
+  const std::string& str() const { return k_; }
+
+ private:
+  std::string k_;
+};
+
+void put(std::vector<int>& v, const SymCt& c) { v.push_back(c.level); }
+void put(std::vector<int>& v, const flow::Col<SymCt>& c) {
+  for (const SymCt& x : c.chunks) v.push_back(x.level);
+}
+void put(std::vector<int>& v, const flow::Moments<SymCt>& m) {
+  v.push_back(m.mu.level);
+  v.push_back(m.var.level);
+}
+void get(const std::vector<int>& v, size_t S, SymCt* c) { *c = SymCt{S, v.at(0)}; }
+void get(const std::vector<int>& v, size_t S, flow::Col<SymCt>* c) {
+  c->chunks.clear();
+  for (int l : v) c->chunks.push_back(SymCt{S, l});
+}
+void get(const std::vector<int>& v, size_t S, flow::Moments<SymCt>* m) {
+  m->mu = SymCt{S, v.at(0)};
+  m->var = SymCt{S, v.at(1)};
+}
+
+struct Memo {
+  Meter delta;
+  std::vector<int> levels;
+};
+std::mutex g_memo_mu;
+std::unordered_map<std::string, Memo> g_memo;
+
+// Run the reference ledger symbolically on a copy of the meter; commit the
+// copy whether it returns or throws (the reference's meter state at its throw).
+template <class F>
+auto ledger(hs_ctx* ctx, const Key& key, F&& f) {
+  using R = decltype(f(std::declval<SymB&>()));
+  {
+    std::lock_guard<std::mutex> g(g_memo_mu);
+    auto it = g_memo.find(key.str());
+    if (it != g_memo.end()) {
+      R r{};
+      get(it->second.levels, ctx->p.S, &r);
+      Meter m = ctx->m;
+      m.mul_ct += it->second.delta.mul_ct;
+      m.mul_pt += it->second.delta.mul_pt;
+      m.add += it->second.delta.add;
+      m.rotate += it->second.delta.rotate;
+      m.bootstrap += it->second.delta.bootstrap;
+      return std::make_pair(r, m);
+    }
+  }
+  Meter m = ctx->m;
+  SymB sb(ctx->p, m);
+  try {
+    R r = f(sb);
+    Memo e;
+    e.delta = Meter{m.mul_ct - ctx->m.mul_ct, m.mul_pt - ctx->m.mul_pt, m.add - ctx->m.add,
+                    m.rotate - ctx->m.rotate, m.bootstrap - ctx->m.bootstrap};
+    put(e.levels, r);
+    std::lock_guard<std::mutex> g(g_memo_mu);
+    if (g_memo.size() > 4096) g_memo.clear();
+    g_memo.emplace(key.str(), std::move(e));
+    return std::make_pair(r, m);
+  } catch (...) {
+    ctx->m = m;
+    throw;
+  }
+}
+
+// ---- per-slot program builder ---------------------------------------------------
+class PB {
+ public:
+  explicit PB(const Params& p) : p_(p), q_(fused_q(p)) { prog_.S = static_cast<unsigned>(p.S); }
+
+  int ld(const double* dev) {
+    if (nin_ >= k::kMaxArr) fail(HS_E_ERROR, "fused program: too many inputs");
+    prog_.in[nin_] = dev;
+    return emit(k::M_LD, reg(), 0, 0, nin_++, 0, 0.0);
+  }
+  int ld(const Ct& c) { return ld(c->device()); }
+  void st(int r, double* dev) {
+    if (nout_ >= k::kMaxArr) fail(HS_E_ERROR, "fused program: too many outputs");
+    prog_.out[nout_] = dev;
+    emit(k::M_ST, -1, r, 0, nout_++, 0, 0.0);
+  }
+  int cnst(double v) {  // encrypt(v) broadcast: q(v) in policy units
+    double u = v;
+    if (p_.quantize) u = std::nearbyint(v * std::ldexp(1.0, p_.scale_bits));
+    return emit(k::M_CONST, reg(), 0, 0, 0, 0, u);
+  }
+  int add(int a, int b) { return emit(k::M_ADD, reg(), a, b, 0, 0, 0.0); }
+  int sub(int a, int b) { return emit(k::M_SUB, reg(), a, b, 0, 0, 0.0); }
+  int mul(int a, int b) { return emit(k::M_MUL, reg(), a, b, 0, 0, 0.0); }
+  int mulc(int a, double c) { return emit(k::M_MULC, reg(), a, 0, 0, 0, c); }
+  int addc(int a, double c) {
+    return emit(k::M_ADDC, reg(), a, 0, 0, 0, p_.quantize ? c * std::ldexp(1.0, p_.scale_bits) : c);
+  }
+
+  // eval_encrypted (chebyshev.hpp:171-189); bootstraps are value-identities here.
+  // The table offset (i0) and lane-split flag (b) are patched in launch().
+  int cheb(int x, const Series& s) {
+    if (!s.native()) {
+      const double span = s.hi - s.lo;
+      x = addc(mulc(x, 2.0 / span), -(s.lo + s.hi) / span);
+    }
+    if (s.degree() >= 63) big_cheb_ = true;
+    chebs_.push_back(std::make_pair(prog_.n, s));
+    return emit(k::M_CHEB, reg(), x, 0, 0, s.degree(), 0.0);
+  }
+  // newton_loop (primitives.hpp:105-132)
+  int newton(int x, int y, int n, int iters) {
+    if (iters <= 0) return y;
+    return emit(k::M_NEWTON, reg(), x, y, n, iters, (n + 1.0) / n);
+  }
+  void zapply(int mu, int inv, const std::vector<Ct>& in, const std::vector<DevBuf>& out) {
+    prog_.nchunks = static_cast<int>(in.size());
+    for (size_t c = 0; c < in.size(); ++c) {
+      prog_.zin[c] = in[c]->device();
+      prog_.zout[c] = out[c].get();
+    }
+    emit(k::M_ZAPPLY, -1, mu, inv, 0, 0, 0.0);
+  }
+
+  // ---- composite primitives -------------------------------------------------------
+  int baseline(int t, double S, int iters) {  // primitives.hpp:173-184
+    int y = cnst(1.0);
+    if (iters > 0) y = newton(mulc(t, 0.5), y, 2, iters);
+    return mulc(y, 1.0 / std::sqrt(S));
+  }
+  int invsqrt(int t, double S, const InvCfg& cfg) {  // primitives.hpp:186-208
+    if (cfg.baseline_mode) return baseline(t, S, cfg.effective_baseline_iters());
+    const Series seed = fit_scaled(TargetKind::InvSqrtShifted, S, cfg.cheb_degree);
+    int y = cheb(addc(t, -1.0), seed);
+    if (cfg.newton_iters > 0) y = newton(mulc(t, S / 2.0), y, 2, cfg.newton_iters);
+    return y;
+  }
+  int inv(int t, double S, const InvCfg& cfg) {  // primitives.hpp:211-217
+    const int y = invsqrt(t, S, cfg);
+    return mul(y, y);
+  }
+  int sqrt_(int t, double S, int degree) {  // primitives.hpp:222-238
+    const Series s = fit_scaled(TargetKind::SqrtShifted, S, degree);
+    return cheb(addc(t, -1.0), s);
+  }
+  int sign(int x, const SignCfg& cfg) {  // primitives.hpp:279-300
+    const std::vector<Series> st = sign_stages(cfg.mode, cfg.custom_polys);
+    int y = x;
+    for (int f = 0; f < cfg.folds; ++f) y = cheb(y, st[static_cast<size_t>(f) % st.size()]);
+    return y;
+  }
+
+  void launch() {
+    Runtime& rt = Runtime::get();
+    const int lanes = big_cheb_ ? rt.prog_lanes : 1;
+    int p = 0;
+    while ((1 << p) < lanes) ++p;
+    // one concatenated table per distinct series (deduplicated), cached on the
+    // device by the series' identity so steady-state calls upload nothing
+    std::string key = std::to_string(static_cast<int>(q_.mode)) + "/" + std::to_string(q_.bits) + "/" +
+                      std::to_string(lanes);
+    std::vector<std::string> ids;
+    for (auto& [ins, s] : chebs_) {
+      const int d = s.degree(), K = cheb_depth(d);
+      const bool split = lanes > 1 && d >= 2 && d == (1 << K) - 1 && K - p >= 1;
+      prog_.ins[ins].b = split ? 1 : 0;
+      std::string id = s.key;
+      if (id.empty()) {
+        id = "u" + std::string(reinterpret_cast<const char*>(s.coeffs.data()), s.coeffs.size() * sizeof(double));
+      }
+      id += split ? "/s" : "/n";
+      ids.push_back(id);
+      key += "|" + id;
+    }
+    if (!chebs_.empty()) {
+      const TableSet ts = tables(key, ids, lanes);
+      for (size_t i = 0; i < chebs_.size(); ++i) {
+        prog_.ins[chebs_[i].first].i0 = ts.off[i];
+        prog_.ins[chebs_[i].first].c = ts.fast[i] ? 1.0 : 0.0;
+      }
+      prog_.tabs = ts.dev.get();
+      prog_.ntab = ts.n;
+    }
+    k::run_prog(q_, prog_, lanes, rt.stream());
+  }
+
+ private:
+  int reg() {
+    if (nreg_ >= k::kRegs) fail(HS_E_ERROR, "fused program: register file exhausted");
+    return nreg_++;
+  }
+  int emit(int op, int dst, int a, int b, int i0, int i1, double c) {
+    if (prog_.n >= k::kMaxInst) fail(HS_E_ERROR, "fused program: too many instructions");
+    prog_.ins[prog_.n++] = k::MInst{op, dst, a, b, i0, i1, c};
+    return dst;
+  }
+
+  struct TableSet {
+    DevBuf dev;
+    std::vector<int> off;
+    std::vector<char> fast;  // magic-rounding range precondition holds (quant.cuh)
+    int n = 0;
+  };
+  TableSet tables(const std::string& key, const std::vector<std::string>& ids, int lanes) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, TableSet> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    TableSet ts;
+    std::vector<double> all;
+    std::map<std::string, int> seen;
+    for (size_t i = 0; i < chebs_.size(); ++i) {
+      // range precondition of the magic-rounding core: 1.001 * sum|c| < 2^11
+      double mag = 0.0;
+      for (double c : cheb_table(chebs_[i].second.coeffs, QSpec{QMode::None, q_.bits})) mag += std::abs(c);
+      ts.fast.push_back(std::isfinite(mag) && 1.001 * mag < 2048.0 ? 1 : 0);
+      auto f = seen.find(ids[i]);
+      if (f != seen.end()) {
+        ts.off.push_back(f->second);
+        continue;
+      }
+      std::vector<double> t = cheb_table(chebs_[i].second.coeffs, q_);
+      if (prog_.ins[chebs_[i].first].b) t = interleave(t, lanes);
+      const int off = static_cast<int>(all.size());
+      all.insert(all.end(), t.begin(), t.end());
+      seen.emplace(ids[i], off);
+      ts.off.push_back(off);
+    }
+    ts.n = static_cast<int>(all.size());
+    Runtime& rt = Runtime::get();
+    ts.dev = rt.alloc(all.size());
+    cuda_ok(cudaMemcpyAsync(ts.dev.get(), all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice,
+                            rt.stream()),
+            "series table upload");
+    rt.sync();
+    if (cache.size() > 512) cache.clear();  // in-flight users hold no reference: frees are stream-ordered
+    return cache.emplace(key, std::move(ts)).first->second;
+  }
+
+  const Params& p_;
+  QSpec q_;
+  k::Prog prog_{};
+  int nreg_ = 0, nin_ = 0, nout_ = 0;
+  bool big_cheb_ = false;
+  std::vector<std::pair<int, Series>> chebs_;
+};
+
+// ---- statistics reduction launches ------------------------------------------------------
+struct MomOut {
+  DevBuf mu, var;
+};
+
+// mean_scaled(col, Bm) and/or variance_to_scale(col, Sv) of up to two columns in one launch
+std::vector<MomOut> run_moments(hs_ctx* ctx, const std::vector<const ColC*>& cols, int mode, double Bm,
+                                double Sv) {
+  Runtime& rt = Runtime::get();
+  const size_t S = ctx->p.S;
+  std::vector<k::MomArgs> args(cols.size());
+  std::vector<MomOut> outs(cols.size());
+  for (size_t i = 0; i < cols.size(); ++i) {
+    const ColC& col = *cols[i];
+    k::MomArgs& a = args[i];
+    a.mode = mode;
+    a.nchunks = static_cast<int>(col.chunks.size());
+    for (size_t c = 0; c < col.chunks.size(); ++c) a.x[c] = col.chunks[c]->device();
+    const double n = static_cast<double>(col.n_valid);
+    a.cm = 1.0 / (Bm * static_cast<double>(col.n_valid));  // stats.hpp:101
+    a.ca = 1.0 / std::sqrt(Sv * n);                         // stats.hpp:117
+    a.cmp = 1.0 / (n * std::sqrt(Sv));                      // stats.hpp:123
+    if (mode & k::MOM_MEAN) outs[i].mu = rt.alloc(S);
+    if (mode & k::MOM_VAR) outs[i].var = rt.alloc(S);
+    a.mu = outs[i].mu.get();
+    a.var = outs[i].var.get();
+  }
+  k::moments(fused_q(ctx->p), args.data(), static_cast<int>(args.size()), S, rt.stream());
+  return outs;
+}
+
+// mean_of_chunks over centred powers (stats.hpp:56-87)
+DevBuf run_central(hs_ctx* ctx, const ColC& x, const double* mux, int power, const ColC* y, const double* muy) {
+  Runtime& rt = Runtime::get();
+  const size_t S = ctx->p.S;
+  k::CentArgs a{};
+  a.power = power;
+  a.nchunks = static_cast<int>(x.chunks.size());
+  for (size_t c = 0; c < x.chunks.size(); ++c) {
+    a.x[c] = x.chunks[c]->device();
+    a.valid[c] = flow::chunk_valid(S, x.n_valid, c);
+    if (y) a.y[c] = y->chunks[c]->device();
+  }
+  a.mux = mux;
+  a.muy = muy;
+  a.inv_n = 1.0 / static_cast<double>(x.n_valid);
+  DevBuf out = rt.alloc(S);
+  a.out = out.get();
+  k::central(fused_q(ctx->p), a, S, rt.stream());
+  return out;
+}
+
+Ct make_out(hs_ctx* ctx, const DevBuf& b, int level) { return ct_device(b, ctx->p.S, level, out_grid(ctx->p)); }
+
+}  // namespace
+
+// =====================================================================================
+Ct eval_encrypted(hs_ctx* ctx, const Series& s, const Ct& ct) {
+  if (!fusable(ctx, {&ct}) || s.coeffs.empty() || !degree_ok(s.degree())) {
+    DevB db(ctx->p, ctx->m);
+    return flow::eval_encrypted(db, s, ct);
+  }
+  auto [r, m] = ledger(ctx, Key("eval", ctx->p).ct(ct).add(s.degree()).add(s.lo).add(s.hi), [&](SymB& sb) { return flow::eval_encrypted(sb, s, sym(ct)); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.cheb(pb.ld(ct), s), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct newton_loop(hs_ctx* ctx, const Ct& x_op, const Ct& y, int n, int iters, size_t n_valid) {
+  if (!fusable(ctx, {&x_op, &y}) || n < 1 || n > k::kMaxFusedNewtonN) {
+    DevB db(ctx->p, ctx->m);
+    return flow::newton_loop(db, x_op, y, n, iters, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("newton_loop", ctx->p).ct(x_op).ct(y).add(n).add(iters).add(n_valid), [&](SymB& sb) { return flow::newton_loop(sb, sym(x_op), sym(y), n, iters, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  const int xr = pb.ld(x_op);
+  pb.st(pb.newton(xr, pb.ld(y), n, iters), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct newton_refine(hs_ctx* ctx, const Ct& x, const Ct& y0, int n, int iters, size_t n_valid) {
+  if (!fusable(ctx, {&x, &y0}) || n < 1 || n > k::kMaxFusedNewtonN) {
+    DevB db(ctx->p, ctx->m);
+    return flow::newton_refine(db, x, y0, n, iters, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("newton_refine", ctx->p).ct(x).ct(y0).add(n).add(iters).add(n_valid), [&](SymB& sb) { return flow::newton_refine(sb, sym(x), sym(y0), n, iters, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  int xr = pb.ld(x);
+  const int yr = pb.ld(y0);
+  if (n >= 2) xr = pb.mulc(xr, 1.0 / n);
+  pb.st(pb.newton(xr, yr, n, iters), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct crypto_invsqrt(hs_ctx* ctx, const Ct& ct, double S, const InvCfg& cfg, size_t n_valid) {
+  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::crypto_invsqrt(db, ct, S, cfg, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("invsqrt", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid), [&](SymB& sb) { return flow::crypto_invsqrt(sb, sym(ct), S, cfg, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.invsqrt(pb.ld(ct), S, cfg), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct baseline_invsqrt(hs_ctx* ctx, const Ct& ct, double S, int iters, size_t n_valid) {
+  if (!fusable(ctx, {&ct})) {
+    DevB db(ctx->p, ctx->m);
+    return flow::baseline_invsqrt(db, ct, S, iters, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("baseline", ctx->p).ct(ct).add(S).add(iters).add(n_valid), [&](SymB& sb) { return flow::baseline_invsqrt(sb, sym(ct), S, iters, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.baseline(pb.ld(ct), S, iters), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct crypto_inv(hs_ctx* ctx, const Ct& ct, double S, const InvCfg& cfg, size_t n_valid) {
+  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::crypto_inv(db, ct, S, cfg, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("inv", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid), [&](SymB& sb) { return flow::crypto_inv(sb, sym(ct), S, cfg, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.inv(pb.ld(ct), S, cfg), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct crypto_sqrt(hs_ctx* ctx, const Ct& ct, double S, int degree, size_t n_valid) {
+  if (!fusable(ctx, {&ct}) || !degree_ok(degree)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::crypto_sqrt(db, ct, S, degree, n_valid);
+  }
+  auto [r, m] = ledger(ctx, Key("sqrt", ctx->p).ct(ct).add(S).add(degree).add(n_valid), [&](SymB& sb) { return flow::crypto_sqrt(sb, sym(ct), S, degree, n_valid); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.sqrt_(pb.ld(ct), S, degree), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct crypto_sign(hs_ctx* ctx, const Ct& ct, const SignCfg& cfg) {
+  if (!fusable(ctx, {&ct}) || !sign_ok(cfg) || cfg.folds > 24) {
+    DevB db(ctx->p, ctx->m);
+    return flow::crypto_sign(db, ct, cfg);
+  }
+  auto [r, m] = ledger(ctx, Key("sign", ctx->p).ct(ct).sign(cfg), [&](SymB& sb) { return flow::crypto_sign(sb, sym(ct), cfg); });
+  PB pb(ctx->p);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  pb.st(pb.sign(pb.ld(ct), cfg), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+// ---- statistics ---------------------------------------------------------------------------
+Ct mean_scaled(hs_ctx* ctx, const ColC& col, double B) {
+  if (!col_ok(ctx, col, 1)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::mean_scaled(db, col, B);
+  }
+  auto [r, m] = ledger(ctx, Key("mean", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::mean_scaled(sb, sym(col), B); });
+  auto o = run_moments(ctx, {&col}, k::MOM_MEAN, B, 1.0);
+  ctx->m = m;
+  return make_out(ctx, o[0].mu, r.level);
+}
+
+Ct variance_to_scale(hs_ctx* ctx, const ColC& col, double S) {
+  if (!col_ok(ctx, col, 2)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::variance_to_scale(db, col, S);
+  }
+  auto [r, m] = ledger(ctx, Key("var_to_scale", ctx->p).col(col).add(S), [&](SymB& sb) { return flow::variance_to_scale(sb, sym(col), S); });
+  auto o = run_moments(ctx, {&col}, k::MOM_VAR, 1.0, S);
+  ctx->m = m;
+  return make_out(ctx, o[0].var, r.level);
+}
+
+Ct variance_scaled(hs_ctx* ctx, const ColC& col, double B) {
+  if (!col_ok(ctx, col, 2)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::variance_scaled(db, col, B);
+  }
+  auto [r, m] = ledger(ctx, Key("var_scaled", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::variance_scaled(sb, sym(col), B); });
+  auto o = run_moments(ctx, {&col}, k::MOM_VAR, 1.0, B * B);
+  ctx->m = m;
+  return make_out(ctx, o[0].var, r.level);
+}
+
+flow::Moments<Ct> moments(hs_ctx* ctx, const ColC& col, double B) {
+  if (!col_ok(ctx, col, 3)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::moments(db, col, B);
+  }
+  auto [r, m] = ledger(ctx, Key("moments", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::moments(sb, sym(col), B); });
+  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  ctx->m = m;
+  flow::Moments<Ct> out;
+  out.mu = make_out(ctx, o[0].mu, r.mu.level);
+  out.var = make_out(ctx, o[0].var, r.var.level);
+  out.n_valid = col.n_valid;
+  return out;
+}
+
+ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
+  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::znorm(db, col, B, cfg);
+  }
+  auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(col).add(B).cfg(cfg), [&](SymB& sb) { return flow::znorm(sb, sym(col), B, cfg); });
+  Runtime& rt = Runtime::get();
+  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  std::vector<DevBuf> outs;
+  for (size_t c = 0; c < col.chunks.size(); ++c) outs.push_back(rt.alloc(ctx->p.S));
+  PB pb(ctx->p);
+  const int var = pb.ld(o[0].var.get());
+  const int inv = pb.invsqrt(var, B * B, cfg);  // crypto_invsqrt(var, B^2)
+  const int mu = pb.ld(o[0].mu.get());
+  pb.zapply(mu, inv, col.chunks, outs);          // mul_ct(sub_ct(chunk, mu), inv)
+  pb.launch();
+  ctx->m = m;
+  ColC z;
+  z.n_valid = col.n_valid;
+  for (size_t c = 0; c < outs.size(); ++c) z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level));
+  return z;
+}
+
+static Ct std_moment(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg, int power) {
+  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg)) {
+    DevB db(ctx->p, ctx->m);
+    return flow::std_moment(db, col, B, cfg, power);
+  }
+  auto [r, m] = ledger(ctx, Key("std_moment", ctx->p).col(col).add(B).cfg(cfg).add(power), [&](SymB& sb) { return flow::std_moment(sb, sym(col), B, cfg, power); });
+  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  DevBuf num = run_central(ctx, col, o[0].mu.get(), power, nullptr, nullptr);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  PB pb(ctx->p);
+  const int inv = pb.invsqrt(pb.ld(o[0].var.get()), B * B, cfg);
+  const int inv2 = pb.mul(inv, inv);
+  const int invp = power == 4 ? pb.mul(inv2, inv2) : pb.mul(inv2, inv);
+  pb.st(pb.mul(pb.ld(num.get()), invp), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct kurtosis(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return std_moment(ctx, col, B, cfg, 4); }
+Ct skewness(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return std_moment(ctx, col, B, cfg, 3); }
+
+Ct coeff_variation(hs_ctx* ctx, const ColC& col, double B, const SignCfg& sc, const InvCfg& cfg) {
+  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg) || !degree_ok(cfg.cheb_degree) || !sign_ok(sc) || sc.folds > 24) {
+    DevB db(ctx->p, ctx->m);
+    return flow::coeff_variation(db, col, B, sc, cfg);
+  }
+  auto [r, m] = ledger(ctx, Key("cv", ctx->p).col(col).add(B).sign(sc).cfg(cfg), [&](SymB& sb) { return flow::coeff_variation(sb, sym(col), B, sc, cfg); });
+  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, B, B * B);  // mean_scaled(col, B), variance_scaled(col, B)
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  PB pb(ctx->p);
+  const int mu_b = pb.ld(o[0].mu.get());
+  const int sgn = pb.sign(mu_b, sc);
+  const int inv_mu = pb.inv(pb.mul(mu_b, sgn), B, cfg);
+  const int sigma = pb.sqrt_(pb.ld(o[0].var.get()), B * B, cfg.cheb_degree);
+  pb.st(pb.mul(pb.mul(sigma, inv_mu), sgn), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+Ct pearson(hs_ctx* ctx, const ColC& x, const ColC& y, double B, const InvCfg& cfg) {
+  if (!col_ok(ctx, x, 3) || !col_ok(ctx, y, 3) || !cfg_ok(cfg) || x.chunks.size() != y.chunks.size()) {
+    DevB db(ctx->p, ctx->m);
+    return flow::pearson(db, x, y, B, cfg);
+  }
+  auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(x).col(y).add(B).cfg(cfg), [&](SymB& sb) { return flow::pearson(sb, sym(x), sym(y), B, cfg); });
+  auto o = run_moments(ctx, {&x, &y}, k::MOM_BOTH, 1.0, B * B);
+  DevBuf cov = run_central(ctx, x, o[0].mu.get(), 2, &y, o[1].mu.get());
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  PB pb(ctx->p);
+  const int ix = pb.invsqrt(pb.ld(o[0].var.get()), B * B, cfg);
+  const int iy = pb.invsqrt(pb.ld(o[1].var.get()), B * B, cfg);
+  const int rr = pb.mul(pb.ld(cov.get()), ix);
+  pb.st(pb.mul(rr, iy), out.get());
+  pb.launch();
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
+}
+
+}  // namespace pipe
+}  // namespace hsg

@@ -1,0 +1,174 @@
+// runtime.cu — device runtime and ciphertext storage (see core.h).
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "core.h"
+
+namespace hsg {
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Params Params::from(const hs_params& p) {
+  Params r;
+  r.S = static_cast<size_t>(p.slot_count);
+  r.max_level = p.max_level;
+  r.scale_bits = p.scale_bits;
+  r.quantize = p.quantize != 0;
+  r.auto_bootstrap = p.auto_bootstrap != 0;
+  r.debug = p.debug_checks != 0;
+  return r;
+}
+
+hs_params Params::to() const {
+  hs_params p{};
+  p.slot_count = S;
+  p.max_level = max_level;
+  p.scale_bits = scale_bits;
+  p.quantize = quantize;
+  p.auto_bootstrap = auto_bootstrap;
+  p.debug_checks = debug;
+  return p;
+}
+
+// CkksParams::validate, ckks.hpp:34-39
+void Params::validate() const {
+  if (S == 0 || (S & (S - 1)) != 0) fail(HS_E_ERROR, "CkksParams: slot_count must be a power of two");
+  if (max_level < 1) fail(HS_E_ERROR, "CkksParams: max_level must be >= 1");
+  if (scale_bits < 1) fail(HS_E_ERROR, "CkksParams: scale_bits must be >= 1");
+}
+
+// ---- Runtime -------------------------------------------------------------------
+namespace {
+std::mutex g_init_mu;
+Runtime* g_rt = nullptr;
+int g_req_device = -1;
+}  // namespace
+
+Runtime::Runtime(int device) {
+  int count = 0;
+  cuda_ok(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (count == 0) fail(HS_E_CUDA, "no CUDA device visible");
+  if (device < 0) cuda_ok(cudaGetDevice(&device), "cudaGetDevice");
+  device_ = device;
+  cuda_ok(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_ok(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  if (prop.major < 10)
+    fail(HS_E_CUDA, std::string("libhestat_gpu targets sm_100a (B200); found ") + prop.name);
+  sms_ = prop.multiProcessorCount;
+  if (const char* e = std::getenv("HESTAT_LANES")) {
+    const int l = std::atoi(e);
+    if (l == 1 || l == 2 || l == 4 || l == 8) prog_lanes = l;
+  }
+  cuda_ok(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  // Keep freed blocks in the stream-ordered pool: ciphertexts are churned per op.
+  cudaMemPool_t pool;
+  cuda_ok(cudaDeviceGetDefaultMemPool(&pool, device_), "cudaDeviceGetDefaultMemPool");
+  uint64_t thr = UINT64_MAX;
+  cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "pool threshold");
+}
+
+Runtime& Runtime::get() {
+  std::lock_guard<std::mutex> g(g_init_mu);
+  if (!g_rt) g_rt = new Runtime(g_req_device);  // intentionally leaked (outlives handles)
+  return *g_rt;
+}
+
+void Runtime::init(int device) {
+  std::lock_guard<std::mutex> g(g_init_mu);
+  if (g_rt) {
+    if (g_rt->device_ != device)
+      fail(HS_E_CUDA, "hs_init: runtime already initialised on another device");
+    return;
+  }
+  g_req_device = device;
+}
+
+DevBuf Runtime::alloc(size_t n) {
+  double* p = nullptr;
+  const size_t bytes = (n ? n : 1) * sizeof(double);
+  cuda_ok(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, stream_), "cudaMallocAsync");
+  cudaStream_t s = stream_;
+  return DevBuf(p, [s](double* q) { cudaFreeAsync(q, s); });  // errors at teardown ignored
+}
+
+void Runtime::sync() { cuda_ok(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+
+const double* Runtime::table(const std::vector<double>& host) {
+  std::string key(reinterpret_cast<const char*>(host.data()), host.size() * sizeof(double));
+  std::lock_guard<std::mutex> g(tab_mu_);
+  auto it = tabs_.find(key);
+  if (it != tabs_.end()) return it->second.get();
+  DevBuf d = alloc(host.size());
+  cuda_ok(cudaMemcpyAsync(d.get(), host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice,
+                          stream_),
+          "table upload");
+  cuda_ok(cudaStreamSynchronize(stream_), "table upload sync");  // host vector may die
+  if (tabs_.size() > 4096) tabs_.clear();  // bounded: entries are tiny, keys by content
+  tabs_.emplace(std::move(key), d);
+  return d.get();
+}
+
+// ---- ciphertext storage -----------------------------------------------------------
+const double* CtData::device() const {
+  std::lock_guard<std::mutex> g(mu);
+  if (!dev) {
+    Runtime& rt = Runtime::get();
+    DevBuf d = rt.alloc(n);
+    if (n)
+      cuda_ok(cudaMemcpyAsync(d.get(), host.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                              rt.stream()),
+              "ciphertext upload");
+    const_cast<CtData*>(this)->dev = d;
+  }
+  return dev.get();
+}
+
+const std::vector<double>& CtData::host_slots() const {
+  std::lock_guard<std::mutex> g(mu);
+  if (!host_ok) {
+    host.resize(n);
+    if (n) {
+      Runtime& rt = Runtime::get();
+      cuda_ok(cudaMemcpyAsync(host.data(), dev.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                              rt.stream()),
+              "ciphertext download");
+      rt.sync();
+    }
+    host_ok = true;
+  }
+  return host;
+}
+
+void CtData::read(double* out, size_t count) const {
+  if (count == 0) return;
+  const std::vector<double>& h = host_slots();
+  std::memcpy(out, h.data(), count * sizeof(double));
+}
+
+Ct ct_device(DevBuf buf, size_t n, int level, int grid) {
+  auto c = std::make_shared<CtData>();
+  c->n = n;
+  c->level = level;
+  c->grid = grid;
+  c->dev = std::move(buf);
+  return c;
+}
+
+Ct ct_host(std::vector<double> v, int level) {
+  auto c = std::make_shared<CtData>();
+  c->n = v.size();
+  c->level = level;
+  c->grid = 0;
+  c->host = std::move(v);
+  c->host_ok = true;
+  return c;
+}
+
+Ct ct_empty() { return ct_host({}, 0); }
+
+}  // namespace hsg

@@ -174,6 +174,12 @@ def golden_cases():
     cases.append(("stat_pearson_len", "stat", P(slot_count=16), dict(which=8, x=[1, 2, 3], B=1.0, y=[1, 2], cfg=Cfg())))
     cases.append(("stat_nonfinite", "stat", P(slot_count=16), dict(which=0, x=[1, float("inf")], B=1.0, y=None, cfg=Cfg())))
     cases.append(("stat_badB", "stat", P(slot_count=16), dict(which=0, x=[1, 2], B=0.0, y=None, cfg=Cfg())))
+    # magnitudes beyond the exact-sum bound (sum|A| >= 2^52 grid units): the fused
+    # reductions must fall back to the literal rotate-and-add butterfly
+    vbig = rng.uniform(1e5, 1e6, 60)
+    for which in (0, 1, 2, 3, 5, 6, 8):
+        cases.append((f"stat{which}_bigsum", "stat", P(slot_count=64),
+                      dict(which=which, x=vbig, B=1e-2 if which != 2 else 1e-4, y=vbig[::-1].copy(), cfg=Cfg())))
     return cases
 
 
