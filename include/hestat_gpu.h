@@ -107,6 +107,15 @@ int hs_sync(void);                       /* drain the library stream */
 void* hs_stream(void);                   /* the library's cudaStream_t (for event timing) */
 int hs_set_fused(int enabled);           /* 1 (default): fused pipelines; 0: op-by-op kernels */
 uint64_t hs_kernel_launches(void);       /* kernels launched by this process so far */
+/* CUDA-graph capture of library calls (launch-bound loops): every fused entry
+ * point is capture-safe once warm (its series tables, scratch and ledger memo
+ * exist).  Handles created inside the capture and released inside it become
+ * graph allocation nodes; replaying re-executes every captured kernel. */
+typedef struct hs_graph hs_graph;
+int hs_graph_begin(void);
+int hs_graph_end(hs_graph** out);
+int hs_graph_launch(hs_graph* g);
+void hs_graph_destroy(hs_graph* g);
 /* diagnostics: FP64-pipe throughput on this GPU (kind 0 DMUL, 1 DADD, 2 DMUL+FRND, 3 DFMA),
  * instructions per second; the roofline denominator of the fused per-slot kernel */
 int hs_diag_fp64_rate(int kind, double* ops_per_s);

@@ -54,6 +54,10 @@ _SIGS = {
     "hs_set_fused": (C.c_int, [C.c_int]),
     "hs_kernel_launches": (C.c_uint64, []),
     "hs_diag_fp64_rate": (C.c_int, [C.c_int, DP]),
+    "hs_graph_begin": (C.c_int, []),
+    "hs_graph_end": (C.c_int, [C.POINTER(C.c_void_p)]),
+    "hs_graph_launch": (C.c_int, [C.c_void_p]),
+    "hs_graph_destroy": (None, [C.c_void_p]),
     "hs_params_validate": (C.c_int, [C.POINTER(hs_params)]),
     "hs_ctx_create": (C.c_int, [C.POINTER(hs_params), C.c_uint64, C.POINTER(CTX)]),
     "hs_ctx_destroy": (None, [CTX]),

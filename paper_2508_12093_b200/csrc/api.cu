@@ -583,3 +583,52 @@ int hs_plain(int which, const double* x, uint64_t n, const double* y, double* ou
 }
 
 }  // extern "C"
+
+// ---- CUDA graphs --------------------------------------------------------------------------------
+struct hs_graph {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+int hs_graph_begin(void) {
+  return guard([&] {
+    cuda_ok(cudaStreamBeginCapture(Runtime::get().stream(), cudaStreamCaptureModeRelaxed), "begin capture");
+  });
+}
+
+int hs_graph_end(hs_graph** out) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new hs_graph;
+    cudaError_t e = cudaStreamEndCapture(Runtime::get().stream(), &h->g);
+    if (e != cudaSuccess) {
+      delete h;
+      cuda_ok(e, "end capture");
+    }
+    e = cudaGraphInstantiate(&h->exec, h->g, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(h->g);
+      delete h;
+      cuda_ok(e, "graph instantiate");
+    }
+    *out = h;
+  });
+}
+
+int hs_graph_launch(hs_graph* g) {
+  return guard([&] {
+    need(g, "graph");
+    cuda_ok(cudaGraphLaunch(g->exec, Runtime::get().stream()), "graph launch");
+  });
+}
+
+void hs_graph_destroy(hs_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->g) cudaGraphDestroy(g->g);
+  delete g;
+}
+
+}  // extern "C"

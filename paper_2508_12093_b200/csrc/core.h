@@ -66,10 +66,11 @@ class Runtime {
   void note_launch(uint64_t n = 1) { launches_ += n; }
   uint64_t launches() const { return launches_.load(); }
   bool fused = true;
-  int prog_lanes = 4;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
+  int prog_lanes = 2;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
 
-  // Device copy of a host table, cached by content (coefficient tables).
-  const double* table(const std::vector<double>& host);
+  // Persistent device scratch buffer `slot` of at least n doubles (grown on
+  // demand).  All device work is ordered on one stream, so reuse is race-free.
+  double* scratch(int slot, size_t n);
 
  private:
   Runtime(int device);
@@ -77,8 +78,9 @@ class Runtime {
   int sms_ = 148;
   cudaStream_t stream_ = nullptr;
   std::atomic<uint64_t> launches_{0};
-  std::mutex tab_mu_;
-  std::unordered_map<std::string, DevBuf> tabs_;
+  std::mutex scratch_mu_;
+  DevBuf scratch_[4];
+  size_t scratch_n_[4] = {0, 0, 0, 0};
 };
 
 // ---- Ciphertext storage ------------------------------------------------------

@@ -48,7 +48,8 @@ enum MOp : int {
   M_MULC,     // r[dst] = mulc(r[a], c)
   M_CHEB,     // r[dst] = ChebEncryptedEval(table @ i0, degree i1) on r[a]
   M_NEWTON,   // r[dst] = newton_loop(x_op = r[a], y = r[b], n = i0, iters = i1, (n+1)/n = c)
-  M_ZAPPLY    // for every chunk: zout[c][slot] = out(mul(sub(in(zin[c][slot]), r[a]), r[b]))
+  M_ZAPPLY,   // for every chunk: zout[c][slot] = out(mul(sub(in(zin[c][slot]), r[a]), r[b]))
+  M_LDR       // r[dst] = per-slot statistic value i0 (stat.cu: 0 mu_x, 1 var_x, 2 mu_y, 3 var_y, 4 num)
 };
 struct MInst {
   int op, dst, a, b, i0, i1;
@@ -111,6 +112,30 @@ struct CentArgs {
   double* out = nullptr;
 };
 void central(QSpec q, const CentArgs& a, size_t S, cudaStream_t s);
+
+// ---- stat.cu: one cooperative kernel per statistic ------------------------------------
+// Phase A  moment terms of 1-2 columns (MomArgs semantics) -> grid-wide sums
+// Phase B  (power > 0) centred power sums (CentArgs semantics) -> grid-wide sum
+// Phase C  the per-slot program, with M_LDR reading the per-slot values
+//          {mu_x, var_x, mu_y, var_y, num}.
+// Each reduction is exact-sum when provable (see slotsum.cuh), else the literal
+// log2(S)-step rotate-and-add butterfly runs through global scratch with a grid
+// barrier per step.
+struct StatArgs {
+  int ncols = 1;          // 1 or 2 columns in phase A
+  int mom_mode = MOM_BOTH;
+  int nchunks = 0;
+  const double* x[kMaxChunks];
+  const double* y[kMaxChunks];
+  uint64_t valid[kMaxChunks];
+  double cm[2] = {0, 0}, ca[2] = {0, 0}, cmp[2] = {0, 0};
+  int power = 0;          // 0: no phase B; 3, 4: centred power of x; 2: x-y product (pearson)
+  double inv_n = 0;
+  double* partial = nullptr;  // >= gridDim.x * 16 doubles
+  double* scratch = nullptr;  // >= 2 * 6 * S doubles (butterfly fallback)
+};
+void run_stat(QSpec q, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s);
+size_t stat_partial_doubles();  // scratch sizing for StatArgs::partial
 
 }  // namespace k
 }  // namespace hsg

@@ -37,11 +37,11 @@ bool fusable(const hs_ctx* ctx, std::initializer_list<const Ct*> cts) {
   return true;
 }
 
-bool col_ok(const hs_ctx* ctx, const ColC& col, int arrays) {
+bool col_ok(const hs_ctx* ctx, const ColC& col) {
   const Params& p = ctx->p;
   if (p.debug || !Runtime::get().fused) return false;
   if (col.chunks.empty() || col.chunks.size() > static_cast<size_t>(k::kMaxChunks)) return false;
-  if (p.S > k::slot_sum_max(arrays)) return false;
+  if (p.S > (1u << 24)) return false;
   for (const Ct& c : col.chunks)
     if (!ct_ok(p, c)) return false;
   return true;
@@ -193,6 +193,7 @@ class PB {
     if (p_.quantize) u = std::nearbyint(v * std::ldexp(1.0, p_.scale_bits));
     return emit(k::M_CONST, reg(), 0, 0, 0, 0, u);
   }
+  int ldr(int k) { return emit(k::M_LDR, reg(), 0, 0, k, 0, 0.0); }  // per-slot statistic value
   int add(int a, int b) { return emit(k::M_ADD, reg(), a, b, 0, 0, 0.0); }
   int sub(int a, int b) { return emit(k::M_SUB, reg(), a, b, 0, 0, 0.0); }
   int mul(int a, int b) { return emit(k::M_MUL, reg(), a, b, 0, 0, 0.0); }
@@ -254,7 +255,11 @@ class PB {
     return y;
   }
 
-  void launch() {
+  void launch() { finish(false, nullptr); }
+  void launch_stat(const k::StatArgs& a) { finish(true, &a); }
+
+ private:
+  void finish(bool stat, const k::StatArgs* a) {
     Runtime& rt = Runtime::get();
     const int lanes = big_cheb_ ? rt.prog_lanes : 1;
     int p = 0;
@@ -285,10 +290,10 @@ class PB {
       prog_.tabs = ts.dev.get();
       prog_.ntab = ts.n;
     }
-    k::run_prog(q_, prog_, lanes, rt.stream());
+    if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
+    else k::run_prog(q_, prog_, lanes, rt.stream());
   }
 
- private:
   int reg() {
     if (nreg_ >= k::kRegs) fail(HS_E_ERROR, "fused program: register file exhausted");
     return nreg_++;
@@ -350,56 +355,29 @@ class PB {
   std::vector<std::pair<int, Series>> chebs_;
 };
 
-// ---- statistics reduction launches ------------------------------------------------------
-struct MomOut {
-  DevBuf mu, var;
-};
-
-// mean_scaled(col, Bm) and/or variance_to_scale(col, Sv) of up to two columns in one launch
-std::vector<MomOut> run_moments(hs_ctx* ctx, const std::vector<const ColC*>& cols, int mode, double Bm,
-                                double Sv) {
+// ---- statistics: one cooperative launch per call (stat.cu) ------------------------------
+// StatArgs for phase A over one or two columns: mean_scaled(col, Bm) and/or
+// variance_to_scale(col, Sv) terms (stats.hpp:97-126).
+k::StatArgs stat_args(hs_ctx* ctx, const std::vector<const ColC*>& cols, int mode, double Bm, double Sv) {
   Runtime& rt = Runtime::get();
   const size_t S = ctx->p.S;
-  std::vector<k::MomArgs> args(cols.size());
-  std::vector<MomOut> outs(cols.size());
+  k::StatArgs a{};
+  a.ncols = static_cast<int>(cols.size());
+  a.mom_mode = mode;
+  a.nchunks = static_cast<int>(cols[0]->chunks.size());
   for (size_t i = 0; i < cols.size(); ++i) {
     const ColC& col = *cols[i];
-    k::MomArgs& a = args[i];
-    a.mode = mode;
-    a.nchunks = static_cast<int>(col.chunks.size());
-    for (size_t c = 0; c < col.chunks.size(); ++c) a.x[c] = col.chunks[c]->device();
+    for (size_t c = 0; c < col.chunks.size(); ++c) (i == 0 ? a.x : a.y)[c] = col.chunks[c]->device();
     const double n = static_cast<double>(col.n_valid);
-    a.cm = 1.0 / (Bm * static_cast<double>(col.n_valid));  // stats.hpp:101
-    a.ca = 1.0 / std::sqrt(Sv * n);                         // stats.hpp:117
-    a.cmp = 1.0 / (n * std::sqrt(Sv));                      // stats.hpp:123
-    if (mode & k::MOM_MEAN) outs[i].mu = rt.alloc(S);
-    if (mode & k::MOM_VAR) outs[i].var = rt.alloc(S);
-    a.mu = outs[i].mu.get();
-    a.var = outs[i].var.get();
+    a.cm[i] = 1.0 / (Bm * static_cast<double>(col.n_valid));  // stats.hpp:101
+    a.ca[i] = 1.0 / std::sqrt(Sv * n);                         // stats.hpp:117
+    a.cmp[i] = 1.0 / (n * std::sqrt(Sv));                      // stats.hpp:123
   }
-  k::moments(fused_q(ctx->p), args.data(), static_cast<int>(args.size()), S, rt.stream());
-  return outs;
-}
-
-// mean_of_chunks over centred powers (stats.hpp:56-87)
-DevBuf run_central(hs_ctx* ctx, const ColC& x, const double* mux, int power, const ColC* y, const double* muy) {
-  Runtime& rt = Runtime::get();
-  const size_t S = ctx->p.S;
-  k::CentArgs a{};
-  a.power = power;
-  a.nchunks = static_cast<int>(x.chunks.size());
-  for (size_t c = 0; c < x.chunks.size(); ++c) {
-    a.x[c] = x.chunks[c]->device();
-    a.valid[c] = flow::chunk_valid(S, x.n_valid, c);
-    if (y) a.y[c] = y->chunks[c]->device();
-  }
-  a.mux = mux;
-  a.muy = muy;
-  a.inv_n = 1.0 / static_cast<double>(x.n_valid);
-  DevBuf out = rt.alloc(S);
-  a.out = out.get();
-  k::central(fused_q(ctx->p), a, S, rt.stream());
-  return out;
+  for (size_t c = 0; c < cols[0]->chunks.size(); ++c) a.valid[c] = flow::chunk_valid(S, cols[0]->n_valid, c);
+  a.inv_n = 1.0 / static_cast<double>(cols[0]->n_valid);  // mean_of_chunks, stats.hpp:83
+  a.partial = rt.scratch(0, k::stat_partial_doubles());
+  a.scratch = rt.scratch(1, 24 * S);
+  return a;
 }
 
 Ct make_out(hs_ctx* ctx, const DevBuf& b, int level) { return ct_device(b, ctx->p.S, level, out_grid(ctx->p)); }
@@ -525,69 +503,80 @@ Ct crypto_sign(hs_ctx* ctx, const Ct& ct, const SignCfg& cfg) {
 
 // ---- statistics ---------------------------------------------------------------------------
 Ct mean_scaled(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col, 1)) {
+  if (!col_ok(ctx, col)) {
     DevB db(ctx->p, ctx->m);
     return flow::mean_scaled(db, col, B);
   }
   auto [r, m] = ledger(ctx, Key("mean", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::mean_scaled(sb, sym(col), B); });
-  auto o = run_moments(ctx, {&col}, k::MOM_MEAN, B, 1.0);
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  PB pb(ctx->p);
+  pb.st(pb.ldr(0), out.get());
+  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_MEAN, B, 1.0));
   ctx->m = m;
-  return make_out(ctx, o[0].mu, r.level);
+  return make_out(ctx, out, r.level);
+}
+
+static Ct variance_impl(hs_ctx* ctx, const ColC& col, double S, const Key& key, bool scaled, double B) {
+  auto [r, m] = ledger(ctx, key, [&](SymB& sb) {
+    return scaled ? flow::variance_scaled(sb, sym(col), B) : flow::variance_to_scale(sb, sym(col), S);
+  });
+  DevBuf out = Runtime::get().alloc(ctx->p.S);
+  PB pb(ctx->p);
+  pb.st(pb.ldr(1), out.get());
+  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_VAR, 1.0, S));
+  ctx->m = m;
+  return make_out(ctx, out, r.level);
 }
 
 Ct variance_to_scale(hs_ctx* ctx, const ColC& col, double S) {
-  if (!col_ok(ctx, col, 2)) {
+  if (!col_ok(ctx, col)) {
     DevB db(ctx->p, ctx->m);
     return flow::variance_to_scale(db, col, S);
   }
-  auto [r, m] = ledger(ctx, Key("var_to_scale", ctx->p).col(col).add(S), [&](SymB& sb) { return flow::variance_to_scale(sb, sym(col), S); });
-  auto o = run_moments(ctx, {&col}, k::MOM_VAR, 1.0, S);
-  ctx->m = m;
-  return make_out(ctx, o[0].var, r.level);
+  return variance_impl(ctx, col, S, Key("var_to_scale", ctx->p).col(col).add(S), false, 0.0);
 }
 
 Ct variance_scaled(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col, 2)) {
+  if (!col_ok(ctx, col)) {
     DevB db(ctx->p, ctx->m);
     return flow::variance_scaled(db, col, B);
   }
-  auto [r, m] = ledger(ctx, Key("var_scaled", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::variance_scaled(sb, sym(col), B); });
-  auto o = run_moments(ctx, {&col}, k::MOM_VAR, 1.0, B * B);
-  ctx->m = m;
-  return make_out(ctx, o[0].var, r.level);
+  return variance_impl(ctx, col, B * B, Key("var_scaled", ctx->p).col(col).add(B), true, B);
 }
 
 flow::Moments<Ct> moments(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col, 3)) {
+  if (!col_ok(ctx, col)) {
     DevB db(ctx->p, ctx->m);
     return flow::moments(db, col, B);
   }
   auto [r, m] = ledger(ctx, Key("moments", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::moments(sb, sym(col), B); });
-  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  Runtime& rt = Runtime::get();
+  DevBuf mu = rt.alloc(ctx->p.S), var = rt.alloc(ctx->p.S);
+  PB pb(ctx->p);
+  pb.st(pb.ldr(0), mu.get());
+  pb.st(pb.ldr(1), var.get());
+  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
   ctx->m = m;
   flow::Moments<Ct> out;
-  out.mu = make_out(ctx, o[0].mu, r.mu.level);
-  out.var = make_out(ctx, o[0].var, r.var.level);
+  out.mu = make_out(ctx, mu, r.mu.level);
+  out.var = make_out(ctx, var, r.var.level);
   out.n_valid = col.n_valid;
   return out;
 }
 
 ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
-  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg)) {
+  if (!col_ok(ctx, col) || !cfg_ok(cfg)) {
     DevB db(ctx->p, ctx->m);
     return flow::znorm(db, col, B, cfg);
   }
   auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(col).add(B).cfg(cfg), [&](SymB& sb) { return flow::znorm(sb, sym(col), B, cfg); });
   Runtime& rt = Runtime::get();
-  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
   std::vector<DevBuf> outs;
   for (size_t c = 0; c < col.chunks.size(); ++c) outs.push_back(rt.alloc(ctx->p.S));
   PB pb(ctx->p);
-  const int var = pb.ld(o[0].var.get());
-  const int inv = pb.invsqrt(var, B * B, cfg);  // crypto_invsqrt(var, B^2)
-  const int mu = pb.ld(o[0].mu.get());
-  pb.zapply(mu, inv, col.chunks, outs);          // mul_ct(sub_ct(chunk, mu), inv)
-  pb.launch();
+  const int inv = pb.invsqrt(pb.ldr(1), B * B, cfg);  // crypto_invsqrt(var, B^2)
+  pb.zapply(pb.ldr(0), inv, col.chunks, outs);        // mul_ct(sub_ct(chunk, mu), inv)
+  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
   ctx->m = m;
   ColC z;
   z.n_valid = col.n_valid;
@@ -596,20 +585,21 @@ ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
 }
 
 static Ct std_moment(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg, int power) {
-  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg)) {
+  if (!col_ok(ctx, col) || !cfg_ok(cfg)) {
     DevB db(ctx->p, ctx->m);
     return flow::std_moment(db, col, B, cfg, power);
   }
-  auto [r, m] = ledger(ctx, Key("std_moment", ctx->p).col(col).add(B).cfg(cfg).add(power), [&](SymB& sb) { return flow::std_moment(sb, sym(col), B, cfg, power); });
-  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
-  DevBuf num = run_central(ctx, col, o[0].mu.get(), power, nullptr, nullptr);
+  auto [r, m] = ledger(ctx, Key("std_moment", ctx->p).col(col).add(B).cfg(cfg).add(power),
+                       [&](SymB& sb) { return flow::std_moment(sb, sym(col), B, cfg, power); });
   DevBuf out = Runtime::get().alloc(ctx->p.S);
   PB pb(ctx->p);
-  const int inv = pb.invsqrt(pb.ld(o[0].var.get()), B * B, cfg);
+  const int inv = pb.invsqrt(pb.ldr(1), B * B, cfg);
   const int inv2 = pb.mul(inv, inv);
   const int invp = power == 4 ? pb.mul(inv2, inv2) : pb.mul(inv2, inv);
-  pb.st(pb.mul(pb.ld(num.get()), invp), out.get());
-  pb.launch();
+  pb.st(pb.mul(pb.ldr(4), invp), out.get());  // mul_ct(numerator, inv^p)
+  k::StatArgs a = stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  a.power = power;
+  pb.launch_stat(a);
   ctx->m = m;
   return make_out(ctx, out, r.level);
 }
@@ -618,39 +608,39 @@ Ct kurtosis(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return 
 Ct skewness(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return std_moment(ctx, col, B, cfg, 3); }
 
 Ct coeff_variation(hs_ctx* ctx, const ColC& col, double B, const SignCfg& sc, const InvCfg& cfg) {
-  if (!col_ok(ctx, col, 3) || !cfg_ok(cfg) || !degree_ok(cfg.cheb_degree) || !sign_ok(sc) || sc.folds > 24) {
+  if (!col_ok(ctx, col) || !cfg_ok(cfg) || !degree_ok(cfg.cheb_degree) || !sign_ok(sc) || sc.folds > 24) {
     DevB db(ctx->p, ctx->m);
     return flow::coeff_variation(db, col, B, sc, cfg);
   }
-  auto [r, m] = ledger(ctx, Key("cv", ctx->p).col(col).add(B).sign(sc).cfg(cfg), [&](SymB& sb) { return flow::coeff_variation(sb, sym(col), B, sc, cfg); });
-  auto o = run_moments(ctx, {&col}, k::MOM_BOTH, B, B * B);  // mean_scaled(col, B), variance_scaled(col, B)
+  auto [r, m] = ledger(ctx, Key("cv", ctx->p).col(col).add(B).sign(sc).cfg(cfg),
+                       [&](SymB& sb) { return flow::coeff_variation(sb, sym(col), B, sc, cfg); });
   DevBuf out = Runtime::get().alloc(ctx->p.S);
   PB pb(ctx->p);
-  const int mu_b = pb.ld(o[0].mu.get());
+  const int mu_b = pb.ldr(0);  // mean_scaled(col, B)
   const int sgn = pb.sign(mu_b, sc);
   const int inv_mu = pb.inv(pb.mul(mu_b, sgn), B, cfg);
-  const int sigma = pb.sqrt_(pb.ld(o[0].var.get()), B * B, cfg.cheb_degree);
+  const int sigma = pb.sqrt_(pb.ldr(1), B * B, cfg.cheb_degree);  // variance_scaled(col, B)
   pb.st(pb.mul(pb.mul(sigma, inv_mu), sgn), out.get());
-  pb.launch();
+  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, B, B * B));
   ctx->m = m;
   return make_out(ctx, out, r.level);
 }
 
 Ct pearson(hs_ctx* ctx, const ColC& x, const ColC& y, double B, const InvCfg& cfg) {
-  if (!col_ok(ctx, x, 3) || !col_ok(ctx, y, 3) || !cfg_ok(cfg) || x.chunks.size() != y.chunks.size()) {
+  if (!col_ok(ctx, x) || !col_ok(ctx, y) || !cfg_ok(cfg) || x.chunks.size() != y.chunks.size()) {
     DevB db(ctx->p, ctx->m);
     return flow::pearson(db, x, y, B, cfg);
   }
-  auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(x).col(y).add(B).cfg(cfg), [&](SymB& sb) { return flow::pearson(sb, sym(x), sym(y), B, cfg); });
-  auto o = run_moments(ctx, {&x, &y}, k::MOM_BOTH, 1.0, B * B);
-  DevBuf cov = run_central(ctx, x, o[0].mu.get(), 2, &y, o[1].mu.get());
+  auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(x).col(y).add(B).cfg(cfg),
+                       [&](SymB& sb) { return flow::pearson(sb, sym(x), sym(y), B, cfg); });
   DevBuf out = Runtime::get().alloc(ctx->p.S);
   PB pb(ctx->p);
-  const int ix = pb.invsqrt(pb.ld(o[0].var.get()), B * B, cfg);
-  const int iy = pb.invsqrt(pb.ld(o[1].var.get()), B * B, cfg);
-  const int rr = pb.mul(pb.ld(cov.get()), ix);
-  pb.st(pb.mul(rr, iy), out.get());
-  pb.launch();
+  const int ix = pb.invsqrt(pb.ldr(1), B * B, cfg);
+  const int iy = pb.invsqrt(pb.ldr(3), B * B, cfg);
+  pb.st(pb.mul(pb.mul(pb.ldr(4), ix), iy), out.get());  // mul_ct(mul_ct(cov, inv_x), inv_y)
+  k::StatArgs a = stat_args(ctx, {&x, &y}, k::MOM_BOTH, 1.0, B * B);
+  a.power = 2;
+  pb.launch_stat(a);
   ctx->m = m;
   return make_out(ctx, out, r.level);
 }

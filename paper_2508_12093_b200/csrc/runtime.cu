@@ -98,19 +98,13 @@ DevBuf Runtime::alloc(size_t n) {
 
 void Runtime::sync() { cuda_ok(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
-const double* Runtime::table(const std::vector<double>& host) {
-  std::string key(reinterpret_cast<const char*>(host.data()), host.size() * sizeof(double));
-  std::lock_guard<std::mutex> g(tab_mu_);
-  auto it = tabs_.find(key);
-  if (it != tabs_.end()) return it->second.get();
-  DevBuf d = alloc(host.size());
-  cuda_ok(cudaMemcpyAsync(d.get(), host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice,
-                          stream_),
-          "table upload");
-  cuda_ok(cudaStreamSynchronize(stream_), "table upload sync");  // host vector may die
-  if (tabs_.size() > 4096) tabs_.clear();  // bounded: entries are tiny, keys by content
-  tabs_.emplace(std::move(key), d);
-  return d.get();
+double* Runtime::scratch(int slot, size_t n) {
+  std::lock_guard<std::mutex> g(scratch_mu_);
+  if (scratch_n_[slot] < n) {
+    scratch_[slot] = alloc(n);  // the old buffer is freed stream-ordered
+    scratch_n_[slot] = n;
+  }
+  return scratch_[slot].get();
 }
 
 // ---- ciphertext storage -----------------------------------------------------------

@@ -1,0 +1,282 @@
+// stat.cu — one cooperative kernel per encrypted statistic (stats.hpp:97-265).
+//
+// A statistic is slot-wise work separated by rotate-and-sum reductions.  Every
+// kernel launch costs ~3 us of device time back to back on B200, and a
+// cluster-local reduction keeps 140 of 148 SMs idle, so each statistic runs as
+// ONE grid-wide cooperative kernel over all SMs:
+//
+//   phase A  per slot, the moment terms of 1-2 columns (mean, squared, mean
+//            part: stats.hpp:41-51, 110-126), summed grid-wide;   grid.sync
+//   phase B  (kurtosis / skewness / pearson) per slot, the centred power or
+//            product terms using phase A's mean (stats.hpp:56-87), summed
+//            grid-wide;                                           grid.sync
+//   phase C  per slot, the fused program (prog.cuh): inverse square root of
+//            the variance and the statistic's epilogue, written straight to the
+//            output ciphertext(s).
+//
+// Reductions: in grid units every term is an integer; when the grid-wide sum
+// of |terms| is provably < 2^53 every addition of the reference's log2(S)-step
+// rotate-and-add is exact, so every slot's result is the exact total (see
+// slotsum.cuh) and one deterministic reduction suffices.  Otherwise (huge
+// magnitudes, or quantize off) the literal butterfly runs through global
+// scratch, one grid barrier per step — bit-identical either way.
+#include <cooperative_groups.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "core.h"
+#include "kernels.h"
+#include "prog.cuh"
+#include "quant.cuh"
+
+namespace hsg {
+namespace k {
+namespace {
+namespace cg = cooperative_groups;
+
+constexpr int kMaxWarps = 32;
+constexpr int kNK = 6;  // reduction arrays: up to 3 per column, 2 columns
+
+struct Reduced {
+  bool uniform;         // exact-sum: every slot holds tot[k]
+  double tot[kNK];
+  const double* res;    // otherwise: butterfly result, array k at res + k * S
+};
+
+// Grid-wide rotate-and-sum of NK per-slot term arrays produced by terms(i, t).
+template <class Q, class TermFn>
+__device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int NK, unsigned S,
+                            double* partial, double* scratch) {
+  __shared__ double red[kMaxWarps][2 * kNK];
+  __shared__ double tot[2 * kNK];
+  const Range BR = block_range(S);
+  Reduced R{};
+  R.res = nullptr;
+  if constexpr (Q::kExactSum) {
+    double acc[2 * kNK];
+#pragma unroll
+    for (int k = 0; k < 2 * kNK; ++k) acc[k] = 0.0;
+    for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
+      double t[kNK];
+      terms(i, t);
+#pragma unroll
+      for (int k = 0; k < kNK; ++k)
+        if (k < NK) {
+          acc[2 * k] += t[k];
+          acc[2 * k + 1] += fabs(t[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * kNK; ++k)
+      for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < 2 * kNK; ++k) red[threadIdx.x >> 5][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < 2 * NK) {
+      double s = 0.0;
+      for (unsigned w = 0; w < blockDim.x / 32; ++w) s += red[w][threadIdx.x];
+      partial[blockIdx.x * 2 * kNK + threadIdx.x] = s;
+    }
+    grid.sync();
+    if (threadIdx.x < 2 * NK) {  // every block sums the partials in the same order
+      double s = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partial + b * 2 * kNK + threadIdx.x);
+      tot[threadIdx.x] = s;
+    }
+    __syncthreads();
+    bool exact = true;
+    for (int k = 0; k < NK; ++k) {
+      R.tot[k] = tot[2 * k];
+      exact = exact && tot[2 * k + 1] < 4503599627370496.0;  // 2^52: true sum < 2^53
+    }
+    __syncthreads();
+    if (exact) {
+      R.uniform = true;
+      return R;
+    }
+  }
+  // literal butterfly (ckks.hpp:218-230) through global memory
+  double* cur = scratch;
+  double* nxt = scratch + static_cast<size_t>(kNK) * S;
+  for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
+    double t[kNK];
+    terms(i, t);
+    for (int k = 0; k < NK; ++k) cur[static_cast<size_t>(k) * S + i] = t[k];
+  }
+  grid.sync();
+  for (unsigned d = 1; d < S; d <<= 1) {
+    for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
+      const unsigned j = (i + d) & (S - 1);
+      for (int k = 0; k < NK; ++k)
+        nxt[static_cast<size_t>(k) * S + i] =
+            q.add(__ldcg(cur + static_cast<size_t>(k) * S + i), __ldcg(cur + static_cast<size_t>(k) * S + j));
+    }
+    grid.sync();
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  R.uniform = false;
+  R.res = cur;
+  return R;
+}
+
+__device__ __forceinline__ double pick(const Reduced& R, int k, unsigned S, unsigned i) {
+  return R.uniform ? R.tot[k] : __ldcg(R.res + static_cast<size_t>(k) * S + i);
+}
+
+template <class Q, int P>
+__global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __grid_constant__ StatArgs a,
+                                                       const __grid_constant__ Prog pg) {
+  extern __shared__ double stab[];
+  cg::grid_group grid = cg::this_grid();
+  for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
+  __syncthreads();
+  const unsigned S = pg.S;
+  const int per_col = (a.mom_mode & MOM_MEAN ? 1 : 0) + (a.mom_mode & MOM_VAR ? 2 : 0);
+  const int NA = per_col * a.ncols;
+
+  // ---- phase A: moment terms (MomArgs semantics) ----
+  auto termsA = [&](unsigned i, double* t) {
+    for (int col = 0; col < a.ncols; ++col) {
+      double* tc = t + col * per_col;
+      for (int c = 0; c < a.nchunks; ++c) {
+        const double X = q.in(__ldg((col == 0 ? a.x[c] : a.y[c]) + i));
+        double v[3];
+        int k = 0;
+        if (a.mom_mode & MOM_MEAN) v[k++] = q.mulc(X, a.cm[col]);  // mul_pt(chunk, 1/(B n))
+        if (a.mom_mode & MOM_VAR) {
+          const double s = q.mulc(X, a.ca[col]);                   // mul_pt(chunk, 1/sqrt(S n))
+          v[k++] = q.mul(s, s);                                    // mul_ct(a, a)
+          v[k++] = q.mulc(X, a.cmp[col]);                          // mul_pt(chunk, 1/(n sqrt(S)))
+        }
+        for (int j = 0; j < per_col; ++j) tc[j] = c == 0 ? v[j] : q.add(tc[j], v[j]);
+      }
+    }
+  };
+  const Reduced RA = grid_sum(q, grid, termsA, NA, S, a.partial, a.scratch);
+
+  // per-slot statistic values {mu_x, var_x, mu_y, var_y}
+  auto mom = [&](unsigned i, double* sv) {
+    for (int col = 0; col < a.ncols; ++col) {
+      const int b0 = col * per_col;
+      int k = 0;
+      if (a.mom_mode & MOM_MEAN) sv[2 * col] = pick(RA, b0 + k++, S, i);
+      if (a.mom_mode & MOM_VAR) {
+        const double sq = pick(RA, b0 + k, S, i), mp = pick(RA, b0 + k + 1, S, i);
+        sv[2 * col + 1] = q.sub(sq, q.mul(mp, mp));  // sub_ct(sq_sum, mul_ct(mp, mp))
+      }
+    }
+  };
+
+  // ---- phase B: centred power / product terms (CentArgs semantics) ----
+  Reduced RB{};
+  RB.uniform = true;
+  RB.tot[0] = 0.0;
+  if (a.power > 0) {
+    auto termsB = [&](unsigned i, double* t) {
+      double sv[4];
+      mom(i, sv);
+      const double mux = sv[0], muy = sv[2];
+      for (int c = 0; c < a.nchunks; ++c) {
+        const double mm = a.valid[c] < S ? q.mulc(mux, i < a.valid[c] ? 1.0 : 0.0) : mux;  // mul_pt(mu, mask)
+        const double cx = q.sub(q.in(__ldg(a.x[c] + i)), mm);
+        double p;
+        if (a.power == 4) {
+          const double sq = q.mul(cx, cx);
+          p = q.mul(sq, sq);
+        } else if (a.power == 3) {
+          const double sq = q.mul(cx, cx);
+          p = q.mul(sq, cx);
+        } else {
+          p = q.mul(cx, q.sub(q.in(__ldg(a.y[c] + i)), muy));
+        }
+        const double term = q.mulc(p, a.inv_n);  // mean_of_chunks: mul_pt(chunk, 1/n)
+        t[0] = c == 0 ? term : q.add(t[0], term);
+      }
+    };
+    RB = grid_sum(q, grid, termsB, 1, S, a.partial + gridDim.x * 2 * kNK,
+                  a.scratch + 2 * static_cast<size_t>(kNK) * S);
+  }
+
+  // ---- phase C: the per-slot program over this block's slot range ----
+  const Range R = block_range(S);
+  if (R.lo >= R.hi) return;
+  const unsigned iters = (R.spb * P + blockDim.x - 1) / blockDim.x;
+  for (unsigned it = 0; it < iters; ++it) {
+    const unsigned g = threadIdx.x + it * blockDim.x;
+    const unsigned slot = R.lo + g / P;
+    const bool live = slot < R.hi;
+    const unsigned s = live ? slot : R.hi - 1;
+    double sv[5];
+    mom(s, sv);
+    sv[4] = a.power > 0 ? pick(RB, 0, S, s) : 0.0;
+    exec<Q, P>(q, pg, stab, s, static_cast<int>(g % P), live, sv);
+  }
+}
+
+template <class F>
+void with_q(QSpec qs, F&& f) {
+  const double s = ldexp(1.0, qs.bits), inv = ldexp(1.0, -qs.bits);
+  switch (qs.mode) {
+    case QMode::None: f(QNone{}); break;
+    case QMode::Grid: f(QGrid{s, inv}); break;
+    default: fail(HS_E_ERROR, "stat kernels take QNone or QGrid only");
+  }
+}
+
+std::mutex g_occ_mu;
+std::unordered_map<const void*, std::unordered_map<size_t, int>> g_occ;
+
+template <class K>
+int max_blocks(K kern, size_t smem, int threads) {
+  std::lock_guard<std::mutex> g(g_occ_mu);
+  auto& m = g_occ[reinterpret_cast<const void*>(kern)];
+  const size_t key = smem * 2048 + static_cast<size_t>(threads);
+  auto it = m.find(key);
+  if (it != m.end()) return it->second;
+  if (smem > 48 * 1024)
+    cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+            "stat smem attr");
+  int per_sm = 0;
+  cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "stat occupancy");
+  const int n = per_sm * Runtime::get().sm_count();
+  m.emplace(key, n);
+  return n;
+}
+
+}  // namespace
+
+size_t stat_partial_doubles() { return 2 * 2 * kNK * static_cast<size_t>(Runtime::get().sm_count()) * 32; }
+
+void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s) {
+  if (p.S == 0) return;
+  with_q(qs, [&](auto Q) {
+    using QT = decltype(Q);
+    const size_t smem = static_cast<size_t>(p.ntab) * sizeof(double);
+    auto go = [&](auto kern, int P) {
+      const int maxt = P == 1 ? prog_max_threads<1>() : (P == 2 ? prog_max_threads<2>() : prog_max_threads<4>());
+      const Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+      const int cap = max_blocks(kern, smem, static_cast<int>(geo.threads));
+      if (cap < static_cast<int>(geo.blocks)) fail(HS_E_CUDA, "stat kernel: grid not co-resident");
+      const int grid = static_cast<int>(geo.blocks);
+      QT qv = Q;
+      StatArgs av = a;
+      Prog pv = p;
+      void* args[] = {&qv, &av, &pv};
+      cuda_ok(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(geo.threads), args,
+                                          smem, s),
+              "stat launch");
+    };
+    if (lanes == 8) go(k_stat<QT, 8>, 8);
+    else if (lanes == 4) go(k_stat<QT, 4>, 4);
+    else if (lanes == 2) go(k_stat<QT, 2>, 2);
+    else go(k_stat<QT, 1>, 1);
+  });
+  Runtime::get().note_launch();
+}
+
+}  // namespace k
+}  // namespace hsg

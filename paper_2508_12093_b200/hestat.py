@@ -574,3 +574,36 @@ def set_fused(enabled: bool) -> None:
 
 def kernel_launches() -> int:
     return int(_abi.lib().hs_kernel_launches())
+
+
+class Graph:
+    """CUDA graph of captured library calls (``with Graph() as g: ...; g.launch()``).
+
+    Capture only warm calls (same shapes already executed once) and release the
+    captured calls' outputs inside the ``with`` block."""
+
+    def __init__(self):
+        self._h = None
+
+    def __enter__(self):
+        _check(_abi.lib().hs_graph_begin())
+        return self
+
+    def __exit__(self, et, ev, tb):
+        h = C.c_void_p()
+        rc = _abi.lib().hs_graph_end(C.byref(h))
+        if et is None:
+            _check(rc)
+            self._h = h
+        return False
+
+    def launch(self) -> None:
+        _check(_abi.lib().hs_graph_launch(self._h))
+
+    def __del__(self):
+        try:
+            if self._h is not None and self._h.value and _abi._lib is not None:
+                _abi._lib.hs_graph_destroy(self._h)
+        except Exception:
+            pass
+        self._h = None

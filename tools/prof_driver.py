@@ -1,6 +1,6 @@
 """Profiling driver (run under ncu on the GPU box): a few C2 znorm calls."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2508_12093_b200 import hestat as H
 from paper_2508_12093_b200 import workloads as W
