@@ -354,12 +354,8 @@ int hs_encode_column(hs_ctx* c, const double* v, uint64_t n, hs_ct** chunks_out,
       need(v, "values");
       need(chunks_out, "chunks_out");
     }
-    for (uint64_t i = 0; i < n; ++i)
-      if (!std::isfinite(v[i])) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
     DevB db(cc->p, cc->m);
-    const size_t S = cc->p.S;
-    std::vector<Ct> chunks;
-    for (size_t off = 0; off < n; off += S) chunks.push_back(db.encrypt(v + off, std::min<size_t>(S, n - off)));
+    std::vector<Ct> chunks = db.encrypt_column(v, static_cast<size_t>(n));
     for (size_t i = 0; i < chunks.size(); ++i) chunks_out[i] = wrap(chunks[i]);
     *n_chunks = chunks.size();
   });
@@ -376,10 +372,11 @@ int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
       const size_t take = std::min(S, remaining);
       const Ct& x = get(col->chunks[i]);
       if (take > x->n) fail(HS_E_LENGTH_MISMATCH, "decode_column: chunk shorter than slot count");
-      x->read(out + o, take);
+      if (take) x->read_async(out + o, take, 0);
       o += take;
       remaining -= take;
     }
+    Runtime::get().sync();
   });
 }
 

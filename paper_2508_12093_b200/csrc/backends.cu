@@ -11,22 +11,60 @@ DevB::DevB(const Params& p, Meter& m) : LedgerBase(p, m) {
   qs_.bits = p.scale_bits;
 }
 
+namespace {
+// Where the device can read the caller's buffer directly (pinned, host-mapped
+// under UVA) the encrypt kernel reads it zero-copy; otherwise stage it through
+// a device buffer.  Returns the device-visible source pointer.
+const double* device_source(const double* v, size_t n, DevBuf* stage, bool* pinned) {
+  Runtime& rt = Runtime::get();
+  cudaPointerAttributes at{};
+  *pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (*pinned && at.devicePointer) return static_cast<const double*>(at.devicePointer);
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return v;
+  *stage = rt.alloc(n);
+  cuda_ok(cudaMemcpyAsync(stage->get(), v, n * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
+          "encrypt upload");
+  return stage->get();
+}
+
+int* bad_flag() {  // host-mapped pinned flag word, one per thread
+  thread_local int* f = nullptr;
+  if (!f) cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&f), sizeof(int), cudaHostAllocMapped), "flag alloc");
+  return f;
+}
+}  // namespace
+
 Ct DevB::encrypt(const double* v, size_t n) const {
   if (n > p_.S) fail(HS_E_TOO_MANY_VALUES, "encrypt: more values than slots");
   Runtime& rt = Runtime::get();
   DevBuf d = rt.alloc(p_.S);
-  if (n) {
-    cudaPointerAttributes at{};
-    const bool pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    cuda_ok(cudaMemcpyAsync(d.get(), v, n * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
-            "encrypt upload");
-    if (pinned) rt.sync();  // the caller may reuse its pinned buffer on return
-  }
-  if (n < p_.S)
-    cuda_ok(cudaMemsetAsync(d.get() + n, 0, (p_.S - n) * sizeof(double), rt.stream()), "encrypt pad");
-  if (p_.quantize) k::requant(qs_, d.get(), d.get(), p_.S, rt.stream());
+  DevBuf stage;
+  bool pinned = false;
+  const double* src = n ? device_source(v, n, &stage, &pinned) : nullptr;
+  k::encrypt(qs_, src, n, d.get(), p_.S, nullptr, rt.stream());
+  if (pinned) rt.sync();  // the caller may reuse its pinned buffer on return
   return ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0);
+}
+
+std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
+  Runtime& rt = Runtime::get();
+  std::vector<Ct> out;
+  if (n == 0) return out;
+  DevBuf stage;
+  bool pinned = false;
+  const double* src = device_source(v, n, &stage, &pinned);
+  int* bad = bad_flag();
+  *bad = 0;
+  for (size_t off = 0; off < n; off += p_.S) {
+    const size_t take = std::min(p_.S, n - off);
+    DevBuf d = rt.alloc(p_.S);
+    k::encrypt(qs_, src + off, take, d.get(), p_.S, bad, rt.stream());
+    out.push_back(ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0));
+  }
+  rt.sync();  // the finiteness verdict (and the caller's buffer) must be settled before returning
+  if (*bad) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
+  return out;
 }
 
 Ct DevB::encrypt_const(double c) const {

@@ -124,6 +124,8 @@ class DevB : public LedgerBase<DevB, Ct> {
 
   int level(const C& c) const { return c ? c->level : 0; }
   C encrypt(const double* v, size_t n) const;  // ckks.hpp:97-104 (const: no meter)
+  // encode_column's chunks (column.hpp:25-39) with the non-finite check on device
+  std::vector<C> encrypt_column(const double* v, size_t n) const;
   C encrypt_const(double c) const;
   C add_ct(const C& a, const C& b) { return addsub(a, b, k::B_ADD); }
   C sub_ct(const C& a, const C& b) { return addsub(a, b, k::B_SUB); }

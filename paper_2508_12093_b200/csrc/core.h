@@ -97,7 +97,8 @@ struct CtData {
   mutable bool host_ok = false;
 
   const double* device() const;                 // uploads a host-only ciphertext once
-  void read(double* out, size_t count) const;   // synchronous D2H (cached)
+  void read(double* out, size_t count) const;   // synchronous D2H into the caller's buffer
+  void read_async(double* out, size_t count, size_t) const;  // enqueue only
   const std::vector<double>& host_slots() const;
 };
 using Ct = std::shared_ptr<const CtData>;

@@ -1,30 +1,22 @@
-// fused.cu — E6-E8: per-slot fused programs and the statistics reduction kernels.
+// fused.cu — E6/E7: the standalone per-slot program kernel (k_prog).
 //
-// Per-slot program (k_prog).  Every inverse-root / Chebyshev / Newton entry
-// point is slot-wise: no rotation occurs between its input and its output, and
-// its op DAG (chebyshev.hpp:113-163, primitives.hpp:105-217) is data-independent.
-// The host replays the DAG's control flow symbolically (flow.h, SymB) for
-// levels and meter, then launches one kernel that evaluates the whole DAG per
-// slot in registers: ~1,050 quantised ops per slot for a degree-511 seed plus
-// 6 Newton steps, with no HBM traffic between ops (16 B/slot algorithmic).
-// The program is a short list of macro instructions (kernels.h MOp) read from
-// the constant bank; the Chebyshev BSGS tree itself is straight-line code
-// (cheb_full<K>) keeping T_1..T_{2^(K-1)} and the recursion partials in
-// registers.  With `lanes` > 1 the top log2(lanes) levels of a full-degree
-// (2^K - 1) tree are split across adjacent threads and recombined with warp
-// shuffles, so 32768 slots fill the 148 SMs.
-//
-// Reduction kernels (moments / central).  The statistics pipelines'
-// rotate-and-sum reductions (stats.hpp:41-87) run through slotsum.cuh with the
-// producing slot-wise ops fused into the prologue and the consuming ones into
-// the epilogue.
+// Every inverse-root / Chebyshev / Newton entry point is slot-wise: no rotation
+// occurs between its input and its output, and its op DAG (chebyshev.hpp:
+// 113-163, primitives.hpp:105-217) is data-independent.  The host replays the
+// DAG's control flow symbolically (flow.h, SymB) for levels and meter, then
+// launches one kernel that evaluates the whole DAG per slot in registers:
+// ~1,050 quantised ops per slot for a degree-511 seed plus 6 Newton steps, with
+// no HBM traffic between ops (16 B/slot algorithmic).  The program is a short
+// list of macro instructions (kernels.h MOp) read from the constant bank; the
+// evaluator itself is prog.cuh (shared with the statistics kernel, stat.cu).
+// Geometry: one block per SM, each owning an equal contiguous slot range, P
+// lanes per slot (prog.cuh prog_geometry).
 #include <cstdio>
 
 #include "core.h"
 #include "kernels.h"
 #include "quant.cuh"
 #include "prog.cuh"
-#include "slotsum.cuh"
 
 namespace hsg {
 namespace k {
@@ -59,87 +51,6 @@ void with_q(QSpec qs, F&& f) {
   }
 }
 
-// ---- statistics reduction functors -----------------------------------------------------
-constexpr int kMaxCols = 2;
-
-template <class Q>
-struct MomPro {
-  Q q;
-  MomArgs a[kMaxCols];
-  template <int NA>
-  __device__ void operator()(unsigned b, unsigned i, double (&v)[NA]) const {
-    const MomArgs& A = a[b];
-    for (int c = 0; c < A.nchunks; ++c) {
-      const double X = q.in(__ldg(A.x[c] + i));
-      double t[3];
-      int k = 0;
-      if (A.mode & MOM_MEAN) t[k++] = q.mulc(X, A.cm);  // mul_pt(chunk, 1/(B n))
-      if (A.mode & MOM_VAR) {
-        const double s = q.mulc(X, A.ca);               // mul_pt(chunk, 1/sqrt(S n))
-        t[k++] = q.mul(s, s);                           // mul_ct(a, a)
-        t[k++] = q.mulc(X, A.cmp);                      // mul_pt(chunk, 1/(n sqrt(S)))
-      }
-#pragma unroll
-      for (int j = 0; j < NA; ++j) v[j] = c == 0 ? t[j] : q.add(v[j], t[j]);
-    }
-  }
-};
-
-template <class Q>
-struct MomEpi {
-  Q q;
-  int mode[kMaxCols];
-  double* mu[kMaxCols];
-  double* var[kMaxCols];
-  template <int NA>
-  __device__ void operator()(unsigned b, unsigned i, const double (&v)[NA]) const {
-    int k = 0;
-    if (mode[b] & MOM_MEAN) mu[b][i] = q.out(v[k++]);
-    if (mode[b] & MOM_VAR) {
-      const double sq_sum = v[k], mp = v[k + 1];
-      var[b][i] = q.out(q.sub(sq_sum, q.mul(mp, mp)));  // sub_ct(sq_sum, mul_ct(mp, mp))
-    }
-  }
-};
-
-template <class Q>
-struct CentPro {
-  Q q;
-  CentArgs a;
-  unsigned S;
-  template <int NA>
-  __device__ void operator()(unsigned, unsigned i, double (&v)[NA]) const {
-    const double mux = q.in(__ldg(a.mux + i));
-    const double muy = a.power == 2 ? q.in(__ldg(a.muy + i)) : 0.0;
-    for (int c = 0; c < a.nchunks; ++c) {
-      const double mm = a.valid[c] < S ? q.mulc(mux, i < a.valid[c] ? 1.0 : 0.0) : mux;  // mul_pt(mu, mask)
-      const double cx = q.sub(q.in(__ldg(a.x[c] + i)), mm);
-      double p;
-      if (a.power == 4) {
-        const double sq = q.mul(cx, cx);
-        p = q.mul(sq, sq);
-      } else if (a.power == 3) {
-        const double sq = q.mul(cx, cx);
-        p = q.mul(sq, cx);
-      } else {
-        p = q.mul(cx, q.sub(q.in(__ldg(a.y[c] + i)), muy));
-      }
-      const double term = q.mulc(p, a.inv_n);  // mean_of_chunks: mul_pt(chunk, 1/n)
-      v[0] = c == 0 ? term : q.add(v[0], term);
-    }
-  }
-};
-
-template <class Q>
-struct CentEpi {
-  Q q;
-  double* out;
-  template <int NA>
-  __device__ void operator()(unsigned, unsigned i, const double (&v)[NA]) const {
-    out[i] = q.out(v[0]);
-  }
-};
-
 }  // namespace
 
 void run_prog(QSpec qs, const Prog& p, int lanes, cudaStream_t s) {
@@ -161,39 +72,6 @@ void run_prog(QSpec qs, const Prog& p, int lanes, cudaStream_t s) {
   });
   cuda_ok(cudaGetLastError(), "prog launch");
   Runtime::get().note_launch();
-}
-
-void moments(QSpec qs, const MomArgs* cols, int ncols, size_t S, cudaStream_t s) {
-  if (ncols < 1 || ncols > kMaxCols) fail(HS_E_ERROR, "moments: bad column batch");
-  const int mode = cols[0].mode;
-  for (int c = 1; c < ncols; ++c)
-    if (cols[c].mode != mode) fail(HS_E_ERROR, "moments: mixed modes in one batch");
-  const int NA = (mode & MOM_MEAN ? 1 : 0) + (mode & MOM_VAR ? 2 : 0);
-  with_q(qs, [&](auto Q) {
-    using QT = decltype(Q);
-    MomPro<QT> pro{};
-    MomEpi<QT> epi{};
-    pro.q = Q;
-    epi.q = Q;
-    for (int c = 0; c < ncols; ++c) {
-      pro.a[c] = cols[c];
-      epi.mode[c] = cols[c].mode;
-      epi.mu[c] = cols[c].mu;
-      epi.var[c] = cols[c].var;
-    }
-    if (NA == 1) launch_slotsum<QT, 1>(Q, pro, epi, S, ncols, s);
-    else if (NA == 2) launch_slotsum<QT, 2>(Q, pro, epi, S, ncols, s);
-    else launch_slotsum<QT, 3>(Q, pro, epi, S, ncols, s);
-  });
-}
-
-void central(QSpec qs, const CentArgs& a, size_t S, cudaStream_t s) {
-  with_q(qs, [&](auto Q) {
-    using QT = decltype(Q);
-    CentPro<QT> pro{Q, a, static_cast<unsigned>(S)};
-    CentEpi<QT> epi{Q, a.out};
-    launch_slotsum<QT, 1>(Q, pro, epi, S, 1, s);
-  });
 }
 
 }  // namespace k

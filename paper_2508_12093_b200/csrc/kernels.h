@@ -3,9 +3,10 @@
 //   ops.cu    E1-E5: slot-wise ops, rotation, requantisation, sum_all_slots
 //             (the log-step rotate-and-add reduction, in shared memory across a
 //             thread-block cluster via DSMEM).
-//   fused.cu  E6-E8: the per-slot program interpreter (Chebyshev BSGS, Newton,
-//             inverse roots, statistic epilogues) and the moment/central-moment
-//             slot-sum kernels of the statistics pipelines.
+//   fused.cu  E6-E7: the per-slot program kernel (prog.cuh: Chebyshev BSGS,
+//             Newton, inverse roots, sign, sqrt).
+//   stat.cu   E8: one cooperative kernel per statistic (moments -> grid barrier
+//             -> centred moments -> grid barrier -> per-slot program).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,6 +31,10 @@ void binary(QSpec q, BinOp op, const double* a, const double* b, double* out, si
 enum ScalOp : int { S_ADD = 0, S_MUL = 1 };
 void scalar(QSpec q, ScalOp op, const double* a, double c, double* out, size_t n, cudaStream_t s);
 void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s);
+// encrypt (ckks.hpp:97-104): out[i] = q(src[i]) for i < n, 0 for n <= i < S; src may
+// be host-mapped pinned memory (zero-copy).  Sets *bad (device- or host-mapped)
+// when any src value is non-finite (column.hpp:28-30 check, done on device).
+void encrypt(QSpec q, const double* src, size_t n, double* out, size_t S, int* bad, cudaStream_t s);
 void rotate(const double* a, double* out, size_t n, size_t shift, cudaStream_t s);
 // sum_all_slots over `batch` ciphertexts of S slots each (a[b], out[b]).
 void slot_sum(QSpec q, const double* const* a, double* const* out, int batch, size_t S, cudaStream_t s);
@@ -78,40 +83,9 @@ struct Prog {
 // Launch one per-slot program over S slots.  lanes = 1, 2, 4 or 8 threads per slot.
 void run_prog(QSpec q, const Prog& p, int lanes, cudaStream_t s);
 
-// ---- fused.cu: statistics slot-sum kernels -------------------------------------------
-// Moments of one column (stats.hpp:41-51, 110-126): per slot over chunks
-//   mean term  t0 = sum_c mulc(X_c, cm)
-//   sq term    t1 = sum_c mul(mulc(X_c, ca), mulc(X_c, ca))
-//   mp term    t2 = sum_c mulc(X_c, cmp)
-// then sum_all_slots of each, then var = sub(t1, mul(t2, t2)).
+// moment modes of the statistics kernel (stats.hpp:97-126): mean_scaled terms,
+// variance_to_scale terms (squares + mean part), or both
 enum MomMode : int { MOM_MEAN = 1, MOM_VAR = 2, MOM_BOTH = 3 };
-struct MomArgs {
-  int mode = MOM_BOTH;
-  int nchunks = 0;
-  const double* x[kMaxChunks];
-  double cm = 0, ca = 0, cmp = 0;
-  double* mu = nullptr;   // MOM_MEAN / MOM_BOTH
-  double* var = nullptr;  // MOM_VAR / MOM_BOTH
-};
-void moments(QSpec q, const MomArgs* cols, int ncols, size_t S, cudaStream_t s);
-
-// Centered power sums (stats.hpp:56-87, 170-210, 239-265): per slot over chunks
-//   cx = sub(X_c, mask_c ? mulc(mux, slot < valid_c) : mux)
-//   p  = power 3: mul(mul(cx,cx), cx); power 4: mul(s,s) with s = mul(cx,cx);
-//        power 2 (pearson): mul(cx, sub(Y_c, muy))
-//   t  = sum_c mulc(p, inv_n);   out = sum_all_slots(t)
-struct CentArgs {
-  int power = 4;
-  int nchunks = 0;
-  const double* x[kMaxChunks];
-  const double* y[kMaxChunks];
-  uint64_t valid[kMaxChunks];  // valid slots per chunk (mask applied to x when < S)
-  const double* mux = nullptr;
-  const double* muy = nullptr;
-  double inv_n = 0;
-  double* out = nullptr;
-};
-void central(QSpec q, const CentArgs& a, size_t S, cudaStream_t s);
 
 // ---- stat.cu: one cooperative kernel per statistic ------------------------------------
 // Phase A  moment terms of 1-2 columns (MomArgs semantics) -> grid-wide sums

@@ -75,6 +75,22 @@ __global__ void __launch_bounds__(kThreads) k_requant(Q q, const double* __restr
     o[i] = q.req(a[i]);
 }
 
+template <class Q>
+__global__ void __launch_bounds__(kThreads) k_encrypt(Q q, const double* __restrict__ src, size_t n,
+                                                       double* __restrict__ o, size_t S, int* bad) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  bool nf = false;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < S; i += stride) {
+    double v = 0.0;
+    if (i < n) {
+      v = src[i];
+      nf = nf || !isfinite(v);
+    }
+    o[i] = q.req(v);
+  }
+  if (bad && __any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
 __global__ void __launch_bounds__(kThreads) k_rotate(const double* __restrict__ a, double* __restrict__ o,
                                                       size_t n, size_t shift) {
   const size_t mask = n - 1;  // n is a power of two
@@ -146,6 +162,13 @@ void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s) {
   if (n == 0) return;
   with_q(q, [&](auto Q) { k_requant<<<grid_for(n), kThreads, 0, s>>>(Q, a, out, n); });
   cuda_ok(cudaGetLastError(), "requant launch");
+  Runtime::get().note_launch();
+}
+
+void encrypt(QSpec q, const double* src, size_t n, double* out, size_t S, int* bad, cudaStream_t s) {
+  if (S == 0) return;
+  with_q(q, [&](auto Q) { k_encrypt<<<grid_for(S), kThreads, 0, s>>>(Q, src, n, out, S, bad); });
+  cuda_ok(cudaGetLastError(), "encrypt launch");
   Runtime::get().note_launch();
 }
 

@@ -33,20 +33,48 @@ __device__ __forceinline__ double ffull(const F& f, const double* t, const doubl
   }
 }
 
+// Any F_K as a loop over 2^(K-kBK) unrolled F_kBK blocks, combined by a carry
+// chain over the upper levels: block j finishes every level m whose bit
+// (m - kBK) of j is set (F_{m+1} = add(mul(F_m(left), T_m), F_m(right))).  The
+// branches are warp-uniform and stk[]/T[] stay in registers (static indices in
+// the unrolled carry loop); the code stays ~3 KB so it lives in the I-cache
+// (a fully unrolled degree-511 tree is ~32 KB of SASS per lane and stalled on
+// instruction fetch).  Same ops on the same operands as ffull<K>: bit-identical.
+constexpr int kBK = 5;
+
 template <int ST, class F>
-__device__ __forceinline__ double ffull_dyn(int K, const F& f, const double* t, const double (&T)[kMaxK]) {
+__device__ __forceinline__ double ffull_small(int K, const F& f, const double* t, const double (&T)[kMaxK]) {
   switch (K) {
     case 0: return ffull<0, ST>(f, t, T);
     case 1: return ffull<1, ST>(f, t, T);
     case 2: return ffull<2, ST>(f, t, T);
     case 3: return ffull<3, ST>(f, t, T);
     case 4: return ffull<4, ST>(f, t, T);
-    case 5: return ffull<5, ST>(f, t, T);
-    case 6: return ffull<6, ST>(f, t, T);
-    case 7: return ffull<7, ST>(f, t, T);
-    case 8: return ffull<8, ST>(f, t, T);
-    default: return ffull<9, ST>(f, t, T);
+    default: return ffull<5, ST>(f, t, T);
   }
+}
+
+template <int ST, class F>
+__device__ __forceinline__ double ffull_dyn(int K, const F& f, const double* t, const double (&T)[kMaxK]) {
+  if (K <= kBK) return ffull_small<ST>(K, f, t, T);
+  const int nb = 1 << (K - kBK);
+  constexpr int BS = (1 << kBK) * ST;
+  double stk[kMaxK];
+  double v = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < nb; ++j) {
+    v = ffull<kBK, ST>(f, t + j * BS, T);
+#pragma unroll
+    for (int m = kBK; m < kMaxK - 1; ++m) {
+      if ((j >> (m - kBK)) & 1) {
+        v = f.add(f.mul(stk[m], T[m]), v);
+      } else {
+        stk[m] = v;
+        break;
+      }
+    }
+  }
+  return v;
 }
 
 __device__ __forceinline__ double tpow(int k, const double (&T)[kMaxK]) {

@@ -140,8 +140,23 @@ const std::vector<double>& CtData::host_slots() const {
 
 void CtData::read(double* out, size_t count) const {
   if (count == 0) return;
-  const std::vector<double>& h = host_slots();
-  std::memcpy(out, h.data(), count * sizeof(double));
+  read_async(out, count, 0);
+  Runtime::get().sync();
+}
+
+// Enqueue a D2H copy of slots [0, count) straight into the caller's buffer
+// (pinned buffers DMA directly; no intermediate host cache).  The caller syncs.
+void CtData::read_async(double* out, size_t count, size_t) const {
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (host_ok) {
+      std::memcpy(out, host.data(), count * sizeof(double));
+      return;
+    }
+  }
+  Runtime& rt = Runtime::get();
+  cuda_ok(cudaMemcpyAsync(out, dev.get(), count * sizeof(double), cudaMemcpyDeviceToHost, rt.stream()),
+          "ciphertext read");
 }
 
 Ct ct_device(DevBuf buf, size_t n, int level, int grid) {

@@ -80,10 +80,17 @@ __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int 
       partial[blockIdx.x * 2 * kNK + threadIdx.x] = s;
     }
     grid.sync();
-    if (threadIdx.x < 2 * NK) {  // every block sums the partials in the same order
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partial + b * 2 * kNK + threadIdx.x);
-      tot[threadIdx.x] = s;
+    // every block sums the gridDim.x partials of each value with the same
+    // lane assignment and shuffle tree (one warp per value, loads in parallel),
+    // so all blocks reach identical totals and the same exactness decision
+    {
+      const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+      for (unsigned k = warp; k < static_cast<unsigned>(2 * NK); k += nwarps) {
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(partial + b * 2 * kNK + k);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) tot[k] = s;
+      }
     }
     __syncthreads();
     bool exact = true;

@@ -414,9 +414,14 @@ def encode_column(ctx: EvalContext, values, name: str = "") -> EncryptedColumn: 
     return EncryptedColumn(chunks, len(v), name)
 
 
-def decode_column(ctx: EvalContext, col: EncryptedColumn) -> np.ndarray:  # column.hpp:41-56
+def decode_column(ctx: EvalContext, col: EncryptedColumn, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """column.hpp:41-56.  Pass a (pinned) float64 `out` of n_valid elements to
+    receive the slots by direct DMA."""
     c, keep = col._c()
-    out = np.empty(max(int(col.n_valid), 0))
+    if out is None:
+        out = np.empty(max(int(col.n_valid), 0))
+    elif out.dtype != np.float64 or not out.flags.c_contiguous or out.size < col.n_valid:
+        raise length_mismatch("decode_column: out must be a contiguous float64 array of n_valid elements")
     _check(_abi.lib().hs_decode_column(ctx._h, C.byref(c), _dp(out) if len(out) else None))
     del keep
     return out

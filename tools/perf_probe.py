@@ -69,3 +69,35 @@ try:
                        "pearson": gt(lambda i: H.pearson(ctx, ncols[i % 64], ncols[(i + 1) % 64], 20.0))})
 except Exception as e:
     print("graph failed", repr(e))
+
+# e2e breakdown (wall clock, pinned host buffers)
+hx = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+hp = torch.empty(32768, dtype=torch.float64).pin_memory()
+def wall(fn, reps=200):
+    for _ in range(5): fn()
+    H.sync()
+    t0 = time.perf_counter()
+    for _ in range(reps): fn()
+    H.sync()
+    return round((time.perf_counter() - t0) * 1e6 / reps, 1)
+col0 = H.encode_column(ctx, hx)
+z0 = H.znorm(ctx, col0, 100.0)
+print("e2e_parts_us", {"encode": wall(lambda: H.encode_column(ctx, hx)),
+                       "znorm_call": wall(lambda: H.znorm(ctx, col0, 100.0)),
+                       "decode": wall(lambda: H.decode_column(ctx, z0)),
+                       "decode_pinned": wall(lambda: H.decode_column(ctx, z0, out=hp.numpy())),
+                       "all": wall(lambda: H.decode_column(ctx, H.znorm(ctx, H.encode_column(ctx, hx), 100.0)))})
+
+# raw transfer costs for 256 KiB (pinned <-> device), torch copies on the default stream
+ht = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+dt = torch.empty(32768, dtype=torch.float64, device="cuda")
+hp = torch.empty(32768, dtype=torch.float64).pin_memory()
+def tw(fn, reps=200):
+    for _ in range(5): fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps): fn(); torch.cuda.synchronize()
+    return round((time.perf_counter() - t0) * 1e6 / reps, 1)
+print("xfer_us", {"h2d_256k": tw(lambda: dt.copy_(ht, non_blocking=True)),
+                  "d2h_256k": tw(lambda: hp.copy_(dt, non_blocking=True)),
+                  "sync_only": tw(lambda: None)})
