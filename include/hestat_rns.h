@@ -1,0 +1,69 @@
+/* hestat_rns.h — C ABI of the Tier-R RNS-CKKS kernels in libhestat_gpu.so.
+ *
+ * BASELINE.json north_star items (1)-(4): forward/inverse NTT, fused tensor
+ * product + relinearisation key switching (ModUp, key inner product, ModDown),
+ * rescale, and Galois rotation + key switch, over limb-major u64 RNS
+ * polynomials resident in HBM.
+ *
+ * Reference boundary: the reference is a CKKS *emulator* — its
+ * Evaluator ops (/root/reference/proj/include/hestat/ckks.hpp:149 mul_ct,
+ * :193 rotate, and the implicit rescale inside q()) have no RNS limbs, so these
+ * entry points have no reference counterpart to bind.  They are the limb-level
+ * realisation of those ops (SURVEY.md §7 item 6, §8 "Tier-R realisation"
+ * column) and are checked limb-for-limb against the CPU RNS oracle
+ * (oracle/rns_oracle.c, tests/test_parity_rns.py).
+ *
+ * Layouts (all device pointers, u64 words):
+ *   ciphertext at level l : [2][l+1][N], NTT form, limb i mod q_i;
+ *   batch of B ciphertexts: B consecutive ciphertexts (stride 2(l+1)N words).
+ * Primes: q_0 (logq0 bits), q_1..q_L (logq bits), p_0..p_{K-1} (logp bits).
+ * Keys are derived on the device from spec.seed (same streams as the oracle)
+ * the first time an op needs them, or ahead of time with hs_rns_prepare_*.
+ * Status codes and hs_last_error() are those of hestat_gpu.h.
+ */
+#ifndef HESTAT_RNS_H
+#define HESTAT_RNS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  uint32_t logN, L, K, dnum; /* ring degree 2^logN; L+1 q-primes; K p-primes; dnum digits */
+  uint32_t logq0, logq, logp;
+  uint64_t seed;             /* secret/key/sample streams (rns_oracle.h) */
+} hs_rns_spec;
+
+typedef struct hs_rns hs_rns;
+
+int hs_rns_create(const hs_rns_spec* spec, hs_rns** out);
+int hs_rns_destroy(hs_rns* ctx);
+int hs_rns_primes(const hs_rns* ctx, uint64_t* out, uint32_t cap); /* q_0..q_L, p_0..p_{K-1} */
+
+/* device memory on the library stream */
+int hs_rns_alloc(uint64_t words, uint64_t** dev);
+int hs_rns_free(uint64_t* dev);
+int hs_rns_upload(uint64_t* dev, const uint64_t* host, uint64_t words);
+int hs_rns_download(uint64_t* host, const uint64_t* dev, uint64_t words);
+
+/* key material (optional: ops generate their key on first use) */
+int hs_rns_prepare_relin(hs_rns* ctx);
+int hs_rns_prepare_rotation(hs_rns* ctx, int64_t k);
+int hs_rns_secret(hs_rns* ctx, uint64_t* dev_out); /* [L+1+K][N] NTT form (tests) */
+
+/* ops; `batch` ciphertexts per call, consecutive in memory */
+int hs_rns_random_ct(hs_rns* ctx, uint32_t level, uint64_t tag, uint64_t* dev_out);
+/* in-place NTT (inverse != 0: iNTT) of `batch` groups of `nlimbs` limbs, limb i
+ * of each group taken mod prime first_prime + i, groups `nlimbs*N` words apart */
+int hs_rns_ntt(hs_rns* ctx, uint64_t* dev, uint32_t first_prime, uint32_t nlimbs, uint32_t batch, int inverse);
+int hs_rns_mul_relin(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                     uint32_t batch);
+int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch); /* out: level-1 */
+int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HESTAT_RNS_H */

@@ -116,6 +116,33 @@ _SIGS = {
     "hs_plain": (C.c_int, [C.c_int, DP, C.c_uint64, DP, DP]),
 }
 
+
+
+class hs_rns_spec(C.Structure):  # include/hestat_rns.h
+    _fields_ = [("logN", C.c_uint32), ("L", C.c_uint32), ("K", C.c_uint32), ("dnum", C.c_uint32),
+                ("logq0", C.c_uint32), ("logq", C.c_uint32), ("logp", C.c_uint32), ("seed", C.c_uint64)]
+
+
+U64P = C.POINTER(C.c_uint64)
+RNS = C.c_void_p
+_SIGS.update({
+    "hs_rns_create": (C.c_int, [C.POINTER(hs_rns_spec), C.POINTER(C.c_void_p)]),
+    "hs_rns_destroy": (C.c_int, [RNS]),
+    "hs_rns_primes": (C.c_int, [RNS, U64P, C.c_uint32]),
+    "hs_rns_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "hs_rns_free": (C.c_int, [C.c_void_p]),
+    "hs_rns_upload": (C.c_int, [C.c_void_p, U64P, C.c_uint64]),
+    "hs_rns_download": (C.c_int, [U64P, C.c_void_p, C.c_uint64]),
+    "hs_rns_prepare_relin": (C.c_int, [RNS]),
+    "hs_rns_prepare_rotation": (C.c_int, [RNS, C.c_int64]),
+    "hs_rns_secret": (C.c_int, [RNS, C.c_void_p]),
+    "hs_rns_random_ct": (C.c_int, [RNS, C.c_uint32, C.c_uint64, C.c_void_p]),
+    "hs_rns_ntt": (C.c_int, [RNS, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
+    "hs_rns_mul_relin": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_rotate": (C.c_int, [RNS, C.c_uint32, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32]),
+})
+
 _lib = None
 
 
@@ -136,5 +163,5 @@ def lib():
 
 
 def symbols():
-    """Every exported entry point declared in include/hestat_gpu.h."""
+    """Every exported entry point declared in include/hestat_gpu.h and include/hestat_rns.h."""
     return sorted(_SIGS)

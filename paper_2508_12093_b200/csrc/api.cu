@@ -9,7 +9,9 @@
 #include "backends.h"
 #include "core.h"
 #include "pipelines.h"
+#include "rns.h"
 #include "series.h"
+#include "hestat_rns.h"
 
 using namespace hsg;
 
@@ -626,6 +628,168 @@ void hs_graph_destroy(hs_graph* g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->g) cudaGraphDestroy(g->g);
   delete g;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- Tier R (hestat_rns.h)
+struct hs_rns {
+  std::unique_ptr<rns::Ctx> c;
+};
+
+namespace {
+rns::Ctx& rctx(hs_rns* h) {
+  need(h, "rns context");
+  return *h->c;
+}
+}  // namespace
+
+extern "C" {
+
+int hs_rns_create(const hs_rns_spec* spec, hs_rns** out) {
+  return guard([&] {
+    need(spec, "spec");
+    need(out, "out");
+    rns::Spec s;
+    s.logN = spec->logN;
+    s.L = spec->L;
+    s.K = spec->K;
+    s.dnum = spec->dnum;
+    s.logq0 = spec->logq0;
+    s.logq = spec->logq;
+    s.logp = spec->logp;
+    s.seed = spec->seed;
+    auto h = std::make_unique<hs_rns>();
+    h->c = std::make_unique<rns::Ctx>(s);
+    *out = h.release();
+  });
+}
+
+int hs_rns_destroy(hs_rns* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    Runtime::get().sync();
+    rns::forget(*ctx->c);
+    delete ctx;
+  });
+}
+
+int hs_rns_primes(const hs_rns* ctx, uint64_t* out, uint32_t cap) {
+  return guard([&] {
+    need(ctx, "rns context");
+    need(out, "out");
+    const auto& p = ctx->c->primes;
+    if (cap < p.size()) fail(HS_E_INVALID_ARG, "hs_rns_primes: buffer too small");
+    std::copy(p.begin(), p.end(), out);
+  });
+}
+
+int hs_rns_alloc(uint64_t words, uint64_t** dev) {
+  return guard([&] {
+    need(dev, "out");
+    Runtime& rt = Runtime::get();
+    void* p = nullptr;
+    cuda_ok(cudaMallocAsync(&p, std::max<uint64_t>(words, 1) * 8, rt.stream()), "cudaMallocAsync");
+    *dev = static_cast<uint64_t*>(p);
+  });
+}
+
+int hs_rns_free(uint64_t* dev) {
+  return guard([&] {
+    if (dev) cuda_ok(cudaFreeAsync(dev, Runtime::get().stream()), "cudaFreeAsync");
+  });
+}
+
+int hs_rns_upload(uint64_t* dev, const uint64_t* host, uint64_t words) {
+  return guard([&] {
+    need(dev, "dev");
+    need(host, "host");
+    Runtime& rt = Runtime::get();
+    cuda_ok(cudaMemcpyAsync(dev, host, words * 8, cudaMemcpyHostToDevice, rt.stream()), "upload");
+    rt.sync();
+  });
+}
+
+int hs_rns_download(uint64_t* host, const uint64_t* dev, uint64_t words) {
+  return guard([&] {
+    need(dev, "dev");
+    need(host, "host");
+    Runtime& rt = Runtime::get();
+    cuda_ok(cudaMemcpyAsync(host, dev, words * 8, cudaMemcpyDeviceToHost, rt.stream()), "download");
+    rt.sync();
+  });
+}
+
+int hs_rns_prepare_relin(hs_rns* ctx) {
+  return guard([&] {
+    rns::Ctx& c = rctx(ctx);
+    c.relin_key();
+    for (uint32_t l = 0; l <= c.spec.L; ++l) rns::prepare_level(c, l);
+  });
+}
+
+int hs_rns_prepare_rotation(hs_rns* ctx, int64_t k) {
+  return guard([&] {
+    rns::Ctx& c = rctx(ctx);
+    c.galois_key(rns::Ctx::galois_elt(k, c.spec.logN));
+    for (uint32_t l = 0; l <= c.spec.L; ++l) rns::prepare_level(c, l);
+  });
+}
+
+int hs_rns_secret(hs_rns* ctx, uint64_t* dev_out) {
+  return guard([&] {
+    rns::Ctx& c = rctx(ctx);
+    need(dev_out, "out");
+    Runtime& rt = Runtime::get();
+    cuda_ok(cudaMemcpyAsync(dev_out, c.d_sk.get(), size_t(c.np) * c.N * 8, cudaMemcpyDeviceToDevice, rt.stream()),
+            "secret");
+  });
+}
+
+int hs_rns_random_ct(hs_rns* ctx, uint32_t level, uint64_t tag, uint64_t* dev_out) {
+  return guard([&] {
+    rns::Ctx& c = rctx(ctx);
+    need(dev_out, "out");
+    if (level > c.spec.L) fail(HS_E_INVALID_ARG, "hs_rns_random_ct: level > L");
+    rns::random_ct(c, level, tag, dev_out);
+  });
+}
+
+int hs_rns_ntt(hs_rns* ctx, uint64_t* dev, uint32_t first_prime, uint32_t nlimbs, uint32_t batch, int inverse) {
+  return guard([&] {
+    rns::Ctx& c = rctx(ctx);
+    need(dev, "dev");
+    if (first_prime + nlimbs > c.np) fail(HS_E_INVALID_ARG, "hs_rns_ntt: prime range out of the basis");
+    std::vector<uint32_t> pm(nlimbs);
+    for (uint32_t i = 0; i < nlimbs; ++i) pm[i] = first_prime + i;
+    rns::ntt(c, dev, pm, batch, size_t(nlimbs) * c.N, inverse != 0);
+  });
+}
+
+int hs_rns_mul_relin(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                     uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    rns::mul_relin(rctx(ctx), level, a, b, out, batch);
+  });
+}
+
+int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(in, "in");
+    need(out, "out");
+    rns::rescale(rctx(ctx), level, in, out, batch);
+  });
+}
+
+int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(in, "in");
+    need(out, "out");
+    rns::rotate(rctx(ctx), level, k, in, out, batch);
+  });
 }
 
 }  // extern "C"

@@ -1,0 +1,130 @@
+// rns.h — Tier R: RNS-CKKS evaluator on B200 (north_star items 1-4).
+//
+// Polynomials are limb-major u64 residues resident in HBM: a ciphertext at level
+// l is [2][l+1][N].  Keys (relinearisation and Galois) are [dnum][L+1+K][N]
+// pairs in NTT form over the full basis q_0..q_L, p_0..p_{K-1}.  Conventions
+// (primes, roots, NTT ordering, deterministic key/ciphertext sampling, digit
+// decomposition, ModUp / ModDown, rescale, Galois index map) are exactly those
+// of oracle/rns_oracle.c, so every kernel is checked limb-for-limb against it
+// (tests/test_parity_rns.py).
+//
+// Modular arithmetic (q < 2^62, 64-bit words):
+//   * Shoup multiply-by-constant: w' = floor(w 2^64 / q); hi = mulhi(a, w');
+//     r = a w - hi q in [0, 2q) for ANY a < 2^64 (so base-conversion inputs need
+//     no pre-reduction);
+//   * Barrett for two variable operands < q: k = bitlen(q), mu = floor(2^2k / q);
+//   * lazy (Harvey) NTT butterflies keep values in [0, 4q) between stages and
+//     canonicalise at the end.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "core.h"
+
+namespace hsg {
+namespace rns {
+
+typedef unsigned __int128 u128;
+
+struct Spec {
+  uint32_t logN = 16, L = 24, K = 9, dnum = 3;
+  uint32_t logq0 = 60, logq = 40, logp = 61;
+  uint64_t seed = 0;
+};
+
+// per-prime constants (device)
+struct PrimeC {
+  uint64_t q;
+  uint64_t mu;       // Barrett floor(2^(2k)/q)
+  uint64_t m64;      // floor(2^64 / q) (reduce64)
+  uint64_t ninv, ninv_sh;
+  uint32_t k;        // bitlen(q)
+  uint32_t pad;
+};
+
+__host__ __device__ inline uint64_t shoup_of(uint64_t w, uint64_t q) {
+  return static_cast<uint64_t>((static_cast<u128>(w) << 64) / q);
+}
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
+  const uint64_t r = a + b;
+  return r >= q ? r - q : r;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+// a * w mod q in [0, 2q), any a < 2^64
+__device__ __forceinline__ uint64_t mul_shoup_lazy(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+  const uint64_t hi = __umul64hi(a, wp);
+  return a * w - hi * q;
+}
+__device__ __forceinline__ uint64_t mul_shoup(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+  const uint64_t r = mul_shoup_lazy(a, w, wp, q);
+  return r >= q ? r - q : r;
+}
+// x mod q for any x < 2^64
+__device__ __forceinline__ uint64_t reduce64(uint64_t x, const PrimeC& p) {
+  const uint64_t r = x - __umul64hi(x, p.m64) * p.q;
+  return r >= p.q ? r - p.q : r;
+}
+// a * b mod q for a, b < q (Barrett)
+__device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const PrimeC& p) {
+  const u128 z = static_cast<u128>(a) * b;
+  const uint64_t x = static_cast<uint64_t>(z >> (p.k - 1));
+  const uint64_t qh = static_cast<uint64_t>((static_cast<u128>(x) * p.mu) >> (p.k + 1));
+  uint64_t r = static_cast<uint64_t>(z) - qh * p.q;
+  if (r >= p.q) r -= p.q;
+  if (r >= p.q) r -= p.q;
+  return r;
+}
+
+// ---- host context -------------------------------------------------------------------
+class Ctx {
+ public:
+  explicit Ctx(const Spec& s);
+  const Spec spec;
+  uint32_t N, nq, np, alpha;
+  std::vector<uint64_t> primes;   // q_0..q_L, p_0..p_{K-1}
+  std::vector<PrimeC> pc;         // host copy
+  DevBuf d_pc;                    // PrimeC[np] (reinterpreted)
+  DevBuf d_tw;                    // [np][4][N]: psi_rev, psi_rev', ipsi_rev, ipsi_rev'
+  DevBuf d_sk;                    // [np][N] secret, NTT form
+  std::mutex key_mu;
+
+  const PrimeC* dpc() const { return reinterpret_cast<const PrimeC*>(d_pc.get()); }
+  const uint64_t* tw(uint32_t prime) const { return reinterpret_cast<const uint64_t*>(d_tw.get()) + size_t(prime) * 4 * N; }
+  // keys (generated on first use, on device)
+  struct Key {
+    DevBuf b, a;  // [dnum][np][N]
+  };
+  const Key& relin_key();
+  const Key& galois_key(uint64_t g);
+  static uint64_t galois_elt(int64_t k, uint32_t logN);
+
+ private:
+  std::unique_ptr<Key> relin_;
+  std::map<uint64_t, std::unique_ptr<Key>> gal_;
+  void make_key(uint64_t keyid, const uint64_t* sprime, Key* out);
+};
+
+// ---- device ops (all on the library stream; pointers are device u64 arrays) --------------
+// In-place NTT of `nlimbs` consecutive limbs (limb l uses prime prime_of[l]); `batch`
+// groups of nlimbs limbs, group stride `gstride` words.  prime_of: host list.
+void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, uint32_t batch, size_t gstride,
+         bool inverse);
+void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out);
+void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
+void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch);
+void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
+// Build (and upload) the per-level key-switching / rescale constants ahead of time,
+// so that ops can be captured into a CUDA graph.
+void prepare_level(Ctx& c, uint32_t level);
+// Drop every cached plan of this context (before destroying it).
+void forget(const Ctx& c);
+
+}  // namespace rns
+}  // namespace hsg

@@ -1,0 +1,137 @@
+"""Python mirror of include/hestat_rns.h (Tier-R RNS-CKKS kernels).
+
+Thin ctypes layer: device buffers are `DeviceBuffer`s of u64 words owned by the
+library's stream-ordered pool; every op runs on the library stream.  There is
+no CPU path: the oracle lives under oracle/ and is used by tests only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .hestat import _check
+
+
+@dataclass
+class RnsSpec:
+    logN: int = 16
+    L: int = 24
+    K: int = 9
+    dnum: int = 3
+    logq0: int = 60
+    logq: int = 40
+    logp: int = 61
+    seed: int = 0
+
+    @property
+    def N(self) -> int:
+        return 1 << self.logN
+
+    def c(self) -> _abi.hs_rns_spec:
+        return _abi.hs_rns_spec(self.logN, self.L, self.K, self.dnum, self.logq0, self.logq, self.logp, self.seed)
+
+    def ct_words(self, level: int) -> int:
+        return 2 * (level + 1) * self.N
+
+
+class DeviceBuffer:
+    """`words` u64 words of device memory (freed stream-ordered on release)."""
+
+    def __init__(self, words: int):
+        p = C.c_void_p()
+        _check(_abi.lib().hs_rns_alloc(words, C.byref(p)))
+        self.ptr, self.words = p.value, words
+
+    def upload(self, a: np.ndarray) -> "DeviceBuffer":
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        if a.size > self.words:
+            raise ValueError("upload larger than the buffer")
+        _check(_abi.lib().hs_rns_upload(self.ptr, a.ctypes.data_as(_abi.U64P), a.size))
+        return self
+
+    def download(self, words: int | None = None) -> np.ndarray:
+        n = self.words if words is None else words
+        out = np.empty(n, dtype=np.uint64)
+        _check(_abi.lib().hs_rns_download(out.ctypes.data_as(_abi.U64P), self.ptr, n))
+        return out
+
+    def offset(self, words: int) -> int:
+        return self.ptr + 8 * words
+
+    def free(self):
+        if self.ptr:
+            _abi.lib().hs_rns_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class RnsContext:
+    """hs_rns: primes, twiddles and (lazily) keys for one parameter set."""
+
+    def __init__(self, spec: RnsSpec):
+        self.spec = spec
+        h = C.c_void_p()
+        _check(_abi.lib().hs_rns_create(C.byref(spec.c()), C.byref(h)))
+        self.h = h.value
+
+    def close(self):
+        if self.h:
+            _abi.lib().hs_rns_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def primes(self) -> np.ndarray:
+        n = self.spec.L + 1 + self.spec.K
+        out = np.zeros(n, dtype=np.uint64)
+        _check(_abi.lib().hs_rns_primes(self.h, out.ctypes.data_as(_abi.U64P), n))
+        return out
+
+    def prepare_relin(self):
+        _check(_abi.lib().hs_rns_prepare_relin(self.h))
+
+    def prepare_rotation(self, k: int):
+        _check(_abi.lib().hs_rns_prepare_rotation(self.h, k))
+
+    def secret(self) -> np.ndarray:
+        n = (self.spec.L + 1 + self.spec.K) * self.spec.N
+        b = DeviceBuffer(n)
+        _check(_abi.lib().hs_rns_secret(self.h, b.ptr))
+        return b.download().reshape(self.spec.L + 1 + self.spec.K, self.spec.N)
+
+    def random_ct(self, level: int, tag: int, out: DeviceBuffer | None = None, offset: int = 0) -> DeviceBuffer:
+        out = out or DeviceBuffer(self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_random_ct(self.h, level, tag, out.offset(offset)))
+        return out
+
+    def ntt(self, buf: DeviceBuffer, first_prime: int, nlimbs: int, batch: int = 1, inverse: bool = False):
+        _check(_abi.lib().hs_rns_ntt(self.h, buf.ptr, first_prime, nlimbs, batch, int(inverse)))
+
+    def mul_relin(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
+                  batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_mul_relin(self.h, level, a.ptr, b.ptr, out.ptr, batch))
+        return out
+
+    def rescale(self, level: int, a: DeviceBuffer, out: DeviceBuffer | None = None, batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        _check(_abi.lib().hs_rns_rescale(self.h, level, a.ptr, out.ptr, batch))
+        return out
+
+    def rotate(self, level: int, k: int, a: DeviceBuffer, out: DeviceBuffer | None = None,
+               batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_rotate(self.h, level, k, a.ptr, out.ptr, batch))
+        return out

@@ -12,12 +12,12 @@ import pytest
 
 from oracle_abi import ROOT, FIT_EXP, FIT_INVSQRT_SHIFTED, FIT_SQRT_SHIFTED, bits, oracle
 
-HEADER = os.path.join(ROOT, "include", "hestat_gpu.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("hestat_gpu.h", "hestat_rns.h")]
 LIB = os.path.join(ROOT, "paper_2508_12093_b200", "libhestat_gpu.so")
 
 
 def declared():
-    txt = open(HEADER).read()
+    txt = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"\b(hs_[a-z0-9_]+)\s*\(", txt)) - {"hs_target_fn"})
 
 

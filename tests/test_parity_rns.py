@@ -1,0 +1,171 @@
+"""GPU: Tier-R kernels (include/hestat_rns.h) limb-for-limb against the CPU RNS
+oracle (oracle/rns_oracle.c) on the same seeded keys and ciphertexts.
+
+Bar: bit-exact u64 limbs for every op (NTT, iNTT, key generation, HMult+relin,
+rescale, rotate), for several (logN, L, K, dnum) shapes including a digit
+count that does not divide L+1, partial top digits at lower levels, batches,
+and the full north_star size N=2^16, L=24.
+"""
+import numpy as np
+import pytest
+
+from rns_abi import RnsOracle, Spec
+
+pytestmark = pytest.mark.gpu
+
+O = RnsOracle()
+
+SHAPES = [
+    Spec(logN=9, L=3, K=2, dnum=2),
+    Spec(logN=10, L=5, K=2, dnum=4, seed=7),      # alpha=2, 3 digits at the top level
+    Spec(logN=12, L=7, K=3, dnum=3, seed=11),     # alpha=3: partial last digit
+    Spec(logN=13, L=4, K=1, dnum=5, seed=3),      # alpha=1, K=1
+]
+
+
+def _ctx(s: Spec):
+    from paper_2508_12093_b200.rns import RnsContext, RnsSpec
+    return RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed))
+
+
+def _buf(a):
+    from paper_2508_12093_b200.rns import DeviceBuffer
+    return DeviceBuffer(a.size).upload(a)
+
+
+_CTX = {}
+
+
+def ctx(s: Spec):
+    key = (s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed)
+    if key not in _CTX:
+        _CTX[key] = _ctx(s)
+    return _CTX[key]
+
+
+@pytest.mark.parametrize("s", SHAPES + [Spec(logN=16, L=24, K=9, dnum=3, seed=1)], ids=str)
+def test_primes_and_secret(s):
+    c = ctx(s)
+    assert np.array_equal(c.primes(), O.primes(s))
+    if s.logN <= 13:
+        assert np.array_equal(c.secret(), O.secret(s))
+
+
+@pytest.mark.parametrize("logN", [9, 10, 11, 12, 13, 14, 15, 16, 17])
+def test_ntt_matches_oracle(logN):
+    s = Spec(logN=logN, L=2, K=1, dnum=1, seed=5)
+    c = ctx(s)
+    primes = O.primes(s)
+    rng = np.random.default_rng(logN)
+    n = len(primes)
+    a = np.stack([rng.integers(0, int(q), s.N, dtype=np.uint64) for q in primes])
+    # two batch groups of all primes
+    host = np.concatenate([a, a[::-1] % primes[:, None]]).reshape(-1)
+    b = _buf(host)
+    c.ntt(b, 0, n, batch=2)
+    got = b.download().reshape(2, n, s.N)
+    for g in range(2):
+        src = a if g == 0 else a[::-1] % primes[:, None]
+        for i in range(n):
+            assert np.array_equal(got[g, i], O.ntt(s, i, src[i])), (g, i)
+    c.ntt(b, 0, n, batch=2, inverse=True)
+    assert np.array_equal(b.download(), host)
+    # inverse of arbitrary (non-NTT) data matches the oracle's iNTT too
+    b2 = _buf(a.reshape(-1))
+    c.ntt(b2, 0, n, inverse=True)
+    got = b2.download().reshape(n, s.N)
+    for i in range(n):
+        assert np.array_equal(got[i], O.ntt(s, i, a[i], inverse=True))
+
+
+def test_ntt_extreme_values():
+    s = Spec(logN=12, L=1, K=1, dnum=1, seed=5)
+    c = ctx(s)
+    primes = O.primes(s)
+    for fill in ("zero", "qm1", "one"):
+        a = np.stack([np.full(s.N, {"zero": 0, "qm1": int(q) - 1, "one": 1}[fill], dtype=np.uint64) for q in primes])
+        b = _buf(a.reshape(-1))
+        c.ntt(b, 0, len(primes))
+        got = b.download().reshape(len(primes), s.N)
+        for i in range(len(primes)):
+            assert np.array_equal(got[i], O.ntt(s, i, a[i]))
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=str)
+def test_random_ct(s):
+    c = ctx(s)
+    for level, tag in ((s.L, 1), (1, 9)):
+        assert np.array_equal(c.random_ct(level, tag).download(), O.random_ct(s, level, tag))
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=str)
+def test_mul_relin_matches_oracle(s):
+    c = ctx(s)
+    for level in sorted({s.L, max(s.L - 2, 0), 0}):
+        a, b = O.random_ct(s, level, 21), O.random_ct(s, level, 22)
+        got = c.mul_relin(level, _buf(a), _buf(b)).download()
+        assert np.array_equal(got, O.mul_relin(s, level, a, b)), level
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=str)
+def test_rescale_matches_oracle(s):
+    c = ctx(s)
+    for level in sorted({s.L, 1}):
+        a = O.random_ct(s, level, 31)
+        got = c.rescale(level, _buf(a)).download()
+        assert np.array_equal(got, O.rescale(s, level, a)), level
+
+
+@pytest.mark.parametrize("s", SHAPES[:3], ids=str)
+@pytest.mark.parametrize("k", [1, 2, 5, -3, 0])
+def test_rotate_matches_oracle(s, k):
+    c = ctx(s)
+    level = s.L - 1
+    a = O.random_ct(s, level, 41)
+    got = c.rotate(level, k, _buf(a)).download()
+    assert np.array_equal(got, O.rotate(s, level, k, a))
+
+
+def test_batched_ops_equal_single():
+    s = SHAPES[1]
+    c = ctx(s)
+    level, B = s.L, 3
+    a = np.concatenate([O.random_ct(s, level, 50 + i) for i in range(B)])
+    b = np.concatenate([O.random_ct(s, level, 60 + i) for i in range(B)])
+    W = s.N * 2 * (level + 1)
+    da, db = _buf(a), _buf(b)
+    m = c.mul_relin(level, da, db, batch=B).download()
+    r = c.rescale(level, da, batch=B).download()
+    rot = c.rotate(level, 3, da, batch=B).download()
+    Wr = s.N * 2 * level
+    for i in range(B):
+        ai, bi = a[i * W:(i + 1) * W], b[i * W:(i + 1) * W]
+        assert np.array_equal(m[i * W:(i + 1) * W], O.mul_relin(s, level, ai, bi))
+        assert np.array_equal(r[i * Wr:(i + 1) * Wr], O.rescale(s, level, ai))
+        assert np.array_equal(rot[i * W:(i + 1) * W], O.rotate(s, level, 3, ai))
+
+
+def test_errors():
+    from paper_2508_12093_b200 import hestat as H
+    from paper_2508_12093_b200.rns import RnsSpec, RnsContext
+    with pytest.raises(H.error):
+        RnsContext(RnsSpec(logN=8, L=2, K=1, dnum=1))
+    c = ctx(SHAPES[0])
+    a = c.random_ct(1, 1)
+    with pytest.raises(H.error):
+        c.rescale(0, a)
+    with pytest.raises(H.error):
+        c.mul_relin(SHAPES[0].L + 1, a, a)
+
+
+def test_full_size_north_star():
+    """N=2^16, L=24, K=9, dnum=3 (BASELINE north_star shape): HMult+relin,
+    rescale and rotate at the top level, limb-exact vs the oracle."""
+    s = Spec(logN=16, L=24, K=9, dnum=3, seed=1)
+    c = ctx(s)
+    level = s.L
+    a, b = O.random_ct(s, level, 1), O.random_ct(s, level, 2)
+    da, db = _buf(a), _buf(b)
+    assert np.array_equal(c.mul_relin(level, da, db).download(), O.mul_relin(s, level, a, b))
+    assert np.array_equal(c.rescale(level, da).download(), O.rescale(s, level, a))
+    assert np.array_equal(c.rotate(level, 1, da).download(), O.rotate(s, level, 1, a))

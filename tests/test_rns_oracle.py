@@ -1,0 +1,148 @@
+"""CPU: validate the Tier-R RNS oracle (oracle/rns_oracle.c) by the algebraic
+identities of RNS-CKKS, checked with exact big-integer CRT in Python:
+
+  * primes are distinct, prime, = 1 mod 2N, of the requested sizes;
+  * NTT/iNTT round-trip and the negacyclic convolution theorem (vs schoolbook);
+  * HMult+relin: phase(out) = phase(a) * phase(b) + e_ks with |e_ks| small;
+  * rescale: q_l * phase(out) - phase(in) is small (rounding term);
+  * rotation: phase(out) = sigma_g(phase(in)) + e_ks.
+phase(c) = c0 + c1 * s over Q_l, s = the oracle's ternary secret.
+"""
+import numpy as np
+import pytest
+
+from rns_abi import RnsOracle, Spec, crt_centred, galois_elt, galois_src
+
+O = RnsOracle()
+SPEC = Spec(logN=9, L=3, K=2, dnum=2)
+
+
+def _is_prime(n):
+    if n < 2:
+        return False
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if n % p == 0:
+            return n == p
+    d, r = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def test_primes():
+    for spec in (SPEC, Spec(logN=16, L=24, K=9, dnum=3)):
+        ps = [int(p) for p in O.primes(spec)]
+        assert len(set(ps)) == len(ps) == spec.L + 1 + spec.K
+        for i, p in enumerate(ps):
+            assert _is_prime(p) and p % (2 * spec.N) == 1
+            bits = spec.logq0 if i == 0 else (spec.logq if i <= spec.L else spec.logp)
+            assert p < (1 << bits) and p > (1 << (bits - 1))
+
+
+def test_ntt_roundtrip_and_convolution():
+    rng = np.random.default_rng(1)
+    N = SPEC.N
+    for pi, q in enumerate(O.primes(SPEC)):
+        q = int(q)
+        a = rng.integers(0, q, N, dtype=np.uint64)
+        b = rng.integers(0, q, N, dtype=np.uint64)
+        fa, fb = O.ntt(SPEC, pi, a), O.ntt(SPEC, pi, b)
+        assert np.array_equal(O.ntt(SPEC, pi, fa, inverse=True), a)
+        prod = O.ntt(SPEC, pi, np.array([(int(x) * int(y)) % q for x, y in zip(fa, fb)], dtype=np.uint64), True)
+        if pi < 2:  # schoolbook negacyclic product (O(N^2) in Python: two primes suffice)
+            ai, bi = [int(x) for x in a], [int(x) for x in b]
+            ref = [0] * N
+            for i in range(N):
+                if ai[i] == 0:
+                    continue
+                for j in range(N):
+                    k = i + j
+                    if k < N:
+                        ref[k] += ai[i] * bi[j]
+                    else:
+                        ref[k - N] -= ai[i] * bi[j]
+            assert [int(x) for x in prod] == [r % q for r in ref]
+
+
+def _phase(ct, level, sk, primes, N):
+    """c0 + c1*s in the NTT domain, per limb -> coefficient form (iNTT)."""
+    nl = level + 1
+    c = ct.reshape(2, nl, N)
+    limbs = []
+    for i in range(nl):
+        q = int(primes[i])
+        v = np.array([(int(c[0, i, n]) + int(c[1, i, n]) * int(sk[i, n])) % q for n in range(N)], dtype=np.uint64)
+        limbs.append(O.ntt(SPEC, i, v, inverse=True))
+    return limbs
+
+
+def _ntt_phase(ct, level, sk, primes, N):
+    nl = level + 1
+    c = ct.reshape(2, nl, N)
+    return [[(int(c[0, i, n]) + int(c[1, i, n]) * int(sk[i, n])) % int(primes[i]) for n in range(N)]
+            for i in range(nl)]
+
+
+@pytest.mark.parametrize("level", [3, 1])
+def test_mul_relin_identity(level):
+    N, primes, sk = SPEC.N, O.primes(SPEC), O.secret(SPEC)
+    a, b = O.random_ct(SPEC, level, 1), O.random_ct(SPEC, level, 2)
+    out = O.mul_relin(SPEC, level, a, b)
+    pa, pb, po = (_ntt_phase(x, level, sk, primes, N) for x in (a, b, out))
+    diff = []
+    for i in range(level + 1):
+        q = int(primes[i])
+        d = np.array([(po[i][n] - pa[i][n] * pb[i][n]) % q for n in range(N)], dtype=np.uint64)
+        diff.append(O.ntt(SPEC, i, d, inverse=True))
+    err = crt_centred(diff, primes[: level + 1])
+    assert max(abs(e) for e in err) < 2 ** 30, max(abs(e) for e in err)
+
+
+def test_rescale_identity():
+    level = 3
+    N, primes, sk = SPEC.N, O.primes(SPEC), O.secret(SPEC)
+    a = O.random_ct(SPEC, level, 3)
+    out = O.rescale(SPEC, level, a)
+    pin = crt_centred(_phase(a, level, sk, primes, N), primes[: level + 1])
+    pout = crt_centred(_phase(out, level - 1, sk, primes, N), primes[:level])
+    Q = 1
+    for p in primes[: level + 1]:
+        Q *= int(p)
+    ql = int(primes[level])
+    worst = 0
+    for x, y in zip(pin, pout):
+        r = (y * ql - x) % Q
+        r = r - Q if r > Q // 2 else r
+        worst = max(worst, abs(r))
+    assert worst <= ql * (N + 2)
+
+
+@pytest.mark.parametrize("k", [1, 5, -3])
+def test_rotate_identity(k):
+    level = 2
+    N, primes, sk = SPEC.N, O.primes(SPEC), O.secret(SPEC)
+    a = O.random_ct(SPEC, level, 4)
+    out = O.rotate(SPEC, level, k, a)
+    g = galois_elt(k, SPEC.logN)
+    pa, po = _ntt_phase(a, level, sk, primes, N), _ntt_phase(out, level, sk, primes, N)
+    # sigma(s) must be applied to phase(in) through sigma of the whole polynomial:
+    # phase(out) ~ sigma(c0 + c1 s) -> in the NTT domain index-permuted
+    src = [galois_src(n, g, SPEC.logN) for n in range(N)]
+    diff = []
+    for i in range(level + 1):
+        q = int(primes[i])
+        d = np.array([(po[i][n] - pa[i][src[n]]) % q for n in range(N)], dtype=np.uint64)
+        diff.append(O.ntt(SPEC, i, d, inverse=True))
+    err = crt_centred(diff, primes[: level + 1])
+    assert max(abs(e) for e in err) < 2 ** 30, max(abs(e) for e in err)
