@@ -1,18 +1,22 @@
 // rns.cu — Tier R kernels and host orchestration (see rns.h).
 //
-//   NTT / iNTT   two shared-memory passes per limb: the first log2(R1) stages
-//                act on columns (stride C = N/R1, coalesced 2048-element tiles),
-//                the remaining stages on contiguous blocks of C; Shoup twiddles,
-//                lazy Harvey butterflies in [0, 4q), canonical output.
-//   tensor       d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 (Barrett).
-//   ModUp        fast base conversion of each digit (coefficient form) to the
-//                extended basis Q_l u P, then NTT of the new limbs.
-//   inner        sum_j ModUp(d_j) * key_j over all digits (streams the key).
-//   ModDown      iNTT of the P limbs, base conversion P -> Q_l, NTT, then
-//                (acc - conv) * P^-1 (+ the tensor's d0/d1 for HMult).
+//   NTT / iNTT   two shared-memory passes per limb (columns, then contiguous
+//                rows), radix-8 register groups, Shoup twiddles, lazy Harvey
+//                butterflies in [0, 4q), canonical output; one launch covers any
+//                list of (input row, output row, prime) triples for a batch.
+//   tensor       d0 = a0 b0, d1 = a0 b1 + a1 b0 (one 128-bit reduction), d2 = a1 b1.
+//   ModUp        fast base conversion of every digit (coefficient form) to the
+//                extended basis Q_l u P in one launch (128-bit accumulation, one
+//                reduction per output), then one batched NTT of all new rows.
+//   inner        sum_j ModUp(d_j) * key_j; each thread keeps its key words in
+//                registers and loops over the batch, so the key streams from HBM
+//                once per call instead of once per ciphertext.
+//   ModDown      in-place iNTT of the P rows, base conversion P -> Q_l, NTT, then
+//                (acc - conv) * P^-1 (+ d0/d1 for HMult, + sigma(c0) for rotate).
 //   rescale      iNTT of the last limb, reduce into q_i, NTT, (c_i - t_i) q_l^-1.
 //   automorph    NTT-domain Galois permutation for 5^k.
-// Every kernel takes a batch index in blockIdx.z (ciphertexts of one call).
+// Every kernel takes its batch index from blockIdx.z.  Ring sizes are powers of
+// two: all index arithmetic is shifts and masks.
 #include "rns.h"
 
 #include <algorithm>
@@ -24,8 +28,7 @@ namespace hsg {
 namespace rns {
 namespace {
 
-constexpr int kT = 256;        // threads per block
-constexpr uint32_t kTile = 2048;  // NTT elements per CTA (16 KB of shared memory)
+constexpr int kT = 256;  // threads per elementwise block
 
 enum : uint64_t { D_SECRET = 1, D_KEY_A = 2, D_KEY_E = 3, D_CT = 4 };
 
@@ -44,143 +47,206 @@ __device__ inline uint64_t lift(int64_t v, uint64_t q) {
 }
 __device__ inline uint32_t bitrev(uint32_t x, uint32_t bits) { return __brev(x) >> (32 - bits); }
 
-struct PrimeMap {
-  uint8_t p[64];
+// (input row, output row, prime) per blockIdx.y of an NTT launch
+constexpr int kMaxRows = 128;
+struct RowMap {
+  uint16_t irow[kMaxRows], orow[kMaxRows];
+  uint8_t prime[kMaxRows];
 };
 
 // ---------------------------------------------------------------- NTT kernels
-// forward, phase 1: the first log2(R1) stages on columns r*C + c
-__global__ void __launch_bounds__(kT) k_ntt_fwd_cols(uint64_t* data, const __grid_constant__ PrimeMap pm, size_t gstride, const PrimeC* pcs,
-                                                     const uint64_t* tw, uint32_t N, uint32_t R1, uint32_t CPB) {
-  __shared__ uint64_t sm[kTile];
-  const uint32_t pi = pm.p[blockIdx.y];
-  const uint64_t q = pcs[pi].q, q2 = 2 * q;
-  const uint64_t* psi = tw + size_t(pi) * 4 * N;
+// One pass = a batch of independent sub-transforms held in shared memory:
+//   column pass: the first log2(R1) stages, transform c = column {r*C + c};
+//   row pass   : the remaining log2(C) stages, transform g = block [g*C, (g+1)*C).
+// Stage m (local), block i of a sub-transform uses twiddle index m*S + i with
+// S = 1 (columns) or R1 + g (rows), so one device routine serves both passes.
+// Each thread runs radix-2^RB groups (RB <= 3 stages) in registers; the first
+// group step reads HBM directly, the last writes HBM directly, the ones between
+// exchange through shared memory (row tiles padded one word in eight so that the
+// short-stride steps are bank-conflict free).
+constexpr int kNT = 512;           // threads per NTT block
+constexpr uint32_t kLogTile = 12;  // 4096 elements per NTT block
+constexpr uint32_t kNTile = 1u << kLogTile;
+
+__device__ __forceinline__ uint32_t spad(uint32_t u) { return u + (u >> 3); }
+
+template <int LOGN, bool ROWS>
+struct NttGeom {
+  static constexpr uint32_t logR1 = LOGN / 2, logC = LOGN - logR1;
+  static constexpr uint32_t logR = ROWS ? logC : logR1;  // sub-transform length of this pass
+  static constexpr uint32_t logTPB = ROWS ? (kLogTile - logC < logR1 ? kLogTile - logC : logR1)
+                                          : (kLogTile - logR1 < logC ? kLogTile - logR1 : logC);
+  static constexpr uint32_t R1 = 1u << logR1;
+};
+
+// One radix-2^RB step (stages DONE .. DONE+RB-1 of this pass) for every group of the tile.
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST>
+__device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint64_t* __restrict__ gout,
+                                         uint64_t* __restrict__ sm, const uint64_t* __restrict__ psi,
+                                         const uint64_t* __restrict__ psip, uint64_t q, uint32_t tile0,
+                                         uint64_t ninv, uint64_t ninv_sh) {
+  using G = NttGeom<LOGN, ROWS>;
+  constexpr uint32_t logR = G::logR, logTPB = G::logTPB, logC = G::logC;
+  constexpr uint32_t logG = logR - RB;  // groups per transform (log)
+  constexpr uint32_t total = 1u << (logG + logTPB);
+  constexpr uint32_t logs = INV ? DONE : logR - 1 - DONE - (RB - 1);  // element stride inside a group (log)
+  const uint64_t q2 = 2 * q;
+#pragma unroll
+  for (uint32_t it = 0; it < (total + kNT - 1) / kNT; ++it) {
+    const uint32_t idx = threadIdx.x + it * kNT;
+    if (total % kNT != 0 && idx >= total) break;
+    uint32_t tr, g;
+    if (ROWS) {
+      g = idx & ((1u << logG) - 1);
+      tr = idx >> logG;
+    } else {
+      tr = idx & ((1u << logTPB) - 1);
+      g = idx >> logTPB;
+    }
+    const uint32_t blk0 = g >> logs;
+    const uint32_t j0 = (blk0 << (logs + RB)) | (g & ((1u << logs) - 1));
+    const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
+    uint64_t x[1 << RB];
+#pragma unroll
+    for (int k = 0; k < (1 << RB); ++k) {
+      const uint32_t e = j0 + (uint32_t(k) << logs);
+      if (FIRST)
+        x[k] = ROWS ? gin[(size_t(tr) << logC) + e] : gin[(size_t(e) << logC) + tr];
+      else
+        x[k] = ROWS ? sm[spad((tr << logR) + e)] : sm[(e << logTPB) + tr];
+    }
+    if (!INV) {
+#pragma unroll
+      for (int st = 0; st < RB; ++st) {
+        const int d = 1 << (RB - 1 - st);
+#pragma unroll
+        for (int b = 0; b < (1 << st); ++b) {
+          const uint32_t wi = ((1u << (DONE + st)) * S) + (blk0 << st) + b;
+          const uint64_t w = __ldg(psi + wi), wp = __ldg(psip + wi);
+#pragma unroll
+          for (int o = 0; o < d; ++o) {
+            const int k0 = b * 2 * d + o;
+            uint64_t X = x[k0];
+            X = X >= q2 ? X - q2 : X;
+            const uint64_t T = mul_shoup_lazy(x[k0 + d], w, wp, q);
+            x[k0] = X + T;
+            x[k0 + d] = X - T + q2;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int st = 0; st < RB; ++st) {
+        const int d = 1 << st;
+        constexpr uint32_t logh0 = logR - 1 - DONE;
+#pragma unroll
+        for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
+          const uint32_t wi = ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b;
+          const uint64_t w = __ldg(psi + wi), wp = __ldg(psip + wi);
+#pragma unroll
+          for (int o = 0; o < d; ++o) {
+            const int k0 = b * 2 * d + o;
+            const uint64_t X = x[k0], Y = x[k0 + d];
+            const uint64_t s2 = X + Y;
+            x[k0] = s2 >= q2 ? s2 - q2 : s2;
+            x[k0 + d] = mul_shoup_lazy(X - Y + q2, w, wp, q);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << RB); ++k) {
+      const uint32_t e = j0 + (uint32_t(k) << logs);
+      uint64_t v = x[k];
+      if (LAST) {
+        if (!INV) {
+          v = v >= q2 ? v - q2 : v;
+          v = v >= q ? v - q : v;
+        } else if (!ROWS) {
+          v = mul_shoup(v, ninv, ninv_sh, q);
+        }
+        if (ROWS)
+          gout[(size_t(tr) << logC) + e] = v;
+        else
+          gout[(size_t(e) << logC) + tr] = v;
+      } else {
+        if (ROWS)
+          sm[spad((tr << logR) + e)] = v;
+        else
+          sm[(e << logTPB) + tr] = v;
+      }
+    }
+  }
+}
+
+// All steps of a pass, unrolled at compile time: radix-8 steps, with the
+// remainder taken as radix-4 (a 4-stage tail becomes 2 + 2).
+template <bool INV, bool ROWS, int LOGN, int DONE>
+__device__ __forceinline__ void ntt_steps(const uint64_t* gin, uint64_t* gout, uint64_t* sm, const uint64_t* psi,
+                                          const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
+                                          uint64_t ninv_sh) {
+  constexpr int logR = NttGeom<LOGN, ROWS>::logR;
+  if constexpr (DONE < logR) {
+    constexpr int rem = logR - DONE;
+    constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
+    if constexpr (DONE > 0) __syncthreads();
+    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR>(gin, gout, sm, psi, psip, q, tile0, ninv,
+                                                                      ninv_sh);
+    ntt_steps<INV, ROWS, LOGN, DONE + RB>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
+  }
+}
+
+// Forward: columns then rows; inverse: rows then columns.  Reads `in`, writes
+// `out` (may alias: every block reads its whole tile before its last step writes).
+// 3 blocks of 512 threads per SM (40 registers): measured 1.3x over 2 blocks.
+template <bool INV, bool ROWS, int LOGN>
+__global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                  size_t out_stride, const __grid_constant__ RowMap rm,
+                                                  const PrimeC* pcs, const uint64_t* tw) {
+  using G = NttGeom<LOGN, ROWS>;
+  __shared__ uint64_t sm[kNTile + kNTile / 8];
+  constexpr uint32_t N = 1u << LOGN;
+  const uint32_t pi = rm.prime[blockIdx.y];
+  const PrimeC& P = pcs[pi];
+  const uint64_t* psi = tw + size_t(pi) * 4 * N + (INV ? 2 * N : 0);
   const uint64_t* psip = psi + N;
-  uint64_t* a = data + blockIdx.z * gstride + size_t(blockIdx.y) * N;
-  const uint32_t C = N / R1, c0 = blockIdx.x * CPB;
-  for (uint32_t e = threadIdx.x; e < R1 * CPB; e += blockDim.x) sm[e] = a[c0 + (e % CPB) + (e / CPB) * C];
-  __syncthreads();
-  for (uint32_t m = 1, tr = R1 / 2; m < R1; m <<= 1, tr >>= 1) {
-    for (uint32_t b = threadIdx.x; b < (R1 / 2) * CPB; b += blockDim.x) {
-      const uint32_t cc = b % CPB, bi = b / CPB, g = bi / tr, r0 = g * 2 * tr + bi % tr;
-      const uint64_t w = __ldg(psi + m + g), wp = __ldg(psip + m + g);
-      uint64_t X = sm[r0 * CPB + cc];
-      const uint64_t Y = sm[(r0 + tr) * CPB + cc];
-      X = X >= q2 ? X - q2 : X;
-      const uint64_t T = mul_shoup_lazy(Y, w, wp, q);
-      sm[r0 * CPB + cc] = X + T;
-      sm[(r0 + tr) * CPB + cc] = X - T + q2;
-    }
-    __syncthreads();
-  }
-  for (uint32_t e = threadIdx.x; e < R1 * CPB; e += blockDim.x) a[c0 + (e % CPB) + (e / CPB) * C] = sm[e];
+  const uint32_t tile0 = blockIdx.x << G::logTPB;  // first sub-transform of this block
+  const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
+  const uint64_t* gi = in + blockIdx.z * in_stride + (size_t(rm.irow[blockIdx.y]) << LOGN) + toff;
+  uint64_t* go = out + blockIdx.z * out_stride + (size_t(rm.orow[blockIdx.y]) << LOGN) + toff;
+  ntt_steps<INV, ROWS, LOGN, 0>(gi, go, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
 }
 
-// forward, phase 2: the remaining stages on contiguous blocks of C; canonical output
-__global__ void __launch_bounds__(kT) k_ntt_fwd_rows(uint64_t* data, const __grid_constant__ PrimeMap pm, size_t gstride, const PrimeC* pcs,
-                                                     const uint64_t* tw, uint32_t N, uint32_t R1, uint32_t BPB) {
-  __shared__ uint64_t sm[kTile];
-  const uint32_t pi = pm.p[blockIdx.y];
-  const uint64_t q = pcs[pi].q, q2 = 2 * q;
-  const uint64_t* psi = tw + size_t(pi) * 4 * N;
-  const uint64_t* psip = psi + N;
-  const uint32_t C = N / R1;
-  uint64_t* a = data + blockIdx.z * gstride + size_t(blockIdx.y) * N + size_t(blockIdx.x) * BPB * C;
-  for (uint32_t e = threadIdx.x; e < BPB * C; e += blockDim.x) sm[e] = a[e];
-  __syncthreads();
-  for (uint32_t m = R1, t = C / 2; m < N; m <<= 1, t >>= 1) {
-    for (uint32_t b = threadIdx.x; b < BPB * C / 2; b += blockDim.x) {
-      const uint32_t k = b / (C / 2), bi = b % (C / 2), g = bi / t, u0 = g * 2 * t + bi % t;
-      const uint32_t gb = blockIdx.x * BPB + k;
-      const uint32_t wi = m + gb * (m / R1) + g;
-      const uint64_t w = __ldg(psi + wi), wp = __ldg(psip + wi);
-      uint64_t X = sm[k * C + u0];
-      const uint64_t Y = sm[k * C + u0 + t];
-      X = X >= q2 ? X - q2 : X;
-      const uint64_t T = mul_shoup_lazy(Y, w, wp, q);
-      sm[k * C + u0] = X + T;
-      sm[k * C + u0 + t] = X - T + q2;
-    }
-    __syncthreads();
-  }
-  for (uint32_t e = threadIdx.x; e < BPB * C; e += blockDim.x) {
-    uint64_t v = sm[e];
-    v = v >= q2 ? v - q2 : v;
-    a[e] = v >= q ? v - q : v;
+template <int LOGN>
+void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
+                const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
+                cudaStream_t s) {
+  using Gc = NttGeom<LOGN, false>;
+  using Gr = NttGeom<LOGN, true>;
+  const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch), gr(1u << (Gr::logR1 - Gr::logTPB), n, batch);
+  if (!inverse) {
+    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw);
+    k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw);
+  } else {
+    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw);
+    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw);
   }
 }
 
-// inverse, phase 1: the first stages (t = 1 .. C/2) on contiguous blocks of C
-__global__ void __launch_bounds__(kT) k_ntt_inv_rows(uint64_t* data, const __grid_constant__ PrimeMap pm, size_t gstride, const PrimeC* pcs,
-                                                     const uint64_t* tw, uint32_t N, uint32_t R1, uint32_t BPB) {
-  __shared__ uint64_t sm[kTile];
-  const uint32_t pi = pm.p[blockIdx.y];
-  const uint64_t q = pcs[pi].q, q2 = 2 * q;
-  const uint64_t* ipsi = tw + size_t(pi) * 4 * N + 2 * N;
-  const uint64_t* ipsip = ipsi + N;
-  const uint32_t C = N / R1;
-  uint64_t* a = data + blockIdx.z * gstride + size_t(blockIdx.y) * N + size_t(blockIdx.x) * BPB * C;
-  for (uint32_t e = threadIdx.x; e < BPB * C; e += blockDim.x) sm[e] = a[e];
-  __syncthreads();
-  for (uint32_t t = 1, h = N / 2; t < C; t <<= 1, h >>= 1) {
-    for (uint32_t b = threadIdx.x; b < BPB * C / 2; b += blockDim.x) {
-      const uint32_t k = b / (C / 2), bi = b % (C / 2), g = bi / t, u0 = g * 2 * t + bi % t;
-      const uint32_t gb = blockIdx.x * BPB + k;
-      const uint32_t wi = h + gb * (C / (2 * t)) + g;
-      const uint64_t w = __ldg(ipsi + wi), wp = __ldg(ipsip + wi);
-      const uint64_t X = sm[k * C + u0], Y = sm[k * C + u0 + t];
-      uint64_t s = X + Y;
-      s = s >= q2 ? s - q2 : s;
-      sm[k * C + u0] = s;
-      sm[k * C + u0 + t] = mul_shoup_lazy(X - Y + q2, w, wp, q);
-    }
-    __syncthreads();
-  }
-  for (uint32_t e = threadIdx.x; e < BPB * C; e += blockDim.x) a[e] = sm[e];
-}
-
-// inverse, phase 2: the last log2(R1) stages on columns, then * N^-1; canonical output
-__global__ void __launch_bounds__(kT) k_ntt_inv_cols(uint64_t* data, const __grid_constant__ PrimeMap pm, size_t gstride, const PrimeC* pcs,
-                                                     const uint64_t* tw, uint32_t N, uint32_t R1, uint32_t CPB) {
-  __shared__ uint64_t sm[kTile];
-  const uint32_t pi = pm.p[blockIdx.y];
-  const PrimeC P = pcs[pi];
-  const uint64_t q = P.q, q2 = 2 * q;
-  const uint64_t* ipsi = tw + size_t(pi) * 4 * N + 2 * N;
-  const uint64_t* ipsip = ipsi + N;
-  uint64_t* a = data + blockIdx.z * gstride + size_t(blockIdx.y) * N;
-  const uint32_t C = N / R1, c0 = blockIdx.x * CPB;
-  for (uint32_t e = threadIdx.x; e < R1 * CPB; e += blockDim.x) sm[e] = a[c0 + (e % CPB) + (e / CPB) * C];
-  __syncthreads();
-  for (uint32_t tr = 1, h = R1 / 2; tr < R1; tr <<= 1, h >>= 1) {
-    for (uint32_t b = threadIdx.x; b < (R1 / 2) * CPB; b += blockDim.x) {
-      const uint32_t cc = b % CPB, bi = b / CPB, g = bi / tr, r0 = g * 2 * tr + bi % tr;
-      const uint64_t w = __ldg(ipsi + h + g), wp = __ldg(ipsip + h + g);
-      const uint64_t X = sm[r0 * CPB + cc], Y = sm[(r0 + tr) * CPB + cc];
-      uint64_t s = X + Y;
-      s = s >= q2 ? s - q2 : s;
-      sm[r0 * CPB + cc] = s;
-      sm[(r0 + tr) * CPB + cc] = mul_shoup_lazy(X - Y + q2, w, wp, q);
-    }
-    __syncthreads();
-  }
-  for (uint32_t e = threadIdx.x; e < R1 * CPB; e += blockDim.x)
-    a[c0 + (e % CPB) + (e / CPB) * C] = mul_shoup(sm[e], P.ninv, P.ninv_sh, q);
-}
-
-// ---------------------------------------------------------------- elementwise
-__global__ void k_random_ct(uint64_t* out, const PrimeC* pcs, uint64_t seed, uint64_t tag, uint32_t nl, uint32_t N) {
-  const size_t total = size_t(2) * nl * N;
+// ---------------------------------------------------------------- sampling / keys
+__global__ void k_random_ct(uint64_t* out, const PrimeC* pcs, uint64_t seed, uint64_t tag, uint32_t nl,
+                            uint32_t logN) {
+  const size_t total = size_t(2 * nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t n = x % N, i = (x / N) % nl, p = x / (size_t(N) * nl);
+    const uint32_t n = x & ((1u << logN) - 1), r = x >> logN, p = r / nl, i = r - p * nl;
     out[x] = uniform_mod(hash64(seed, D_CT, tag * 1024 + p * 64 + i, n), pcs[i].q);
   }
 }
 
-__global__ void k_secret(uint64_t* sk, const PrimeC* pcs, uint64_t seed, uint32_t np, uint32_t N) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(np) * N; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t n = x % N, i = x / N;
+__global__ void k_secret(uint64_t* sk, const PrimeC* pcs, uint64_t seed, uint32_t np, uint32_t logN) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(np) << logN);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t n = x & ((1u << logN) - 1), i = x >> logN;
     sk[x] = lift(static_cast<int64_t>(hash64(seed, D_SECRET, 0, n) % 3) - 1, pcs[i].q);
   }
 }
@@ -191,9 +257,10 @@ __device__ inline int64_t cbd(uint64_t h) {
 
 // key digit j: a uniform (NTT form), e small (coefficient form, NTT'd by the host after)
 __global__ void k_key_ae(uint64_t* a, uint64_t* e, const PrimeC* pcs, uint64_t seed, uint64_t keyid, uint32_t j,
-                         uint32_t np, uint32_t N) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(np) * N; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t n = x % N, i = x / N;
+                         uint32_t np, uint32_t logN) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(np) << logN);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t n = x & ((1u << logN) - 1), i = x >> logN;
     const uint64_t q = pcs[i].q;
     a[x] = uniform_mod(hash64(seed, D_KEY_A, keyid * 4096 + j * 64 + i, n), q);
     e[x] = lift(cbd(hash64(seed, D_KEY_E, keyid * 4096 + j, n)), q);
@@ -203,9 +270,10 @@ __global__ void k_key_ae(uint64_t* a, uint64_t* e, const PrimeC* pcs, uint64_t s
 // b = e - a s + [i in digit j] P_i s'
 __global__ void k_key_b(uint64_t* b, const uint64_t* a, const uint64_t* e, const uint64_t* s, const uint64_t* sp,
                         const PrimeC* pcs, const uint64_t* Pmod, uint32_t j, uint32_t alpha, uint32_t nq,
-                        uint32_t np, uint32_t N) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(np) * N; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t i = x / N;
+                        uint32_t np, uint32_t logN) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(np) << logN);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = x >> logN;
     const PrimeC& P = pcs[i];
     uint64_t v = sub_mod(e[x], mul_mod(a[x], s[x], P), P.q);
     if (i < nq && i / alpha == j) v = add_mod(v, mul_mod(Pmod[i], sp[x], P), P.q);
@@ -213,9 +281,10 @@ __global__ void k_key_b(uint64_t* b, const uint64_t* a, const uint64_t* e, const
   }
 }
 
-__global__ void k_square(uint64_t* out, const uint64_t* in, const PrimeC* pcs, uint32_t np, uint32_t N) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(np) * N; x += size_t(gridDim.x) * blockDim.x)
-    out[x] = mul_mod(in[x], in[x], pcs[x / N]);
+__global__ void k_square(uint64_t* out, const uint64_t* in, const PrimeC* pcs, uint32_t np, uint32_t logN) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(np) << logN);
+       x += size_t(gridDim.x) * blockDim.x)
+    out[x] = mul_mod(in[x], in[x], pcs[x >> logN]);
 }
 
 __device__ inline uint32_t galois_src(uint32_t j, uint64_t g, uint32_t logN) {
@@ -224,140 +293,179 @@ __device__ inline uint32_t galois_src(uint32_t j, uint64_t g, uint32_t logN) {
   return bitrev(static_cast<uint32_t>((e - 1) >> 1), logN);
 }
 
-// out[p][i][n] = in[p][i][src(n)] for `npoly` polys of nl limbs
+// out[r][n] = in[r][src(n)] for `rows` rows per batch item
 __global__ void k_automorph(uint64_t* out, const uint64_t* in, uint64_t g, uint32_t logN, uint32_t rows,
                             size_t gstride) {
-  const uint32_t N = 1u << logN;
   const uint64_t* src = in + blockIdx.z * gstride;
   uint64_t* dst = out + blockIdx.z * gstride;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(rows) * N; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t n = x % N;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(rows) << logN);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t n = x & ((1u << logN) - 1);
     dst[x] = src[(x - n) + galois_src(n, g, logN)];
   }
 }
 
-// tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 (all NTT form, nl limbs)
-__global__ void k_tensor(const uint64_t* a, const uint64_t* b, uint64_t* d0, uint64_t* d1, uint64_t* d2,
-                         const PrimeC* pcs, uint32_t nl, uint32_t N, size_t ct_stride, size_t d_stride) {
+// ---------------------------------------------------------------- HMult / key switching
+// tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 (NTT form, nl limbs)
+__global__ void k_tensor(const uint64_t* a, const uint64_t* b, uint64_t* d, const PrimeC* pcs, uint32_t nl,
+                         uint32_t logN, size_t ct_stride, size_t d_stride) {
   const uint64_t* A = a + blockIdx.z * ct_stride;
   const uint64_t* Bb = b + blockIdx.z * ct_stride;
-  const size_t off = blockIdx.z * d_stride, half = size_t(nl) * N;
+  uint64_t* D = d + blockIdx.z * d_stride;
+  const size_t half = size_t(nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
-    const PrimeC& P = pcs[x / N];
+    const PrimeC& P = pcs[x >> logN];
     const uint64_t a0 = A[x], a1 = A[half + x], b0 = Bb[x], b1 = Bb[half + x];
-    d0[off + x] = mul_mod(a0, b0, P);
-    d1[off + x] = add_mod(mul_mod(a0, b1, P), mul_mod(a1, b0, P), P.q);
-    d2[off + x] = mul_mod(a1, b1, P);
+    D[x] = mul_mod(a0, b0, P);
+    D[half + x] = reduce128(static_cast<u128>(a0) * b1 + static_cast<u128>(a1) * b0, P);
+    D[2 * half + x] = mul_mod(a1, b1, P);
   }
 }
 
-// ---------------------------------------------------------------- key switching
-// Base-conversion constants of one (source set -> target set) conversion:
-//   y_i = [x_i * hinv_i]_{src_i};  out_t = sum_i y_i * h[t][i] mod t  (Shoup constants)
-struct Conv {
+// One base conversion job: y_i = [x_i * hinv_i]_{src_i};  out_t = sum_i y_i h[t][i] mod t.
+constexpr int kMaxSrc = 32, kMaxTgt = 64;
+struct ConvJob {
   uint32_t nsrc, ntgt;
-  uint8_t src[32];      // source prime indices
-  uint8_t tgt[64];      // target prime indices
-  uint8_t tgt_row[64];  // destination row (limb) of each target in the output array
-  uint64_t hinv[32], hinv_sh[32];
+  uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
+  uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
+  uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
+  uint64_t h[kMaxTgt][kMaxSrc];
 };
 
-__global__ void k_conv(const uint64_t* in, uint32_t in_row0, uint64_t* out, const Conv* cv, const PrimeC* pcs,
-                       const uint64_t* h, const uint64_t* h_sh, uint32_t N, size_t in_stride, size_t out_stride) {
-  const Conv& C = *cv;
-  const uint64_t* I = in + blockIdx.z * in_stride;
-  uint64_t* O = out + blockIdx.z * out_stride;
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    uint64_t y[32];
-    for (uint32_t i = 0; i < C.nsrc; ++i)
-      y[i] = mul_shoup(I[size_t(in_row0 + i) * N + n], C.hinv[i], C.hinv_sh[i], pcs[C.src[i]].q);
-    for (uint32_t t = blockIdx.y; t < C.ntgt; t += gridDim.y) {
-      const uint64_t qt = pcs[C.tgt[t]].q, q2 = 2 * qt;
-      const uint64_t* ht = h + size_t(t) * 32;
-      const uint64_t* hs = h_sh + size_t(t) * 32;
-      uint64_t acc = 0;
-      for (uint32_t i = 0; i < C.nsrc; ++i) {
-        acc += mul_shoup_lazy(y[i], ht[i], hs[i], qt);
-        acc = acc >= q2 ? acc - q2 : acc;
+// A = nsrc (compile time, <= 15 so the 128-bit sums cannot overflow), or 0 for a
+// run-time count (partial reductions every 15 terms).
+template <int A>
+__global__ void __launch_bounds__(kT) k_conv(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
+                                             const ConvJob* jobs, const PrimeC* pcs, uint32_t logN) {
+  constexpr int AS = A ? A : kMaxSrc;
+  __shared__ uint64_t h_s[kMaxTgt * AS];
+  __shared__ PrimeC tq[kMaxTgt];
+  __shared__ uint64_t hinv_s[AS], hinvsh_s[AS], qs_s[AS];
+  __shared__ uint32_t orow_s[kMaxTgt];
+  const ConvJob& J = jobs[blockIdx.y];
+  const uint32_t nsrc = A ? A : J.nsrc, ntgt = J.ntgt;
+  for (uint32_t k = threadIdx.x; k < ntgt * nsrc; k += blockDim.x) h_s[k] = J.h[k / nsrc][k % nsrc];
+  for (uint32_t k = threadIdx.x; k < ntgt; k += blockDim.x) {
+    tq[k] = pcs[J.tgt[k]];
+    orow_s[k] = J.out_row + J.tgt_row[k];
+  }
+  for (uint32_t k = threadIdx.x; k < nsrc; k += blockDim.x) {
+    hinv_s[k] = J.hinv[k];
+    hinvsh_s[k] = J.hinv_sh[k];
+    qs_s[k] = pcs[J.src[k]].q;
+  }
+  __syncthreads();
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t* I = in + blockIdx.z * in_stride + (size_t(J.in_row) << logN) + n;
+  uint64_t* O = out + blockIdx.z * out_stride + n;
+  uint64_t y[AS];
+#pragma unroll
+  for (int i = 0; i < AS; ++i)
+    if (A || i < int(nsrc)) y[i] = mul_shoup(I[size_t(i) << logN], hinv_s[i], hinvsh_s[i], qs_s[i]);
+  for (uint32_t t = 0; t < ntgt; ++t) {
+    const uint64_t* ht = h_s + t * nsrc;
+    u128 acc = 0;
+    if (A) {
+#pragma unroll
+      for (int i = 0; i < AS; ++i) acc += static_cast<u128>(y[i]) * ht[i];
+    } else {
+      for (uint32_t i = 0; i < nsrc; ++i) {
+        acc += static_cast<u128>(y[i]) * ht[i];
+        if (i % 15 == 14) acc = reduce128(acc, tq[t]);
       }
-      O[size_t(C.tgt_row[t]) * N + n] = acc >= qt ? acc - qt : acc;
     }
+    O[size_t(orow_s[t]) << logN] = reduce128(acc, tq[t]);
   }
 }
 
-// acc_w[x] = sum_j ext_j[x] * key_w[j][gi(x)]  (w = 0: b, 1: a), nx rows
-__global__ void k_ks_inner(const uint64_t* ext, uint64_t* acc, const uint64_t* kb, const uint64_t* ka, const __grid_constant__ PrimeMap pm,
-                           const PrimeC* pcs, uint32_t nd, uint32_t nx, uint32_t np, uint32_t N, size_t ext_stride,
-                           size_t acc_stride) {
-  const uint64_t* E = ext + blockIdx.z * ext_stride;
-  uint64_t* A = acc + blockIdx.z * acc_stride;
-  const size_t rowN = size_t(nx) * N;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < rowN; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t row = x / N, n = x % N, gi = pm.p[row];
-    const PrimeC& P = pcs[gi];
-    uint64_t s0 = 0, s1 = 0;
-    for (uint32_t j = 0; j < nd; ++j) {
-      const uint64_t e = E[size_t(j) * rowN + x];
-      const size_t kx = (size_t(j) * np + gi) * N + n;
-      s0 = add_mod(s0, mul_mod(e, __ldg(kb + kx), P), P.q);
-      s1 = add_mod(s1, mul_mod(e, __ldg(ka + kx), P), P.q);
+// acc_w[x] = sum_j e_j[x] * key_w[j][prime(x)] over the nx extended rows, w = 0 (b), 1 (a);
+// e_j[x] = d[x] on digit j's own rows (NTT form, never converted), ext_j[x] elsewhere.
+// Each thread holds its key words and walks the whole batch.
+constexpr int kMaxDigits = 15;
+template <int ND>
+__global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext_stride, const uint64_t* d,
+                                                 size_t d_stride, uint64_t* acc, size_t acc_stride,
+                                                 const uint64_t* kb, const uint64_t* ka, const PrimeC* pcs,
+                                                 uint32_t nx, uint32_t nl, uint32_t np, uint32_t nq, uint32_t alpha,
+                                                 uint32_t logN, uint32_t batch) {
+  const size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  const uint32_t row = x >> logN, n = x & ((1u << logN) - 1);
+  if (row >= nx) return;
+  const uint32_t gi = row < nl ? row : nq + (row - nl);
+  const PrimeC P = pcs[gi];
+  uint64_t kbr[ND], kar[ND];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) {
+    const size_t kx = (size_t(j * np + gi) << logN) + n;
+    kbr[j] = __ldg(kb + kx);
+    kar[j] = __ldg(ka + kx);
+  }
+  const uint32_t own = row < nl ? row / alpha : 0xFFFFFFFFu;
+  const size_t rowsN = size_t(nx) << logN;
+#pragma unroll 2
+  for (uint32_t b = 0; b < batch; ++b) {
+    const uint64_t* E = ext + b * ext_stride + x;
+    uint64_t e[ND];
+#pragma unroll
+    for (int j = 0; j < ND; ++j) e[j] = uint32_t(j) == own ? d[b * d_stride + x] : E[j * rowsN];
+    u128 s0 = 0, s1 = 0;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      s0 += static_cast<u128>(e[j]) * kbr[j];
+      s1 += static_cast<u128>(e[j]) * kar[j];
     }
-    A[x] = s0;
-    A[rowN + x] = s1;
+    uint64_t* Ac = acc + b * acc_stride + x;
+    Ac[0] = reduce128(s0, P);
+    Ac[rowsN] = reduce128(s1, P);
   }
 }
 
 // out_w[i] = (acc_w[i] - conv_w[i]) * pinv_i (+ add_w[i] when given)
 __global__ void k_moddown(const uint64_t* acc, const uint64_t* conv, const uint64_t* add0, const uint64_t* add1,
                           uint64_t* out, const PrimeC* pcs, const uint64_t* pinv, const uint64_t* pinv_sh, uint32_t nl,
-                          uint32_t nx, uint32_t N, size_t acc_stride, size_t conv_stride, size_t add_stride,
+                          uint32_t nx, uint32_t logN, size_t acc_stride, size_t conv_stride, size_t add_stride,
                           size_t out_stride) {
   const uint64_t* A = acc + blockIdx.z * acc_stride;
   const uint64_t* Cv = conv + blockIdx.z * conv_stride;
   uint64_t* O = out + blockIdx.z * out_stride;
-  const size_t half = size_t(nl) * N;
+  const size_t half = size_t(nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * half; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t w = x / half;
-    const size_t r = x - w * half;
-    const uint32_t i = r / N;
+    const uint32_t w = x >= half;
+    const size_t r = x - (w ? half : 0);
+    const uint32_t i = r >> logN;
     const uint64_t q = pcs[i].q;
-    uint64_t v = mul_shoup(sub_mod(A[size_t(w) * nx * N + r], Cv[x], q), pinv[i], pinv_sh[i], q);
+    uint64_t v = mul_shoup(sub_mod(A[(size_t(w * nx) << logN) + r], Cv[x], q), pinv[i], pinv_sh[i], q);
     const uint64_t* ad = w == 0 ? add0 : add1;
     if (ad) v = add_mod(v, ad[blockIdx.z * add_stride + r], q);
     O[x] = v;
   }
 }
 
-__global__ void k_rescale_sub(const uint64_t* in, const uint64_t* t, uint64_t* out, const PrimeC* pcs,
-                              const uint64_t* qinv, const uint64_t* qinv_sh, uint32_t level, uint32_t N,
-                              size_t in_stride, size_t t_stride, size_t out_stride) {
-  const size_t per = size_t(level) * N;
+// ---------------------------------------------------------------- rescale
+// t[p][i][n] = last[p][n] mod q_i (the last limb, coefficient form, replicated into every q_i)
+__global__ void k_rescale_spread(const uint64_t* last, uint64_t* t, const PrimeC* pcs, uint32_t level, uint32_t logN,
+                                 size_t last_stride, size_t t_stride) {
+  const size_t per = size_t(level) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * per; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = x / per;
-    const size_t r = x - p * per;
-    const uint32_t i = r / N;
+    const uint32_t p = x >= per;
+    const size_t r = x - (p ? per : 0);
+    const uint32_t i = r >> logN, n = r & ((1u << logN) - 1);
+    t[blockIdx.z * t_stride + x] = reduce64(last[blockIdx.z * last_stride + (size_t(p) << logN) + n], pcs[i]);
+  }
+}
+
+__global__ void k_rescale_sub(const uint64_t* in, const uint64_t* t, uint64_t* out, const PrimeC* pcs,
+                              const uint64_t* qinv, const uint64_t* qinv_sh, uint32_t level, uint32_t logN,
+                              size_t in_stride, size_t t_stride, size_t out_stride) {
+  const size_t per = size_t(level) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * per; x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t p = x >= per;
+    const size_t r = x - (p ? per : 0);
+    const uint32_t i = r >> logN;
     const uint64_t q = pcs[i].q;
-    const uint64_t c = in[blockIdx.z * in_stride + size_t(p) * (level + 1) * N + r];
+    const uint64_t c = in[blockIdx.z * in_stride + (size_t(p * (level + 1)) << logN) + r];
     out[blockIdx.z * out_stride + x] = mul_shoup(sub_mod(c, t[blockIdx.z * t_stride + x], q), qinv[i], qinv_sh[i], q);
   }
-}
-
-// t[p][i][n] = last[p][n] mod q_i (the last limb, coefficient form, replicated into every q_i)
-__global__ void k_rescale_spread(const uint64_t* last, uint64_t* t, const PrimeC* pcs, uint32_t level, uint32_t N,
-                                 size_t last_stride, size_t t_stride) {
-  const size_t per = size_t(level) * N;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * per; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = x / per;
-    const size_t r = x - p * per;
-    const uint32_t i = r / N, n = r % N;
-    t[blockIdx.z * t_stride + x] = reduce64(last[blockIdx.z * last_stride + size_t(p) * N + n], pcs[i]);
-  }
-}
-
-__global__ void k_copy_rows(const uint64_t* in, uint64_t* out, uint32_t rows, uint32_t N, size_t in_stride,
-                            size_t out_stride) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < size_t(rows) * N; x += size_t(gridDim.x) * blockDim.x)
-    out[blockIdx.z * out_stride + x] = in[blockIdx.z * in_stride + x];
 }
 
 // host helpers -----------------------------------------------------------------------
@@ -420,13 +528,58 @@ DevBuf upload(const std::vector<T>& v) {
   return d;
 }
 
-PrimeMap map_of(const std::vector<uint32_t>& p) {
-  PrimeMap m{};
-  for (size_t i = 0; i < p.size() && i < 64; ++i) m.p[i] = static_cast<uint8_t>(p[i]);
-  return m;
+template <class T>
+T* dptr(const DevBuf& b) {
+  return reinterpret_cast<T*>(b.get());
+}
+
+std::vector<uint32_t> iota_rows(uint32_t n, uint32_t first = 0) {
+  std::vector<uint32_t> v(n);
+  for (uint32_t i = 0; i < n; ++i) v[i] = first + i;
+  return v;
 }
 
 }  // namespace
+
+// ================================================================== NTT launch
+void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
+              const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
+              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse) {
+  if (irows.empty() || batch == 0) return;
+  if (irows.size() != orows.size() || irows.size() != primes.size()) fail(HS_E_INVALID_ARG, "ntt_rows: size mismatch");
+  Runtime& rt = Runtime::get();
+  cudaStream_t s = rt.stream();
+  const uint32_t logN = c.spec.logN;
+  const uint64_t* tw = dptr<const uint64_t>(c.d_tw);
+  for (size_t base = 0; base < irows.size(); base += kMaxRows) {
+    const uint32_t n = static_cast<uint32_t>(std::min<size_t>(kMaxRows, irows.size() - base));
+    RowMap rm{}, rm2{};
+    for (uint32_t i = 0; i < n; ++i) {
+      rm.irow[i] = static_cast<uint16_t>(irows[base + i]);
+      rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
+      rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
+    }
+    switch (logN) {
+#define HS_NTT_CASE(L) \
+  case L:              \
+    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, s); \
+    break;
+      HS_NTT_CASE(9) HS_NTT_CASE(10) HS_NTT_CASE(11) HS_NTT_CASE(12) HS_NTT_CASE(13) HS_NTT_CASE(14)
+      HS_NTT_CASE(15) HS_NTT_CASE(16) HS_NTT_CASE(17)
+#undef HS_NTT_CASE
+      default:
+        fail(HS_E_INVALID_ARG, "ntt: unsupported ring degree");
+    }
+    cuda_ok(cudaGetLastError(), "ntt launch");
+    rt.note_launch(2);
+  }
+}
+
+void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, uint32_t batch, size_t gstride,
+         bool inverse) {
+  const auto rows = iota_rows(static_cast<uint32_t>(prime_of.size()));
+  ntt_rows(c, data, gstride, data, gstride, rows, rows, prime_of, batch, inverse);
+}
 
 // ================================================================== context
 uint64_t Ctx::galois_elt(int64_t k, uint32_t logN) {
@@ -441,12 +594,14 @@ uint64_t Ctx::galois_elt(int64_t k, uint32_t logN) {
 Ctx::Ctx(const Spec& s) : spec(s) {
   if (s.logN < 9 || s.logN > 17) fail(HS_E_INVALID_ARG, "rns: logN must be in [9, 17]");
   if (s.dnum < 1 || s.K < 1 || s.L + 1 + s.K > 64) fail(HS_E_INVALID_ARG, "rns: bad prime counts");
+  if (s.dnum > s.L + 1) fail(HS_E_INVALID_ARG, "rns: dnum larger than the number of q primes");
   if (s.logq0 > 61 || s.logq > 61 || s.logp > 61 || s.logq < 20) fail(HS_E_INVALID_ARG, "rns: primes must be 20..61 bits");
   N = 1u << s.logN;
   nq = s.L + 1;
   np = nq + s.K;
   alpha = (nq + s.dnum - 1) / s.dnum;
-  if (alpha > 32) fail(HS_E_INVALID_ARG, "rns: digits wider than 32 primes");
+  if (alpha > kMaxSrc || s.K > kMaxSrc) fail(HS_E_INVALID_ARG, "rns: digits / special primes wider than 32 primes");
+  if ((nq + alpha - 1) / alpha > kMaxDigits) fail(HS_E_INVALID_ARG, "rns: more than 15 digits");
   // primes (rns_oracle.c rnso_primes)
   const uint64_t twoN = 2ULL << s.logN;
   const uint32_t bits[3] = {s.logq0, s.logq, s.logp}, cnt[3] = {1, s.L, s.K};
@@ -471,6 +626,8 @@ Ctx::Ctx(const Spec& s) : spec(s) {
     p.k = 64 - __builtin_clzll(q);
     p.mu = static_cast<uint64_t>((static_cast<u128>(1) << (2 * p.k)) / q);
     p.m64 = static_cast<uint64_t>((static_cast<u128>(1) << 64) / q);
+    p.r64 = static_cast<uint64_t>((static_cast<u128>(1) << 64) % q);
+    p.r64_sh = shoup_of(p.r64, q);
     p.ninv = h_inv(N % q, q);
     p.ninv_sh = shoup_of(p.ninv, q);
     pc.push_back(p);
@@ -494,11 +651,9 @@ Ctx::Ctx(const Spec& s) : spec(s) {
   // secret key (NTT form over every prime)
   Runtime& rt = Runtime::get();
   d_sk = rt.alloc(size_t(np) * N);
-  k_secret<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(reinterpret_cast<uint64_t*>(d_sk.get()), dpc(), s.seed, np, N);
+  k_secret<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(dptr<uint64_t>(d_sk), dpc(), s.seed, np, s.logN);
   cuda_ok(cudaGetLastError(), "secret");
-  std::vector<uint32_t> all(np);
-  for (uint32_t i = 0; i < np; ++i) all[i] = i;
-  ntt(*this, reinterpret_cast<uint64_t*>(d_sk.get()), all, 1, 0, false);
+  ntt(*this, dptr<uint64_t>(d_sk), iota_rows(np), 1, 0, false);
   rt.sync();
 }
 
@@ -515,19 +670,17 @@ void Ctx::make_key(uint64_t keyid, const uint64_t* sprime, Key* out) {
     Pm[i] = v;
   }
   DevBuf dP = upload(Pm);
-  std::vector<uint32_t> all(np);
-  for (uint32_t i = 0; i < np; ++i) all[i] = i;
-  uint64_t* B = reinterpret_cast<uint64_t*>(out->b.get());
-  uint64_t* A = reinterpret_cast<uint64_t*>(out->a.get());
-  uint64_t* E = reinterpret_cast<uint64_t*>(e.get());
+  const auto all = iota_rows(np);
+  uint64_t* B = dptr<uint64_t>(out->b);
+  uint64_t* A = dptr<uint64_t>(out->a);
+  uint64_t* E = dptr<uint64_t>(e);
   for (uint32_t j = 0; j < spec.dnum; ++j) {
     uint64_t* aj = A + size_t(j) * np * N;
     uint64_t* bj = B + size_t(j) * np * N;
-    k_key_ae<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(aj, E, dpc(), spec.seed, keyid, j, np, N);
+    k_key_ae<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(aj, E, dpc(), spec.seed, keyid, j, np, spec.logN);
     ntt(*this, E, all, 1, 0, false);
-    k_key_b<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(bj, aj, E, reinterpret_cast<const uint64_t*>(d_sk.get()),
-                                                             sprime, dpc(), reinterpret_cast<const uint64_t*>(dP.get()),
-                                                             j, alpha, nq, np, N);
+    k_key_b<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(bj, aj, E, dptr<const uint64_t>(d_sk), sprime, dpc(),
+                                                             dptr<const uint64_t>(dP), j, alpha, nq, np, spec.logN);
     cuda_ok(cudaGetLastError(), "keygen");
   }
   rt.sync();
@@ -538,10 +691,10 @@ const Ctx::Key& Ctx::relin_key() {
   if (!relin_) {
     Runtime& rt = Runtime::get();
     DevBuf s2 = rt.alloc(size_t(np) * N);
-    k_square<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(reinterpret_cast<uint64_t*>(s2.get()),
-                                                              reinterpret_cast<const uint64_t*>(d_sk.get()), dpc(), np, N);
+    k_square<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(dptr<uint64_t>(s2), dptr<const uint64_t>(d_sk), dpc(),
+                                                              np, spec.logN);
     relin_ = std::make_unique<Key>();
-    make_key(0, reinterpret_cast<const uint64_t*>(s2.get()), relin_.get());
+    make_key(0, dptr<const uint64_t>(s2), relin_.get());
   }
   return *relin_;
 }
@@ -552,91 +705,65 @@ const Ctx::Key& Ctx::galois_key(uint64_t g) {
   if (it != gal_.end()) return *it->second;
   Runtime& rt = Runtime::get();
   DevBuf sg = rt.alloc(size_t(np) * N);
-  k_automorph<<<dim3(grid_of(size_t(np) * N), 1, 1), kT, 0, rt.stream()>>>(
-      reinterpret_cast<uint64_t*>(sg.get()), reinterpret_cast<const uint64_t*>(d_sk.get()), g, spec.logN, np, 0);
+  k_automorph<<<dim3(grid_of(size_t(np) * N), 1, 1), kT, 0, rt.stream()>>>(dptr<uint64_t>(sg),
+                                                                          dptr<const uint64_t>(d_sk), g, spec.logN, np, 0);
   auto k = std::make_unique<Key>();
-  make_key(1 + g, reinterpret_cast<const uint64_t*>(sg.get()), k.get());
+  make_key(1 + g, dptr<const uint64_t>(sg), k.get());
   return *gal_.emplace(g, std::move(k)).first->second;
 }
 
 // ================================================================== device ops
-void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, uint32_t batch, size_t gstride,
-         bool inverse) {
-  if (prime_of.empty() || batch == 0) return;
-  Runtime& rt = Runtime::get();
-  const uint32_t N = c.N, s1 = c.spec.logN / 2, R1 = 1u << s1, C = N / R1;
-  const uint32_t CPB = std::min<uint32_t>(kTile / R1, C), BPB = std::min<uint32_t>(kTile / C, R1);
-  const PrimeMap pm = map_of(prime_of);
-  const uint32_t nl = static_cast<uint32_t>(prime_of.size());
-  const dim3 g1(C / CPB, nl, batch), g2(N / (BPB * C), nl, batch);
-  const uint64_t* tw = reinterpret_cast<const uint64_t*>(c.d_tw.get());
-  if (!inverse) {
-    k_ntt_fwd_cols<<<g1, kT, 0, rt.stream()>>>(data, pm, gstride, c.dpc(), tw, N, R1, CPB);
-    k_ntt_fwd_rows<<<g2, kT, 0, rt.stream()>>>(data, pm, gstride, c.dpc(), tw, N, R1, BPB);
-  } else {
-    k_ntt_inv_rows<<<g2, kT, 0, rt.stream()>>>(data, pm, gstride, c.dpc(), tw, N, R1, BPB);
-    k_ntt_inv_cols<<<g1, kT, 0, rt.stream()>>>(data, pm, gstride, c.dpc(), tw, N, R1, CPB);
-  }
-  cuda_ok(cudaGetLastError(), "ntt launch");
-  rt.note_launch(2);
-}
-
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out) {
   Runtime& rt = Runtime::get();
   k_random_ct<<<grid_of(size_t(2) * (level + 1) * c.N), kT, 0, rt.stream()>>>(out, c.dpc(), c.spec.seed, tag, level + 1,
-                                                                             c.N);
+                                                                             c.spec.logN);
   cuda_ok(cudaGetLastError(), "random_ct");
   rt.note_launch();
 }
 
 namespace {
 
-// Base-conversion plan (host-built, device-resident, cached per (level, digit)).
-struct ConvPlan {
-  DevBuf cv, h, h_sh;
-};
-
-ConvPlan build_conv(const Ctx& c, const std::vector<uint32_t>& src, const std::vector<uint32_t>& tgt,
-                    const std::vector<uint32_t>& tgt_row) {
-  Conv cv{};
-  cv.nsrc = static_cast<uint32_t>(src.size());
-  cv.ntgt = static_cast<uint32_t>(tgt.size());
-  std::vector<uint64_t> h(tgt.size() * 32, 0), hs(tgt.size() * 32, 0);
+void fill_conv(const Ctx& c, const std::vector<uint32_t>& src, const std::vector<uint32_t>& tgt,
+               const std::vector<uint32_t>& tgt_row, uint32_t in_row, uint32_t out_row, ConvJob* cv) {
+  std::memset(cv, 0, sizeof *cv);
+  cv->nsrc = static_cast<uint32_t>(src.size());
+  cv->ntgt = static_cast<uint32_t>(tgt.size());
+  cv->in_row = in_row;
+  cv->out_row = out_row;
   for (size_t i = 0; i < src.size(); ++i) {
     const uint64_t qi = c.primes[src[i]];
     uint64_t v = 1;
     for (size_t m = 0; m < src.size(); ++m)
       if (m != i) v = h_mulmod(v, c.primes[src[m]] % qi, qi);
-    cv.src[i] = static_cast<uint8_t>(src[i]);
-    cv.hinv[i] = h_inv(v, qi);
-    cv.hinv_sh[i] = shoup_of(cv.hinv[i], qi);
+    cv->src[i] = static_cast<uint8_t>(src[i]);
+    cv->hinv[i] = h_inv(v, qi);
+    cv->hinv_sh[i] = shoup_of(cv->hinv[i], qi);
   }
   for (size_t t = 0; t < tgt.size(); ++t) {
     const uint64_t qt = c.primes[tgt[t]];
-    cv.tgt[t] = static_cast<uint8_t>(tgt[t]);
-    cv.tgt_row[t] = static_cast<uint8_t>(tgt_row[t]);
+    cv->tgt[t] = static_cast<uint8_t>(tgt[t]);
+    cv->tgt_row[t] = static_cast<uint8_t>(tgt_row[t]);
     for (size_t i = 0; i < src.size(); ++i) {
       uint64_t v = 1;
       for (size_t m = 0; m < src.size(); ++m)
         if (m != i) v = h_mulmod(v, c.primes[src[m]] % qt, qt);
-      h[t * 32 + i] = v;
-      hs[t * 32 + i] = shoup_of(v, qt);
+      cv->h[t][i] = v;
     }
   }
-  ConvPlan p;
-  p.cv = upload(std::vector<Conv>{cv});
-  p.h = upload(h);
-  p.h_sh = upload(hs);
-  return p;
 }
 
+// Per-level plan: conversion jobs, NTT row lists and scalar tables (device resident).
 struct KsPlan {
   uint32_t nl, nx, nd;
-  std::vector<uint32_t> ext_primes;  // extended basis row -> prime
-  std::vector<ConvPlan> up;          // per digit
-  ConvPlan down;                     // P -> Q_l
-  DevBuf pinv, pinv_sh;              // [nl] P^-1 mod q_i
-  DevBuf qinv, qinv_sh;              // [level] q_level^-1 mod q_i (rescale)
+  std::vector<uint32_t> ext_primes;   // extended basis row -> prime
+  DevBuf up_jobs;                     // ConvJob[nd]: digit j -> ext rows of block j
+  uint32_t n_full = 0;                // digits [0, n_full) have alpha sources; the rest fewer
+  std::vector<uint32_t> up_rows, up_primes;  // ext rows (j*nx + x) to NTT after ModUp
+  DevBuf down_jobs;                   // ConvJob[2]: acc_w P rows -> conv rows w*nl..
+  std::vector<uint32_t> p_rows, p_primes;    // acc P rows (both halves) for the iNTT
+  std::vector<uint32_t> cv_rows, cv_primes;  // conv rows (both halves) for the NTT
+  DevBuf pinv, pinv_sh;               // [nl] P^-1 mod q_i
+  DevBuf qinv, qinv_sh;               // [level] q_level^-1 mod q_i (rescale)
 };
 
 std::mutex g_plan_mu;
@@ -644,34 +771,52 @@ std::map<std::pair<const Ctx*, uint32_t>, std::unique_ptr<KsPlan>> g_plans;
 
 std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
   auto p = std::make_unique<KsPlan>();
-  p->nl = level + 1;
-  p->nx = p->nl + c.spec.K;
-  p->nd = (p->nl + c.alpha - 1) / c.alpha;
-  for (uint32_t i = 0; i < p->nl; ++i) p->ext_primes.push_back(i);
-  for (uint32_t k = 0; k < c.spec.K; ++k) p->ext_primes.push_back(c.nq + k);
+  const uint32_t nl = level + 1, K = c.spec.K;
+  p->nl = nl;
+  p->nx = nl + K;
+  p->nd = (nl + c.alpha - 1) / c.alpha;
+  for (uint32_t i = 0; i < nl; ++i) p->ext_primes.push_back(i);
+  for (uint32_t k = 0; k < K; ++k) p->ext_primes.push_back(c.nq + k);
+  std::vector<ConvJob> up(p->nd);
   for (uint32_t j = 0; j < p->nd; ++j) {
-    const uint32_t lo = j * c.alpha, hi = std::min(lo + c.alpha, p->nl);
+    const uint32_t lo = j * c.alpha, hi = std::min(lo + c.alpha, nl);
+    if (hi - lo == c.alpha) p->n_full = j + 1;
     std::vector<uint32_t> src, tgt, row;
     for (uint32_t i = lo; i < hi; ++i) src.push_back(i);
     for (uint32_t x = 0; x < p->nx; ++x)
       if (x < lo || x >= hi) {
         tgt.push_back(p->ext_primes[x]);
         row.push_back(x);
+        p->up_rows.push_back(j * p->nx + x);
+        p->up_primes.push_back(p->ext_primes[x]);
       }
-    p->up.push_back(build_conv(c, src, tgt, row));
+    fill_conv(c, src, tgt, row, lo, j * p->nx, &up[j]);
   }
+  p->up_jobs = upload(up);
+  std::vector<ConvJob> down(2);
   std::vector<uint32_t> src, tgt, row;
-  for (uint32_t k = 0; k < c.spec.K; ++k) src.push_back(c.nq + k);
-  for (uint32_t i = 0; i < p->nl; ++i) {
+  for (uint32_t k = 0; k < K; ++k) src.push_back(c.nq + k);
+  for (uint32_t i = 0; i < nl; ++i) {
     tgt.push_back(i);
     row.push_back(i);
   }
-  p->down = build_conv(c, src, tgt, row);
-  std::vector<uint64_t> pinv(p->nl), pinv_sh(p->nl);
-  for (uint32_t i = 0; i < p->nl; ++i) {
+  for (uint32_t w = 0; w < 2; ++w) {
+    fill_conv(c, src, tgt, row, w * p->nx + nl, w * nl, &down[w]);
+    for (uint32_t k = 0; k < K; ++k) {
+      p->p_rows.push_back(w * p->nx + nl + k);
+      p->p_primes.push_back(c.nq + k);
+    }
+    for (uint32_t i = 0; i < nl; ++i) {
+      p->cv_rows.push_back(w * nl + i);
+      p->cv_primes.push_back(i);
+    }
+  }
+  p->down_jobs = upload(down);
+  std::vector<uint64_t> pinv(nl), pinv_sh(nl);
+  for (uint32_t i = 0; i < nl; ++i) {
     const uint64_t q = c.primes[i];
     uint64_t v = 1;
-    for (uint32_t k = 0; k < c.spec.K; ++k) v = h_mulmod(v, c.primes[c.nq + k] % q, q);
+    for (uint32_t k = 0; k < K; ++k) v = h_mulmod(v, c.primes[c.nq + k] % q, q);
     pinv[i] = h_inv(v, q);
     pinv_sh[i] = shoup_of(pinv[i], q);
   }
@@ -695,6 +840,32 @@ const KsPlan& ks_plan(const Ctx& c, uint32_t level) {
   return *g_plans.emplace(key, build_plan(c, level)).first->second;
 }
 
+template <int A>
+void launch_conv_a(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
+                   uint32_t njobs, const Ctx& c, uint32_t batch, cudaStream_t s) {
+  const dim3 g((c.N + kT - 1) / kT, njobs, batch);
+  k_conv<A><<<g, kT, 0, s>>>(in, in_stride, out, out_stride, jobs, c.dpc(), c.spec.logN);
+}
+
+void launch_conv(uint32_t nsrc, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
+                 const ConvJob* jobs, uint32_t njobs, const Ctx& c, uint32_t batch) {
+  if (njobs == 0) return;
+  cudaStream_t s = Runtime::get().stream();
+  switch (nsrc) {
+#define HS_CONV_CASE(a) \
+  case a:               \
+    launch_conv_a<a>(in, in_stride, out, out_stride, jobs, njobs, c, batch, s); \
+    break;
+    HS_CONV_CASE(1) HS_CONV_CASE(2) HS_CONV_CASE(3) HS_CONV_CASE(4) HS_CONV_CASE(5) HS_CONV_CASE(6)
+    HS_CONV_CASE(7) HS_CONV_CASE(8) HS_CONV_CASE(9) HS_CONV_CASE(10) HS_CONV_CASE(11) HS_CONV_CASE(12)
+#undef HS_CONV_CASE
+    default:
+      launch_conv_a<0>(in, in_stride, out, out_stride, jobs, njobs, c, batch, s);
+  }
+  cuda_ok(cudaGetLastError(), "conv launch");
+  Runtime::get().note_launch();
+}
+
 // Key-switch `batch` polynomials d ([nl][N] each, NTT form, stride d_stride) with key
 // kk; out_w = ModDown(acc_w) + add_w  ([2][nl][N] per batch item, stride out_stride).
 void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, const Ctx::Key& kk, const uint64_t* add0,
@@ -702,122 +873,110 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   Runtime& rt = Runtime::get();
   cudaStream_t s = rt.stream();
   const KsPlan& P = ks_plan(c, level);
-  const uint32_t N = c.N, nl = P.nl, nx = P.nx, nd = P.nd, K = c.spec.K;
-  const size_t ext_stride = size_t(nd) * nx * N, acc_stride = size_t(2) * nx * N;
-  DevBuf dc = rt.alloc(size_t(batch) * nl * N);
+  const uint32_t N = c.N, logN = c.spec.logN, nl = P.nl, nx = P.nx, nd = P.nd;
+  const size_t dc_stride = size_t(nl) * N, ext_stride = size_t(nd) * nx * N, acc_stride = size_t(2) * nx * N,
+               cv_stride = size_t(2) * nl * N;
+  DevBuf dc = rt.alloc(size_t(batch) * dc_stride);
   DevBuf ext = rt.alloc(size_t(batch) * ext_stride);
   DevBuf acc = rt.alloc(size_t(batch) * acc_stride);
-  uint64_t* DC = reinterpret_cast<uint64_t*>(dc.get());
-  uint64_t* EXT = reinterpret_cast<uint64_t*>(ext.get());
-  uint64_t* ACC = reinterpret_cast<uint64_t*>(acc.get());
-  std::vector<uint32_t> qmap(nl);
-  for (uint32_t i = 0; i < nl; ++i) qmap[i] = i;
-  // d -> coefficient form
-  k_copy_rows<<<dim3(grid_of(size_t(nl) * N), 1, batch), kT, 0, s>>>(d, DC, nl, N, d_stride, size_t(nl) * N);
-  ntt(c, DC, qmap, batch, size_t(nl) * N, true);
-  // ModUp per digit: own rows copied (NTT form), new rows base-converted then NTT'd
-  for (uint32_t j = 0; j < nd; ++j) {
-    const uint32_t lo = j * c.alpha, hi = std::min(lo + c.alpha, nl);
-    uint64_t* Ej = EXT + size_t(j) * nx * N;
-    k_copy_rows<<<dim3(grid_of(size_t(hi - lo) * N), 1, batch), kT, 0, s>>>(d + size_t(lo) * N, Ej + size_t(lo) * N,
-                                                                          hi - lo, N, d_stride, ext_stride);
-    const ConvPlan& cp = P.up[j];
-    const uint32_t ntgt = nx - (hi - lo);
-    k_conv<<<dim3((N + kT - 1) / kT, std::min<uint32_t>(ntgt, 8), batch), kT, 0, s>>>(
-        DC, lo, Ej, reinterpret_cast<const Conv*>(cp.cv.get()), c.dpc(), reinterpret_cast<const uint64_t*>(cp.h.get()),
-        reinterpret_cast<const uint64_t*>(cp.h_sh.get()), N, size_t(nl) * N, ext_stride);
-    // NTT the converted rows: [0, lo) and [hi, nx) as two contiguous runs
-    if (lo > 0) {
-      std::vector<uint32_t> pm(P.ext_primes.begin(), P.ext_primes.begin() + lo);
-      ntt(c, Ej, pm, batch, ext_stride, false);
+  DevBuf conv = rt.alloc(size_t(batch) * cv_stride);
+  uint64_t* DC = dptr<uint64_t>(dc);
+  uint64_t* EXT = dptr<uint64_t>(ext);
+  uint64_t* ACC = dptr<uint64_t>(acc);
+  uint64_t* CV = dptr<uint64_t>(conv);
+  const auto qrows = iota_rows(nl);
+  // ModUp: d -> coefficient form (out of place), convert every digit, NTT the new rows
+  ntt_rows(c, d, d_stride, DC, dc_stride, qrows, qrows, qrows, batch, true);
+  const ConvJob* up = dptr<const ConvJob>(P.up_jobs);
+  launch_conv(c.alpha, DC, dc_stride, EXT, ext_stride, up, P.n_full, c, batch);
+  if (P.n_full < nd)
+    launch_conv(nl - P.n_full * c.alpha, DC, dc_stride, EXT, ext_stride, up + P.n_full, nd - P.n_full, c, batch);
+  ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
+  // inner product with the key (each key word read once per call)
+  {
+    const unsigned g = (unsigned)((size_t(nx) * N + kT - 1) / kT);
+    const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
+    switch (nd) {
+#define HS_INNER_CASE(D)                                                                                          \
+  case D:                                                                                                         \
+    k_ks_inner<D><<<g, kT, 0, s>>>(EXT, ext_stride, d, d_stride, ACC, acc_stride, KB, KA, c.dpc(), nx, nl, c.np, \
+                                   c.nq, c.alpha, logN, batch);                                                   \
+    break;
+      HS_INNER_CASE(1) HS_INNER_CASE(2) HS_INNER_CASE(3) HS_INNER_CASE(4) HS_INNER_CASE(5) HS_INNER_CASE(6)
+      HS_INNER_CASE(7) HS_INNER_CASE(8) HS_INNER_CASE(9) HS_INNER_CASE(10) HS_INNER_CASE(11) HS_INNER_CASE(12)
+      HS_INNER_CASE(13) HS_INNER_CASE(14) HS_INNER_CASE(15)
+#undef HS_INNER_CASE
+      default:
+        fail(HS_E_INVALID_ARG, "key switch: more than 15 digits");
     }
-    std::vector<uint32_t> pm2(P.ext_primes.begin() + hi, P.ext_primes.end());
-    ntt(c, Ej + size_t(hi) * N, pm2, batch, ext_stride, false);
   }
-  // inner product with the key
-  k_ks_inner<<<dim3(grid_of(size_t(nx) * N), 1, batch), kT, 0, s>>>(
-      EXT, ACC, reinterpret_cast<const uint64_t*>(kk.b.get()), reinterpret_cast<const uint64_t*>(kk.a.get()),
-      map_of(P.ext_primes), c.dpc(), nd, nx, c.np, N, ext_stride, acc_stride);
-  // ModDown: P rows -> coefficient form -> base-convert into Q_l -> NTT -> combine
-  DevBuf pc = rt.alloc(size_t(batch) * 2 * K * N);
-  DevBuf conv = rt.alloc(size_t(batch) * 2 * nl * N);
-  uint64_t* PC = reinterpret_cast<uint64_t*>(pc.get());
-  uint64_t* CV = reinterpret_cast<uint64_t*>(conv.get());
-  std::vector<uint32_t> pmap(K);
-  for (uint32_t k = 0; k < K; ++k) pmap[k] = c.nq + k;
-  for (uint32_t w = 0; w < 2; ++w) {
-    k_copy_rows<<<dim3(grid_of(size_t(K) * N), 1, batch), kT, 0, s>>>(ACC + size_t(w) * nx * N + size_t(nl) * N,
-                                                                     PC + size_t(w) * K * N, K, N, acc_stride,
-                                                                     size_t(2) * K * N);
-    ntt(c, PC + size_t(w) * K * N, pmap, batch, size_t(2) * K * N, true);
-    k_conv<<<dim3((N + kT - 1) / kT, std::min<uint32_t>(nl, 8), batch), kT, 0, s>>>(
-        PC + size_t(w) * K * N, 0, CV + size_t(w) * nl * N, reinterpret_cast<const Conv*>(P.down.cv.get()), c.dpc(),
-        reinterpret_cast<const uint64_t*>(P.down.h.get()), reinterpret_cast<const uint64_t*>(P.down.h_sh.get()), N,
-        size_t(2) * K * N, size_t(2) * nl * N);
-  }
-  ntt(c, CV, qmap, 2 * batch, size_t(nl) * N, false);  // both halves: 2*batch groups of nl rows
+  // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
+  ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);
+  launch_conv(c.spec.K, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), 2, c, batch);
+  ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv_rows, P.cv_rows, P.cv_primes, batch, false);
   k_moddown<<<dim3(grid_of(size_t(2) * nl * N), 1, batch), kT, 0, s>>>(
-      ACC, CV, add0, add1, out, c.dpc(), reinterpret_cast<const uint64_t*>(P.pinv.get()),
-      reinterpret_cast<const uint64_t*>(P.pinv_sh.get()), nl, nx, N, acc_stride, size_t(2) * nl * N, add_stride,
-      out_stride);
+      ACC, CV, add0, add1, out, c.dpc(), dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh), nl, nx, logN,
+      acc_stride, cv_stride, add_stride, out_stride);
   cuda_ok(cudaGetLastError(), "key switch");
-  rt.note_launch(6 + 4 * nd);
+  rt.note_launch(2);
 }
 
 }  // namespace
 
 void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_relin: level > L");
+  if (batch == 0) return;
   Runtime& rt = Runtime::get();
   const uint32_t N = c.N, nl = level + 1;
   const size_t ct = size_t(2) * nl * N, half = size_t(nl) * N;
   const Ctx::Key& key = c.relin_key();
   DevBuf d = rt.alloc(size_t(batch) * 3 * half);
-  uint64_t* D = reinterpret_cast<uint64_t*>(d.get());
+  uint64_t* D = dptr<uint64_t>(d);
   // layout per batch item: [d0 | d1 | d2], stride 3*half
-  k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, D + half, D + 2 * half, c.dpc(), nl, N, ct,
-                                                                 3 * half);
+  k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half);
   rt.note_launch();
   key_switch(c, level, D + 2 * half, 3 * half, key, D, D + half, 3 * half, out, ct, batch);
 }
 
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
+  if (batch == 0) return;
   Runtime& rt = Runtime::get();
   cudaStream_t s = rt.stream();
-  const uint32_t N = c.N, nl = level + 1;
+  const uint32_t N = c.N, logN = c.spec.logN, nl = level + 1;
   const size_t in_stride = size_t(2) * nl * N, out_stride = size_t(2) * level * N;
+  const KsPlan& P = ks_plan(c, level);
   DevBuf last = rt.alloc(size_t(batch) * 2 * N);
   DevBuf t = rt.alloc(size_t(batch) * out_stride);
-  uint64_t* LAST = reinterpret_cast<uint64_t*>(last.get());
-  uint64_t* T = reinterpret_cast<uint64_t*>(t.get());
-  for (uint32_t p = 0; p < 2; ++p)
-    k_copy_rows<<<dim3(grid_of(N), 1, batch), kT, 0, s>>>(in + (size_t(p) * nl + level) * N, LAST + size_t(p) * N, 1, N,
-                                                        in_stride, size_t(2) * N);
-  ntt(c, LAST, {level}, 2 * batch, N, true);
-  k_rescale_spread<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(LAST, T, c.dpc(), level, N, size_t(2) * N,
+  uint64_t* LAST = dptr<uint64_t>(last);
+  uint64_t* T = dptr<uint64_t>(t);
+  // last limb of both polys -> coefficient form (out of place)
+  ntt_rows(c, in, in_stride, LAST, size_t(2) * N, {level, nl + level}, {0, 1}, {level, level}, batch, true);
+  k_rescale_spread<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(LAST, T, c.dpc(), level, logN, size_t(2) * N,
                                                                      out_stride);
-  std::vector<uint32_t> qmap(level);
-  for (uint32_t i = 0; i < level; ++i) qmap[i] = i;
-  ntt(c, T, qmap, 2 * batch, size_t(level) * N, false);
-  const KsPlan& P = ks_plan(c, level);
-  const uint64_t* QI = reinterpret_cast<const uint64_t*>(P.qinv.get());
-  const uint64_t* QS = reinterpret_cast<const uint64_t*>(P.qinv_sh.get());
-  k_rescale_sub<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(in, T, out, c.dpc(), QI, QS, level, N, in_stride,
-                                                                  out_stride, out_stride);
+  std::vector<uint32_t> rows(2 * level), primes(2 * level);
+  for (uint32_t i = 0; i < 2 * level; ++i) {
+    rows[i] = i;
+    primes[i] = i % level;
+  }
+  ntt_rows(c, T, out_stride, T, out_stride, rows, rows, primes, batch, false);
+  k_rescale_sub<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(in, T, out, c.dpc(), dptr<const uint64_t>(P.qinv),
+                                                                  dptr<const uint64_t>(P.qinv_sh), level, logN,
+                                                                  in_stride, out_stride, out_stride);
   cuda_ok(cudaGetLastError(), "rescale");
-  rt.note_launch(5);
+  rt.note_launch(2);
 }
 
 void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rotate: level > L");
+  if (batch == 0) return;
   Runtime& rt = Runtime::get();
   const uint32_t N = c.N, nl = level + 1;
   const size_t ct = size_t(2) * nl * N;
   const uint64_t g = Ctx::galois_elt(k, c.spec.logN);
   const Ctx::Key& key = c.galois_key(g);
   DevBuf perm = rt.alloc(size_t(batch) * ct);
-  uint64_t* PM = reinterpret_cast<uint64_t*>(perm.get());
+  uint64_t* PM = dptr<uint64_t>(perm);
   k_automorph<<<dim3(grid_of(ct), 1, batch), kT, 0, rt.stream()>>>(PM, in, g, c.spec.logN, 2 * nl, ct);
   rt.note_launch();
   // out0 = sigma(c0) + ks0, out1 = ks1

@@ -43,6 +43,7 @@ struct PrimeC {
   uint64_t q;
   uint64_t mu;       // Barrett floor(2^(2k)/q)
   uint64_t m64;      // floor(2^64 / q) (reduce64)
+  uint64_t r64, r64_sh;  // 2^64 mod q and its Shoup constant (128-bit reduction)
   uint64_t ninv, ninv_sh;
   uint32_t k;        // bitlen(q)
   uint32_t pad;
@@ -82,6 +83,16 @@ __device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const PrimeC
   return r;
 }
 
+// x mod q for any x < 2^128: hi * (2^64 mod q) (Shoup) + lo (reduce64), one fold
+__device__ __forceinline__ uint64_t reduce128(u128 x, const PrimeC& p) {
+  const uint64_t hi = static_cast<uint64_t>(x >> 64), lo = static_cast<uint64_t>(x);
+  uint64_t r = mul_shoup_lazy(hi, p.r64, p.r64_sh, p.q);  // [0, 2q)
+  r += lo - __umul64hi(lo, p.m64) * p.q;                 // + [0, 2q)
+  const uint64_t q2 = 2 * p.q;
+  r = r >= q2 ? r - q2 : r;
+  return r >= p.q ? r - p.q : r;
+}
+
 // ---- host context -------------------------------------------------------------------
 class Ctx {
  public:
@@ -116,6 +127,11 @@ class Ctx {
 // groups of nlimbs limbs, group stride `gstride` words.  prime_of: host list.
 void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, uint32_t batch, size_t gstride,
          bool inverse);
+// Batched NTT over an explicit row list: row irows[i] of each input batch item
+// (stride in_stride words) -> row orows[i] of the output item, mod primes[i].
+void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
+              const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
+              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse);
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out);
 void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch);
