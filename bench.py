@@ -21,6 +21,14 @@ ciphertexts processed by all ranks.
 --impl reference runs the reference's own CPU implementation (oracle/_ref, the
 unmodified reference headers compiled here; else the oracle port) on all host
 cores on the same workload.
+
+tier_r (same JSON line): the north_star RNS-CKKS primitives at N=2^16, L=24,
+K=9, dnum=3 on a batch of 64 random ciphertexts under seeded keys (C5 shape):
+HMult+relin/s, HMult+relin+rescale, rotate, rescale, NTT, each as device time
+per ciphertext and as a fraction of the HBM roofline using BASELINE.md §4's
+algorithmic bytes; the RNS oracle (port, 1 core) is the CPU stand-in.
+`python bench.py --c5` prints the full C5 sweep (N in 2^14..2^16 x L in
+8/16/24/32), one JSON line per (N, L).
 """
 from __future__ import annotations
 
@@ -171,6 +179,162 @@ def run_reference(args):
     return 0
 
 
+# ---- Tier R (RNS-CKKS primitives) -----------------------------------------------------------------
+def hbm_peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 7700.0, "B200_PROFILING.md fallback (no MEASURED_PEAKS.json)"
+
+
+def rns_alg_bytes(logN, L, K, dnum, level):
+    """BASELINE.md §4 algorithmic bytes per ciphertext-op (u64 words)."""
+    N, l = 1 << logN, level
+    key = 2 * dnum * (l + 1 + K) * N * 8
+    return {
+        "ntt": 2 * 2 * (l + 1) * N * 8,  # both polynomials of one ciphertext, read + write
+        "mul_relin": 4 * (l + 1) * N * 8 + key + 2 * (l + 1) * N * 8,
+        "mul_relin_rescale": 4 * (l + 1) * N * 8 + key + 2 * l * N * 8,
+        "rotate": 2 * (l + 1) * N * 8 + key + 2 * (l + 1) * N * 8,
+        "rescale": 2 * (l + 1) * N * 8 + 2 * l * N * 8,
+    }
+
+
+def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None):
+    """Device time per ciphertext of each Tier-R op (CUDA-graph replay of `reps`
+    batched calls), inputs resident; returns {op: us_per_ct}, launches per op."""
+    from paper_2508_12093_b200 import _abi
+    from paper_2508_12093_b200 import hestat as H
+    from paper_2508_12093_b200.rns import DeviceBuffer, RnsContext, RnsSpec
+    spec = RnsSpec(logN, L, K, dnum, seed=1)
+    c = RnsContext(spec)
+    c.prepare_relin()
+    c.prepare_rotation(1)
+    W = spec.ct_words(L)
+    x, y, out = DeviceBuffer(batch * W), DeviceBuffer(batch * W), DeviceBuffer(batch * W)
+    for i in range(batch):
+        c.random_ct(L, 1 + i, x, i * W)
+        c.random_ct(L, 1000 + i, y, i * W)
+    H.sync()
+    fns = {
+        "ntt": lambda: c.ntt(x, 0, L + 1, batch=2 * batch),
+        "intt": lambda: c.ntt(x, 0, L + 1, batch=2 * batch, inverse=True),
+        "mul_relin": lambda: c.mul_relin(L, x, y, out, batch=batch),
+        "mul_relin_rescale": lambda: c.mul_relin_rescale(L, x, y, out, batch=batch),
+        "rescale": lambda: c.rescale(L, x, out, batch=batch),
+        "rotate": lambda: c.rotate(L, 1, x, out, batch=batch),
+    }
+    res, launches = {}, {}
+    for name, fn in fns.items():
+        if ops and name not in ops:
+            continue
+        fn()
+        H.sync()
+        l0 = H.kernel_launches()
+        with H.Graph() as g:
+            for _ in range(reps):
+                fn()
+        launches[name] = (H.kernel_launches() - l0) // reps
+        g.launch()
+        H.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.launch()
+        e1.record(stream)
+        e1.synchronize()
+        res[name] = 1e3 * e0.elapsed_time(e1) / (reps * batch)
+        del g
+    for b in (x, y, out):
+        b.free()
+    c.close()
+    H.sync()
+    return res, launches
+
+
+def rns_parity_small():
+    """Limb-exact check of the bench path at a small shape against the RNS oracle."""
+    from rns_abi import RnsOracle, Spec
+    from paper_2508_12093_b200.rns import DeviceBuffer, RnsContext, RnsSpec
+    s = Spec(logN=12, L=5, K=2, dnum=3, seed=9)
+    O = RnsOracle()
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed))
+    a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
+    da, db = DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)
+    ok = np.array_equal(c.mul_relin_rescale(s.L, da, db).download(), O.rescale(s, s.L, O.mul_relin(s, s.L, a, b)))
+    ok &= np.array_equal(c.rotate(s.L, 1, da).download(), O.rotate(s, s.L, 1, a))
+    c.close()
+    return bool(ok)
+
+
+def rns_cpu_baseline(logN, L, K, dnum):
+    """RNS oracle (plain C, 1 core) HMult+relin per ciphertext: (t(3 cts) - t(1 ct)) / 2,
+    so the once-per-call key generation drops out."""
+    from rns_abi import RnsOracle, Spec
+    O = RnsOracle()
+    s = Spec(logN=logN, L=L, K=K, dnum=dnum, seed=1)
+    a = np.concatenate([O.random_ct(s, L, 1 + i) for i in range(3)])
+    b = np.concatenate([O.random_ct(s, L, 100 + i) for i in range(3)])
+    W = 2 * (L + 1) * s.N
+    t0 = time.perf_counter()
+    O.mul_relin_many(s, L, a[:W], b[:W], 1)
+    t1 = time.perf_counter()
+    O.mul_relin_many(s, L, a, b, 3)
+    t3 = time.perf_counter() - t1
+    per = (t3 - (t1 - t0)) / 2
+    return {"value": 1.0 / per, "unit": "HMult+relin/s", "cores": 1, "kind": "port",
+            "sample": f"RNS oracle (oracle/rns_oracle.c), N=2^{logN} L={L} K={K} dnum={dnum}: "
+                      "3 HMult+relin minus 1 (key generation excluded), single thread",
+            "ms_per_op": 1e3 * per}
+
+
+def tier_r_section(torch, stream, batch=64, with_cpu=True):
+    logN, L, K, dnum = 16, 24, 9, 3
+    peak, src = hbm_peak_gbs()
+    us, launches = rns_measure(torch, stream, logN, L, K, dnum, batch)
+    ab = rns_alg_bytes(logN, L, K, dnum, L)
+    ab["intt"] = ab["ntt"]
+    ops = {}
+    for k, v in us.items():
+        gbs = ab[k] / (v * 1e-6) / 1e9
+        ops[k] = {"us_per_ct": round(v, 2), "ops_per_s": round(1e6 / v, 1), "alg_bytes": ab[k],
+                  "achieved_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4), "launches": launches[k]}
+    sec = {"metric": "HMult+relin/s", "value": round(1e6 / us["mul_relin"], 1), "unit": "HMult+relin/s",
+           "config": {"workload": "C5 tier R: batch of 64 random ciphertexts under seeded keys",
+                      "logN": logN, "L": L, "K": K, "dnum": dnum, "level": L, "batch": batch,
+                      "word": "u64", "l2": "inputs > L2 (64 x 25.6 MiB per operand)"},
+           "ops": ops,
+           "roofline": {"bound": "hbm", "kernel": "HMult+relin (whole op, BASELINE.md §4 bytes)",
+                        "achieved": ops["mul_relin"]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                        "frac": ops["mul_relin"]["hbm_frac"], "traffic": None, "peak_source": src,
+                        "note": "integer-pipe bound (ncu: ALU pipe ~60% in the NTT), not HBM bound"},
+           "parity_vs_oracle": rns_parity_small()}
+    if with_cpu:
+        sec["cpu_baseline"] = rns_cpu_baseline(logN, L, K, dnum)
+    return sec
+
+
+def c5_sweep(args):
+    import torch
+    torch.cuda.set_device(0)
+    from paper_2508_12093_b200 import hestat as H
+    H.init(0)
+    stream = torch.cuda.ExternalStream(H.stream_handle())
+    peak, src = hbm_peak_gbs()
+    for logN in (14, 15, 16):
+        for L in (8, 16, 24, 32):
+            dnum = 3
+            K = (L + 1 + dnum - 1) // dnum
+            us, launches = rns_measure(torch, stream, logN, L, K, dnum, args.batch)
+            ab = rns_alg_bytes(logN, L, K, dnum, L)
+            ab["intt"] = ab["ntt"]
+            line = {"sweep": "C5 tier R", "logN": logN, "L": L, "K": K, "dnum": dnum, "batch": args.batch,
+                    "peak_gbs": peak, "ops": {k: {"us_per_ct": round(v, 2), "ops_per_s": round(1e6 / v, 1),
+                                                  "hbm_frac": round(ab[k] / (v * 1e-6) / 1e9 / peak, 4)}
+                                              for k, v in us.items()}}
+            print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---- GPU leg ---------------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -179,8 +343,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tier-r", action="store_true")
+    ap.add_argument("--c5", action="store_true", help="print the C5 tier-R sweep instead")
+    ap.add_argument("--batch", type=int, default=64)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.c5:
+        return c5_sweep(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -336,6 +505,8 @@ def main():
                            "note": "graph replay per call, includes ~1-2 us node overhead"},
             "clocks": clk.summary(),
         }
+        if not args.no_tier_r:
+            line["tier_r"] = tier_r_section(torch, stream, args.batch, with_cpu=not args.no_cpu_baseline and ws == 1)
         if not args.no_cpu_baseline and ws == 1:
             cb, cout = cpu_baseline(x)
             cb["parity_vs_gpu"] = bool(np.array_equal(bits(cout), bits(z)))

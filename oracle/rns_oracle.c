@@ -418,10 +418,12 @@ static size_t key_words(const ctx_t* c) {
   return (size_t)c->s.dnum * (c->s.L + 1 + c->s.K) * ((size_t)1 << c->s.logN);
 }
 
-void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+void rnso_mul_relin_many(const rns_spec* s, uint32_t level, uint32_t count, const uint64_t* a, const uint64_t* b,
+                         uint64_t* out) {
   ctx_t c;
   ctx_init(&c, s);
   const uint32_t N = 1u << s->logN, nl = level + 1, np = s->L + 1 + s->K;
+  const size_t ct = (size_t)2 * nl * N;
   uint64_t* sk = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
   uint64_t* s2 = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
   secret_ntt(&c, sk);
@@ -432,26 +434,28 @@ void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const 
   uint64_t* ka = (uint64_t*)malloc(key_words(&c) * sizeof(uint64_t));
   make_key(&c, 0, sk, s2, kb, ka);
   uint64_t* d2 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
-  const uint64_t *a0 = a, *a1 = a + (size_t)nl * N, *b0 = b, *b1 = b + (size_t)nl * N;
-  uint64_t *o0 = out, *o1 = out + (size_t)nl * N;
-  for (uint32_t i = 0; i < nl; ++i) {
-    const uint64_t q = c.primes[i];
-    for (uint32_t n = 0; n < N; ++n) {
-      const size_t x = (size_t)i * N + n;
-      o0[x] = mulmod(a0[x], b0[x], q);
-      o1[x] = addmod(mulmod(a0[x], b1[x], q), mulmod(a1[x], b0[x], q), q);
-      d2[x] = mulmod(a1[x], b1[x], q);
-    }
-  }
   uint64_t* k0 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
   uint64_t* k1 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
-  key_switch(&c, level, d2, kb, ka, k0, k1);
-  for (uint32_t i = 0; i < nl; ++i)
-    for (uint32_t n = 0; n < N; ++n) {
-      const size_t x = (size_t)i * N + n;
-      o0[x] = addmod(o0[x], k0[x], c.primes[i]);
-      o1[x] = addmod(o1[x], k1[x], c.primes[i]);
+  for (uint32_t m = 0; m < count; ++m) {
+    const uint64_t *a0 = a + m * ct, *a1 = a0 + (size_t)nl * N, *b0 = b + m * ct, *b1 = b0 + (size_t)nl * N;
+    uint64_t *o0 = out + m * ct, *o1 = o0 + (size_t)nl * N;
+    for (uint32_t i = 0; i < nl; ++i) {
+      const uint64_t q = c.primes[i];
+      for (uint32_t n = 0; n < N; ++n) {
+        const size_t x = (size_t)i * N + n;
+        o0[x] = mulmod(a0[x], b0[x], q);
+        o1[x] = addmod(mulmod(a0[x], b1[x], q), mulmod(a1[x], b0[x], q), q);
+        d2[x] = mulmod(a1[x], b1[x], q);
+      }
     }
+    key_switch(&c, level, d2, kb, ka, k0, k1);
+    for (uint32_t i = 0; i < nl; ++i)
+      for (uint32_t n = 0; n < N; ++n) {
+        const size_t x = (size_t)i * N + n;
+        o0[x] = addmod(o0[x], k0[x], c.primes[i]);
+        o1[x] = addmod(o1[x], k1[x], c.primes[i]);
+      }
+  }
   free(sk);
   free(s2);
   free(kb);
@@ -460,6 +464,10 @@ void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const 
   free(k0);
   free(k1);
   ctx_free(&c);
+}
+
+void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  rnso_mul_relin_many(s, level, 1, a, b, out);
 }
 
 void rnso_rescale(const rns_spec* s, uint32_t level, const uint64_t* in, uint64_t* out) {

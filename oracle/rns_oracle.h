@@ -46,6 +46,9 @@ void rnso_random_ct(const rns_spec* s, uint32_t level, uint64_t tag, uint64_t* c
 
 /* HMult + relinearisation (no rescale): a, b, out are [2][level+1][N] in NTT form */
 void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out);
+/* the same for `count` consecutive ciphertext pairs, key generated once (CPU baseline timing) */
+void rnso_mul_relin_many(const rns_spec* s, uint32_t level, uint32_t count, const uint64_t* a, const uint64_t* b,
+                         uint64_t* out);
 /* rescale by q_level: in [2][level+1][N] -> out [2][level][N], NTT form */
 void rnso_rescale(const rns_spec* s, uint32_t level, const uint64_t* in, uint64_t* out);
 /* rotation by k slots (Galois element 5^k mod 2N) + key switch, NTT form */

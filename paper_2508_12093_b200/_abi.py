@@ -139,6 +139,7 @@ _SIGS.update({
     "hs_rns_random_ct": (C.c_int, [RNS, C.c_uint32, C.c_uint64, C.c_void_p]),
     "hs_rns_ntt": (C.c_int, [RNS, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
     "hs_rns_mul_relin": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_mul_relin_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_rotate": (C.c_int, [RNS, C.c_uint32, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32]),
 })

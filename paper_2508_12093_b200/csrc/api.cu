@@ -776,6 +776,16 @@ int hs_rns_mul_relin(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint6
   });
 }
 
+int hs_rns_mul_relin_rescale(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                             uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    rns::mul_relin_rescale(rctx(ctx), level, a, b, out, batch);
+  });
+}
+
 int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch) {
   return guard([&] {
     need(in, "in");

@@ -938,6 +938,14 @@ void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uin
   key_switch(c, level, D + 2 * half, 3 * half, key, D, D + half, 3 * half, out, ct, batch);
 }
 
+void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
+  if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_relin_rescale: level must be in [1, L]");
+  if (batch == 0) return;
+  DevBuf t = Runtime::get().alloc(size_t(batch) * 2 * (level + 1) * c.N);
+  mul_relin(c, level, a, b, dptr<uint64_t>(t), batch);
+  rescale(c, level, dptr<const uint64_t>(t), out, batch);
+}
+
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
   if (batch == 0) return;

@@ -135,6 +135,8 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out);
 void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch);
+// HMult + relinearisation + rescale (out at level - 1): the composition of the two ops.
+void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
 // Build (and upload) the per-level key-switching / rescale constants ahead of time,
 // so that ops can be captured into a CUDA graph.

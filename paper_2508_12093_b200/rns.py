@@ -125,6 +125,12 @@ class RnsContext:
         _check(_abi.lib().hs_rns_mul_relin(self.h, level, a.ptr, b.ptr, out.ptr, batch))
         return out
 
+    def mul_relin_rescale(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
+                          batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        _check(_abi.lib().hs_rns_mul_relin_rescale(self.h, level, a.ptr, b.ptr, out.ptr, batch))
+        return out
+
     def rescale(self, level: int, a: DeviceBuffer, out: DeviceBuffer | None = None, batch: int = 1) -> DeviceBuffer:
         out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
         _check(_abi.lib().hs_rns_rescale(self.h, level, a.ptr, out.ptr, batch))

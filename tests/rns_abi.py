@@ -70,6 +70,11 @@ class RnsOracle:
         self.lib.rnso_mul_relin(C.byref(s.c()), C.c_uint32(level), _u(a), _u(b), _u(out))
         return out
 
+    def mul_relin_many(self, s: Spec, level: int, a: np.ndarray, b: np.ndarray, count: int) -> np.ndarray:
+        out = np.zeros(count * 2 * (level + 1) * s.N, dtype=np.uint64)
+        self.lib.rnso_mul_relin_many(C.byref(s.c()), C.c_uint32(level), C.c_uint32(count), _u(a), _u(b), _u(out))
+        return out
+
     def rescale(self, s: Spec, level: int, a: np.ndarray) -> np.ndarray:
         out = np.zeros(2 * level * s.N, dtype=np.uint64)
         self.lib.rnso_rescale(C.byref(s.c()), C.c_uint32(level), _u(a), _u(out))

@@ -108,6 +108,15 @@ def test_mul_relin_matches_oracle(s):
 
 
 @pytest.mark.parametrize("s", SHAPES, ids=str)
+def test_mul_relin_rescale_matches_oracle(s):
+    c = ctx(s)
+    level = s.L
+    a, b = O.random_ct(s, level, 23), O.random_ct(s, level, 24)
+    got = c.mul_relin_rescale(level, _buf(a), _buf(b)).download()
+    assert np.array_equal(got, O.rescale(s, level, O.mul_relin(s, level, a, b)))
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=str)
 def test_rescale_matches_oracle(s):
     c = ctx(s)
     for level in sorted({s.L, 1}):
@@ -138,6 +147,7 @@ def test_batched_ops_equal_single():
     r = c.rescale(level, da, batch=B).download()
     rot = c.rotate(level, 3, da, batch=B).download()
     Wr = s.N * 2 * level
+    assert np.array_equal(m, O.mul_relin_many(s, level, a, b, B))
     for i in range(B):
         ai, bi = a[i * W:(i + 1) * W], b[i * W:(i + 1) * W]
         assert np.array_equal(m[i * W:(i + 1) * W], O.mul_relin(s, level, ai, bi))
