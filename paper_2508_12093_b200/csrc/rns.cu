@@ -62,13 +62,16 @@ struct RowMap {
 // S = 1 (columns) or R1 + g (rows), so one device routine serves both passes.
 // Each thread runs radix-2^RB groups (RB <= 3 stages) in registers; the first
 // group step reads HBM directly, the last writes HBM directly, the ones between
-// exchange through shared memory (row tiles padded one word in eight so that the
-// short-stride steps are bank-conflict free).
+// exchange through shared memory (row tiles XOR-swizzled, see swz()).
 constexpr int kNT = 512;           // threads per NTT block
 constexpr uint32_t kLogTile = 12;  // 4096 elements per NTT block
 constexpr uint32_t kNTile = 1u << kLogTile;
 
-__device__ __forceinline__ uint32_t spad(uint32_t u) { return u + (u >> 3); }
+// Row-tile shared-memory swizzle: a bijection inside aligned 16-word groups that
+// makes every store/load pattern of every radix step (logN 10..17, forward and
+// inverse) hit 16 distinct 8-byte bank slots per half-warp (exhaustively checked
+// offline against the step access patterns below).
+__device__ __forceinline__ uint32_t swz(uint32_t u) { return u ^ (((u >> 2) ^ (u >> 3)) & 15u); }
 
 template <int LOGN, bool ROWS>
 struct NttGeom {
@@ -113,7 +116,7 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint6
       if (FIRST)
         x[k] = ROWS ? gin[(size_t(tr) << logC) + e] : gin[(size_t(e) << logC) + tr];
       else
-        x[k] = ROWS ? sm[spad((tr << logR) + e)] : sm[(e << logTPB) + tr];
+        x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
     }
     if (!INV) {
 #pragma unroll
@@ -171,7 +174,7 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint6
           gout[(size_t(e) << logC) + tr] = v;
       } else {
         if (ROWS)
-          sm[spad((tr << logR) + e)] = v;
+          sm[swz((tr << logR) + e)] = v;
         else
           sm[(e << logTPB) + tr] = v;
       }
@@ -196,15 +199,156 @@ __device__ __forceinline__ void ntt_steps(const uint64_t* gin, uint64_t* gout, u
   }
 }
 
+// ---- FP64 path for primes below 2^42 (the 40-bit q_i) ------------------------------
+// Residues are carried as exact integers in fp64 registers.  A twiddle product
+// y*w mod q is hi = fl(y w), lo = fma(y, w, -hi) (exact), k = rint(hi / q) (magic
+// constant), r = fma(-k, q, hi) + lo: every step is exact because all values are
+// integers below 2^53, and |r| < 1.1 q.  Forward (Cooley-Tukey) outputs X +- T grow
+// by at most 1.1 q per stage (< 19 q after 16 stages), so no reduction is needed
+// inside a pass; inverse (Gentleman-Sande) sums double per stage and are folded
+// back below 0.6 q after every radix step.  Pass outputs are canonical u64.  The
+// arithmetic runs on the FP64 pipe, leaving the integer ALU (the bottleneck of the
+// 64-bit Shoup path) to addressing.  Results are identical: the NTT of canonical
+// input is a unique canonical vector.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: fl(x + M) - M = rint(x), |x| < 2^51
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double u2d(uint64_t v) {  // exact for v < 2^52
+  return __dadd_rn(__longlong_as_double(static_cast<long long>(v | 0x4330000000000000ULL)), -kTwo52);
+}
+__device__ __forceinline__ uint64_t d2u(double r) {  // r integer in [0, 2^52)
+  return static_cast<uint64_t>(__double_as_longlong(__dadd_rn(r, kTwo52))) & 0xFFFFFFFFFFFFFULL;
+}
+__device__ __forceinline__ double fp_mulmod(double y, double w, double q, double qinv) {
+  const double hi = __dmul_rn(y, w);
+  const double lo = __fma_rn(y, w, -hi);
+  const double k = __dadd_rn(__fma_rn(hi, qinv, kMagic), -kMagic);
+  return __dadd_rn(__fma_rn(-k, q, hi), lo);
+}
+__device__ __forceinline__ double fp_fold(double x, double q, double qinv) {  // -> |r| < 0.6 q
+  const double k = __dadd_rn(__fma_rn(x, qinv, kMagic), -kMagic);
+  return __fma_rn(-k, q, x);
+}
+__device__ __forceinline__ uint64_t fp_canon(double x, double q, double qinv) {
+  double r = fp_fold(x, q, qinv);
+  r = r < 0.0 ? __dadd_rn(r, q) : r;
+  return d2u(r);
+}
+
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST>
+__device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, uint64_t* __restrict__ gout,
+                                            double* __restrict__ sm, const double* __restrict__ tw, double q,
+                                            double qinv, uint32_t tile0, double ninv) {
+  using G = NttGeom<LOGN, ROWS>;
+  constexpr uint32_t logR = G::logR, logTPB = G::logTPB, logC = G::logC;
+  constexpr uint32_t logG = logR - RB;
+  constexpr uint32_t total = 1u << (logG + logTPB);
+  constexpr uint32_t logs = INV ? DONE : logR - 1 - DONE - (RB - 1);
+#pragma unroll
+  for (uint32_t it = 0; it < (total + kNT - 1) / kNT; ++it) {
+    const uint32_t idx = threadIdx.x + it * kNT;
+    if (total % kNT != 0 && idx >= total) break;
+    uint32_t tr, g;
+    if (ROWS) {
+      g = idx & ((1u << logG) - 1);
+      tr = idx >> logG;
+    } else {
+      tr = idx & ((1u << logTPB) - 1);
+      g = idx >> logTPB;
+    }
+    const uint32_t blk0 = g >> logs;
+    const uint32_t j0 = (blk0 << (logs + RB)) | (g & ((1u << logs) - 1));
+    const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
+    double x[1 << RB];
+#pragma unroll
+    for (int k = 0; k < (1 << RB); ++k) {
+      const uint32_t e = j0 + (uint32_t(k) << logs);
+      if (FIRST)
+        x[k] = u2d(ROWS ? gin[(size_t(tr) << logC) + e] : gin[(size_t(e) << logC) + tr]);
+      else
+        x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
+    }
+    if (!INV) {
+#pragma unroll
+      for (int st = 0; st < RB; ++st) {
+        const int d = 1 << (RB - 1 - st);
+#pragma unroll
+        for (int b = 0; b < (1 << st); ++b) {
+          const double w = __ldg(tw + ((1u << (DONE + st)) * S) + (blk0 << st) + b);
+#pragma unroll
+          for (int o = 0; o < d; ++o) {
+            const int k0 = b * 2 * d + o;
+            const double T = fp_mulmod(x[k0 + d], w, q, qinv);
+            const double X = x[k0];
+            x[k0] = __dadd_rn(X, T);
+            x[k0 + d] = __dadd_rn(X, -T);
+          }
+        }
+      }
+    } else {
+      constexpr uint32_t logh0 = logR - 1 - DONE;
+#pragma unroll
+      for (int st = 0; st < RB; ++st) {
+        const int d = 1 << st;
+#pragma unroll
+        for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
+          const double w = __ldg(tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b);
+#pragma unroll
+          for (int o = 0; o < d; ++o) {
+            const int k0 = b * 2 * d + o;
+            const double X = x[k0], Y = x[k0 + d];
+            x[k0] = __dadd_rn(X, Y);
+            x[k0 + d] = fp_mulmod(__dadd_rn(X, -Y), w, q, qinv);
+          }
+        }
+      }
+      if (!LAST) {
+#pragma unroll
+        for (int k = 0; k < (1 << RB); ++k) x[k] = fp_fold(x[k], q, qinv);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << RB); ++k) {
+      const uint32_t e = j0 + (uint32_t(k) << logs);
+      if (LAST) {
+        const double v = (INV && !ROWS) ? fp_mulmod(x[k], ninv, q, qinv) : x[k];
+        const uint64_t u = fp_canon(v, q, qinv);
+        if (ROWS)
+          gout[(size_t(tr) << logC) + e] = u;
+        else
+          gout[(size_t(e) << logC) + tr] = u;
+      } else {
+        if (ROWS)
+          sm[swz((tr << logR) + e)] = x[k];
+        else
+          sm[(e << logTPB) + tr] = x[k];
+      }
+    }
+  }
+}
+
+template <bool INV, bool ROWS, int LOGN, int DONE>
+__device__ __forceinline__ void ntt_steps_fp(const uint64_t* gin, uint64_t* gout, double* sm, const double* tw,
+                                             double q, double qinv, uint32_t tile0, double ninv) {
+  constexpr int logR = NttGeom<LOGN, ROWS>::logR;
+  if constexpr (DONE < logR) {
+    constexpr int rem = logR - DONE;
+    constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
+    if constexpr (DONE > 0) __syncthreads();
+    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR>(gin, gout, sm, tw, q, qinv, tile0, ninv);
+    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB>(gin, gout, sm, tw, q, qinv, tile0, ninv);
+  }
+}
+
 // Forward: columns then rows; inverse: rows then columns.  Reads `in`, writes
 // `out` (may alias: every block reads its whole tile before its last step writes).
 // 3 blocks of 512 threads per SM (40 registers): measured 1.3x over 2 blocks.
 template <bool INV, bool ROWS, int LOGN>
 __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                   size_t out_stride, const __grid_constant__ RowMap rm,
-                                                  const PrimeC* pcs, const uint64_t* tw) {
+                                                  const PrimeC* pcs, const uint64_t* tw, const double* twd) {
   using G = NttGeom<LOGN, ROWS>;
-  __shared__ uint64_t sm[kNTile + kNTile / 8];
+  __shared__ uint64_t sm[kNTile];
   constexpr uint32_t N = 1u << LOGN;
   const uint32_t pi = rm.prime[blockIdx.y];
   const PrimeC& P = pcs[pi];
@@ -214,22 +358,26 @@ __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t 
   const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
   const uint64_t* gi = in + blockIdx.z * in_stride + (size_t(rm.irow[blockIdx.y]) << LOGN) + toff;
   uint64_t* go = out + blockIdx.z * out_stride + (size_t(rm.orow[blockIdx.y]) << LOGN) + toff;
-  ntt_steps<INV, ROWS, LOGN, 0>(gi, go, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+  if (P.fp)
+    ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, go, reinterpret_cast<double*>(sm), twd + size_t(pi) * 2 * N + (INV ? N : 0),
+                                     P.qd, P.qinvd, tile0, static_cast<double>(P.ninv));
+  else
+    ntt_steps<INV, ROWS, LOGN, 0>(gi, go, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
 }
 
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
-                cudaStream_t s) {
+                const double* twd, cudaStream_t s) {
   using Gc = NttGeom<LOGN, false>;
   using Gr = NttGeom<LOGN, true>;
   const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch), gr(1u << (Gr::logR1 - Gr::logTPB), n, batch);
   if (!inverse) {
-    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw);
-    k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw);
+    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd);
+    k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd);
   } else {
-    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw);
-    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw);
+    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd);
+    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd);
   }
 }
 
@@ -551,6 +699,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
   cudaStream_t s = rt.stream();
   const uint32_t logN = c.spec.logN;
   const uint64_t* tw = dptr<const uint64_t>(c.d_tw);
+  const double* twd = dptr<const double>(c.d_twd);
   for (size_t base = 0; base < irows.size(); base += kMaxRows) {
     const uint32_t n = static_cast<uint32_t>(std::min<size_t>(kMaxRows, irows.size() - base));
     RowMap rm{}, rm2{};
@@ -562,7 +711,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
     switch (logN) {
 #define HS_NTT_CASE(L) \
   case L:              \
-    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, s); \
+    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s); \
     break;
       HS_NTT_CASE(9) HS_NTT_CASE(10) HS_NTT_CASE(11) HS_NTT_CASE(12) HS_NTT_CASE(13) HS_NTT_CASE(14)
       HS_NTT_CASE(15) HS_NTT_CASE(16) HS_NTT_CASE(17)
@@ -619,6 +768,7 @@ Ctx::Ctx(const Spec& s) : spec(s) {
   }
   // per-prime constants and twiddle tables
   std::vector<uint64_t> tw(size_t(np) * 4 * N);
+  std::vector<double> twd(size_t(np) * 2 * N);
   for (uint32_t i = 0; i < np; ++i) {
     const uint64_t q = primes[i];
     PrimeC p{};
@@ -630,6 +780,9 @@ Ctx::Ctx(const Spec& s) : spec(s) {
     p.r64_sh = shoup_of(p.r64, q);
     p.ninv = h_inv(N % q, q);
     p.ninv_sh = shoup_of(p.ninv, q);
+    p.fp = q < (1ULL << 42) ? 1u : 0u;
+    p.qd = static_cast<double>(q);
+    p.qinvd = 1.0 / static_cast<double>(q);
     pc.push_back(p);
     uint64_t psi = 0;
     for (uint64_t x = 2;; ++x) {
@@ -644,10 +797,13 @@ Ctx::Ctx(const Spec& s) : spec(s) {
       t[N + k] = shoup_of(t[k], q);
       t[2 * N + k] = h_pow(ipsi, r, q);
       t[3 * N + k] = shoup_of(t[2 * N + k], q);
+      twd[size_t(i) * 2 * N + k] = static_cast<double>(t[k]);
+      twd[size_t(i) * 2 * N + N + k] = static_cast<double>(t[2 * N + k]);
     }
   }
   d_pc = upload(pc);
   d_tw = upload(tw);
+  d_twd = upload(twd);
   // secret key (NTT form over every prime)
   Runtime& rt = Runtime::get();
   d_sk = rt.alloc(size_t(np) * N);
