@@ -53,11 +53,30 @@ int hs_rns_prepare_relin(hs_rns* ctx);
 int hs_rns_prepare_rotation(hs_rns* ctx, int64_t k);
 int hs_rns_secret(hs_rns* ctx, uint64_t* dev_out); /* [L+1+K][N] NTT form (tests) */
 
+/* CKKS encoding (host, canonical embedding; slot j <-> zeta^(5^j), so hs_rns_rotate
+ * by k is a left rotation of the slots by k, ckks.hpp:193-202):
+ * n <= N/2 real values -> N coefficients round(scale * m_k), and back. */
+int hs_rns_encode(uint32_t logN, const double* z, uint64_t n, double scale, int64_t* coeffs);
+int hs_rns_decode(uint32_t logN, const int64_t* coeffs, double scale, double* z, uint64_t n);
+/* symmetric RLWE encryption at `level` (seeded by spec.seed and tag) of host
+ * coefficients / of slot values; decryption through q_0 (|scale * value| < q_0/2) */
+int hs_rns_encrypt_coeffs(hs_rns* ctx, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* dev_out);
+int hs_rns_encrypt(hs_rns* ctx, uint32_t level, const double* z, uint64_t n, double scale, uint64_t tag,
+                   uint64_t* dev_out);
+int hs_rns_decrypt_coeffs(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, int64_t* coeffs);
+int hs_rns_decrypt(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, double scale, double* z, uint64_t n);
+
 /* ops; `batch` ciphertexts per call, consecutive in memory */
 int hs_rns_random_ct(hs_rns* ctx, uint32_t level, uint64_t tag, uint64_t* dev_out);
 /* in-place NTT (inverse != 0: iNTT) of `batch` groups of `nlimbs` limbs, limb i
  * of each group taken mod prime first_prime + i, groups `nlimbs*N` words apart */
 int hs_rns_ntt(hs_rns* ctx, uint64_t* dev, uint32_t first_prime, uint32_t nlimbs, uint32_t batch, int inverse);
+/* limb-wise ops (ckks.hpp add_ct/sub_ct :113-133; add_pt :137 with c = round(value * scale);
+ * integer constant multiply, rescale separately for mul_pt :168) */
+int hs_rns_add(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
+int hs_rns_sub(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
+int hs_rns_add_const(hs_rns* ctx, uint32_t level, const uint64_t* a, int64_t c, uint64_t* out, uint32_t batch);
+int hs_rns_mul_const(hs_rns* ctx, uint32_t level, const uint64_t* a, int64_t c, uint64_t* out, uint32_t batch);
 int hs_rns_mul_relin(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out,
                      uint32_t batch);
 /* HMult + relin + rescale: out at level-1 ([2][level][N] per ciphertext) */

@@ -85,7 +85,7 @@ uint64_t rnso_hash(uint64_t seed, uint64_t domain, uint64_t a, uint64_t b) {
   return z ^ (z >> 31);
 }
 
-enum { D_SECRET = 1, D_KEY_A = 2, D_KEY_E = 3, D_CT = 4 };
+enum { D_SECRET = 1, D_KEY_A = 2, D_KEY_E = 3, D_CT = 4, D_ENC_A = 5, D_ENC_E = 6 };
 
 /* --------------------------------------------------------------------- primes */
 int rnso_primes(const rns_spec* s, uint64_t* out) {
@@ -529,5 +529,45 @@ void rnso_rotate(const rns_spec* s, uint32_t level, int64_t k, const uint64_t* i
   free(ka);
   free(c0);
   free(c1);
+  ctx_free(&c);
+}
+
+/* ------------------------------------------------------------ encryption */
+/* symmetric RLWE: c1 = a (uniform, NTT form), c0 = NTT(m + e) - a s */
+void rnso_encrypt_coeffs(const rns_spec* s, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* ct) {
+  ctx_t c;
+  ctx_init(&c, s);
+  const uint32_t N = 1u << s->logN, nl = level + 1, np = s->L + 1 + s->K;
+  uint64_t* sk = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
+  secret_ntt(&c, sk);
+  for (uint32_t i = 0; i < nl; ++i) {
+    const uint64_t q = c.primes[i];
+    uint64_t* c0 = ct + (size_t)i * N;
+    uint64_t* c1 = ct + ((size_t)nl + i) * N;
+    for (uint32_t n = 0; n < N; ++n) {
+      c0[n] = lift(coeffs[n] + cbd(rnso_hash(s->seed, D_ENC_E, tag, n)), q);
+      c1[n] = uniform(rnso_hash(s->seed, D_ENC_A, tag * 64 + i, n), q);
+    }
+    ntt_fwd(&c, i, c0);
+    for (uint32_t n = 0; n < N; ++n) c0[n] = submod(c0[n], mulmod(c1[n], sk[(size_t)i * N + n], q), q);
+  }
+  free(sk);
+  ctx_free(&c);
+}
+
+/* m = c0 + c1 s on limb 0, centred mod q_0 */
+void rnso_decrypt_coeffs(const rns_spec* s, uint32_t level, const uint64_t* ct, int64_t* coeffs) {
+  ctx_t c;
+  ctx_init(&c, s);
+  const uint32_t N = 1u << s->logN, nl = level + 1, np = s->L + 1 + s->K;
+  uint64_t* sk = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
+  uint64_t* m = (uint64_t*)malloc((size_t)N * sizeof(uint64_t));
+  secret_ntt(&c, sk);
+  const uint64_t q = c.primes[0];
+  for (uint32_t n = 0; n < N; ++n) m[n] = addmod(ct[n], mulmod(ct[(size_t)nl * N + n], sk[n], q), q);
+  ntt_inv(&c, 0, m);
+  for (uint32_t n = 0; n < N; ++n) coeffs[n] = m[n] > q / 2 ? -(int64_t)(q - m[n]) : (int64_t)m[n];
+  free(sk);
+  free(m);
   ctx_free(&c);
 }

@@ -53,6 +53,11 @@ void rnso_mul_relin_many(const rns_spec* s, uint32_t level, uint32_t count, cons
 void rnso_rescale(const rns_spec* s, uint32_t level, const uint64_t* in, uint64_t* out);
 /* rotation by k slots (Galois element 5^k mod 2N) + key switch, NTT form */
 void rnso_rotate(const rns_spec* s, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out);
+/* symmetric RLWE encryption of N integer coefficients at `level`: c1 = a (uniform,
+ * NTT form, stream D_ENC_A/tag), c0 = NTT(m + e) - a s (e: CBD, stream D_ENC_E/tag) */
+void rnso_encrypt_coeffs(const rns_spec* s, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* ct);
+/* decryption on q_0: centred c0 + c1 s (coefficient form) */
+void rnso_decrypt_coeffs(const rns_spec* s, uint32_t level, const uint64_t* ct, int64_t* coeffs);
 /* secret key (ternary) as residues over all L+1+K primes, NTT form: [L+1+K][N] */
 void rnso_secret(const rns_spec* s, uint64_t* sk);
 

@@ -137,6 +137,16 @@ _SIGS.update({
     "hs_rns_prepare_rotation": (C.c_int, [RNS, C.c_int64]),
     "hs_rns_secret": (C.c_int, [RNS, C.c_void_p]),
     "hs_rns_random_ct": (C.c_int, [RNS, C.c_uint32, C.c_uint64, C.c_void_p]),
+    "hs_rns_encode": (C.c_int, [C.c_uint32, DP, C.c_uint64, C.c_double, C.POINTER(C.c_int64)]),
+    "hs_rns_decode": (C.c_int, [C.c_uint32, C.POINTER(C.c_int64), C.c_double, DP, C.c_uint64]),
+    "hs_rns_add": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_sub": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_add_const": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32]),
+    "hs_rns_mul_const": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32]),
+    "hs_rns_encrypt_coeffs": (C.c_int, [RNS, C.c_uint32, C.POINTER(C.c_int64), C.c_uint64, C.c_void_p]),
+    "hs_rns_encrypt": (C.c_int, [RNS, C.c_uint32, DP, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p]),
+    "hs_rns_decrypt_coeffs": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.POINTER(C.c_int64)]),
+    "hs_rns_decrypt": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_double, DP, C.c_uint64]),
     "hs_rns_ntt": (C.c_int, [RNS, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
     "hs_rns_mul_relin": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_mul_relin_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),

@@ -10,6 +10,7 @@
 #include "core.h"
 #include "pipelines.h"
 #include "rns.h"
+#include "rns_codec.h"
 #include "series.h"
 #include "hestat_rns.h"
 
@@ -755,6 +756,65 @@ int hs_rns_random_ct(hs_rns* ctx, uint32_t level, uint64_t tag, uint64_t* dev_ou
   });
 }
 
+int hs_rns_encode(uint32_t logN, const double* z, uint64_t n, double scale, int64_t* coeffs) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    if (logN < 2 || logN > 17) fail(HS_E_INVALID_ARG, "hs_rns_encode: logN out of range");
+    if (n && !z) fail(HS_E_INVALID_ARG, "null values");
+    if (n > (1u << logN) / 2) fail(HS_E_TOO_MANY_VALUES, "hs_rns_encode: more values than slots");
+    if (!(scale > 0.0) || !std::isfinite(scale)) fail(HS_E_INVALID_ARG, "hs_rns_encode: bad scale");
+    for (uint64_t i = 0; i < n; ++i)
+      if (!std::isfinite(z[i])) fail(HS_E_NON_FINITE_VALUE, "hs_rns_encode: non-finite value");
+    rns::encode(logN, z, n, scale, coeffs);
+  });
+}
+
+int hs_rns_decode(uint32_t logN, const int64_t* coeffs, double scale, double* z, uint64_t n) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    if (logN < 2 || logN > 17) fail(HS_E_INVALID_ARG, "hs_rns_decode: logN out of range");
+    if (n > (1u << logN) / 2) fail(HS_E_TOO_MANY_VALUES, "hs_rns_decode: more values than slots");
+    if (n && !z) fail(HS_E_INVALID_ARG, "null output");
+    if (!(scale > 0.0) || !std::isfinite(scale)) fail(HS_E_INVALID_ARG, "hs_rns_decode: bad scale");
+    rns::decode(logN, coeffs, scale, z, n);
+  });
+}
+
+int hs_rns_encrypt_coeffs(hs_rns* ctx, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* dev_out) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    need(dev_out, "out");
+    rns::encrypt_coeffs(rctx(ctx), level, coeffs, tag, dev_out);
+  });
+}
+
+int hs_rns_encrypt(hs_rns* ctx, uint32_t level, const double* z, uint64_t n, double scale, uint64_t tag,
+                   uint64_t* dev_out) {
+  std::vector<int64_t> co;
+  int rc = guard([&] { co.resize(rctx(ctx).N); });
+  if (rc) return rc;
+  rc = hs_rns_encode(ctx->c->spec.logN, z, n, scale, co.data());
+  if (rc) return rc;
+  return hs_rns_encrypt_coeffs(ctx, level, co.data(), tag, dev_out);
+}
+
+int hs_rns_decrypt_coeffs(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, int64_t* coeffs) {
+  return guard([&] {
+    need(dev_ct, "ciphertext");
+    need(coeffs, "coeffs");
+    rns::decrypt_coeffs(rctx(ctx), level, dev_ct, coeffs);
+  });
+}
+
+int hs_rns_decrypt(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, double scale, double* z, uint64_t n) {
+  std::vector<int64_t> co;
+  int rc = guard([&] { co.resize(rctx(ctx).N); });
+  if (rc) return rc;
+  rc = hs_rns_decrypt_coeffs(ctx, level, dev_ct, co.data());
+  if (rc) return rc;
+  return hs_rns_decode(ctx->c->spec.logN, co.data(), scale, z, n);
+}
+
 int hs_rns_ntt(hs_rns* ctx, uint64_t* dev, uint32_t first_prime, uint32_t nlimbs, uint32_t batch, int inverse) {
   return guard([&] {
     rns::Ctx& c = rctx(ctx);
@@ -763,6 +823,40 @@ int hs_rns_ntt(hs_rns* ctx, uint64_t* dev, uint32_t first_prime, uint32_t nlimbs
     std::vector<uint32_t> pm(nlimbs);
     for (uint32_t i = 0; i < nlimbs; ++i) pm[i] = first_prime + i;
     rns::ntt(c, dev, pm, batch, size_t(nlimbs) * c.N, inverse != 0);
+  });
+}
+
+int hs_rns_add(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    rns::add_sub(rctx(ctx), level, a, b, out, batch, false);
+  });
+}
+
+int hs_rns_sub(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    rns::add_sub(rctx(ctx), level, a, b, out, batch, true);
+  });
+}
+
+int hs_rns_add_const(hs_rns* ctx, uint32_t level, const uint64_t* a, int64_t c, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(out, "out");
+    rns::const_op(rctx(ctx), level, a, c, out, batch, false);
+  });
+}
+
+int hs_rns_mul_const(hs_rns* ctx, uint32_t level, const uint64_t* a, int64_t c, uint64_t* out, uint32_t batch) {
+  return guard([&] {
+    need(a, "a");
+    need(out, "out");
+    rns::const_op(rctx(ctx), level, a, c, out, batch, true);
   });
 }
 

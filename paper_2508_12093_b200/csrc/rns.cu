@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kT = 256;  // threads per elementwise block
 
-enum : uint64_t { D_SECRET = 1, D_KEY_A = 2, D_KEY_E = 3, D_CT = 4 };
+enum : uint64_t { D_SECRET = 1, D_KEY_A = 2, D_KEY_E = 3, D_CT = 4, D_ENC_A = 5, D_ENC_E = 6 };
 
 __host__ __device__ inline uint64_t hash64(uint64_t seed, uint64_t domain, uint64_t a, uint64_t b) {
   uint64_t z = seed ^ (domain * 0x9E3779B97F4A7C15ULL) ^ (a * 0xC2B2AE3D27D4EB4FULL) ^ (b * 0x165667B19E3779F9ULL);
@@ -389,6 +389,62 @@ __global__ void k_random_ct(uint64_t* out, const PrimeC* pcs, uint64_t seed, uin
     const uint32_t n = x & ((1u << logN) - 1), r = x >> logN, p = r / nl, i = r - p * nl;
     out[x] = uniform_mod(hash64(seed, D_CT, tag * 1024 + p * 64 + i, n), pcs[i].q);
   }
+}
+
+// Symmetric RLWE encryption of integer coefficients m (rns_oracle.c rnso_encrypt_coeffs):
+// c1 = a (uniform, NTT form), c0 = NTT(m + e) - a s.  This kernel writes [m + e]_{q_i}
+// (coefficient form) into the c0 rows and a into the c1 rows.
+__global__ void k_enc_me(const int64_t* coeffs, uint64_t* ct, const PrimeC* pcs, uint64_t seed, uint64_t tag,
+                         uint32_t nl, uint32_t logN) {
+  const size_t half = size_t(nl) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = x >> logN, n = x & ((1u << logN) - 1);
+    const uint64_t q = pcs[i].q;
+    const int64_t h = static_cast<int64_t>(__popcll(hash64(seed, D_ENC_E, tag, n) & 0x1FFFFFULL)) -
+                      static_cast<int64_t>(__popcll((hash64(seed, D_ENC_E, tag, n) >> 21) & 0x1FFFFFULL));
+    ct[x] = lift(coeffs[n] + h, q);
+    ct[half + x] = uniform_mod(hash64(seed, D_ENC_A, tag * 64 + i, n), q);
+  }
+}
+
+__global__ void k_enc_as(uint64_t* ct, const uint64_t* sk, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
+  const size_t half = size_t(nl) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
+    const PrimeC& P = pcs[x >> logN];
+    ct[x] = sub_mod(ct[x], mul_mod(ct[half + x], sk[x], P), P.q);
+  }
+}
+
+__global__ void k_addsub(const uint64_t* a, const uint64_t* b, uint64_t* out, const PrimeC* pcs, uint32_t nl,
+                         uint32_t logN, size_t total, bool sub) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total; x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = (x >> logN) % nl;
+    const uint64_t q = pcs[i].q;
+    out[x] = sub ? sub_mod(a[x], b[x], q) : add_mod(a[x], b[x], q);
+  }
+}
+
+// kv[i] = [k]_{q_i}; add: c0 += kv (constant polynomial = constant in NTT form), mul: both polys *= kv
+__global__ void k_constop(const uint64_t* a, const uint64_t* kv, const uint64_t* kvs, uint64_t* out,
+                          const PrimeC* pcs, uint32_t nl, uint32_t logN, size_t total, bool mul) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total; x += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = x >> logN;
+    const uint32_t i = r % nl, poly = (r / nl) & 1;
+    const uint64_t q = pcs[i].q;
+    if (mul)
+      out[x] = mul_shoup(a[x], kv[i], kvs[i], q);
+    else
+      out[x] = poly == 0 ? add_mod(a[x], kv[i], q) : a[x];
+  }
+}
+
+// decryption on limb 0: out = c0 + c1 s mod q_0 (NTT form; iNTT'd by the host after)
+__global__ void k_dec0(const uint64_t* ct, const uint64_t* sk, uint64_t* out, const PrimeC* pcs, uint32_t nl,
+                       uint32_t logN) {
+  const PrimeC P = pcs[0];
+  const size_t half = size_t(nl) << logN;
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < (1u << logN); n += gridDim.x * blockDim.x)
+    out[n] = add_mod(ct[n], mul_mod(ct[half + n], sk[n], P), P.q);
 }
 
 __global__ void k_secret(uint64_t* sk, const PrimeC* pcs, uint64_t seed, uint32_t np, uint32_t logN) {
@@ -869,6 +925,68 @@ const Ctx::Key& Ctx::galois_key(uint64_t g) {
 }
 
 // ================================================================== device ops
+void encrypt_coeffs(const Ctx& c, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* out) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns encrypt: level > L");
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1, logN = c.spec.logN;
+  DevBuf dco = rt.alloc(c.N);
+  cuda_ok(cudaMemcpyAsync(dco.get(), coeffs, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
+  k_enc_me<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const int64_t>(dco), out, c.dpc(), c.spec.seed, tag,
+                                                              nl, logN);
+  ntt(c, out, iota_rows(nl), 1, 0, false);
+  k_enc_as<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, dptr<const uint64_t>(c.d_sk), c.dpc(), nl, logN);
+  cuda_ok(cudaGetLastError(), "encrypt");
+  rt.note_launch(2);
+  rt.sync();  // the host coefficient buffer may be released by the caller
+}
+
+void decrypt_coeffs(const Ctx& c, uint32_t level, const uint64_t* ct, int64_t* coeffs) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns decrypt: level > L");
+  Runtime& rt = Runtime::get();
+  DevBuf m = rt.alloc(c.N);
+  k_dec0<<<grid_of(c.N), kT, 0, rt.stream()>>>(ct, dptr<const uint64_t>(c.d_sk), dptr<uint64_t>(m), c.dpc(),
+                                               level + 1, c.spec.logN);
+  ntt(c, dptr<uint64_t>(m), {0}, 1, 0, true);
+  std::vector<uint64_t> h(c.N);
+  cuda_ok(cudaMemcpyAsync(h.data(), m.get(), size_t(c.N) * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
+  rt.sync();
+  rt.note_launch();
+  const uint64_t q = c.primes[0], half = q / 2;
+  for (uint32_t n = 0; n < c.N; ++n)
+    coeffs[n] = h[n] > half ? -static_cast<int64_t>(q - h[n]) : static_cast<int64_t>(h[n]);
+}
+
+void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
+             bool sub) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns add: level > L");
+  Runtime& rt = Runtime::get();
+  const size_t total = size_t(batch) * 2 * (level + 1) * c.N;
+  k_addsub<<<grid_of(total), kT, 0, rt.stream()>>>(a, b, out, c.dpc(), level + 1, c.spec.logN, total, sub);
+  cuda_ok(cudaGetLastError(), "add");
+  rt.note_launch();
+}
+
+void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns const op: level > L");
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1;
+  std::vector<uint64_t> kv(2 * nl);
+  for (uint32_t i = 0; i < nl; ++i) {
+    const uint64_t q = c.primes[i];
+    const uint64_t m = k >= 0 ? static_cast<uint64_t>(k) % q : (q - static_cast<uint64_t>(-(k + 1)) % q - 1) % q;
+    kv[i] = m;
+    kv[nl + i] = shoup_of(m, q);
+  }
+  DevBuf d = rt.alloc(2 * nl);
+  cuda_ok(cudaMemcpyAsync(d.get(), kv.data(), kv.size() * 8, cudaMemcpyHostToDevice, rt.stream()), "const upload");
+  const size_t total = size_t(batch) * 2 * nl * c.N;
+  k_constop<<<grid_of(total), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(d), dptr<const uint64_t>(d) + nl, out,
+                                                     c.dpc(), nl, c.spec.logN, total, mul);
+  cuda_ok(cudaGetLastError(), "const op");
+  rt.note_launch();
+  rt.sync();  // the pageable host constant table is released on return
+}
+
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out) {
   Runtime& rt = Runtime::get();
   k_random_ct<<<grid_of(size_t(2) * (level + 1) * c.N), kT, 0, rt.stream()>>>(out, c.dpc(), c.spec.seed, tag, level + 1,

@@ -134,7 +134,17 @@ void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, ui
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
               const std::vector<uint32_t>& primes, uint32_t batch, bool inverse);
+// Symmetric RLWE encryption of N integer coefficients (host array) at `level`
+// (c1 = a, c0 = NTT(m + e) - a s; seeded by spec.seed and `tag`), and decryption
+// to centred integers mod q_0 (valid while |m| < q_0 / 2).
+void encrypt_coeffs(const Ctx& c, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* out);
+void decrypt_coeffs(const Ctx& c, uint32_t level, const uint64_t* ct, int64_t* coeffs);
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out);
+// out = a +- b (limb-wise), batch ciphertexts at `level`
+void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
+             bool sub);
+// out = a + c (constant polynomial, c0 only) or a * c (both polys); c a signed integer
+void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul);
 void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch);
 // HMult + relinearisation + rescale (out at level - 1): the composition of the two ops.

@@ -37,6 +37,24 @@ class RnsSpec:
         return 2 * (level + 1) * self.N
 
 
+def encode(logN: int, z, scale: float) -> np.ndarray:
+    """CKKS canonical-embedding encoding (host): <= N/2 reals -> N int64 coefficients."""
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
+    out = np.zeros(1 << logN, dtype=np.int64)
+    _check(_abi.lib().hs_rns_encode(logN, z.ctypes.data_as(C.POINTER(C.c_double)), z.size, scale,
+                                    out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def decode(logN: int, coeffs: np.ndarray, scale: float, n: int | None = None) -> np.ndarray:
+    co = np.ascontiguousarray(coeffs, dtype=np.int64)
+    n = (1 << logN) // 2 if n is None else n
+    out = np.zeros(n, dtype=np.float64)
+    _check(_abi.lib().hs_rns_decode(logN, co.ctypes.data_as(C.POINTER(C.c_int64)), scale,
+                                    out.ctypes.data_as(C.POINTER(C.c_double)), n))
+    return out
+
+
 class DeviceBuffer:
     """`words` u64 words of device memory (freed stream-ordered on release)."""
 
@@ -114,6 +132,56 @@ class RnsContext:
     def random_ct(self, level: int, tag: int, out: DeviceBuffer | None = None, offset: int = 0) -> DeviceBuffer:
         out = out or DeviceBuffer(self.spec.ct_words(level))
         _check(_abi.lib().hs_rns_random_ct(self.h, level, tag, out.offset(offset)))
+        return out
+
+    # ---- CKKS encoding / encryption ----
+    def encode(self, z, scale: float) -> np.ndarray:
+        return encode(self.spec.logN, z, scale)
+
+    def decode(self, coeffs: np.ndarray, scale: float, n: int | None = None) -> np.ndarray:
+        return decode(self.spec.logN, coeffs, scale, n)
+
+    def add(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
+            batch: int = 1, sub: bool = False) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        f = _abi.lib().hs_rns_sub if sub else _abi.lib().hs_rns_add
+        _check(f(self.h, level, a.ptr, b.ptr, out.ptr, batch))
+        return out
+
+    def add_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
+                  batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_add_const(self.h, level, a.ptr, int(c), out.ptr, batch))
+        return out
+
+    def mul_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
+                  batch: int = 1) -> DeviceBuffer:
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_mul_const(self.h, level, a.ptr, int(c), out.ptr, batch))
+        return out
+
+    def encrypt_coeffs(self, level: int, coeffs: np.ndarray, tag: int, out: DeviceBuffer | None = None) -> DeviceBuffer:
+        co = np.ascontiguousarray(coeffs, dtype=np.int64)
+        out = out or DeviceBuffer(self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_encrypt_coeffs(self.h, level, co.ctypes.data_as(C.POINTER(C.c_int64)), tag, out.ptr))
+        return out
+
+    def encrypt(self, level: int, z, scale: float, tag: int, out: DeviceBuffer | None = None) -> DeviceBuffer:
+        z = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
+        out = out or DeviceBuffer(self.spec.ct_words(level))
+        _check(_abi.lib().hs_rns_encrypt(self.h, level, z.ctypes.data_as(C.POINTER(C.c_double)), z.size, scale, tag,
+                                         out.ptr))
+        return out
+
+    def decrypt_coeffs(self, level: int, ct: DeviceBuffer) -> np.ndarray:
+        out = np.zeros(self.spec.N, dtype=np.int64)
+        _check(_abi.lib().hs_rns_decrypt_coeffs(self.h, level, ct.ptr, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def decrypt(self, level: int, ct: DeviceBuffer, scale: float, n: int | None = None) -> np.ndarray:
+        n = self.spec.N // 2 if n is None else n
+        out = np.zeros(n, dtype=np.float64)
+        _check(_abi.lib().hs_rns_decrypt(self.h, level, ct.ptr, scale, out.ctypes.data_as(C.POINTER(C.c_double)), n))
         return out
 
     def ntt(self, buf: DeviceBuffer, first_prime: int, nlimbs: int, batch: int = 1, inverse: bool = False):

@@ -70,6 +70,19 @@ class RnsOracle:
         self.lib.rnso_mul_relin(C.byref(s.c()), C.c_uint32(level), _u(a), _u(b), _u(out))
         return out
 
+    def encrypt_coeffs(self, s: Spec, level: int, coeffs: np.ndarray, tag: int) -> np.ndarray:
+        co = np.ascontiguousarray(coeffs, dtype=np.int64)
+        out = np.zeros(2 * (level + 1) * s.N, dtype=np.uint64)
+        self.lib.rnso_encrypt_coeffs(C.byref(s.c()), C.c_uint32(level), co.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     C.c_uint64(tag), _u(out))
+        return out
+
+    def decrypt_coeffs(self, s: Spec, level: int, ct: np.ndarray) -> np.ndarray:
+        out = np.zeros(s.N, dtype=np.int64)
+        self.lib.rnso_decrypt_coeffs(C.byref(s.c()), C.c_uint32(level), _u(np.ascontiguousarray(ct)),
+                                     out.ctypes.data_as(C.POINTER(C.c_int64)))
+        return out
+
     def mul_relin_many(self, s: Spec, level: int, a: np.ndarray, b: np.ndarray, count: int) -> np.ndarray:
         out = np.zeros(count * 2 * (level + 1) * s.N, dtype=np.uint64)
         self.lib.rnso_mul_relin_many(C.byref(s.c()), C.c_uint32(level), C.c_uint32(count), _u(a), _u(b), _u(out))

@@ -146,3 +146,81 @@ def test_rotate_identity(k):
         diff.append(O.ntt(SPEC, i, d, inverse=True))
     err = crt_centred(diff, primes[: level + 1])
     assert max(abs(e) for e in err) < 2 ** 30, max(abs(e) for e in err)
+
+
+# ---- CKKS codec (host functions of libhestat_gpu.so; no device work) and oracle encryption ----------
+def _codec():
+    from paper_2508_12093_b200 import rns
+    return rns
+
+
+@pytest.mark.parametrize("logN", [6, 10, 14, 16])
+def test_codec_round_trip(logN):
+    R = _codec()
+    rng = np.random.default_rng(logN)
+    S = 1 << (logN - 1)
+    z = rng.uniform(-100, 100, S)
+    co = R.encode(logN, z, 2.0 ** 40)
+    back = R.decode(logN, co, 2.0 ** 40)
+    assert np.max(np.abs(back - z)) < 1e-9
+    # a constant vector encodes to the constant polynomial
+    c = R.encode(logN, np.full(S, 1.5), 2.0 ** 40)
+    assert c[0] == round(1.5 * 2 ** 40) and np.max(np.abs(c[1:])) <= 1
+
+
+def _negacyclic(a, b):
+    N = len(a)
+    out = [0] * N
+    for i, x in enumerate(a):
+        if x == 0:
+            continue
+        for j, y in enumerate(b):
+            k = i + j
+            if k < N:
+                out[k] += x * y
+            else:
+                out[k - N] -= x * y
+    return out
+
+
+def test_codec_slot_semantics():
+    """Polynomial product = slot-wise product; X -> X^(5^k) = left rotation by k (ckks.hpp:193)."""
+    R = _codec()
+    logN, N = 6, 64
+    rng = np.random.default_rng(3)
+    z1, z2 = rng.uniform(-1, 1, N // 2), rng.uniform(-1, 1, N // 2)
+    s = 2.0 ** 20
+    m1, m2 = [int(v) for v in R.encode(logN, z1, s)], [int(v) for v in R.encode(logN, z2, s)]
+    prod = np.array(_negacyclic(m1, m2), dtype=np.float64)
+    got = R.decode(logN, np.rint(prod / s).astype(np.int64), s)
+    assert np.max(np.abs(got - z1 * z2)) < 1e-4
+    for k in (1, 3, -2):
+        g = galois_elt(k, logN)
+        rot = [0] * N
+        for i, v in enumerate(m1):
+            e = i * g % (2 * N)
+            if e < N:
+                rot[e] += v
+            else:
+                rot[e - N] -= v
+        out = R.decode(logN, np.array(rot, dtype=np.int64), s)
+        assert np.max(np.abs(out - np.roll(z1, -k))) < 1e-5
+
+
+def test_codec_errors():
+    from paper_2508_12093_b200 import hestat as H
+    R = _codec()
+    with pytest.raises(H.too_many_values):
+        R.encode(6, np.zeros(33), 2.0 ** 40)
+    with pytest.raises(H.non_finite_value):
+        R.encode(6, np.array([1.0, float("nan")]), 2.0 ** 40)
+
+
+def test_oracle_encrypt_decrypt():
+    N = SPEC.N
+    rng = np.random.default_rng(9)
+    m = rng.integers(-(2 ** 50), 2 ** 50, N)
+    for level in (SPEC.L, 0):
+        ct = O.encrypt_coeffs(SPEC, level, m, 7)
+        d = O.decrypt_coeffs(SPEC, level, ct)
+        assert np.max(np.abs(d - m)) <= 21  # centred-binomial error
