@@ -26,6 +26,8 @@
 
 #include <stdint.h>
 
+#include "hestat_gpu.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -84,6 +86,32 @@ int hs_rns_mul_relin_rescale(hs_rns* ctx, uint32_t level, const uint64_t* a, con
                              uint32_t batch);
 int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch); /* out: level-1 */
 int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
+
+/* ---- the reference's statistics over RNS ciphertexts -------------------------------
+ * An EvalContext (hs_params: slot_count must be N/2) whose ops run on Tier-R
+ * kernels: the reference's DAG (stats.hpp / primitives.hpp / chebyshev.hpp), level
+ * ledger, CostMeter and errors, with bootstrap() a logical level reset over a deep
+ * modulus chain (L >= the statistic's no-bootstrap depth).  Inputs are encrypted
+ * (column.hpp:25-39 chunking), outputs decrypted: out receives the first out_n
+ * slots of each result ciphertext (znorm: the n normalised values), out_levels
+ * the results' logical levels. */
+typedef struct hs_rns_eval hs_rns_eval;
+enum {
+  HS_RNS_INVSQRT = 0,   /* crypto_invsqrt(x, S = B)      primitives.hpp:186 */
+  HS_RNS_MEAN = 1,      /* mean_scaled(x, B)             stats.hpp:97  */
+  HS_RNS_VARIANCE = 2,  /* variance_scaled(x, B)         stats.hpp:130 */
+  HS_RNS_MOMENTS = 3,   /* moments(x, B): mu, var        stats.hpp:138 */
+  HS_RNS_ZNORM = 4,     /* znorm(x, B)                   stats.hpp:153 */
+  HS_RNS_KURTOSIS = 5,  /* kurtosis(x, B)                stats.hpp:170 */
+  HS_RNS_SKEWNESS = 6,  /* skewness(x, B)                stats.hpp:192 */
+  HS_RNS_PEARSON = 7    /* pearson(x, y, B)              stats.hpp:239 */
+};
+int hs_rns_eval_create(hs_rns* ctx, const hs_params* p, hs_rns_eval** out);
+int hs_rns_eval_destroy(hs_rns_eval* e);
+int hs_rns_eval_meter(const hs_rns_eval* e, hs_meter* out);
+int hs_rns_eval_set_meter(hs_rns_eval* e, const hs_meter* m);
+int hs_rns_eval_stat(hs_rns_eval* e, int which, const double* x, uint64_t n, const double* y, uint64_t ny, double B,
+                     const hs_invroot_cfg* cfg, double* out, uint64_t out_n, int32_t* out_levels);
 
 #ifdef __cplusplus
 }

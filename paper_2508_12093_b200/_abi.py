@@ -147,6 +147,12 @@ _SIGS.update({
     "hs_rns_encrypt": (C.c_int, [RNS, C.c_uint32, DP, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p]),
     "hs_rns_decrypt_coeffs": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.POINTER(C.c_int64)]),
     "hs_rns_decrypt": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_double, DP, C.c_uint64]),
+    "hs_rns_eval_create": (C.c_int, [RNS, C.POINTER(hs_params), C.POINTER(C.c_void_p)]),
+    "hs_rns_eval_destroy": (C.c_int, [C.c_void_p]),
+    "hs_rns_eval_meter": (C.c_int, [C.c_void_p, C.POINTER(hs_meter)]),
+    "hs_rns_eval_set_meter": (C.c_int, [C.c_void_p, C.POINTER(hs_meter)]),
+    "hs_rns_eval_stat": (C.c_int, [C.c_void_p, C.c_int, DP, C.c_uint64, DP, C.c_uint64, C.c_double,
+                                   C.POINTER(hs_invroot_cfg), DP, C.c_uint64, C.POINTER(C.c_int32)]),
     "hs_rns_ntt": (C.c_int, [RNS, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
     "hs_rns_mul_relin": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_mul_relin_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),

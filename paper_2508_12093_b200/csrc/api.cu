@@ -11,6 +11,8 @@
 #include "pipelines.h"
 #include "rns.h"
 #include "rns_codec.h"
+#include "rns_eval.h"
+#include "flow.h"
 #include "series.h"
 #include "hestat_rns.h"
 
@@ -637,6 +639,11 @@ void hs_graph_destroy(hs_graph* g) {
 struct hs_rns {
   std::unique_ptr<rns::Ctx> c;
 };
+struct hs_rns_eval {  // EvalContext (params + meter) bound to an RNS context
+  rns::Ctx* r = nullptr;
+  Params p;
+  Meter m;
+};
 
 namespace {
 rns::Ctx& rctx(hs_rns* h) {
@@ -893,6 +900,109 @@ int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, ui
     need(in, "in");
     need(out, "out");
     rns::rotate(rctx(ctx), level, k, in, out, batch);
+  });
+}
+
+// ---- Tier R statistics: the reference's EvalContext over RNS ciphertexts (rns_eval.h)
+int hs_rns_eval_create(hs_rns* r, const hs_params* p, hs_rns_eval** out) {
+  return guard([&] {
+    need(p, "params");
+    need(out, "out");
+    rns::Ctx& c = rctx(r);
+    Params pp = Params::from(*p);
+    pp.validate();
+    if (pp.S != c.N / 2) fail(HS_E_INVALID_ARG, "hs_rns_eval_create: slot_count must be N/2");
+    auto e = std::make_unique<hs_rns_eval>();
+    e->r = &c;
+    e->p = pp;
+    *out = e.release();
+  });
+}
+
+int hs_rns_eval_destroy(hs_rns_eval* e) {
+  return guard([&] { delete e; });
+}
+
+int hs_rns_eval_meter(const hs_rns_eval* e, hs_meter* out) {
+  return guard([&] {
+    need(e, "eval");
+    need(out, "out");
+    *out = hs_meter{e->m.mul_ct, e->m.mul_pt, e->m.add, e->m.rotate, e->m.bootstrap};
+  });
+}
+
+int hs_rns_eval_set_meter(hs_rns_eval* e, const hs_meter* m) {
+  return guard([&] {
+    need(e, "eval");
+    need(m, "meter");
+    e->m = Meter{m->mul_ct, m->mul_pt, m->add, m->rotate, m->bootstrap};
+  });
+}
+
+int hs_rns_eval_stat(hs_rns_eval* e, int which, const double* x, uint64_t n, const double* y, uint64_t ny, double B,
+                     const hs_invroot_cfg* cfg, double* out, uint64_t out_n, int32_t* out_levels) {
+  return guard([&] {
+    need(e, "eval");
+    need(out, "out");
+    if (n && !x) fail(HS_E_INVALID_ARG, "null column");
+    rns::RnsB b(*e->r, e->p, e->m);
+    const flow::InvCfg ic = cfg_of(cfg);
+    auto column = [&](const double* v, uint64_t len) {
+      if (len && !v) fail(HS_E_INVALID_ARG, "null column");
+      flow::Col<rns::RCt> col;
+      col.chunks = b.encrypt_column(v, len);
+      col.n_valid = len;
+      return col;
+    };
+    std::vector<rns::RCt> res;
+    switch (which) {
+      case HS_RNS_INVSQRT: {  // t in one ciphertext, S = B
+        if (n > e->p.S) fail(HS_E_TOO_MANY_VALUES, "invsqrt: more values than slots");
+        res.push_back(flow::crypto_invsqrt(b, b.encrypt(x, n), B, ic, n));
+        break;
+      }
+      case HS_RNS_MEAN: res.push_back(flow::mean_scaled(b, column(x, n), B)); break;
+      case HS_RNS_VARIANCE: res.push_back(flow::variance_scaled(b, column(x, n), B)); break;
+      case HS_RNS_MOMENTS: {
+        auto m = flow::moments(b, column(x, n), B);
+        res.push_back(m.mu);
+        res.push_back(m.var);
+        break;
+      }
+      case HS_RNS_ZNORM: {
+        auto z = flow::znorm(b, column(x, n), B, ic);
+        res = z.chunks;
+        break;
+      }
+      case HS_RNS_KURTOSIS: res.push_back(flow::std_moment(b, column(x, n), B, ic, 4)); break;
+      case HS_RNS_SKEWNESS: res.push_back(flow::std_moment(b, column(x, n), B, ic, 3)); break;
+      case HS_RNS_PEARSON: {
+        auto cx = column(x, n);
+        auto cy = column(y, ny);
+        res.push_back(flow::pearson(b, cx, cy, B, ic));
+        break;
+      }
+      default:
+        fail(HS_E_INVALID_ARG, "hs_rns_eval_stat: unknown statistic");
+    }
+    // znorm: the n values across chunks; others: the first out_n slots of each result
+    size_t w = 0;
+    if (which == HS_RNS_ZNORM) {
+      for (size_t i = 0; i < res.size() && w < out_n; ++i) {
+        const size_t take = std::min<size_t>(e->p.S, out_n - w);
+        const std::vector<double> v = b.decrypt(res[i], take);
+        std::copy(v.begin(), v.end(), out + w);
+        w += take;
+      }
+    } else {
+      for (const auto& r : res) {
+        const std::vector<double> v = b.decrypt(r, out_n);
+        std::copy(v.begin(), v.end(), out + w);
+        w += out_n;
+      }
+    }
+    if (out_levels)
+      for (size_t i = 0; i < res.size(); ++i) out_levels[i] = res[i]->level;
   });
 }
 

@@ -407,6 +407,29 @@ __global__ void k_enc_me(const int64_t* coeffs, uint64_t* ct, const PrimeC* pcs,
   }
 }
 
+// c0 rows (coefficient form) += e (CBD, stream D_ENC_E/tag); c1 rows = a (uniform, NTT form)
+__global__ void k_enc_res(uint64_t* ct, const PrimeC* pcs, uint64_t seed, uint64_t tag, uint32_t nl, uint32_t logN) {
+  const size_t half = size_t(nl) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = x >> logN, n = x & ((1u << logN) - 1);
+    const uint64_t q = pcs[i].q, h = hash64(seed, D_ENC_E, tag, n);
+    const int64_t e = static_cast<int64_t>(__popcll(h & 0x1FFFFFULL)) - static_cast<int64_t>(__popcll((h >> 21) & 0x1FFFFFULL));
+    ct[x] = add_mod(ct[x], lift(e, q), q);
+    ct[half + x] = uniform_mod(hash64(seed, D_ENC_A, tag * 64 + i, n), q);
+  }
+}
+
+// decryption on limbs 0..use-1: out[i] = c0_i + c1_i s_i (NTT form)
+__global__ void k_dec(const uint64_t* ct, const uint64_t* sk, uint64_t* out, const PrimeC* pcs, uint32_t nl,
+                      uint32_t use, uint32_t logN) {
+  const size_t half = size_t(nl) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(use) << logN);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const PrimeC& P = pcs[x >> logN];
+    out[x] = add_mod(ct[x], mul_mod(ct[half + x], sk[x], P), P.q);
+  }
+}
+
 __global__ void k_enc_as(uint64_t* ct, const uint64_t* sk, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
   const size_t half = size_t(nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
@@ -435,6 +458,24 @@ __global__ void k_constop(const uint64_t* a, const uint64_t* kv, const uint64_t*
       out[x] = mul_shoup(a[x], kv[i], kvs[i], q);
     else
       out[x] = poly == 0 ? add_mod(a[x], kv[i], q) : a[x];
+  }
+}
+
+// plaintext limbs from signed integer coefficients: pt[i][n] = [coeffs[n]]_{q_i}
+__global__ void k_lift(const int64_t* coeffs, uint64_t* pt, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(nl) << logN);
+       x += size_t(gridDim.x) * blockDim.x)
+    pt[x] = lift(coeffs[x & ((1u << logN) - 1)], pcs[x >> logN].q);
+}
+
+// out = a * pt on both polynomials (NTT form)
+__global__ void k_mul_plain(const uint64_t* a, const uint64_t* pt, uint64_t* out, const PrimeC* pcs, uint32_t nl,
+                            uint32_t logN) {
+  const size_t half = size_t(nl) << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * half; x += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = x < half ? x : x - half;
+    const PrimeC& P = pcs[r >> logN];
+    out[x] = mul_mod(a[x], pt[r], P);
   }
 }
 
@@ -956,6 +997,23 @@ void decrypt_coeffs(const Ctx& c, uint32_t level, const uint64_t* ct, int64_t* c
     coeffs[n] = h[n] > half ? -static_cast<int64_t>(q - h[n]) : static_cast<int64_t>(h[n]);
 }
 
+void mul_plain_coeffs(const Ctx& c, uint32_t level, const uint64_t* a, const int64_t* coeffs, uint64_t* out) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_plain: level > L");
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1, logN = c.spec.logN;
+  DevBuf dco = rt.alloc(c.N);
+  DevBuf pt = rt.alloc(size_t(nl) * c.N);
+  cuda_ok(cudaMemcpyAsync(dco.get(), coeffs, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
+  k_lift<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const int64_t>(dco), dptr<uint64_t>(pt), c.dpc(), nl,
+                                                            logN);
+  ntt(c, dptr<uint64_t>(pt), iota_rows(nl), 1, 0, false);
+  k_mul_plain<<<grid_of(size_t(2) * nl * c.N), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(pt), out, c.dpc(), nl,
+                                                                     logN);
+  cuda_ok(cudaGetLastError(), "mul_plain");
+  rt.note_launch(2);
+  rt.sync();  // the host coefficient buffer may be released by the caller
+}
+
 void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
              bool sub) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns add: level > L");
@@ -966,16 +1024,33 @@ void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b,
   rt.note_launch();
 }
 
-void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul) {
+__int128 i128_of(double v) {
+  if (!(std::fabs(v) < 8.5e37)) fail(HS_E_ERROR, "rns: encoded value out of the 127-bit range");
+  const bool neg = v < 0;
+  const double m = neg ? -v : v;
+  const double two64 = 18446744073709551616.0;
+  const double hi = std::floor(m / two64);
+  const double lo = m - hi * two64;  // exact: m has 53 significant bits
+  const unsigned __int128 r =
+      (static_cast<unsigned __int128>(static_cast<uint64_t>(hi)) << 64) + static_cast<uint64_t>(lo);
+  return neg ? -static_cast<__int128>(r) : static_cast<__int128>(r);
+}
+
+uint64_t residue(__int128 k, uint64_t q) {
+  __int128 r = k % static_cast<__int128>(q);
+  if (r < 0) r += q;
+  return static_cast<uint64_t>(r);
+}
+
+void const_op_res(const Ctx& c, uint32_t level, const uint64_t* a, const std::vector<uint64_t>& res, uint64_t* out,
+                  uint32_t batch, bool mul) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns const op: level > L");
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1;
   std::vector<uint64_t> kv(2 * nl);
   for (uint32_t i = 0; i < nl; ++i) {
-    const uint64_t q = c.primes[i];
-    const uint64_t m = k >= 0 ? static_cast<uint64_t>(k) % q : (q - static_cast<uint64_t>(-(k + 1)) % q - 1) % q;
-    kv[i] = m;
-    kv[nl + i] = shoup_of(m, q);
+    kv[i] = res[i];
+    kv[nl + i] = shoup_of(res[i], c.primes[i]);
   }
   DevBuf d = rt.alloc(2 * nl);
   cuda_ok(cudaMemcpyAsync(d.get(), kv.data(), kv.size() * 8, cudaMemcpyHostToDevice, rt.stream()), "const upload");
@@ -985,6 +1060,83 @@ void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64
   cuda_ok(cudaGetLastError(), "const op");
   rt.note_launch();
   rt.sync();  // the pageable host constant table is released on return
+}
+
+void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul) {
+  std::vector<uint64_t> res(level + 1);
+  for (uint32_t i = 0; i <= level && i < c.primes.size(); ++i) res[i] = residue(k, c.primes[i]);
+  const_op_res(c, level, a, res, out, batch, mul);
+}
+
+void const_op_big(const Ctx& c, uint32_t level, const uint64_t* a, double k, uint64_t* out, uint32_t batch,
+                  bool mul) {
+  const __int128 v = i128_of(std::nearbyint(k));
+  std::vector<uint64_t> res(level + 1);
+  for (uint32_t i = 0; i <= level && i < c.primes.size(); ++i) res[i] = residue(v, c.primes[i]);
+  const_op_res(c, level, a, res, out, batch, mul);
+}
+
+void residues_of(const Ctx& c, uint32_t nl, const double* coeffs, std::vector<uint64_t>* out) {
+  out->assign(size_t(nl) * c.N, 0);
+  for (uint32_t n = 0; n < c.N; ++n) {
+    const __int128 v = i128_of(coeffs[n]);
+    for (uint32_t i = 0; i < nl; ++i) (*out)[size_t(i) * c.N + n] = residue(v, c.primes[i]);
+  }
+}
+
+void encrypt_residues(const Ctx& c, uint32_t level, const uint64_t* res, uint64_t tag, uint64_t* out) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns encrypt: level > L");
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1, logN = c.spec.logN;
+  cuda_ok(cudaMemcpyAsync(out, res, size_t(nl) * c.N * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
+  k_enc_res<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, c.dpc(), c.spec.seed, tag, nl, logN);
+  ntt(c, out, iota_rows(nl), 1, 0, false);
+  k_enc_as<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, dptr<const uint64_t>(c.d_sk), c.dpc(), nl, logN);
+  cuda_ok(cudaGetLastError(), "encrypt");
+  rt.note_launch(2);
+  rt.sync();
+}
+
+void mul_plain_residues(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* res, uint64_t* out) {
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1;
+  DevBuf pt = rt.alloc(size_t(nl) * c.N);
+  cuda_ok(cudaMemcpyAsync(pt.get(), res, size_t(nl) * c.N * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
+  ntt(c, dptr<uint64_t>(pt), iota_rows(nl), 1, 0, false);
+  k_mul_plain<<<grid_of(size_t(2) * nl * c.N), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(pt), out, c.dpc(), nl,
+                                                                     c.spec.logN);
+  cuda_ok(cudaGetLastError(), "mul_plain");
+  rt.note_launch();
+  rt.sync();
+}
+
+void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeffs) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns decrypt: level > L");
+  Runtime& rt = Runtime::get();
+  const uint32_t nl = level + 1, use = level >= 1 ? 2 : 1;
+  DevBuf m = rt.alloc(size_t(use) * c.N);
+  k_dec<<<grid_of(size_t(use) * c.N), kT, 0, rt.stream()>>>(ct, dptr<const uint64_t>(c.d_sk), dptr<uint64_t>(m),
+                                                             c.dpc(), nl, use, c.spec.logN);
+  ntt(c, dptr<uint64_t>(m), iota_rows(use), 1, 0, true);
+  std::vector<uint64_t> h(size_t(use) * c.N);
+  cuda_ok(cudaMemcpyAsync(h.data(), m.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
+  rt.sync();
+  rt.note_launch();
+  const uint64_t q0 = c.primes[0];
+  if (use == 1) {
+    for (uint32_t n = 0; n < c.N; ++n)
+      coeffs[n] = h[n] > q0 / 2 ? -static_cast<double>(q0 - h[n]) : static_cast<double>(h[n]);
+    return;
+  }
+  const uint64_t q1 = c.primes[1];
+  const uint64_t q0inv = h_inv(q0 % q1, q1);
+  const unsigned __int128 Q = static_cast<unsigned __int128>(q0) * q1;
+  for (uint32_t n = 0; n < c.N; ++n) {
+    const uint64_t a0 = h[n], a1 = h[c.N + n];
+    const uint64_t t = h_mulmod((a1 + q1 - a0 % q1) % q1, q0inv, q1);
+    const unsigned __int128 v = a0 + static_cast<unsigned __int128>(q0) * t;  // CRT value in [0, q0 q1)
+    coeffs[n] = v > Q / 2 ? -static_cast<double>(Q - v) : static_cast<double>(v);
+  }
 }
 
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out) {

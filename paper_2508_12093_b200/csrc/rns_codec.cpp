@@ -98,6 +98,27 @@ void encode(uint32_t logN, const double* z, size_t n, double scale, int64_t* coe
   }
 }
 
+void encode_real(uint32_t logN, const double* z, size_t n, double scale, double* coeffs) {
+  const FftPlan& p = plan(logN);
+  const uint32_t N = 1u << logN, S = N / 2;
+  if (n > S) throw std::invalid_argument("encode: more values than slots");
+  std::vector<cd> a(p.n, cd(0.0, 0.0));
+  for (size_t j = 0; j < n; ++j) a[p.t[j]] = cd(z[j], 0.0);
+  fft(a, p, -1);
+  const double f = 2.0 / static_cast<double>(N);
+  for (uint32_t k = 0; k < N; ++k) coeffs[k] = std::nearbyint(a[k].real() * f * scale);
+}
+
+void decode_real(uint32_t logN, const double* coeffs, double scale, double* z, size_t n) {
+  const FftPlan& p = plan(logN);
+  const uint32_t N = 1u << logN, S = N / 2;
+  if (n > S) throw std::invalid_argument("decode: more values than slots");
+  std::vector<cd> a(p.n, cd(0.0, 0.0));
+  for (uint32_t k = 0; k < N; ++k) a[k] = cd(coeffs[k] / scale, 0.0);
+  fft(a, p, +1);
+  for (size_t j = 0; j < n; ++j) z[j] = a[p.t[j]].real();
+}
+
 void decode(uint32_t logN, const int64_t* coeffs, double scale, double* z, size_t n) {
   const FftPlan& p = plan(logN);
   const uint32_t N = 1u << logN, S = N / 2;

@@ -1,0 +1,81 @@
+// rns_eval.h — the reference's EvalContext semantics over real RNS-CKKS ciphertexts.
+//
+// RnsB is a third backend for flow.h (next to SymB and DevB): the same control
+// flow (levels, CostMeter, auto-bootstrap decisions, errors — ckks.hpp:113-240)
+// drives Tier-R kernels instead of slot kernels, so every statistic of the
+// reference runs on RNS ciphertexts with the reference's DAG.
+//
+//   logical level  the reference's level (ledger; bootstrap resets it);
+//   physical level the RNS chain position (limbs q_0..q_p).  Every mul_ct /
+//                  mul_pt consumes one physical level (rescale); bootstrap is a
+//                  logical reset only ("deep chain"), so the chain
+//                  must be at least the DAG's no-bootstrap depth.
+//   scale          exact per physical level: sigma_0 = 2^logq (~ the rescaling primes),
+//                  sigma_p = sqrt(sigma_{p-1} q_p).  Then HMult+rescale of two
+//                  level-p ciphertexts lands exactly on sigma_{p-1}; plaintext
+//                  constants are encoded at sigma_{p-1} q_p / sigma_p so mul_pt also
+//                  lands on sigma_{p-1}; operands at different physical levels are
+//                  aligned by dropping limbs and one constant-multiply + rescale.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "backends.h"
+#include "core.h"
+#include "rns.h"
+
+namespace hsg {
+namespace rns {
+
+struct RCtData {
+  DevBuf buf;  // u64 [2][phys+1][N], NTT form
+  int phys = 0;
+  int level = 0;
+  size_t n = 0;
+};
+using RCt = std::shared_ptr<const RCtData>;
+
+class RnsB : public LedgerBase<RnsB, RCt> {
+ public:
+  using C = RCt;
+  RnsB(Ctx& c, const Params& p, Meter& m);
+
+  int level(const C& c) const { return c ? c->level : 0; }
+  C encrypt(const double* v, size_t n);
+  std::vector<C> encrypt_column(const double* v, size_t n);  // column.hpp:25-39
+  C encrypt_const(double c);
+  C add_ct(const C& a, const C& b) { return addsub(a, b, false); }
+  C sub_ct(const C& a, const C& b) { return addsub(a, b, true); }
+  C add_pt(const C& a, double c);
+  C bootstrap(const C& a);
+  C mul_ct(C a, C b);
+  C mul_pt(C a, double c);
+  C mul_pt_vec(C a, const std::vector<double>& v);
+  C rotate(const C& a, long k);
+  C sum_all_slots(const C& a, size_t n_valid);
+
+  double first_slot(const C& c);
+  void check_open_domain(const C& c, size_t n_valid, double lo, double hi, const char* who);
+  void check_eval_domain(const C& c, double lo, double hi);
+  void check_divergence(const C& c, size_t n_valid);
+  void check_sqrt_domain(const C& c, size_t n_valid);
+  void check_sign_domain(const C& c);
+
+  std::vector<double> decrypt(const C& c, size_t n);
+  double scale(int phys) const { return sigma_[static_cast<size_t>(phys)]; }
+
+ private:
+  C addsub(const C& a, const C& b, bool sub);
+  C prepare_mul_pt(C a);
+  C align(const C& x, int p);  // same value at physical level p (<= x->phys), scale sigma_p
+  C make(DevBuf b, int phys, int level) const;
+  size_t words(int phys) const { return size_t(2) * (phys + 1) * c_.N; }
+  size_t sz(const C& c) const { return c ? c->n : 0; }
+  Ctx& c_;
+  std::vector<double> sigma_;
+  uint64_t tag_ = 1;
+};
+
+}  // namespace rns
+}  // namespace hsg

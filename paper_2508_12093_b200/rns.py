@@ -209,3 +209,61 @@ class RnsContext:
         out = out or DeviceBuffer(batch * self.spec.ct_words(level))
         _check(_abi.lib().hs_rns_rotate(self.h, level, k, a.ptr, out.ptr, batch))
         return out
+
+
+# ---- the reference's statistics over RNS ciphertexts (hs_rns_eval_*) --------------------------
+INVSQRT, MEAN, VARIANCE, MOMENTS, ZNORM, KURTOSIS, SKEWNESS, PEARSON = range(8)
+
+
+class RnsEval:
+    """EvalContext semantics (levels, CostMeter, errors) over Tier-R ciphertexts:
+    inputs are encrypted, the reference's DAG runs on RNS kernels, outputs are
+    decrypted.  params.slot_count must be N/2 of the RNS context."""
+
+    def __init__(self, ctx: RnsContext, params=None):
+        from .hestat import CkksParams
+        self.ctx = ctx
+        self.params = params or CkksParams(slot_count=ctx.spec.N // 2)
+        h = C.c_void_p()
+        _check(_abi.lib().hs_rns_eval_create(ctx.h, C.byref(self.params._c()), C.byref(h)))
+        self.h = h.value
+
+    def close(self):
+        if self.h:
+            _abi.lib().hs_rns_eval_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def meter(self):
+        from .hestat import CostMeter
+        m = _abi.hs_meter()
+        _check(_abi.lib().hs_rns_eval_meter(self.h, C.byref(m)))
+        return CostMeter(m.mul_ct, m.mul_pt, m.add, m.rotate, m.bootstrap)
+
+    def reset_meter(self):
+        _check(_abi.lib().hs_rns_eval_set_meter(self.h, C.byref(_abi.hs_meter())))
+
+    def stat(self, which: int, x, B: float, y=None, cfg=None, out_n: int = 1):
+        """Returns (values, levels): values are the first out_n decrypted slots of each
+        result (znorm: the n normalised values); levels the results' logical levels."""
+        from .hestat import InvRootConfig
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+        yp, ny = None, 0
+        if y is not None:
+            y = np.ascontiguousarray(np.asarray(y, dtype=np.float64).reshape(-1))
+            yp, ny = y.ctypes.data_as(C.POINTER(C.c_double)), y.size
+        nres = 2 if which == MOMENTS else 1
+        if which == ZNORM:
+            out_n = x.size
+        out = np.zeros(out_n * (1 if which == ZNORM else nres), dtype=np.float64)
+        levels = np.zeros(max(nres, (x.size + self.params.slot_count - 1) // self.params.slot_count), dtype=np.int32)
+        c = (cfg or InvRootConfig())._c()
+        _check(_abi.lib().hs_rns_eval_stat(self.h, which, x.ctypes.data_as(C.POINTER(C.c_double)), x.size, yp, ny,
+                                           float(B), C.byref(c), out.ctypes.data_as(C.POINTER(C.c_double)), out_n,
+                                           levels.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out, levels
