@@ -257,7 +257,7 @@ def rns_parity_small():
     from paper_2508_12093_b200.rns import DeviceBuffer, RnsContext, RnsSpec
     s = Spec(logN=12, L=5, K=2, dnum=3, seed=9)
     O = RnsOracle()
-    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed))
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed, h=s.h))
     a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
     da, db = DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)
     ok = np.array_equal(c.mul_relin_rescale(s.L, da, db).download(), O.rescale(s, s.L, O.mul_relin(s, s.L, a, b)))

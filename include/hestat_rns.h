@@ -35,6 +35,7 @@ extern "C" {
 typedef struct {
   uint32_t logN, L, K, dnum; /* ring degree 2^logN; L+1 q-primes; K p-primes; dnum digits */
   uint32_t logq0, logq, logp;
+  uint32_t h;                /* secret Hamming weight: 0 = dense ternary, else ~h nonzeros (sparse) */
   uint64_t seed;             /* secret/key/sample streams (rns_oracle.h) */
 } hs_rns_spec;
 

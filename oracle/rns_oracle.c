@@ -11,7 +11,9 @@
  *               twiddle psi^bitrev(m+i); inverse Gentleman-Sande + N^-1.
  *   hash        splitmix64 finaliser of seed ^ mixes of (domain, a, b).
  *   uniform     residue = (hash * q) >> 64.
- *   ternary s   hash % 3 - 1 per coefficient; error e: centered binomial,
+ *   ternary s   h = 0: hash % 3 - 1 per coefficient; h > 0 (sparse): s_n = +-1 with
+ *               probability h/N (hash(1, n) < h 2^64 / N), sign from hash(2, n) & 1;
+ *               error e: centered binomial,
  *               popcount(h & 2^21-1) - popcount((h >> 21) & 2^21-1).
  *   digits      dnum digits of alpha = ceil((L+1)/dnum) consecutive q primes.
  *   key j       (b_j, a_j) over all L+1+K primes, NTT form:
@@ -229,7 +231,12 @@ void rnso_random_ct(const rns_spec* s, uint32_t level, uint64_t tag, uint64_t* c
 }
 
 /* ------------------------------------------------------------------ keys */
-static int64_t ternary(uint64_t seed, uint32_t n) { return (int64_t)(rnso_hash(seed, D_SECRET, 0, n) % 3) - 1; }
+static int64_t ternary(const rns_spec* s, uint32_t n) {
+  if (s->h == 0) return (int64_t)(rnso_hash(s->seed, D_SECRET, 0, n) % 3) - 1;
+  const uint64_t thr = (uint64_t)s->h << (64 - s->logN);
+  if (rnso_hash(s->seed, D_SECRET, 1, n) >= thr) return 0;
+  return (rnso_hash(s->seed, D_SECRET, 2, n) & 1) ? -1 : 1;
+}
 static int64_t cbd(uint64_t h) {
   return (int64_t)__builtin_popcountll(h & 0x1FFFFFULL) - (int64_t)__builtin_popcountll((h >> 21) & 0x1FFFFFULL);
 }
@@ -239,7 +246,7 @@ static uint64_t lift(int64_t v, uint64_t q) { return v >= 0 ? (uint64_t)v % q : 
 static void secret_ntt(ctx_t* c, uint64_t* sk) {
   const uint32_t N = 1u << c->s.logN, np = c->s.L + 1 + c->s.K;
   for (uint32_t i = 0; i < np; ++i) {
-    for (uint32_t n = 0; n < N; ++n) sk[(size_t)i * N + n] = lift(ternary(c->s.seed, n), c->primes[i]);
+    for (uint32_t n = 0; n < N; ++n) sk[(size_t)i * N + n] = lift(ternary(&c->s, n), c->primes[i]);
     ntt_fwd(c, i, sk + (size_t)i * N);
   }
 }

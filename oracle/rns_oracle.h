@@ -28,6 +28,7 @@ typedef struct {
   uint32_t K;         /* special primes p_0..p_{K-1} */
   uint32_t dnum;      /* key-switching digits; alpha = ceil((L+1)/dnum) primes per digit */
   uint32_t logq0, logq, logp;
+  uint32_t h;         /* secret: 0 = dense ternary, else sparse with ~h nonzeros */
   uint64_t seed;
 } rns_spec;
 

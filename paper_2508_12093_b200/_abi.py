@@ -120,7 +120,8 @@ _SIGS = {
 
 class hs_rns_spec(C.Structure):  # include/hestat_rns.h
     _fields_ = [("logN", C.c_uint32), ("L", C.c_uint32), ("K", C.c_uint32), ("dnum", C.c_uint32),
-                ("logq0", C.c_uint32), ("logq", C.c_uint32), ("logp", C.c_uint32), ("seed", C.c_uint64)]
+                ("logq0", C.c_uint32), ("logq", C.c_uint32), ("logp", C.c_uint32), ("h", C.c_uint32),
+                ("seed", C.c_uint64)]
 
 
 U64P = C.POINTER(C.c_uint64)

@@ -666,6 +666,7 @@ int hs_rns_create(const hs_rns_spec* spec, hs_rns** out) {
     s.logq0 = spec->logq0;
     s.logq = spec->logq;
     s.logp = spec->logp;
+    s.h = spec->h;
     s.seed = spec->seed;
     auto h = std::make_unique<hs_rns>();
     h->c = std::make_unique<rns::Ctx>(s);

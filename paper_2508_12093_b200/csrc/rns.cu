@@ -488,11 +488,19 @@ __global__ void k_dec0(const uint64_t* ct, const uint64_t* sk, uint64_t* out, co
     out[n] = add_mod(ct[n], mul_mod(ct[half + n], sk[n], P), P.q);
 }
 
-__global__ void k_secret(uint64_t* sk, const PrimeC* pcs, uint64_t seed, uint32_t np, uint32_t logN) {
+// dense ternary (h = 0) or sparse with ~h nonzeros (rns_oracle.c ternary)
+__global__ void k_secret(uint64_t* sk, const PrimeC* pcs, uint64_t seed, uint32_t h, uint32_t np, uint32_t logN) {
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(np) << logN);
        x += size_t(gridDim.x) * blockDim.x) {
     const uint32_t n = x & ((1u << logN) - 1), i = x >> logN;
-    sk[x] = lift(static_cast<int64_t>(hash64(seed, D_SECRET, 0, n) % 3) - 1, pcs[i].q);
+    int64_t v;
+    if (h == 0)
+      v = static_cast<int64_t>(hash64(seed, D_SECRET, 0, n) % 3) - 1;
+    else if (hash64(seed, D_SECRET, 1, n) >= (static_cast<uint64_t>(h) << (64 - logN)))
+      v = 0;
+    else
+      v = (hash64(seed, D_SECRET, 2, n) & 1) ? -1 : 1;
+    sk[x] = lift(v, pcs[i].q);
   }
 }
 
@@ -841,6 +849,7 @@ Ctx::Ctx(const Spec& s) : spec(s) {
   if (s.logN < 9 || s.logN > 17) fail(HS_E_INVALID_ARG, "rns: logN must be in [9, 17]");
   if (s.dnum < 1 || s.K < 1 || s.L + 1 + s.K > 64) fail(HS_E_INVALID_ARG, "rns: bad prime counts");
   if (s.dnum > s.L + 1) fail(HS_E_INVALID_ARG, "rns: dnum larger than the number of q primes");
+  if (s.h >= (1u << s.logN)) fail(HS_E_INVALID_ARG, "rns: secret Hamming weight must be below N");
   if (s.logq0 > 61 || s.logq > 61 || s.logp > 61 || s.logq < 20) fail(HS_E_INVALID_ARG, "rns: primes must be 20..61 bits");
   N = 1u << s.logN;
   nq = s.L + 1;
@@ -904,7 +913,7 @@ Ctx::Ctx(const Spec& s) : spec(s) {
   // secret key (NTT form over every prime)
   Runtime& rt = Runtime::get();
   d_sk = rt.alloc(size_t(np) * N);
-  k_secret<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(dptr<uint64_t>(d_sk), dpc(), s.seed, np, s.logN);
+  k_secret<<<grid_of(size_t(np) * N), kT, 0, rt.stream()>>>(dptr<uint64_t>(d_sk), dpc(), s.seed, s.h, np, s.logN);
   cuda_ok(cudaGetLastError(), "secret");
   ntt(*this, dptr<uint64_t>(d_sk), iota_rows(np), 1, 0, false);
   rt.sync();

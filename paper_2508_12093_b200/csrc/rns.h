@@ -35,6 +35,7 @@ typedef unsigned __int128 u128;
 struct Spec {
   uint32_t logN = 16, L = 24, K = 9, dnum = 3;
   uint32_t logq0 = 60, logq = 40, logp = 61;
+  uint32_t h = 0;  // secret Hamming weight: 0 dense ternary, else sparse (~h nonzeros)
   uint64_t seed = 0;
 };
 

@@ -197,6 +197,9 @@ RCt RnsB::sum_all_slots(const RCt& a, size_t n_valid) {  // ckks.hpp:218-230
 }
 
 std::vector<double> RnsB::decrypt(const RCt& c, size_t n) {
+  // q_0 alone cannot hold sigma_0 * value for |value| >= 2^(log q_0 - log sigma_0 - 1): decrypt through two limbs
+  if (c->phys < 1)
+    fail(HS_E_LEVEL_EXHAUSTED, "rns decrypt: result at the last RNS limb (chain must exceed the statistic's depth)");
   std::vector<double> co(c_.N);
   decrypt_crt(c_, c->phys, reinterpret_cast<const uint64_t*>(c->buf.get()), co.data());
   std::vector<double> z(n);

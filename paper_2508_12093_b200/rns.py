@@ -25,13 +25,15 @@ class RnsSpec:
     logq: int = 40
     logp: int = 61
     seed: int = 0
+    h: int = 0  # secret Hamming weight: 0 dense ternary, else sparse
 
     @property
     def N(self) -> int:
         return 1 << self.logN
 
     def c(self) -> _abi.hs_rns_spec:
-        return _abi.hs_rns_spec(self.logN, self.L, self.K, self.dnum, self.logq0, self.logq, self.logp, self.seed)
+        return _abi.hs_rns_spec(self.logN, self.L, self.K, self.dnum, self.logq0, self.logq, self.logp, self.h,
+                                self.seed)
 
     def ct_words(self, level: int) -> int:
         return 2 * (level + 1) * self.N

@@ -15,7 +15,8 @@ U64P = C.POINTER(C.c_uint64)
 
 class RnsSpec(C.Structure):
     _fields_ = [("logN", C.c_uint32), ("L", C.c_uint32), ("K", C.c_uint32), ("dnum", C.c_uint32),
-                ("logq0", C.c_uint32), ("logq", C.c_uint32), ("logp", C.c_uint32), ("seed", C.c_uint64)]
+                ("logq0", C.c_uint32), ("logq", C.c_uint32), ("logp", C.c_uint32), ("h", C.c_uint32),
+                ("seed", C.c_uint64)]
 
 
 @dataclass
@@ -28,9 +29,10 @@ class Spec:
     logq: int = 40
     logp: int = 61
     seed: int = 2025
+    h: int = 0
 
     def c(self) -> RnsSpec:
-        return RnsSpec(self.logN, self.L, self.K, self.dnum, self.logq0, self.logq, self.logp, self.seed)
+        return RnsSpec(self.logN, self.L, self.K, self.dnum, self.logq0, self.logq, self.logp, self.h, self.seed)
 
     @property
     def N(self) -> int:

@@ -20,12 +20,13 @@ SHAPES = [
     Spec(logN=10, L=5, K=2, dnum=4, seed=7),      # alpha=2, 3 digits at the top level
     Spec(logN=12, L=7, K=3, dnum=3, seed=11),     # alpha=3: partial last digit
     Spec(logN=13, L=4, K=1, dnum=5, seed=3),      # alpha=1, K=1
+    Spec(logN=12, L=5, K=3, dnum=3, seed=8, h=64),  # sparse secret (~64 nonzeros)
 ]
 
 
 def _ctx(s: Spec):
     from paper_2508_12093_b200.rns import RnsContext, RnsSpec
-    return RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed))
+    return RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed, h=s.h))
 
 
 def _buf(a):
@@ -37,7 +38,7 @@ _CTX = {}
 
 
 def ctx(s: Spec):
-    key = (s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed)
+    key = (s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed, s.h)
     if key not in _CTX:
         _CTX[key] = _ctx(s)
     return _CTX[key]

@@ -21,7 +21,7 @@ DELTA = 2.0 ** 40
 
 def _ctx(s):
     from paper_2508_12093_b200.rns import RnsContext, RnsSpec
-    return RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.seed))
+    return RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed, h=s.h))
 
 
 @pytest.fixture(scope="module")

@@ -109,6 +109,28 @@ def test_mul_relin_identity(level):
     assert max(abs(e) for e in err) < 2 ** 30, max(abs(e) for e in err)
 
 
+def test_sparse_secret_weight_and_identity():
+    s = Spec(logN=9, L=3, K=2, dnum=2, seed=4, h=32)
+    sk = O.secret(s)
+    q0 = int(O.primes(s)[0])
+    coeff = O.ntt(s, 0, sk[0], inverse=True)
+    nz = [int(v) for v in coeff if v != 0]
+    assert 16 <= len(nz) <= 56 and all(v in (1, q0 - 1) for v in nz)
+    # HMult+relin still decrypts to the product under the sparse key
+    level = 3
+    primes = O.primes(s)
+    a, b = O.random_ct(s, level, 1), O.random_ct(s, level, 2)
+    out = O.mul_relin(s, level, a, b)
+    pa, pb, po = (_ntt_phase(x, level, sk, primes, s.N) for x in (a, b, out))
+    diff = []
+    for i in range(level + 1):
+        q = int(primes[i])
+        d = np.array([(po[i][n] - pa[i][n] * pb[i][n]) % q for n in range(s.N)], dtype=np.uint64)
+        diff.append(O.ntt(s, i, d, inverse=True))
+    err = crt_centred(diff, primes[: level + 1])
+    assert max(abs(e) for e in err) < 2 ** 30
+
+
 def test_rescale_identity():
     level = 3
     N, primes, sk = SPEC.N, O.primes(SPEC), O.secret(SPEC)
