@@ -287,6 +287,40 @@ def rns_cpu_baseline(logN, L, K, dnum):
             "ms_per_op": 1e3 * per}
 
 
+def rns_znorm(torch, stream, reps=3):
+    """C2 Z-score on real RNS-CKKS ciphertexts (N=2^16, 2^15 slots): the reference's DAG
+    over Tier-R kernels (hs_rns_eval_stat), decrypted and compared with the reference's
+    output.  Wall time per ciphertext, keys warm (encrypt + evaluate + decrypt)."""
+    from oracle_abi import Params, ST_ZNORM, oracle
+    from paper_2508_12093_b200 import hestat as H
+    from paper_2508_12093_b200 import rns as R
+    from paper_2508_12093_b200 import workloads as W
+    L = 28
+    spec = R.RnsSpec(logN=16, L=L, K=(L + 3) // 3 + 1, dnum=3, logq0=61, logq=60, logp=61, seed=5, h=192)
+    ctx = R.RnsContext(spec)
+    ev = R.RnsEval(ctx, H.CkksParams(slot_count=S))
+    x = W.normal(H.synthetic_uniform, SEED, S, 50.0, 10.0)
+    ev.stat(R.ZNORM, x, B)  # keys (relin + 15 rotations) and plans
+    walls, z = [], None
+    for _ in range(reps):
+        ev.reset_meter()
+        t0 = time.perf_counter()
+        z, _ = ev.stat(R.ZNORM, x, B)
+        walls.append(time.perf_counter() - t0)
+    ref = oracle().stat(Params(slot_count=S), ST_ZNORM, x, B)
+    m = ev.meter()
+    out = {"metric": "encrypted Z-score ms per 2^15-slot ciphertext (RNS-CKKS)", "value": round(1e3 * min(walls), 2),
+           "unit": "ms/ciphertext",
+           "config": {"logN": 16, "L": L, "K": spec.K, "dnum": 3, "logq0": 61, "logq": 60, "logp": 61,
+                      "secret_hamming_weight": 192, "bootstrap": "logical level reset over the deep chain",
+                      "timing": "wall, keys warm, encrypt + znorm DAG + decrypt, best of %d" % reps},
+           "rel_err_vs_reference": float(np.max(np.abs(z - ref.out)) / np.max(np.abs(ref.out))),
+           "meter_equal": (m.mul_ct, m.mul_pt, m.add, m.rotate, m.bootstrap) == ref.meter}
+    ev.close()
+    ctx.close()
+    return out
+
+
 def tier_r_section(torch, stream, batch=64, with_cpu=True):
     logN, L, K, dnum = 16, 24, 9, 3
     peak, src = hbm_peak_gbs()
@@ -307,7 +341,8 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
                         "achieved": ops["mul_relin"]["achieved_gbs"], "peak": peak, "unit": "GB/s",
                         "frac": ops["mul_relin"]["hbm_frac"], "traffic": None, "peak_source": src,
                         "note": "integer-pipe bound (ncu: ALU pipe ~60% in the NTT), not HBM bound"},
-           "parity_vs_oracle": rns_parity_small()}
+           "parity_vs_oracle": rns_parity_small(),
+           "znorm": rns_znorm(torch, stream)}
     if with_cpu:
         sec["cpu_baseline"] = rns_cpu_baseline(logN, L, K, dnum)
     return sec

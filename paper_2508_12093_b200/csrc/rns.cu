@@ -448,24 +448,37 @@ __global__ void k_addsub(const uint64_t* a, const uint64_t* b, uint64_t* out, co
 }
 
 // kv[i] = [k]_{q_i}; add: c0 += kv (constant polynomial = constant in NTT form), mul: both polys *= kv
-__global__ void k_constop(const uint64_t* a, const uint64_t* kv, const uint64_t* kvs, uint64_t* out,
-                          const PrimeC* pcs, uint32_t nl, uint32_t logN, size_t total, bool mul) {
+// per-prime constant residues and Shoup factors, passed by value (no upload, no sync)
+struct ConstTab {
+  uint64_t k[64], ks[64];
+};
+
+__global__ void k_constop(const uint64_t* a, const __grid_constant__ ConstTab kt, uint64_t* out, const PrimeC* pcs,
+                          uint32_t nl, uint32_t logN, size_t total, bool mul) {
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total; x += size_t(gridDim.x) * blockDim.x) {
     const size_t r = x >> logN;
     const uint32_t i = r % nl, poly = (r / nl) & 1;
     const uint64_t q = pcs[i].q;
     if (mul)
-      out[x] = mul_shoup(a[x], kv[i], kvs[i], q);
+      out[x] = mul_shoup(a[x], kt.k[i], kt.ks[i], q);
     else
-      out[x] = poly == 0 ? add_mod(a[x], kv[i], q) : a[x];
+      out[x] = poly == 0 ? add_mod(a[x], kt.k[i], q) : a[x];
   }
 }
 
-// plaintext limbs from signed integer coefficients: pt[i][n] = [coeffs[n]]_{q_i}
-__global__ void k_lift(const int64_t* coeffs, uint64_t* pt, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
+// residues of integer-valued doubles (|v| < 2^127): pt[i][n] = [co[n]]_{q_i}
+__global__ void k_residues(const double* co, uint64_t* pt, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < (size_t(nl) << logN);
-       x += size_t(gridDim.x) * blockDim.x)
-    pt[x] = lift(coeffs[x & ((1u << logN) - 1)], pcs[x >> logN].q);
+       x += size_t(gridDim.x) * blockDim.x) {
+    const PrimeC& P = pcs[x >> logN];
+    const double v = co[x & ((1u << logN) - 1)];
+    const double m = fabs(v);
+    const double hi = floor(__dmul_rn(m, 5.421010862427522e-20));  // * 2^-64 (exact)
+    const double lo = __dsub_rn(m, __dmul_rn(hi, 18446744073709551616.0));
+    const u128 w = (static_cast<u128>(static_cast<uint64_t>(hi)) << 64) + static_cast<uint64_t>(lo);
+    const uint64_t r = reduce128(w, P);
+    pt[x] = (v < 0 && r) ? P.q - r : r;
+  }
 }
 
 // out = a * pt on both polynomials (NTT form)
@@ -1006,23 +1019,6 @@ void decrypt_coeffs(const Ctx& c, uint32_t level, const uint64_t* ct, int64_t* c
     coeffs[n] = h[n] > half ? -static_cast<int64_t>(q - h[n]) : static_cast<int64_t>(h[n]);
 }
 
-void mul_plain_coeffs(const Ctx& c, uint32_t level, const uint64_t* a, const int64_t* coeffs, uint64_t* out) {
-  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_plain: level > L");
-  Runtime& rt = Runtime::get();
-  const uint32_t nl = level + 1, logN = c.spec.logN;
-  DevBuf dco = rt.alloc(c.N);
-  DevBuf pt = rt.alloc(size_t(nl) * c.N);
-  cuda_ok(cudaMemcpyAsync(dco.get(), coeffs, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
-  k_lift<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const int64_t>(dco), dptr<uint64_t>(pt), c.dpc(), nl,
-                                                            logN);
-  ntt(c, dptr<uint64_t>(pt), iota_rows(nl), 1, 0, false);
-  k_mul_plain<<<grid_of(size_t(2) * nl * c.N), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(pt), out, c.dpc(), nl,
-                                                                     logN);
-  cuda_ok(cudaGetLastError(), "mul_plain");
-  rt.note_launch(2);
-  rt.sync();  // the host coefficient buffer may be released by the caller
-}
-
 void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
              bool sub) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns add: level > L");
@@ -1056,19 +1052,15 @@ void const_op_res(const Ctx& c, uint32_t level, const uint64_t* a, const std::ve
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns const op: level > L");
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1;
-  std::vector<uint64_t> kv(2 * nl);
+  ConstTab kt{};
   for (uint32_t i = 0; i < nl; ++i) {
-    kv[i] = res[i];
-    kv[nl + i] = shoup_of(res[i], c.primes[i]);
+    kt.k[i] = res[i];
+    kt.ks[i] = shoup_of(res[i], c.primes[i]);
   }
-  DevBuf d = rt.alloc(2 * nl);
-  cuda_ok(cudaMemcpyAsync(d.get(), kv.data(), kv.size() * 8, cudaMemcpyHostToDevice, rt.stream()), "const upload");
   const size_t total = size_t(batch) * 2 * nl * c.N;
-  k_constop<<<grid_of(total), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(d), dptr<const uint64_t>(d) + nl, out,
-                                                     c.dpc(), nl, c.spec.logN, total, mul);
+  k_constop<<<grid_of(total), kT, 0, rt.stream()>>>(a, kt, out, c.dpc(), nl, c.spec.logN, total, mul);
   cuda_ok(cudaGetLastError(), "const op");
   rt.note_launch();
-  rt.sync();  // the pageable host constant table is released on return
 }
 
 void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul) {
@@ -1085,37 +1077,34 @@ void const_op_big(const Ctx& c, uint32_t level, const uint64_t* a, double k, uin
   const_op_res(c, level, a, res, out, batch, mul);
 }
 
-void residues_of(const Ctx& c, uint32_t nl, const double* coeffs, std::vector<uint64_t>* out) {
-  out->assign(size_t(nl) * c.N, 0);
-  for (uint32_t n = 0; n < c.N; ++n) {
-    const __int128 v = i128_of(coeffs[n]);
-    for (uint32_t i = 0; i < nl; ++i) (*out)[size_t(i) * c.N + n] = residue(v, c.primes[i]);
-  }
-}
-
-void encrypt_residues(const Ctx& c, uint32_t level, const uint64_t* res, uint64_t tag, uint64_t* out) {
+void encrypt_real(const Ctx& c, uint32_t level, const double* co, uint64_t tag, uint64_t* out) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns encrypt: level > L");
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1, logN = c.spec.logN;
-  cuda_ok(cudaMemcpyAsync(out, res, size_t(nl) * c.N * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
+  DevBuf d = rt.alloc(c.N);
+  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
+  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const double>(d), out, c.dpc(), nl, logN);
   k_enc_res<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, c.dpc(), c.spec.seed, tag, nl, logN);
   ntt(c, out, iota_rows(nl), 1, 0, false);
   k_enc_as<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, dptr<const uint64_t>(c.d_sk), c.dpc(), nl, logN);
   cuda_ok(cudaGetLastError(), "encrypt");
-  rt.note_launch(2);
-  rt.sync();
+  rt.note_launch(3);
+  rt.sync();  // the caller's coefficient buffer may be released on return
 }
 
-void mul_plain_residues(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* res, uint64_t* out) {
+void mul_plain_real(const Ctx& c, uint32_t level, const uint64_t* a, const double* co, uint64_t* out) {
   Runtime& rt = Runtime::get();
-  const uint32_t nl = level + 1;
+  const uint32_t nl = level + 1, logN = c.spec.logN;
+  DevBuf d = rt.alloc(c.N);
   DevBuf pt = rt.alloc(size_t(nl) * c.N);
-  cuda_ok(cudaMemcpyAsync(pt.get(), res, size_t(nl) * c.N * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
+  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
+  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const double>(d), dptr<uint64_t>(pt), c.dpc(), nl,
+                                                                logN);
   ntt(c, dptr<uint64_t>(pt), iota_rows(nl), 1, 0, false);
   k_mul_plain<<<grid_of(size_t(2) * nl * c.N), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(pt), out, c.dpc(), nl,
-                                                                     c.spec.logN);
+                                                                     logN);
   cuda_ok(cudaGetLastError(), "mul_plain");
-  rt.note_launch();
+  rt.note_launch(2);
   rt.sync();
 }
 

@@ -141,15 +141,14 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
 void encrypt_coeffs(const Ctx& c, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* out);
 void decrypt_coeffs(const Ctx& c, uint32_t level, const uint64_t* ct, int64_t* coeffs);
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out);
-// out = a * m (plaintext given as N signed integer coefficients, host array)
-void mul_plain_coeffs(const Ctx& c, uint32_t level, const uint64_t* a, const int64_t* coeffs, uint64_t* out);
 // Big-constant / real-valued variants used by the statistics backend (rns_eval.cu):
 // integer-valued doubles up to 2^126 are reduced exactly through 128-bit integers.
 void const_op_big(const Ctx& c, uint32_t level, const uint64_t* a, double k, uint64_t* out, uint32_t batch,
                   bool mul);
-void residues_of(const Ctx& c, uint32_t nl, const double* coeffs, std::vector<uint64_t>* out);  // [nl][N]
-void encrypt_residues(const Ctx& c, uint32_t level, const uint64_t* res, uint64_t tag, uint64_t* out);
-void mul_plain_residues(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* res, uint64_t* out);
+// encryption of / multiplication by a plaintext given as N integer-valued double
+// coefficients (host), reduced into the RNS limbs on the device
+void encrypt_real(const Ctx& c, uint32_t level, const double* co, uint64_t tag, uint64_t* out);
+void mul_plain_real(const Ctx& c, uint32_t level, const uint64_t* a, const double* co, uint64_t* out);
 // decryption through q_0 q_1 (CRT; q_0 alone at level 0): centred coefficients as doubles
 void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeffs);
 // out = a +- b (limb-wise), batch ciphertexts at `level`

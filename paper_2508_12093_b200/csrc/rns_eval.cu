@@ -34,10 +34,8 @@ RCt RnsB::encrypt(const double* v, size_t n) {  // ckks.hpp:97-104
   const int L = static_cast<int>(c_.spec.L);
   std::vector<double> co(c_.N);
   encode_real(c_.spec.logN, v, n, sigma_[L], co.data());
-  std::vector<uint64_t> res;
-  residues_of(c_, L + 1, co.data(), &res);
   DevBuf b = Runtime::get().alloc(words(L));
-  encrypt_residues(c_, L, res.data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
+  encrypt_real(c_, L, co.data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
   return make(b, L, p_.max_level);
 }
 
@@ -160,12 +158,9 @@ RCt RnsB::mul_pt_vec(RCt a, const std::vector<double>& v) {  // ckks.hpp:179-189
   std::vector<double> co(c_.N);
   encode_real(c_.spec.logN, v.data(), v.size(), sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p],
               co.data());
-  std::vector<uint64_t> res;
-  residues_of(c_, p + 1, co.data(), &res);
   Runtime& rt = Runtime::get();
   DevBuf m = rt.alloc(words(p));
-  mul_plain_residues(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), res.data(),
-                     reinterpret_cast<uint64_t*>(m.get()));
+  mul_plain_real(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), co.data(), reinterpret_cast<uint64_t*>(m.get()));
   DevBuf o = rt.alloc(words(p - 1));
   rescale(c_, p, reinterpret_cast<const uint64_t*>(m.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_pt;
