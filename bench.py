@@ -348,12 +348,78 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
     return sec
 
 
+def c5_tier_e(torch, stream, S_, batch=64, pools=8, reps=3, ops=None):
+    """C5 tier E: batched EvalContext ops on `batch` ciphertexts of S_ U[-1,1] slots.
+    Device time per batch via graph replay over `pools` distinct input batches (> L2);
+    HBM roofline with SURVEY §8(d) bytes: 24 B/slot (add, mul_ct), 16 B/slot (mul_pt, rotate)."""
+    from paper_2508_12093_b200 import hestat as H
+    ctx = H.EvalContext(H.CkksParams(slot_count=S_))
+    rng = np.random.default_rng(S_)
+    base = [ctx.encrypt(rng.uniform(-1, 1, S_)) for _ in range(batch)]
+    # distinct pools: rotated copies (each its own allocation)
+    a = [ctx.rotate_batch(base, 97 * p + 1) for p in range(pools)]
+    b = [ctx.rotate_batch(base, 131 * p + 7) for p in range(pools)]
+    H.sync()
+    logS = S_.bit_length() - 1
+    fns = {"mul_ct": (lambda p: ctx.mul_ct_batch(a[p], b[p]), 24),
+           "add": (lambda p: ctx.add_ct_batch(a[p], b[p]), 24),
+           "mul_pt": (lambda p: ctx.mul_pt_batch(a[p], 0.731), 16)}
+    for j in range(logS):
+        fns[f"rotate_{1 << j}"] = ((lambda k: (lambda p: ctx.rotate_batch(a[p], k)))(1 << j), 16)
+    peak, _ = hbm_peak_gbs()
+    res = {}
+    for name, (fn, bps) in fns.items():
+        if ops and name not in ops:
+            continue
+        for p in range(pools):
+            fn(p)
+        H.sync()
+        with H.Graph() as g:
+            for r in range(reps):
+                for p in range(pools):
+                    fn(p)
+        g.launch()
+        H.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.launch()
+        e1.record(stream)
+        e1.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / (reps * pools)  # per batch
+        gbs = bps * S_ * batch / (us * 1e-6) / 1e9
+        res[name] = {"us_per_batch": round(us, 2), "ops_per_s": round(batch / (us * 1e-6), 1),
+                     "achieved_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4)}
+        del g
+    return res
+
+
+def c5_tier_e_cpu(S_, batch=64):
+    """The reference's own op (oracle/_ref shim) on all host threads: mul_ct over a batch."""
+    from oracle_abi import Params
+    lib, kind = cpu_lib()
+    p = Params(slot_count=S_)
+    rng = np.random.default_rng(S_)
+    xs = [rng.uniform(-1, 1, S_) for _ in range(batch)]
+    enc = [lib.encrypt(p, x) for x in xs]
+    threads = min(os.cpu_count() or 1, batch)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda e: lib.op(p, 3, e.out, e.levels[0], e.out, e.levels[0]), enc))
+    wall = time.perf_counter() - t0
+    return {"value": round(batch / wall, 1), "unit": "mul_ct/s", "cores": threads, "kind": kind,
+            "sample": f"{batch} mul_ct of {S_} slots through the reference's EvalContext::mul_ct, {threads} threads"}
+
+
 def c5_sweep(args):
     import torch
     torch.cuda.set_device(0)
     from paper_2508_12093_b200 import hestat as H
     H.init(0)
     stream = torch.cuda.ExternalStream(H.stream_handle())
+    for S_ in (8192, 16384, 32768):
+        line = {"sweep": "C5 tier E", "slots": S_, "batch": args.batch, "ops": c5_tier_e(torch, stream, S_, args.batch),
+                "cpu_baseline": c5_tier_e_cpu(S_, args.batch)}
+        print(json.dumps(line), flush=True)
     peak, src = hbm_peak_gbs()
     for logN in (14, 15, 16):
         for L in (8, 16, 24, 32):
@@ -540,6 +606,12 @@ def main():
                            "note": "graph replay per call, includes ~1-2 us node overhead"},
             "clocks": clk.summary(),
         }
+        c5 = c5_tier_e(torch, stream, S, args.batch, ops=("mul_ct", "add", "mul_pt", "rotate_1"))
+        line["c5_tier_e"] = {"metric": "mul_ct/s (batch of 64 x 2^15 slots)", "value": c5["mul_ct"]["ops_per_s"],
+                             "unit": "mul_ct/s", "ops": c5,
+                             "l2": "8 distinct input batches (384 MiB for mul_ct) cycled per replay"}
+        if not args.no_cpu_baseline and ws == 1:
+            line["c5_tier_e"]["cpu_baseline"] = c5_tier_e_cpu(S, args.batch)
         if not args.no_tier_r:
             line["tier_r"] = tier_r_section(torch, stream, args.batch, with_cpu=not args.no_cpu_baseline and ws == 1)
         if not args.no_cpu_baseline and ws == 1:

@@ -149,6 +149,15 @@ int hs_mul_pt_vec(hs_ctx* ctx, const hs_ct* a, const double* p, uint64_t n, hs_c
 int hs_rotate(hs_ctx* ctx, const hs_ct* a, int64_t k, hs_ct** out);                  /* :193 */
 int hs_bootstrap(hs_ctx* ctx, const hs_ct* a, hs_ct** out);                          /* :207 */
 int hs_sum_all_slots(hs_ctx* ctx, const hs_ct* a, uint64_t n_valid, hs_ct** out);    /* :218 */
+/* batched forms (C5 workloads, no reference counterpart: the reference issues n separate
+ * calls): out[i] = op(a[i](, b[i])) with exactly the single op's semantics per element
+ * (levels, auto-bootstrap, meter, errors in element order); one kernel per 64 ciphertexts */
+int hs_add_ct_batch(hs_ctx* ctx, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out);
+int hs_sub_ct_batch(hs_ctx* ctx, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out);
+int hs_mul_ct_batch(hs_ctx* ctx, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out);
+int hs_add_pt_batch(hs_ctx* ctx, const hs_ct* const* a, double c, uint64_t n, hs_ct** out);
+int hs_mul_pt_batch(hs_ctx* ctx, const hs_ct* const* a, double c, uint64_t n, hs_ct** out);
+int hs_rotate_batch(hs_ctx* ctx, const hs_ct* const* a, int64_t k, uint64_t n, hs_ct** out);
 
 /* ---- Chebyshev (chebyshev.hpp) --------------------------------------------- */
 double hs_scaled_target(int kind, double S, double t);                               /* :39  */

@@ -82,6 +82,12 @@ _SIGS = {
     "hs_rotate": (C.c_int, [CTX, CT, C.c_int64, PCT]),
     "hs_bootstrap": (C.c_int, [CTX, CT, PCT]),
     "hs_sum_all_slots": (C.c_int, [CTX, CT, C.c_uint64, PCT]),
+    "hs_add_ct_batch": (C.c_int, [CTX, PCT, PCT, C.c_uint64, PCT]),
+    "hs_sub_ct_batch": (C.c_int, [CTX, PCT, PCT, C.c_uint64, PCT]),
+    "hs_mul_ct_batch": (C.c_int, [CTX, PCT, PCT, C.c_uint64, PCT]),
+    "hs_add_pt_batch": (C.c_int, [CTX, PCT, C.c_double, C.c_uint64, PCT]),
+    "hs_mul_pt_batch": (C.c_int, [CTX, PCT, C.c_double, C.c_uint64, PCT]),
+    "hs_rotate_batch": (C.c_int, [CTX, PCT, C.c_int64, C.c_uint64, PCT]),
     "hs_scaled_target": (C.c_double, [C.c_int, C.c_double, C.c_double]),
     "hs_cheb_eval_depth": (C.c_int32, [C.c_int32]),
     "hs_fit": (C.c_int, [TARGET_FN, C.c_void_p, C.c_int32, C.c_double, C.c_double, DP]),

@@ -246,6 +246,39 @@ int hs_sum_all_slots(hs_ctx* c, const hs_ct* a, uint64_t n_valid, hs_ct** out) {
   HS_OP(*out = wrap(db.sum_all_slots(get(a), static_cast<size_t>(n_valid))));
 }
 
+// ---- batched ops (C5) ---------------------------------------------------------------------
+namespace {
+std::vector<Ct> gets(const hs_ct* const* a, uint64_t n) {
+  if (n) need(a, "ciphertext array");
+  std::vector<Ct> v;
+  v.reserve(n);
+  for (uint64_t i = 0; i < n; ++i) v.push_back(get(a[i]));
+  return v;
+}
+void put_all(const std::vector<Ct>& v, hs_ct** out) {
+  for (size_t i = 0; i < v.size(); ++i) out[i] = wrap(v[i]);
+}
+}  // namespace
+
+int hs_add_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_ADD), out));
+}
+int hs_sub_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_SUB), out));
+}
+int hs_mul_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_MUL), out));
+}
+int hs_add_pt_batch(hs_ctx* c, const hs_ct* const* a, double k, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.scalar_batch(gets(a, n), k, k::S_ADD), out));
+}
+int hs_mul_pt_batch(hs_ctx* c, const hs_ct* const* a, double k, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.scalar_batch(gets(a, n), k, k::S_MUL), out));
+}
+int hs_rotate_batch(hs_ctx* c, const hs_ct* const* a, int64_t k, uint64_t n, hs_ct** out) {
+  HS_OP(put_all(db.rotate_batch(gets(a, n), static_cast<long>(k)), out));
+}
+
 // ---- Chebyshev ------------------------------------------------------------------------------
 double hs_scaled_target(int kind, double S, double t) {
   return scaled_target(kind == 1 ? TargetKind::SqrtShifted : TargetKind::InvSqrtShifted, S, t);

@@ -173,6 +173,99 @@ Ct DevB::sum_all_slots(const C& a, size_t n_valid) {  // ckks.hpp:218-230
   return ct_device(o, p_.S, a->level, grid);
 }
 
+// ---- batched ops (C5) -------------------------------------------------------------------------
+std::vector<Ct> DevB::binary_batch(const std::vector<Ct>& a, const std::vector<Ct>& b, k::BinOp op) {
+  if (a.size() != b.size()) fail(HS_E_LENGTH_MISMATCH, "batch: operand counts differ");
+  const size_t n = a.size();
+  std::vector<Ct> x(a), y(b);
+  std::vector<int> lvl(n);
+  for (size_t i = 0; i < n; ++i) {  // ckks.hpp:113-164, element by element
+    check_shape(sz(x[i]));
+    check_shape(sz(y[i]));
+    if (op == k::B_MUL) {
+      if (std::min(x[i]->level, y[i]->level) < 1) {
+        if (!p_.auto_bootstrap) fail(HS_E_LEVEL_EXHAUSTED, "mul_ct: no multiplicative level left");
+        if (x[i]->level < 1) x[i] = bootstrap(x[i]);
+        if (y[i]->level < 1) y[i] = bootstrap(y[i]);
+      }
+      ++m_.mul_ct;
+      lvl[i] = std::min(x[i]->level, y[i]->level) - 1;
+    } else {
+      ++m_.add;
+      lvl[i] = std::min(x[i]->level, y[i]->level);
+    }
+  }
+  std::vector<Ct> out;
+  if (n == 0) return out;
+  Runtime& rt = Runtime::get();
+  DevBuf block = rt.alloc(n * p_.S);
+  std::vector<const double*> pa(n), pb(n);
+  std::vector<double*> po(n);
+  for (size_t i = 0; i < n; ++i) {
+    pa[i] = x[i]->device();
+    pb[i] = y[i]->device();
+    po[i] = block.get() + i * p_.S;
+  }
+  k::binary_batch(qs_, op, pa.data(), pb.data(), po.data(), n, p_.S, rt.stream());
+  for (size_t i = 0; i < n; ++i)
+    out.push_back(ct_device(DevBuf(block, po[i]), p_.S, lvl[i], p_.quantize ? p_.scale_bits : 0));
+  return out;
+}
+
+std::vector<Ct> DevB::scalar_batch(const std::vector<Ct>& a, double c, k::ScalOp op) {
+  const size_t n = a.size();
+  std::vector<Ct> x(a);
+  std::vector<int> lvl(n);
+  for (size_t i = 0; i < n; ++i) {  // ckks.hpp:137-176
+    check_shape(sz(x[i]));
+    if (op == k::S_MUL) {
+      x[i] = prepare_mul_pt(x[i]);
+      ++m_.mul_pt;
+      lvl[i] = x[i]->level - 1;
+    } else {
+      ++m_.add;
+      lvl[i] = x[i]->level;
+    }
+  }
+  std::vector<Ct> out;
+  if (n == 0) return out;
+  Runtime& rt = Runtime::get();
+  DevBuf block = rt.alloc(n * p_.S);
+  std::vector<const double*> pa(n);
+  std::vector<double*> po(n);
+  for (size_t i = 0; i < n; ++i) {
+    pa[i] = x[i]->device();
+    po[i] = block.get() + i * p_.S;
+  }
+  k::scalar_batch(qs_, op, pa.data(), c, po.data(), n, p_.S, rt.stream());
+  for (size_t i = 0; i < n; ++i)
+    out.push_back(ct_device(DevBuf(block, po[i]), p_.S, lvl[i], p_.quantize ? p_.scale_bits : 0));
+  return out;
+}
+
+std::vector<Ct> DevB::rotate_batch(const std::vector<Ct>& a, long kk) {  // ckks.hpp:193-202
+  const size_t n = a.size();
+  for (size_t i = 0; i < n; ++i) {
+    check_shape(sz(a[i]));
+    ++m_.rotate;
+  }
+  std::vector<Ct> out;
+  if (n == 0) return out;
+  const long S = static_cast<long>(p_.S);
+  const size_t shift = static_cast<size_t>(((kk % S) + S) % S);
+  Runtime& rt = Runtime::get();
+  DevBuf block = rt.alloc(n * p_.S);
+  std::vector<const double*> pa(n);
+  std::vector<double*> po(n);
+  for (size_t i = 0; i < n; ++i) {
+    pa[i] = a[i]->device();
+    po[i] = block.get() + i * p_.S;
+  }
+  k::rotate_batch(pa.data(), po.data(), n, p_.S, shift, rt.stream());
+  for (size_t i = 0; i < n; ++i) out.push_back(ct_device(DevBuf(block, po[i]), p_.S, a[i]->level, a[i]->grid));
+  return out;
+}
+
 // ---- debug-mode value checks (host reads; debug is the diagnostics path) ----
 double DevB::first_slot(const C& c) {  // stats.hpp:89-91 (decrypt(ct, 1)[0])
   double v = 0.0;

@@ -137,6 +137,13 @@ class DevB : public LedgerBase<DevB, Ct> {
   C rotate(const C& a, long k);
   C sum_all_slots(const C& a, size_t n_valid);
 
+  // Batched ops (C5): element i has exactly the single op's semantics (ledger in
+  // element order, per-element auto-bootstrap); one kernel per 64 ciphertexts,
+  // outputs are views of one allocation.
+  std::vector<C> binary_batch(const std::vector<C>& a, const std::vector<C>& b, k::BinOp op);
+  std::vector<C> scalar_batch(const std::vector<C>& a, double c, k::ScalOp op);
+  std::vector<C> rotate_batch(const std::vector<C>& a, long k);
+
   double first_slot(const C& c);
   void check_open_domain(const C& c, size_t n_valid, double lo, double hi, const char* who);
   void check_eval_domain(const C& c, double lo, double hi);

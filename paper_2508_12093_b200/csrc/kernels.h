@@ -36,6 +36,12 @@ void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s);
 // when any src value is non-finite (column.hpp:28-30 check, done on device).
 void encrypt(QSpec q, const double* src, size_t n, double* out, size_t S, int* bad, cudaStream_t s);
 void rotate(const double* a, double* out, size_t n, size_t shift, cudaStream_t s);
+// batched forms (C5 workloads): `count` independent ciphertexts, one launch per 64
+void binary_batch(QSpec q, BinOp op, const double* const* a, const double* const* b, double* const* o,
+                  size_t count, size_t n, cudaStream_t s);
+void scalar_batch(QSpec q, ScalOp op, const double* const* a, double c, double* const* o, size_t count, size_t n,
+                  cudaStream_t s);
+void rotate_batch(const double* const* a, double* const* o, size_t count, size_t n, size_t shift, cudaStream_t s);
 // sum_all_slots over `batch` ciphertexts of S slots each (a[b], out[b]).
 void slot_sum(QSpec q, const double* const* a, double* const* out, int batch, size_t S, cudaStream_t s);
 // largest S the single-launch cluster kernel handles with `arrays` concurrent sums

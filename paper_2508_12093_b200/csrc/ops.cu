@@ -22,6 +22,7 @@ namespace k {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kBatch = 64;  // ciphertexts per batched launch (pointer table passed by value)
 
 inline unsigned grid_for(size_t n_items) {
   const size_t want = (n_items + kThreads - 1) / kThreads;
@@ -107,6 +108,59 @@ __global__ void __launch_bounds__(kThreads) k_sum_step(Q q, const double* __rest
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
     o[i] = q.add(a[i], a[(i + d) & mask]);
+}
+
+// ---- batched forms (C5): blockIdx.y = ciphertext of the batch, pointers by value ----
+struct BatchPtrs {
+  const double* a[kBatch];
+  const double* b[kBatch];
+  double* o[kBatch];
+};
+
+template <class Q, int OP>
+__global__ void __launch_bounds__(kThreads) k_binary_batch(Q q, const __grid_constant__ BatchPtrs p, size_t n) {
+  const unsigned e = blockIdx.y;
+  const size_t n2 = n / 2, stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const double2* a2 = reinterpret_cast<const double2*>(p.a[e]);
+  const double2* b2 = reinterpret_cast<const double2*>(p.b[e]);
+  double2* o2 = reinterpret_cast<double2*>(p.o[e]);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+    const double2 x = __ldg(a2 + i), y = __ldg(b2 + i);
+    o2[i] = make_double2(bin<Q, OP>(q, x.x, y.x), bin<Q, OP>(q, x.y, y.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p.o[e][n - 1] = bin<Q, OP>(q, p.a[e][n - 1], p.b[e][n - 1]);
+}
+
+template <class Q, int OP>
+__global__ void __launch_bounds__(kThreads) k_scalar_batch(Q q, const __grid_constant__ BatchPtrs p, double c,
+                                                            size_t n) {
+  const unsigned e = blockIdx.y;
+  const size_t n2 = n / 2, stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const double2* a2 = reinterpret_cast<const double2*>(p.a[e]);
+  double2* o2 = reinterpret_cast<double2*>(p.o[e]);
+  auto f = [&](double x) { return OP == S_ADD ? q.addc(x, c) : q.mulc(x, c); };
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+    const double2 x = __ldg(a2 + i);
+    o2[i] = make_double2(f(x.x), f(x.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p.o[e][n - 1] = f(p.a[e][n - 1]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_rotate_batch(const __grid_constant__ BatchPtrs p, size_t n,
+                                                            size_t shift) {
+  const unsigned e = blockIdx.y;
+  const size_t mask = n - 1, stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const double* a = p.a[e];
+  double* o = p.o[e];
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    o[i] = __ldg(a + ((i + shift) & mask));
+}
+
+// x-blocks per ciphertext: ~8 grid-stride iterations per thread, at least one wave over the batch
+inline unsigned batch_gx(size_t items, size_t count) {
+  const size_t per = (items + kThreads * 8 - 1) / (kThreads * 8);
+  const size_t wave = (static_cast<size_t>(Runtime::get().sm_count()) * 8 + count - 1) / count;
+  return static_cast<unsigned>(std::max<size_t>(1, std::max(per, std::min(wave, (items + kThreads - 1) / kThreads))));
 }
 
 template <class F>
@@ -223,6 +277,63 @@ void slot_sum(QSpec q, const double* const* a, double* const* out, int batch, si
       src = bufs[w];
       w ^= 1;
     }
+  }
+}
+
+void binary_batch(QSpec q, BinOp op, const double* const* a, const double* const* b, double* const* o,
+                  size_t count, size_t n, cudaStream_t s) {
+  for (size_t base = 0; base < count; base += kBatch) {
+    const size_t m = std::min<size_t>(kBatch, count - base);
+    BatchPtrs p{};
+    for (size_t i = 0; i < m; ++i) {
+      p.a[i] = a[base + i];
+      p.b[i] = b[base + i];
+      p.o[i] = o[base + i];
+    }
+    const dim3 g(batch_gx((n + 1) / 2, m), static_cast<unsigned>(m));
+    with_q(q, [&](auto Q) {
+      using QT = decltype(Q);
+      if (op == B_ADD) k_binary_batch<QT, B_ADD><<<g, kThreads, 0, s>>>(Q, p, n);
+      else if (op == B_SUB) k_binary_batch<QT, B_SUB><<<g, kThreads, 0, s>>>(Q, p, n);
+      else k_binary_batch<QT, B_MUL><<<g, kThreads, 0, s>>>(Q, p, n);
+    });
+    cuda_ok(cudaGetLastError(), "binary batch launch");
+    Runtime::get().note_launch();
+  }
+}
+
+void scalar_batch(QSpec q, ScalOp op, const double* const* a, double c, double* const* o, size_t count, size_t n,
+                  cudaStream_t s) {
+  for (size_t base = 0; base < count; base += kBatch) {
+    const size_t m = std::min<size_t>(kBatch, count - base);
+    BatchPtrs p{};
+    for (size_t i = 0; i < m; ++i) {
+      p.a[i] = a[base + i];
+      p.o[i] = o[base + i];
+    }
+    const dim3 g(batch_gx((n + 1) / 2, m), static_cast<unsigned>(m));
+    with_q(q, [&](auto Q) {
+      using QT = decltype(Q);
+      if (op == S_ADD) k_scalar_batch<QT, S_ADD><<<g, kThreads, 0, s>>>(Q, p, c, n);
+      else k_scalar_batch<QT, S_MUL><<<g, kThreads, 0, s>>>(Q, p, c, n);
+    });
+    cuda_ok(cudaGetLastError(), "scalar batch launch");
+    Runtime::get().note_launch();
+  }
+}
+
+void rotate_batch(const double* const* a, double* const* o, size_t count, size_t n, size_t shift, cudaStream_t s) {
+  for (size_t base = 0; base < count; base += kBatch) {
+    const size_t m = std::min<size_t>(kBatch, count - base);
+    BatchPtrs p{};
+    for (size_t i = 0; i < m; ++i) {
+      p.a[i] = a[base + i];
+      p.o[i] = o[base + i];
+    }
+    const dim3 g(batch_gx(n, m), static_cast<unsigned>(m));
+    k_rotate_batch<<<g, kThreads, 0, s>>>(p, n, shift);
+    cuda_ok(cudaGetLastError(), "rotate batch launch");
+    Runtime::get().note_launch();
   }
 }
 

@@ -229,6 +229,39 @@ class EvalContext:  # ckks.hpp:83-257
     def sum_all_slots(self, a: Ciphertext, n_valid: int) -> Ciphertext:
         return _out(_abi.lib().hs_sum_all_slots, self._h, a._h, int(n_valid))
 
+    # ---- batched forms (C5): the single op's semantics per element, one launch per 64 ----
+    def _batch(self, fn, a, *rest):
+        n = len(a)
+        arr = (C.c_void_p * max(n, 1))(*[x._h.value for x in a])
+        outs = (C.c_void_p * max(n, 1))()
+        if rest and isinstance(rest[0], (list, tuple)):
+            b = rest[0]
+            if len(b) != n:
+                raise length_mismatch("batch: operand counts differ")
+            barr = (C.c_void_p * max(n, 1))(*[x._h.value for x in b])
+            _check(fn(self._h, arr, barr, n, outs))
+        else:
+            _check(fn(self._h, arr, *rest, n, outs))
+        return [Ciphertext._own(C.c_void_p(outs[i])) for i in range(n)]
+
+    def add_ct_batch(self, a, b):
+        return self._batch(_abi.lib().hs_add_ct_batch, a, list(b))
+
+    def sub_ct_batch(self, a, b):
+        return self._batch(_abi.lib().hs_sub_ct_batch, a, list(b))
+
+    def mul_ct_batch(self, a, b):
+        return self._batch(_abi.lib().hs_mul_ct_batch, a, list(b))
+
+    def add_pt_batch(self, a, c: float):
+        return self._batch(_abi.lib().hs_add_pt_batch, a, float(c))
+
+    def mul_pt_batch(self, a, c: float):
+        return self._batch(_abi.lib().hs_mul_pt_batch, a, float(c))
+
+    def rotate_batch(self, a, k: int):
+        return self._batch(_abi.lib().hs_rotate_batch, a, int(k))
+
 
 # ---- chebyshev.hpp ------------------------------------------------------------------------------
 @dataclass
