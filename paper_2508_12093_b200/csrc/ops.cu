@@ -146,14 +146,32 @@ __global__ void __launch_bounds__(kThreads) k_scalar_batch(Q q, const __grid_con
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p.o[e][n - 1] = f(p.a[e][n - 1]);
 }
 
+// out[i] = a[(i + shift) mod n], two slots per thread with 16-byte loads: an even shift
+// is an aligned double2 read; an odd one reads the aligned pair ending at i+shift and
+// takes the next slot from the neighbouring lane (shuffle); lane 31 and the last live
+// lane read it from memory.
 __global__ void __launch_bounds__(kThreads) k_rotate_batch(const __grid_constant__ BatchPtrs p, size_t n,
                                                             size_t shift) {
   const unsigned e = blockIdx.y;
-  const size_t mask = n - 1, stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t mask = n - 1, n2 = n / 2, stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const double* a = p.a[e];
-  double* o = p.o[e];
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
-    o[i] = __ldg(a + ((i + shift) & mask));
+  double2* o2 = reinterpret_cast<double2*>(p.o[e]);
+  const bool odd = shift & 1;
+  const unsigned lane = threadIdx.x & 31;
+  // grid-stride loop with a warp-uniform trip count so the shuffle sees full warps
+  for (size_t base = blockIdx.x * static_cast<size_t>(blockDim.x); base < n2; base += stride) {
+    const size_t i = base + threadIdx.x;
+    const bool live = i < n2;
+    const size_t j = (2 * i + shift - (odd ? 1 : 0)) & mask;  // even index
+    double2 v = live ? __ldg(reinterpret_cast<const double2*>(a + j)) : make_double2(0.0, 0.0);
+    if (!odd) {
+      if (live) o2[i] = v;
+      continue;
+    }
+    double nx = __shfl_down_sync(0xffffffffu, v.x, 1);
+    if ((lane == 31 || i + 1 >= n2) && live) nx = __ldg(a + ((j + 2) & mask));
+    if (live) o2[i] = make_double2(v.y, nx);
+  }
 }
 
 // x-blocks per ciphertext: ~8 grid-stride iterations per thread, at least one wave over the batch
@@ -323,6 +341,11 @@ void scalar_batch(QSpec q, ScalOp op, const double* const* a, double c, double* 
 }
 
 void rotate_batch(const double* const* a, double* const* o, size_t count, size_t n, size_t shift, cudaStream_t s) {
+  if (n < 2) {  // one slot: every rotation is the identity
+    for (size_t i = 0; i < count; ++i)
+      cuda_ok(cudaMemcpyAsync(o[i], a[i], n * sizeof(double), cudaMemcpyDeviceToDevice, s), "rotate copy");
+    return;
+  }
   for (size_t base = 0; base < count; base += kBatch) {
     const size_t m = std::min<size_t>(kBatch, count - base);
     BatchPtrs p{};
@@ -330,7 +353,7 @@ void rotate_batch(const double* const* a, double* const* o, size_t count, size_t
       p.a[i] = a[base + i];
       p.o[i] = o[base + i];
     }
-    const dim3 g(batch_gx(n, m), static_cast<unsigned>(m));
+    const dim3 g(batch_gx(n / 2, m), static_cast<unsigned>(m));
     k_rotate_batch<<<g, kThreads, 0, s>>>(p, n, shift);
     cuda_ok(cudaGetLastError(), "rotate batch launch");
     Runtime::get().note_launch();

@@ -51,7 +51,7 @@ def test_scalar_batch_equals_single(op, c):
     assert ctx.meter().as_tuple() == ref.meter().as_tuple()
 
 
-@pytest.mark.parametrize("k", [1, 2, 1024, -5, S + 3])
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 1024, 1023, -5, S - 1, S + 3])
 def test_rotate_batch_equals_single(k):
     ctx, ref = _ctx(), _ctx()
     a = _cts(ctx, 9, 4)
@@ -60,6 +60,17 @@ def test_rotate_batch_equals_single(k):
         s = ref.rotate(x, k)
         assert np.array_equal(bits(o.slots()), bits(s.slots())) and o.level() == s.level()
     assert ctx.meter().as_tuple() == ref.meter().as_tuple()
+
+
+@pytest.mark.parametrize("slots", [1, 2, 64])
+def test_rotate_batch_small(slots):
+    from paper_2508_12093_b200 import hestat as H
+    ctx = H.EvalContext(H.CkksParams(slot_count=slots))
+    a = [ctx.encrypt(np.arange(slots) + 10.0 * i) for i in range(3)]
+    for k in (0, 1, 3):
+        out = ctx.rotate_batch(a, k)
+        for o, x in zip(out, a):
+            assert np.array_equal(o.slots(), np.roll(x.slots(), -k))
 
 
 def test_batch_auto_bootstrap_per_element():
