@@ -76,18 +76,41 @@ __global__ void __launch_bounds__(kThreads) k_requant(Q q, const double* __restr
     o[i] = q.req(a[i]);
 }
 
-template <class Q>
+// encrypt (ckks.hpp:97-104): zero-pad to S, quantise, flag non-finite inputs.  `src`
+// may be host memory mapped into the device (zero-copy over PCIe): two slots per
+// thread with 16-byte reads when `src` is 16-byte aligned, so each PCIe read carries
+// more payload.
+template <class Q, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_encrypt(Q q, const double* __restrict__ src, size_t n,
                                                        double* __restrict__ o, size_t S, int* bad) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   bool nf = false;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < S; i += stride) {
-    double v = 0.0;
-    if (i < n) {
-      v = src[i];
-      nf = nf || !isfinite(v);
+  if (VEC) {
+    double2* o2 = reinterpret_cast<double2*>(o);
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < S / 2; i += stride) {
+      double2 v = make_double2(0.0, 0.0);
+      if (2 * i + 1 < n) {
+        v = *reinterpret_cast<const double2*>(src + 2 * i);
+      } else if (2 * i < n) {
+        v.x = src[2 * i];
+      }
+      nf = nf || !isfinite(v.x) || !isfinite(v.y);
+      o2[i] = make_double2(q.req(v.x), q.req(v.y));
     }
-    o[i] = q.req(v);
+    if ((S & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const double v = S - 1 < n ? src[S - 1] : 0.0;
+      nf = nf || !isfinite(v);
+      o[S - 1] = q.req(v);
+    }
+  } else {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < S; i += stride) {
+      double v = 0.0;
+      if (i < n) {
+        v = src[i];
+        nf = nf || !isfinite(v);
+      }
+      o[i] = q.req(v);
+    }
   }
   if (bad && __any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
@@ -239,7 +262,13 @@ void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s) {
 
 void encrypt(QSpec q, const double* src, size_t n, double* out, size_t S, int* bad, cudaStream_t s) {
   if (S == 0) return;
-  with_q(q, [&](auto Q) { k_encrypt<<<grid_for(S), kThreads, 0, s>>>(Q, src, n, out, S, bad); });
+  const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  with_q(q, [&](auto Q) {
+    if (vec)
+      k_encrypt<decltype(Q), true><<<grid_for((S + 1) / 2), kThreads, 0, s>>>(Q, src, n, out, S, bad);
+    else
+      k_encrypt<decltype(Q), false><<<grid_for(S), kThreads, 0, s>>>(Q, src, n, out, S, bad);
+  });
   cuda_ok(cudaGetLastError(), "encrypt launch");
   Runtime::get().note_launch();
 }

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "core.h"
+#include "kernels.h"
 
 namespace hsg {
 
@@ -155,6 +156,8 @@ void CtData::read_async(double* out, size_t count, size_t) const {
     }
   }
   Runtime& rt = Runtime::get();
+  // copy-engine DMA straight into the caller's buffer (measured faster than SM stores
+  // into host-mapped memory for 256 KiB on this box: 23.5 vs 29 us per decode call)
   cuda_ok(cudaMemcpyAsync(out, dev.get(), count * sizeof(double), cudaMemcpyDeviceToHost, rt.stream()),
           "ciphertext read");
 }
