@@ -200,13 +200,19 @@ def rns_alg_bytes(logN, L, K, dnum, level):
     }
 
 
-def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None):
+def special_primes(L, dnum, logq0=60, logq=40, logp=44):
+    """K special primes of logp bits with P >= the largest digit modulus (q_0 + alpha-1 q's)."""
+    alpha = (L + 1 + dnum - 1) // dnum
+    return -(-(logq0 + (alpha - 1) * logq) // logp)
+
+
+def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None, logp=44):
     """Device time per ciphertext of each Tier-R op (CUDA-graph replay of `reps`
     batched calls), inputs resident; returns {op: us_per_ct}, launches per op."""
     from paper_2508_12093_b200 import _abi
     from paper_2508_12093_b200 import hestat as H
     from paper_2508_12093_b200.rns import DeviceBuffer, RnsContext, RnsSpec
-    spec = RnsSpec(logN, L, K, dnum, seed=1)
+    spec = RnsSpec(logN, L, K, dnum, logp=logp, seed=1)
     c = RnsContext(spec)
     c.prepare_relin()
     c.prepare_rotation(1)
@@ -266,12 +272,12 @@ def rns_parity_small():
     return bool(ok)
 
 
-def rns_cpu_baseline(logN, L, K, dnum):
+def rns_cpu_baseline(logN, L, K, dnum, logp=44):
     """RNS oracle (plain C, 1 core) HMult+relin per ciphertext: (t(3 cts) - t(1 ct)) / 2,
     so the once-per-call key generation drops out."""
     from rns_abi import RnsOracle, Spec
     O = RnsOracle()
-    s = Spec(logN=logN, L=L, K=K, dnum=dnum, seed=1)
+    s = Spec(logN=logN, L=L, K=K, dnum=dnum, seed=1, logp=logp)
     a = np.concatenate([O.random_ct(s, L, 1 + i) for i in range(3)])
     b = np.concatenate([O.random_ct(s, L, 100 + i) for i in range(3)])
     W = 2 * (L + 1) * s.N
@@ -282,7 +288,7 @@ def rns_cpu_baseline(logN, L, K, dnum):
     t3 = time.perf_counter() - t1
     per = (t3 - (t1 - t0)) / 2
     return {"value": 1.0 / per, "unit": "HMult+relin/s", "cores": 1, "kind": "port",
-            "sample": f"RNS oracle (oracle/rns_oracle.c), N=2^{logN} L={L} K={K} dnum={dnum}: "
+            "sample": f"RNS oracle (oracle/rns_oracle.c), N=2^{logN} L={L} K={K} dnum={dnum} logp={logp}: "
                       "3 HMult+relin minus 1 (key generation excluded), single thread",
             "ms_per_op": 1e3 * per}
 
@@ -322,7 +328,8 @@ def rns_znorm(torch, stream, reps=3):
 
 
 def tier_r_section(torch, stream, batch=64, with_cpu=True):
-    logN, L, K, dnum = 16, 24, 9, 3
+    logN, L, dnum, logp = 16, 24, 3, 44
+    K = special_primes(L, dnum, logp=logp)
     peak, src = hbm_peak_gbs()
     us, launches = rns_measure(torch, stream, logN, L, K, dnum, batch)
     ab = rns_alg_bytes(logN, L, K, dnum, L)
@@ -335,7 +342,8 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
     sec = {"metric": "HMult+relin/s", "value": round(1e6 / us["mul_relin"], 1), "unit": "HMult+relin/s",
            "config": {"workload": "C5 tier R: batch of 64 random ciphertexts under seeded keys",
                       "logN": logN, "L": L, "K": K, "dnum": dnum, "level": L, "batch": batch,
-                      "word": "u64", "l2": "inputs > L2 (64 x 25.6 MiB per operand)"},
+                      "logq0": 60, "logq": 40, "logp": logp, "word": "u64",
+                      "l2": "inputs > L2 (64 x 25.6 MiB per operand)"},
            "ops": ops,
            "roofline": {"bound": "hbm", "kernel": "HMult+relin (whole op, BASELINE.md §4 bytes)",
                         "achieved": ops["mul_relin"]["achieved_gbs"], "peak": peak, "unit": "GB/s",
@@ -344,7 +352,7 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
            "parity_vs_oracle": rns_parity_small(),
            "znorm": rns_znorm(torch, stream)}
     if with_cpu:
-        sec["cpu_baseline"] = rns_cpu_baseline(logN, L, K, dnum)
+        sec["cpu_baseline"] = rns_cpu_baseline(logN, L, K, dnum, logp)
     return sec
 
 
@@ -424,11 +432,11 @@ def c5_sweep(args):
     for logN in (14, 15, 16):
         for L in (8, 16, 24, 32):
             dnum = 3
-            K = (L + 1 + dnum - 1) // dnum
+            K = special_primes(L, dnum)
             us, launches = rns_measure(torch, stream, logN, L, K, dnum, args.batch)
             ab = rns_alg_bytes(logN, L, K, dnum, L)
             ab["intt"] = ab["ntt"]
-            line = {"sweep": "C5 tier R", "logN": logN, "L": L, "K": K, "dnum": dnum, "batch": args.batch,
+            line = {"sweep": "C5 tier R", "logN": logN, "L": L, "K": K, "dnum": dnum, "logp": 44, "batch": args.batch,
                     "peak_gbs": peak, "ops": {k: {"us_per_ct": round(v, 2), "ops_per_s": round(1e6 / v, 1),
                                                   "hbm_frac": round(ab[k] / (v * 1e-6) / 1e9 / peak, 4)}
                                               for k, v in us.items()}}

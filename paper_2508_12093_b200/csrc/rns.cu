@@ -20,6 +20,7 @@
 #include "rns.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -199,13 +200,13 @@ __device__ __forceinline__ void ntt_steps(const uint64_t* gin, uint64_t* gout, u
   }
 }
 
-// ---- FP64 path for primes below 2^42 (the 40-bit q_i) ------------------------------
+// ---- FP64 path for primes below 2^45 (40-bit q_i, <= 44-bit special primes) --------
 // Residues are carried as exact integers in fp64 registers.  A twiddle product
 // y*w mod q is hi = fl(y w), lo = fma(y, w, -hi) (exact), k = rint(hi / q) (magic
 // constant), r = fma(-k, q, hi) + lo: every step is exact because all values are
-// integers below 2^53, and |r| < 1.1 q.  Forward (Cooley-Tukey) outputs X +- T grow
-// by at most 1.1 q per stage (< 19 q after 16 stages), so no reduction is needed
-// inside a pass; inverse (Gentleman-Sande) sums double per stage and are folded
+// integers below 2^53, and |r| < 1.5 q.  Forward (Cooley-Tukey) outputs X +- T grow
+// by at most 1.5 q per stage (< 26 q < 2^49.7 after 16 stages, so hi/q stays inside
+// the magic constant's 2^51 range), so no reduction is needed inside a pass; inverse (Gentleman-Sande) sums double per stage and are folded
 // back below 0.6 q after every radix step.  Pass outputs are canonical u64.  The
 // arithmetic runs on the FP64 pipe, leaving the integer ALU (the bottleneck of the
 // 64-bit Shoup path) to addressing.  Results are identical: the NTT of canonical
@@ -380,6 +381,16 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
     k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd);
   }
 }
+
+}  // namespace
+}  // namespace rns
+}  // namespace hsg
+
+#include "ntt_cluster.cuh"
+
+namespace hsg {
+namespace rns {
+namespace {
 
 // ---------------------------------------------------------------- sampling / keys
 __global__ void k_random_ct(uint64_t* out, const PrimeC* pcs, uint64_t seed, uint64_t tag, uint32_t nl,
@@ -808,6 +819,19 @@ std::vector<uint32_t> iota_rows(uint32_t n, uint32_t first = 0) {
 }  // namespace
 
 // ================================================================== NTT launch
+namespace {
+// The single-pass cluster NTT (ntt_cluster.cuh) halves HBM traffic but measured slower
+// than the two-pass kernels (38 vs 31 us per ciphertext NTT at N=2^16, L=24: cluster
+// barriers and DSMEM latency, 33 co-resident clusters); opt-in with HS_NTT_CLUSTER=1.
+bool use_cluster_ntt(uint32_t logN) {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_NTT_CLUSTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0 && logN >= 14 && logN <= 16;
+}
+}  // namespace
+
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
               const std::vector<uint32_t>& primes, uint32_t batch, bool inverse) {
@@ -825,6 +849,15 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
       rm.irow[i] = static_cast<uint16_t>(irows[base + i]);
       rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
       rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
+    }
+    if (use_cluster_ntt(logN)) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
+      switch (logN) {
+        case 14: launch_ntt_cluster<14>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
+        case 15: launch_ntt_cluster<15>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
+        default: launch_ntt_cluster<16>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
+      }
+      rt.note_launch(1);
+      continue;
     }
     switch (logN) {
 #define HS_NTT_CASE(L) \
@@ -899,7 +932,7 @@ Ctx::Ctx(const Spec& s) : spec(s) {
     p.r64_sh = shoup_of(p.r64, q);
     p.ninv = h_inv(N % q, q);
     p.ninv_sh = shoup_of(p.ninv, q);
-    p.fp = q < (1ULL << 42) ? 1u : 0u;
+    p.fp = q < (1ULL << 45) ? 1u : 0u;
     p.qd = static_cast<double>(q);
     p.qinvd = 1.0 / static_cast<double>(q);
     pc.push_back(p);

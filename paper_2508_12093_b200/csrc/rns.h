@@ -48,7 +48,7 @@ struct PrimeC {
   uint64_t ninv, ninv_sh;
   double qd, qinvd;  // q and 1/q in fp64 (FP64 NTT path)
   uint32_t k;        // bitlen(q)
-  uint32_t fp;       // 1: q < 2^42, NTT on the FP64 pipe (rns.cu)
+  uint32_t fp;       // 1: q < 2^45, NTT on the FP64 pipe (rns.cu)
 };
 
 __host__ __device__ inline uint64_t shoup_of(uint64_t w, uint64_t q) {
@@ -105,7 +105,7 @@ class Ctx {
   std::vector<PrimeC> pc;         // host copy
   DevBuf d_pc;                    // PrimeC[np] (reinterpreted)
   DevBuf d_tw;                    // [np][4][N]: psi_rev, psi_rev', ipsi_rev, ipsi_rev'
-  DevBuf d_twd;                   // [np][2][N]: psi_rev, ipsi_rev as fp64 (primes < 2^42)
+  DevBuf d_twd;                   // [np][2][N]: psi_rev, ipsi_rev as fp64 (primes < 2^45)
   DevBuf d_sk;                    // [np][N] secret, NTT form
   std::mutex key_mu;
 

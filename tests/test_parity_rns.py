@@ -21,6 +21,7 @@ SHAPES = [
     Spec(logN=12, L=7, K=3, dnum=3, seed=11),     # alpha=3: partial last digit
     Spec(logN=13, L=4, K=1, dnum=5, seed=3),      # alpha=1, K=1
     Spec(logN=12, L=5, K=3, dnum=3, seed=8, h=64),  # sparse secret (~64 nonzeros)
+    Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44),  # 44-bit special primes: FP64 NTT path at its bound
 ]
 
 
@@ -52,9 +53,10 @@ def test_primes_and_secret(s):
         assert np.array_equal(c.secret(), O.secret(s))
 
 
-@pytest.mark.parametrize("logN", [9, 10, 11, 12, 13, 14, 15, 16, 17])
-def test_ntt_matches_oracle(logN):
-    s = Spec(logN=logN, L=2, K=1, dnum=1, seed=5)
+@pytest.mark.parametrize("logN,logp", [(9, 61), (10, 61), (11, 61), (12, 61), (13, 61), (14, 61), (15, 61),
+                                        (16, 61), (17, 61), (16, 44), (17, 44)])
+def test_ntt_matches_oracle(logN, logp):
+    s = Spec(logN=logN, L=2, K=1, dnum=1, seed=5, logp=logp)
     c = ctx(s)
     primes = O.primes(s)
     rng = np.random.default_rng(logN)
@@ -79,8 +81,9 @@ def test_ntt_matches_oracle(logN):
         assert np.array_equal(got[i], O.ntt(s, i, a[i], inverse=True))
 
 
-def test_ntt_extreme_values():
-    s = Spec(logN=12, L=1, K=1, dnum=1, seed=5)
+@pytest.mark.parametrize("logp", [61, 44])
+def test_ntt_extreme_values(logp):
+    s = Spec(logN=16, L=1, K=1, dnum=1, seed=5, logp=logp)
     c = ctx(s)
     primes = O.primes(s)
     for fill in ("zero", "qm1", "one"):
@@ -180,3 +183,32 @@ def test_full_size_north_star():
     assert np.array_equal(c.mul_relin(level, da, db).download(), O.mul_relin(s, level, a, b))
     assert np.array_equal(c.rescale(level, da).download(), O.rescale(s, level, a))
     assert np.array_equal(c.rotate(level, 1, da).download(), O.rotate(s, level, 1, a))
+
+
+def test_cluster_ntt_option_matches_oracle():
+    """The opt-in single-pass cluster NTT (HS_NTT_CLUSTER=1) gives the same limbs."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from rns_abi import RnsOracle, Spec
+from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
+O = RnsOracle()
+for logN, logp in ((14, 61), (15, 44), (16, 44), (16, 61)):
+    s = Spec(logN=logN, L=3, K=2, dnum=2, seed=6, logp=logp)
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
+    a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
+    got = c.mul_relin(s.L, DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)).download()
+    assert np.array_equal(got, O.mul_relin(s, s.L, a, b)), logN
+    x = DeviceBuffer(a.size).upload(a)
+    c.ntt(x, 0, s.L + 1, batch=2, inverse=True)
+    c.ntt(x, 0, s.L + 1, batch=2)
+    assert np.array_equal(x.download(), a), logN
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_NTT_CLUSTER": "1"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

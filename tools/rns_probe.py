@@ -46,7 +46,7 @@ def main():
     ap.add_argument("--K", type=int, default=9)
     ap.add_argument("--dnum", type=int, default=3)
     ap.add_argument("--batch", type=int, default=8)
-    ap.add_argument("--logp", type=int, default=61)
+    ap.add_argument("--logp", type=int, default=44)
     ap.add_argument("--peak", type=float, default=6.5456e12)
     a = ap.parse_args()
     spec = RnsSpec(a.logN, a.L, a.K, a.dnum, logp=a.logp, seed=1)
