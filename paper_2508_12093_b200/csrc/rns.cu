@@ -11,8 +11,9 @@
 //   inner        sum_j ModUp(d_j) * key_j; each thread keeps its key words in
 //                registers and loops over the batch, so the key streams from HBM
 //                once per call instead of once per ciphertext.
-//   ModDown      in-place iNTT of the P rows, base conversion P -> Q_l, NTT, then
-//                (acc - conv) * P^-1 (+ d0/d1 for HMult, + sigma(c0) for rotate).
+//   ModDown      in-place iNTT of the P rows, base conversion P -> Q_l, NTT whose last
+//                pass applies (acc - conv) * P^-1 (+ d0/d1 for HMult, + sigma(c0) for
+//                rotate) instead of storing the converted rows.
 //   rescale      iNTT of the last limb, reduce into q_i, NTT, (c_i - t_i) q_l^-1.
 //   automorph    NTT-domain Galois permutation for 5^k.
 // Every kernel takes its batch index from blockIdx.z.  Ring sizes are powers of
@@ -72,6 +73,36 @@ constexpr uint32_t kNTile = 1u << kLogTile;
 // makes every store/load pattern of every radix step (logN 10..17, forward and
 // inverse) hit 16 distinct 8-byte bank slots per half-warp (exhaustively checked
 // offline against the step access patterns below).
+// Where the last NTT step puts a canonical output word: straight to HBM, or (ModDown
+// epilogue of key switching) out = (acc - v) * P^-1 (+ add) without materialising v.
+struct PlainStore {
+  uint64_t* g;
+  __device__ void operator()(size_t off, uint64_t v) const { g[off] = v; }
+};
+
+struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
+  const uint64_t* acc;
+  const uint64_t* add0;
+  const uint64_t* add1;
+  uint64_t* out;
+  const uint64_t* pinv;
+  const uint64_t* pinv_sh;
+  size_t acc_stride, add_stride, out_stride;
+  uint32_t nl, nx;
+};
+
+struct MdStore {
+  const uint64_t* acc;  // acc_w row i (this tile)
+  const uint64_t* add;  // add_w row i (this tile) or null
+  uint64_t* out;        // out_w row i (this tile)
+  uint64_t q, pinv, pinv_sh;
+  __device__ void operator()(size_t off, uint64_t v) const {
+    uint64_t r = mul_shoup(sub_mod(acc[off], v, q), pinv, pinv_sh, q);
+    if (add) r = add_mod(r, add[off], q);
+    out[off] = r;
+  }
+};
+
 __device__ __forceinline__ uint32_t swz(uint32_t u) { return u ^ (((u >> 2) ^ (u >> 3)) & 15u); }
 
 template <int LOGN, bool ROWS>
@@ -84,8 +115,8 @@ struct NttGeom {
 };
 
 // One radix-2^RB step (stages DONE .. DONE+RB-1 of this pass) for every group of the tile.
-template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST>
-__device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint64_t* __restrict__ gout,
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class ST>
+__device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, const ST& gout,
                                          uint64_t* __restrict__ sm, const uint64_t* __restrict__ psi,
                                          const uint64_t* __restrict__ psip, uint64_t q, uint32_t tile0,
                                          uint64_t ninv, uint64_t ninv_sh) {
@@ -169,10 +200,7 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint6
         } else if (!ROWS) {
           v = mul_shoup(v, ninv, ninv_sh, q);
         }
-        if (ROWS)
-          gout[(size_t(tr) << logC) + e] = v;
-        else
-          gout[(size_t(e) << logC) + tr] = v;
+        gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr, v);
       } else {
         if (ROWS)
           sm[swz((tr << logR) + e)] = v;
@@ -185,8 +213,8 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, uint6
 
 // All steps of a pass, unrolled at compile time: radix-8 steps, with the
 // remainder taken as radix-4 (a 4-stage tail becomes 2 + 2).
-template <bool INV, bool ROWS, int LOGN, int DONE>
-__device__ __forceinline__ void ntt_steps(const uint64_t* gin, uint64_t* gout, uint64_t* sm, const uint64_t* psi,
+template <bool INV, bool ROWS, int LOGN, int DONE, class ST>
+__device__ __forceinline__ void ntt_steps(const uint64_t* gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
                                           const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
                                           uint64_t ninv_sh) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
@@ -194,9 +222,9 @@ __device__ __forceinline__ void ntt_steps(const uint64_t* gin, uint64_t* gout, u
     constexpr int rem = logR - DONE;
     constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
     if constexpr (DONE > 0) __syncthreads();
-    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR>(gin, gout, sm, psi, psip, q, tile0, ninv,
-                                                                      ninv_sh);
-    ntt_steps<INV, ROWS, LOGN, DONE + RB>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
+    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, ST>(gin, gout, sm, psi, psip, q, tile0, ninv,
+                                                                          ninv_sh);
+    ntt_steps<INV, ROWS, LOGN, DONE + RB, ST>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
   }
 }
 
@@ -236,8 +264,8 @@ __device__ __forceinline__ uint64_t fp_canon(double x, double q, double qinv) {
   return d2u(r);
 }
 
-template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST>
-__device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, uint64_t* __restrict__ gout,
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class ST>
+__device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
                                             double qinv, uint32_t tile0, double ninv) {
   using G = NttGeom<LOGN, ROWS>;
@@ -313,11 +341,7 @@ __device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, ui
       const uint32_t e = j0 + (uint32_t(k) << logs);
       if (LAST) {
         const double v = (INV && !ROWS) ? fp_mulmod(x[k], ninv, q, qinv) : x[k];
-        const uint64_t u = fp_canon(v, q, qinv);
-        if (ROWS)
-          gout[(size_t(tr) << logC) + e] = u;
-        else
-          gout[(size_t(e) << logC) + tr] = u;
+        gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr, fp_canon(v, q, qinv));
       } else {
         if (ROWS)
           sm[swz((tr << logR) + e)] = x[k];
@@ -328,26 +352,28 @@ __device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, ui
   }
 }
 
-template <bool INV, bool ROWS, int LOGN, int DONE>
-__device__ __forceinline__ void ntt_steps_fp(const uint64_t* gin, uint64_t* gout, double* sm, const double* tw,
+template <bool INV, bool ROWS, int LOGN, int DONE, class ST>
+__device__ __forceinline__ void ntt_steps_fp(const uint64_t* gin, const ST& gout, double* sm, const double* tw,
                                              double q, double qinv, uint32_t tile0, double ninv) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
     if constexpr (DONE > 0) __syncthreads();
-    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR>(gin, gout, sm, tw, q, qinv, tile0, ninv);
-    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB>(gin, gout, sm, tw, q, qinv, tile0, ninv);
+    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, ST>(gin, gout, sm, tw, q, qinv, tile0,
+                                                                             ninv);
+    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, ST>(gin, gout, sm, tw, q, qinv, tile0, ninv);
   }
 }
 
 // Forward: columns then rows; inverse: rows then columns.  Reads `in`, writes
 // `out` (may alias: every block reads its whole tile before its last step writes).
 // 3 blocks of 512 threads per SM (40 registers): measured 1.3x over 2 blocks.
-template <bool INV, bool ROWS, int LOGN>
+template <bool INV, bool ROWS, int LOGN, bool EPI = false>
 __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                   size_t out_stride, const __grid_constant__ RowMap rm,
-                                                  const PrimeC* pcs, const uint64_t* tw, const double* twd) {
+                                                  const PrimeC* pcs, const uint64_t* tw, const double* twd,
+                                                  const __grid_constant__ MdEpi epi) {
   using G = NttGeom<LOGN, ROWS>;
   __shared__ uint64_t sm[kNTile];
   constexpr uint32_t N = 1u << LOGN;
@@ -359,26 +385,47 @@ __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t 
   const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
   const uint64_t* gi = in + blockIdx.z * in_stride + (size_t(rm.irow[blockIdx.y]) << LOGN) + toff;
   uint64_t* go = out + blockIdx.z * out_stride + (size_t(rm.orow[blockIdx.y]) << LOGN) + toff;
-  if (P.fp)
-    ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, go, reinterpret_cast<double*>(sm), twd + size_t(pi) * 2 * N + (INV ? N : 0),
-                                     P.qd, P.qinvd, tile0, static_cast<double>(P.ninv));
-  else
-    ntt_steps<INV, ROWS, LOGN, 0>(gi, go, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+  const double* twp = twd + size_t(pi) * 2 * N + (INV ? N : 0);
+  if constexpr (EPI) {  // row r = w * nl + i of the ModDown conversion output
+    const uint32_t r = rm.orow[blockIdx.y], w = r / epi.nl, i = r - w * epi.nl;
+    const uint64_t* ad = w == 0 ? epi.add0 : epi.add1;
+    MdStore st{epi.acc + blockIdx.z * epi.acc_stride + (size_t(w * epi.nx + i) << LOGN) + toff,
+               ad ? ad + blockIdx.z * epi.add_stride + (size_t(i) << LOGN) + toff : nullptr,
+               epi.out + blockIdx.z * epi.out_stride + (size_t(w * epi.nl + i) << LOGN) + toff,
+               P.q, epi.pinv[i], epi.pinv_sh[i]};
+    if (P.fp)
+      ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
+                                       static_cast<double>(P.ninv));
+    else
+      ntt_steps<INV, ROWS, LOGN, 0>(gi, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+  } else {
+    const PlainStore st{go};
+    if (P.fp)
+      ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
+                                       static_cast<double>(P.ninv));
+    else
+      ntt_steps<INV, ROWS, LOGN, 0>(gi, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+  }
 }
 
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
-                const double* twd, cudaStream_t s) {
+                const double* twd, cudaStream_t s, const MdEpi* epi) {
   using Gc = NttGeom<LOGN, false>;
   using Gr = NttGeom<LOGN, true>;
   const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch), gr(1u << (Gr::logR1 - Gr::logTPB), n, batch);
+  const MdEpi none{};
   if (!inverse) {
-    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd);
-    k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd);
+    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
+    if (epi)
+      k_ntt_pass<false, true, LOGN, true><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd,
+                                                              *epi);
+    else
+      k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
   } else {
-    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd);
-    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd);
+    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
+    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
   }
 }
 
@@ -697,27 +744,6 @@ __global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext
   }
 }
 
-// out_w[i] = (acc_w[i] - conv_w[i]) * pinv_i (+ add_w[i] when given)
-__global__ void k_moddown(const uint64_t* acc, const uint64_t* conv, const uint64_t* add0, const uint64_t* add1,
-                          uint64_t* out, const PrimeC* pcs, const uint64_t* pinv, const uint64_t* pinv_sh, uint32_t nl,
-                          uint32_t nx, uint32_t logN, size_t acc_stride, size_t conv_stride, size_t add_stride,
-                          size_t out_stride) {
-  const uint64_t* A = acc + blockIdx.z * acc_stride;
-  const uint64_t* Cv = conv + blockIdx.z * conv_stride;
-  uint64_t* O = out + blockIdx.z * out_stride;
-  const size_t half = size_t(nl) << logN;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * half; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t w = x >= half;
-    const size_t r = x - (w ? half : 0);
-    const uint32_t i = r >> logN;
-    const uint64_t q = pcs[i].q;
-    uint64_t v = mul_shoup(sub_mod(A[(size_t(w * nx) << logN) + r], Cv[x], q), pinv[i], pinv_sh[i], q);
-    const uint64_t* ad = w == 0 ? add0 : add1;
-    if (ad) v = add_mod(v, ad[blockIdx.z * add_stride + r], q);
-    O[x] = v;
-  }
-}
-
 // ---------------------------------------------------------------- rescale
 // t[p][i][n] = last[p][n] mod q_i (the last limb, coefficient form, replicated into every q_i)
 __global__ void k_rescale_spread(const uint64_t* last, uint64_t* t, const PrimeC* pcs, uint32_t level, uint32_t logN,
@@ -834,7 +860,8 @@ bool use_cluster_ntt(uint32_t logN) {
 
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
-              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse) {
+              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue) {
+  const MdEpi* epi = static_cast<const MdEpi*>(epilogue);
   if (irows.empty() || batch == 0) return;
   if (irows.size() != orows.size() || irows.size() != primes.size()) fail(HS_E_INVALID_ARG, "ntt_rows: size mismatch");
   Runtime& rt = Runtime::get();
@@ -850,7 +877,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
       rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
       rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
     }
-    if (use_cluster_ntt(logN)) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
+    if (use_cluster_ntt(logN) && !epi) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
       switch (logN) {
         case 14: launch_ntt_cluster<14>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
         case 15: launch_ntt_cluster<15>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
@@ -862,7 +889,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
     switch (logN) {
 #define HS_NTT_CASE(L) \
   case L:              \
-    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s); \
+    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s, epi); \
     break;
       HS_NTT_CASE(9) HS_NTT_CASE(10) HS_NTT_CASE(11) HS_NTT_CASE(12) HS_NTT_CASE(13) HS_NTT_CASE(14)
       HS_NTT_CASE(15) HS_NTT_CASE(16) HS_NTT_CASE(17)
@@ -1370,12 +1397,12 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
   ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);
   launch_conv(c.spec.K, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), 2, c, batch);
-  ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv_rows, P.cv_rows, P.cv_primes, batch, false);
-  k_moddown<<<dim3(grid_of(size_t(2) * nl * N), 1, batch), kT, 0, s>>>(
-      ACC, CV, add0, add1, out, c.dpc(), dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh), nl, nx, logN,
-      acc_stride, cv_stride, add_stride, out_stride);
+  // NTT of the converted rows with the ModDown combine fused into its last pass:
+  // out_w = (acc_w - conv_w) * P^-1 (+ add_w), conv_w never stored
+  const MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh),
+                  acc_stride, add_stride, out_stride, nl, nx};
+  ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv_rows, P.cv_rows, P.cv_primes, batch, false, &epi);
   cuda_ok(cudaGetLastError(), "key switch");
-  rt.note_launch(2);
 }
 
 }  // namespace
