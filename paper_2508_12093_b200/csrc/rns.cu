@@ -14,7 +14,8 @@
 //   ModDown      in-place iNTT of the P rows, base conversion P -> Q_l, NTT whose last
 //                pass applies (acc - conv) * P^-1 (+ d0/d1 for HMult, + sigma(c0) for
 //                rotate) instead of storing the converted rows.
-//   rescale      iNTT of the last limb, reduce into q_i, NTT, (c_i - t_i) q_l^-1.
+//   rescale      iNTT of the last limb; one NTT over the remaining limbs whose column
+//                pass loads [c_l]_{q_i} and whose row pass stores (c_i - t_i) q_l^-1.
 //   automorph    NTT-domain Galois permutation for 5^k.
 // Every kernel takes its batch index from blockIdx.z.  Ring sizes are powers of
 // two: all index arithmetic is shifts and masks.
@@ -80,6 +81,34 @@ struct PlainStore {
   __device__ void operator()(size_t off, uint64_t v) const { g[off] = v; }
 };
 
+struct PlainLoad {
+  const uint64_t* g;
+  __device__ uint64_t operator()(size_t off) const { return g[off]; }
+};
+
+struct RsLoad {  // rescale: [c_l]_{q_i} read straight from the coefficient-form last limb
+  const uint64_t* last;
+  PrimeC P;
+  __device__ uint64_t operator()(size_t off) const { return reduce64(last[off], P); }
+};
+
+struct RsStore {  // rescale: out = (c_i - NTT([c_l]_{q_i})) * q_l^-1
+  const uint64_t* in;
+  uint64_t* out;
+  uint64_t q, qinv, qinv_sh;
+  __device__ void operator()(size_t off, uint64_t v) const { out[off] = mul_shoup(sub_mod(in[off], v, q), qinv, qinv_sh, q); }
+};
+
+struct RsEpi {  // the rescale's spread and combine fused into its NTT passes
+  const uint64_t* last;
+  const uint64_t* in;
+  uint64_t* out;
+  const uint64_t* qinv;
+  const uint64_t* qinv_sh;
+  size_t last_stride, in_stride, out_stride;
+  uint32_t level;
+};
+
 struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
   const uint64_t* acc;
   const uint64_t* add0;
@@ -115,8 +144,8 @@ struct NttGeom {
 };
 
 // One radix-2^RB step (stages DONE .. DONE+RB-1 of this pass) for every group of the tile.
-template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class ST>
-__device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, const ST& gout,
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST>
+__device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
                                          uint64_t* __restrict__ sm, const uint64_t* __restrict__ psi,
                                          const uint64_t* __restrict__ psip, uint64_t q, uint32_t tile0,
                                          uint64_t ninv, uint64_t ninv_sh) {
@@ -146,7 +175,7 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, const
     for (int k = 0; k < (1 << RB); ++k) {
       const uint32_t e = j0 + (uint32_t(k) << logs);
       if (FIRST)
-        x[k] = ROWS ? gin[(size_t(tr) << logC) + e] : gin[(size_t(e) << logC) + tr];
+        x[k] = gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr);
       else
         x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
     }
@@ -213,8 +242,8 @@ __device__ __forceinline__ void ntt_step(const uint64_t* __restrict__ gin, const
 
 // All steps of a pass, unrolled at compile time: radix-8 steps, with the
 // remainder taken as radix-4 (a 4-stage tail becomes 2 + 2).
-template <bool INV, bool ROWS, int LOGN, int DONE, class ST>
-__device__ __forceinline__ void ntt_steps(const uint64_t* gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
+template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST>
+__device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
                                           const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
                                           uint64_t ninv_sh) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
@@ -222,9 +251,9 @@ __device__ __forceinline__ void ntt_steps(const uint64_t* gin, const ST& gout, u
     constexpr int rem = logR - DONE;
     constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
     if constexpr (DONE > 0) __syncthreads();
-    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, ST>(gin, gout, sm, psi, psip, q, tile0, ninv,
-                                                                          ninv_sh);
-    ntt_steps<INV, ROWS, LOGN, DONE + RB, ST>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
+    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, psi, psip, q, tile0,
+                                                                              ninv, ninv_sh);
+    ntt_steps<INV, ROWS, LOGN, DONE + RB, LD, ST>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
   }
 }
 
@@ -264,8 +293,8 @@ __device__ __forceinline__ uint64_t fp_canon(double x, double q, double qinv) {
   return d2u(r);
 }
 
-template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class ST>
-__device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, const ST& gout,
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST>
+__device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
                                             double qinv, uint32_t tile0, double ninv) {
   using G = NttGeom<LOGN, ROWS>;
@@ -293,7 +322,7 @@ __device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, co
     for (int k = 0; k < (1 << RB); ++k) {
       const uint32_t e = j0 + (uint32_t(k) << logs);
       if (FIRST)
-        x[k] = u2d(ROWS ? gin[(size_t(tr) << logC) + e] : gin[(size_t(e) << logC) + tr]);
+        x[k] = u2d(gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr));
       else
         x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
     }
@@ -352,28 +381,35 @@ __device__ __forceinline__ void ntt_step_fp(const uint64_t* __restrict__ gin, co
   }
 }
 
-template <bool INV, bool ROWS, int LOGN, int DONE, class ST>
-__device__ __forceinline__ void ntt_steps_fp(const uint64_t* gin, const ST& gout, double* sm, const double* tw,
+template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST>
+__device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, double* sm, const double* tw,
                                              double q, double qinv, uint32_t tile0, double ninv) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
     if constexpr (DONE > 0) __syncthreads();
-    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, ST>(gin, gout, sm, tw, q, qinv, tile0,
-                                                                             ninv);
-    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, ST>(gin, gout, sm, tw, q, qinv, tile0, ninv);
+    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, tw, q, qinv, tile0,
+                                                                                 ninv);
+    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST>(gin, gout, sm, tw, q, qinv, tile0, ninv);
   }
 }
 
 // Forward: columns then rows; inverse: rows then columns.  Reads `in`, writes
 // `out` (may alias: every block reads its whole tile before its last step writes).
 // 3 blocks of 512 threads per SM (40 registers): measured 1.3x over 2 blocks.
-template <bool INV, bool ROWS, int LOGN, bool EPI = false>
+// MODE 0: plain; 1: ModDown epilogue (forward row pass); 2: rescale spread as the
+// load of the forward column pass; 3: rescale combine as the store of the row pass.
+struct PassEpi {
+  MdEpi md;
+  RsEpi rs;
+};
+
+template <bool INV, bool ROWS, int LOGN, int MODE = 0>
 __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                   size_t out_stride, const __grid_constant__ RowMap rm,
                                                   const PrimeC* pcs, const uint64_t* tw, const double* twd,
-                                                  const __grid_constant__ MdEpi epi) {
+                                                  const __grid_constant__ PassEpi epi) {
   using G = NttGeom<LOGN, ROWS>;
   __shared__ uint64_t sm[kNTile];
   constexpr uint32_t N = 1u << LOGN;
@@ -386,41 +422,57 @@ __global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t 
   const uint64_t* gi = in + blockIdx.z * in_stride + (size_t(rm.irow[blockIdx.y]) << LOGN) + toff;
   uint64_t* go = out + blockIdx.z * out_stride + (size_t(rm.orow[blockIdx.y]) << LOGN) + toff;
   const double* twp = twd + size_t(pi) * 2 * N + (INV ? N : 0);
-  if constexpr (EPI) {  // row r = w * nl + i of the ModDown conversion output
-    const uint32_t r = rm.orow[blockIdx.y], w = r / epi.nl, i = r - w * epi.nl;
-    const uint64_t* ad = w == 0 ? epi.add0 : epi.add1;
-    MdStore st{epi.acc + blockIdx.z * epi.acc_stride + (size_t(w * epi.nx + i) << LOGN) + toff,
-               ad ? ad + blockIdx.z * epi.add_stride + (size_t(i) << LOGN) + toff : nullptr,
-               epi.out + blockIdx.z * epi.out_stride + (size_t(w * epi.nl + i) << LOGN) + toff,
-               P.q, epi.pinv[i], epi.pinv_sh[i]};
+  auto run = [&](const auto& ld, const auto& st) {
     if (P.fp)
-      ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
+      ntt_steps_fp<INV, ROWS, LOGN, 0>(ld, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
                                        static_cast<double>(P.ninv));
     else
-      ntt_steps<INV, ROWS, LOGN, 0>(gi, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+      ntt_steps<INV, ROWS, LOGN, 0>(ld, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+  };
+  if constexpr (MODE == 1) {  // row r = w * nl + i of the ModDown conversion output
+    const MdEpi& e = epi.md;
+    const uint32_t r = rm.orow[blockIdx.y], w = r / e.nl, i = r - w * e.nl;
+    const uint64_t* ad = w == 0 ? e.add0 : e.add1;
+    const MdStore st{e.acc + blockIdx.z * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff,
+                     ad ? ad + blockIdx.z * e.add_stride + (size_t(i) << LOGN) + toff : nullptr,
+                     e.out + blockIdx.z * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff, P.q, e.pinv[i],
+                     e.pinv_sh[i]};
+    run(PlainLoad{gi}, st);
+  } else if constexpr (MODE == 2) {  // row r = p * level + i: [last_p]_{q_i}
+    const RsEpi& e = epi.rs;
+    const uint32_t r = rm.orow[blockIdx.y], p = r / e.level;
+    run(RsLoad{e.last + blockIdx.z * e.last_stride + (size_t(p) << LOGN) + toff, P}, PlainStore{go});
+  } else if constexpr (MODE == 3) {
+    const RsEpi& e = epi.rs;
+    const uint32_t r = rm.orow[blockIdx.y], p = r / e.level, i = r - p * e.level;
+    const RsStore st{e.in + blockIdx.z * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
+                     e.out + blockIdx.z * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
+                     e.qinv_sh[i]};
+    run(PlainLoad{gi}, st);
   } else {
-    const PlainStore st{go};
-    if (P.fp)
-      ntt_steps_fp<INV, ROWS, LOGN, 0>(gi, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
-                                       static_cast<double>(P.ninv));
-    else
-      ntt_steps<INV, ROWS, LOGN, 0>(gi, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+    run(PlainLoad{gi}, PlainStore{go});
   }
 }
 
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
-                const double* twd, cudaStream_t s, const MdEpi* epi) {
+                const double* twd, cudaStream_t s, const MdEpi* md, const RsEpi* rs) {
   using Gc = NttGeom<LOGN, false>;
   using Gr = NttGeom<LOGN, true>;
   const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch), gr(1u << (Gr::logR1 - Gr::logTPB), n, batch);
-  const MdEpi none{};
+  PassEpi none{}, ep{};
+  if (md) ep.md = *md;
+  if (rs) ep.rs = *rs;
   if (!inverse) {
-    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
-    if (epi)
-      k_ntt_pass<false, true, LOGN, true><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd,
-                                                              *epi);
+    if (rs)
+      k_ntt_pass<false, false, LOGN, 2><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
+    else
+      k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
+    if (md)
+      k_ntt_pass<false, true, LOGN, 1><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+    else if (rs)
+      k_ntt_pass<false, true, LOGN, 3><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
     else
       k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
   } else {
@@ -745,32 +797,6 @@ __global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext
 }
 
 // ---------------------------------------------------------------- rescale
-// t[p][i][n] = last[p][n] mod q_i (the last limb, coefficient form, replicated into every q_i)
-__global__ void k_rescale_spread(const uint64_t* last, uint64_t* t, const PrimeC* pcs, uint32_t level, uint32_t logN,
-                                 size_t last_stride, size_t t_stride) {
-  const size_t per = size_t(level) << logN;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * per; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = x >= per;
-    const size_t r = x - (p ? per : 0);
-    const uint32_t i = r >> logN, n = r & ((1u << logN) - 1);
-    t[blockIdx.z * t_stride + x] = reduce64(last[blockIdx.z * last_stride + (size_t(p) << logN) + n], pcs[i]);
-  }
-}
-
-__global__ void k_rescale_sub(const uint64_t* in, const uint64_t* t, uint64_t* out, const PrimeC* pcs,
-                              const uint64_t* qinv, const uint64_t* qinv_sh, uint32_t level, uint32_t logN,
-                              size_t in_stride, size_t t_stride, size_t out_stride) {
-  const size_t per = size_t(level) << logN;
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < 2 * per; x += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = x >= per;
-    const size_t r = x - (p ? per : 0);
-    const uint32_t i = r >> logN;
-    const uint64_t q = pcs[i].q;
-    const uint64_t c = in[blockIdx.z * in_stride + (size_t(p * (level + 1)) << logN) + r];
-    out[blockIdx.z * out_stride + x] = mul_shoup(sub_mod(c, t[blockIdx.z * t_stride + x], q), qinv[i], qinv_sh[i], q);
-  }
-}
-
 // host helpers -----------------------------------------------------------------------
 uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t q) { return static_cast<uint64_t>(static_cast<u128>(a) * b % q); }
 uint64_t h_pow(uint64_t a, uint64_t e, uint64_t q) {
@@ -860,8 +886,10 @@ bool use_cluster_ntt(uint32_t logN) {
 
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
-              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue) {
+              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue,
+              const void* rescale_epi) {
   const MdEpi* epi = static_cast<const MdEpi*>(epilogue);
+  const RsEpi* rs = static_cast<const RsEpi*>(rescale_epi);
   if (irows.empty() || batch == 0) return;
   if (irows.size() != orows.size() || irows.size() != primes.size()) fail(HS_E_INVALID_ARG, "ntt_rows: size mismatch");
   Runtime& rt = Runtime::get();
@@ -877,7 +905,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
       rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
       rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
     }
-    if (use_cluster_ntt(logN) && !epi) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
+    if (use_cluster_ntt(logN) && !epi && !rs) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
       switch (logN) {
         case 14: launch_ntt_cluster<14>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
         case 15: launch_ntt_cluster<15>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
@@ -889,7 +917,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
     switch (logN) {
 #define HS_NTT_CASE(L) \
   case L:              \
-    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s, epi); \
+    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s, epi, rs); \
     break;
       HS_NTT_CASE(9) HS_NTT_CASE(10) HS_NTT_CASE(11) HS_NTT_CASE(12) HS_NTT_CASE(13) HS_NTT_CASE(14)
       HS_NTT_CASE(15) HS_NTT_CASE(16) HS_NTT_CASE(17)
@@ -1434,8 +1462,7 @@ void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
   if (batch == 0) return;
   Runtime& rt = Runtime::get();
-  cudaStream_t s = rt.stream();
-  const uint32_t N = c.N, logN = c.spec.logN, nl = level + 1;
+  const uint32_t N = c.N, nl = level + 1;
   const size_t in_stride = size_t(2) * nl * N, out_stride = size_t(2) * level * N;
   const KsPlan& P = ks_plan(c, level);
   DevBuf last = rt.alloc(size_t(batch) * 2 * N);
@@ -1444,19 +1471,17 @@ void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t
   uint64_t* T = dptr<uint64_t>(t);
   // last limb of both polys -> coefficient form (out of place)
   ntt_rows(c, in, in_stride, LAST, size_t(2) * N, {level, nl + level}, {0, 1}, {level, level}, batch, true);
-  k_rescale_spread<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(LAST, T, c.dpc(), level, logN, size_t(2) * N,
-                                                                     out_stride);
+  // NTT of [c_l]_{q_i} for every remaining limb: the spread is the column pass's load,
+  // (c_i - t_i) q_l^-1 the row pass's store (t never materialised after the first pass)
   std::vector<uint32_t> rows(2 * level), primes(2 * level);
   for (uint32_t i = 0; i < 2 * level; ++i) {
     rows[i] = i;
     primes[i] = i % level;
   }
-  ntt_rows(c, T, out_stride, T, out_stride, rows, rows, primes, batch, false);
-  k_rescale_sub<<<dim3(grid_of(out_stride), 1, batch), kT, 0, s>>>(in, T, out, c.dpc(), dptr<const uint64_t>(P.qinv),
-                                                                  dptr<const uint64_t>(P.qinv_sh), level, logN,
-                                                                  in_stride, out_stride, out_stride);
+  const RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh), size_t(2) * N,
+                  in_stride, out_stride, level};
+  ntt_rows(c, T, out_stride, T, out_stride, rows, rows, primes, batch, false, nullptr, &rse);
   cuda_ok(cudaGetLastError(), "rescale");
-  rt.note_launch(2);
 }
 
 void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch) {

@@ -132,11 +132,12 @@ void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, ui
          bool inverse);
 // Batched NTT over an explicit row list: row irows[i] of each input batch item
 // (stride in_stride words) -> row orows[i] of the output item, mod primes[i].
-// `epilogue` (forward only, internal): a ModDown combine applied by the last pass
-// instead of storing the transform (rns.cu MdEpi).
+// `epilogue` / `rescale_epi` (forward only, internal): the ModDown combine or the
+// rescale spread/combine fused into the passes (rns.cu MdEpi, RsEpi).
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
-              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue = nullptr);
+              const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue = nullptr,
+              const void* rescale_epi = nullptr);
 // Symmetric RLWE encryption of N integer coefficients (host array) at `level`
 // (c1 = a, c0 = NTT(m + e) - a s; seeded by spec.seed and `tag`), and decryption
 // to centred integers mod q_0 (valid while |m| < q_0 / 2).
