@@ -710,25 +710,36 @@ struct ConvJob {
 
 // A = nsrc (compile time, <= 15 so the 128-bit sums cannot overflow), or 0 for a
 // run-time count (partial reductions every 15 terms).
+// Targets are processed in groups: one through the 128-bit integer MAC (ALU / IMAD
+// pipes) and, when they and every source prime are below 2^45, one or two through
+// exact fp64 modular products (fp_mulmod, FP64 pipe), so the pipes work at once.
 template <int A>
 __global__ void __launch_bounds__(kT) k_conv(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
                                              const ConvJob* jobs, const PrimeC* pcs, uint32_t logN) {
   constexpr int AS = A ? A : kMaxSrc;
   __shared__ uint64_t h_s[kMaxTgt * AS];
+  __shared__ double hd_s[A ? kMaxTgt * AS : 1];
   __shared__ PrimeC tq[kMaxTgt];
   __shared__ uint64_t hinv_s[AS], hinvsh_s[AS], qs_s[AS];
   __shared__ uint32_t orow_s[kMaxTgt];
+  __shared__ int src_fp;
   const ConvJob& J = jobs[blockIdx.y];
   const uint32_t nsrc = A ? A : J.nsrc, ntgt = J.ntgt;
-  for (uint32_t k = threadIdx.x; k < ntgt * nsrc; k += blockDim.x) h_s[k] = J.h[k / nsrc][k % nsrc];
+  if (threadIdx.x == 0) src_fp = 1;
+  for (uint32_t k = threadIdx.x; k < ntgt * nsrc; k += blockDim.x) {
+    h_s[k] = J.h[k / nsrc][k % nsrc];
+    if (A) hd_s[k] = static_cast<double>(h_s[k]);  // exact for targets below 2^45 (the only ones read)
+  }
   for (uint32_t k = threadIdx.x; k < ntgt; k += blockDim.x) {
     tq[k] = pcs[J.tgt[k]];
     orow_s[k] = J.out_row + J.tgt_row[k];
   }
+  __syncthreads();
   for (uint32_t k = threadIdx.x; k < nsrc; k += blockDim.x) {
     hinv_s[k] = J.hinv[k];
     hinvsh_s[k] = J.hinv_sh[k];
     qs_s[k] = pcs[J.src[k]].q;
+    if (!pcs[J.src[k]].fp) src_fp = 0;
   }
   __syncthreads();
   const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -738,19 +749,70 @@ __global__ void __launch_bounds__(kT) k_conv(const uint64_t* in, size_t in_strid
 #pragma unroll
   for (int i = 0; i < AS; ++i)
     if (A || i < int(nsrc)) y[i] = mul_shoup(I[size_t(i) << logN], hinv_s[i], hinvsh_s[i], qs_s[i]);
-  for (uint32_t t = 0; t < ntgt; ++t) {
-    const uint64_t* ht = h_s + t * nsrc;
-    u128 acc = 0;
-    if (A) {
+  if constexpr (A != 0) {
+    double yd[A];
 #pragma unroll
-      for (int i = 0; i < AS; ++i) acc += static_cast<u128>(y[i]) * ht[i];
-    } else {
+    for (int i = 0; i < A; ++i) yd[i] = u2d(y[i]);  // exact when the sources are < 2^45 (no XU convert)
+    const bool sfp = src_fp != 0;
+    uint32_t t = 0;
+    // groups of three targets: one integer MAC + two fp64 chains when eligible
+    for (; sfp && t + 2 < ntgt; t += 3) {
+      if (!tq[t + 1].fp || !tq[t + 2].fp) break;
+      const uint64_t* h0 = h_s + t * A;
+      const double *h1 = hd_s + (t + 1) * A, *h2 = hd_s + (t + 2) * A;
+      const double q1 = tq[t + 1].qd, q1inv = tq[t + 1].qinvd, q2 = tq[t + 2].qd, q2inv = tq[t + 2].qinvd;
+      u128 acc0 = 0;
+      double r1 = 0.0, r2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < A; ++i) {
+        acc0 += static_cast<u128>(y[i]) * h0[i];
+        r1 = __dadd_rn(r1, fp_mulmod(yd[i], h1[i], q1, q1inv));
+        r2 = __dadd_rn(r2, fp_mulmod(yd[i], h2[i], q2, q2inv));
+      }
+      O[size_t(orow_s[t]) << logN] = reduce128(acc0, tq[t]);
+      O[size_t(orow_s[t + 1]) << logN] = fp_canon(r1, q1, q1inv);
+      O[size_t(orow_s[t + 2]) << logN] = fp_canon(r2, q2, q2inv);
+    }
+    for (; t < ntgt; t += 2) {
+      const uint64_t* h0 = h_s + t * A;
+      u128 acc0 = 0;
+      if (t + 1 < ntgt && sfp && tq[t + 1].fp) {
+        const double* h1 = hd_s + (t + 1) * A;
+        const double q1 = tq[t + 1].qd, q1inv = tq[t + 1].qinvd;
+        double r1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+          acc0 += static_cast<u128>(y[i]) * h0[i];
+          r1 = __dadd_rn(r1, fp_mulmod(yd[i], h1[i], q1, q1inv));
+        }
+        O[size_t(orow_s[t]) << logN] = reduce128(acc0, tq[t]);
+        O[size_t(orow_s[t + 1]) << logN] = fp_canon(r1, q1, q1inv);
+      } else if (t + 1 < ntgt) {
+        const uint64_t* h1 = h0 + A;
+        u128 acc1 = 0;
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+          acc0 += static_cast<u128>(y[i]) * h0[i];
+          acc1 += static_cast<u128>(y[i]) * h1[i];
+        }
+        O[size_t(orow_s[t]) << logN] = reduce128(acc0, tq[t]);
+        O[size_t(orow_s[t + 1]) << logN] = reduce128(acc1, tq[t + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < A; ++i) acc0 += static_cast<u128>(y[i]) * h0[i];
+        O[size_t(orow_s[t]) << logN] = reduce128(acc0, tq[t]);
+      }
+    }
+  } else {
+    for (uint32_t t = 0; t < ntgt; ++t) {
+      const uint64_t* ht = h_s + t * nsrc;
+      u128 acc = 0;
       for (uint32_t i = 0; i < nsrc; ++i) {
         acc += static_cast<u128>(y[i]) * ht[i];
         if (i % 15 == 14) acc = reduce128(acc, tq[t]);
       }
+      O[size_t(orow_s[t]) << logN] = reduce128(acc, tq[t]);
     }
-    O[size_t(orow_s[t]) << logN] = reduce128(acc, tq[t]);
   }
 }
 
