@@ -44,10 +44,25 @@ struct Reduced {
   const double* res;    // otherwise: butterfly result, array k at res + k * S
 };
 
+#ifdef HS_STAT_TIMING
+__device__ unsigned long long g_stat_t[8];
+__device__ __forceinline__ void stamp(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_stat_t[k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void stamp(int) {}
+#endif
+
 // Grid-wide rotate-and-sum of NK per-slot term arrays produced by terms(i, t).
-template <class Q, class TermFn>
+// `idle` runs between publishing this block's partials and the grid barrier (work
+// that overlaps the wait for the slowest block, e.g. staging the Chebyshev table).
+template <class Q, class TermFn, class IdleFn>
 __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int NK, unsigned S,
-                            double* partial, double* scratch) {
+                            double* partial, double* scratch, IdleFn idle) {
   __shared__ double red[kMaxWarps][2 * kNK];
   __shared__ double tot[2 * kNK];
   const Range BR = block_range(S);
@@ -79,20 +94,40 @@ __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int 
       for (unsigned w = 0; w < blockDim.x / 32; ++w) s += red[w][threadIdx.x];
       partial[blockIdx.x * 2 * kNK + threadIdx.x] = s;
     }
+    stamp(5);
+    idle();
     grid.sync();
-    // every block sums the gridDim.x partials of each value with the same
-    // lane assignment and shuffle tree (one warp per value, loads in parallel),
-    // so all blocks reach identical totals and the same exactness decision
+    stamp(6);
+    // every block sums the gridDim.x partials of every value; all terms are integers
+    // and the checked bound keeps every partial sum below 2^53, so the totals are
+    // exact in any order: all threads load in parallel (one L2 round trip), then a
+    // shared-memory tree per value
     {
-      const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-      for (unsigned k = warp; k < static_cast<unsigned>(2 * NK); k += nwarps) {
-        double s = 0.0;
-        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(partial + b * 2 * kNK + k);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) tot[k] = s;
+      constexpr unsigned NV = 2 * kNK;
+      const unsigned nb = gridDim.x, nt = blockDim.x;
+      // thread t sums blocks t, t + nt, ... for every value (gridDim.x <= 2 * nt in practice)
+      double accp[NV];
+#pragma unroll
+      for (unsigned k = 0; k < NV; ++k) accp[k] = 0.0;
+      for (unsigned b = threadIdx.x; b < nb; b += nt)
+#pragma unroll
+        for (unsigned k = 0; k < NV; ++k)
+          if (k < static_cast<unsigned>(2 * NK)) accp[k] += __ldcg(partial + b * 2 * kNK + k);
+#pragma unroll
+      for (unsigned k = 0; k < NV; ++k)
+        for (int o = 16; o > 0; o >>= 1) accp[k] += __shfl_xor_sync(0xffffffffu, accp[k], o);
+      if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (unsigned k = 0; k < NV; ++k) red[threadIdx.x >> 5][k] = accp[k];
+      __syncthreads();
+      if (threadIdx.x < static_cast<unsigned>(2 * NK)) {
+        double t = 0.0;
+        for (unsigned w = 0; w < nt / 32; ++w) t += red[w][threadIdx.x];
+        tot[threadIdx.x] = t;
       }
     }
     __syncthreads();
+    stamp(7);
     bool exact = true;
     for (int k = 0; k < NK; ++k) {
       R.tot[k] = tot[2 * k];
@@ -105,6 +140,7 @@ __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int 
     }
   }
   // literal butterfly (ckks.hpp:218-230) through global memory
+  if constexpr (!Q::kExactSum) idle();
   double* cur = scratch;
   double* nxt = scratch + static_cast<size_t>(kNK) * S;
   for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
@@ -134,13 +170,17 @@ __device__ __forceinline__ double pick(const Reduced& R, int k, unsigned S, unsi
   return R.uniform ? R.tot[k] : __ldcg(R.res + static_cast<size_t>(k) * S + i);
 }
 
+
 template <class Q, int P>
 __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __grid_constant__ StatArgs a,
                                                        const __grid_constant__ Prog pg) {
   extern __shared__ double stab[];
+  stamp(0);
   cg::grid_group grid = cg::this_grid();
-  for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
-  __syncthreads();
+  // the table is first needed in phase B/C: stage it while waiting at phase A's barrier
+  auto stage = [&] {
+    for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
+  };
   const unsigned S = pg.S;
   const int per_col = (a.mom_mode & MOM_MEAN ? 1 : 0) + (a.mom_mode & MOM_VAR ? 2 : 0);
   const int NA = per_col * a.ncols;
@@ -163,7 +203,9 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
       }
     }
   };
-  const Reduced RA = grid_sum(q, grid, termsA, NA, S, a.partial, a.scratch);
+  stamp(1);
+  const Reduced RA = grid_sum(q, grid, termsA, NA, S, a.partial, a.scratch, stage);
+  stamp(2);
 
   // per-slot statistic values {mu_x, var_x, mu_y, var_y}
   auto mom = [&](unsigned i, double* sv) {
@@ -205,10 +247,11 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
       }
     };
     RB = grid_sum(q, grid, termsB, 1, S, a.partial + gridDim.x * 2 * kNK,
-                  a.scratch + 2 * static_cast<size_t>(kNK) * S);
+                  a.scratch + 2 * static_cast<size_t>(kNK) * S, [] {});
   }
 
   // ---- phase C: the per-slot program over this block's slot range ----
+  stamp(3);
   const Range R = block_range(S);
   if (R.lo >= R.hi) return;
   const unsigned iters = (R.spb * P + blockDim.x - 1) / blockDim.x;
@@ -222,6 +265,7 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
     sv[4] = a.power > 0 ? pick(RB, 0, S, s) : 0.0;
     exec<Q, P>(q, pg, stab, s, static_cast<int>(g % P), live, sv);
   }
+  stamp(4);
 }
 
 template <class F>
@@ -287,3 +331,9 @@ void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_
 
 }  // namespace k
 }  // namespace hsg
+
+#ifdef HS_STAT_TIMING
+extern "C" void hs_debug_stat_times(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, hsg::k::g_stat_t, sizeof(unsigned long long) * 8);
+}
+#endif
