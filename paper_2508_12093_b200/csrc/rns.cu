@@ -66,8 +66,12 @@ struct RowMap {
 // Each thread runs radix-2^RB groups (RB <= 3 stages) in registers; the first
 // group step reads HBM directly, the last writes HBM directly, the ones between
 // exchange through shared memory (row tiles XOR-swizzled, see swz()).
-constexpr int kNT = 512;           // threads per NTT block
-constexpr uint32_t kLogTile = 12;  // 4096 elements per NTT block
+#ifndef HS_NTT_LOGTILE
+#define HS_NTT_LOGTILE 11
+#define HS_NTT_MINB 6
+#endif
+constexpr uint32_t kLogTile = HS_NTT_LOGTILE;  // elements per NTT block (log2)
+constexpr int kNT = 1 << (HS_NTT_LOGTILE - 3);  // threads per NTT block: one radix-8 group each
 constexpr uint32_t kNTile = 1u << kLogTile;
 
 // Row-tile shared-memory swizzle: a bijection inside aligned 16-word groups that
@@ -406,7 +410,7 @@ struct PassEpi {
 };
 
 template <bool INV, bool ROWS, int LOGN, int MODE = 0>
-__global__ void __launch_bounds__(kNT, 3) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
+__global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                   size_t out_stride, const __grid_constant__ RowMap rm,
                                                   const PrimeC* pcs, const uint64_t* tw, const double* twd,
                                                   const __grid_constant__ PassEpi epi) {

@@ -14,6 +14,8 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2508_12093_b200 import _abi  # noqa: E402
+if os.environ.get("HESTAT_LIB"):  # A/B a variant build of the library
+    _abi.LIB_PATH = os.environ["HESTAT_LIB"]
 from paper_2508_12093_b200.rns import DeviceBuffer, RnsContext, RnsSpec  # noqa: E402
 
 
