@@ -446,17 +446,25 @@ class EncryptedColumn:  # column.hpp:19-23
     name: str = ""
 
     def _c(self):
+        # the ctypes view is cached while the chunk list and n_valid are unchanged (e2e path)
+        key = (tuple(map(id, self.chunks)), int(self.n_valid))
+        cache = self.__dict__.get("_cview")
+        if cache is not None and cache[0] == key:
+            return cache[1], cache[2]
         arr = (C.c_void_p * max(len(self.chunks), 1))(*[c._h.value for c in self.chunks])
-        return hs_column(C.cast(arr, C.POINTER(C.c_void_p)), len(self.chunks), int(self.n_valid)), arr
+        col = hs_column(C.cast(arr, C.POINTER(C.c_void_p)), len(self.chunks), int(self.n_valid))
+        self.__dict__["_cview"] = (key, col, arr)
+        return col, arr
 
 
 def encode_column(ctx: EvalContext, values, name: str = "") -> EncryptedColumn:  # column.hpp:25-39
-    v = _arr(values)
-    S = ctx.params().slot_count
+    v = values if (isinstance(values, np.ndarray) and values.dtype == np.float64 and values.ndim == 1
+                   and values.flags.c_contiguous) else _arr(values)
+    S = ctx._p.slot_count
     nch = (len(v) + S - 1) // S
     arr = (C.c_void_p * max(nch, 1))()
     got = C.c_uint64(0)
-    _check(_abi.lib().hs_encode_column(ctx._h, _dp(v), len(v), C.cast(arr, C.POINTER(C.c_void_p)), C.byref(got)))
+    _check(_abi.lib().hs_encode_column(ctx._h, _dp(v), len(v), arr, C.byref(got)))
     chunks = [Ciphertext._own(C.c_void_p(arr[i])) for i in range(got.value)]
     return EncryptedColumn(chunks, len(v), name)
 
@@ -513,7 +521,7 @@ def znorm(ctx: EvalContext, col: EncryptedColumn, B: float,
           cfg: Optional[InvRootConfig] = None) -> EncryptedColumn:  # :153-166
     c, keep = col._c()
     arr = (C.c_void_p * max(len(col.chunks), 1))()
-    _check(_abi.lib().hs_znorm(ctx._h, C.byref(c), float(B), _cfg(cfg), C.cast(arr, C.POINTER(C.c_void_p))))
+    _check(_abi.lib().hs_znorm(ctx._h, C.byref(c), float(B), _cfg(cfg), arr))
     del keep
     return EncryptedColumn([Ciphertext._own(C.c_void_p(arr[i])) for i in range(len(col.chunks))],
                            col.n_valid, col.name)
