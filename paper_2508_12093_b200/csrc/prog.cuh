@@ -40,7 +40,10 @@ __device__ __forceinline__ double ffull(const F& f, const double* t, const doubl
 // the unrolled carry loop); the code stays ~3 KB so it lives in the I-cache
 // (a fully unrolled degree-511 tree is ~32 KB of SASS per lane and stalled on
 // instruction fetch).  Same ops on the same operands as ffull<K>: bit-identical.
-constexpr int kBK = 5;
+#ifndef HS_KBK
+#define HS_KBK 5
+#endif
+constexpr int kBK = HS_KBK;
 
 template <int ST, class F>
 __device__ __forceinline__ double ffull_small(int K, const F& f, const double* t, const double (&T)[kMaxK]) {

@@ -71,7 +71,11 @@ struct RowMap {
 #define HS_NTT_MINB 6
 #endif
 constexpr uint32_t kLogTile = HS_NTT_LOGTILE;  // elements per NTT block (log2)
-constexpr int kNT = 1 << (HS_NTT_LOGTILE - 3);  // threads per NTT block: one radix-8 group each
+#ifndef HS_NTT_MAXRB
+#define HS_NTT_MAXRB 3
+#endif
+constexpr int kMaxRB = HS_NTT_MAXRB;  // largest radix (log2) of a register step
+constexpr int kNT = 1 << (HS_NTT_LOGTILE - kMaxRB);  // threads per NTT block: one largest-radix group each
 constexpr uint32_t kNTile = 1u << kLogTile;
 
 // Row-tile shared-memory swizzle: a bijection inside aligned 16-word groups that
@@ -244,8 +248,13 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
   }
 }
 
-// All steps of a pass, unrolled at compile time: radix-8 steps, with the
-// remainder taken as radix-4 (a 4-stage tail becomes 2 + 2).
+// All steps of a pass, unrolled at compile time.  Radix-8 steps with the remainder
+// taken as radix-4 (a 4-stage tail becomes 2 + 2); with kMaxRB = 4, radix-16 steps
+// (5 and 6 stages become 3 + 2 and 3 + 3).
+constexpr int pick_rb(int rem) {
+  if (kMaxRB >= 4) return rem <= 4 ? rem : (rem <= 6 ? 3 : 4);
+  return rem == 4 ? 2 : (rem < 3 ? rem : 3);
+}
 template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST>
 __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
                                           const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
@@ -253,7 +262,7 @@ __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
-    constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
+    constexpr int RB = pick_rb(rem);
     if constexpr (DONE > 0) __syncthreads();
     ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, psi, psip, q, tile0,
                                                                               ninv, ninv_sh);
@@ -391,7 +400,7 @@ __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, doub
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
-    constexpr int RB = rem == 4 ? 2 : (rem < 3 ? rem : 3);
+    constexpr int RB = pick_rb(rem);
     if constexpr (DONE > 0) __syncthreads();
     ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, tw, q, qinv, tile0,
                                                                                  ninv);
@@ -707,6 +716,7 @@ constexpr int kMaxSrc = 32, kMaxTgt = 64;
 struct ConvJob {
   uint32_t nsrc, ntgt;
   uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
+  uint32_t frag_off, pad_;   // k_conv_mma: this job's B fragments (uint2 index into the plan's table)
   uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
   uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
   uint64_t h[kMaxTgt][kMaxSrc];
@@ -817,6 +827,142 @@ __global__ void __launch_bounds__(kT) k_conv(const uint64_t* in, size_t in_strid
       }
       O[size_t(orow_s[t]) << logN] = reduce128(acc, tq[t]);
     }
+  }
+}
+
+// ---- base conversion on the tensor cores (IMMA u8 m16n8k32) ----------------------------
+// out_t[n] = sum_i y_i[n] h[t][i] mod q_t as an exact integer GEMM over bytes:
+//   A[n][8i + a] = byte a of y_i[n]                      (the u64 residues as they lie)
+//   B[8i + a][b] = byte b of (h[t][i] 2^(8a) mod q_t)    (host-built per job, in
+//                                                         fragment order: conv_frags)
+//   C[n][b] = sum_k A[n][k] B[k][b] < 8 nsrc 255^2 < 2^23   (exact in s32)
+//   out_t[n] = sum_b C[n][b] 2^(8b) mod q_t: lo/hi 4-byte halves (< 2^47 each), one
+//              reduce128 of hi 2^32 + lo.
+// The result is congruent to sum_i y_i h[t][i] and canonical, so it equals k_conv's
+// word for word.  A block converts 128 coefficients (4 warps x 2 m16 tiles) of one job;
+// per target a warp issues 2 KS IMMAs, parks C in shared memory and every lane finishes
+// one coefficient (coalesced row store).  The u128 MAC chain of k_conv (~90 ALU
+// instructions per output) becomes ~30.
+constexpr int kConvMmaRows = 128;
+
+__device__ __forceinline__ void imma_u8(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+template <int KS>
+constexpr size_t conv_mma_smem() {
+  return size_t(kConvMmaRows) * (KS * 8 + 4) * 4 + 4 * 2 * 256 * 4;
+}
+
+struct ConvTgt {
+  double qd, qinvd, c32d;  // fp targets: q, 1/q, 2^32 mod q
+  uint32_t orow, fp;
+};
+
+template <int KS>  // k-steps of 32 bytes: nsrc <= 4 KS
+__global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                           size_t out_stride, const ConvJob* jobs, const uint2* frags,
+                                                           const PrimeC* pcs, uint32_t logN) {
+  constexpr int RSW = KS * 8 + 4;  // A row stride in words: fragment loads hit 32 distinct banks
+  extern __shared__ uint4 dyn_smem[];
+  uint32_t* As = reinterpret_cast<uint32_t*>(dyn_smem);       // [128][RSW]
+  int* stg = reinterpret_cast<int*>(As + kConvMmaRows * RSW);  // [4 warps][2][32][8]
+  __shared__ PrimeC tq[kMaxTgt];
+  __shared__ ConvTgt tc[kMaxTgt];
+  __shared__ uint64_t hinv_s[4 * KS], hinvsh_s[4 * KS], qs_s[4 * KS];
+  const ConvJob& J = jobs[blockIdx.y];
+  const uint32_t nsrc = J.nsrc, ntgt = J.ntgt;
+  for (uint32_t k = threadIdx.x; k < ntgt; k += kConvMmaRows) {
+    const PrimeC P = pcs[J.tgt[k]];
+    tq[k] = P;
+    const uint64_t c32 = (uint64_t(1) << 32) % P.q;
+    tc[k] = ConvTgt{P.qd, P.qinvd, static_cast<double>(c32), J.out_row + J.tgt_row[k], P.fp};
+  }
+  if (threadIdx.x < nsrc) {
+    hinv_s[threadIdx.x] = J.hinv[threadIdx.x];
+    hinvsh_s[threadIdx.x] = J.hinv_sh[threadIdx.x];
+    qs_s[threadIdx.x] = pcs[J.src[threadIdx.x]].q;
+  }
+  __syncthreads();
+  const uint32_t n0 = blockIdx.x * kConvMmaRows;
+  {  // y_i = [x_i hinv_i]_{q_i}: thread = coefficient, the u64 words are the A row's bytes
+    const uint64_t* I = in + blockIdx.z * in_stride + (size_t(J.in_row) << logN) + n0 + threadIdx.x;
+    uint2* row = reinterpret_cast<uint2*>(As + threadIdx.x * RSW);
+    uint64_t x[4 * KS];
+#pragma unroll
+    for (int i = 0; i < 4 * KS; ++i) x[i] = uint32_t(i) < nsrc ? __ldcs(I + (size_t(i) << logN)) : 0;  // all loads in flight
+#pragma unroll
+    for (int i = 0; i < 4 * KS; ++i) {
+      const uint64_t y = uint32_t(i) < nsrc ? mul_shoup(x[i], hinv_s[i], hinvsh_s[i], qs_s[i]) : 0;
+      row[i] = make_uint2(static_cast<uint32_t>(y), static_cast<uint32_t>(y >> 32));
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  uint32_t a[2][KS][4];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint32_t* r0 = As + (warp * 32 + m * 16 + g) * RSW + ks * 8 + t4;
+      const uint32_t* r1 = r0 + 8 * RSW;
+      a[m][ks][0] = r0[0];
+      a[m][ks][1] = r1[0];
+      a[m][ks][2] = r0[4];
+      a[m][ks][3] = r1[4];
+    }
+  uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + lane;
+  int* const S0 = stg + warp * 512;
+  int2* const W0 = reinterpret_cast<int2*>(S0 + g * 8 + 2 * t4);  // this lane's C slots (rows g, g+8, 16+g, 24+g)
+  const uint4* const R0 = reinterpret_cast<const uint4*>(S0 + lane * 8);  // this lane's coefficient row
+  const uint2* F = frags + J.frag_off + lane;
+  // one target: KS x 2 IMMAs -> C parked in buffer `buf` (256 ints) -> the lane's row
+  auto mma_park = [&](uint32_t t, int buf) {
+    uint2 b[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = __ldg(F + (t * KS + ks) * 32);  // same 256 B for every warp: L1
+    int c[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      imma_u8(c[0], a[0][ks], b[ks]);
+      imma_u8(c[1], a[1][ks], b[ks]);
+    }
+    int2* W = W0 + buf * 128;
+    W[0] = make_int2(c[0][0], c[0][1]);
+    W[32] = make_int2(c[0][2], c[0][3]);
+    W[64] = make_int2(c[1][0], c[1][1]);
+    W[96] = make_int2(c[1][2], c[1][3]);
+  };
+  auto finish = [&](uint32_t t, int buf) {
+    const uint4 u = R0[buf * 64], v = R0[buf * 64 + 1];
+    const uint64_t lo = uint64_t(u.x) + (uint64_t(u.y) << 8) + (uint64_t(u.z) << 16) + (uint64_t(u.w) << 24);
+    const uint64_t hi = uint64_t(v.x) + (uint64_t(v.y) << 8) + (uint64_t(v.z) << 16) + (uint64_t(v.w) << 24);
+    const ConvTgt T = tc[t];
+    uint64_t r;
+    if (T.fp) {  // lo + hi (2^32 mod q) on the FP64 pipe: lo, hi < 2^47, every step exact
+      const double h = fp_mulmod(u2d(hi), T.c32d, T.qd, T.qinvd);
+      r = fp_canon(__dadd_rn(h, u2d(lo)), T.qd, T.qinvd);
+    } else {
+      r = reduce128((static_cast<u128>(hi) << 32) + lo, tq[t]);
+    }
+    O[size_t(T.orow) << logN] = r;
+  };
+  uint32_t t = 0;
+#pragma unroll 1
+  for (; t + 1 < ntgt; t += 2) {  // two targets per round: their IMMA and epilogue chains interleave
+    mma_park(t, 0);
+    mma_park(t + 1, 1);
+    __syncwarp();
+    finish(t, 0);
+    finish(t + 1, 1);
+    __syncwarp();
+  }
+  if (t < ntgt) {
+    mma_park(t, 0);
+    __syncwarp();
+    finish(t, 0);
   }
 }
 
@@ -1330,6 +1476,40 @@ void fill_conv(const Ctx& c, const std::vector<uint32_t>& src, const std::vector
   }
 }
 
+// k_conv_mma's B operand for one job, in mma fragment order: [target][k-step][lane] ->
+// (b0, b1) = bytes B[32 ks + 4 (lane & 3) + 0..3][lane >> 2] and the same at k + 16, where
+// B[8i + a][b] = byte b of (h[t][i] 2^(8a) mod q_t).
+uint32_t conv_ks(uint32_t nsrc) { return (nsrc + 3) / 4; }
+
+void conv_frags(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
+  const uint32_t KS = conv_ks(J.nsrc), K = 32 * KS;
+  std::vector<uint8_t> hb(size_t(8) * K);
+  for (uint32_t t = 0; t < J.ntgt; ++t) {
+    const uint64_t qt = c.primes[J.tgt[t]];
+    std::fill(hb.begin(), hb.end(), 0);
+    for (uint32_t i = 0; i < J.nsrc; ++i)
+      for (uint32_t a = 0; a < 8; ++a) {
+        const uint64_t v = h_mulmod(J.h[t][i] % qt, h_pow(2, 8 * a, qt), qt);
+        for (uint32_t b = 0; b < 8; ++b) hb[size_t(b) * K + 8 * i + a] = static_cast<uint8_t>(v >> (8 * b));
+      }
+    for (uint32_t ks = 0; ks < KS; ++ks)
+      for (uint32_t lane = 0; lane < 32; ++lane) {
+        const uint8_t* col = hb.data() + size_t(lane >> 2) * K + 32 * ks + 4 * (lane & 3);
+        auto pack = [](const uint8_t* p) {
+          return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+        };
+        f->push_back(make_uint2(pack(col), pack(col + 16)));
+      }
+  }
+}
+
+void attach_frags(const Ctx& c, std::vector<ConvJob>* jobs, std::vector<uint2>* f) {
+  for (ConvJob& J : *jobs) {
+    J.frag_off = static_cast<uint32_t>(f->size());
+    conv_frags(c, J, f);
+  }
+}
+
 // Per-level plan: conversion jobs, NTT row lists and scalar tables (device resident).
 struct KsPlan {
   uint32_t nl, nx, nd;
@@ -1340,6 +1520,7 @@ struct KsPlan {
   DevBuf down_jobs;                   // ConvJob[2]: acc_w P rows -> conv rows w*nl..
   std::vector<uint32_t> p_rows, p_primes;    // acc P rows (both halves) for the iNTT
   std::vector<uint32_t> cv_rows, cv_primes;  // conv rows (both halves) for the NTT
+  DevBuf frags;                       // k_conv_mma B fragments of every job above
   DevBuf pinv, pinv_sh;               // [nl] P^-1 mod q_i
   DevBuf qinv, qinv_sh;               // [level] q_level^-1 mod q_i (rescale)
 };
@@ -1370,7 +1551,8 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
       }
     fill_conv(c, src, tgt, row, lo, j * p->nx, &up[j]);
   }
-  p->up_jobs = upload(up);
+  std::vector<uint2> frags;
+  attach_frags(c, &up, &frags);
   std::vector<ConvJob> down(2);
   std::vector<uint32_t> src, tgt, row;
   for (uint32_t k = 0; k < K; ++k) src.push_back(c.nq + k);
@@ -1389,7 +1571,10 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
       p->cv_primes.push_back(i);
     }
   }
+  attach_frags(c, &down, &frags);
+  p->up_jobs = upload(up);
   p->down_jobs = upload(down);
+  p->frags = upload(frags);
   std::vector<uint64_t> pinv(nl), pinv_sh(nl);
   for (uint32_t i = 0; i < nl; ++i) {
     const uint64_t q = c.primes[i];
@@ -1425,10 +1610,47 @@ void launch_conv_a(const uint64_t* in, size_t in_stride, uint64_t* out, size_t o
   k_conv<A><<<g, kT, 0, s>>>(in, in_stride, out, out_stride, jobs, c.dpc(), c.spec.logN);
 }
 
-void launch_conv(uint32_t nsrc, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
-                 const ConvJob* jobs, uint32_t njobs, const Ctx& c, uint32_t batch) {
+bool use_conv_mma() {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_CONV_MMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return mode != 0;
+}
+
+template <int KS>
+void launch_conv_mma(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
+                     const uint2* frags, uint32_t njobs, uint32_t ntgt, const Ctx& c, uint32_t batch, cudaStream_t s) {
+  static const bool attr = [] {
+    cuda_ok(cudaFuncSetAttribute(k_conv_mma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(conv_mma_smem<KS>())),
+            "conv_mma smem");
+    return true;
+  }();
+  (void)attr;
+  const dim3 g(c.N / kConvMmaRows, njobs, batch);
+  (void)ntgt;
+  k_conv_mma<KS><<<g, kConvMmaRows, conv_mma_smem<KS>(), s>>>(in, in_stride, out, out_stride, jobs, frags,
+                                                                   c.dpc(), c.spec.logN);
+}
+
+// nsrc sources per job (all jobs of a call alike), ntgt targets at most per job.
+void launch_conv(uint32_t nsrc, uint32_t ntgt, const uint64_t* in, size_t in_stride, uint64_t* out,
+                 size_t out_stride, const ConvJob* jobs, const uint2* frags, uint32_t njobs, const Ctx& c,
+                 uint32_t batch) {
   if (njobs == 0) return;
   cudaStream_t s = Runtime::get().stream();
+  if (frags && use_conv_mma() && conv_ks(nsrc) <= 4 && c.N % kConvMmaRows == 0) {
+    switch (conv_ks(nsrc)) {
+      case 1: launch_conv_mma<1>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s); break;
+      case 2: launch_conv_mma<2>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s); break;
+      case 3: launch_conv_mma<3>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s); break;
+      default: launch_conv_mma<4>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s);
+    }
+    cuda_ok(cudaGetLastError(), "conv_mma launch");
+    Runtime::get().note_launch();
+    return;
+  }
   switch (nsrc) {
 #define HS_CONV_CASE(a) \
   case a:               \
@@ -1466,9 +1688,12 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   // ModUp: d -> coefficient form (out of place), convert every digit, NTT the new rows
   ntt_rows(c, d, d_stride, DC, dc_stride, qrows, qrows, qrows, batch, true);
   const ConvJob* up = dptr<const ConvJob>(P.up_jobs);
-  launch_conv(c.alpha, DC, dc_stride, EXT, ext_stride, up, P.n_full, c, batch);
-  if (P.n_full < nd)
-    launch_conv(nl - P.n_full * c.alpha, DC, dc_stride, EXT, ext_stride, up + P.n_full, nd - P.n_full, c, batch);
+  const uint2* FR = dptr<const uint2>(P.frags);
+  launch_conv(c.alpha, nx - c.alpha, DC, dc_stride, EXT, ext_stride, up, FR, P.n_full, c, batch);
+  if (P.n_full < nd) {
+    const uint32_t rest = nl - P.n_full * c.alpha;
+    launch_conv(rest, nx - rest, DC, dc_stride, EXT, ext_stride, up + P.n_full, FR, nd - P.n_full, c, batch);
+  }
   ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
   // inner product with the key (each key word read once per call)
   {
@@ -1490,7 +1715,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   }
   // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
   ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);
-  launch_conv(c.spec.K, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), 2, c, batch);
+  launch_conv(c.spec.K, nl, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), FR, 2, c, batch);
   // NTT of the converted rows with the ModDown combine fused into its last pass:
   // out_w = (acc_w - conv_w) * P^-1 (+ add_w), conv_w never stored
   const MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh),

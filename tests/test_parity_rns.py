@@ -212,3 +212,49 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_NTT_CLUSTER": "1"},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+# Base-conversion widths of k_conv_mma (KS = ceil(sources / 4) k-steps): alpha 1..16 sources per
+# digit, ModDown with K special primes, 61-bit targets (integer epilogue) and 44-bit ones (FP64
+# epilogue), and alpha = 17 (more than 16 sources: the ALU conversion kernel).
+CONV_SHAPES = [
+    Spec(logN=10, L=15, K=2, dnum=1, seed=21),            # alpha=16: KS=4; ModDown K=2: KS=1
+    Spec(logN=10, L=11, K=5, dnum=2, seed=22, logp=44),   # alpha=6: KS=2; K=5: KS=2
+    Spec(logN=10, L=9, K=12, dnum=5, seed=23, logp=44),   # alpha=2; ModDown 12 sources: KS=3
+    Spec(logN=10, L=16, K=3, dnum=1, seed=24),            # alpha=17: fallback conversion
+    Spec(logN=11, L=13, K=4, dnum=2, seed=25),            # alpha=7, 61-bit special targets
+]
+
+
+@pytest.mark.parametrize("s", CONV_SHAPES, ids=str)
+def test_conv_widths_mul_relin_and_rotate(s):
+    c = ctx(s)
+    for level in (s.L, s.L - 1, max(1, s.L // 2)):
+        a, b = O.random_ct(s, level, 31 + level), O.random_ct(s, level, 57 + level)
+        got = c.mul_relin(level, _buf(a), _buf(b)).download()
+        assert np.array_equal(got, O.mul_relin(s, level, a, b)), level
+        assert np.array_equal(c.rotate(level, 3, _buf(a)).download(), O.rotate(s, level, 3, a)), level
+
+
+def test_alu_conversion_option_matches_oracle():
+    """HS_CONV_MMA=0 (the ALU/FP64 base conversion instead of the tensor-core one) gives the same limbs."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from rns_abi import RnsOracle, Spec
+from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
+O = RnsOracle()
+for s in (Spec(logN=12, L=7, K=3, dnum=3, seed=11), Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44)):
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
+    a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
+    got = c.mul_relin(s.L, DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)).download()
+    assert np.array_equal(got, O.mul_relin(s, s.L, a, b)), s
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_CONV_MMA": "0"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
