@@ -50,6 +50,14 @@ __device__ inline uint64_t lift(int64_t v, uint64_t q) {
 }
 __device__ inline uint32_t bitrev(uint32_t x, uint32_t bits) { return __brev(x) >> (32 - bits); }
 
+// NTT-domain automorphism X -> X^g: slot n of the result is slot galois_src(n) of the input
+__device__ inline uint32_t galois_src(uint32_t j, uint64_t g, uint32_t logN) {
+  const uint64_t mask = (2ULL << logN) - 1;
+  const uint64_t e = ((2ULL * bitrev(j, logN) + 1) * g) & mask;
+  return bitrev(static_cast<uint32_t>((e - 1) >> 1), logN);
+}
+
+
 // (input row, output row, prime) per blockIdx.y of an NTT launch
 constexpr int kMaxRows = 128;
 struct RowMap {
@@ -128,15 +136,69 @@ struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
   uint32_t nl, nx;
 };
 
+// Key-switch inputs produced on the fly instead of materialised: mul_relin's tensor
+// (d = a1 b1, add_0 = a0 b0, add_1 = a0 b1 + a1 b0) and rotate's automorphism
+// (d = sigma(c1), add_0 = sigma(c0)).  The iNTT that starts ModUp loads d through
+// TnLoad / PermLoad, and the ModDown store adds add_w through AddTensor / AddPerm.
+enum KsSrcMode : int { KS_PLAIN = 0, KS_TENSOR = 1, KS_PERM = 2 };
+struct KsSrc {
+  int mode = KS_PLAIN;
+  const uint64_t* a = nullptr;  // tensor: first ciphertext; automorphism: the input ciphertext
+  const uint64_t* b = nullptr;  // tensor: second ciphertext
+  size_t stride = 0;            // per batch item
+  uint64_t g = 0;               // Galois element
+  uint32_t nl = 0;
+};
+
+struct TnLoad {  // d = a1 b1 (this tile of limb i)
+  const uint64_t* a1;
+  const uint64_t* b1;
+  PrimeC P;
+  __device__ uint64_t operator()(size_t off) const { return mul_mod(a1[off], b1[off], P); }
+};
+
+template <int LOGN>
+struct PermLoad {  // d = sigma_g(c1): row = limb i of c1 (whole row), toff = this tile's first word
+  const uint64_t* row;
+  uint64_t g;
+  uint32_t toff;
+  __device__ uint64_t operator()(size_t off) const { return row[galois_src(toff + uint32_t(off), g, LOGN)]; }
+};
+
+struct AddRow {  // + add_w[i] (materialised) or nothing
+  const uint64_t* p;
+  __device__ uint64_t operator()(size_t off, uint64_t r, uint64_t q) const { return p ? add_mod(r, p[off], q) : r; }
+};
+
+struct AddTensor {  // + a0 b0 (w = 0) or + a0 b1 + a1 b0 (w = 1), same reductions as k_tensor
+  const uint64_t *a0, *a1, *b0, *b1;
+  PrimeC P;
+  int w;
+  __device__ uint64_t operator()(size_t off, uint64_t r, uint64_t q) const {
+    const uint64_t t = w == 0 ? mul_mod(a0[off], b0[off], P)
+                              : reduce128(static_cast<u128>(a0[off]) * b1[off] + static_cast<u128>(a1[off]) * b0[off], P);
+    return add_mod(r, t, q);
+  }
+};
+
+template <int LOGN>
+struct AddPerm {  // + sigma_g(c0) (w = 0 only: row null for w = 1)
+  const uint64_t* row;
+  uint64_t g;
+  uint32_t toff;
+  __device__ uint64_t operator()(size_t off, uint64_t r, uint64_t q) const {
+    return row ? add_mod(r, row[galois_src(toff + uint32_t(off), g, LOGN)], q) : r;
+  }
+};
+
+template <class AddF>
 struct MdStore {
   const uint64_t* acc;  // acc_w row i (this tile)
-  const uint64_t* add;  // add_w row i (this tile) or null
   uint64_t* out;        // out_w row i (this tile)
   uint64_t q, pinv, pinv_sh;
+  AddF add;
   __device__ void operator()(size_t off, uint64_t v) const {
-    uint64_t r = mul_shoup(sub_mod(acc[off], v, q), pinv, pinv_sh, q);
-    if (add) r = add_mod(r, add[off], q);
-    out[off] = r;
+    out[off] = add(off, mul_shoup(sub_mod(acc[off], v, q), pinv, pinv_sh, q), q);
   }
 };
 
@@ -416,6 +478,7 @@ __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, doub
 struct PassEpi {
   MdEpi md;
   RsEpi rs;
+  KsSrc ks;
 };
 
 template <bool INV, bool ROWS, int LOGN, int MODE = 0>
@@ -442,15 +505,36 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* i
     else
       ntt_steps<INV, ROWS, LOGN, 0>(ld, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
   };
-  if constexpr (MODE == 1) {  // row r = w * nl + i of the ModDown conversion output
+  if constexpr (MODE == 1 || MODE == 6 || MODE == 7) {  // row r = w * nl + i of the ModDown conversion output
     const MdEpi& e = epi.md;
     const uint32_t r = rm.orow[blockIdx.y], w = r / e.nl, i = r - w * e.nl;
-    const uint64_t* ad = w == 0 ? e.add0 : e.add1;
-    const MdStore st{e.acc + blockIdx.z * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff,
-                     ad ? ad + blockIdx.z * e.add_stride + (size_t(i) << LOGN) + toff : nullptr,
-                     e.out + blockIdx.z * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff, P.q, e.pinv[i],
-                     e.pinv_sh[i]};
-    run(PlainLoad{gi}, st);
+    const uint64_t* acc = e.acc + blockIdx.z * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff;
+    uint64_t* o = e.out + blockIdx.z * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff;
+    if constexpr (MODE == 1) {
+      const uint64_t* ad = w == 0 ? e.add0 : e.add1;
+      run(PlainLoad{gi}, MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+                                         AddRow{ad ? ad + blockIdx.z * e.add_stride + (size_t(i) << LOGN) + toff : nullptr}});
+    } else if constexpr (MODE == 6) {
+      const KsSrc& k = epi.ks;
+      const uint64_t* a0 = k.a + blockIdx.z * k.stride + (size_t(i) << LOGN) + toff;
+      const uint64_t* b0 = k.b + blockIdx.z * k.stride + (size_t(i) << LOGN) + toff;
+      const size_t h = size_t(k.nl) << LOGN;
+      run(PlainLoad{gi}, MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+                                            AddTensor{a0, a0 + h, b0, b0 + h, P, int(w)}});
+    } else {
+      const KsSrc& k = epi.ks;
+      const uint64_t* c0 = w == 0 ? k.a + blockIdx.z * k.stride + (size_t(i) << LOGN) : nullptr;
+      run(PlainLoad{gi}, MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+                                                AddPerm<LOGN>{c0, k.g, uint32_t(toff)}});
+    }
+  } else if constexpr (MODE == 4 || MODE == 5) {  // inverse row pass of d = a1 b1 / sigma(c1), limb irow
+    const KsSrc& k = epi.ks;
+    const uint32_t i = rm.irow[blockIdx.y];
+    const uint64_t* r1 = k.a + blockIdx.z * k.stride + (size_t(k.nl + i) << LOGN);
+    if constexpr (MODE == 4)
+      run(TnLoad{r1 + toff, k.b + blockIdx.z * k.stride + (size_t(k.nl + i) << LOGN) + toff, P}, PlainStore{go});
+    else
+      run(PermLoad<LOGN>{r1, k.g, uint32_t(toff)}, PlainStore{go});
   } else if constexpr (MODE == 2) {  // row r = p * level + i: [last_p]_{q_i}
     const RsEpi& e = epi.rs;
     const uint32_t r = rm.orow[blockIdx.y], p = r / e.level;
@@ -470,13 +554,31 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* i
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
-                const double* twd, cudaStream_t s, const MdEpi* md, const RsEpi* rs) {
+                const double* twd, cudaStream_t s, const MdEpi* md, const RsEpi* rs, const KsSrc* ks) {
   using Gc = NttGeom<LOGN, false>;
   using Gr = NttGeom<LOGN, true>;
   const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch), gr(1u << (Gr::logR1 - Gr::logTPB), n, batch);
   PassEpi none{}, ep{};
   if (md) ep.md = *md;
   if (rs) ep.rs = *rs;
+  const int ksm = ks ? ks->mode : KS_PLAIN;
+  if (ks) ep.ks = *ks;
+  if (!inverse && md && ksm != KS_PLAIN) {
+    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
+    if (ksm == KS_TENSOR)
+      k_ntt_pass<false, true, LOGN, 6><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+    else
+      k_ntt_pass<false, true, LOGN, 7><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+    return;
+  }
+  if (inverse && ksm != KS_PLAIN) {
+    if (ksm == KS_TENSOR)
+      k_ntt_pass<true, true, LOGN, 4><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
+    else
+      k_ntt_pass<true, true, LOGN, 5><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
+    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
+    return;
+  }
   if (!inverse) {
     if (rs)
       k_ntt_pass<false, false, LOGN, 2><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
@@ -676,11 +778,6 @@ __global__ void k_square(uint64_t* out, const uint64_t* in, const PrimeC* pcs, u
     out[x] = mul_mod(in[x], in[x], pcs[x >> logN]);
 }
 
-__device__ inline uint32_t galois_src(uint32_t j, uint64_t g, uint32_t logN) {
-  const uint64_t mask = (2ULL << logN) - 1;
-  const uint64_t e = ((2ULL * bitrev(j, logN) + 1) * g) & mask;
-  return bitrev(static_cast<uint32_t>((e - 1) >> 1), logN);
-}
 
 // out[r][n] = in[r][src(n)] for `rows` rows per batch item
 __global__ void k_automorph(uint64_t* out, const uint64_t* in, uint64_t g, uint32_t logN, uint32_t rows,
@@ -975,7 +1072,7 @@ __global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext
                                                  size_t d_stride, uint64_t* acc, size_t acc_stride,
                                                  const uint64_t* kb, const uint64_t* ka, const PrimeC* pcs,
                                                  uint32_t nx, uint32_t nl, uint32_t np, uint32_t nq, uint32_t alpha,
-                                                 uint32_t logN, uint32_t batch) {
+                                                 uint32_t logN, uint32_t batch, const KsSrc src) {
   const size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
   const uint32_t row = x >> logN, n = x & ((1u << logN) - 1);
   if (row >= nx) return;
@@ -990,12 +1087,21 @@ __global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext
   }
   const uint32_t own = row < nl ? row / alpha : 0xFFFFFFFFu;
   const size_t rowsN = size_t(nx) << logN;
+  // d on the digit's own rows: materialised, or the tensor / automorphism of the inputs
+  auto own_word = [&](uint32_t b) -> uint64_t {
+    if (src.mode == KS_TENSOR) {
+      const size_t o = b * src.stride + (size_t(nl + row) << logN) + n;
+      return mul_mod(src.a[o], src.b[o], P);
+    }
+    if (src.mode == KS_PERM) return src.a[b * src.stride + (size_t(nl + row) << logN) + galois_src(n, src.g, logN)];
+    return d[b * d_stride + x];
+  };
 #pragma unroll 2
   for (uint32_t b = 0; b < batch; ++b) {
     const uint64_t* E = ext + b * ext_stride + x;
     uint64_t e[ND];
 #pragma unroll
-    for (int j = 0; j < ND; ++j) e[j] = uint32_t(j) == own ? d[b * d_stride + x] : E[j * rowsN];
+    for (int j = 0; j < ND; ++j) e[j] = uint32_t(j) == own ? own_word(b) : E[j * rowsN];
     u128 s0 = 0, s1 = 0;
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
@@ -1099,9 +1205,10 @@ bool use_cluster_ntt(uint32_t logN) {
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
               const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue,
-              const void* rescale_epi) {
+              const void* rescale_epi, const void* ks_src) {
   const MdEpi* epi = static_cast<const MdEpi*>(epilogue);
   const RsEpi* rs = static_cast<const RsEpi*>(rescale_epi);
+  const KsSrc* ks = static_cast<const KsSrc*>(ks_src);
   if (irows.empty() || batch == 0) return;
   if (irows.size() != orows.size() || irows.size() != primes.size()) fail(HS_E_INVALID_ARG, "ntt_rows: size mismatch");
   Runtime& rt = Runtime::get();
@@ -1117,7 +1224,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
       rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
       rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
     }
-    if (use_cluster_ntt(logN) && !epi && !rs) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
+    if (use_cluster_ntt(logN) && !epi && !rs && !ks) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
       switch (logN) {
         case 14: launch_ntt_cluster<14>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
         case 15: launch_ntt_cluster<15>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
@@ -1129,7 +1236,7 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
     switch (logN) {
 #define HS_NTT_CASE(L) \
   case L:              \
-    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s, epi, rs); \
+    launch_ntt<L>(in, in_stride, out, out_stride, rm, rm2, n, batch, inverse, c.dpc(), tw, twd, s, epi, rs, ks); \
     break;
       HS_NTT_CASE(9) HS_NTT_CASE(10) HS_NTT_CASE(11) HS_NTT_CASE(12) HS_NTT_CASE(13) HS_NTT_CASE(14)
       HS_NTT_CASE(15) HS_NTT_CASE(16) HS_NTT_CASE(17)
@@ -1610,6 +1717,17 @@ void launch_conv_a(const uint64_t* in, size_t in_stride, uint64_t* out, size_t o
   k_conv<A><<<g, kT, 0, s>>>(in, in_stride, out, out_stride, jobs, c.dpc(), c.spec.logN);
 }
 
+// HS_KS_FUSION bit 0: rotate's automorphism inside the key switch (default on: 184 -> 176 us
+// per ciphertext at N=2^16, L=24); bit 1: mul_relin's tensor product inside it (default off:
+// the extra loads and products in the register-capped ModDown pass cost more than k_tensor).
+bool use_ks_fusion(int mode_bit) {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_KS_FUSION");
+    return e ? std::atoi(e) : 1;
+  }();
+  return (mode & mode_bit) != 0;
+}
+
 bool use_conv_mma() {
   static const int mode = [] {
     const char* e = std::getenv("HS_CONV_MMA");
@@ -1668,8 +1786,11 @@ void launch_conv(uint32_t nsrc, uint32_t ntgt, const uint64_t* in, size_t in_str
 
 // Key-switch `batch` polynomials d ([nl][N] each, NTT form, stride d_stride) with key
 // kk; out_w = ModDown(acc_w) + add_w  ([2][nl][N] per batch item, stride out_stride).
+// With src (mode KS_TENSOR / KS_PERM), d and add_w are not materialised: the first
+// iNTT pass computes d from src and the ModDown store adds add_w from src.
 void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, const Ctx::Key& kk, const uint64_t* add0,
-                const uint64_t* add1, size_t add_stride, uint64_t* out, size_t out_stride, uint32_t batch) {
+                const uint64_t* add1, size_t add_stride, uint64_t* out, size_t out_stride, uint32_t batch,
+                const KsSrc* src = nullptr) {
   Runtime& rt = Runtime::get();
   cudaStream_t s = rt.stream();
   const KsPlan& P = ks_plan(c, level);
@@ -1686,7 +1807,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   uint64_t* CV = dptr<uint64_t>(conv);
   const auto qrows = iota_rows(nl);
   // ModUp: d -> coefficient form (out of place), convert every digit, NTT the new rows
-  ntt_rows(c, d, d_stride, DC, dc_stride, qrows, qrows, qrows, batch, true);
+  ntt_rows(c, d, d_stride, DC, dc_stride, qrows, qrows, qrows, batch, true, nullptr, nullptr, src);
   const ConvJob* up = dptr<const ConvJob>(P.up_jobs);
   const uint2* FR = dptr<const uint2>(P.frags);
   launch_conv(c.alpha, nx - c.alpha, DC, dc_stride, EXT, ext_stride, up, FR, P.n_full, c, batch);
@@ -1699,11 +1820,12 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   {
     const unsigned g = (unsigned)((size_t(nx) * N + kT - 1) / kT);
     const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
+    const KsSrc ksrc = src ? *src : KsSrc{};
     switch (nd) {
 #define HS_INNER_CASE(D)                                                                                          \
   case D:                                                                                                         \
     k_ks_inner<D><<<g, kT, 0, s>>>(EXT, ext_stride, d, d_stride, ACC, acc_stride, KB, KA, c.dpc(), nx, nl, c.np, \
-                                   c.nq, c.alpha, logN, batch);                                                   \
+                                   c.nq, c.alpha, logN, batch, ksrc);                                             \
     break;
       HS_INNER_CASE(1) HS_INNER_CASE(2) HS_INNER_CASE(3) HS_INNER_CASE(4) HS_INNER_CASE(5) HS_INNER_CASE(6)
       HS_INNER_CASE(7) HS_INNER_CASE(8) HS_INNER_CASE(9) HS_INNER_CASE(10) HS_INNER_CASE(11) HS_INNER_CASE(12)
@@ -1720,7 +1842,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   // out_w = (acc_w - conv_w) * P^-1 (+ add_w), conv_w never stored
   const MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh),
                   acc_stride, add_stride, out_stride, nl, nx};
-  ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv_rows, P.cv_rows, P.cv_primes, batch, false, &epi);
+  ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv_rows, P.cv_rows, P.cv_primes, batch, false, &epi, nullptr, src);
   cuda_ok(cudaGetLastError(), "key switch");
 }
 
@@ -1733,6 +1855,16 @@ void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uin
   const uint32_t N = c.N, nl = level + 1;
   const size_t ct = size_t(2) * nl * N, half = size_t(nl) * N;
   const Ctx::Key& key = c.relin_key();
+  if (use_ks_fusion(2)) {  // tensor product computed inside the key switch's first and last passes
+    KsSrc src;
+    src.mode = KS_TENSOR;
+    src.a = a;
+    src.b = b;
+    src.stride = ct;
+    src.nl = nl;
+    key_switch(c, level, nullptr, 0, key, nullptr, nullptr, 0, out, ct, batch, &src);
+    return;
+  }
   DevBuf d = rt.alloc(size_t(batch) * 3 * half);
   uint64_t* D = dptr<uint64_t>(d);
   // layout per batch item: [d0 | d1 | d2], stride 3*half
@@ -1783,6 +1915,16 @@ void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out
   const size_t ct = size_t(2) * nl * N;
   const uint64_t g = Ctx::galois_elt(k, c.spec.logN);
   const Ctx::Key& key = c.galois_key(g);
+  if (use_ks_fusion(1)) {  // automorphism applied by the key switch's first-pass load and last-pass store
+    KsSrc src;
+    src.mode = KS_PERM;
+    src.a = in;
+    src.stride = ct;
+    src.g = g;
+    src.nl = nl;
+    key_switch(c, level, nullptr, 0, key, nullptr, nullptr, 0, out, ct, batch, &src);
+    return;
+  }
   DevBuf perm = rt.alloc(size_t(batch) * ct);
   uint64_t* PM = dptr<uint64_t>(perm);
   k_automorph<<<dim3(grid_of(ct), 1, batch), kT, 0, rt.stream()>>>(PM, in, g, c.spec.logN, 2 * nl, ct);

@@ -137,7 +137,7 @@ void ntt(const Ctx& c, uint64_t* data, const std::vector<uint32_t>& prime_of, ui
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
               const std::vector<uint32_t>& irows, const std::vector<uint32_t>& orows,
               const std::vector<uint32_t>& primes, uint32_t batch, bool inverse, const void* epilogue = nullptr,
-              const void* rescale_epi = nullptr);
+              const void* rescale_epi = nullptr, const void* ks_src = nullptr);
 // Symmetric RLWE encryption of N integer coefficients (host array) at `level`
 // (c1 = a, c0 = NTT(m + e) - a s; seeded by spec.seed and `tag`), and decryption
 // to centred integers mod q_0 (valid while |m| < q_0 / 2).

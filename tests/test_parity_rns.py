@@ -258,3 +258,33 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_CONV_MMA": "0"},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode", ["0", "3"])
+def test_key_switch_fusion_options_match_oracle(mode):
+    """HS_KS_FUSION=0 (tensor and automorphism materialised) and =3 (both computed inside the key
+    switch's passes) give the same limbs as the oracle for HMult and rotations."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from rns_abi import RnsOracle, Spec
+from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
+O = RnsOracle()
+for s in (Spec(logN=9, L=3, K=2, dnum=2), Spec(logN=12, L=7, K=3, dnum=3, seed=11),
+          Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44)):
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
+    for level in (s.L, s.L - 1):
+        a, b = O.random_ct(s, level, 1), O.random_ct(s, level, 2)
+        A, B = DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)
+        assert np.array_equal(c.mul_relin(level, A, B).download(), O.mul_relin(s, level, a, b)), s
+        for k in (1, -3):
+            assert np.array_equal(c.rotate(level, k, A).download(), O.rotate(s, level, k, a)), (s, k)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_KS_FUSION": mode},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
