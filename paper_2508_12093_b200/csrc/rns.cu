@@ -551,6 +551,128 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* i
   }
 }
 
+// ---- ModUp's last NTT pass fused with the key-switch inner product -------------------
+// One block = one tile of extended limb x (blockIdx.z) of one batch item (blockIdx.x,
+// fastest, so the blocks that share a key tile run together and read it from L2).  For
+// every digit j: the row pass of ext_j[x] (its column pass already ran) or, on the
+// digit's own limbs, the NTT-form input itself; the last NTT step multiplies by the
+// key words and accumulates into shared memory (the same thread owns the same words in
+// every digit).  acc_w[x] = sum_j e_j[x] key_w[j][x] is written once: the extended
+// rows never go back to HBM after their NTT and k_ks_inner disappears.
+struct InnerArgs {
+  const uint64_t* ext;  // [nd][nx][N] per batch item, after the column pass
+  size_t ext_stride;
+  const uint64_t* d;    // own limbs (NTT form) [nl][N], unless src says otherwise
+  size_t d_stride;
+  KsSrc src;
+  const uint64_t* kb;   // keys [dnum][np][N]
+  const uint64_t* ka;
+  uint64_t* acc;        // [2][nx][N] per batch item
+  size_t acc_stride;
+  uint32_t nx, nl, nd, alpha, np, nq;
+};
+
+struct SmStore {  // last NTT step: back into the tile, in place (a group's outputs are its inputs' words)
+  uint64_t* sm;
+  __device__ void operator()(size_t off, uint64_t v) const { sm[swz(uint32_t(off))] = v; }
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(kNT, 4) k_ntt_rows_inner(const __grid_constant__ InnerArgs A, const PrimeC* pcs,
+                                                          const uint64_t* tw, const double* twd) {
+  using G = NttGeom<LOGN, true>;
+  constexpr uint32_t N = 1u << LOGN;
+  constexpr uint32_t TILE = 1u << (G::logTPB + G::logC);
+  constexpr uint32_t PER = (TILE + kNT - 1) / kNT;  // words per thread in the MAC phase
+  __shared__ uint64_t sm[kNTile];
+  __shared__ double acc_s[2][kNTile];  // thread t owns words t + kNT r (conflict-free)
+  const uint32_t b = blockIdx.x, x = blockIdx.z;
+  const uint32_t gi = x < A.nl ? x : A.nq + (x - A.nl);
+  const PrimeC& P = pcs[gi];
+  const uint32_t tile0 = blockIdx.y << G::logTPB;
+  const size_t toff = size_t(tile0) << G::logC;
+  const uint64_t* psi = tw + size_t(gi) * 4 * N;
+  const uint64_t* psip = psi + N;
+  const double* twp = twd + size_t(gi) * 2 * N;
+  const uint32_t own = x < A.nl ? x / A.alpha : 0xFFFFFFFFu;
+  uint64_t* accu0 = reinterpret_cast<uint64_t*>(acc_s[0]);
+  uint64_t* accu1 = reinterpret_cast<uint64_t*>(acc_s[1]);
+  for (uint32_t j = 0; j < A.nd; ++j) {
+    const size_t krow = (size_t(j * A.np + gi) << LOGN) + toff;
+    uint64_t v[PER];
+    if (j == own) {  // the digit's own limb: d itself (NTT form), no conversion
+#pragma unroll
+      for (uint32_t r = 0; r < PER; ++r) {
+        const uint32_t e = threadIdx.x + r * kNT;
+        if (TILE % kNT != 0 && e >= TILE) break;
+        const uint32_t n = uint32_t(toff) + e;
+        if (A.src.mode == KS_TENSOR) {
+          const size_t o = b * A.src.stride + (size_t(A.nl + x) << LOGN) + n;
+          v[r] = mul_mod(A.src.a[o], A.src.b[o], P);
+        } else if (A.src.mode == KS_PERM) {
+          v[r] = A.src.a[b * A.src.stride + (size_t(A.nl + x) << LOGN) + galois_src(n, A.src.g, LOGN)];
+        } else {
+          v[r] = A.d[b * A.d_stride + (size_t(x) << LOGN) + n];
+        }
+      }
+    } else {
+      const PlainLoad ld{A.ext + b * A.ext_stride + (size_t(j * A.nx + x) << LOGN) + toff};
+      __syncthreads();  // the previous digit is done with sm
+      if (P.fp)
+        ntt_steps_fp<false, true, LOGN, 0>(ld, SmStore{sm}, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
+                                           static_cast<double>(P.ninv));
+      else
+        ntt_steps<false, true, LOGN, 0>(ld, SmStore{sm}, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+      __syncthreads();
+#pragma unroll
+      for (uint32_t r = 0; r < PER; ++r) {
+        const uint32_t e = threadIdx.x + r * kNT;
+        if (TILE % kNT != 0 && e >= TILE) break;
+        v[r] = sm[swz(e)];
+      }
+    }
+    // acc_w += v * key_w[j]: all key words of this thread in flight at once
+    uint64_t k0[PER], k1[PER];
+#pragma unroll
+    for (uint32_t r = 0; r < PER; ++r) {
+      const uint32_t e = threadIdx.x + r * kNT;
+      if (TILE % kNT != 0 && e >= TILE) break;
+      k0[r] = __ldg(A.kb + krow + e);
+      k1[r] = __ldg(A.ka + krow + e);
+    }
+#pragma unroll
+    for (uint32_t r = 0; r < PER; ++r) {
+      const uint32_t e = threadIdx.x + r * kNT;
+      if (TILE % kNT != 0 && e >= TILE) break;
+      if (P.fp) {  // exact fp64 products (|t| < q); sums of <= 15 terms stay below 2^53
+        const double y = u2d(v[r]);
+        const double t0 = fp_mulmod(y, u2d(k0[r]), P.qd, P.qinvd);
+        const double t1 = fp_mulmod(y, u2d(k1[r]), P.qd, P.qinvd);
+        acc_s[0][e] = j == 0 ? t0 : __dadd_rn(acc_s[0][e], t0);
+        acc_s[1][e] = j == 0 ? t1 : __dadd_rn(acc_s[1][e], t1);
+      } else {
+        const uint64_t t0 = mul_mod(v[r], k0[r], P), t1 = mul_mod(v[r], k1[r], P);
+        accu0[e] = j == 0 ? t0 : add_mod(accu0[e], t0, P.q);
+        accu1[e] = j == 0 ? t1 : add_mod(accu1[e], t1, P.q);
+      }
+    }
+  }
+  uint64_t* o0 = A.acc + b * A.acc_stride + (size_t(x) << LOGN) + toff;
+  uint64_t* o1 = o0 + (size_t(A.nx) << LOGN);
+#pragma unroll
+  for (uint32_t r = 0; r < PER; ++r) {
+    const uint32_t e = threadIdx.x + r * kNT;
+    if (TILE % kNT != 0 && e >= TILE) break;
+    if (P.fp) {
+      o0[e] = fp_canon(acc_s[0][e], P.qd, P.qinvd);
+      o1[e] = fp_canon(acc_s[1][e], P.qd, P.qinvd);
+    } else {
+      o0[e] = accu0[e];
+      o1[e] = accu1[e];
+    }
+  }
+}
+
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
@@ -1720,6 +1842,59 @@ void launch_conv_a(const uint64_t* in, size_t in_stride, uint64_t* out, size_t o
 // HS_KS_FUSION bit 0: rotate's automorphism inside the key switch (default on: 184 -> 176 us
 // per ciphertext at N=2^16, L=24); bit 1: mul_relin's tensor product inside it (default off:
 // the extra loads and products in the register-capped ModDown pass cost more than k_tensor).
+// HS_KS_INNER=1: ModUp's row pass fused with the key inner product (k_ntt_rows_inner).  Off by
+// default: correct, but 892 us per 16 ciphertexts against 404 + 362 us for the row pass plus
+// k_ks_inner (three dependent load/NTT/MAC phases per block at 4 blocks/SM expose the load
+// latency that six independent row-pass blocks hide).
+bool use_inner_fusion() {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_KS_INNER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0;
+}
+
+template <int LOGN>
+void launch_cols_and_inner(const Ctx& c, uint64_t* ext, size_t ext_stride, const std::vector<uint32_t>& rows,
+                           const std::vector<uint32_t>& primes, const InnerArgs& ia, uint32_t batch, cudaStream_t s) {
+  using Gc = NttGeom<LOGN, false>;
+  using Gr = NttGeom<LOGN, true>;
+  const uint64_t* tw = dptr<const uint64_t>(c.d_tw);
+  const double* twd = dptr<const double>(c.d_twd);
+  PassEpi none{};
+  for (size_t base = 0; base < rows.size(); base += kMaxRows) {  // column passes of the converted rows, in place
+    const uint32_t n = static_cast<uint32_t>(std::min<size_t>(kMaxRows, rows.size() - base));
+    RowMap rm{};
+    for (uint32_t i = 0; i < n; ++i) {
+      rm.irow[i] = rm.orow[i] = static_cast<uint16_t>(rows[base + i]);
+      rm.prime[i] = static_cast<uint8_t>(primes[base + i]);
+    }
+    const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch);
+    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(ext, ext_stride, ext, ext_stride, rm, c.dpc(), tw, twd, none);
+    Runtime::get().note_launch();
+  }
+  const dim3 g(batch, 1u << (Gr::logR1 - Gr::logTPB), ia.nx);
+  k_ntt_rows_inner<LOGN><<<g, kNT, 0, s>>>(ia, c.dpc(), tw, twd);
+  Runtime::get().note_launch();
+}
+
+void cols_and_inner(const Ctx& c, uint64_t* ext, size_t ext_stride, const std::vector<uint32_t>& rows,
+                    const std::vector<uint32_t>& primes, const InnerArgs& ia, uint32_t batch) {
+  cudaStream_t s = Runtime::get().stream();
+  switch (c.spec.logN) {
+#define HS_CI_CASE(L) \
+  case L:             \
+    launch_cols_and_inner<L>(c, ext, ext_stride, rows, primes, ia, batch, s); \
+    break;
+    HS_CI_CASE(9) HS_CI_CASE(10) HS_CI_CASE(11) HS_CI_CASE(12) HS_CI_CASE(13) HS_CI_CASE(14) HS_CI_CASE(15)
+    HS_CI_CASE(16) HS_CI_CASE(17)
+#undef HS_CI_CASE
+    default:
+      fail(HS_E_INVALID_ARG, "ntt: unsupported ring degree");
+  }
+  cuda_ok(cudaGetLastError(), "modup ntt + inner product");
+}
+
 bool use_ks_fusion(int mode_bit) {
   static const int mode = [] {
     const char* e = std::getenv("HS_KS_FUSION");
@@ -1815,11 +1990,18 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
     const uint32_t rest = nl - P.n_full * c.alpha;
     launch_conv(rest, nx - rest, DC, dc_stride, EXT, ext_stride, up + P.n_full, FR, nd - P.n_full, c, batch);
   }
+  const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
+  if (use_inner_fusion() && nd <= 15) {
+    // column pass of the converted rows, then their row pass with the key inner product
+    // as its store (acc_w written once, the NTT'd extended rows never stored)
+    const InnerArgs ia{EXT, ext_stride, d, d_stride, src ? *src : KsSrc{}, KB, KA, ACC, acc_stride,
+                       nx, nl, nd, c.alpha, c.np, c.nq};
+    cols_and_inner(c, EXT, ext_stride, P.up_rows, P.up_primes, ia, batch);
+  } else {
   ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
   // inner product with the key (each key word read once per call)
   {
     const unsigned g = (unsigned)((size_t(nx) * N + kT - 1) / kT);
-    const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
     const KsSrc ksrc = src ? *src : KsSrc{};
     switch (nd) {
 #define HS_INNER_CASE(D)                                                                                          \
@@ -1834,6 +2016,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
       default:
         fail(HS_E_INVALID_ARG, "key switch: more than 15 digits");
     }
+  }
   }
   // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
   ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);

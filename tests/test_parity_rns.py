@@ -260,10 +260,11 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode", ["0", "3"])
-def test_key_switch_fusion_options_match_oracle(mode):
-    """HS_KS_FUSION=0 (tensor and automorphism materialised) and =3 (both computed inside the key
-    switch's passes) give the same limbs as the oracle for HMult and rotations."""
+@pytest.mark.parametrize("mode,inner", [("0", "0"), ("3", "0"), ("1", "1"), ("3", "1")])
+def test_key_switch_fusion_options_match_oracle(mode, inner):
+    """HS_KS_FUSION=0 (tensor and automorphism materialised) / =3 (both computed inside the key
+    switch's passes), with and without HS_KS_INNER=1 (ModUp row pass fused with the key inner
+    product), give the same limbs as the oracle for HMult and rotations."""
     import os
     import subprocess
     import sys
@@ -285,6 +286,7 @@ for s in (Spec(logN=9, L=3, K=2, dnum=2), Spec(logN=12, L=7, K=3, dnum=3, seed=1
 print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_KS_FUSION": mode},
+    r = subprocess.run([sys.executable, "-c", code], cwd=root,
+                       env={**os.environ, "HS_KS_FUSION": mode, "HS_KS_INNER": inner},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
