@@ -69,8 +69,9 @@ class Runtime {
   int prog_lanes = 2;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
 
   // Persistent device scratch buffer `slot` of at least n doubles (grown on
-  // demand).  All device work is ordered on one stream, so reuse is race-free.
-  double* scratch(int slot, size_t n);
+  // demand; zero-filled when (re)allocated if `zero`).  All device work is ordered
+  // on one stream, so reuse is race-free.
+  double* scratch(int slot, size_t n, bool zero = false);
 
  private:
   Runtime(int device);

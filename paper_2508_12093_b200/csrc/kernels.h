@@ -111,7 +111,7 @@ struct StatArgs {
   double cm[2] = {0, 0}, ca[2] = {0, 0}, cmp[2] = {0, 0};
   int power = 0;          // 0: no phase B; 3, 4: centred power of x; 2: x-y product (pearson)
   double inv_n = 0;
-  double* partial = nullptr;  // >= gridDim.x * 16 doubles
+  double* partial = nullptr;  // stat_partial_doubles(), zero between launches: grid-wide totals + counters
   double* scratch = nullptr;  // >= 2 * 6 * S doubles (butterfly fallback)
 };
 void run_stat(QSpec q, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s);

@@ -375,7 +375,7 @@ k::StatArgs stat_args(hs_ctx* ctx, const std::vector<const ColC*>& cols, int mod
   }
   for (size_t c = 0; c < cols[0]->chunks.size(); ++c) a.valid[c] = flow::chunk_valid(S, cols[0]->n_valid, c);
   a.inv_n = 1.0 / static_cast<double>(cols[0]->n_valid);  // mean_of_chunks, stats.hpp:83
-  a.partial = rt.scratch(0, k::stat_partial_doubles());
+  a.partial = rt.scratch(0, k::stat_partial_doubles(), true);
   a.scratch = rt.scratch(1, 24 * S);
   return a;
 }

@@ -99,11 +99,12 @@ DevBuf Runtime::alloc(size_t n) {
 
 void Runtime::sync() { cuda_ok(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
-double* Runtime::scratch(int slot, size_t n) {
+double* Runtime::scratch(int slot, size_t n, bool zero) {
   std::lock_guard<std::mutex> g(scratch_mu_);
   if (scratch_n_[slot] < n) {
     scratch_[slot] = alloc(n);  // the old buffer is freed stream-ordered
     scratch_n_[slot] = n;
+    if (zero) cuda_ok(cudaMemsetAsync(scratch_[slot].get(), 0, n * sizeof(double), stream_), "scratch zero");
   }
   return scratch_[slot].get();
 }

@@ -62,7 +62,7 @@ __device__ __forceinline__ void stamp(int) {}
 // that overlaps the wait for the slowest block, e.g. staging the Chebyshev table).
 template <class Q, class TermFn, class IdleFn>
 __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int NK, unsigned S,
-                            double* partial, double* scratch, IdleFn idle) {
+                            double* accum, unsigned* count, double* scratch, IdleFn idle) {
   __shared__ double red[kMaxWarps][2 * kNK];
   __shared__ double tot[2 * kNK];
   const Range BR = block_range(S);
@@ -89,44 +89,26 @@ __device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int 
 #pragma unroll
       for (int k = 0; k < 2 * kNK; ++k) red[threadIdx.x >> 5][k] = acc[k];
     __syncthreads();
+    // this block's sums go straight into the grid-wide totals: every term is an integer
+    // and the checked bound keeps every partial sum below 2^53, so the atomic additions
+    // are exact in any order (and a failed bound is never under-reported: rounding is
+    // monotone and 2^52 is representable)
     if (threadIdx.x < 2 * NK) {
       double s = 0.0;
       for (unsigned w = 0; w < blockDim.x / 32; ++w) s += red[w][threadIdx.x];
-      partial[blockIdx.x * 2 * kNK + threadIdx.x] = s;
+      atomicAdd(accum + threadIdx.x, s);
     }
     stamp(5);
     idle();
     grid.sync();
     stamp(6);
-    // every block sums the gridDim.x partials of every value; all terms are integers
-    // and the checked bound keeps every partial sum below 2^53, so the totals are
-    // exact in any order: all threads load in parallel (one L2 round trip), then a
-    // shared-memory tree per value
-    {
-      constexpr unsigned NV = 2 * kNK;
-      const unsigned nb = gridDim.x, nt = blockDim.x;
-      // thread t sums blocks t, t + nt, ... for every value (gridDim.x <= 2 * nt in practice)
-      double accp[NV];
-#pragma unroll
-      for (unsigned k = 0; k < NV; ++k) accp[k] = 0.0;
-      for (unsigned b = threadIdx.x; b < nb; b += nt)
-#pragma unroll
-        for (unsigned k = 0; k < NV; ++k)
-          if (k < static_cast<unsigned>(2 * NK)) accp[k] += __ldcg(partial + b * 2 * kNK + k);
-#pragma unroll
-      for (unsigned k = 0; k < NV; ++k)
-        for (int o = 16; o > 0; o >>= 1) accp[k] += __shfl_xor_sync(0xffffffffu, accp[k], o);
-      if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (unsigned k = 0; k < NV; ++k) red[threadIdx.x >> 5][k] = accp[k];
-      __syncthreads();
-      if (threadIdx.x < static_cast<unsigned>(2 * NK)) {
-        double t = 0.0;
-        for (unsigned w = 0; w < nt / 32; ++w) t += red[w][threadIdx.x];
-        tot[threadIdx.x] = t;
-      }
-    }
+    if (threadIdx.x < 2 * NK) tot[threadIdx.x] = __ldcg(accum + threadIdx.x);
     __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(count, 1u) == gridDim.x - 1) {
+      // the last block to read the totals zeroes them for the next launch
+      for (int k = 0; k < 2 * NK; ++k) accum[k] = 0.0;
+      *count = 0u;
+    }
     stamp(7);
     bool exact = true;
     for (int k = 0; k < NK; ++k) {
@@ -204,7 +186,8 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
     }
   };
   stamp(1);
-  const Reduced RA = grid_sum(q, grid, termsA, NA, S, a.partial, a.scratch, stage);
+  unsigned* counts = reinterpret_cast<unsigned*>(a.partial + 4 * kNK);
+  const Reduced RA = grid_sum(q, grid, termsA, NA, S, a.partial, counts, a.scratch, stage);
   stamp(2);
 
   // per-slot statistic values {mu_x, var_x, mu_y, var_y}
@@ -246,7 +229,7 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
         t[0] = c == 0 ? term : q.add(t[0], term);
       }
     };
-    RB = grid_sum(q, grid, termsB, 1, S, a.partial + gridDim.x * 2 * kNK,
+    RB = grid_sum(q, grid, termsB, 1, S, a.partial + 2 * kNK, counts + 1,
                   a.scratch + 2 * static_cast<size_t>(kNK) * S, [] {});
   }
 
@@ -300,7 +283,7 @@ int max_blocks(K kern, size_t smem, int threads) {
 
 }  // namespace
 
-size_t stat_partial_doubles() { return 2 * 2 * kNK * static_cast<size_t>(Runtime::get().sm_count()) * 32; }
+size_t stat_partial_doubles() { return 4 * kNK + 2; }  // two sets of 2 kNK totals, two block counters
 
 void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s) {
   if (p.S == 0) return;
