@@ -356,6 +356,17 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
     return sec
 
 
+def kstat_traffic():
+    """DRAM bytes per k_stat launch from the committed ncu --set full summary (None if absent)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_kstat_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["dram_bytes_read"] + d["dram_bytes_write"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def c5_tier_e(torch, stream, S_, batch=64, pools=8, reps=3, ops=None):
     """C5 tier E: batched EvalContext ops on `batch` ciphertexts of S_ U[-1,1] slots.
     Device time per batch via graph replay over `pools` distinct input batches (> L2);
@@ -579,7 +590,11 @@ def main():
     # grid-unit formulation of quant.cuh: mul_ct 3, mul_pt 2, add_pt 2, add/sub 1
     mul_ct, mul_pt, add_pt, add_ct = 263 + 18, 256 + 6 + 1, 256 + 8 + 1, 255 + 8 + 6
     fp64_per_slot = 3 * mul_ct + 2 * mul_pt + 2 * add_pt + add_ct
-    achieved = fp64_per_slot * S / (prog_us * 1e-6) / 1e12
+    prog_achieved = fp64_per_slot * S / (prog_us * 1e-6) / 1e12
+    # the step kernel (k_stat, one launch per znorm) adds to the invsqrt program, per slot:
+    # phase A moment terms (3 mul_pt + 1 mul_ct = 9), their exact sums (sum and |sum| of 3 terms = 6),
+    # the variance (sub + mul_ct = 4) and z = (x - mu) * inv (sub + mul_ct = 4)
+    step_per_slot = fp64_per_slot + 9 + 6 + 4 + 4
     from paper_2508_12093_b200 import _abi
     import ctypes
     rate = ctypes.c_double(0)
@@ -593,6 +608,8 @@ def main():
     dev_ms, e2e_ms = float(t[0]), float(t[1])
     if rank == 0:
         value = dev_ms / (args.steps * ws)
+        step_us = 1e3 * dev_ms / args.steps  # one k_stat launch per step, CUDA events over the timed region
+        achieved = step_per_slot * S / (step_us * 1e-6) / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": False,
@@ -604,12 +621,20 @@ def main():
                     "d2h_bytes_per_step": S * 8, "wall_ms_per_step": e2e_wall_ms / e2e_steps},
             "gpu_launches": int(launches),
             "api_loop_ms_per_step": api_ms / args.steps,
-            "roofline": {"bound": "fp64", "kernel": "k_prog (fused crypto_invsqrt, degree 511 + 6 Newton)",
+            "roofline": {"bound": "fp64",
+                         "kernel": "k_stat<QGrid,2> (the step: fused C2 znorm = moments, grid-wide exact sums, "
+                                   "invsqrt degree 511 + 6 Newton, (x - mu) * inv)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None, "duration_us": prog_us,
-                         "work": f"{fp64_per_slot} fp64 ops/slot x {S} slots",
+                         "traffic": kstat_traffic(), "duration_us": step_us,
+                         "work": f"{step_per_slot} fp64 ops/slot x {S} slots",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
-                                        "MEASURED_PEAKS.json has no FP64 figure"},
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "traffic_source": "profiles/r1_kstat_ncu.json (ncu --set full, cold caches: input, "
+                                           "code and parameters; algorithmic 512 KiB)",
+                         "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",
+                                            "duration_us": prog_us, "achieved": prog_achieved,
+                                            "frac": prog_achieved / peak,
+                                            "work": f"{fp64_per_slot} fp64 ops/slot x {S} slots"}},
             "kernels_us": {"moments_stat_kernel": mom_us, "invsqrt_prog_kernel": prog_us,
                            "note": "graph replay per call, includes ~1-2 us node overhead"},
             "clocks": clk.summary(),
