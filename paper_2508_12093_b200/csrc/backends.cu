@@ -15,16 +15,15 @@ namespace {
 // Where the device can read the caller's buffer directly (pinned, host-mapped
 // under UVA) the encrypt kernel reads it zero-copy; otherwise stage it through
 // a device buffer.  Returns the device-visible source pointer.
-const double* device_source(const double* v, size_t n, DevBuf* stage, bool* pinned) {
+const double* device_source(const double* v, size_t n, DevBuf* stage, bool* pinned, cudaStream_t s) {
   Runtime& rt = Runtime::get();
   cudaPointerAttributes at{};
   *pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
   cudaGetLastError();
   if (*pinned && at.devicePointer) return static_cast<const double*>(at.devicePointer);
   if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return v;
-  *stage = rt.alloc(n);
-  cuda_ok(cudaMemcpyAsync(stage->get(), v, n * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
-          "encrypt upload");
+  *stage = s == rt.stream() ? rt.alloc(n) : rt.alloc_on(n, s);
+  cuda_ok(cudaMemcpyAsync(stage->get(), v, n * sizeof(double), cudaMemcpyHostToDevice, s), "encrypt upload");
   return stage->get();
 }
 
@@ -41,7 +40,7 @@ Ct DevB::encrypt(const double* v, size_t n) const {
   DevBuf d = rt.alloc(p_.S);
   DevBuf stage;
   bool pinned = false;
-  const double* src = n ? device_source(v, n, &stage, &pinned) : nullptr;
+  const double* src = n ? device_source(v, n, &stage, &pinned, rt.stream()) : nullptr;
   k::encrypt(qs_, src, n, d.get(), p_.S, nullptr, rt.stream());
   if (pinned) rt.sync();  // the caller may reuse its pinned buffer on return
   return ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0);
@@ -51,18 +50,25 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
   Runtime& rt = Runtime::get();
   std::vector<Ct> out;
   if (n == 0) return out;
+  // On the upload stream (unless the compute stream is being captured): the host input is
+  // read and encrypted beside whatever the compute stream is running, and only this work is
+  // waited for below.
+  const bool side = !rt.capturing();
+  cudaStream_t s = side ? rt.upload_stream() : rt.stream();
   DevBuf stage;
   bool pinned = false;
-  const double* src = device_source(v, n, &stage, &pinned);
+  const double* src = device_source(v, n, &stage, &pinned, s);
   int* bad = bad_flag();
   *bad = 0;
   for (size_t off = 0; off < n; off += p_.S) {
     const size_t take = std::min(p_.S, n - off);
-    DevBuf d = rt.alloc(p_.S);
-    k::encrypt(qs_, src + off, take, d.get(), p_.S, bad, rt.stream());
+    DevBuf d = side ? rt.alloc_on(p_.S, s) : rt.alloc(p_.S);
+    k::encrypt(qs_, src + off, take, d.get(), p_.S, bad, s);
     out.push_back(ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0));
   }
-  rt.sync();  // the finiteness verdict (and the caller's buffer) must be settled before returning
+  // the finiteness verdict (and the caller's buffer) must be settled before returning; the
+  // outputs are then complete for any later compute-stream work
+  cuda_ok(cudaStreamSynchronize(s), "encode_column sync");
   if (*bad) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
   return out;
 }

@@ -8,6 +8,7 @@
 // slots() reads.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -59,9 +60,17 @@ class Runtime {
   static void init(int device); // optional explicit device choice (before first use)
 
   cudaStream_t stream() const { return stream_; }
+  // Host-input stream of encode_column: its copy/encrypt kernels run beside the compute
+  // stream's kernels (a caller can encode the next column while the current one computes).
+  // encode_column synchronises it before returning, so its outputs are complete for any
+  // later work on the compute stream without an event.
+  cudaStream_t upload_stream() const { return upload_; }
+  bool capturing() const;                   // the compute stream is being captured into a graph
   int device() const { return device_; }
   int sm_count() const { return sms_; }
   DevBuf alloc(size_t n_doubles);           // stream-ordered; freed stream-ordered
+  // allocated in `on`'s order, freed in the compute stream's order (where its consumers run)
+  DevBuf alloc_on(size_t n_doubles, cudaStream_t on);
   void sync();
   void note_launch(uint64_t n = 1) { launches_ += n; }
   uint64_t launches() const { return launches_.load(); }
@@ -78,11 +87,23 @@ class Runtime {
   int device_ = 0;
   int sms_ = 148;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t upload_ = nullptr;
   std::atomic<uint64_t> launches_{0};
   std::mutex scratch_mu_;
   DevBuf scratch_[4];
   size_t scratch_n_[4] = {0, 0, 0, 0};
 };
+
+// L1/shared carveout (percent of the unified 228 KB) shared by the statistics kernels and
+// encode_column's k_encrypt: SMs only host kernels of one carveout at a time, so both use
+// the same small one (k_stat needs <= ~15 KB of shared memory).  HS_CARVEOUT overrides.
+inline int carveout_pct() {
+  static const int v = [] {
+    const char* e = std::getenv("HS_CARVEOUT");
+    return e ? std::atoi(e) : 10;
+  }();
+  return v;
+}
 
 // ---- Ciphertext storage ------------------------------------------------------
 // grid > 0 records that every slot is a multiple of 2^-grid (the output of a

@@ -68,7 +68,10 @@ struct MInst {
 };
 constexpr int kMaxInst = 40;
 constexpr int kMaxArr = 6;
-constexpr int kMaxChunks = 48;
+#ifndef HS_MAXCH
+#define HS_MAXCH 48
+#endif
+constexpr int kMaxChunks = HS_MAXCH;
 constexpr int kRegs = 24;
 constexpr int kMaxFusedDegree = 1023;
 constexpr int kMaxFusedNewtonN = 6;

@@ -80,8 +80,13 @@ __global__ void __launch_bounds__(kThreads) k_requant(Q q, const double* __restr
 // may be host memory mapped into the device (zero-copy over PCIe): two slots per
 // thread with 16-byte reads when `src` is 16-byte aligned, so each PCIe read carries
 // more payload.
+// Small blocks (64 threads, <= 32 registers): they fit in the register file a running
+// statistics kernel leaves free on every SM sub-partition (k_stat: 448 threads x 120
+// registers), so encode_column on the upload stream overlaps the compute stream instead
+// of queueing behind it.
+constexpr int kEncThreads = 64;
 template <class Q, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_encrypt(Q q, const double* __restrict__ src, size_t n,
+__global__ void __launch_bounds__(kEncThreads, 32) k_encrypt(Q q, const double* __restrict__ src, size_t n,
                                                        double* __restrict__ o, size_t S, int* bad) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   bool nf = false;
@@ -260,14 +265,31 @@ void requant(QSpec q, const double* a, double* out, size_t n, cudaStream_t s) {
   Runtime::get().note_launch();
 }
 
+inline unsigned enc_grid(size_t n_items) {
+  const size_t want = (n_items + kEncThreads - 1) / kEncThreads;
+  const size_t cap = static_cast<size_t>(Runtime::get().sm_count()) * 16;
+  return static_cast<unsigned>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
 void encrypt(QSpec q, const double* src, size_t n, double* out, size_t S, int* bad, cudaStream_t s) {
   if (S == 0) return;
   const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  static const bool attr = [] {  // same carveout as the statistics kernels (stat.cu): SMs are shared
+    for (const void* f : {reinterpret_cast<const void*>(k_encrypt<QGrid, true>),
+                          reinterpret_cast<const void*>(k_encrypt<QGrid, false>),
+                          reinterpret_cast<const void*>(k_encrypt<QExact, true>),
+                          reinterpret_cast<const void*>(k_encrypt<QExact, false>),
+                          reinterpret_cast<const void*>(k_encrypt<QNone, true>),
+                          reinterpret_cast<const void*>(k_encrypt<QNone, false>)})
+      cuda_ok(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct()), "encrypt carveout");
+    return true;
+  }();
+  (void)attr;
   with_q(q, [&](auto Q) {
     if (vec)
-      k_encrypt<decltype(Q), true><<<grid_for((S + 1) / 2), kThreads, 0, s>>>(Q, src, n, out, S, bad);
+      k_encrypt<decltype(Q), true><<<enc_grid((S + 1) / 2), kEncThreads, 0, s>>>(Q, src, n, out, S, bad);
     else
-      k_encrypt<decltype(Q), false><<<grid_for(S), kThreads, 0, s>>>(Q, src, n, out, S, bad);
+      k_encrypt<decltype(Q), false><<<enc_grid(S), kEncThreads, 0, s>>>(Q, src, n, out, S, bad);
   });
   cuda_ok(cudaGetLastError(), "encrypt launch");
   Runtime::get().note_launch();

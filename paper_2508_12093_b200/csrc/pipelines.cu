@@ -1,4 +1,6 @@
 // pipelines.cu — fused executors (see pipelines.h).
+#include <chrono>
+#include <cstdio>
 #include "pipelines.h"
 
 #include <cmath>
@@ -290,8 +292,17 @@ class PB {
       prog_.tabs = ts.dev.get();
       prog_.ntab = ts.n;
     }
+#ifdef HS_HOST_PROFILE
+    static double tl = 0;
+    static int nl = 0;
+    auto l0 = std::chrono::steady_clock::now();
+#endif
     if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
     else k::run_prog(q_, prog_, lanes, rt.stream());
+#ifdef HS_HOST_PROFILE
+    tl += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - l0).count();
+    if (++nl % 200 == 0) std::fprintf(stderr, "run_stat/run_prog host us/call %.2f (n=%d)\n", tl / nl, nl);
+#endif
   }
 
   int reg() {
@@ -569,15 +580,36 @@ ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
     DevB db(ctx->p, ctx->m);
     return flow::znorm(db, col, B, cfg);
   }
+#ifdef HS_HOST_PROFILE
+  auto T = [] { return std::chrono::steady_clock::now(); };
+  static double acc[6] = {0, 0, 0, 0, 0, 0};
+  static int calls = 0;
+  auto t0 = T();
+#define HS_HP(i) acc[i] += std::chrono::duration<double, std::micro>(T() - t0).count(), t0 = T()
+#else
+#define HS_HP(i)
+#endif
   auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(col).add(B).cfg(cfg), [&](SymB& sb) { return flow::znorm(sb, sym(col), B, cfg); });
+  HS_HP(0);
   Runtime& rt = Runtime::get();
   std::vector<DevBuf> outs;
   for (size_t c = 0; c < col.chunks.size(); ++c) outs.push_back(rt.alloc(ctx->p.S));
+  HS_HP(1);
   PB pb(ctx->p);
   const int inv = pb.invsqrt(pb.ldr(1), B * B, cfg);  // crypto_invsqrt(var, B^2)
   pb.zapply(pb.ldr(0), inv, col.chunks, outs);        // mul_ct(sub_ct(chunk, mu), inv)
-  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
+  HS_HP(2);
+  const k::StatArgs sa = stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+  HS_HP(3);
+  pb.launch_stat(sa);
+  HS_HP(4);
   ctx->m = m;
+#ifdef HS_HOST_PROFILE
+  if (++calls % 200 == 0)
+    std::fprintf(stderr, "znorm host us/call: ledger %.2f alloc %.2f program %.2f args %.2f launch %.2f\n",
+                 acc[0] / calls, acc[1] / calls, acc[2] / calls, acc[3] / calls, acc[4] / calls);
+#endif
+#undef HS_HP
   ColC z;
   z.n_valid = col.n_valid;
   for (size_t c = 0; c < outs.size(); ++c) z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level));

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 namespace hsg {
 namespace rns {
@@ -481,22 +482,29 @@ struct PassEpi {
   KsSrc ks;
 };
 
-template <bool INV, bool ROWS, int LOGN, int MODE = 0>
-__global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
-                                                  size_t out_stride, const __grid_constant__ RowMap rm,
-                                                  const PrimeC* pcs, const uint64_t* tw, const double* twd,
-                                                  const __grid_constant__ PassEpi epi) {
+struct CgLoad {  // L2-coherent load (skips L1): the second pass of the fused NTT reads rows another block just wrote
+  const uint64_t* g;
+  __device__ uint64_t operator()(size_t off) const { return __ldcg(g + off); }
+};
+
+// One pass over tile bx of row-map entry by, batch item bz (the body of k_ntt_pass and
+// of both phases of k_ntt_fused).  CG: plain loads of the pass input go through L2 only.
+template <bool INV, bool ROWS, int LOGN, int MODE, bool CG>
+__device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t bz, uint64_t* sm, const uint64_t* in,
+                                             size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
+                                             const PrimeC* pcs, const uint64_t* tw, const double* twd,
+                                             const PassEpi& epi) {
   using G = NttGeom<LOGN, ROWS>;
-  __shared__ uint64_t sm[kNTile];
+  using PlainLd = std::conditional_t<CG, CgLoad, PlainLoad>;
   constexpr uint32_t N = 1u << LOGN;
-  const uint32_t pi = rm.prime[blockIdx.y];
+  const uint32_t pi = rm.prime[by];
   const PrimeC& P = pcs[pi];
   const uint64_t* psi = tw + size_t(pi) * 4 * N + (INV ? 2 * N : 0);
   const uint64_t* psip = psi + N;
-  const uint32_t tile0 = blockIdx.x << G::logTPB;  // first sub-transform of this block
+  const uint32_t tile0 = bx << G::logTPB;  // first sub-transform of this block
   const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
-  const uint64_t* gi = in + blockIdx.z * in_stride + (size_t(rm.irow[blockIdx.y]) << LOGN) + toff;
-  uint64_t* go = out + blockIdx.z * out_stride + (size_t(rm.orow[blockIdx.y]) << LOGN) + toff;
+  const uint64_t* gi = in + bz * in_stride + (size_t(rm.irow[by]) << LOGN) + toff;
+  uint64_t* go = out + bz * out_stride + (size_t(rm.orow[by]) << LOGN) + toff;
   const double* twp = twd + size_t(pi) * 2 * N + (INV ? N : 0);
   auto run = [&](const auto& ld, const auto& st) {
     if (P.fp)
@@ -507,47 +515,126 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* i
   };
   if constexpr (MODE == 1 || MODE == 6 || MODE == 7) {  // row r = w * nl + i of the ModDown conversion output
     const MdEpi& e = epi.md;
-    const uint32_t r = rm.orow[blockIdx.y], w = r / e.nl, i = r - w * e.nl;
-    const uint64_t* acc = e.acc + blockIdx.z * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff;
-    uint64_t* o = e.out + blockIdx.z * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff;
+    const uint32_t r = rm.orow[by], w = r / e.nl, i = r - w * e.nl;
+    const uint64_t* acc = e.acc + bz * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff;
+    uint64_t* o = e.out + bz * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff;
     if constexpr (MODE == 1) {
       const uint64_t* ad = w == 0 ? e.add0 : e.add1;
-      run(PlainLoad{gi}, MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
-                                         AddRow{ad ? ad + blockIdx.z * e.add_stride + (size_t(i) << LOGN) + toff : nullptr}});
+      run(PlainLd{gi}, MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+                                         AddRow{ad ? ad + bz * e.add_stride + (size_t(i) << LOGN) + toff : nullptr}});
     } else if constexpr (MODE == 6) {
       const KsSrc& k = epi.ks;
-      const uint64_t* a0 = k.a + blockIdx.z * k.stride + (size_t(i) << LOGN) + toff;
-      const uint64_t* b0 = k.b + blockIdx.z * k.stride + (size_t(i) << LOGN) + toff;
+      const uint64_t* a0 = k.a + bz * k.stride + (size_t(i) << LOGN) + toff;
+      const uint64_t* b0 = k.b + bz * k.stride + (size_t(i) << LOGN) + toff;
       const size_t h = size_t(k.nl) << LOGN;
-      run(PlainLoad{gi}, MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(PlainLd{gi}, MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                             AddTensor{a0, a0 + h, b0, b0 + h, P, int(w)}});
     } else {
       const KsSrc& k = epi.ks;
-      const uint64_t* c0 = w == 0 ? k.a + blockIdx.z * k.stride + (size_t(i) << LOGN) : nullptr;
-      run(PlainLoad{gi}, MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      const uint64_t* c0 = w == 0 ? k.a + bz * k.stride + (size_t(i) << LOGN) : nullptr;
+      run(PlainLd{gi}, MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                                 AddPerm<LOGN>{c0, k.g, uint32_t(toff)}});
     }
   } else if constexpr (MODE == 4 || MODE == 5) {  // inverse row pass of d = a1 b1 / sigma(c1), limb irow
     const KsSrc& k = epi.ks;
-    const uint32_t i = rm.irow[blockIdx.y];
-    const uint64_t* r1 = k.a + blockIdx.z * k.stride + (size_t(k.nl + i) << LOGN);
+    const uint32_t i = rm.irow[by];
+    const uint64_t* r1 = k.a + bz * k.stride + (size_t(k.nl + i) << LOGN);
     if constexpr (MODE == 4)
-      run(TnLoad{r1 + toff, k.b + blockIdx.z * k.stride + (size_t(k.nl + i) << LOGN) + toff, P}, PlainStore{go});
+      run(TnLoad{r1 + toff, k.b + bz * k.stride + (size_t(k.nl + i) << LOGN) + toff, P}, PlainStore{go});
     else
       run(PermLoad<LOGN>{r1, k.g, uint32_t(toff)}, PlainStore{go});
   } else if constexpr (MODE == 2) {  // row r = p * level + i: [last_p]_{q_i}
     const RsEpi& e = epi.rs;
-    const uint32_t r = rm.orow[blockIdx.y], p = r / e.level;
-    run(RsLoad{e.last + blockIdx.z * e.last_stride + (size_t(p) << LOGN) + toff, P}, PlainStore{go});
+    const uint32_t r = rm.orow[by], p = r / e.level;
+    run(RsLoad{e.last + bz * e.last_stride + (size_t(p) << LOGN) + toff, P}, PlainStore{go});
   } else if constexpr (MODE == 3) {
     const RsEpi& e = epi.rs;
-    const uint32_t r = rm.orow[blockIdx.y], p = r / e.level, i = r - p * e.level;
-    const RsStore st{e.in + blockIdx.z * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
-                     e.out + blockIdx.z * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
+    const uint32_t r = rm.orow[by], p = r / e.level, i = r - p * e.level;
+    const RsStore st{e.in + bz * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
+                     e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
                      e.qinv_sh[i]};
-    run(PlainLoad{gi}, st);
+    run(PlainLd{gi}, st);
   } else {
-    run(PlainLoad{gi}, PlainStore{go});
+    run(PlainLd{gi}, PlainStore{go});
+  }
+}
+
+template <bool INV, bool ROWS, int LOGN, int MODE = 0>
+__global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                  size_t out_stride, const __grid_constant__ RowMap rm,
+                                                  const PrimeC* pcs, const uint64_t* tw, const double* twd,
+                                                  const __grid_constant__ PassEpi epi) {
+  __shared__ uint64_t sm[kNTile];
+  ntt_pass_dev<INV, ROWS, LOGN, MODE, false>(blockIdx.x, blockIdx.y, blockIdx.z, sm, in, in_stride, out, out_stride, rm,
+                                             pcs, tw, twd, epi);
+}
+
+// ---- both passes in one launch, the intermediate kept in L2 ---------------------------
+// The two-launch NTT writes every limb's first-pass output to HBM and reads it back.  Here
+// blocks take tickets in order: ticket block s holds the first-pass tiles of limb s and the
+// second-pass tiles of limb s - lag.  A second-pass block waits (acquire) until all first-
+// pass tiles of its limb have signalled; those hold smaller tickets, so they are already
+// resident and never wait themselves (no deadlock for any grid size).  With lag ~ 2x the
+// resident blocks, the limb's first-pass output (written in place into `out`) is still in
+// L2 when the second pass reads and overwrites it, so HBM sees one read and one write per
+// word.  Counters self-reset: the last block to finish zeroes them for the next launch
+// (CUDA-graph safe).
+struct FuseCtl {
+  uint32_t* ctr;  // [0] ticket, [1] finished blocks, [2 + limb] first-pass tiles done
+  uint32_t ny, nlimb, lag, total, bz0;  // bz0: first batch item of this launch
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool INV, int LOGN, int M1, int M2>
+__global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_fused(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                   size_t out_stride, const __grid_constant__ RowMap rm,
+                                                   const __grid_constant__ RowMap rm2, const PrimeC* pcs,
+                                                   const uint64_t* tw, const double* twd,
+                                                   const __grid_constant__ PassEpi epi,
+                                                   const __grid_constant__ FuseCtl ctl) {
+  constexpr bool R1 = INV, R2 = !INV;  // forward: columns then rows; inverse: rows then columns
+  using G1 = NttGeom<LOGN, R1>;
+  using G2 = NttGeom<LOGN, R2>;
+  constexpr uint32_t nt1 = R1 ? 1u << (G1::logR1 - G1::logTPB) : 1u << (G1::logC - G1::logTPB);
+  constexpr uint32_t nt2 = R2 ? 1u << (G2::logR1 - G2::logTPB) : 1u << (G2::logC - G2::logTPB);
+  __shared__ uint64_t sm[kNTile];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) s_t = atomicAdd(&ctl.ctr[0], 1u);
+  __syncthreads();
+  const uint32_t t = s_t, s = t / (nt1 + nt2), r = t - s * (nt1 + nt2);
+  uint32_t* cnt = ctl.ctr + 2;
+  if (r < nt1) {
+    if (s < ctl.nlimb) {
+      const uint32_t by = s % ctl.ny, bz = s / ctl.ny + ctl.bz0;
+      ntt_pass_dev<INV, R1, LOGN, M1, false>(r, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&cnt[s], 1u);
+      }
+    }
+  } else if (s >= ctl.lag) {
+    const uint32_t limb = s - ctl.lag, by = limb % ctl.ny, bz = limb / ctl.ny + ctl.bz0;
+    if (threadIdx.x == 0) {
+      while (ld_acquire_u32(&cnt[limb]) < nt1) __nanosleep(64);
+    }
+    __syncthreads();
+    ntt_pass_dev<INV, R2, LOGN, M2, true>(r - nt1, by, bz, sm, out, out_stride, out, out_stride, rm2, pcs, tw, twd,
+                                          epi);
+  }
+  // the last block out resets the counters for the next launch
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctl.ctr[1], 1u) == ctl.total - 1;
+  __syncthreads();
+  if (s_last) {
+    for (uint32_t i = threadIdx.x; i < ctl.nlimb; i += blockDim.x) cnt[i] = 0;
+    if (threadIdx.x == 0) ctl.ctr[0] = ctl.ctr[1] = 0;
   }
 }
 
@@ -673,6 +760,55 @@ __global__ void __launch_bounds__(kNT, 4) k_ntt_rows_inner(const __grid_constant
   }
 }
 
+// HS_NTT_FUSED=1: both NTT passes in one launch with the intermediate in L2 (k_ntt_fused).
+// Off by default: it does halve the DRAM traffic (ncu, N=2^16, 32 polys x 25 limbs: 838 MB
+// against 1604 MB for the two launches) but runs 30.6 against 27.9 us per ciphertext, since
+// the passes are bound by FP64-pipe issue and latency, not by HBM.  HS_NTT_LAG scales the
+// ticket lag (default 2 x the resident blocks).
+bool use_fused_ntt() {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_NTT_FUSED");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0;
+}
+
+constexpr uint32_t kFuseMaxLimbs = 1u << 16;  // limbs per fused launch (the counter buffer is fixed-size)
+
+uint32_t* fuse_counters() {
+  // fixed size, allocated once and zeroed: CUDA graphs captured with this pointer stay valid
+  static uint32_t* p = reinterpret_cast<uint32_t*>(Runtime::get().scratch(3, (kFuseMaxLimbs + 2) / 2 + 1, true));
+  return p;
+}
+
+template <bool INV, int LOGN, int M1, int M2>
+void launch_fused(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
+                  const RowMap& rm2, uint32_t n, uint32_t batch, const PrimeC* pcs, const uint64_t* tw,
+                  const double* twd, const PassEpi& ep, cudaStream_t s) {
+  using G1 = NttGeom<LOGN, INV>;
+  using G2 = NttGeom<LOGN, !INV>;
+  constexpr uint32_t nt1 = INV ? 1u << (G1::logR1 - G1::logTPB) : 1u << (G1::logC - G1::logTPB);
+  constexpr uint32_t nt2 = !INV ? 1u << (G2::logR1 - G2::logTPB) : 1u << (G2::logC - G2::logTPB);
+  static const uint32_t lag = [] {
+    int per_sm = 0;
+    cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ntt_fused<INV, LOGN, M1, M2>, kNT, 0),
+            "fused ntt occupancy");
+    const char* e = std::getenv("HS_NTT_LAG");
+    const double f = e ? std::atof(e) : 2.0;
+    const double resident = double(std::max(per_sm, 1)) * Runtime::get().sm_count();
+    return std::max<uint32_t>(1, static_cast<uint32_t>(f * resident / (nt1 + nt2)) + 1);
+  }();
+  uint32_t* ctr = fuse_counters();
+  const uint32_t per = std::max<uint32_t>(1, kFuseMaxLimbs / n);  // batch items per launch
+  for (uint32_t b0 = 0; b0 < batch; b0 += per) {
+    const uint32_t nb = std::min(per, batch - b0), nlimb = n * nb;
+    const uint32_t total = (nlimb + lag) * (nt1 + nt2);
+    const FuseCtl ctl{ctr, n, nlimb, lag, total, b0};
+    k_ntt_fused<INV, LOGN, M1, M2><<<total, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, rm2, pcs, tw, twd, ep,
+                                                         ctl);
+  }
+}
+
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
@@ -685,6 +821,26 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
   if (rs) ep.rs = *rs;
   const int ksm = ks ? ks->mode : KS_PLAIN;
   if (ks) ep.ks = *ks;
+  if (use_fused_ntt()) {
+    const PassEpi& e = (md || rs || ks) ? ep : none;
+    if (!inverse && md && ksm == KS_TENSOR)
+      launch_fused<false, LOGN, 0, 6>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (!inverse && md && ksm == KS_PERM)
+      launch_fused<false, LOGN, 0, 7>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (inverse && ksm == KS_TENSOR)
+      launch_fused<true, LOGN, 4, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (inverse && ksm == KS_PERM)
+      launch_fused<true, LOGN, 5, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (!inverse && rs)
+      launch_fused<false, LOGN, 2, 3>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (!inverse && md)
+      launch_fused<false, LOGN, 0, 1>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (!inverse)
+      launch_fused<false, LOGN, 0, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else
+      launch_fused<true, LOGN, 0, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    return;
+  }
   if (!inverse && md && ksm != KS_PLAIN) {
     k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
     if (ksm == KS_TENSOR)

@@ -65,11 +65,17 @@ Runtime::Runtime(int device) {
     if (l == 1 || l == 2 || l == 4 || l == 8) prog_lanes = l;
   }
   cuda_ok(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_ok(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking), "cudaStreamCreate (upload)");
   // Keep freed blocks in the stream-ordered pool: ciphertexts are churned per op.
   cudaMemPool_t pool;
   cuda_ok(cudaDeviceGetDefaultMemPool(&pool, device_), "cudaDeviceGetDefaultMemPool");
   uint64_t thr = UINT64_MAX;
   cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "pool threshold");
+  // An upload-stream allocation must never wait on compute-stream work behind a pending
+  // free (that would serialise encode_column behind the running statistic): reuse a block
+  // freed on the other stream only once its free has completed.
+  int no = 0;
+  cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no), "pool reuse attr");
 }
 
 Runtime& Runtime::get() {
@@ -95,6 +101,21 @@ DevBuf Runtime::alloc(size_t n) {
   cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, stream_), "cudaMallocAsync");
   cudaStream_t s = stream_;
   return DevBuf(p, [s](double* q) { cudaFreeAsync(q, s); });  // errors at teardown ignored
+}
+
+DevBuf Runtime::alloc_on(size_t n, cudaStream_t on) {
+  double* p = nullptr;
+  const size_t bytes = (n ? n : 1) * sizeof(double);
+  cuda_ok(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, on), "cudaMallocAsync");
+  cudaStream_t s = stream_;
+  return DevBuf(p, [s](double* q) { cudaFreeAsync(q, s); });
+}
+
+bool Runtime::capturing() const {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cuda_ok(cudaStreamIsCapturing(stream_, &st), "cudaStreamIsCapturing");
+  return st != cudaStreamCaptureStatusNone;
 }
 
 void Runtime::sync() { cuda_ok(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }

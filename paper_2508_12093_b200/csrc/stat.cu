@@ -22,6 +22,7 @@
 // scratch, one grid barrier per step — bit-identical either way.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -57,11 +58,38 @@ __device__ __forceinline__ void stamp(int k) {
 __device__ __forceinline__ void stamp(int) {}
 #endif
 
+// Grid barrier over a plain launch (the grid is sized to be co-resident: one block per
+// SM, checked against the occupancy calculator on the host).  One word per barrier
+// sequence: block 0 adds 2^31 - (blocks - 1), every other block adds 1, so the top bit
+// flips exactly when all blocks have arrived and the word's low bits are unchanged
+// afterwards (ready for the next barrier and the next launch).  Release on arrival,
+// acquire while polling.  A plain launch lets encode_column's kernels (upload stream)
+// share the SMs with a running statistic.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+struct GridBar {
+  unsigned* bar;
+  __device__ void sync() const {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      unsigned old;
+      asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+      while (((old ^ ld_acquire_u32(bar)) & 0x80000000u) == 0) {
+      }
+    }
+    __syncthreads();
+  }
+};
+
 // Grid-wide rotate-and-sum of NK per-slot term arrays produced by terms(i, t).
 // `idle` runs between publishing this block's partials and the grid barrier (work
 // that overlaps the wait for the slowest block, e.g. staging the Chebyshev table).
 template <class Q, class TermFn, class IdleFn>
-__device__ Reduced grid_sum(const Q& q, cg::grid_group& grid, TermFn terms, int NK, unsigned S,
+__device__ Reduced grid_sum(const Q& q, const GridBar& grid, TermFn terms, int NK, unsigned S,
                             double* accum, unsigned* count, double* scratch, IdleFn idle) {
   __shared__ double red[kMaxWarps][2 * kNK];
   __shared__ double tot[2 * kNK];
@@ -158,7 +186,7 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
                                                        const __grid_constant__ Prog pg) {
   extern __shared__ double stab[];
   stamp(0);
-  cg::grid_group grid = cg::this_grid();
+  const GridBar grid{reinterpret_cast<unsigned*>(a.partial + 4 * kNK + 1)};
   // the table is first needed in phase B/C: stage it while waiting at phase A's barrier
   auto stage = [&] {
     for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
@@ -261,6 +289,15 @@ void with_q(QSpec qs, F&& f) {
   }
 }
 
+// HS_COOP=1: launch through cudaLaunchCooperativeKernel (the barrier is the same either way)
+bool coop_launch() {
+  static const bool on = [] {
+    const char* e = std::getenv("HS_COOP");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 std::mutex g_occ_mu;
 std::unordered_map<const void*, std::unordered_map<size_t, int>> g_occ;
 
@@ -274,6 +311,8 @@ int max_blocks(K kern, size_t smem, int threads) {
   if (smem > 48 * 1024)
     cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
             "stat smem attr");
+  // same L1/shared carveout as k_encrypt, so an SM can host both at once
+  cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct()), "stat carveout");
   int per_sm = 0;
   cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "stat occupancy");
   const int n = per_sm * Runtime::get().sm_count();
@@ -283,7 +322,8 @@ int max_blocks(K kern, size_t smem, int threads) {
 
 }  // namespace
 
-size_t stat_partial_doubles() { return 4 * kNK + 2; }  // two sets of 2 kNK totals, two block counters
+// two sets of 2 kNK totals, two block counters, the grid barrier's two words
+size_t stat_partial_doubles() { return 4 * kNK + 2; }
 
 void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s) {
   if (p.S == 0) return;
@@ -299,10 +339,15 @@ void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_
       QT qv = Q;
       StatArgs av = a;
       Prog pv = p;
-      void* args[] = {&qv, &av, &pv};
-      cuda_ok(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(geo.threads), args,
-                                          smem, s),
-              "stat launch");
+      if (coop_launch()) {
+        void* args[] = {&qv, &av, &pv};
+        cuda_ok(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(geo.threads), args,
+                                            smem, s),
+                "stat launch");
+      } else {
+        kern<<<grid, geo.threads, smem, s>>>(qv, av, pv);
+        cuda_ok(cudaGetLastError(), "stat launch");
+      }
     };
     if (lanes == 8) go(k_stat<QT, 8>, 8);
     else if (lanes == 4) go(k_stat<QT, 4>, 4);

@@ -214,6 +214,41 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_fused_ntt_option_matches_oracle():
+    """The opt-in one-launch NTT (HS_NTT_FUSED=1: ticket-ordered passes, intermediate in L2) gives
+    the same limbs for every fused epilogue (plain, ModDown with tensor / automorphism sources,
+    rescale) at odd and even ring degrees, several batch items, and lags shorter than the grid."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from rns_abi import RnsOracle, Spec
+from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
+O = RnsOracle()
+for logN, logp in ((10, 61), (13, 44), (15, 44), (16, 61)):
+    s = Spec(logN=logN, L=4, K=2, dnum=2, seed=7, logp=logp)
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
+    a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
+    da, db = DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)
+    assert np.array_equal(c.mul_relin(s.L, da, db).download(), O.mul_relin(s, s.L, a, b)), logN
+    assert np.array_equal(c.rotate(s.L, 5, da).download(), O.rotate(s, s.L, 5, a)), logN
+    assert np.array_equal(c.rescale(s.L, da).download(), O.rescale(s, s.L, a)), logN
+    x = DeviceBuffer(a.size).upload(a)
+    c.ntt(x, 0, s.L + 1, batch=2, inverse=True)
+    c.ntt(x, 0, s.L + 1, batch=2)
+    assert np.array_equal(x.download(), a), logN
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for lag in ("2", "0.01"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root,
+                           env={**os.environ, "HS_NTT_FUSED": "1", "HS_NTT_LAG": lag},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 # Base-conversion widths of k_conv_mma (KS = ceil(sources / 4) k-steps): alpha 1..16 sources per
 # digit, ModDown with K special primes, 61-bit targets (integer epilogue) and 44-bit ones (FP64
 # epilogue), and alpha = 17 (more than 16 sources: the ALU conversion kernel).

@@ -48,6 +48,33 @@ int main() {
   }
   std::printf("C++ e2e: encode %.1f us, znorm enqueue %.1f us, decode (incl. wait) %.1f us, total %.1f us\n",
               t_enc / N, t_z / N, t_dec / N, (t_enc + t_z + t_dec) / N);
+  {  // pipelined: encode step k+1 while step k computes
+    hs_ct* cur = nullptr;
+    uint64_t nch = 0;
+    auto t0 = now();
+    hs_encode_column(ctx, x, S, &cur, &nch);
+    double pz = 0, pe = 0, pd = 0;
+    for (int it = 0; it < N; ++it) {
+      hs_column col{&cur, 1, S};
+      hs_ct* out = nullptr;
+      auto a = now();
+      hs_znorm(ctx, &col, 100.0, &cfg, &out);
+      auto b = now();
+      hs_ct* next = nullptr;
+      if (it + 1 < N) hs_encode_column(ctx, x, S, &next, &nch);
+      auto c = now();
+      hs_column zc{&out, 1, S};
+      hs_decode_column(ctx, &zc, z);
+      auto d = now();
+      pz += us(a, b), pe += us(b, c), pd += us(c, d);
+      hs_ct_release(cur);
+      hs_ct_release(out);
+      cur = next;
+    }
+    auto t1 = now();
+    std::printf("C++ e2e pipelined: %.1f us/step (znorm enqueue %.1f, encode next %.1f, decode %.1f)\n",
+                us(t0, t1) / N, pz / N, pe / N, pd / N);
+  }
   // znorm enqueue alone, device kept busy
   hs_ct* chunk = nullptr;
   uint64_t nch = 0;

@@ -39,3 +39,17 @@ t0=time.perf_counter()
 for _ in range(N): zc=H.znorm(ctx, col, 100.0)
 H.sync()
 print("znorm only loop %.1f us" % (1e6*(time.perf_counter()-t0)/N))
+# pipelined: encode step k+1 while step k computes
+t = [0, 0, 0]
+col = H.encode_column(ctx, xin)
+for k in range(N):
+    t0 = time.perf_counter(); zc = H.znorm(ctx, col, 100.0); t1 = time.perf_counter()
+    col = H.encode_column(ctx, xin); t2 = time.perf_counter()
+    H.decode_column(ctx, zc, out=zout); t3 = time.perf_counter()
+    t[0] += t1 - t0; t[1] += t2 - t1; t[2] += t3 - t2
+print("pipelined: znorm(enqueue) %.1f us, encode next %.1f us, decode %.1f us, total %.1f" % tuple([1e6*v/N for v in t]+[1e6*sum(t)/N]))
+import cProfile, pstats
+pr = cProfile.Profile(); pr.enable()
+for k in range(N):
+    zc = H.znorm(ctx, col, 100.0); col = H.encode_column(ctx, xin); H.decode_column(ctx, zc, out=zout)
+pr.disable(); pstats.Stats(pr).sort_stats("tottime").print_stats(12)
