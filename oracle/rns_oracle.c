@@ -307,8 +307,13 @@ static void make_key(ctx_t* c, uint64_t keyid, const uint64_t* s_ntt, const uint
 
 /* ------------------------------------------------------------ key switching */
 /* d: [level+1][N] NTT form.  out0/out1: [level+1][N] NTT form. */
-static void key_switch(ctx_t* c, uint32_t level, const uint64_t* d, const uint64_t* kb, const uint64_t* ka,
-                       uint64_t* out0, uint64_t* out1) {
+static void moddown_rescale(ctx_t* c, uint32_t level, uint64_t* acc, const uint64_t* dt, uint64_t* out);
+
+/* Hybrid key switching of d (NTT form, level+1 limbs).  dterm == NULL: out_w = ModDown_P(acc_w)
+   (level+1 limbs).  dterm = {d0, d1}: HMult's rescale fused into ModDown, out_w =
+   ModDown_{P q_level}(acc_w + P d_w) (level limbs), see moddown_rescale. */
+static void key_switch_x(ctx_t* c, uint32_t level, const uint64_t* d, const uint64_t* kb, const uint64_t* ka,
+                         uint64_t* out0, uint64_t* out1, const uint64_t* const* dterm) {
   const uint32_t N = 1u << c->s.logN, nq = c->s.L + 1, K = c->s.K, np = nq + K, al = alpha_of(&c->s);
   const uint32_t nl = level + 1, nx = nl + K; /* extended basis: q_0..q_level, p_0..p_{K-1} */
   uint32_t idx[RNS_MAX_PRIMES];              /* extended index -> global prime index */
@@ -370,6 +375,15 @@ static void key_switch(ctx_t* c, uint32_t level, const uint64_t* d, const uint64
       }
     }
   }
+  if (dterm) {
+    moddown_rescale(c, level, acc0, dterm[0], out0);
+    moddown_rescale(c, level, acc1, dterm[1], out1);
+    free(dc);
+    free(ext);
+    free(acc0);
+    free(acc1);
+    return;
+  }
   /* ModDown: (acc - Conv_P->Q(acc_P)) * P^-1 on q_0..q_level */
   uint64_t phat_inv[RNS_MAX_PRIMES];
   for (uint32_t k = 0; k < K; ++k) {
@@ -419,6 +433,74 @@ static void key_switch(ctx_t* c, uint32_t level, const uint64_t* d, const uint64
   free(ext);
   free(acc0);
   free(acc1);
+}
+
+static void key_switch(ctx_t* c, uint32_t level, const uint64_t* d, const uint64_t* kb, const uint64_t* ka,
+                       uint64_t* out0, uint64_t* out1) {
+  key_switch_x(c, level, d, kb, ka, out0, out1, NULL);
+}
+
+/* ModDown by P q_level with HMult's tensor term folded in (the rescale of HMult+relin+rescale
+   merged into the key switch's ModDown): x = acc + P d over q_0..q_level (x = acc on the P
+   primes); the removed primes R = {q_level, p_0..p_{K-1}} go to coefficient form, are converted
+   to q_0..q_{level-1} (fast base conversion), and out_i = (x_i - conv_i) (P q_level)^-1.  One
+   rounding instead of ModDown's and the rescale's: the limbs differ from mul_relin followed by
+   rescale, the decrypted value is the same up to the (smaller) rounding error. */
+static void moddown_rescale(ctx_t* c, uint32_t level, uint64_t* acc, const uint64_t* dt, uint64_t* out) {
+  const uint32_t N = 1u << c->s.logN, nq = c->s.L + 1, K = c->s.K, nl = level + 1, nr = K + 1;
+  uint32_t ridx[RNS_MAX_PRIMES]; /* removed primes, as acc rows level .. level + K */
+  ridx[0] = level;
+  for (uint32_t k = 0; k < K; ++k) ridx[1 + k] = nq + k;
+  uint64_t Pql = 1; /* [P]_{q_level} */
+  for (uint32_t k = 0; k < K; ++k) Pql = mulmod(Pql, c->primes[nq + k] % c->primes[level], c->primes[level]);
+  uint64_t* rc = (uint64_t*)malloc((size_t)nr * N * sizeof(uint64_t));
+  uint64_t* conv = (uint64_t*)malloc((size_t)N * sizeof(uint64_t));
+  for (uint32_t r = 0; r < nr; ++r) {
+    const uint64_t* src = acc + (size_t)(r == 0 ? level : nl + r - 1) * N;
+    uint64_t* dst = rc + (size_t)r * N;
+    for (uint32_t n = 0; n < N; ++n)
+      dst[n] = r == 0 ? addmod(src[n], mulmod(dt[(size_t)level * N + n], Pql, c->primes[level]), c->primes[level])
+                      : src[n];
+    ntt_inv(c, ridx[r], dst);
+  }
+  uint64_t rhat_inv[RNS_MAX_PRIMES];
+  for (uint32_t r = 0; r < nr; ++r) {
+    const uint64_t pr = c->primes[ridx[r]];
+    uint64_t v = 1;
+    for (uint32_t m = 0; m < nr; ++m)
+      if (m != r) v = mulmod(v, c->primes[ridx[m]] % pr, pr);
+    rhat_inv[r] = invmod(v, pr);
+  }
+  for (uint32_t i = 0; i < level; ++i) {
+    const uint64_t q = c->primes[i];
+    uint64_t rhat_q[RNS_MAX_PRIMES], Rq = 1, Pq = 1;
+    for (uint32_t r = 0; r < nr; ++r) {
+      uint64_t v = 1;
+      for (uint32_t m = 0; m < nr; ++m)
+        if (m != r) v = mulmod(v, c->primes[ridx[m]] % q, q);
+      rhat_q[r] = v;
+      Rq = mulmod(Rq, c->primes[ridx[r]] % q, q);
+    }
+    for (uint32_t k = 0; k < K; ++k) Pq = mulmod(Pq, c->primes[nq + k] % q, q);
+    const uint64_t rinv = invmod(Rq, q);
+    for (uint32_t n = 0; n < N; ++n) {
+      uint64_t sum = 0;
+      for (uint32_t r = 0; r < nr; ++r) {
+        const uint64_t pr = c->primes[ridx[r]];
+        const uint64_t xr = mulmod(rc[(size_t)r * N + n], rhat_inv[r], pr);
+        sum = addmod(sum, mulmod(xr % q, rhat_q[r], q), q);
+      }
+      conv[n] = sum;
+    }
+    ntt_fwd(c, i, conv);
+    for (uint32_t n = 0; n < N; ++n) {
+      const size_t x = (size_t)i * N + n;
+      const uint64_t xi = addmod(acc[x], mulmod(dt[x], Pq, q), q);
+      out[x] = mulmod(submod(xi, conv[n], q), rinv, q);
+    }
+  }
+  free(rc);
+  free(conv);
 }
 
 static size_t key_words(const ctx_t* c) {
@@ -475,6 +557,46 @@ void rnso_mul_relin_many(const rns_spec* s, uint32_t level, uint32_t count, cons
 
 void rnso_mul_relin(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out) {
   rnso_mul_relin_many(s, level, 1, a, b, out);
+}
+
+/* HMult + relinearisation + rescale with the rescale merged into ModDown (moddown_rescale):
+   out has level limbs per polynomial. */
+void rnso_mul_relin_rescale(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  ctx_t c;
+  ctx_init(&c, s);
+  const uint32_t N = 1u << s->logN, nl = level + 1, np = s->L + 1 + s->K;
+  uint64_t* sk = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
+  uint64_t* s2 = (uint64_t*)malloc((size_t)np * N * sizeof(uint64_t));
+  secret_ntt(&c, sk);
+  for (uint32_t i = 0; i < np; ++i)
+    for (uint32_t n = 0; n < N; ++n)
+      s2[(size_t)i * N + n] = mulmod(sk[(size_t)i * N + n], sk[(size_t)i * N + n], c.primes[i]);
+  uint64_t* kb = (uint64_t*)malloc(key_words(&c) * sizeof(uint64_t));
+  uint64_t* ka = (uint64_t*)malloc(key_words(&c) * sizeof(uint64_t));
+  make_key(&c, 0, sk, s2, kb, ka);
+  uint64_t* d0 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
+  uint64_t* d1 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
+  uint64_t* d2 = (uint64_t*)malloc((size_t)nl * N * sizeof(uint64_t));
+  const uint64_t *a0 = a, *a1 = a + (size_t)nl * N, *b0 = b, *b1 = b + (size_t)nl * N;
+  for (uint32_t i = 0; i < nl; ++i) {
+    const uint64_t q = c.primes[i];
+    for (uint32_t n = 0; n < N; ++n) {
+      const size_t x = (size_t)i * N + n;
+      d0[x] = mulmod(a0[x], b0[x], q);
+      d1[x] = addmod(mulmod(a0[x], b1[x], q), mulmod(a1[x], b0[x], q), q);
+      d2[x] = mulmod(a1[x], b1[x], q);
+    }
+  }
+  const uint64_t* dt[2] = {d0, d1};
+  key_switch_x(&c, level, d2, kb, ka, out, out + (size_t)level * N, dt);
+  free(sk);
+  free(s2);
+  free(kb);
+  free(ka);
+  free(d0);
+  free(d1);
+  free(d2);
+  ctx_free(&c);
 }
 
 void rnso_rescale(const rns_spec* s, uint32_t level, const uint64_t* in, uint64_t* out) {

@@ -52,6 +52,8 @@ void rnso_mul_relin_many(const rns_spec* s, uint32_t level, uint32_t count, cons
                          uint64_t* out);
 /* rescale by q_level: in [2][level+1][N] -> out [2][level][N], NTT form */
 void rnso_rescale(const rns_spec* s, uint32_t level, const uint64_t* in, uint64_t* out);
+/* HMult + relin + rescale, the rescale merged into ModDown (ModDown by P q_level): level limbs out */
+void rnso_mul_relin_rescale(const rns_spec* s, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out);
 /* rotation by k slots (Galois element 5^k mod 2N) + key switch, NTT form */
 void rnso_rotate(const rns_spec* s, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out);
 /* symmetric RLWE encryption of N integer coefficients at `level`: c1 = a (uniform,

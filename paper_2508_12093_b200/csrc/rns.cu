@@ -135,6 +135,9 @@ struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
   const uint64_t* pinv_sh;
   size_t acc_stride, add_stride, out_stride;
   uint32_t nl, nx;
+  // ModDown merged with HMult's rescale (pinv = (P q_l)^-1): add_w enters scaled by q_l^-1
+  const uint64_t* ascale = nullptr;
+  const uint64_t* ascale_sh = nullptr;
 };
 
 // Key-switch inputs produced on the fly instead of materialised: mul_relin's tensor
@@ -169,6 +172,14 @@ struct PermLoad {  // d = sigma_g(c1): row = limb i of c1 (whole row), toff = th
 struct AddRow {  // + add_w[i] (materialised) or nothing
   const uint64_t* p;
   __device__ uint64_t operator()(size_t off, uint64_t r, uint64_t q) const { return p ? add_mod(r, p[off], q) : r; }
+};
+
+struct AddRowScaled {  // + add_w[i] q_l^-1 (ModDown by P q_l: (acc + P d - conv) (P q_l)^-1)
+  const uint64_t* p;
+  uint64_t sc, sc_sh;
+  __device__ uint64_t operator()(size_t off, uint64_t r, uint64_t q) const {
+    return add_mod(r, mul_shoup(p[off], sc, sc_sh, q), q);
+  }
 };
 
 struct AddTensor {  // + a0 b0 (w = 0) or + a0 b1 + a1 b0 (w = 1), same reductions as k_tensor
@@ -318,18 +329,28 @@ constexpr int pick_rb(int rem) {
   if (kMaxRB >= 4) return rem <= 4 ? rem : (rem <= 6 ? 3 : 4);
   return rem == 4 ? 2 : (rem < 3 ? rem : 3);
 }
-template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST>
+// Called once per pass, right after the barrier that follows the first step (every
+// thread has consumed its inputs): the persistent kernel issues the next tile's loads there.
+struct NoPf {
+  __device__ void operator()() const {}
+};
+
+template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf>
 __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
                                           const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
-                                          uint64_t ninv_sh) {
+                                          uint64_t ninv_sh, const PF& pf = PF{}) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = pick_rb(rem);
     if constexpr (DONE > 0) __syncthreads();
+    if constexpr (DONE > 0 && DONE == pick_rb(logR)) pf();
     ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, psi, psip, q, tile0,
                                                                               ninv, ninv_sh);
-    ntt_steps<INV, ROWS, LOGN, DONE + RB, LD, ST>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh);
+    ntt_steps<INV, ROWS, LOGN, DONE + RB, LD, ST, PF>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh, pf);
+  } else if constexpr (DONE == pick_rb(logR) && !std::is_same_v<PF, NoPf>) {  // single-step pass
+    __syncthreads();
+    pf();
   }
 }
 
@@ -369,10 +390,32 @@ __device__ __forceinline__ uint64_t fp_canon(double x, double q, double qinv) {
   return d2u(r);
 }
 
+// Row-pass twiddles staged in shared memory: for local stage m the tile's rows use the
+// contiguous run tw[2^m (R1 + tile0) + (0 .. TPB 2^m)), stored at tws[TPB (2^m - 1) + ...].
+template <int LOGN>
+struct RowTw {
+  using G = NttGeom<LOGN, true>;
+  static constexpr uint32_t TPB = 1u << G::logTPB;
+  static constexpr uint32_t words = TPB * ((1u << G::logC) - 1);
+  __device__ static constexpr uint32_t off(uint32_t m) { return TPB * ((1u << m) - 1); }
+};
+
+template <int LOGN>
+__device__ __forceinline__ void stage_row_tw(double* tws, const double* tw, uint32_t tile0) {
+  using T = RowTw<LOGN>;
+#pragma unroll
+  for (uint32_t m = 0; m < T::G::logC; ++m) {
+    const double* src = tw + (size_t(1) << m) * (T::G::R1 + tile0);
+    double* dst = tws + T::off(m);
+    for (uint32_t k = threadIdx.x; k < (T::TPB << m); k += kNT) dst[k] = __ldg(src + k);
+  }
+}
+
 template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST>
 __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
-                                            double qinv, uint32_t tile0, double ninv) {
+                                            double qinv, uint32_t tile0, double ninv,
+                                            const double* __restrict__ tws) {
   using G = NttGeom<LOGN, ROWS>;
   constexpr uint32_t logR = G::logR, logTPB = G::logTPB, logC = G::logC;
   constexpr uint32_t logG = logR - RB;
@@ -408,7 +451,8 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
         const int d = 1 << (RB - 1 - st);
 #pragma unroll
         for (int b = 0; b < (1 << st); ++b) {
-          const double w = __ldg(tw + ((1u << (DONE + st)) * S) + (blk0 << st) + b);
+          const double w = ROWS && tws ? tws[RowTw<LOGN>::off(DONE + st) + (tr << (DONE + st)) + (blk0 << st) + b]
+                                       : __ldg(tw + ((1u << (DONE + st)) * S) + (blk0 << st) + b);
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
@@ -426,7 +470,9 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
         const int d = 1 << st;
 #pragma unroll
         for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
-          const double w = __ldg(tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b);
+          const double w = ROWS && tws
+                               ? tws[RowTw<LOGN>::off(logh0 - st) + (tr << (logh0 - st)) + (blk0 << (RB - 1 - st)) + b]
+                               : __ldg(tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b);
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
@@ -457,17 +503,22 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
   }
 }
 
-template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST>
+template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf>
 __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, double* sm, const double* tw,
-                                             double q, double qinv, uint32_t tile0, double ninv) {
+                                             double q, double qinv, uint32_t tile0, double ninv,
+                                             const double* tws = nullptr, const PF& pf = PF{}) {
   constexpr int logR = NttGeom<LOGN, ROWS>::logR;
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = pick_rb(rem);
     if constexpr (DONE > 0) __syncthreads();
+    if constexpr (DONE > 0 && DONE == pick_rb(logR)) pf();
     ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, tw, q, qinv, tile0,
-                                                                                 ninv);
-    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST>(gin, gout, sm, tw, q, qinv, tile0, ninv);
+                                                                                 ninv, tws);
+    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST, PF>(gin, gout, sm, tw, q, qinv, tile0, ninv, tws, pf);
+  } else if constexpr (DONE == pick_rb(logR) && !std::is_same_v<PF, NoPf>) {
+    __syncthreads();
+    pf();
   }
 }
 
@@ -487,15 +538,61 @@ struct CgLoad {  // L2-coherent load (skips L1): the second pass of the fused NT
   __device__ uint64_t operator()(size_t off) const { return __ldcg(g + off); }
 };
 
+// The pass tile staged in shared memory.  Row tiles keep their global layout (contiguous);
+// column tiles are stored row by row with stride TPB (the global layout's stride 2^logC
+// would put every row of a warp's access on the same banks).
+template <int LOGN, bool ROWS>
+struct StageLoad {
+  const uint64_t* s;
+  __device__ uint64_t operator()(size_t off) const {
+    using G = NttGeom<LOGN, ROWS>;
+    if constexpr (ROWS) return s[off];
+    else return s[((off >> G::logC) << G::logTPB) | (off & ((1u << G::logTPB) - 1))];
+  }
+};
+
+template <class L>
+__device__ __forceinline__ L mk_ld(const uint64_t* g, const uint64_t* stage) {
+  if constexpr (std::is_same_v<L, PlainLoad> || std::is_same_v<L, CgLoad>) return L{g};
+  else return L{stage};
+}
+
+// Issue the asynchronous copy of one pass tile (global -> shared, 16 B per cp.async).
+template <int LOGN, bool ROWS>
+__device__ __forceinline__ void stage_tile(uint64_t* st, const uint64_t* g) {
+  using G = NttGeom<LOGN, ROWS>;
+  constexpr uint32_t words = 1u << (G::logR + G::logTPB);
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(st));
+  for (uint32_t c = threadIdx.x; c < words / 2; c += kNT) {
+    size_t src;
+    uint32_t dst;
+    if constexpr (ROWS) {
+      src = 2 * size_t(c);
+      dst = 2 * c;
+    } else {  // row r of the column tile: TPB consecutive words at r * 2^logC
+      constexpr uint32_t per = (1u << G::logTPB) / 2;  // 16-byte chunks per row
+      const uint32_t r = c / per, k = c % per;
+      src = (size_t(r) << G::logC) + 2 * k;
+      dst = (r << G::logTPB) + 2 * k;
+    }
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + dst * 8), "l"(g + src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // One pass over tile bx of row-map entry by, batch item bz (the body of k_ntt_pass and
 // of both phases of k_ntt_fused).  CG: plain loads of the pass input go through L2 only.
-template <bool INV, bool ROWS, int LOGN, int MODE, bool CG>
+// sm: kNTile words for the tile, plus (row passes) RowTw<LOGN>::words doubles of staged twiddles.
+// LDK: how a plain pass input is read -- 0 global, 1 global through L2 only (fused NTT's
+// second pass), 2 from the tile staged in shared memory by the persistent kernel.
+template <bool INV, bool ROWS, int LOGN, int MODE, int LDK, class PF = NoPf>
 __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t bz, uint64_t* sm, const uint64_t* in,
                                              size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                                              const PrimeC* pcs, const uint64_t* tw, const double* twd,
-                                             const PassEpi& epi) {
+                                             const PassEpi& epi, bool use_row_tw = true,
+                                             const uint64_t* stage = nullptr, const PF& pf = PF{}) {
   using G = NttGeom<LOGN, ROWS>;
-  using PlainLd = std::conditional_t<CG, CgLoad, PlainLoad>;
+  using PlainLd = std::conditional_t<LDK == 2, StageLoad<LOGN, ROWS>, std::conditional_t<LDK == 1, CgLoad, PlainLoad>>;
   constexpr uint32_t N = 1u << LOGN;
   const uint32_t pi = rm.prime[by];
   const PrimeC& P = pcs[pi];
@@ -506,33 +603,45 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
   const uint64_t* gi = in + bz * in_stride + (size_t(rm.irow[by]) << LOGN) + toff;
   uint64_t* go = out + bz * out_stride + (size_t(rm.orow[by]) << LOGN) + toff;
   const double* twp = twd + size_t(pi) * 2 * N + (INV ? N : 0);
+  double* tws = nullptr;
+  if constexpr (ROWS) {
+    if (P.fp && use_row_tw) {  // uniform per block
+      tws = reinterpret_cast<double*>(sm) + kNTile;
+      stage_row_tw<LOGN>(tws, twp, tile0);
+      __syncthreads();
+    }
+  }
   auto run = [&](const auto& ld, const auto& st) {
     if (P.fp)
       ntt_steps_fp<INV, ROWS, LOGN, 0>(ld, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
-                                       static_cast<double>(P.ninv));
+                                       static_cast<double>(P.ninv), tws, pf);
     else
-      ntt_steps<INV, ROWS, LOGN, 0>(ld, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
+      ntt_steps<INV, ROWS, LOGN, 0>(ld, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh, pf);
   };
-  if constexpr (MODE == 1 || MODE == 6 || MODE == 7) {  // row r = w * nl + i of the ModDown conversion output
+  if constexpr (MODE == 1 || MODE == 6 || MODE == 7 || MODE == 8) {  // row r = w * nl + i of the ModDown conversion output
     const MdEpi& e = epi.md;
     const uint32_t r = rm.orow[by], w = r / e.nl, i = r - w * e.nl;
     const uint64_t* acc = e.acc + bz * e.acc_stride + (size_t(w * e.nx + i) << LOGN) + toff;
     uint64_t* o = e.out + bz * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff;
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 8) {
+      const uint64_t* ad = (w == 0 ? e.add0 : e.add1) + bz * e.add_stride + (size_t(i) << LOGN) + toff;
+      run(mk_ld<PlainLd>(gi, stage), MdStore<AddRowScaled>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+                                                           AddRowScaled{ad, e.ascale[i], e.ascale_sh[i]}});
+    } else if constexpr (MODE == 1) {
       const uint64_t* ad = w == 0 ? e.add0 : e.add1;
-      run(PlainLd{gi}, MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi, stage), MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                          AddRow{ad ? ad + bz * e.add_stride + (size_t(i) << LOGN) + toff : nullptr}});
     } else if constexpr (MODE == 6) {
       const KsSrc& k = epi.ks;
       const uint64_t* a0 = k.a + bz * k.stride + (size_t(i) << LOGN) + toff;
       const uint64_t* b0 = k.b + bz * k.stride + (size_t(i) << LOGN) + toff;
       const size_t h = size_t(k.nl) << LOGN;
-      run(PlainLd{gi}, MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi, stage), MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                             AddTensor{a0, a0 + h, b0, b0 + h, P, int(w)}});
     } else {
       const KsSrc& k = epi.ks;
       const uint64_t* c0 = w == 0 ? k.a + bz * k.stride + (size_t(i) << LOGN) : nullptr;
-      run(PlainLd{gi}, MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi, stage), MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                                 AddPerm<LOGN>{c0, k.g, uint32_t(toff)}});
     }
   } else if constexpr (MODE == 4 || MODE == 5) {  // inverse row pass of d = a1 b1 / sigma(c1), limb irow
@@ -553,20 +662,69 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
     const RsStore st{e.in + bz * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
                      e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
                      e.qinv_sh[i]};
-    run(PlainLd{gi}, st);
+    run(mk_ld<PlainLd>(gi, stage), st);
   } else {
-    run(PlainLd{gi}, PlainStore{go});
+    run(mk_ld<PlainLd>(gi, stage), PlainStore{go});
   }
 }
+
+// Build switch HS_ROW_TW=1: row-pass twiddles (a distinct run per row) staged in shared
+// memory at block start instead of read through L1/L2.  Off: measured slower (HMult+relin
+// 198 against 184 us per ciphertext): the staging phase and the doubled shared memory per
+// block cost more than the twiddle loads they replace.
+#ifndef HS_ROW_TW
+#define HS_ROW_TW 0
+#endif
+constexpr bool row_tw_on = HS_ROW_TW != 0;
 
 template <bool INV, bool ROWS, int LOGN, int MODE = 0>
 __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                   size_t out_stride, const __grid_constant__ RowMap rm,
                                                   const PrimeC* pcs, const uint64_t* tw, const double* twd,
                                                   const __grid_constant__ PassEpi epi) {
+  __shared__ uint64_t sm[kNTile + (ROWS && row_tw_on ? RowTw<LOGN>::words : 0)];
+  ntt_pass_dev<INV, ROWS, LOGN, MODE, 0>(blockIdx.x, blockIdx.y, blockIdx.z, sm, in, in_stride, out, out_stride, rm,
+                                             pcs, tw, twd, epi, row_tw_on);
+}
+
+// ---- persistent pass with the next tile's load in flight ------------------------------
+// ncu on the one-tile-per-block passes: half the issue slots idle, the top stall
+// long_scoreboard (every block waits for its own tile from HBM before any arithmetic).
+// Here a block walks tiles t, t + grid, ... and copies tile t + grid into shared memory
+// (cp.async) as soon as tile t's first register step has read its inputs, so the HBM
+// latency of the next tile hides behind the remaining radix steps and the stores of the
+// current one.  Passes whose input is plain words only (modes 0, 1, 3, 6, 7).
+template <bool INV, bool ROWS, int LOGN, int MODE = 0>
+#ifndef HS_NTT_DB_MINB
+#define HS_NTT_DB_MINB 4
+#endif
+__global__ void __launch_bounds__(kNT, HS_NTT_DB_MINB) k_ntt_pass_db(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                     size_t out_stride, const __grid_constant__ RowMap rm,
+                                                     const PrimeC* pcs, const uint64_t* tw, const double* twd,
+                                                     const __grid_constant__ PassEpi epi, uint32_t ntx, uint32_t ny,
+                                                     uint32_t total) {
+  using G = NttGeom<LOGN, ROWS>;
   __shared__ uint64_t sm[kNTile];
-  ntt_pass_dev<INV, ROWS, LOGN, MODE, false>(blockIdx.x, blockIdx.y, blockIdx.z, sm, in, in_stride, out, out_stride, rm,
-                                             pcs, tw, twd, epi);
+  __shared__ __align__(16) uint64_t stage[1u << (G::logR + G::logTPB)];
+  auto src = [&](uint32_t t) {
+    const uint32_t bx = t % ntx, rest = t / ntx, by = rest % ny, bz = rest / ny;
+    const uint32_t tile0 = bx << G::logTPB;
+    const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
+    return in + bz * in_stride + (size_t(rm.irow[by]) << LOGN) + toff;
+  };
+  uint32_t t = blockIdx.x;
+  if (t < total) stage_tile<LOGN, ROWS>(stage, src(t));
+  for (; t < total; t += gridDim.x) {
+    const uint32_t bx = t % ntx, rest = t / ntx, by = rest % ny, bz = rest / ny;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint32_t nt = t + gridDim.x;
+    auto pf = [&]() {
+      if (nt < total) stage_tile<LOGN, ROWS>(stage, src(nt));
+    };
+    ntt_pass_dev<INV, ROWS, LOGN, MODE, 2>(bx, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi,
+                                           row_tw_on, stage, pf);
+  }
 }
 
 // ---- both passes in one launch, the intermediate kept in L2 ---------------------------
@@ -602,7 +760,7 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_fused(const uint64_t* 
   using G2 = NttGeom<LOGN, R2>;
   constexpr uint32_t nt1 = R1 ? 1u << (G1::logR1 - G1::logTPB) : 1u << (G1::logC - G1::logTPB);
   constexpr uint32_t nt2 = R2 ? 1u << (G2::logR1 - G2::logTPB) : 1u << (G2::logC - G2::logTPB);
-  __shared__ uint64_t sm[kNTile];
+  __shared__ uint64_t sm[kNTile + (row_tw_on ? RowTw<LOGN>::words : 0)];
   __shared__ uint32_t s_t;
   if (threadIdx.x == 0) s_t = atomicAdd(&ctl.ctr[0], 1u);
   __syncthreads();
@@ -611,7 +769,8 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_fused(const uint64_t* 
   if (r < nt1) {
     if (s < ctl.nlimb) {
       const uint32_t by = s % ctl.ny, bz = s / ctl.ny + ctl.bz0;
-      ntt_pass_dev<INV, R1, LOGN, M1, false>(r, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi);
+      ntt_pass_dev<INV, R1, LOGN, M1, 0>(r, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi,
+                                             row_tw_on);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
@@ -624,8 +783,8 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_fused(const uint64_t* 
       while (ld_acquire_u32(&cnt[limb]) < nt1) __nanosleep(64);
     }
     __syncthreads();
-    ntt_pass_dev<INV, R2, LOGN, M2, true>(r - nt1, by, bz, sm, out, out_stride, out, out_stride, rm2, pcs, tw, twd,
-                                          epi);
+    ntt_pass_dev<INV, R2, LOGN, M2, 1>(r - nt1, by, bz, sm, out, out_stride, out, out_stride, rm2, pcs, tw, twd,
+                                          epi, row_tw_on);
   }
   // the last block out resets the counters for the next launch
   __shared__ bool s_last;
@@ -809,6 +968,44 @@ void launch_fused(const uint64_t* in, size_t in_stride, uint64_t* out, size_t ou
   }
 }
 
+// HS_NTT_DB=1: passes with plain inputs run as the persistent k_ntt_pass_db (next tile
+// prefetched by cp.async).  Off by default: correct, but 33.0 against 27.9 us per
+// ciphertext NTT at N=2^16, L=24 (64 registers, 4 blocks/SM; 40 registers spill and run
+// 33.5) -- the long_scoreboard stalls of the one-tile blocks are covered by the other
+// resident blocks already, and the extra shared-memory tile costs occupancy.
+bool use_db_ntt() {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_NTT_DB");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0;
+}
+
+template <bool INV, bool ROWS, int LOGN, int MODE>
+void launch_pass(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
+                 uint32_t n, uint32_t batch, const PrimeC* pcs, const uint64_t* tw, const double* twd,
+                 const PassEpi& ep, cudaStream_t s) {
+  using G = NttGeom<LOGN, ROWS>;
+  const uint32_t ntx = ROWS ? 1u << (G::logR1 - G::logTPB) : 1u << (G::logC - G::logTPB);
+  constexpr bool plain_in = MODE == 0 || MODE == 1 || MODE == 3 || MODE == 6 || MODE == 7 || MODE == 8;
+  if constexpr (plain_in) {
+    if (use_db_ntt()) {
+      static const uint32_t resident = [] {
+        int per_sm = 0;
+        cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ntt_pass_db<INV, ROWS, LOGN, MODE>, kNT, 0),
+                "ntt db occupancy");
+        return static_cast<uint32_t>(std::max(per_sm, 1) * Runtime::get().sm_count());
+      }();
+      const uint32_t total = ntx * n * batch;
+      k_ntt_pass_db<INV, ROWS, LOGN, MODE><<<std::min(total, resident), kNT, 0, s>>>(
+          in, in_stride, out, out_stride, rm, pcs, tw, twd, ep, ntx, n, total);
+      return;
+    }
+  }
+  k_ntt_pass<INV, ROWS, LOGN, MODE><<<dim3(ntx, n, batch), kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw,
+                                                                        twd, ep);
+}
+
 template <int LOGN>
 void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                 const RowMap& rm2, uint32_t n, uint32_t batch, bool inverse, const PrimeC* pcs, const uint64_t* tw,
@@ -833,6 +1030,8 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
       launch_fused<true, LOGN, 5, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
     else if (!inverse && rs)
       launch_fused<false, LOGN, 2, 3>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
+    else if (!inverse && md && md->ascale)
+      launch_fused<false, LOGN, 0, 8>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
     else if (!inverse && md)
       launch_fused<false, LOGN, 0, 1>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
     else if (!inverse)
@@ -841,36 +1040,39 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
       launch_fused<true, LOGN, 0, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
     return;
   }
+  const PassEpi& E = ep;
   if (!inverse && md && ksm != KS_PLAIN) {
-    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
+    launch_pass<false, false, LOGN, 0>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, none, s);
     if (ksm == KS_TENSOR)
-      k_ntt_pass<false, true, LOGN, 6><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+      launch_pass<false, true, LOGN, 6>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, E, s);
     else
-      k_ntt_pass<false, true, LOGN, 7><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+      launch_pass<false, true, LOGN, 7>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, E, s);
     return;
   }
   if (inverse && ksm != KS_PLAIN) {
     if (ksm == KS_TENSOR)
-      k_ntt_pass<true, true, LOGN, 4><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
+      launch_pass<true, true, LOGN, 4>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, E, s);
     else
-      k_ntt_pass<true, true, LOGN, 5><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
-    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
+      launch_pass<true, true, LOGN, 5>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, E, s);
+    launch_pass<true, false, LOGN, 0>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, none, s);
     return;
   }
   if (!inverse) {
     if (rs)
-      k_ntt_pass<false, false, LOGN, 2><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, ep);
+      launch_pass<false, false, LOGN, 2>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, E, s);
     else
-      k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
-    if (md)
-      k_ntt_pass<false, true, LOGN, 1><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+      launch_pass<false, false, LOGN, 0>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, none, s);
+    if (md && md->ascale)
+      launch_pass<false, true, LOGN, 8>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, E, s);
+    else if (md)
+      launch_pass<false, true, LOGN, 1>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, E, s);
     else if (rs)
-      k_ntt_pass<false, true, LOGN, 3><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, ep);
+      launch_pass<false, true, LOGN, 3>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, E, s);
     else
-      k_ntt_pass<false, true, LOGN><<<gr, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
+      launch_pass<false, true, LOGN, 0>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, none, s);
   } else {
-    k_ntt_pass<true, true, LOGN><<<gr, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw, twd, none);
-    k_ntt_pass<true, false, LOGN><<<gc, kNT, 0, s>>>(out, out_stride, out, out_stride, rm2, pcs, tw, twd, none);
+    launch_pass<true, true, LOGN, 0>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, none, s);
+    launch_pass<true, false, LOGN, 0>(out, out_stride, out, out_stride, rm2, n, batch, pcs, tw, twd, none, s);
   }
 }
 
@@ -1908,6 +2110,12 @@ struct KsPlan {
   DevBuf frags;                       // k_conv_mma B fragments of every job above
   DevBuf pinv, pinv_sh;               // [nl] P^-1 mod q_i
   DevBuf qinv, qinv_sh;               // [level] q_level^-1 mod q_i (rescale)
+  // ModDown by P q_level (HMult's rescale merged into the key switch), level >= 1:
+  DevBuf rd_jobs;                      // ConvJob[2]: acc_w rows level..level+K -> conv rows w*level..
+  std::vector<uint32_t> r_rows, r_primes;    // acc rows q_level + P (both halves) for the iNTT
+  std::vector<uint32_t> cv2_rows, cv2_primes;  // conv rows (both halves, level limbs) for the NTT
+  DevBuf pqinv, pqinv_sh;             // [level] (P q_level)^-1 mod q_i
+  uint64_t pql = 0, pql_sh = 0;       // [P]_{q_level}
 };
 
 std::mutex g_plan_mu;
@@ -1957,6 +2165,44 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
     }
   }
   attach_frags(c, &down, &frags);
+  std::vector<ConvJob> rdown;
+  if (level >= 1) {
+    rdown.resize(2);
+    std::vector<uint32_t> rsrc{level}, rtgt, rrow;
+    for (uint32_t k = 0; k < K; ++k) rsrc.push_back(c.nq + k);
+    for (uint32_t i = 0; i < level; ++i) {
+      rtgt.push_back(i);
+      rrow.push_back(i);
+    }
+    for (uint32_t w = 0; w < 2; ++w) {
+      fill_conv(c, rsrc, rtgt, rrow, w * p->nx + level, w * level, &rdown[w]);
+      for (uint32_t k = 0; k <= K; ++k) {
+        p->r_rows.push_back(w * p->nx + level + k);
+        p->r_primes.push_back(rsrc[k]);
+      }
+      for (uint32_t i = 0; i < level; ++i) {
+        p->cv2_rows.push_back(w * level + i);
+        p->cv2_primes.push_back(i);
+      }
+    }
+    attach_frags(c, &rdown, &frags);
+    const uint64_t ql = c.primes[level];
+    uint64_t v = 1;
+    for (uint32_t k = 0; k < K; ++k) v = h_mulmod(v, c.primes[c.nq + k] % ql, ql);
+    p->pql = v;
+    p->pql_sh = shoup_of(v, ql);
+    std::vector<uint64_t> pq(level), pq_sh(level);
+    for (uint32_t i = 0; i < level; ++i) {
+      const uint64_t q = c.primes[i];
+      uint64_t u = ql % q;
+      for (uint32_t k = 0; k < K; ++k) u = h_mulmod(u, c.primes[c.nq + k] % q, q);
+      pq[i] = h_inv(u, q);
+      pq_sh[i] = shoup_of(pq[i], q);
+    }
+    p->pqinv = upload(pq);
+    p->pqinv_sh = upload(pq_sh);
+    p->rd_jobs = upload(rdown);
+  }
   p->up_jobs = upload(up);
   p->down_jobs = upload(down);
   p->frags = upload(frags);
@@ -2119,9 +2365,26 @@ void launch_conv(uint32_t nsrc, uint32_t ntgt, const uint64_t* in, size_t in_str
 // kk; out_w = ModDown(acc_w) + add_w  ([2][nl][N] per batch item, stride out_stride).
 // With src (mode KS_TENSOR / KS_PERM), d and add_w are not materialised: the first
 // iNTT pass computes d from src and the ModDown store adds add_w from src.
+// acc_w[q_level row] += [P]_{q_level} add_w[q_level row] (NTT form): the P d_w term of
+// ModDown by P q_level on the one removed Q prime (on the P primes, P d_w = 0).
+__global__ void k_acc_fold(uint64_t* acc, size_t acc_stride, const uint64_t* add0, const uint64_t* add1,
+                           size_t add_stride, uint32_t nx, uint32_t level, uint32_t logN, uint64_t v, uint64_t v_sh,
+                           uint64_t q) {
+  const uint32_t N = 1u << logN;
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x, w = blockIdx.y;
+  if (n >= N) return;
+  uint64_t* a = acc + blockIdx.z * acc_stride + (size_t(w * nx + level) << logN) + n;
+  const uint64_t* d = (w == 0 ? add0 : add1) + blockIdx.z * add_stride + (size_t(level) << logN) + n;
+  *a = add_mod(*a, mul_shoup(*d, v, v_sh, q), q);
+}
+
+// rescale = true (mul_relin_rescale, add_w required): HMult's rescale merged into ModDown --
+// out_w = (acc_w + P add_w - Conv_{P q_l -> Q_{l-1}}) (P q_l)^-1 over q_0..q_{l-1}, one
+// conversion from K + 1 removed primes instead of ModDown's K plus the rescale's iNTT/NTT of
+// every limb.  Matches oracle/rns_oracle.c moddown_rescale word for word.
 void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, const Ctx::Key& kk, const uint64_t* add0,
                 const uint64_t* add1, size_t add_stride, uint64_t* out, size_t out_stride, uint32_t batch,
-                const KsSrc* src = nullptr) {
+                const KsSrc* src = nullptr, bool rescale = false) {
   Runtime& rt = Runtime::get();
   cudaStream_t s = rt.stream();
   const KsPlan& P = ks_plan(c, level);
@@ -2174,6 +2437,21 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
     }
   }
   }
+  if (rescale) {
+    const uint32_t lv = level;
+    k_acc_fold<<<dim3((N + kT - 1) / kT, 2, batch), kT, 0, s>>>(ACC, acc_stride, add0, add1, add_stride, nx, lv, logN,
+                                                                 P.pql, P.pql_sh, c.primes[lv]);
+    rt.note_launch();
+    ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.r_rows, P.r_rows, P.r_primes, batch, true);
+    launch_conv(c.spec.K + 1, lv, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.rd_jobs), FR, 2, c, batch);
+    MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pqinv), dptr<const uint64_t>(P.pqinv_sh),
+              acc_stride, add_stride, out_stride, lv, nx};
+    epi.ascale = dptr<const uint64_t>(P.qinv);
+    epi.ascale_sh = dptr<const uint64_t>(P.qinv_sh);
+    ntt_rows(c, CV, cv_stride, CV, cv_stride, P.cv2_rows, P.cv2_rows, P.cv2_primes, batch, false, &epi);
+    cuda_ok(cudaGetLastError(), "key switch (ModDown by P q_l)");
+    return;
+  }
   // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
   ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);
   launch_conv(c.spec.K, nl, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), FR, 2, c, batch);
@@ -2212,10 +2490,34 @@ void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uin
   key_switch(c, level, D + 2 * half, 3 * half, key, D, D + half, 3 * half, out, ct, batch);
 }
 
+// HS_MD_RESCALE (default 1): mul_relin_rescale merges the rescale into the key switch's
+// ModDown (ModDown by P q_l); 0 = mul_relin followed by rescale.  The two give different
+// limbs (one rounding instead of two); the oracle has both (rnso_mul_relin_rescale and
+// rnso_rescale(rnso_mul_relin)).
+static bool use_md_rescale() {
+  static const int mode = [] {
+    const char* e = std::getenv("HS_MD_RESCALE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return mode != 0;
+}
+
 void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_relin_rescale: level must be in [1, L]");
   if (batch == 0) return;
-  DevBuf t = Runtime::get().alloc(size_t(batch) * 2 * (level + 1) * c.N);
+  Runtime& rt = Runtime::get();
+  if (use_md_rescale()) {
+    const uint32_t N = c.N, nl = level + 1;
+    const size_t ct = size_t(2) * nl * N, half = size_t(nl) * N;
+    DevBuf d = rt.alloc(size_t(batch) * 3 * half);
+    uint64_t* D = dptr<uint64_t>(d);
+    k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half);
+    rt.note_launch();
+    key_switch(c, level, D + 2 * half, 3 * half, c.relin_key(), D, D + half, 3 * half, out, size_t(2) * level * N,
+               batch, nullptr, true);
+    return;
+  }
+  DevBuf t = rt.alloc(size_t(batch) * 2 * (level + 1) * c.N);
   mul_relin(c, level, a, b, dptr<uint64_t>(t), batch);
   rescale(c, level, dptr<const uint64_t>(t), out, batch);
 }

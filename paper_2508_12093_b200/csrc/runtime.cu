@@ -74,8 +74,10 @@ Runtime::Runtime(int device) {
   // An upload-stream allocation must never wait on compute-stream work behind a pending
   // free (that would serialise encode_column behind the running statistic): reuse a block
   // freed on the other stream only once its free has completed.
+#ifndef HS_POOL_XDEP
   int no = 0;
   cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no), "pool reuse attr");
+#endif
 }
 
 Runtime& Runtime::get() {

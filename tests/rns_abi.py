@@ -90,6 +90,12 @@ class RnsOracle:
         self.lib.rnso_mul_relin_many(C.byref(s.c()), C.c_uint32(level), C.c_uint32(count), _u(a), _u(b), _u(out))
         return out
 
+    def mul_relin_rescale(self, s: Spec, level: int, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        """HMult + relin + rescale with the rescale merged into ModDown (ModDown by P q_level)."""
+        out = np.zeros(2 * level * s.N, dtype=np.uint64)
+        self.lib.rnso_mul_relin_rescale(C.byref(s.c()), C.c_uint32(level), _u(a), _u(b), _u(out))
+        return out
+
     def rescale(self, s: Spec, level: int, a: np.ndarray) -> np.ndarray:
         out = np.zeros(2 * level * s.N, dtype=np.uint64)
         self.lib.rnso_rescale(C.byref(s.c()), C.c_uint32(level), _u(a), _u(out))

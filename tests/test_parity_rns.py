@@ -113,11 +113,36 @@ def test_mul_relin_matches_oracle(s):
 
 @pytest.mark.parametrize("s", SHAPES, ids=str)
 def test_mul_relin_rescale_matches_oracle(s):
+    """HMult + relin + rescale with the rescale merged into ModDown (ModDown by P q_l)."""
     c = ctx(s)
-    level = s.L
-    a, b = O.random_ct(s, level, 23), O.random_ct(s, level, 24)
-    got = c.mul_relin_rescale(level, _buf(a), _buf(b)).download()
-    assert np.array_equal(got, O.rescale(s, level, O.mul_relin(s, level, a, b)))
+    for level in sorted({s.L, max(s.L // 2, 1), 1}):
+        a, b = O.random_ct(s, level, 23), O.random_ct(s, level, 24)
+        got = c.mul_relin_rescale(level, _buf(a), _buf(b)).download()
+        assert np.array_equal(got, O.mul_relin_rescale(s, level, a, b)), level
+
+
+def test_mul_relin_rescale_composed_option_matches_oracle():
+    """HS_MD_RESCALE=0: mul_relin followed by rescale (two roundings) -- the oracle's composition."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from rns_abi import RnsOracle, Spec
+from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
+O = RnsOracle()
+for s in (Spec(logN=12, L=5, K=2, dnum=3, seed=9), Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44)):
+    c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
+    a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
+    got = c.mul_relin_rescale(s.L, DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)).download()
+    assert np.array_equal(got, O.rescale(s, s.L, O.mul_relin(s, s.L, a, b))), s
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_MD_RESCALE": "0"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("s", SHAPES, ids=str)
@@ -215,8 +240,8 @@ print("ok")
 
 
 def test_fused_ntt_option_matches_oracle():
-    """The opt-in one-launch NTT (HS_NTT_FUSED=1: ticket-ordered passes, intermediate in L2) gives
-    the same limbs for every fused epilogue (plain, ModDown with tensor / automorphism sources,
+    """The opt-in one-launch NTT (HS_NTT_FUSED=1: ticket-ordered passes, intermediate in L2) and
+    the persistent prefetching passes (HS_NTT_DB=1) give the same limbs for every fused epilogue (plain, ModDown with tensor / automorphism sources,
     rescale) at odd and even ring degrees, several batch items, and lags shorter than the grid."""
     import os
     import subprocess
@@ -242,11 +267,12 @@ for logN, logp in ((10, 61), (13, 44), (15, 44), (16, 61)):
 print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for lag in ("2", "0.01"):
-        r = subprocess.run([sys.executable, "-c", code], cwd=root,
-                           env={**os.environ, "HS_NTT_FUSED": "1", "HS_NTT_LAG": lag},
+    # also the persistent prefetching pass kernel (HS_NTT_DB=1)
+    for extra in ({"HS_NTT_FUSED": "1", "HS_NTT_LAG": "2"}, {"HS_NTT_FUSED": "1", "HS_NTT_LAG": "0.01"},
+                  {"HS_NTT_DB": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **extra},
                            capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+        assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stderr[-2000:])
 
 
 # Base-conversion widths of k_conv_mma (KS = ceil(sources / 4) k-steps): alpha 1..16 sources per

@@ -150,6 +150,28 @@ def test_rescale_identity():
     assert worst <= ql * (N + 2)
 
 
+@pytest.mark.parametrize("level", [3, 1])
+def test_fused_mul_relin_rescale_identity(level):
+    """ModDown by P q_level with the tensor term folded in (rnso_mul_relin_rescale) decrypts to the
+    same value as mul_relin followed by rescale, up to the rounding of the two divisions."""
+    N, primes, sk = SPEC.N, O.primes(SPEC), O.secret(SPEC)
+    a, b = O.random_ct(SPEC, level, 11), O.random_ct(SPEC, level, 12)
+    fused = O.mul_relin_rescale(SPEC, level, a, b)
+    composed = O.rescale(SPEC, level, O.mul_relin(SPEC, level, a, b))
+    assert fused.shape == composed.shape and not np.array_equal(fused, composed)
+    pf = crt_centred(_phase(fused, level - 1, sk, primes, N), primes[:level])
+    pc = crt_centred(_phase(composed, level - 1, sk, primes, N), primes[:level])
+    Q = 1
+    for p in primes[:level]:
+        Q *= int(p)
+    worst = 0
+    for x, y in zip(pf, pc):
+        r = (x - y) % Q
+        r = r - Q if r > Q // 2 else r
+        worst = max(worst, abs(r))
+    assert worst <= 4 * N, worst
+
+
 @pytest.mark.parametrize("k", [1, 5, -3])
 def test_rotate_identity(k):
     level = 2
