@@ -86,6 +86,10 @@ int hs_rns_mul_relin(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint6
 int hs_rns_mul_relin_rescale(hs_rns* ctx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out,
                              uint32_t batch);
 int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch); /* out: level-1 */
+/* rescale(c * in) in one pass pair, c * in never stored (RnsB's mul_pt and level alignment); replaces
+   the reference evaluator's mul_pt + rescale (ckks.hpp:168-176 at the RNS level) */
+int hs_rns_rescale_mul_const(hs_rns* ctx, uint32_t level, const uint64_t* in, int64_t c, uint64_t* out,
+                             uint32_t batch);
 int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
 
 /* ---- the reference's statistics over RNS ciphertexts -------------------------------

@@ -164,6 +164,7 @@ _SIGS.update({
     "hs_rns_mul_relin": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_mul_relin_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_rns_rescale_mul_const": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32]),
     "hs_rns_rotate": (C.c_int, [RNS, C.c_uint32, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32]),
 })
 

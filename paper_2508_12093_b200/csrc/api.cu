@@ -929,6 +929,15 @@ int hs_rns_rescale(hs_rns* ctx, uint32_t level, const uint64_t* in, uint64_t* ou
   });
 }
 
+int hs_rns_rescale_mul_const(hs_rns* ctx, uint32_t level, const uint64_t* in, int64_t c, uint64_t* out,
+                             uint32_t batch) {
+  return guard([&] {
+    need(in, "in");
+    need(out, "out");
+    rns::rescale_mul_big(rctx(ctx), level, in, static_cast<double>(c), out, batch);
+  });
+}
+
 int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch) {
   return guard([&] {
     need(in, "in");

@@ -103,19 +103,33 @@ struct PlainLoad {
   __device__ uint64_t operator()(size_t off) const { return g[off]; }
 };
 
-struct RsLoad {  // rescale: [c_l]_{q_i} read straight from the coefficient-form last limb
+// Rescale of k c (k an integer constant, per-limb residues k_i; k = 1: plain rescale).  The
+// product is never stored: iNTT(k_l c_l) = k_l iNTT(c_l) mod q_l, so the spread multiplies
+// the coefficient-form last limb by k_l, and the combine computes (k_i c_i - t_i) q_l^-1 --
+// the same canonical words as multiplying first and rescaling after.
+struct RsLoad {  // rescale: [k_l c_l]_{q_i} read straight from the coefficient-form last limb
   const uint64_t* last;
   PrimeC P;
-  __device__ uint64_t operator()(size_t off) const { return reduce64(last[off], P); }
+  bool kon;
+  uint64_t kl, kl_sh, ql;
+  __device__ uint64_t operator()(size_t off) const {
+    return reduce64(kon ? mul_shoup(last[off], kl, kl_sh, ql) : last[off], P);
+  }
 };
 
-struct RsStore {  // rescale: out = (c_i - NTT([c_l]_{q_i})) * q_l^-1
+struct RsStore {  // rescale: out = (k_i c_i - NTT([k_l c_l]_{q_i})) * q_l^-1
   const uint64_t* in;
   uint64_t* out;
   uint64_t q, qinv, qinv_sh;
-  __device__ void operator()(size_t off, uint64_t v) const { out[off] = mul_shoup(sub_mod(in[off], v, q), qinv, qinv_sh, q); }
+  bool kon;
+  uint64_t k, k_sh;
+  __device__ void operator()(size_t off, uint64_t v) const {
+    const uint64_t c = kon ? mul_shoup(in[off], k, k_sh, q) : in[off];
+    out[off] = mul_shoup(sub_mod(c, v, q), qinv, qinv_sh, q);
+  }
 };
 
+constexpr int kRsMaxLimbs = 64;
 struct RsEpi {  // the rescale's spread and combine fused into its NTT passes
   const uint64_t* last;
   const uint64_t* in;
@@ -124,6 +138,8 @@ struct RsEpi {  // the rescale's spread and combine fused into its NTT passes
   const uint64_t* qinv_sh;
   size_t last_stride, in_stride, out_stride;
   uint32_t level;
+  bool kon = false;  // rescale of k c: k's residues and Shoup companions, limbs 0..level
+  uint64_t k[kRsMaxLimbs], k_sh[kRsMaxLimbs];
 };
 
 struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
@@ -655,13 +671,15 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
   } else if constexpr (MODE == 2) {  // row r = p * level + i: [last_p]_{q_i}
     const RsEpi& e = epi.rs;
     const uint32_t r = rm.orow[by], p = r / e.level;
-    run(RsLoad{e.last + bz * e.last_stride + (size_t(p) << LOGN) + toff, P}, PlainStore{go});
+    run(RsLoad{e.last + bz * e.last_stride + (size_t(p) << LOGN) + toff, P, e.kon, e.k[e.level], e.k_sh[e.level],
+               pcs[e.level].q},
+        PlainStore{go});
   } else if constexpr (MODE == 3) {
     const RsEpi& e = epi.rs;
     const uint32_t r = rm.orow[by], p = r / e.level, i = r - p * e.level;
     const RsStore st{e.in + bz * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
                      e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
-                     e.qinv_sh[i]};
+                     e.qinv_sh[i], e.kon, e.k[i], e.k_sh[i]};
     run(mk_ld<PlainLd>(gi, stage), st);
   } else {
     run(mk_ld<PlainLd>(gi, stage), PlainStore{go});
@@ -1956,6 +1974,13 @@ void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64
   const_op_res(c, level, a, res, out, batch, mul);
 }
 
+void rescale_mul_big(Ctx& c, uint32_t level, const uint64_t* a, double k, uint64_t* out, uint32_t batch) {
+  const __int128 v = i128_of(std::nearbyint(k));
+  std::vector<uint64_t> res(level + 1);
+  for (uint32_t i = 0; i <= level && i < c.primes.size(); ++i) res[i] = residue(v, c.primes[i]);
+  rescale_mul(c, level, a, &res, out, batch);
+}
+
 void const_op_big(const Ctx& c, uint32_t level, const uint64_t* a, double k, uint64_t* out, uint32_t batch,
                   bool mul) {
   const __int128 v = i128_of(std::nearbyint(k));
@@ -2523,7 +2548,14 @@ void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t
 }
 
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch) {
+  rescale_mul(c, level, in, nullptr, out, batch);
+}
+
+void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<uint64_t>* kres, uint64_t* out,
+                 uint32_t batch) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
+  if (kres && (kres->size() < level + 1 || level + 1 > uint32_t(kRsMaxLimbs)))
+    fail(HS_E_INVALID_ARG, "rns rescale_mul: constant residues");
   if (batch == 0) return;
   Runtime& rt = Runtime::get();
   const uint32_t N = c.N, nl = level + 1;
@@ -2542,8 +2574,15 @@ void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t
     rows[i] = i;
     primes[i] = i % level;
   }
-  const RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh), size_t(2) * N,
-                  in_stride, out_stride, level};
+  RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh), size_t(2) * N,
+            in_stride, out_stride, level};
+  if (kres) {
+    rse.kon = true;
+    for (uint32_t i = 0; i <= level; ++i) {
+      rse.k[i] = (*kres)[i] % c.primes[i];
+      rse.k_sh[i] = shoup_of(rse.k[i], c.primes[i]);
+    }
+  }
   ntt_rows(c, T, out_stride, T, out_stride, rows, rows, primes, batch, false, nullptr, &rse);
   cuda_ok(cudaGetLastError(), "rescale");
 }

@@ -161,6 +161,12 @@ void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b,
 void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64_t* out, uint32_t batch, bool mul);
 void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t batch);
+// rescale(k * in) without materialising k * in (kres: residues of the integer k, limbs 0..level;
+// null = 1); the words equal const_op(mul) followed by rescale
+void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<uint64_t>* kres, uint64_t* out,
+                 uint32_t batch);
+// the same for k = nearbyint(kd), |kd| < 2^127
+void rescale_mul_big(Ctx& c, uint32_t level, const uint64_t* a, double kd, uint64_t* out, uint32_t batch);
 // HMult + relinearisation + rescale (out at level - 1): the composition of the two ops.
 void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
 void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);

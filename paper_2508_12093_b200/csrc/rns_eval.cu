@@ -72,10 +72,8 @@ RCt RnsB::align(const RCt& x, int p) {
   }
   // scale sigma_k * C / q_k = sigma_p  =>  C = sigma_p q_k / sigma_k
   const double C = sigma_[p] * static_cast<double>(c_.primes[k]) / sigma_[k];
-  DevBuf m = rt.alloc(words(k));
-  const_op_big(c_, k, at, C, reinterpret_cast<uint64_t*>(m.get()), 1, true);
   DevBuf o = rt.alloc(words(p));
-  rescale(c_, k, reinterpret_cast<const uint64_t*>(m.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
+  rescale_mul_big(c_, k, at, C, reinterpret_cast<uint64_t*>(o.get()), 1);  // rescale(C x), C x never stored
   return make(o, p, x->level);
 }
 
@@ -139,12 +137,8 @@ RCt RnsB::mul_pt(RCt a, double c) {  // ckks.hpp:168-176
   if (p < 1) fail(HS_E_LEVEL_EXHAUSTED, "mul_pt: RNS modulus chain exhausted (deep chain too short)");
   // constant at sigma_{p-1} q_p / sigma_p: the product rescales onto sigma_{p-1} exactly
   const double C = c * sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p];
-  Runtime& rt = Runtime::get();
-  DevBuf m = rt.alloc(words(p));
-  const_op_big(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), C, reinterpret_cast<uint64_t*>(m.get()), 1,
-               true);
-  DevBuf o = rt.alloc(words(p - 1));
-  rescale(c_, p, reinterpret_cast<const uint64_t*>(m.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
+  DevBuf o = Runtime::get().alloc(words(p - 1));
+  rescale_mul_big(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), C, reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_pt;
   return make(o, p - 1, a->level - 1);
 }

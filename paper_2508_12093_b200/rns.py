@@ -206,6 +206,13 @@ class RnsContext:
         _check(_abi.lib().hs_rns_rescale(self.h, level, a.ptr, out.ptr, batch))
         return out
 
+    def rescale_mul_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
+                          batch: int = 1) -> DeviceBuffer:
+        """rescale(c * a) without materialising c * a (|c| < 2^53: passed exactly as a double)."""
+        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        _check(_abi.lib().hs_rns_rescale_mul_const(self.h, level, a.ptr, int(c), out.ptr, batch))
+        return out
+
     def rotate(self, level: int, k: int, a: DeviceBuffer, out: DeviceBuffer | None = None,
                batch: int = 1) -> DeviceBuffer:
         out = out or DeviceBuffer(batch * self.spec.ct_words(level))

@@ -145,6 +145,30 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def _const_mul(s, level, a, k):
+    """c * a limb by limb (numpy restatement with exact integers)."""
+    primes = [int(p) for p in O.primes(s)]
+    ct = a.reshape(2, level + 1, s.N)
+    out = np.empty_like(ct)
+    for i in range(level + 1):
+        q = primes[i]
+        kr = k % q
+        out[:, i, :] = np.array([(int(v) * kr) % q for v in ct[:, i, :].reshape(-1)], dtype=np.uint64).reshape(2, s.N)
+    return out.reshape(-1)
+
+
+@pytest.mark.parametrize("s", SHAPES[:3], ids=str)
+@pytest.mark.parametrize("k", [3, -7, (1 << 50) + 12345])
+def test_rescale_mul_const_matches_oracle(s, k):
+    """rescale(k c) fused (spread multiplies the last limb by k_l, combine computes k_i c_i) equals
+    the oracle's rescale of the materialised product, word for word."""
+    c = ctx(s)
+    level = s.L
+    a = O.random_ct(s, level, 41)
+    got = c.rescale_mul_const(level, _buf(a), k).download()
+    assert np.array_equal(got, O.rescale(s, level, _const_mul(s, level, a, k)))
+
+
 @pytest.mark.parametrize("s", SHAPES, ids=str)
 def test_rescale_matches_oracle(s):
     c = ctx(s)
