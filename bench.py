@@ -344,6 +344,11 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
         gbs = ab[k] / (v * 1e-6) / 1e9
         ops[k] = {"us_per_ct": round(v, 2), "ops_per_s": round(1e6 / v, 1), "alg_bytes": ab[k],
                   "achieved_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4), "launches": launches[k]}
+        tr = rns_traffic("ntt" if k == "intt" else k, logN, L, K)
+        if tr:  # real DRAM bytes (ncu) moved per ciphertext at this op's bench time
+            ops[k]["dram_bytes"] = round(tr)
+            ops[k]["dram_gbs"] = round(tr / (v * 1e-6) / 1e9, 1)
+            ops[k]["dram_frac"] = round(tr / (v * 1e-6) / 1e9 / peak, 4)
     sec = {"metric": "HMult+relin/s", "value": round(1e6 / us["mul_relin"], 1), "unit": "HMult+relin/s",
            "config": {"workload": "C5 tier R: batch of 64 random ciphertexts under seeded keys",
                       "logN": logN, "L": L, "K": K, "dnum": dnum, "level": L, "batch": batch,
@@ -352,13 +357,33 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
            "ops": ops,
            "roofline": {"bound": "hbm", "kernel": "HMult+relin (whole op, BASELINE.md §4 bytes)",
                         "achieved": ops["mul_relin"]["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                        "frac": ops["mul_relin"]["hbm_frac"], "traffic": None, "peak_source": src,
-                        "note": "integer-pipe bound (ncu: ALU pipe ~60% in the NTT), not HBM bound"},
+                        "frac": ops["mul_relin"]["hbm_frac"], "traffic": rns_traffic("mul_relin", logN, L, K),
+                        "peak_source": src,
+                        "traffic_source": "profiles/r1_tier_r_traffic.json (ncu dram bytes per ciphertext, "
+                                          "tools/rns_traffic.py, batch 16)",
+                        "note": "the key switch's intermediates and the two-pass NTTs go through HBM (real traffic "
+                                "~3.5x the algorithmic bytes); the NTT passes are FP64-issue/latency bound "
+                                "(ncu: FP64 pipe 40-56%, issue 47-51%), see profiles/r1_tier_r.md"},
            "parity_vs_oracle": rns_parity_small(),
            "znorm": rns_znorm(torch, stream)}
     if with_cpu:
         sec["cpu_baseline"] = rns_cpu_baseline(logN, L, K, dnum, logp)
     return sec
+
+
+def rns_traffic(op, logN, L, K):
+    """DRAM bytes per ciphertext of a Tier-R op from profiles/r1_tier_r_traffic.json (None if absent
+    or captured at another shape)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_tier_r_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        sh = d["shape"]
+        if (sh["logN"], sh["L"], sh["K"]) != (logN, L, K):
+            return None
+        return d["ops"][op]["dram_bytes_per_ct"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def kstat_traffic():

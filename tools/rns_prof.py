@@ -38,6 +38,8 @@ for _ in range(a.reps):
         c.ntt(x, 0, l + 1, batch=2 * B, inverse=True)
     elif a.op == "mul_relin":
         c.mul_relin(l, x, y, out, batch=B)
+    elif a.op == "mul_relin_rescale":
+        c.mul_relin_rescale(l, x, y, out, batch=B)
     elif a.op == "rescale":
         c.rescale(l, x, out, batch=B)
     elif a.op == "rotate":
