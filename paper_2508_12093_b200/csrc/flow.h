@@ -68,6 +68,14 @@ class Bsgs {
     const int d = static_cast<int>(coeffs.size()) - 1;
     if (d <= 0) return b_.add_pt(b_.sub_ct(x_, x_), coeffs.empty() ? 0.0 : coeffs[0]);
     build_powers(cheb_depth(d));
+    // Backends with a batched tree (RnsB): a full tree (d = 2^K - 1) runs level by level,
+    // one batched op per stage -- the same ops on the same operands as eval() below.
+    if constexpr (requires(B& bb, const C& xx, const std::vector<double>& cc, const std::vector<C>& pp) {
+                    bb.bsgs_full_tree(xx, cc, pp);
+                  }) {
+      const int K = cheb_depth(d);
+      if (d == (1 << K) - 1 && K >= 2 && b_.bsgs_batch_ok(x_, pw_, K)) return b_.bsgs_full_tree(x_, coeffs, pw_);
+    }
     return eval(coeffs);
   }
 

@@ -140,6 +140,14 @@ struct RsEpi {  // the rescale's spread and combine fused into its NTT passes
   uint32_t level;
   bool kon = false;  // rescale of k c: k's residues and Shoup companions, limbs 0..level
   uint64_t k[kRsMaxLimbs], k_sh[kRsMaxLimbs];
+  // per batch item constants instead (device, [batch][2][level + 1]: residues then Shoup)
+  const uint64_t* kitems = nullptr;
+  __device__ uint64_t kk(uint32_t bz, uint32_t i) const {
+    return kitems ? kitems[size_t(bz) * 2 * (level + 1) + i] : k[i];
+  }
+  __device__ uint64_t kk_sh(uint32_t bz, uint32_t i) const {
+    return kitems ? kitems[size_t(bz) * 2 * (level + 1) + level + 1 + i] : k_sh[i];
+  }
 };
 
 struct MdEpi {  // k_moddown fused into the last pass of the conv-rows NTT
@@ -671,15 +679,15 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
   } else if constexpr (MODE == 2) {  // row r = p * level + i: [last_p]_{q_i}
     const RsEpi& e = epi.rs;
     const uint32_t r = rm.orow[by], p = r / e.level;
-    run(RsLoad{e.last + bz * e.last_stride + (size_t(p) << LOGN) + toff, P, e.kon, e.k[e.level], e.k_sh[e.level],
-               pcs[e.level].q},
+    run(RsLoad{e.last + bz * e.last_stride + (size_t(p) << LOGN) + toff, P, e.kon, e.kk(bz, e.level),
+               e.kk_sh(bz, e.level), pcs[e.level].q},
         PlainStore{go});
   } else if constexpr (MODE == 3) {
     const RsEpi& e = epi.rs;
     const uint32_t r = rm.orow[by], p = r / e.level, i = r - p * e.level;
     const RsStore st{e.in + bz * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
                      e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
-                     e.qinv_sh[i], e.kon, e.k[i], e.k_sh[i]};
+                     e.qinv_sh[i], e.kon, e.kk(bz, i), e.kk_sh(bz, i)};
     run(mk_ld<PlainLd>(gi, stage), st);
   } else {
     run(mk_ld<PlainLd>(gi, stage), PlainStore{go});
@@ -1292,9 +1300,9 @@ __global__ void k_automorph(uint64_t* out, const uint64_t* in, uint64_t g, uint3
 // ---------------------------------------------------------------- HMult / key switching
 // tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 (NTT form, nl limbs)
 __global__ void k_tensor(const uint64_t* a, const uint64_t* b, uint64_t* d, const PrimeC* pcs, uint32_t nl,
-                         uint32_t logN, size_t ct_stride, size_t d_stride) {
+                         uint32_t logN, size_t ct_stride, size_t d_stride, size_t b_stride) {
   const uint64_t* A = a + blockIdx.z * ct_stride;
-  const uint64_t* Bb = b + blockIdx.z * ct_stride;
+  const uint64_t* Bb = b + blockIdx.z * b_stride;
   uint64_t* D = d + blockIdx.z * d_stride;
   const size_t half = size_t(nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
@@ -1952,6 +1960,36 @@ uint64_t residue(__int128 k, uint64_t q) {
   return static_cast<uint64_t>(r);
 }
 
+// add_pt with a per-item constant (RnsB's batched BSGS leaves): out_b = a_b + k_b on poly 0
+__global__ void k_addc_items(const uint64_t* a, const uint64_t* kt, uint64_t* out, const PrimeC* pcs, uint32_t nl,
+                             uint32_t logN, size_t total) {
+  const size_t per = size_t(2) * nl << logN;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total; x += size_t(gridDim.x) * blockDim.x) {
+    const size_t b = x / per, w = x - b * per, r = w >> logN;
+    const uint32_t i = r % nl;
+    out[x] = r < nl ? add_mod(a[x], kt[b * nl + i], pcs[i].q) : a[x];
+  }
+}
+
+void add_const_items(const Ctx& c, uint32_t level, const uint64_t* a, const std::vector<uint64_t>& kitems,
+                     uint64_t* out, uint32_t batch) {
+  if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns const op: level > L");
+  const uint32_t nl = level + 1;
+  if (kitems.size() < size_t(batch) * nl) fail(HS_E_INVALID_ARG, "rns add_const_items: item residues");
+  Runtime& rt = Runtime::get();
+  std::vector<uint64_t> tab(size_t(batch) * nl);
+  for (uint32_t b = 0; b < batch; ++b)
+    for (uint32_t i = 0; i < nl; ++i) tab[size_t(b) * nl + i] = kitems[size_t(b) * nl + i] % c.primes[i];
+  DevBuf kdev = rt.alloc(tab.size());
+  cuda_ok(cudaMemcpyAsync(kdev.get(), tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, rt.stream()),
+          "const items");
+  const size_t total = size_t(batch) * 2 * nl * c.N;
+  k_addc_items<<<grid_of(total), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(kdev), out, c.dpc(), nl, c.spec.logN,
+                                                        total);
+  cuda_ok(cudaGetLastError(), "const items");
+  rt.note_launch();
+}
+
 void const_op_res(const Ctx& c, uint32_t level, const uint64_t* a, const std::vector<uint64_t>& res, uint64_t* out,
                   uint32_t batch, bool mul) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns const op: level > L");
@@ -1972,6 +2010,11 @@ void const_op(const Ctx& c, uint32_t level, const uint64_t* a, int64_t k, uint64
   std::vector<uint64_t> res(level + 1);
   for (uint32_t i = 0; i <= level && i < c.primes.size(); ++i) res[i] = residue(k, c.primes[i]);
   const_op_res(c, level, a, res, out, batch, mul);
+}
+
+void residues_of(const Ctx& c, uint32_t level, double k, uint64_t* res) {
+  const __int128 v = i128_of(std::nearbyint(k));
+  for (uint32_t i = 0; i <= level && i < c.primes.size(); ++i) res[i] = residue(v, c.primes[i]);
 }
 
 void rescale_mul_big(Ctx& c, uint32_t level, const uint64_t* a, double k, uint64_t* out, uint32_t batch) {
@@ -2510,7 +2553,8 @@ void mul_relin(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uin
   DevBuf d = rt.alloc(size_t(batch) * 3 * half);
   uint64_t* D = dptr<uint64_t>(d);
   // layout per batch item: [d0 | d1 | d2], stride 3*half
-  k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half);
+  k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half,
+                                                                   ct);
   rt.note_launch();
   key_switch(c, level, D + 2 * half, 3 * half, key, D, D + half, 3 * half, out, ct, batch);
 }
@@ -2527,16 +2571,18 @@ static bool use_md_rescale() {
   return mode != 0;
 }
 
-void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch) {
+void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
+                       bool b_shared) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns mul_relin_rescale: level must be in [1, L]");
   if (batch == 0) return;
   Runtime& rt = Runtime::get();
-  if (use_md_rescale()) {
+  if (b_shared || use_md_rescale()) {
     const uint32_t N = c.N, nl = level + 1;
     const size_t ct = size_t(2) * nl * N, half = size_t(nl) * N;
     DevBuf d = rt.alloc(size_t(batch) * 3 * half);
     uint64_t* D = dptr<uint64_t>(d);
-    k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half);
+    k_tensor<<<dim3(grid_of(half), 1, batch), kT, 0, rt.stream()>>>(a, b, D, c.dpc(), nl, c.spec.logN, ct, 3 * half,
+                                                                     b_shared ? 0 : ct);
     rt.note_launch();
     key_switch(c, level, D + 2 * half, 3 * half, c.relin_key(), D, D + half, 3 * half, out, size_t(2) * level * N,
                batch, nullptr, true);
@@ -2553,20 +2599,43 @@ void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t
 
 void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<uint64_t>* kres, uint64_t* out,
                  uint32_t batch) {
+  rescale_mul_items(c, level, in, false, kres, nullptr, out, batch);
+}
+
+// rescale(k_b * in_b) for every batch item b: kres = one constant for all items (or null = 1),
+// kitems = per-item residues [batch][level + 1] (RnsB's batched BSGS leaves); shared_in: every
+// item reads the same input ciphertext (its last limb goes to coefficient form once).
+void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_in, const std::vector<uint64_t>* kres,
+                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
   if (kres && (kres->size() < level + 1 || level + 1 > uint32_t(kRsMaxLimbs)))
     fail(HS_E_INVALID_ARG, "rns rescale_mul: constant residues");
+  if (kitems && kitems->size() < size_t(batch) * (level + 1)) fail(HS_E_INVALID_ARG, "rns rescale_mul: item residues");
   if (batch == 0) return;
   Runtime& rt = Runtime::get();
   const uint32_t N = c.N, nl = level + 1;
-  const size_t in_stride = size_t(2) * nl * N, out_stride = size_t(2) * level * N;
+  const size_t in_stride = shared_in ? 0 : size_t(2) * nl * N, out_stride = size_t(2) * level * N;
   const KsPlan& P = ks_plan(c, level);
-  DevBuf last = rt.alloc(size_t(batch) * 2 * N);
+  const uint32_t nlast = shared_in ? 1 : batch;
+  DevBuf last = rt.alloc(size_t(nlast) * 2 * N);
   DevBuf t = rt.alloc(size_t(batch) * out_stride);
   uint64_t* LAST = dptr<uint64_t>(last);
   uint64_t* T = dptr<uint64_t>(t);
+  DevBuf kdev;
+  if (kitems) {  // [batch][2][nl]: residues then Shoup companions
+    std::vector<uint64_t> tab(size_t(batch) * 2 * nl);
+    for (uint32_t b = 0; b < batch; ++b)
+      for (uint32_t i = 0; i < nl; ++i) {
+        const uint64_t v = (*kitems)[size_t(b) * nl + i] % c.primes[i];
+        tab[size_t(b) * 2 * nl + i] = v;
+        tab[size_t(b) * 2 * nl + nl + i] = shoup_of(v, c.primes[i]);
+      }
+    kdev = rt.alloc(tab.size());
+    cuda_ok(cudaMemcpyAsync(kdev.get(), tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, rt.stream()),
+            "rescale constants");
+  }
   // last limb of both polys -> coefficient form (out of place)
-  ntt_rows(c, in, in_stride, LAST, size_t(2) * N, {level, nl + level}, {0, 1}, {level, level}, batch, true);
+  ntt_rows(c, in, size_t(2) * nl * N, LAST, size_t(2) * N, {level, nl + level}, {0, 1}, {level, level}, nlast, true);
   // NTT of [c_l]_{q_i} for every remaining limb: the spread is the column pass's load,
   // (c_i - t_i) q_l^-1 the row pass's store (t never materialised after the first pass)
   std::vector<uint32_t> rows(2 * level), primes(2 * level);
@@ -2574,9 +2643,12 @@ void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<u
     rows[i] = i;
     primes[i] = i % level;
   }
-  RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh), size_t(2) * N,
-            in_stride, out_stride, level};
-  if (kres) {
+  RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh),
+            shared_in ? 0 : size_t(2) * N, in_stride, out_stride, level};
+  if (kitems) {
+    rse.kon = true;
+    rse.kitems = dptr<const uint64_t>(kdev);
+  } else if (kres) {
     rse.kon = true;
     for (uint32_t i = 0; i <= level; ++i) {
       rse.k[i] = (*kres)[i] % c.primes[i];

@@ -167,8 +167,18 @@ void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<u
                  uint32_t batch);
 // the same for k = nearbyint(kd), |kd| < 2^127
 void rescale_mul_big(Ctx& c, uint32_t level, const uint64_t* a, double kd, uint64_t* out, uint32_t batch);
+// per-item constants kitems [batch][level + 1] (or one constant kres); shared_in: all items read `in`
+void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_in, const std::vector<uint64_t>* kres,
+                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch);
+// out_b = a_b + k_b (k_b residues [batch][level + 1], added to poly 0)
+void add_const_items(const Ctx& c, uint32_t level, const uint64_t* a, const std::vector<uint64_t>& kitems,
+                     uint64_t* out, uint32_t batch);
+// residues of the integer nearbyint(k), limbs 0..level
+void residues_of(const Ctx& c, uint32_t level, double k, uint64_t* res);
 // HMult + relinearisation + rescale (out at level - 1): the composition of the two ops.
-void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch);
+// b_shared: every batch item multiplies by the same b (stride 0)
+void mul_relin_rescale(Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
+                       bool b_shared = false);
 void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
 // Build (and upload) the per-level key-switching / rescale constants ahead of time,
 // so that ops can be captured into a CUDA graph.

@@ -5,10 +5,13 @@
 #include "rns_eval.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "rns_codec.h"
+#include "series.h"
 
 namespace hsg {
 namespace rns {
@@ -20,9 +23,10 @@ RnsB::RnsB(Ctx& c, const Params& p, Meter& m) : LedgerBase(p, m), c_(c) {
   for (uint32_t l = 1; l <= c.spec.L; ++l) sigma_[l] = std::sqrt(sigma_[l - 1] * static_cast<double>(c.primes[l]));
 }
 
-RCt RnsB::make(DevBuf b, int phys, int level) const {
+RCt RnsB::make(DevBuf b, int phys, int level, size_t off) const {
   auto d = std::make_shared<RCtData>();
   d->buf = std::move(b);
+  d->off = off;
   d->phys = phys;
   d->level = level;
   d->n = p_.S;
@@ -55,7 +59,7 @@ RCt RnsB::encrypt_const(double c) {
 RCt RnsB::align(const RCt& x, int p) {
   if (x->phys == p) return x;
   Runtime& rt = Runtime::get();
-  const uint64_t* src = reinterpret_cast<const uint64_t*>(x->buf.get());
+  const uint64_t* src = x->ptr();
   const int k = p + 1;  // drop limbs down to level p+1, then one scaled rescale to p
   DevBuf t;
   const uint64_t* at = src;
@@ -83,7 +87,7 @@ RCt RnsB::addsub(const RCt& a, const RCt& b, bool sub) {  // ckks.hpp:113-133
   const int p = std::min(a->phys, b->phys);
   const RCt x = align(a, p), y = align(b, p);
   DevBuf o = Runtime::get().alloc(words(p));
-  add_sub(c_, p, reinterpret_cast<const uint64_t*>(x->buf.get()), reinterpret_cast<const uint64_t*>(y->buf.get()),
+  add_sub(c_, p, x->ptr(), y->ptr(),
           reinterpret_cast<uint64_t*>(o.get()), 1, sub);
   ++m_.add;
   return make(o, p, std::min(a->level, b->level));
@@ -92,7 +96,7 @@ RCt RnsB::addsub(const RCt& a, const RCt& b, bool sub) {  // ckks.hpp:113-133
 RCt RnsB::add_pt(const RCt& a, double c) {  // ckks.hpp:137-144
   check_shape(sz(a));
   DevBuf o = Runtime::get().alloc(words(a->phys));
-  const_op_big(c_, a->phys, reinterpret_cast<const uint64_t*>(a->buf.get()), c * sigma_[a->phys],
+  const_op_big(c_, a->phys, a->ptr(), c * sigma_[a->phys],
                reinterpret_cast<uint64_t*>(o.get()), 1, false);
   ++m_.add;
   return make(o, a->phys, a->level);
@@ -101,7 +105,7 @@ RCt RnsB::add_pt(const RCt& a, double c) {  // ckks.hpp:137-144
 RCt RnsB::bootstrap(const RCt& a) {  // ckks.hpp:207-213: logical level reset (deep chain)
   check_shape(sz(a));
   ++m_.bootstrap;
-  return make(a->buf, a->phys, p_.max_level);
+  return make(a->buf, a->phys, p_.max_level, a->off);
 }
 
 RCt RnsB::mul_ct(RCt a, RCt b) {  // ckks.hpp:149-164
@@ -116,8 +120,8 @@ RCt RnsB::mul_ct(RCt a, RCt b) {  // ckks.hpp:149-164
   if (p < 1) fail(HS_E_LEVEL_EXHAUSTED, "mul_ct: RNS modulus chain exhausted (deep chain too short)");
   const RCt x = align(a, p), y = a == b ? x : align(b, p);
   DevBuf o = Runtime::get().alloc(words(p - 1));
-  mul_relin_rescale(c_, p, reinterpret_cast<const uint64_t*>(x->buf.get()),
-                    reinterpret_cast<const uint64_t*>(y->buf.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
+  mul_relin_rescale(c_, p, x->ptr(),
+                    y->ptr(), reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_ct;
   return make(o, p - 1, std::min(a->level, b->level) - 1);
 }
@@ -138,7 +142,7 @@ RCt RnsB::mul_pt(RCt a, double c) {  // ckks.hpp:168-176
   // constant at sigma_{p-1} q_p / sigma_p: the product rescales onto sigma_{p-1} exactly
   const double C = c * sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p];
   DevBuf o = Runtime::get().alloc(words(p - 1));
-  rescale_mul_big(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), C, reinterpret_cast<uint64_t*>(o.get()), 1);
+  rescale_mul_big(c_, p, a->ptr(), C, reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_pt;
   return make(o, p - 1, a->level - 1);
 }
@@ -154,7 +158,7 @@ RCt RnsB::mul_pt_vec(RCt a, const std::vector<double>& v) {  // ckks.hpp:179-189
               co.data());
   Runtime& rt = Runtime::get();
   DevBuf m = rt.alloc(words(p));
-  mul_plain_real(c_, p, reinterpret_cast<const uint64_t*>(a->buf.get()), co.data(), reinterpret_cast<uint64_t*>(m.get()));
+  mul_plain_real(c_, p, a->ptr(), co.data(), reinterpret_cast<uint64_t*>(m.get()));
   DevBuf o = rt.alloc(words(p - 1));
   rescale(c_, p, reinterpret_cast<const uint64_t*>(m.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_pt;
@@ -166,7 +170,7 @@ RCt RnsB::rotate(const RCt& a, long kk) {  // ckks.hpp:193-202
   const long n = static_cast<long>(p_.S);
   const long shift = ((kk % n) + n) % n;
   DevBuf o = Runtime::get().alloc(words(a->phys));
-  rns::rotate(c_, a->phys, shift, reinterpret_cast<const uint64_t*>(a->buf.get()),
+  rns::rotate(c_, a->phys, shift, a->ptr(),
               reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.rotate;
   return make(o, a->phys, a->level);
@@ -185,12 +189,152 @@ RCt RnsB::sum_all_slots(const RCt& a, size_t n_valid) {  // ckks.hpp:218-230
   return acc;
 }
 
+// ---- batched BSGS ---------------------------------------------------------------------
+RnsB::Batch RnsB::slice(const Batch& b, uint32_t first, uint32_t count) const {
+  Batch r = b;
+  r.off = b.off + size_t(first) * words(b.phys);
+  r.n = count;
+  return r;
+}
+
+// RnsB::align for n ciphertexts at once (same constant, same rescale): words identical
+RnsB::Batch RnsB::align_batch(const Batch& b, int p) {
+  if (b.phys == p) return b;
+  Runtime& rt = Runtime::get();
+  const int k = p + 1;
+  const uint64_t* at = b.ptr();
+  DevBuf t;
+  if (b.phys > k) {  // drop limbs: rows 0..k of every polynomial of every item
+    t = rt.alloc(size_t(b.n) * words(k));
+    const size_t row = c_.N * sizeof(uint64_t);
+    cuda_ok(cudaMemcpy2DAsync(t.get(), size_t(k + 1) * row, at, size_t(b.phys + 1) * row, size_t(k + 1) * row,
+                              size_t(2) * b.n, cudaMemcpyDeviceToDevice, rt.stream()),
+            "drop limbs (batch)");
+    at = reinterpret_cast<const uint64_t*>(t.get());
+  }
+  const double C = sigma_[p] * static_cast<double>(c_.primes[k]) / sigma_[k];
+  std::vector<uint64_t> res(k + 1);
+  residues_of(c_, k, C, res.data());
+  Batch o;
+  o.buf = rt.alloc(size_t(b.n) * words(p));
+  o.phys = p;
+  o.level = b.level;
+  o.n = b.n;
+  rescale_mul_items(c_, k, at, false, &res, nullptr, reinterpret_cast<uint64_t*>(o.buf.get()), b.n);
+  return o;
+}
+
+// HS_RNS_BSGS=0: always the op-by-op recursion (A/B and parity switch)
+static bool bsgs_batch_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HS_RNS_BSGS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool RnsB::bsgs_batch_ok(const RCt& x, const std::vector<RCt>& pw, int K) const {
+  if (!bsgs_batch_enabled() || !x || K < 2 || static_cast<int>(pw.size()) < K) return false;
+  int lv = x->level, ph = x->phys;
+  if (lv < 1 || ph < 1) return false;
+  --lv, --ph;  // leaves: mul_pt then add_pt
+  for (int h = 1; h < K; ++h) {
+    const RCt& T = pw[h];
+    if (!T || lv < 1 || T->level < 1) return false;
+    const int p = std::min(ph, T->phys);
+    if (p < 1) return false;
+    const int hl = std::min(lv, T->level) - 1, hp = p - 1;
+    lv = std::min(hl, lv);
+    ph = std::min(hp, ph);
+  }
+  return true;
+}
+
+RCt RnsB::bsgs_full_tree(const RCt& x, const std::vector<double>& coeffs, const std::vector<RCt>& pw) {
+  int K = 0;
+  while ((size_t(1) << K) < coeffs.size()) ++K;
+  // leaf coefficients through the reference's own split (chebyshev.hpp:140-158), placed in
+  // the storage order that makes every stage's q- and r-children contiguous halves
+  std::vector<std::vector<uint32_t>> order(K);
+  order[K - 1] = {0};
+  for (int h = K - 1; h >= 1; --h) {
+    for (uint32_t v : order[h]) order[h - 1].push_back(2 * v + 1);  // q-children first
+    for (uint32_t v : order[h]) order[h - 1].push_back(2 * v);      // then r-children
+  }
+  const uint32_t n0 = 1u << (K - 1);
+  std::vector<double> c0(n0), c1(n0);
+  std::vector<uint32_t> pos(n0);
+  for (uint32_t i = 0; i < n0; ++i) pos[order[0][i]] = i;
+  std::function<void(const std::vector<double>&, int, uint32_t)> collect =
+      [&](const std::vector<double>& c, int h, uint32_t j) {
+        if (h == 0) {
+          c0[pos[j]] = c[0];
+          c1[pos[j]] = c.size() > 1 ? c[1] : 0.0;
+          return;
+        }
+        std::vector<double> q, r;
+        split_series(c, &q, &r);
+        collect(q, h - 1, 2 * j + 1);
+        collect(r, h - 1, 2 * j);
+      };
+  collect(coeffs, K - 1, 0);
+
+  Runtime& rt = Runtime::get();
+  // leaves: mul_pt(x, c1) (rescale of c1' x, x shared), then add_pt(., c0)
+  const int p0 = x->phys;
+  Batch R;
+  R.phys = p0 - 1;
+  R.level = x->level - 1;
+  R.n = n0;
+  R.buf = rt.alloc(size_t(n0) * words(R.phys));
+  {
+    std::vector<uint64_t> km(size_t(n0) * (p0 + 1)), ka(size_t(n0) * p0);
+    for (uint32_t i = 0; i < n0; ++i) {  // the constants exactly as mul_pt / add_pt compute them
+      residues_of(c_, p0, c1[i] * sigma_[p0 - 1] * static_cast<double>(c_.primes[p0]) / sigma_[p0],
+                  &km[size_t(i) * (p0 + 1)]);
+      residues_of(c_, p0 - 1, c0[i] * sigma_[p0 - 1], &ka[size_t(i) * p0]);
+    }
+    uint64_t* o = reinterpret_cast<uint64_t*>(R.buf.get());
+    rescale_mul_items(c_, p0, x->ptr(), true, nullptr, &km, o, n0);
+    m_.mul_pt += n0;
+    add_const_items(c_, p0 - 1, o, ka, o, n0);
+    m_.add += n0;
+  }
+  // height h: head = mul_ct(q-child, T_{2^h}); node = add_ct(head, r-child)
+  for (int h = 1; h < K; ++h) {
+    const uint32_t nh = R.n / 2;
+    Batch Q = slice(R, 0, nh), Rr = slice(R, nh, nh);
+    const RCt& T = pw[h];
+    const int p = std::min(Q.phys, T->phys);
+    Q = align_batch(Q, p);
+    const RCt Ta = align(T, p);
+    Batch H;
+    H.phys = p - 1;
+    H.level = std::min(Q.level, T->level) - 1;
+    H.n = nh;
+    H.buf = rt.alloc(size_t(nh) * words(H.phys));
+    mul_relin_rescale(c_, p, Q.ptr(), Ta->ptr(), reinterpret_cast<uint64_t*>(H.buf.get()), nh, true);
+    m_.mul_ct += nh;
+    const int p2 = std::min(H.phys, Rr.phys);
+    const Batch Ha = align_batch(H, p2), Ra = align_batch(Rr, p2);
+    Batch S;
+    S.phys = p2;
+    S.level = std::min(H.level, Rr.level);
+    S.n = nh;
+    S.buf = rt.alloc(size_t(nh) * words(p2));
+    add_sub(c_, p2, Ha.ptr(), Ra.ptr(), reinterpret_cast<uint64_t*>(S.buf.get()), nh, false);
+    m_.add += nh;
+    R = S;
+  }
+  return make(R.buf, R.phys, R.level, R.off);
+}
+
 std::vector<double> RnsB::decrypt(const RCt& c, size_t n) {
   // q_0 alone cannot hold sigma_0 * value for |value| >= 2^(log q_0 - log sigma_0 - 1): decrypt through two limbs
   if (c->phys < 1)
     fail(HS_E_LEVEL_EXHAUSTED, "rns decrypt: result at the last RNS limb (chain must exceed the statistic's depth)");
   std::vector<double> co(c_.N);
-  decrypt_crt(c_, c->phys, reinterpret_cast<const uint64_t*>(c->buf.get()), co.data());
+  decrypt_crt(c_, c->phys, c->ptr(), co.data());
   std::vector<double> z(n);
   decode_real(c_.spec.logN, co.data(), sigma_[c->phys], z.data(), n);
   return z;

@@ -29,10 +29,12 @@ namespace hsg {
 namespace rns {
 
 struct RCtData {
-  DevBuf buf;  // u64 [2][phys+1][N], NTT form
+  DevBuf buf;      // u64 [2][phys+1][N], NTT form, at word offset `off` (a batched op's output slice)
+  size_t off = 0;
   int phys = 0;
   int level = 0;
   size_t n = 0;
+  const uint64_t* ptr() const { return reinterpret_cast<const uint64_t*>(buf.get()) + off; }
 };
 using RCt = std::shared_ptr<const RCtData>;
 
@@ -65,11 +67,28 @@ class RnsB : public LedgerBase<RnsB, RCt> {
   std::vector<double> decrypt(const C& c, size_t n);
   double scale(int phys) const { return sigma_[static_cast<size_t>(phys)]; }
 
+  // Batched BSGS (flow.h Bsgs::run): a full tree (2^K coefficients) evaluated level by level,
+  // each stage one batched op over all its nodes -- the same ops on the same operands as the
+  // recursion (identical limbs, meter and levels), ~K stages instead of ~2^K op calls.
+  // bsgs_batch_ok: every multiplication of the tree has operands at level >= 1 and physical
+  // level >= 1 (no auto-bootstrap, no level_exhausted inside), else the recursion runs.
+  bool bsgs_batch_ok(const C& x, const std::vector<C>& pw, int K) const;
+  C bsgs_full_tree(const C& x, const std::vector<double>& coeffs, const std::vector<C>& pw);
+
  private:
+  struct Batch {  // n ciphertexts at one (phys, level), contiguous from ptr
+    DevBuf buf;
+    size_t off = 0;
+    int phys = 0, level = 0;
+    uint32_t n = 0;
+    const uint64_t* ptr() const { return reinterpret_cast<const uint64_t*>(buf.get()) + off; }
+  };
+  Batch slice(const Batch& b, uint32_t first, uint32_t count) const;
+  Batch align_batch(const Batch& b, int p);
   C addsub(const C& a, const C& b, bool sub);
   C prepare_mul_pt(C a);
   C align(const C& x, int p);  // same value at physical level p (<= x->phys), scale sigma_p
-  C make(DevBuf b, int phys, int level) const;
+  C make(DevBuf b, int phys, int level, size_t off = 0) const;
   size_t words(int phys) const { return size_t(2) * (phys + 1) * c_.N; }
   size_t sz(const C& c) const { return c ? c->n : 0; }
   Ctx& c_;

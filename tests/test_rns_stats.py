@@ -202,3 +202,39 @@ def test_znorm_full_size_north_star():
     assert ref.rc == 0
     _check_vector(z, ref.out)
     assert _meter(e) == ref.meter and lv[0] == ref.levels[0]
+
+
+def test_batched_bsgs_matches_recursion():
+    """RnsB's level-order batched BSGS (one batched op per tree stage) and the op-by-op
+    recursion (HS_RNS_BSGS=0) give bit-identical decrypted outputs, meters and levels."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, hashlib; sys.path[:0] = ["tests", "."]
+import numpy as np
+import test_rns_stats as T
+from paper_2508_12093_b200 import rns as R
+from paper_2508_12093_b200 import hestat as H
+x = T._normal(5, T.S, 50.0, 10.0)
+y = 0.6 * x + T._normal(6, T.S, 0.0, 4.0)
+out = []
+e = T._eval(T.LOGN, T.L)
+v, lv = e.stat(R.ZNORM, x, 100.0)
+out.append((v.tobytes(), tuple(lv), T._meter(e)))
+e = T._eval(T.LOGN, T.L)
+v, lv = e.stat(R.PEARSON, x, 20.0, y=y)
+out.append((v.tobytes(), tuple(lv), T._meter(e)))
+e = T._eval(T.LOGN, T.L)
+v, lv = e.stat(R.INVSQRT, np.linspace(0.01, 1.0, T.S), 1.0, cfg=H.InvRootConfig(cheb_degree=15, newton_iters=2))
+out.append((v.tobytes(), tuple(lv), T._meter(e)))
+print(hashlib.sha256(repr(out).encode()).hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = []
+    for mode in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_RNS_BSGS": mode},
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
