@@ -1319,7 +1319,7 @@ constexpr int kMaxSrc = 32, kMaxTgt = 64;
 struct ConvJob {
   uint32_t nsrc, ntgt;
   uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
-  uint32_t frag_off, pad_;   // k_conv_mma: this job's B fragments (uint2 index into the plan's table)
+  uint32_t frag_off, frag_off2;  // B fragments of k_conv_mma / k_conv_mma2 (uint2 index into the plan's table)
   uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
   uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
   uint64_t h[kMaxTgt][kMaxSrc];
@@ -1566,6 +1566,127 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
     mma_park(t, 0);
     __syncwarp();
     finish(t, 0);
+  }
+}
+
+// ---- base conversion, targets on the MMA's N dimension (HS_CONV_MMA=2) -------------------
+// The same exact byte-split product as k_conv_mma, with the roles of the two small
+// dimensions swapped: one m16n8k32 IMMA covers 8 TARGETS for one output byte b,
+//   B_b[8i + a][t] = byte b of (h[t][i] 2^(8a) mod q_t),   C_b[n][t] = sum_k A[n][k] B_b[k][t],
+// so each thread's accumulator fragment already holds whole outputs (rows g, g+8 of each
+// m16 tile, targets 2 (lane & 3) + 0..1): out_t[n] = sum_b C_b 2^(8b) is accumulated in
+// registers (lo: b < 4, hi: b >= 4, one IMAD.WIDE per byte) instead of parking C in shared
+// memory.  Groups whose targets are all < 2^45 skip bytes 6 and 7 (h' < 2^45).  Same epilogue
+// arithmetic as k_conv_mma, so the words are identical.
+template <int KS>
+#ifndef HS_CONV2_MINB
+#define HS_CONV2_MINB 4
+#endif
+__global__ void __launch_bounds__(kConvMmaRows, HS_CONV2_MINB) k_conv_mma2(const uint64_t* in, size_t in_stride, uint64_t* out,
+                                                             size_t out_stride, const ConvJob* jobs,
+                                                             const uint2* frags, const PrimeC* pcs, uint32_t logN) {
+  constexpr int RSW = KS * 8 + 4;
+  extern __shared__ uint4 dyn_smem[];
+  uint32_t* As = reinterpret_cast<uint32_t*>(dyn_smem);  // [128][RSW]
+  __shared__ PrimeC tq[kMaxTgt];
+  __shared__ ConvTgt tc[kMaxTgt];
+  __shared__ uint64_t hinv_s[4 * KS], hinvsh_s[4 * KS], qs_s[4 * KS];
+  __shared__ uint8_t gfp[kMaxTgt / 8];
+  const ConvJob& J = jobs[blockIdx.y];
+  const uint32_t nsrc = J.nsrc, ntgt = J.ntgt, ngrp = (ntgt + 7) / 8;
+  for (uint32_t k = threadIdx.x; k < ntgt; k += kConvMmaRows) {
+    const PrimeC P = pcs[J.tgt[k]];
+    tq[k] = P;
+    const uint64_t c32 = (uint64_t(1) << 32) % P.q;
+    tc[k] = ConvTgt{P.qd, P.qinvd, static_cast<double>(c32), J.out_row + J.tgt_row[k], P.fp};
+  }
+  if (threadIdx.x < nsrc) {
+    hinv_s[threadIdx.x] = J.hinv[threadIdx.x];
+    hinvsh_s[threadIdx.x] = J.hinv_sh[threadIdx.x];
+    qs_s[threadIdx.x] = pcs[J.src[threadIdx.x]].q;
+  }
+  __syncthreads();
+  if (threadIdx.x < ngrp) {
+    bool all = true;
+    for (uint32_t t = 8 * threadIdx.x; t < min(8 * threadIdx.x + 8, ntgt); ++t) all = all && tq[t].fp;
+    gfp[threadIdx.x] = all ? 1 : 0;
+  }
+  const uint32_t n0 = blockIdx.x * kConvMmaRows;
+  {  // y_i = [x_i hinv_i]_{q_i}: thread = coefficient, the u64 words are the A row's bytes
+    const uint64_t* I = in + blockIdx.z * in_stride + (size_t(J.in_row) << logN) + n0 + threadIdx.x;
+    uint2* row = reinterpret_cast<uint2*>(As + threadIdx.x * RSW);
+    uint64_t x[4 * KS];
+#pragma unroll
+    for (int i = 0; i < 4 * KS; ++i) x[i] = uint32_t(i) < nsrc ? __ldcs(I + (size_t(i) << logN)) : 0;
+#pragma unroll
+    for (int i = 0; i < 4 * KS; ++i) {
+      const uint64_t y = uint32_t(i) < nsrc ? mul_shoup(x[i], hinv_s[i], hinvsh_s[i], qs_s[i]) : 0;
+      row[i] = make_uint2(static_cast<uint32_t>(y), static_cast<uint32_t>(y >> 32));
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  uint32_t a[2][KS][4];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint32_t* r0 = As + (warp * 32 + m * 16 + g) * RSW + ks * 8 + t4;
+      const uint32_t* r1 = r0 + 8 * RSW;
+      a[m][ks][0] = r0[0];
+      a[m][ks][1] = r1[0];
+      a[m][ks][2] = r0[4];
+      a[m][ks][3] = r1[4];
+    }
+  uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + g;
+  const uint2* F = frags + J.frag_off2 + lane;
+#pragma unroll 1
+  for (uint32_t grp = 0; grp < ngrp; ++grp) {
+    uint64_t lo[2][4], hi[2][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) lo[m][r] = hi[m][r] = 0;
+    const int nb = gfp[grp] ? 6 : 8;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      if (b >= nb) break;
+      uint2 bf[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(F + ((grp * 8 + b) * KS + ks) * 32);
+      int c[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        imma_u8(c[0], a[0][ks], bf[ks]);
+        imma_u8(c[1], a[1][ks], bf[ks]);
+      }
+      const uint32_t mulb = 1u << (8 * (b & 3));
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint64_t v = uint64_t(static_cast<uint32_t>(c[m][r])) * mulb;
+          if (b < 4) lo[m][r] += v;
+          else hi[m][r] += v;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t t = grp * 8 + 2 * t4 + (r & 1);
+      if (t >= ntgt) continue;
+      const ConvTgt T = tc[t];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        uint64_t v;
+        if (T.fp) {
+          const double h = fp_mulmod(u2d(hi[m][r]), T.c32d, T.qd, T.qinvd);
+          v = fp_canon(__dadd_rn(h, u2d(lo[m][r])), T.qd, T.qinvd);
+        } else {
+          v = reduce128((static_cast<u128>(hi[m][r]) << 32) + lo[m][r], tq[t]);
+        }
+        O[(size_t(T.orow) << logN) + m * 16 + (r >= 2 ? 8 : 0)] = v;
+      }
+    }
   }
 }
 
@@ -2158,10 +2279,42 @@ void conv_frags(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
   }
 }
 
+// k_conv_mma2's B operand: [target group of 8][output byte b][k-step][lane] -> (b0, b1) = bytes
+// B_b[32 ks + 4 (lane & 3) + 0..3][lane >> 2] and the same at k + 16, B_b[8i + a][t'] = byte b of
+// (h[8 group + t'][i] 2^(8a) mod q_t) (0 beyond the job's targets).
+void conv_frags2(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
+  const uint32_t KS = conv_ks(J.nsrc), K = 32 * KS, ngrp = (J.ntgt + 7) / 8;
+  std::vector<uint8_t> hb(size_t(8) * 8 * K);  // [byte][t'][k]
+  for (uint32_t grp = 0; grp < ngrp; ++grp) {
+    std::fill(hb.begin(), hb.end(), 0);
+    for (uint32_t tp = 0; tp < 8; ++tp) {
+      const uint32_t t = 8 * grp + tp;
+      if (t >= J.ntgt) break;
+      const uint64_t qt = c.primes[J.tgt[t]];
+      for (uint32_t i = 0; i < J.nsrc; ++i)
+        for (uint32_t a = 0; a < 8; ++a) {
+          const uint64_t v = h_mulmod(J.h[t][i] % qt, h_pow(2, 8 * a, qt), qt);
+          for (uint32_t b = 0; b < 8; ++b) hb[(size_t(b) * 8 + tp) * K + 8 * i + a] = static_cast<uint8_t>(v >> (8 * b));
+        }
+    }
+    for (uint32_t b = 0; b < 8; ++b)
+      for (uint32_t ks = 0; ks < KS; ++ks)
+        for (uint32_t lane = 0; lane < 32; ++lane) {
+          const uint8_t* col = hb.data() + (size_t(b) * 8 + (lane >> 2)) * K + 32 * ks + 4 * (lane & 3);
+          auto pack = [](const uint8_t* p) {
+            return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+          };
+          f->push_back(make_uint2(pack(col), pack(col + 16)));
+        }
+  }
+}
+
 void attach_frags(const Ctx& c, std::vector<ConvJob>* jobs, std::vector<uint2>* f) {
   for (ConvJob& J : *jobs) {
     J.frag_off = static_cast<uint32_t>(f->size());
     conv_frags(c, J, f);
+    J.frag_off2 = static_cast<uint32_t>(f->size());
+    conv_frags2(c, J, f);
   }
 }
 
@@ -2373,17 +2526,31 @@ bool use_ks_fusion(int mode_bit) {
   return (mode & mode_bit) != 0;
 }
 
-bool use_conv_mma() {
+// HS_CONV_MMA: 1 = k_conv_mma (C parked in shared memory per target), 2 = k_conv_mma2 (targets
+// on the MMA's N dimension), 0 = the ALU/FP64 k_conv
+int use_conv_mma() {
   static const int mode = [] {
     const char* e = std::getenv("HS_CONV_MMA");
     return e ? std::atoi(e) : 1;
   }();
-  return mode != 0;
+  return mode;
+}
+
+template <int KS>
+void launch_conv_mma2(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
+                      const uint2* frags, uint32_t njobs, const Ctx& c, uint32_t batch, cudaStream_t s) {
+  constexpr size_t smem = size_t(kConvMmaRows) * (KS * 8 + 4) * 4;
+  const dim3 g(c.N / kConvMmaRows, njobs, batch);
+  k_conv_mma2<KS><<<g, kConvMmaRows, smem, s>>>(in, in_stride, out, out_stride, jobs, frags, c.dpc(), c.spec.logN);
 }
 
 template <int KS>
 void launch_conv_mma(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
                      const uint2* frags, uint32_t njobs, uint32_t ntgt, const Ctx& c, uint32_t batch, cudaStream_t s) {
+  if (use_conv_mma() == 2) {
+    launch_conv_mma2<KS>(in, in_stride, out, out_stride, jobs, frags, njobs, c, batch, s);
+    return;
+  }
   static const bool attr = [] {
     cuda_ok(cudaFuncSetAttribute(k_conv_mma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(conv_mma_smem<KS>())),

@@ -321,8 +321,10 @@ def test_conv_widths_mul_relin_and_rotate(s):
         assert np.array_equal(c.rotate(level, 3, _buf(a)).download(), O.rotate(s, level, 3, a)), level
 
 
-def test_alu_conversion_option_matches_oracle():
-    """HS_CONV_MMA=0 (the ALU/FP64 base conversion instead of the tensor-core one) gives the same limbs."""
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_alu_conversion_option_matches_oracle(mode):
+    """HS_CONV_MMA=0 (the ALU/FP64 base conversion instead of the tensor-core one) and HS_CONV_MMA=2
+    (targets on the MMA's N dimension, k_conv_mma2) give the same limbs."""
     import os
     import subprocess
     import sys
@@ -332,15 +334,17 @@ import numpy as np
 from rns_abi import RnsOracle, Spec
 from paper_2508_12093_b200.rns import RnsContext, RnsSpec, DeviceBuffer
 O = RnsOracle()
-for s in (Spec(logN=12, L=7, K=3, dnum=3, seed=11), Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44)):
+for s in (Spec(logN=12, L=7, K=3, dnum=3, seed=11), Spec(logN=13, L=6, K=3, dnum=3, seed=9, logp=44),
+          Spec(logN=10, L=15, K=2, dnum=1, seed=21), Spec(logN=10, L=9, K=12, dnum=5, seed=23, logp=44)):
     c = RnsContext(RnsSpec(s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, seed=s.seed))
     a, b = O.random_ct(s, s.L, 1), O.random_ct(s, s.L, 2)
     got = c.mul_relin(s.L, DeviceBuffer(a.size).upload(a), DeviceBuffer(b.size).upload(b)).download()
     assert np.array_equal(got, O.mul_relin(s, s.L, a, b)), s
+    assert np.array_equal(c.rotate(s.L, 3, DeviceBuffer(a.size).upload(a)).download(), O.rotate(s, s.L, 3, a)), s
 print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_CONV_MMA": "0"},
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "HS_CONV_MMA": mode},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
