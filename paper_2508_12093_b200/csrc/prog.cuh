@@ -57,6 +57,10 @@ __device__ __forceinline__ double ffull_small(int K, const F& f, const double* t
   }
 }
 
+#ifndef HS_BLK_UNROLL
+#define HS_BLK_UNROLL 4
+#endif
+constexpr int kBlkUnroll = HS_BLK_UNROLL;  // leaf blocks in flight per thread (ILP of the tree walk)
 template <int ST, class F>
 __device__ __forceinline__ double ffull_dyn(int K, const F& f, const double* t, const double (&T)[kMaxK]) {
   if (K <= kBK) return ffull_small<ST>(K, f, t, T);
@@ -64,7 +68,7 @@ __device__ __forceinline__ double ffull_dyn(int K, const F& f, const double* t, 
   constexpr int BS = (1 << kBK) * ST;
   double stk[kMaxK];
   double v = 0.0;
-#pragma unroll 1
+#pragma unroll(kBlkUnroll)
   for (int j = 0; j < nb; ++j) {
     v = ffull<kBK, ST>(f, t + j * BS, T);
 #pragma unroll
