@@ -289,11 +289,14 @@ void with_q(QSpec qs, F&& f) {
   }
 }
 
-// HS_COOP=1: launch through cudaLaunchCooperativeKernel (the barrier is the same either way)
+// HS_COOP (default 1): launch through cudaLaunchCooperativeKernel, which guarantees the grid is
+// co-resident even when other streams' kernels hold SMs; 0 = a plain launch (the occupancy
+// check above still sizes the grid to fit).  The barrier is the same either way, and the two
+// measured alike (device time and host enqueue).
 bool coop_launch() {
   static const bool on = [] {
     const char* e = std::getenv("HS_COOP");
-    return e && std::atoi(e) != 0;
+    return !e || std::atoi(e) != 0;
   }();
   return on;
 }

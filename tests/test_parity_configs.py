@@ -45,3 +45,35 @@ def test_config_gpu(key):
     assert np.array_equal(bits(out), bits(oout[: len(out)]))
     if hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == d["input_sha256"]:
         assert _sha(out) == d["sha256"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"HS_COOP": "0"}, {"HESTAT_LANES": "1"}, {"HESTAT_LANES": "4"}])
+def test_znorm_launch_options_bit_exact(env):
+    """The statistics kernel under a plain launch (HS_COOP=0) and other lane splits gives the
+    oracle's bits for the C2 Z-score (pipelined encode on the upload stream included)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys; sys.path[:0] = ["tests", "."]
+import numpy as np
+from paper_2508_12093_b200 import hestat as H, workloads as W
+from oracle_abi import Params, ST_ZNORM, bits, oracle
+H.init(0)
+S = 32768
+x = W.normal(H.synthetic_uniform, 21, S, 50.0, 10.0)
+ctx = H.EvalContext(H.CkksParams(slot_count=S))
+ref = oracle().stat(Params(slot_count=S), ST_ZNORM, x, 100.0)
+col = H.encode_column(ctx, x)
+for _ in range(3):
+    zc = H.znorm(ctx, col, 100.0)
+    col = H.encode_column(ctx, x)
+    z = H.decode_column(ctx, zc)
+    assert np.array_equal(bits(z), bits(ref.out))
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
