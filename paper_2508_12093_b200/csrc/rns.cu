@@ -390,6 +390,11 @@ __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_
 // 64-bit Shoup path) to addressing.  Results are identical: the NTT of canonical
 // input is a unique canonical vector.
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: fl(x + M) - M = rint(x), |x| < 2^51
+#ifndef HS_NTT_RAW
+#define HS_NTT_RAW 1
+#endif
+// intermediate between the two passes as raw fp64 (HS_NTT_RAW=0: canonical u64 words)
+constexpr int kRawOut = HS_NTT_RAW ? 1 : 0, kRawIn = HS_NTT_RAW ? 2 : 0;
 constexpr double kTwo52 = 4503599627370496.0;
 
 __device__ __forceinline__ double u2d(uint64_t v) {  // exact for v < 2^52
@@ -435,7 +440,11 @@ __device__ __forceinline__ void stage_row_tw(double* tws, const double* tw, uint
   }
 }
 
-template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST>
+// RAWM: 0 canonical u64 in and out; 1 (first pass of a two-pass NTT) the output stays as raw
+// fp64 bits (unreduced forward / folded inverse values) for the second pass; 2 (second pass)
+// the input is those raw fp64 bits.  Saves the canonicalisation and the integer-to-double
+// conversion between the passes (the intermediate is read by nothing else).
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST, int RAWM = 0>
 __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
                                             double qinv, uint32_t tile0, double ninv,
@@ -464,10 +473,12 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
 #pragma unroll
     for (int k = 0; k < (1 << RB); ++k) {
       const uint32_t e = j0 + (uint32_t(k) << logs);
-      if (FIRST)
-        x[k] = u2d(gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr));
-      else
+      if (FIRST) {
+        const uint64_t g = gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr);
+        x[k] = RAWM == 2 ? __longlong_as_double(static_cast<long long>(g)) : u2d(g);
+      } else {
         x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
+      }
     }
     if (!INV) {
 #pragma unroll
@@ -506,7 +517,7 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
           }
         }
       }
-      if (!LAST) {
+      if (!LAST || RAWM == 1) {
 #pragma unroll
         for (int k = 0; k < (1 << RB); ++k) x[k] = fp_fold(x[k], q, qinv);
       }
@@ -514,7 +525,10 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
 #pragma unroll
     for (int k = 0; k < (1 << RB); ++k) {
       const uint32_t e = j0 + (uint32_t(k) << logs);
-      if (LAST) {
+      if (LAST && RAWM == 1) {
+        gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr,
+             static_cast<uint64_t>(__double_as_longlong(x[k])));
+      } else if (LAST) {
         const double v = (INV && !ROWS) ? fp_mulmod(x[k], ninv, q, qinv) : x[k];
         gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr, fp_canon(v, q, qinv));
       } else {
@@ -527,7 +541,7 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
   }
 }
 
-template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf>
+template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf, int RAWM = 0>
 __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, double* sm, const double* tw,
                                              double q, double qinv, uint32_t tile0, double ninv,
                                              const double* tws = nullptr, const PF& pf = PF{}) {
@@ -537,9 +551,9 @@ __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, doub
     constexpr int RB = pick_rb(rem);
     if constexpr (DONE > 0) __syncthreads();
     if constexpr (DONE > 0 && DONE == pick_rb(logR)) pf();
-    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, tw, q, qinv, tile0,
-                                                                                 ninv, tws);
-    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST, PF>(gin, gout, sm, tw, q, qinv, tile0, ninv, tws, pf);
+    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST, RAWM>(gin, gout, sm, tw, q, qinv,
+                                                                                       tile0, ninv, tws);
+    ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST, PF, RAWM>(gin, gout, sm, tw, q, qinv, tile0, ninv, tws, pf);
   } else if constexpr (DONE == pick_rb(logR) && !std::is_same_v<PF, NoPf>) {
     __syncthreads();
     pf();
@@ -636,9 +650,10 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
     }
   }
   auto run = [&](const auto& ld, const auto& st) {
-    if (P.fp)
-      ntt_steps_fp<INV, ROWS, LOGN, 0>(ld, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
-                                       static_cast<double>(P.ninv), tws, pf);
+    if (P.fp)  // first pass (forward columns / inverse rows) leaves raw fp64 words for the second
+      ntt_steps_fp<INV, ROWS, LOGN, 0, std::decay_t<decltype(ld)>, std::decay_t<decltype(st)>, PF,
+                   (ROWS == INV) ? kRawOut : kRawIn>(ld, st, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
+                                                    static_cast<double>(P.ninv), tws, pf);
     else
       ntt_steps<INV, ROWS, LOGN, 0>(ld, st, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh, pf);
   };
@@ -891,8 +906,8 @@ __global__ void __launch_bounds__(kNT, 4) k_ntt_rows_inner(const __grid_constant
       const PlainLoad ld{A.ext + b * A.ext_stride + (size_t(j * A.nx + x) << LOGN) + toff};
       __syncthreads();  // the previous digit is done with sm
       if (P.fp)
-        ntt_steps_fp<false, true, LOGN, 0>(ld, SmStore{sm}, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0,
-                                           static_cast<double>(P.ninv));
+        ntt_steps_fp<false, true, LOGN, 0, PlainLoad, SmStore, NoPf, kRawIn>(  // ext rows after their column pass
+            ld, SmStore{sm}, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0, static_cast<double>(P.ninv));
       else
         ntt_steps<false, true, LOGN, 0>(ld, SmStore{sm}, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
       __syncthreads();
