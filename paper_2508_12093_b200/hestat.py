@@ -135,7 +135,9 @@ class Ciphertext:  # ckks.hpp:64-78
 
     @classmethod
     def _own(cls, h: C.c_void_p) -> "Ciphertext":
-        return cls(_handle=h)
+        o = object.__new__(cls)
+        o._h = h
+        return o
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -446,15 +448,36 @@ class EncryptedColumn:  # column.hpp:19-23
     name: str = ""
 
     def _c(self):
-        # the ctypes view is cached while the chunk list and n_valid are unchanged (e2e path)
+        # the ctypes view is cached while the chunk list and n_valid are unchanged (columns made
+        # by encode_column / znorm are born with it: the handle array the C call filled)
         key = (tuple(map(id, self.chunks)), int(self.n_valid))
         cache = self.__dict__.get("_cview")
         if cache is not None and cache[0] == key:
             return cache[1], cache[2]
-        arr = (C.c_void_p * max(len(self.chunks), 1))(*[c._h.value for c in self.chunks])
-        col = hs_column(C.cast(arr, C.POINTER(C.c_void_p)), len(self.chunks), int(self.n_valid))
+        arr = _ptr_array(len(self.chunks))(*[c._h.value for c in self.chunks])
+        col = hs_column(arr, len(self.chunks), int(self.n_valid))
         self.__dict__["_cview"] = (key, col, arr)
         return col, arr
+
+    @classmethod
+    def _from_handles(cls, arr, n: int, n_valid: int, name: str) -> "EncryptedColumn":
+        """Wrap n handles a C call wrote into arr (owned from here on), view cached."""
+        own = Ciphertext._own
+        chunks = [own(C.c_void_p(arr[i])) for i in range(n)]
+        col = cls(chunks, n_valid, name)
+        col.__dict__["_cview"] = ((tuple(map(id, chunks)), int(n_valid)), hs_column(arr, n, int(n_valid)), arr)
+        return col
+
+
+_PTR_ARRAYS = {}
+
+
+def _ptr_array(n: int):
+    """ctypes array type c_void_p * max(n, 1), cached."""
+    t = _PTR_ARRAYS.get(n)
+    if t is None:
+        t = _PTR_ARRAYS[n] = C.c_void_p * max(n, 1)
+    return t
 
 
 def encode_column(ctx: EvalContext, values, name: str = "") -> EncryptedColumn:  # column.hpp:25-39
@@ -462,11 +485,10 @@ def encode_column(ctx: EvalContext, values, name: str = "") -> EncryptedColumn: 
                    and values.flags.c_contiguous) else _arr(values)
     S = ctx._p.slot_count
     nch = (len(v) + S - 1) // S
-    arr = (C.c_void_p * max(nch, 1))()
+    arr = _ptr_array(nch)()
     got = C.c_uint64(0)
     _check(_abi.lib().hs_encode_column(ctx._h, _dp(v), len(v), arr, C.byref(got)))
-    chunks = [Ciphertext._own(C.c_void_p(arr[i])) for i in range(got.value)]
-    return EncryptedColumn(chunks, len(v), name)
+    return EncryptedColumn._from_handles(arr, got.value, len(v), name)
 
 
 def decode_column(ctx: EvalContext, col: EncryptedColumn, out: Optional[np.ndarray] = None) -> np.ndarray:
@@ -520,11 +542,11 @@ def moments(ctx: EvalContext, col: EncryptedColumn, B: float) -> MomentSet:  # :
 def znorm(ctx: EvalContext, col: EncryptedColumn, B: float,
           cfg: Optional[InvRootConfig] = None) -> EncryptedColumn:  # :153-166
     c, keep = col._c()
-    arr = (C.c_void_p * max(len(col.chunks), 1))()
+    n = len(col.chunks)
+    arr = _ptr_array(n)()
     _check(_abi.lib().hs_znorm(ctx._h, C.byref(c), float(B), _cfg(cfg), arr))
     del keep
-    return EncryptedColumn([Ciphertext._own(C.c_void_p(arr[i])) for i in range(len(col.chunks))],
-                           col.n_valid, col.name)
+    return EncryptedColumn._from_handles(arr, n, col.n_valid, col.name)
 
 
 def kurtosis(ctx: EvalContext, col: EncryptedColumn, B: float,

@@ -28,10 +28,12 @@ def main():
     ap.add_argument("--logq", type=int, default=60)
     ap.add_argument("--extraK", type=int, default=1)
     ap.add_argument("--h", type=int, default=192)
+    ap.add_argument("--logp", type=int, default=61)
+    ap.add_argument("--K", type=int, default=0, help="special primes (default: alpha + extraK)")
     a = ap.parse_args()
     S = 1 << (a.logN - 1)
-    K = (a.L + 3) // 3 + a.extraK
-    ctx = R.RnsContext(R.RnsSpec(logN=a.logN, L=a.L, K=K, dnum=3, logq0=61, logq=a.logq, logp=61, seed=3, h=a.h))
+    K = a.K or (a.L + 3) // 3 + a.extraK
+    ctx = R.RnsContext(R.RnsSpec(logN=a.logN, L=a.L, K=K, dnum=3, logq0=61, logq=a.logq, logp=a.logp, seed=3, h=a.h))
     ev = R.RnsEval(ctx, H.CkksParams(slot_count=S))
     rng = np.random.default_rng(11)
     x2 = 50 + 10 * rng.standard_normal(S)                 # C2
