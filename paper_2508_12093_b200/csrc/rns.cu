@@ -117,15 +117,16 @@ struct RsLoad {  // rescale: [k_l c_l]_{q_i} read straight from the coefficient-
   }
 };
 
-struct RsStore {  // rescale: out = (k_i c_i - NTT([k_l c_l]_{q_i})) * q_l^-1
+struct RsStore {  // rescale: out = (k_i c_i - NTT([k_l c_l]_{q_i})) * q_l^-1 (+ a_i: a fused add_pt)
   const uint64_t* in;
   uint64_t* out;
   uint64_t q, qinv, qinv_sh;
   bool kon;
   uint64_t k, k_sh;
+  uint64_t addc = 0;
   __device__ void operator()(size_t off, uint64_t v) const {
     const uint64_t c = kon ? mul_shoup(in[off], k, k_sh, q) : in[off];
-    out[off] = mul_shoup(sub_mod(c, v, q), qinv, qinv_sh, q);
+    out[off] = add_mod(mul_shoup(sub_mod(c, v, q), qinv, qinv_sh, q), addc, q);
   }
 };
 
@@ -142,6 +143,8 @@ struct RsEpi {  // the rescale's spread and combine fused into its NTT passes
   uint64_t k[kRsMaxLimbs], k_sh[kRsMaxLimbs];
   // per batch item constants instead (device, [batch][2][level + 1]: residues then Shoup)
   const uint64_t* kitems = nullptr;
+  // per batch item constant added to polynomial 0 of the output (device, [batch][level]), or null
+  const uint64_t* aitems = nullptr;
   __device__ uint64_t kk(uint32_t bz, uint32_t i) const {
     return kitems ? kitems[size_t(bz) * 2 * (level + 1) + i] : k[i];
   }
@@ -702,7 +705,8 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
     const uint32_t r = rm.orow[by], p = r / e.level, i = r - p * e.level;
     const RsStore st{e.in + bz * e.in_stride + (size_t(p * (e.level + 1) + i) << LOGN) + toff,
                      e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
-                     e.qinv_sh[i], e.kon, e.kk(bz, i), e.kk_sh(bz, i)};
+                     e.qinv_sh[i], e.kon, e.kk(bz, i), e.kk_sh(bz, i),
+                     (e.aitems && p == 0) ? e.aitems[size_t(bz) * e.level + i] : 0};
     run(mk_ld<PlainLd>(gi, stage), st);
   } else {
     run(mk_ld<PlainLd>(gi, stage), PlainStore{go});
@@ -2781,14 +2785,15 @@ void rescale(Ctx& c, uint32_t level, const uint64_t* in, uint64_t* out, uint32_t
 
 void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<uint64_t>* kres, uint64_t* out,
                  uint32_t batch) {
-  rescale_mul_items(c, level, in, false, kres, nullptr, out, batch);
+  rescale_mul_items(c, level, in, false, kres, nullptr, out, batch, nullptr);
 }
 
 // rescale(k_b * in_b) for every batch item b: kres = one constant for all items (or null = 1),
 // kitems = per-item residues [batch][level + 1] (RnsB's batched BSGS leaves); shared_in: every
 // item reads the same input ciphertext (its last limb goes to coefficient form once).
 void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_in, const std::vector<uint64_t>* kres,
-                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch) {
+                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch,
+                       const std::vector<uint64_t>* aitems) {
   if (level < 1 || level > c.spec.L) fail(HS_E_INVALID_ARG, "rns rescale: level must be in [1, L]");
   if (kres && (kres->size() < level + 1 || level + 1 > uint32_t(kRsMaxLimbs)))
     fail(HS_E_INVALID_ARG, "rns rescale_mul: constant residues");
@@ -2804,14 +2809,21 @@ void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_i
   uint64_t* LAST = dptr<uint64_t>(last);
   uint64_t* T = dptr<uint64_t>(t);
   DevBuf kdev;
-  if (kitems) {  // [batch][2][nl]: residues then Shoup companions
-    std::vector<uint64_t> tab(size_t(batch) * 2 * nl);
-    for (uint32_t b = 0; b < batch; ++b)
-      for (uint32_t i = 0; i < nl; ++i) {
-        const uint64_t v = (*kitems)[size_t(b) * nl + i] % c.primes[i];
-        tab[size_t(b) * 2 * nl + i] = v;
-        tab[size_t(b) * 2 * nl + nl + i] = shoup_of(v, c.primes[i]);
-      }
+  if (aitems && aitems->size() < size_t(batch) * level) fail(HS_E_INVALID_ARG, "rns rescale_mul: item addends");
+  if (kitems || aitems) {  // [batch][2][nl]: residues then Shoup companions; then [batch][level] addends
+    const size_t ka = kitems ? size_t(batch) * 2 * nl : 0;
+    std::vector<uint64_t> tab(ka + (aitems ? size_t(batch) * level : 0));
+    if (kitems)
+      for (uint32_t b = 0; b < batch; ++b)
+        for (uint32_t i = 0; i < nl; ++i) {
+          const uint64_t v = (*kitems)[size_t(b) * nl + i] % c.primes[i];
+          tab[size_t(b) * 2 * nl + i] = v;
+          tab[size_t(b) * 2 * nl + nl + i] = shoup_of(v, c.primes[i]);
+        }
+    if (aitems)
+      for (uint32_t b = 0; b < batch; ++b)
+        for (uint32_t i = 0; i < level; ++i)
+          tab[ka + size_t(b) * level + i] = (*aitems)[size_t(b) * level + i] % c.primes[i];
     kdev = rt.alloc(tab.size());
     cuda_ok(cudaMemcpyAsync(kdev.get(), tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, rt.stream()),
             "rescale constants");
@@ -2827,6 +2839,7 @@ void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_i
   }
   RsEpi rse{LAST, in, out, dptr<const uint64_t>(P.qinv), dptr<const uint64_t>(P.qinv_sh),
             shared_in ? 0 : size_t(2) * N, in_stride, out_stride, level};
+  if (aitems) rse.aitems = dptr<const uint64_t>(kdev) + (kitems ? size_t(batch) * 2 * nl : 0);
   if (kitems) {
     rse.kon = true;
     rse.kitems = dptr<const uint64_t>(kdev);

@@ -167,9 +167,11 @@ void rescale_mul(Ctx& c, uint32_t level, const uint64_t* in, const std::vector<u
                  uint32_t batch);
 // the same for k = nearbyint(kd), |kd| < 2^127
 void rescale_mul_big(Ctx& c, uint32_t level, const uint64_t* a, double kd, uint64_t* out, uint32_t batch);
-// per-item constants kitems [batch][level + 1] (or one constant kres); shared_in: all items read `in`
+// per-item constants kitems [batch][level + 1] (or one constant kres); shared_in: all items read `in`;
+// aitems [batch][level]: a per-item constant added to polynomial 0 of the result (a fused add_pt)
 void rescale_mul_items(Ctx& c, uint32_t level, const uint64_t* in, bool shared_in, const std::vector<uint64_t>* kres,
-                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch);
+                       const std::vector<uint64_t>* kitems, uint64_t* out, uint32_t batch,
+                       const std::vector<uint64_t>* aitems = nullptr);
 // out_b = a_b + k_b (k_b residues [batch][level + 1], added to poly 0)
 void add_const_items(const Ctx& c, uint32_t level, const uint64_t* a, const std::vector<uint64_t>& kitems,
                      uint64_t* out, uint32_t batch);

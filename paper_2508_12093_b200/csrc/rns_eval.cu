@@ -295,9 +295,8 @@ RCt RnsB::bsgs_full_tree(const RCt& x, const std::vector<double>& coeffs, const 
       residues_of(c_, p0 - 1, c0[i] * sigma_[p0 - 1], &ka[size_t(i) * p0]);
     }
     uint64_t* o = reinterpret_cast<uint64_t*>(R.buf.get());
-    rescale_mul_items(c_, p0, x->ptr(), true, nullptr, &km, o, n0);
+    rescale_mul_items(c_, p0, x->ptr(), true, nullptr, &km, o, n0, &ka);  // add_pt fused into the store
     m_.mul_pt += n0;
-    add_const_items(c_, p0 - 1, o, ka, o, n0);
     m_.add += n0;
   }
   // height h: head = mul_ct(q-child, T_{2^h}); node = add_ct(head, r-child)
