@@ -447,6 +447,23 @@ __device__ __forceinline__ void stage_row_tw(double* tws, const double* tw, uint
 // fp64 bits (unreduced forward / folded inverse values) for the second pass; 2 (second pass)
 // the input is those raw fp64 bits.  Saves the canonicalisation and the integer-to-double
 // conversion between the passes (the intermediate is read by nothing else).
+// n consecutive twiddles (n a power of two <= 8, constant after unrolling; the start is
+// n-aligned): 16-byte loads for n >= 2
+__device__ __forceinline__ void ldg_tw(double (&w)[8], const double* p, int n) {
+  if (n == 1) {
+    w[0] = __ldg(p);
+  } else {
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (2 * i >= n) break;
+      const double2 v = __ldg(p2 + i);
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
+  }
+}
+
 template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST, int RAWM = 0>
 __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
@@ -487,10 +504,12 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
 #pragma unroll
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << (RB - 1 - st);
+        double wv[8];  // the stage's 2^st twiddles are consecutive: 16-byte loads
+        if (!(ROWS && tws)) ldg_tw(wv, tw + ((1u << (DONE + st)) * S) + (blk0 << st), 1 << st);
 #pragma unroll
         for (int b = 0; b < (1 << st); ++b) {
           const double w = ROWS && tws ? tws[RowTw<LOGN>::off(DONE + st) + (tr << (DONE + st)) + (blk0 << st) + b]
-                                       : __ldg(tw + ((1u << (DONE + st)) * S) + (blk0 << st) + b);
+                                       : wv[b];
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
@@ -506,11 +525,13 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
 #pragma unroll
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << st;
+        double wv[8];
+        if (!(ROWS && tws)) ldg_tw(wv, tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)), 1 << (RB - 1 - st));
 #pragma unroll
         for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
           const double w = ROWS && tws
                                ? tws[RowTw<LOGN>::off(logh0 - st) + (tr << (logh0 - st)) + (blk0 << (RB - 1 - st)) + b]
-                               : __ldg(tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b);
+                               : wv[b];
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
