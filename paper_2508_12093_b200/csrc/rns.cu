@@ -1494,9 +1494,14 @@ __device__ __forceinline__ void imma_u8(int (&c)[4], const uint32_t (&a)[4], uin
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
 }
 
+#ifndef HS_CONV_TPR
+#define HS_CONV_TPR 2
+#endif
+constexpr int kConvTpr = HS_CONV_TPR;  // targets per round of k_conv_mma (IMMA/epilogue chains interleaved)
+
 template <int KS>
 constexpr size_t conv_mma_smem() {
-  return size_t(kConvMmaRows) * (KS * 8 + 4) * 4 + 4 * 2 * 256 * 4;
+  return size_t(kConvMmaRows) * (KS * 8 + 4) * 4 + 4 * kConvTpr * 256 * 4;
 }
 
 struct ConvTgt {
@@ -1557,7 +1562,7 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
       a[m][ks][3] = r1[4];
     }
   uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + lane;
-  int* const S0 = stg + warp * 512;
+  int* const S0 = stg + warp * (256 * kConvTpr);
   int2* const W0 = reinterpret_cast<int2*>(S0 + g * 8 + 2 * t4);  // this lane's C slots (rows g, g+8, 16+g, 24+g)
   const uint4* const R0 = reinterpret_cast<const uint4*>(S0 + lane * 8);  // this lane's coefficient row
   const uint2* F = frags + J.frag_off + lane;
@@ -1594,18 +1599,20 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
   };
   uint32_t t = 0;
 #pragma unroll 1
-  for (; t + 1 < ntgt; t += 2) {  // two targets per round: their IMMA and epilogue chains interleave
-    mma_park(t, 0);
-    mma_park(t + 1, 1);
+  for (; t + kConvTpr <= ntgt; t += kConvTpr) {  // kConvTpr targets per round: IMMA and epilogue chains interleave
+#pragma unroll
+    for (int u = 0; u < kConvTpr; ++u) mma_park(t + u, u);
     __syncwarp();
-    finish(t, 0);
-    finish(t + 1, 1);
+#pragma unroll
+    for (int u = 0; u < kConvTpr; ++u) finish(t + u, u);
     __syncwarp();
   }
-  if (t < ntgt) {
+#pragma unroll 1
+  for (; t < ntgt; ++t) {
     mma_park(t, 0);
     __syncwarp();
     finish(t, 0);
+    __syncwarp();
   }
 }
 
