@@ -306,7 +306,7 @@ def rns_znorm(torch, stream, reps=3):
     from paper_2508_12093_b200 import hestat as H
     from paper_2508_12093_b200 import rns as R
     from paper_2508_12093_b200 import workloads as W
-    L = 28
+    L = 25  # the Z-score DAG's no-bootstrap depth (24) + 1: decryption goes through q_0 q_1
     spec = R.RnsSpec(logN=16, L=L, K=(L + 3) // 3 + 1, dnum=3, logq0=61, logq=60, logp=61, seed=5, h=192)
     ctx = R.RnsContext(spec)
     ev = R.RnsEval(ctx, H.CkksParams(slot_count=S))
