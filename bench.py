@@ -327,6 +327,21 @@ def rns_znorm(torch, stream, reps=3):
                       "timing": "wall, keys warm, encrypt + znorm DAG + decrypt, best of %d" % reps},
            "rel_err_vs_reference": float(np.max(np.abs(z - ref.out)) / np.max(np.abs(ref.out))),
            "meter_equal": (m.mul_ct, m.mul_pt, m.add, m.rotate, m.bootstrap) == ref.meter}
+    # the paper's Z-score size: 1M samples on [0, 100] = 31 chunks, same chain
+    x1m = np.random.default_rng(SEED).uniform(0.0, 100.0, 1_000_000)
+    walls = []
+    for _ in range(2):
+        ev.reset_meter()
+        t0 = time.perf_counter()
+        z1, _ = ev.stat(R.ZNORM, x1m, B)
+        walls.append(time.perf_counter() - t0)
+    r1 = oracle().stat(Params(slot_count=S), ST_ZNORM, x1m, B)
+    m1 = ev.meter()
+    out["znorm_1m"] = {"value": round(1e3 * min(walls), 1), "unit": "ms per 1M-sample column (31 ciphertexts)",
+                       "rel_err_vs_reference": float(np.max(np.abs(z1 - r1.out)) / np.max(np.abs(r1.out))),
+                       "meter_equal": (m1.mul_ct, m1.mul_pt, m1.add, m1.rotate, m1.bootstrap) == r1.meter,
+                       "note": "the paper's Lattigo CPU Z-score of 1M samples is 141.29 s with 2 real bootstraps "
+                               "(PAPER.md:498); here bootstrap is the reference's logical level reset"}
     ev.close()
     ctx.close()
     return out

@@ -1031,11 +1031,18 @@ int hs_rns_eval_stat(hs_rns_eval* e, int which, const double* x, uint64_t n, con
     // znorm: the n values across chunks; others: the first out_n slots of each result
     size_t w = 0;
     if (which == HS_RNS_ZNORM) {
-      for (size_t i = 0; i < res.size() && w < out_n; ++i) {
-        const size_t take = std::min<size_t>(e->p.S, out_n - w);
-        const std::vector<double> v = b.decrypt(res[i], take);
+      std::vector<rns::RCt> cts;
+      std::vector<size_t> ns;
+      for (size_t i = 0, left = out_n; i < res.size() && left > 0; ++i) {
+        const size_t take = std::min<size_t>(e->p.S, left);
+        cts.push_back(res[i]);
+        ns.push_back(take);
+        left -= take;
+      }
+      const auto vs = b.decrypt_many(cts, ns);
+      for (const auto& v : vs) {
         std::copy(v.begin(), v.end(), out + w);
-        w += take;
+        w += v.size();
       }
     } else {
       for (const auto& r : res) {

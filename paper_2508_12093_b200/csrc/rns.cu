@@ -1201,6 +1201,22 @@ __global__ void k_dec(const uint64_t* ct, const uint64_t* sk, uint64_t* out, con
   }
 }
 
+// CRT of the two lowest limbs of a decryption: v = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, q0 q1),
+// as (lo, hi) words; the host centres and converts (the modular work stays off the host)
+__global__ void k_crt2(const uint64_t* m, uint64_t* v, const PrimeC* pcs, uint64_t q0inv, uint64_t q0inv_sh,
+                       uint32_t logN) {
+  const uint32_t N = 1u << logN;
+  const uint64_t q0 = pcs[0].q, q1 = pcs[1].q;
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const uint64_t a0 = m[n], a1 = m[N + n];
+    const uint64_t d = sub_mod(a1, a0 % q1, q1);
+    const uint64_t t = mul_shoup(d, q0inv, q0inv_sh, q1);
+    const u128 r = static_cast<u128>(q0) * t + a0;
+    v[2 * size_t(n)] = static_cast<uint64_t>(r);
+    v[2 * size_t(n) + 1] = static_cast<uint64_t>(r >> 64);
+  }
+}
+
 __global__ void k_enc_as(uint64_t* ct, const uint64_t* sk, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
   const size_t half = size_t(nl) << logN;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < half; x += size_t(gridDim.x) * blockDim.x) {
@@ -2239,24 +2255,29 @@ void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeff
   k_dec<<<grid_of(size_t(use) * c.N), kT, 0, rt.stream()>>>(ct, dptr<const uint64_t>(c.d_sk), dptr<uint64_t>(m),
                                                              c.dpc(), nl, use, c.spec.logN);
   ntt(c, dptr<uint64_t>(m), iota_rows(use), 1, 0, true);
-  std::vector<uint64_t> h(size_t(use) * c.N);
-  cuda_ok(cudaMemcpyAsync(h.data(), m.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
-  rt.sync();
-  rt.note_launch();
   const uint64_t q0 = c.primes[0];
   if (use == 1) {
+    std::vector<uint64_t> h(c.N);
+    cuda_ok(cudaMemcpyAsync(h.data(), m.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
+    rt.sync();
+    rt.note_launch();
     for (uint32_t n = 0; n < c.N; ++n)
       coeffs[n] = h[n] > q0 / 2 ? -static_cast<double>(q0 - h[n]) : static_cast<double>(h[n]);
     return;
   }
   const uint64_t q1 = c.primes[1];
   const uint64_t q0inv = h_inv(q0 % q1, q1);
+  DevBuf v = rt.alloc(size_t(2) * c.N);
+  k_crt2<<<grid_of(c.N), kT, 0, rt.stream()>>>(dptr<const uint64_t>(m), dptr<uint64_t>(v), c.dpc(), q0inv,
+                                                shoup_of(q0inv, q1), c.spec.logN);
+  std::vector<uint64_t> h(size_t(2) * c.N);
+  cuda_ok(cudaMemcpyAsync(h.data(), v.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
+  rt.sync();
+  rt.note_launch(2);
   const unsigned __int128 Q = static_cast<unsigned __int128>(q0) * q1;
-  for (uint32_t n = 0; n < c.N; ++n) {
-    const uint64_t a0 = h[n], a1 = h[c.N + n];
-    const uint64_t t = h_mulmod((a1 + q1 - a0 % q1) % q1, q0inv, q1);
-    const unsigned __int128 v = a0 + static_cast<unsigned __int128>(q0) * t;  // CRT value in [0, q0 q1)
-    coeffs[n] = v > Q / 2 ? -static_cast<double>(Q - v) : static_cast<double>(v);
+  for (uint32_t n = 0; n < c.N; ++n) {  // CRT value in [0, q0 q1), centred
+    const unsigned __int128 r = (static_cast<unsigned __int128>(h[2 * size_t(n) + 1]) << 64) | h[2 * size_t(n)];
+    coeffs[n] = r > Q / 2 ? -static_cast<double>(Q - r) : static_cast<double>(r);
   }
 }
 

@@ -63,20 +63,30 @@ const FftPlan& plan(uint32_t logN) {
   return plans.emplace(logN, std::move(p)).first->second;
 }
 
-// in-place radix-2 FFT, X_t = sum_k x_k exp(sign * 2 pi i k t / n)
+// in-place radix-2 FFT, X_t = sum_k x_k exp(sign * 2 pi i k t / n).  The complex product is
+// written out (re = ar wr - ai wi, im = ar wi + ai wr): the same roundings as std::complex's
+// operator* on finite values (no contraction: -ffp-contract=off), without its out-of-line
+// NaN/Inf recovery call, which made this loop ~5x slower.
 void fft(std::vector<cd>& a, const FftPlan& p, int sign) {
   const uint32_t n = p.n;
   for (uint32_t k = 0; k < n; ++k)
     if (k < p.rev[k]) std::swap(a[k], a[p.rev[k]]);
+  double* x = reinterpret_cast<double*>(a.data());  // interleaved re, im (std::complex layout)
+  const double* w = reinterpret_cast<const double*>(p.w.data());
+  const double sg = sign < 0 ? -1.0 : 1.0;
   for (uint32_t len = 2; len <= n; len <<= 1) {
     const uint32_t half = len / 2, step = n / len;
     for (uint32_t i = 0; i < n; i += len)
       for (uint32_t k = 0; k < half; ++k) {
-        cd w = p.w[k * step];
-        if (sign < 0) w = std::conj(w);
-        const cd u = a[i + k], v = a[i + k + half] * w;
-        a[i + k] = u + v;
-        a[i + k + half] = u - v;
+        const double wr = w[2 * size_t(k) * step], wi = sg * w[2 * size_t(k) * step + 1];
+        double* u = x + 2 * size_t(i + k);
+        double* v = x + 2 * size_t(i + k + half);
+        const double vr = v[0] * wr - v[1] * wi, vi = v[0] * wi + v[1] * wr;
+        const double ur = u[0], ui = u[1];
+        u[0] = ur + vr;
+        u[1] = ui + vi;
+        v[0] = ur - vr;
+        v[1] = ui - vi;
       }
   }
 }

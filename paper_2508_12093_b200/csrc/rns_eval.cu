@@ -5,6 +5,11 @@
 #include "rns_eval.h"
 
 #include <cmath>
+#include <algorithm>
+#include <thread>
+#include <mutex>
+#include <exception>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -43,11 +48,57 @@ RCt RnsB::encrypt(const double* v, size_t n) {  // ckks.hpp:97-104
   return make(b, L, p_.max_level);
 }
 
+// Run f(i) for i < n on up to `hw` host threads (the chunks' host FFTs are independent).
+template <class F>
+static void parallel_chunks(size_t n, F&& f) {
+  const size_t hw = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), 16));
+  if (n <= 1 || hw == 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> ts;
+  std::exception_ptr err;
+  std::mutex em;
+  for (size_t t = 0; t < std::min(hw, n); ++t)
+    ts.emplace_back([&] {
+      for (size_t i; (i = next.fetch_add(1)) < n;) {
+        try {
+          f(i);
+        } catch (...) {
+          std::lock_guard<std::mutex> g(em);
+          if (!err) err = std::current_exception();
+        }
+      }
+    });
+  for (auto& t : ts) t.join();
+  if (err) std::rethrow_exception(err);
+}
+
 std::vector<RCt> RnsB::encrypt_column(const double* v, size_t n) {  // column.hpp:25-39
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(v[i])) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
+  // the chunks' canonical-embedding encodings on host threads, then the encryptions in order
+  // (the per-chunk randomness tags follow the chunk order, as in encrypt())
+  const size_t nch = (n + p_.S - 1) / p_.S;
+  const int L = static_cast<int>(c_.spec.L);
+  std::vector<std::vector<double>> co(nch, std::vector<double>(c_.N));
+  parallel_chunks(nch, [&](size_t k) {
+    const size_t off = k * p_.S;
+    encode_real(c_.spec.logN, v + off, std::min(p_.S, n - off), sigma_[L], co[k].data());
+  });
   std::vector<RCt> out;
-  for (size_t off = 0; off < n; off += p_.S) out.push_back(encrypt(v + off, std::min(p_.S, n - off)));
+  for (size_t k = 0; k < nch; ++k) {
+    DevBuf b = Runtime::get().alloc(words(L));
+    encrypt_real(c_, L, co[k].data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
+    out.push_back(make(b, L, p_.max_level));
+  }
+  return out;
+}
+
+std::vector<std::vector<double>> RnsB::decrypt_many(const std::vector<RCt>& cts, const std::vector<size_t>& ns) {
+  std::vector<std::vector<double>> out(cts.size());
+  parallel_chunks(cts.size(), [&](size_t k) { out[k] = decrypt(cts[k], ns[k]); });
   return out;
 }
 

@@ -65,6 +65,8 @@ class RnsB : public LedgerBase<RnsB, RCt> {
   void check_sign_domain(const C& c);
 
   std::vector<double> decrypt(const C& c, size_t n);
+  // several results at once: the host side (CRT words -> coefficients -> FFT) on host threads
+  std::vector<std::vector<double>> decrypt_many(const std::vector<C>& cts, const std::vector<size_t>& ns);
   double scale(int phys) const { return sigma_[static_cast<size_t>(phys)]; }
 
   // Batched BSGS (flow.h Bsgs::run): a full tree (2^K coefficients) evaluated level by level,
