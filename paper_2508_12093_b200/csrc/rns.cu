@@ -252,6 +252,37 @@ struct NttGeom {
   static constexpr uint32_t R1 = 1u << logR1;
 };
 
+// n consecutive twiddles (n a power of two <= 8, constant after unrolling; the start is
+// n-aligned): 16-byte loads for n >= 2
+__device__ __forceinline__ void ldg_tw(uint64_t (&w)[8], const uint64_t* p, int n) {
+  if (n == 1) {
+    w[0] = __ldg(p);
+  } else {
+    const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (2 * i >= n) break;
+      const ulonglong2 v = __ldg(p2 + i);
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
+  }
+}
+__device__ __forceinline__ void ldg_tw(double (&w)[8], const double* p, int n) {
+  if (n == 1) {
+    w[0] = __ldg(p);
+  } else {
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (2 * i >= n) break;
+      const double2 v = __ldg(p2 + i);
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
+  }
+}
+
 // One radix-2^RB step (stages DONE .. DONE+RB-1 of this pass) for every group of the tile.
 template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST>
 __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
@@ -292,10 +323,13 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
 #pragma unroll
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << (RB - 1 - st);
+        uint64_t wv[8], wpv[8];  // the stage's 2^st consecutive twiddles: 16-byte loads
+        const uint32_t wi0 = ((1u << (DONE + st)) * S) + (blk0 << st);
+        ldg_tw(wv, psi + wi0, 1 << st);
+        ldg_tw(wpv, psip + wi0, 1 << st);
 #pragma unroll
         for (int b = 0; b < (1 << st); ++b) {
-          const uint32_t wi = ((1u << (DONE + st)) * S) + (blk0 << st) + b;
-          const uint64_t w = __ldg(psi + wi), wp = __ldg(psip + wi);
+          const uint64_t w = wv[b], wp = wpv[b];
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
@@ -312,10 +346,13 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << st;
         constexpr uint32_t logh0 = logR - 1 - DONE;
+        uint64_t wv[8], wpv[8];
+        const uint32_t wi0 = ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st));
+        ldg_tw(wv, psi + wi0, 1 << (RB - 1 - st));
+        ldg_tw(wpv, psip + wi0, 1 << (RB - 1 - st));
 #pragma unroll
         for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
-          const uint32_t wi = ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)) + b;
-          const uint64_t w = __ldg(psi + wi), wp = __ldg(psip + wi);
+          const uint64_t w = wv[b], wp = wpv[b];
 #pragma unroll
           for (int o = 0; o < d; ++o) {
             const int k0 = b * 2 * d + o;
@@ -447,23 +484,6 @@ __device__ __forceinline__ void stage_row_tw(double* tws, const double* tw, uint
 // fp64 bits (unreduced forward / folded inverse values) for the second pass; 2 (second pass)
 // the input is those raw fp64 bits.  Saves the canonicalisation and the integer-to-double
 // conversion between the passes (the intermediate is read by nothing else).
-// n consecutive twiddles (n a power of two <= 8, constant after unrolling; the start is
-// n-aligned): 16-byte loads for n >= 2
-__device__ __forceinline__ void ldg_tw(double (&w)[8], const double* p, int n) {
-  if (n == 1) {
-    w[0] = __ldg(p);
-  } else {
-    const double2* p2 = reinterpret_cast<const double2*>(p);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (2 * i >= n) break;
-      const double2 v = __ldg(p2 + i);
-      w[2 * i] = v.x;
-      w[2 * i + 1] = v.y;
-    }
-  }
-}
-
 template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST, class LD, class ST, int RAWM = 0>
 __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
