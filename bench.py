@@ -307,7 +307,9 @@ def rns_znorm(torch, stream, reps=3):
     from paper_2508_12093_b200 import rns as R
     from paper_2508_12093_b200 import workloads as W
     L = 25  # the Z-score DAG's no-bootstrap depth (24) + 1: decryption goes through q_0 q_1
-    spec = R.RnsSpec(logN=16, L=L, K=(L + 3) // 3 + 1, dnum=3, logq0=61, logq=60, logp=61, seed=5, h=192)
+    # dnum = 2 (13 limbs per digit, K = 14 so P exceeds a digit's modulus): 117 ms against 122 (dnum 3),
+    # 130 (4), 159 (1) at the same accuracy (tools/rns_znorm_dnum.py)
+    spec = R.RnsSpec(logN=16, L=L, K=14, dnum=2, logq0=61, logq=60, logp=61, seed=5, h=192)
     ctx = R.RnsContext(spec)
     ev = R.RnsEval(ctx, H.CkksParams(slot_count=S))
     x = W.normal(H.synthetic_uniform, SEED, S, 50.0, 10.0)
@@ -322,7 +324,7 @@ def rns_znorm(torch, stream, reps=3):
     m = ev.meter()
     out = {"metric": "encrypted Z-score ms per 2^15-slot ciphertext (RNS-CKKS)", "value": round(1e3 * min(walls), 2),
            "unit": "ms/ciphertext",
-           "config": {"logN": 16, "L": L, "K": spec.K, "dnum": 3, "logq0": 61, "logq": 60, "logp": 61,
+           "config": {"logN": 16, "L": L, "K": spec.K, "dnum": spec.dnum, "logq0": 61, "logq": 60, "logp": 61,
                       "secret_hamming_weight": 192, "bootstrap": "logical level reset over the deep chain",
                       "timing": "wall, keys warm, encrypt + znorm DAG + decrypt, best of %d" % reps},
            "rel_err_vs_reference": float(np.max(np.abs(z - ref.out)) / np.max(np.abs(ref.out))),
