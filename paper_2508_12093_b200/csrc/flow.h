@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cmath>
+#include <concepts>
 #include <cstddef>
 #include <limits>
 #include <memory>
@@ -233,9 +234,36 @@ inline size_t chunk_valid(size_t S, size_t n_valid, size_t i) {  // :32-37
   return off >= n_valid ? 0 : std::min(S, n_valid - off);
 }
 
+// Backends with batched chunk ops (RnsB): one batched mul_pt / square over a column's chunks
+// when they allow it (same level, nothing to bootstrap); the same ops on the same operands as
+// the per-chunk loops, so values, meter and levels are unchanged.
+template <class B>
+concept BatchedChunks = requires(B& b, const std::vector<typename B::C>& v, double c) {
+  { b.mul_pt_many(v, c) } -> std::same_as<std::vector<typename B::C>>;
+  { b.square_many(v) } -> std::same_as<std::vector<typename B::C>>;
+};
+
+template <class B>
+std::vector<typename B::C> mul_pt_chunks(B& b, const std::vector<typename B::C>& xs, double c) {
+  if constexpr (BatchedChunks<B>) {
+    if (xs.size() > 1 && b.batch_ok(xs)) return b.mul_pt_many(xs, c);
+  }
+  std::vector<typename B::C> out;
+  out.reserve(xs.size());
+  for (const auto& x : xs) out.push_back(b.mul_pt(x, c));
+  return out;
+}
+
 template <class B>
 typename B::C scaled_slot_sum(B& b, const Col<typename B::C>& col, double c) {  // :41-51
   typename B::C acc{};
+  if constexpr (BatchedChunks<B>) {
+    if (col.chunks.size() > 1 && b.batch_ok(col.chunks)) {
+      const auto terms = b.mul_pt_many(col.chunks, c);
+      for (size_t i = 0; i < terms.size(); ++i) acc = i == 0 ? terms[i] : b.add_ct(acc, terms[i]);
+      return b.sum_all_slots(acc, b.params().S);
+    }
+  }
   for (size_t i = 0; i < col.chunks.size(); ++i) {
     const typename B::C term = b.mul_pt(col.chunks[i], c);
     acc = i == 0 ? term : b.add_ct(acc, term);
@@ -286,10 +314,28 @@ typename B::C variance_to_scale(B& b, const Col<typename B::C>& col, double S) {
   if (S <= 0.0) fail(HS_E_ERROR, "variance_to_scale: scale must be positive");
   const double n = static_cast<double>(col.n_valid);
   typename B::C sq_sum{};
-  for (size_t i = 0; i < col.chunks.size(); ++i) {
-    const typename B::C a = b.mul_pt(col.chunks[i], 1.0 / std::sqrt(S * n));
-    const typename B::C sq = b.mul_ct(a, a);
-    sq_sum = i == 0 ? sq : b.add_ct(sq_sum, sq);
+  bool done = false;
+  if constexpr (BatchedChunks<B>) {
+    if (col.chunks.size() > 1 && b.batch_ok(col.chunks)) {
+      const auto as = b.mul_pt_many(col.chunks, 1.0 / std::sqrt(S * n));
+      if (b.batch_ok(as)) {
+        const auto sqs = b.square_many(as);
+        for (size_t i = 0; i < sqs.size(); ++i) sq_sum = i == 0 ? sqs[i] : b.add_ct(sq_sum, sqs[i]);
+      } else {  // (unreachable for uniform chunks) the per-chunk squares
+        for (size_t i = 0; i < as.size(); ++i) {
+          const typename B::C sq = b.mul_ct(as[i], as[i]);
+          sq_sum = i == 0 ? sq : b.add_ct(sq_sum, sq);
+        }
+      }
+      done = true;
+    }
+  }
+  if (!done) {
+    for (size_t i = 0; i < col.chunks.size(); ++i) {
+      const typename B::C a = b.mul_pt(col.chunks[i], 1.0 / std::sqrt(S * n));
+      const typename B::C sq = b.mul_ct(a, a);
+      sq_sum = i == 0 ? sq : b.add_ct(sq_sum, sq);
+    }
   }
   sq_sum = b.sum_all_slots(sq_sum, b.params().S);
   const typename B::C mean_part = scaled_slot_sum(b, col, 1.0 / (n * std::sqrt(S)));

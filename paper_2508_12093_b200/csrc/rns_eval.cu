@@ -88,10 +88,10 @@ std::vector<RCt> RnsB::encrypt_column(const double* v, size_t n) {  // column.hp
     encode_real(c_.spec.logN, v + off, std::min(p_.S, n - off), sigma_[L], co[k].data());
   });
   std::vector<RCt> out;
+  DevBuf b = Runtime::get().alloc(nch * words(L));  // one contiguous buffer: chunk ops batch without copies
   for (size_t k = 0; k < nch; ++k) {
-    DevBuf b = Runtime::get().alloc(words(L));
-    encrypt_real(c_, L, co[k].data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
-    out.push_back(make(b, L, p_.max_level));
+    encrypt_real(c_, L, co[k].data(), tag_++, reinterpret_cast<uint64_t*>(b.get()) + k * words(L));
+    out.push_back(make(b, L, p_.max_level, k * words(L)));
   }
   return out;
 }
@@ -282,6 +282,73 @@ static bool bsgs_batch_enabled() {
     return !e || std::atoi(e) != 0;
   }();
   return on;
+}
+
+bool RnsB::batch_ok(const std::vector<RCt>& xs) const {
+  if (!bsgs_batch_enabled() || xs.empty() || !xs[0]) return false;
+  for (const RCt& x : xs)
+    if (!x || x->phys != xs[0]->phys || x->level != xs[0]->level || x->n != xs[0]->n) return false;
+  return xs[0]->phys >= 1 && xs[0]->level >= 1;
+}
+
+RnsB::Batch RnsB::gather(const std::vector<RCt>& xs) {
+  Batch b;
+  b.phys = xs[0]->phys;
+  b.level = xs[0]->level;
+  b.n = static_cast<uint32_t>(xs.size());
+  const size_t w = words(b.phys);
+  bool contiguous = true;
+  for (size_t i = 1; i < xs.size() && contiguous; ++i)
+    contiguous = xs[i]->buf == xs[0]->buf && xs[i]->off == xs[0]->off + i * w;
+  if (contiguous) {
+    b.buf = xs[0]->buf;
+    b.off = xs[0]->off;
+    return b;
+  }
+  Runtime& rt = Runtime::get();
+  b.buf = rt.alloc(size_t(b.n) * w);
+  for (size_t i = 0; i < xs.size(); ++i)
+    cuda_ok(cudaMemcpyAsync(reinterpret_cast<uint64_t*>(b.buf.get()) + i * w, xs[i]->ptr(), w * 8,
+                            cudaMemcpyDeviceToDevice, rt.stream()),
+            "gather chunks");
+  return b;
+}
+
+std::vector<RCt> RnsB::split(const Batch& b) {
+  std::vector<RCt> out;
+  for (uint32_t i = 0; i < b.n; ++i) out.push_back(make(b.buf, b.phys, b.level, b.off + size_t(i) * words(b.phys)));
+  return out;
+}
+
+std::vector<RCt> RnsB::mul_pt_many(const std::vector<RCt>& xs, double c) {  // mul_pt (ckks.hpp:168-176) per chunk
+  for (const RCt& x : xs) check_shape(sz(x));
+  const Batch X = gather(xs);
+  const int p = X.phys;
+  const double C = c * sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p];  // exactly as mul_pt
+  std::vector<uint64_t> res(p + 1);
+  residues_of(c_, p, C, res.data());
+  Batch o;
+  o.phys = p - 1;
+  o.level = X.level - 1;
+  o.n = X.n;
+  o.buf = Runtime::get().alloc(size_t(o.n) * words(o.phys));
+  rescale_mul_items(c_, p, X.ptr(), false, &res, nullptr, reinterpret_cast<uint64_t*>(o.buf.get()), X.n);
+  m_.mul_pt += X.n;
+  return split(o);
+}
+
+std::vector<RCt> RnsB::square_many(const std::vector<RCt>& xs) {  // mul_ct(a, a) (ckks.hpp:149-164) per chunk
+  for (const RCt& x : xs) check_shape(sz(x));
+  const Batch X = gather(xs);
+  const int p = X.phys;
+  Batch o;
+  o.phys = p - 1;
+  o.level = X.level - 1;
+  o.n = X.n;
+  o.buf = Runtime::get().alloc(size_t(o.n) * words(o.phys));
+  mul_relin_rescale(c_, p, X.ptr(), X.ptr(), reinterpret_cast<uint64_t*>(o.buf.get()), X.n);
+  m_.mul_ct += X.n;
+  return split(o);
 }
 
 bool RnsB::bsgs_batch_ok(const RCt& x, const std::vector<RCt>& pw, int K) const {

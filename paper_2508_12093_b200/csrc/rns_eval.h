@@ -75,6 +75,11 @@ class RnsB : public LedgerBase<RnsB, RCt> {
   // bsgs_batch_ok: every multiplication of the tree has operands at level >= 1 and physical
   // level >= 1 (no auto-bootstrap, no level_exhausted inside), else the recursion runs.
   bool bsgs_batch_ok(const C& x, const std::vector<C>& pw, int K) const;
+  // Batched chunk ops (flow.h BatchedChunks): every chunk at the same physical and logical level
+  // >= 1 (nothing to bootstrap); one rescale / HMult launch set for the whole column.
+  bool batch_ok(const std::vector<C>& xs) const;
+  std::vector<C> mul_pt_many(const std::vector<C>& xs, double c);
+  std::vector<C> square_many(const std::vector<C>& xs);
   C bsgs_full_tree(const C& x, const std::vector<double>& coeffs, const std::vector<C>& pw);
 
  private:
@@ -86,6 +91,8 @@ class RnsB : public LedgerBase<RnsB, RCt> {
     const uint64_t* ptr() const { return reinterpret_cast<const uint64_t*>(buf.get()) + off; }
   };
   Batch slice(const Batch& b, uint32_t first, uint32_t count) const;
+  Batch gather(const std::vector<C>& xs);  // contiguous view (a copy unless they already are)
+  std::vector<C> split(const Batch& b);   // one ciphertext handle per item (slices)
   Batch align_batch(const Batch& b, int p);
   C addsub(const C& a, const C& b, bool sub);
   C prepare_mul_pt(C a);

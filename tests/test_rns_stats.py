@@ -205,8 +205,9 @@ def test_znorm_full_size_north_star():
 
 
 def test_batched_bsgs_matches_recursion():
-    """RnsB's level-order batched BSGS (one batched op per tree stage) and the op-by-op
-    recursion (HS_RNS_BSGS=0) give bit-identical decrypted outputs, meters and levels."""
+    """RnsB's level-order batched BSGS (one batched op per tree stage) and batched chunk ops
+    (mul_pt / squares over a column's chunks) against the op-by-op paths (HS_RNS_BSGS=0):
+    bit-identical decrypted outputs, meters and levels."""
     import os
     import subprocess
     import sys
@@ -227,6 +228,13 @@ v, lv = e.stat(R.PEARSON, x, 20.0, y=y)
 out.append((v.tobytes(), tuple(lv), T._meter(e)))
 e = T._eval(T.LOGN, T.L)
 v, lv = e.stat(R.INVSQRT, np.linspace(0.01, 1.0, T.S), 1.0, cfg=H.InvRootConfig(cheb_degree=15, newton_iters=2))
+out.append((v.tobytes(), tuple(lv), T._meter(e)))
+x3 = T._normal(9, 3 * T.S + 100, 50.0, 10.0)   # 4 chunks, the last partial: batched chunk ops
+e = T._eval(T.LOGN, T.L)
+v, lv = e.stat(R.ZNORM, x3, 100.0)
+out.append((v.tobytes(), tuple(lv), T._meter(e)))
+e = T._eval(T.LOGN, T.L)
+v, lv = e.stat(R.KURTOSIS, x3, 20.0)
 out.append((v.tobytes(), tuple(lv), T._meter(e)))
 print(hashlib.sha256(repr(out).encode()).hexdigest())
 '''
