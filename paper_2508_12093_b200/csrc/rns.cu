@@ -1663,7 +1663,7 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
 // arithmetic as k_conv_mma, so the words are identical.
 template <int KS>
 #ifndef HS_CONV2_MINB
-#define HS_CONV2_MINB 4
+#define HS_CONV2_MINB 6
 #endif
 __global__ void __launch_bounds__(kConvMmaRows, HS_CONV2_MINB) k_conv_mma2(const uint64_t* in, size_t in_stride, uint64_t* out,
                                                              size_t out_stride, const ConvJob* jobs,
@@ -1709,63 +1709,53 @@ __global__ void __launch_bounds__(kConvMmaRows, HS_CONV2_MINB) k_conv_mma2(const
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  uint32_t a[2][KS][4];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
+  uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + g;
+  const uint2* F = frags + J.frag_off2 + lane;
+  // one m16 tile at a time (its A fragments from shared memory): half the accumulators in registers
+#pragma unroll 1
+  for (int m = 0; m < 2; ++m) {
+    uint32_t a[KS][4];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const uint32_t* r0 = As + (warp * 32 + m * 16 + g) * RSW + ks * 8 + t4;
       const uint32_t* r1 = r0 + 8 * RSW;
-      a[m][ks][0] = r0[0];
-      a[m][ks][1] = r1[0];
-      a[m][ks][2] = r0[4];
-      a[m][ks][3] = r1[4];
+      a[ks][0] = r0[0];
+      a[ks][1] = r1[0];
+      a[ks][2] = r0[4];
+      a[ks][3] = r1[4];
     }
-  uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + g;
-  const uint2* F = frags + J.frag_off2 + lane;
 #pragma unroll 1
-  for (uint32_t grp = 0; grp < ngrp; ++grp) {
-    uint64_t lo[2][4], hi[2][4];
+    for (uint32_t grp = 0; grp < ngrp; ++grp) {
+      uint64_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+      const int nb = gfp[grp] ? 6 : 8;
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+      for (int b = 0; b < 8; ++b) {
+        if (b >= nb) break;
+        uint2 bf[KS];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) lo[m][r] = hi[m][r] = 0;
-    const int nb = gfp[grp] ? 6 : 8;
+        for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(F + ((grp * 8 + b) * KS + ks) * 32);
+        int c[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      if (b >= nb) break;
-      uint2 bf[KS];
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(F + ((grp * 8 + b) * KS + ks) * 32);
-      int c[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        imma_u8(c[0], a[0][ks], bf[ks]);
-        imma_u8(c[1], a[1][ks], bf[ks]);
-      }
-      const uint32_t mulb = 1u << (8 * (b & 3));
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
+        for (int ks = 0; ks < KS; ++ks) imma_u8(c, a[ks], bf[ks]);
+        const uint32_t mulb = 1u << (8 * (b & 3));
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const uint64_t v = uint64_t(static_cast<uint32_t>(c[m][r])) * mulb;
-          if (b < 4) lo[m][r] += v;
-          else hi[m][r] += v;
+          const uint64_t v = uint64_t(static_cast<uint32_t>(c[r])) * mulb;
+          if (b < 4) lo[r] += v;
+          else hi[r] += v;
         }
-    }
+      }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t t = grp * 8 + 2 * t4 + (r & 1);
-      if (t >= ntgt) continue;
-      const ConvTgt T = tc[t];
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t t = grp * 8 + 2 * t4 + (r & 1);
+        if (t >= ntgt) continue;
+        const ConvTgt T = tc[t];
         uint64_t v;
         if (T.fp) {
-          const double h = fp_mulmod(u2d(hi[m][r]), T.c32d, T.qd, T.qinvd);
-          v = fp_canon(__dadd_rn(h, u2d(lo[m][r])), T.qd, T.qinvd);
+          const double h = fp_mulmod(u2d(hi[r]), T.c32d, T.qd, T.qinvd);
+          v = fp_canon(__dadd_rn(h, u2d(lo[r])), T.qd, T.qinvd);
         } else {
-          v = reduce128((static_cast<u128>(hi[m][r]) << 32) + lo[m][r], tq[t]);
+          v = reduce128((static_cast<u128>(hi[r]) << 32) + lo[r], tq[t]);
         }
         O[(size_t(T.orow) << logN) + m * 16 + (r >= 2 ? 8 : 0)] = v;
       }
