@@ -17,8 +17,19 @@
 
 #include "hestat/errors.hpp"
 #include "hestat_gpu.h"
+#include "hestat_rns.h"
 
 namespace hestat {
+
+// Backend choice at context creation (an extension; the reference has only the emulator).
+// EvalContext(params, seed) is the emulator-semantics GPU backend (Tier E) unless the process
+// runs with HESTAT_BACKEND=rns; EvalContext(params, seed, RnsBackend{}) is always RNS-CKKS: the
+// same operator surface over real RLWE ciphertexts (hestat_rns.h, "RNS-backed EvalContexts").
+struct RnsBackend {
+  int boot = HS_RNS_BOOT_REFRESH;  // or HS_RNS_BOOT_LOGICAL (deep chain, `depth`-deep)
+  bool has_spec = false;           // false: parameters derived from the CkksParams
+  hs_rns_spec spec{};
+};
 
 struct CkksParams {  // ckks.hpp:19-42
   std::size_t slot_count = 32768;
@@ -130,7 +141,17 @@ class EvalContext {
     gpu::check(hs_ctx_create(&p, rng_seed, &h));
     h_ = std::shared_ptr<hs_ctx>(h, hs_ctx_destroy);
   }
-  EvalContext(const EvalContext& o) : EvalContext(o.params_, o.seed_) { meter_ = o.meter_; }
+  EvalContext(CkksParams params, std::uint64_t rng_seed, const RnsBackend& rns) : params_(params), seed_(rng_seed) {
+    const hs_params p = params_.to_c();
+    hs_ctx* h = nullptr;
+    gpu::check(hs_ctx_create_rns(&p, rng_seed, rns.has_spec ? &rns.spec : nullptr, rns.boot, &h));
+    h_ = std::shared_ptr<hs_ctx>(h, hs_ctx_destroy);
+  }
+  EvalContext(const EvalContext& o) : params_(o.params_), meter_(o.meter_), seed_(o.seed_) {
+    hs_ctx* h = nullptr;
+    gpu::check(hs_ctx_clone(o.h_.get(), &h));
+    h_ = std::shared_ptr<hs_ctx>(h, hs_ctx_destroy);
+  }
   EvalContext& operator=(const EvalContext& o) {
     if (this != &o) {
       EvalContext t(o);
@@ -143,6 +164,7 @@ class EvalContext {
   }
 
   const CkksParams& params() const { return params_; }
+  bool rns_backed() const { return hs_ctx_backend(h_.get()) == 1; }  // extension: which backend runs
   CostMeter& meter() { return meter_; }
   const CostMeter& meter() const { return meter_; }
   std::uint64_t rng_seed() const { return seed_; }

@@ -123,6 +123,7 @@ int hs_diag_fp64_rate(int kind, double* ops_per_s);
 /* ---- EvalContext (ckks.hpp:83-93) --------------------------------------- */
 int hs_params_validate(const hs_params* p);                          /* CkksParams::validate */
 int hs_ctx_create(const hs_params* p, uint64_t rng_seed, hs_ctx** out);
+int hs_ctx_clone(const hs_ctx* ctx, hs_ctx** out);                   /* EvalContext copy (same backend) */
 void hs_ctx_destroy(hs_ctx* ctx);
 int hs_ctx_params(const hs_ctx* ctx, hs_params* out);
 int hs_ctx_meter(const hs_ctx* ctx, hs_meter* out);

@@ -92,6 +92,31 @@ int hs_rns_rescale_mul_const(hs_rns* ctx, uint32_t level, const uint64_t* in, in
                              uint32_t batch);
 int hs_rns_rotate(hs_rns* ctx, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out, uint32_t batch);
 
+/* ---- RNS-backed EvalContexts: the reference's operator surface on RNS-CKKS ----------
+ * An hs_ctx created here (or by hs_ctx_create when the environment has HESTAT_BACKEND=rns)
+ * runs every hestat_gpu.h entry point taking a context -- encrypt/decrypt, the EvalContext ops
+ * (ckks.hpp:97-230), Chebyshev, the inverse-root primitives, columns and every statistic
+ * (stats.hpp) -- on RNS-CKKS ciphertexts with the Tier-R kernels: the reference's control flow,
+ * levels, CostMeter and errors unchanged, values encrypted under the context's keys (seeded by
+ * rng_seed).  hs_ct handles it returns hold RNS ciphertexts; hs_ct_read (Ciphertext::slots())
+ * decrypts them.  Handles from hs_ct_new (host slot vectors) are encrypted on first use.
+ * spec = NULL derives the parameter set from the CkksParams (N = 2 slot_count, 61/60-bit primes,
+ * dense ternary secret):
+ *   HS_RNS_BOOT_REFRESH  bootstrap() (a level reset in the reference, ckks.hpp:207-213) refreshes
+ *                        the ciphertext with the secret key (decrypt + re-encrypt at the top of the
+ *                        chain); chain = max_level + 1 primes (logQP ~1150 bits at max_level 11,
+ *                        inside the 128-bit budget at N = 2^16).  Trusted-refresh model.
+ *   HS_RNS_BOOT_LOGICAL  bootstrap() resets only the logical level; the chain must cover the whole
+ *                        DAG (HESTAT_RNS_DEPTH, default 28); no key material beyond the evaluation
+ *                        keys is used during evaluation, but the chain exceeds the 128-bit budget.
+ * Environment for hs_ctx_create: HESTAT_BACKEND=rns, HESTAT_RNS_BOOT=refresh|logical,
+ * HESTAT_RNS_DEPTH=d. */
+enum { HS_RNS_BOOT_REFRESH = 0, HS_RNS_BOOT_LOGICAL = 1 };
+int hs_ctx_create_rns(const hs_params* p, uint64_t rng_seed, const hs_rns_spec* spec, int boot, hs_ctx** out);
+int hs_ctx_backend(const hs_ctx* ctx);                                  /* 0 emulator (Tier E), 1 RNS */
+int hs_ctx_rns_spec(const hs_ctx* ctx, hs_rns_spec* out, int* boot);    /* the RNS parameter set in use */
+int hs_ct_backend(const hs_ct* ct);                                     /* 1: an RNS ciphertext */
+
 /* ---- the reference's statistics over RNS ciphertexts -------------------------------
  * An EvalContext (hs_params: slot_count must be N/2) whose ops run on Tier-R
  * kernels: the reference's DAG (stats.hpp / primitives.hpp / chebyshev.hpp), level

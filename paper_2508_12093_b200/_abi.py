@@ -60,6 +60,7 @@ _SIGS = {
     "hs_graph_destroy": (None, [C.c_void_p]),
     "hs_params_validate": (C.c_int, [C.POINTER(hs_params)]),
     "hs_ctx_create": (C.c_int, [C.POINTER(hs_params), C.c_uint64, C.POINTER(CTX)]),
+    "hs_ctx_clone": (C.c_int, [CTX, C.POINTER(CTX)]),
     "hs_ctx_destroy": (None, [CTX]),
     "hs_ctx_params": (C.c_int, [CTX, C.POINTER(hs_params)]),
     "hs_ctx_meter": (C.c_int, [CTX, C.POINTER(hs_meter)]),
@@ -166,6 +167,11 @@ _SIGS.update({
     "hs_rns_rescale": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_rescale_mul_const": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32]),
     "hs_rns_rotate": (C.c_int, [RNS, C.c_uint32, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "hs_ctx_create_rns": (C.c_int, [C.POINTER(hs_params), C.c_uint64, C.POINTER(hs_rns_spec), C.c_int,
+                                    C.POINTER(CTX)]),
+    "hs_ctx_backend": (C.c_int, [CTX]),
+    "hs_ctx_rns_spec": (C.c_int, [CTX, C.POINTER(hs_rns_spec), C.POINTER(C.c_int)]),
+    "hs_ct_backend": (C.c_int, [CT]),
 })
 
 _lib = None

@@ -22,8 +22,19 @@ namespace {
 
 thread_local std::string g_err;
 
+// Every entry point runs under one process-wide (recursive) lock: the library's device work
+// shares one stream and process-wide scratch (statistics partials, grid-barrier words), and a
+// call sequence like stat_args -> launch must not interleave with another thread's call that
+// regrows that scratch.  hs_graph_begin takes the lock once more and hs_graph_end releases it,
+// so while one thread captures a graph, other threads' calls wait instead of being recorded
+// into it.  The reference's concurrency model (independent EvalContexts on worker threads,
+// ckks.hpp:80-82, hestat_cli.cpp:77-111) stays valid: calls are serialised, not refused.
+std::recursive_mutex g_api_mu;
+thread_local int g_capture_depth = 0;
+
 template <class F>
 int guard(F&& f) {
+  std::lock_guard<std::recursive_mutex> lk(g_api_mu);
   try {
     f();
     return HS_OK;
@@ -45,10 +56,35 @@ void need(const void* p, const char* what) {
 
 const Ct& get(const hs_ct* h) {
   need(h, "ciphertext");
+  if (!h->p && h->r) fail(HS_E_INVALID_ARG, "an RNS ciphertext passed to a Tier-E (emulator) context");
   return h->p;
 }
 
-hs_ct* wrap(Ct c) { return new hs_ct{std::move(c)}; }
+hs_ct* wrap(Ct c) {
+  auto* h = new hs_ct;
+  h->p = std::move(c);
+  return h;
+}
+
+// ---- RNS-backed contexts (hs_ctx::rns) ----
+rns::RCt rget(hs_ctx* c, const hs_ct* h) {
+  need(h, "ciphertext");
+  if (h->r) return h->r;
+  return c->rns->adopt(h->p);  // a host-constructed (or Tier-E) handle: encrypted on first use
+}
+std::vector<rns::RCt> rgets(hs_ctx* c, const hs_ct* const* a, uint64_t n) {
+  if (n) need(a, "ciphertext array");
+  std::vector<rns::RCt> v;
+  for (uint64_t i = 0; i < n; ++i) v.push_back(rget(c, a[i]));
+  return v;
+}
+hs_ct* rwrap(hs_ctx* c, rns::RCt r) {
+  auto* h = new hs_ct;
+  h->r = std::move(r);
+  h->home = c->rns;
+  return h;
+}
+Meter& meter_of(hs_ctx* c) { return c->rns ? c->rns->m : c->m; }
 
 hs_ctx* ctxp(hs_ctx* c) {
   need(c, "context");
@@ -94,6 +130,55 @@ pipe::ColC col_of(const hs_column* c) {
 }
 
 size_t nv_of(uint64_t n) { return n == HS_ALL_SLOTS ? flow::kAllSlots : static_cast<size_t>(n); }
+
+flow::Col<rns::RCt> rcol_of(hs_ctx* c, const hs_column* col) {
+  need(col, "column");
+  flow::Col<rns::RCt> r;
+  r.n_valid = col->n_valid;
+  for (uint64_t i = 0; i < col->n_chunks; ++i) r.chunks.push_back(rget(c, col->chunks[i]));
+  return r;
+}
+
+rns::Spec spec_of(const hs_rns_spec& spec) {
+  rns::Spec s;
+  s.logN = spec.logN;
+  s.L = spec.L;
+  s.K = spec.K;
+  s.dnum = spec.dnum;
+  s.logq0 = spec.logq0;
+  s.logq = spec.logq;
+  s.logp = spec.logp;
+  s.h = spec.h;
+  s.seed = spec.seed;
+  return s;
+}
+
+// An RNS-backed EvalContext: spec = null derives the parameter set from the CkksParams
+// (rns::default_spec); boot = HS_RNS_BOOT_*.
+hs_ctx* make_rns_ctx(const Params& q, uint64_t seed, const hs_rns_spec* spec, int boot, uint32_t depth) {
+  if (boot != HS_RNS_BOOT_REFRESH && boot != HS_RNS_BOOT_LOGICAL)
+    fail(HS_E_INVALID_ARG, "rns context: unknown bootstrap mode");
+  const rns::Boot bm = boot == HS_RNS_BOOT_REFRESH ? rns::Boot::Refresh : rns::Boot::Logical;
+  const rns::Spec s = spec ? spec_of(*spec) : rns::default_spec(q, bm, depth, seed);
+  if ((size_t(1) << s.logN) != 2 * q.S) fail(HS_E_INVALID_ARG, "rns context: slot_count must be N/2");
+  auto c = std::make_unique<hs_ctx>();
+  c->p = q;
+  c->seed = seed;
+  c->rns = std::make_shared<rns::Home>(std::make_shared<rns::Ctx>(s), q, bm);
+  return c.release();
+}
+
+// HESTAT_BACKEND=rns makes every EvalContext RNS-backed (reference programs run unmodified on
+// RNS-CKKS ciphertexts); HESTAT_RNS_BOOT=logical + HESTAT_RNS_DEPTH=d selects the deep chain.
+bool env_rns(int* boot, uint32_t* depth) {
+  const char* e = std::getenv("HESTAT_BACKEND");
+  if (!e || std::strcmp(e, "rns") != 0) return false;
+  const char* b = std::getenv("HESTAT_RNS_BOOT");
+  *boot = (b && std::strcmp(b, "logical") == 0) ? HS_RNS_BOOT_LOGICAL : HS_RNS_BOOT_REFRESH;
+  const char* d = std::getenv("HESTAT_RNS_DEPTH");
+  *depth = d ? static_cast<uint32_t>(std::atoi(d)) : 28;
+  return true;
+}
 
 }  // namespace
 
@@ -143,6 +228,12 @@ int hs_ctx_create(const hs_params* p, uint64_t seed, hs_ctx** out) {
     need(out, "out");
     Params q = Params::from(*p);
     q.validate();  // EvalContext ctor, ckks.hpp:85-88
+    int boot = 0;
+    uint32_t depth = 0;
+    if (env_rns(&boot, &depth)) {
+      *out = make_rns_ctx(q, seed, nullptr, boot, depth);
+      return;
+    }
     auto* c = new hs_ctx;
     c->p = q;
     c->seed = seed;
@@ -150,7 +241,51 @@ int hs_ctx_create(const hs_params* p, uint64_t seed, hs_ctx** out) {
   });
 }
 
-void hs_ctx_destroy(hs_ctx* c) { delete c; }
+int hs_ctx_create_rns(const hs_params* p, uint64_t seed, const hs_rns_spec* spec, int boot, hs_ctx** out) {
+  return guard([&] {
+    need(p, "params");
+    need(out, "out");
+    Params q = Params::from(*p);
+    q.validate();
+    *out = make_rns_ctx(q, seed, spec, boot, 28);
+  });
+}
+
+int hs_ctx_backend(const hs_ctx* c) { return c && c->rns ? 1 : 0; }
+
+// EvalContext's copy (the reference copies params, meter and seed): an RNS-backed copy shares the
+// RNS context (primes, keys) and gets its own meter and backend state.
+int hs_ctx_clone(const hs_ctx* c, hs_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    const hs_ctx* src = ctxp(c);
+    auto d = std::make_unique<hs_ctx>();
+    d->p = src->p;
+    d->seed = src->seed;
+    d->m = src->m;
+    if (src->rns) {
+      d->rns = std::make_shared<rns::Home>(src->rns->c, src->p, src->rns->b->boot_mode());
+      d->rns->m = src->rns->m;
+    }
+    *out = d.release();
+  });
+}
+
+int hs_ctx_rns_spec(const hs_ctx* c, hs_rns_spec* out, int* boot) {
+  return guard([&] {
+    need(out, "out");
+    if (!ctxp(c)->rns) fail(HS_E_INVALID_ARG, "hs_ctx_rns_spec: not an RNS-backed context");
+    const rns::Spec& s = c->rns->c->spec;
+    *out = hs_rns_spec{s.logN, s.L, s.K, s.dnum, s.logq0, s.logq, s.logp, s.h, s.seed};
+    if (boot) *boot = c->rns->b->boot_mode() == rns::Boot::Refresh ? HS_RNS_BOOT_REFRESH : HS_RNS_BOOT_LOGICAL;
+  });
+}
+
+void hs_ctx_destroy(hs_ctx* c) {
+  if (!c) return;
+  std::lock_guard<std::recursive_mutex> lk(g_api_mu);
+  delete c;
+}
 
 int hs_ctx_params(const hs_ctx* c, hs_params* out) {
   return guard([&] {
@@ -162,7 +297,7 @@ int hs_ctx_params(const hs_ctx* c, hs_params* out) {
 int hs_ctx_meter(const hs_ctx* c, hs_meter* out) {
   return guard([&] {
     need(out, "out");
-    const Meter& m = ctxp(c)->m;
+    const Meter& m = meter_of(const_cast<hs_ctx*>(ctxp(c)));
     *out = hs_meter{m.mul_ct, m.mul_pt, m.add, m.rotate, m.bootstrap};
   });
 }
@@ -170,7 +305,7 @@ int hs_ctx_meter(const hs_ctx* c, hs_meter* out) {
 int hs_ctx_set_meter(hs_ctx* c, const hs_meter* m) {
   return guard([&] {
     need(m, "meter");
-    ctxp(c)->m = Meter{m->mul_ct, m->mul_pt, m->add, m->rotate, m->bootstrap};
+    meter_of(ctxp(c)) = Meter{m->mul_ct, m->mul_pt, m->add, m->rotate, m->bootstrap};
   });
 }
 
@@ -185,13 +320,33 @@ int hs_ct_new(const double* slots, uint64_t n, int32_t level, hs_ct** out) {
   });
 }
 
-hs_ct* hs_ct_retain(hs_ct* ct) { return ct ? new hs_ct{ct->p} : nullptr; }
-void hs_ct_release(hs_ct* ct) { delete ct; }
-int32_t hs_ct_level(const hs_ct* ct) { return ct && ct->p ? ct->p->level : 0; }
-uint64_t hs_ct_size(const hs_ct* ct) { return ct && ct->p ? ct->p->n : 0; }
+hs_ct* hs_ct_retain(hs_ct* ct) { return ct ? new hs_ct(*ct) : nullptr; }
+void hs_ct_release(hs_ct* ct) {
+  if (!ct) return;
+  std::lock_guard<std::recursive_mutex> lk(g_api_mu);  // stream-ordered frees of shared buffers
+  delete ct;
+}
+int32_t hs_ct_level(const hs_ct* ct) {
+  if (ct && ct->r) return ct->r->level;
+  return ct && ct->p ? ct->p->level : 0;
+}
+uint64_t hs_ct_size(const hs_ct* ct) {
+  if (ct && ct->r) return ct->r->n;
+  return ct && ct->p ? ct->p->n : 0;
+}
+int hs_ct_backend(const hs_ct* ct) { return ct && ct->r ? 1 : 0; }
 
 int hs_ct_read(const hs_ct* ct, double* out, uint64_t n) {
   return guard([&] {
+    need(ct, "ciphertext");
+    if (ct->r) {  // Ciphertext::slots() of an RNS ciphertext: decrypted with its context's key
+      if (n > ct->r->n) fail(HS_E_TOO_MANY_VALUES, "hs_ct_read: n exceeds ciphertext size");
+      if (!n) return;
+      need(out, "out");
+      const std::vector<double> v = ct->home->b->decrypt(ct->r, static_cast<size_t>(n));
+      std::copy(v.begin(), v.end(), out);
+      return;
+    }
     const Ct& c = get(ct);
     if (n > c->n) fail(HS_E_TOO_MANY_VALUES, "hs_ct_read: n exceeds ciphertext size");
     if (n) need(out, "out");
@@ -205,6 +360,10 @@ int hs_encrypt(const hs_ctx* c, const double* v, uint64_t n, hs_ct** out) {
     need(out, "out");
     if (n) need(v, "values");
     hs_ctx* cc = const_cast<hs_ctx*>(ctxp(c));
+    if (cc->rns) {  // RLWE encryption at the top of the chain (no meter update either)
+      *out = rwrap(cc, cc->rns->b->encrypt(v, static_cast<size_t>(n)));
+      return;
+    }
     DevB db(cc->p, cc->m);  // encrypt is const: no meter update
     *out = wrap(db.encrypt(v, static_cast<size_t>(n)));
   });
@@ -214,6 +373,15 @@ int hs_decrypt(const hs_ctx* c, const hs_ct* ct, uint64_t n, double* out) {  // 
   return guard([&] {
     const hs_ctx* cc = ctxp(c);
     if (n > cc->p.S) fail(HS_E_TOO_MANY_VALUES, "decrypt: n exceeds slot count");
+    need(ct, "ciphertext");
+    if (ct->r) {
+      if (n > ct->r->n) fail(HS_E_LENGTH_MISMATCH, "decrypt: ciphertext shorter than n");
+      if (!n) return;
+      need(out, "out");
+      const std::vector<double> v = ct->home->b->decrypt(ct->r, static_cast<size_t>(n));
+      std::copy(v.begin(), v.end(), out);
+      return;
+    }
     const Ct& x = get(ct);
     if (n > x->n) fail(HS_E_LENGTH_MISMATCH, "decrypt: ciphertext shorter than n");
     if (n) need(out, "out");
@@ -221,29 +389,58 @@ int hs_decrypt(const hs_ctx* c, const hs_ct* ct, uint64_t n, double* out) {  // 
   });
 }
 
-#define HS_OP(body)                       \
+// body: the Tier-E op on DevB `db`; rbody: the same op on the context's RNS backend `rb`
+#define HS_OP2(body, rbody)               \
   return guard([&] {                      \
     need(out, "out");                     \
     hs_ctx* cc = ctxp(c);                 \
+    if (cc->rns) {                        \
+      rns::RnsB& rb = *cc->rns->b;        \
+      (void)rb;                           \
+      rbody;                              \
+      return;                             \
+    }                                     \
     DevB db(cc->p, cc->m);                \
     body;                                 \
   })
+#define HS_OP(body) HS_OP2(body, fail(HS_E_INVALID_ARG, "not available on an RNS-backed context"))
 
-int hs_add_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.add_ct(get(a), get(b)))); }
-int hs_sub_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.sub_ct(get(a), get(b)))); }
-int hs_add_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) { HS_OP(*out = wrap(db.add_pt(get(a), k))); }
-int hs_mul_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) { HS_OP(*out = wrap(db.mul_ct(get(a), get(b)))); }
-int hs_mul_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) { HS_OP(*out = wrap(db.mul_pt(get(a), k))); }
-int hs_mul_pt_vec(hs_ctx* c, const hs_ct* a, const double* p, uint64_t n, hs_ct** out) {
-  HS_OP({
-    if (n) need(p, "plaintext");
-    *out = wrap(db.mul_pt_vec(get(a), std::vector<double>(p, p + n)));
-  });
+int hs_add_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) {
+  HS_OP2(*out = wrap(db.add_ct(get(a), get(b))), *out = rwrap(cc, rb.add_ct(rget(cc, a), rget(cc, b))));
 }
-int hs_rotate(hs_ctx* c, const hs_ct* a, int64_t k, hs_ct** out) { HS_OP(*out = wrap(db.rotate(get(a), static_cast<long>(k)))); }
-int hs_bootstrap(hs_ctx* c, const hs_ct* a, hs_ct** out) { HS_OP(*out = wrap(db.bootstrap(get(a)))); }
+int hs_sub_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) {
+  HS_OP2(*out = wrap(db.sub_ct(get(a), get(b))), *out = rwrap(cc, rb.sub_ct(rget(cc, a), rget(cc, b))));
+}
+int hs_add_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) {
+  HS_OP2(*out = wrap(db.add_pt(get(a), k)), *out = rwrap(cc, rb.add_pt(rget(cc, a), k)));
+}
+int hs_mul_ct(hs_ctx* c, const hs_ct* a, const hs_ct* b, hs_ct** out) {
+  HS_OP2(*out = wrap(db.mul_ct(get(a), get(b))), *out = rwrap(cc, rb.mul_ct(rget(cc, a), rget(cc, b))));
+}
+int hs_mul_pt(hs_ctx* c, const hs_ct* a, double k, hs_ct** out) {
+  HS_OP2(*out = wrap(db.mul_pt(get(a), k)), *out = rwrap(cc, rb.mul_pt(rget(cc, a), k)));
+}
+int hs_mul_pt_vec(hs_ctx* c, const hs_ct* a, const double* p, uint64_t n, hs_ct** out) {
+  HS_OP2(
+      {
+        if (n) need(p, "plaintext");
+        *out = wrap(db.mul_pt_vec(get(a), std::vector<double>(p, p + n)));
+      },
+      {
+        if (n) need(p, "plaintext");
+        *out = rwrap(cc, rb.mul_pt_vec(rget(cc, a), std::vector<double>(p, p + n)));
+      });
+}
+int hs_rotate(hs_ctx* c, const hs_ct* a, int64_t k, hs_ct** out) {
+  HS_OP2(*out = wrap(db.rotate(get(a), static_cast<long>(k))),
+         *out = rwrap(cc, rb.rotate(rget(cc, a), static_cast<long>(k))));
+}
+int hs_bootstrap(hs_ctx* c, const hs_ct* a, hs_ct** out) {
+  HS_OP2(*out = wrap(db.bootstrap(get(a))), *out = rwrap(cc, rb.bootstrap(rget(cc, a))));
+}
 int hs_sum_all_slots(hs_ctx* c, const hs_ct* a, uint64_t n_valid, hs_ct** out) {
-  HS_OP(*out = wrap(db.sum_all_slots(get(a), static_cast<size_t>(n_valid))));
+  HS_OP2(*out = wrap(db.sum_all_slots(get(a), static_cast<size_t>(n_valid))),
+         *out = rwrap(cc, rb.sum_all_slots(rget(cc, a), static_cast<size_t>(n_valid))));
 }
 
 // ---- batched ops (C5) ---------------------------------------------------------------------
@@ -260,24 +457,49 @@ void put_all(const std::vector<Ct>& v, hs_ct** out) {
 }
 }  // namespace
 
+// RNS-backed contexts: element by element, in element order (same ledger semantics)
+#define HS_RBATCH2(expr)                                              \
+  {                                                                   \
+    const auto A = rgets(cc, a, n), Bv = rgets(cc, b, n);             \
+    std::vector<rns::RCt> r;                                          \
+    for (uint64_t i = 0; i < n; ++i) r.push_back(expr);               \
+    for (uint64_t i = 0; i < n; ++i) out[i] = rwrap(cc, r[i]);        \
+  }
+#define HS_RBATCH1(expr)                                              \
+  {                                                                   \
+    const auto A = rgets(cc, a, n);                                   \
+    std::vector<rns::RCt> r;                                          \
+    for (uint64_t i = 0; i < n; ++i) r.push_back(expr);               \
+    for (uint64_t i = 0; i < n; ++i) out[i] = rwrap(cc, r[i]);        \
+  }
 int hs_add_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_ADD), out));
+  HS_OP2(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_ADD), out), HS_RBATCH2(rb.add_ct(A[i], Bv[i])));
 }
 int hs_sub_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_SUB), out));
+  HS_OP2(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_SUB), out), HS_RBATCH2(rb.sub_ct(A[i], Bv[i])));
 }
 int hs_mul_ct_batch(hs_ctx* c, const hs_ct* const* a, const hs_ct* const* b, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_MUL), out));
+  HS_OP2(put_all(db.binary_batch(gets(a, n), gets(b, n), k::B_MUL), out), HS_RBATCH2(rb.mul_ct(A[i], Bv[i])));
 }
 int hs_add_pt_batch(hs_ctx* c, const hs_ct* const* a, double k, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.scalar_batch(gets(a, n), k, k::S_ADD), out));
+  HS_OP2(put_all(db.scalar_batch(gets(a, n), k, k::S_ADD), out), HS_RBATCH1(rb.add_pt(A[i], k)));
 }
 int hs_mul_pt_batch(hs_ctx* c, const hs_ct* const* a, double k, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.scalar_batch(gets(a, n), k, k::S_MUL), out));
+  HS_OP2(put_all(db.scalar_batch(gets(a, n), k, k::S_MUL), out), HS_RBATCH1(rb.mul_pt(A[i], k)));
 }
 int hs_rotate_batch(hs_ctx* c, const hs_ct* const* a, int64_t k, uint64_t n, hs_ct** out) {
-  HS_OP(put_all(db.rotate_batch(gets(a, n), static_cast<long>(k)), out));
+  HS_OP2(put_all(db.rotate_batch(gets(a, n), static_cast<long>(k)), out),
+         HS_RBATCH1(rb.rotate(A[i], static_cast<long>(k))));
 }
+
+// Inside a guard: run `rexpr` on the context's RNS backend (rb, cc) when it has one.
+#define HS_RNS_BRANCH(rexpr)              \
+  if (ctxp(c)->rns) {                     \
+    hs_ctx* cc = c;                       \
+    rns::RnsB& rb = *cc->rns->b;          \
+    rexpr;                                \
+    return;                               \
+  }
 
 // ---- Chebyshev ------------------------------------------------------------------------------
 double hs_scaled_target(int kind, double S, double t) {
@@ -325,6 +547,7 @@ int hs_eval_encrypted(hs_ctx* c, const double* coeffs, uint64_t n, double lo, do
     s.coeffs.assign(coeffs, coeffs + n);
     s.lo = lo;
     s.hi = hi;
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::eval_encrypted(rb, s, rget(cc, ct))));
     *out = wrap(pipe::eval_encrypted(ctxp(c), s, get(ct)));
   });
 }
@@ -334,6 +557,7 @@ int hs_newton_loop(hs_ctx* c, const hs_ct* x_op, const hs_ct* y, int32_t n, int3
                    hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::newton_loop(rb, rget(cc, x_op), rget(cc, y), n, iters, nv_of(n_valid))));
     *out = wrap(pipe::newton_loop(ctxp(c), get(x_op), get(y), n, iters, nv_of(n_valid)));
   });
 }
@@ -342,6 +566,7 @@ int hs_newton_refine(hs_ctx* c, const hs_ct* x, const hs_ct* y0, int32_t n, int3
                      hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::newton_refine(rb, rget(cc, x), rget(cc, y0), n, iters, nv_of(n_valid))));
     *out = wrap(pipe::newton_refine(ctxp(c), get(x), get(y0), n, iters, nv_of(n_valid)));
   });
 }
@@ -350,6 +575,7 @@ int hs_crypto_invsqrt(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg
                       hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::crypto_invsqrt(rb, rget(cc, ct), S, cfg_of(cfg), nv_of(n_valid))));
     *out = wrap(pipe::crypto_invsqrt(ctxp(c), get(ct), S, cfg_of(cfg), nv_of(n_valid)));
   });
 }
@@ -357,6 +583,7 @@ int hs_crypto_invsqrt(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg
 int hs_baseline_invsqrt(hs_ctx* c, const hs_ct* ct, double S, int32_t iters, uint64_t n_valid, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::baseline_invsqrt(rb, rget(cc, ct), S, iters, nv_of(n_valid))));
     *out = wrap(pipe::baseline_invsqrt(ctxp(c), get(ct), S, iters, nv_of(n_valid)));
   });
 }
@@ -365,6 +592,7 @@ int hs_crypto_inv(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg* cf
                   hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::crypto_inv(rb, rget(cc, ct), S, cfg_of(cfg), nv_of(n_valid))));
     *out = wrap(pipe::crypto_inv(ctxp(c), get(ct), S, cfg_of(cfg), nv_of(n_valid)));
   });
 }
@@ -372,6 +600,7 @@ int hs_crypto_inv(hs_ctx* c, const hs_ct* ct, double S, const hs_invroot_cfg* cf
 int hs_crypto_sqrt(hs_ctx* c, const hs_ct* ct, double S, int32_t degree, uint64_t n_valid, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::crypto_sqrt(rb, rget(cc, ct), S, degree, nv_of(n_valid))));
     *out = wrap(pipe::crypto_sqrt(ctxp(c), get(ct), S, degree, nv_of(n_valid)));
   });
 }
@@ -379,6 +608,7 @@ int hs_crypto_sqrt(hs_ctx* c, const hs_ct* ct, double S, int32_t degree, uint64_
 int hs_crypto_sign(hs_ctx* c, const hs_ct* ct, const hs_sign_cfg* cfg, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::crypto_sign(rb, rget(cc, ct), sign_of(cfg))));
     *out = wrap(pipe::crypto_sign(ctxp(c), get(ct), sign_of(cfg)));
   });
 }
@@ -391,6 +621,12 @@ int hs_encode_column(hs_ctx* c, const double* v, uint64_t n, hs_ct** chunks_out,
     if (n) {
       need(v, "values");
       need(chunks_out, "chunks_out");
+    }
+    if (cc->rns) {  // column.hpp:25-39 over RLWE encryptions
+      std::vector<rns::RCt> ch = cc->rns->b->encrypt_column(v, static_cast<size_t>(n));
+      for (size_t i = 0; i < ch.size(); ++i) chunks_out[i] = rwrap(cc, ch[i]);
+      *n_chunks = ch.size();
+      return;
     }
     DevB db(cc->p, cc->m);
     std::vector<Ct> chunks = db.encrypt_column(v, static_cast<size_t>(n));
@@ -406,6 +642,24 @@ int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
     if (col->n_valid > col->n_chunks * S) fail(HS_E_LENGTH_MISMATCH, "decode_column: n_valid exceeds packed capacity");
     if (col->n_valid) need(out, "out");
     size_t remaining = col->n_valid, o = 0;
+    if (ctxp(c)->rns) {  // decrypt the chunks (host FFTs on worker threads)
+      std::vector<rns::RCt> cts;
+      std::vector<size_t> ns;
+      for (uint64_t i = 0; i < col->n_chunks && remaining; ++i) {
+        const size_t take = std::min(S, remaining);
+        cts.push_back(rget(const_cast<hs_ctx*>(c), col->chunks[i]));
+        if (!cts.back() || take > cts.back()->n)
+          fail(HS_E_LENGTH_MISMATCH, "decode_column: chunk shorter than slot count");
+        ns.push_back(take);
+        remaining -= take;
+      }
+      const auto vs = c->rns->b->decrypt_many(cts, ns);
+      for (const auto& v : vs) {
+        std::copy(v.begin(), v.end(), out + o);
+        o += v.size();
+      }
+      return;
+    }
     for (uint64_t i = 0; i < col->n_chunks; ++i) {
       const size_t take = std::min(S, remaining);
       const Ct& x = get(col->chunks[i]);
@@ -422,6 +676,7 @@ int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
 int hs_mean_scaled(hs_ctx* c, const hs_column* col, double B, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::mean_scaled(rb, rcol_of(cc, col), B)));
     *out = wrap(pipe::mean_scaled(ctxp(c), col_of(col), B));
   });
 }
@@ -429,6 +684,7 @@ int hs_mean_scaled(hs_ctx* c, const hs_column* col, double B, hs_ct** out) {
 int hs_variance_to_scale(hs_ctx* c, const hs_column* col, double S, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::variance_to_scale(rb, rcol_of(cc, col), S)));
     *out = wrap(pipe::variance_to_scale(ctxp(c), col_of(col), S));
   });
 }
@@ -436,6 +692,7 @@ int hs_variance_to_scale(hs_ctx* c, const hs_column* col, double S, hs_ct** out)
 int hs_variance_scaled(hs_ctx* c, const hs_column* col, double B, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::variance_scaled(rb, rcol_of(cc, col), B)));
     *out = wrap(pipe::variance_scaled(ctxp(c), col_of(col), B));
   });
 }
@@ -444,6 +701,11 @@ int hs_moments(hs_ctx* c, const hs_column* col, double B, hs_ct** mu, hs_ct** va
   return guard([&] {
     need(mu, "mu");
     need(var, "var");
+    HS_RNS_BRANCH({
+      auto m = flow::moments(rb, rcol_of(cc, col), B);
+      *mu = rwrap(cc, m.mu);
+      *var = rwrap(cc, m.var);
+    });
     auto m = pipe::moments(ctxp(c), col_of(col), B);
     *mu = wrap(m.mu);
     *var = wrap(m.var);
@@ -452,6 +714,11 @@ int hs_moments(hs_ctx* c, const hs_column* col, double B, hs_ct** mu, hs_ct** va
 
 int hs_znorm(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out_chunks) {
   return guard([&] {
+    HS_RNS_BRANCH({
+      auto z = flow::znorm(rb, rcol_of(cc, col), B, cfg_of(cfg));
+      if (!z.chunks.empty()) need(out_chunks, "out_chunks");
+      for (size_t i = 0; i < z.chunks.size(); ++i) out_chunks[i] = rwrap(cc, z.chunks[i]);
+    });
     auto z = pipe::znorm(ctxp(c), col_of(col), B, cfg_of(cfg));
     if (!z.chunks.empty()) need(out_chunks, "out_chunks");
     for (size_t i = 0; i < z.chunks.size(); ++i) out_chunks[i] = wrap(z.chunks[i]);
@@ -461,6 +728,7 @@ int hs_znorm(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cf
 int hs_kurtosis(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::std_moment(rb, rcol_of(cc, col), B, cfg_of(cfg), 4)));
     *out = wrap(pipe::kurtosis(ctxp(c), col_of(col), B, cfg_of(cfg)));
   });
 }
@@ -468,6 +736,7 @@ int hs_kurtosis(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg*
 int hs_skewness(hs_ctx* c, const hs_column* col, double B, const hs_invroot_cfg* cfg, hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::std_moment(rb, rcol_of(cc, col), B, cfg_of(cfg), 3)));
     *out = wrap(pipe::skewness(ctxp(c), col_of(col), B, cfg_of(cfg)));
   });
 }
@@ -476,6 +745,7 @@ int hs_coeff_variation(hs_ctx* c, const hs_column* col, double B, const hs_sign_
                        hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::coeff_variation(rb, rcol_of(cc, col), B, sign_of(sc), cfg_of(cfg))));
     *out = wrap(pipe::coeff_variation(ctxp(c), col_of(col), B, sign_of(sc), cfg_of(cfg)));
   });
 }
@@ -484,6 +754,7 @@ int hs_pearson(hs_ctx* c, const hs_column* x, const hs_column* y, double B, cons
                hs_ct** out) {
   return guard([&] {
     need(out, "out");
+    HS_RNS_BRANCH(*out = rwrap(cc, flow::pearson(rb, rcol_of(cc, x), rcol_of(cc, y), B, cfg_of(cfg))));
     *out = wrap(pipe::pearson(ctxp(c), col_of(x), col_of(y), B, cfg_of(cfg)));
   });
 }
@@ -628,12 +899,26 @@ struct hs_graph {
 extern "C" {
 
 int hs_graph_begin(void) {
-  return guard([&] {
+  const int rc = guard([&] {
+    if (g_capture_depth) fail(HS_E_INVALID_ARG, "hs_graph_begin: this thread is already capturing");
     cuda_ok(cudaStreamBeginCapture(Runtime::get().stream(), cudaStreamCaptureModeRelaxed), "begin capture");
   });
+  if (rc == HS_OK) {  // held until hs_graph_end on this thread
+    g_api_mu.lock();
+    ++g_capture_depth;
+  }
+  return rc;
 }
 
 int hs_graph_end(hs_graph** out) {
+  struct Release {  // the capture's lock goes, whatever the outcome of ending it
+    ~Release() {
+      if (g_capture_depth) {
+        --g_capture_depth;
+        g_api_mu.unlock();
+      }
+    }
+  } release;
   return guard([&] {
     need(out, "out");
     auto* h = new hs_graph;
@@ -670,10 +955,10 @@ void hs_graph_destroy(hs_graph* g) {
 
 // ---------------------------------------------------------------- Tier R (hestat_rns.h)
 struct hs_rns {
-  std::unique_ptr<rns::Ctx> c;
+  std::shared_ptr<rns::Ctx> c;
 };
-struct hs_rns_eval {  // EvalContext (params + meter) bound to an RNS context
-  rns::Ctx* r = nullptr;
+struct hs_rns_eval {  // EvalContext (params + meter) bound to an RNS context (kept alive by it)
+  std::shared_ptr<rns::Ctx> r;
   Params p;
   Meter m;
 };
@@ -691,18 +976,8 @@ int hs_rns_create(const hs_rns_spec* spec, hs_rns** out) {
   return guard([&] {
     need(spec, "spec");
     need(out, "out");
-    rns::Spec s;
-    s.logN = spec->logN;
-    s.L = spec->L;
-    s.K = spec->K;
-    s.dnum = spec->dnum;
-    s.logq0 = spec->logq0;
-    s.logq = spec->logq;
-    s.logp = spec->logp;
-    s.h = spec->h;
-    s.seed = spec->seed;
     auto h = std::make_unique<hs_rns>();
-    h->c = std::make_unique<rns::Ctx>(s);
+    h->c = std::make_shared<rns::Ctx>(spec_of(*spec));
     *out = h.release();
   });
 }
@@ -711,8 +986,7 @@ int hs_rns_destroy(hs_rns* ctx) {
   return guard([&] {
     if (!ctx) return;
     Runtime::get().sync();
-    rns::forget(*ctx->c);
-    delete ctx;
+    delete ctx;  // the RNS context itself goes with its last user (EvalContexts, ciphertexts)
   });
 }
 
@@ -956,7 +1230,7 @@ int hs_rns_eval_create(hs_rns* r, const hs_params* p, hs_rns_eval** out) {
     pp.validate();
     if (pp.S != c.N / 2) fail(HS_E_INVALID_ARG, "hs_rns_eval_create: slot_count must be N/2");
     auto e = std::make_unique<hs_rns_eval>();
-    e->r = &c;
+    e->r = r->c;
     e->p = pp;
     *out = e.release();
   });

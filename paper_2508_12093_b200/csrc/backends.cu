@@ -41,6 +41,8 @@ Ct DevB::encrypt(const double* v, size_t n) const {
   DevBuf stage;
   bool pinned = false;
   const double* src = n ? device_source(v, n, &stage, &pinned, rt.stream()) : nullptr;
+  if (pinned && rt.capturing())  // a captured graph would keep reading the caller's buffer later
+    fail(HS_E_INVALID_ARG, "encrypt of a pinned host buffer cannot be captured into a graph");
   k::encrypt(qs_, src, n, d.get(), p_.S, nullptr, rt.stream());
   if (pinned) rt.sync();  // the caller may reuse its pinned buffer on return
   return ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0);
@@ -50,11 +52,14 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
   Runtime& rt = Runtime::get();
   std::vector<Ct> out;
   if (n == 0) return out;
-  // On the upload stream (unless the compute stream is being captured): the host input is
-  // read and encrypted beside whatever the compute stream is running, and only this work is
-  // waited for below.
-  const bool side = !rt.capturing();
-  cudaStream_t s = side ? rt.upload_stream() : rt.stream();
+  // The column is read from host memory and its finiteness verdict is needed before
+  // returning (a stream synchronisation), neither of which a CUDA graph can capture.
+  if (rt.capturing())
+    fail(HS_E_INVALID_ARG, "encode_column cannot run inside hs_graph_begin/hs_graph_end: encode the "
+                           "columns first and capture the computation on them");
+  // On the upload stream: the host input is read and encrypted beside whatever the compute
+  // stream is running, and only this work is waited for below.
+  cudaStream_t s = rt.upload_stream();
   DevBuf stage;
   bool pinned = false;
   const double* src = device_source(v, n, &stage, &pinned, s);
@@ -62,7 +67,7 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
   *bad = 0;
   for (size_t off = 0; off < n; off += p_.S) {
     const size_t take = std::min(p_.S, n - off);
-    DevBuf d = side ? rt.alloc_on(p_.S, s) : rt.alloc(p_.S);
+    DevBuf d = rt.alloc_on(p_.S, s);
     k::encrypt(qs_, src + off, take, d.get(), p_.S, bad, s);
     out.push_back(ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0));
   }

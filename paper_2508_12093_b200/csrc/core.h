@@ -137,12 +137,25 @@ struct Column {
 
 }  // namespace hsg
 
-// ABI handle types
+namespace hsg {
+namespace rns {
+struct RCtData;
+struct Home;
+}  // namespace rns
+}  // namespace hsg
+
+// ABI handle types.  A context is Tier E (slot vectors with the reference's emulator
+// semantics) unless `rns` is set, in which case every op runs on RNS-CKKS ciphertexts
+// (Tier R, rns_eval.h); a handle then carries `r` and the context's RNS home (keys, scales),
+// which decrypts it for hs_ct_read (Ciphertext::slots()).
 struct hs_ct {
   hsg::Ct p;
+  std::shared_ptr<const hsg::rns::RCtData> r;
+  std::shared_ptr<hsg::rns::Home> home;
 };
 struct hs_ctx {
   hsg::Params p;
   hsg::Meter m;
   uint64_t seed = 0;
+  std::shared_ptr<hsg::rns::Home> rns;
 };

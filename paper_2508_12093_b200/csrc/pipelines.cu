@@ -26,8 +26,12 @@ using flow::SignCfg;
 QSpec fused_q(const Params& p) { return QSpec{p.quantize ? QMode::Grid : QMode::None, p.scale_bits}; }
 int out_grid(const Params& p) { return p.quantize ? p.scale_bits : 0; }
 
+// Grid-unit carriers (QGrid) form products A*B = ab 2^(2s): fused kernels only for scales whose
+// square stays far inside the fp64 exponent range; larger scale_bits run the literal q() kernels.
+constexpr int kMaxFusedScaleBits = 400;
+
 bool ct_ok(const Params& p, const Ct& c) {
-  return c && c->n == p.S && (!p.quantize || c->grid == p.scale_bits);
+  return c && c->n == p.S && (!p.quantize || (c->grid == p.scale_bits && p.scale_bits <= kMaxFusedScaleBits));
 }
 
 bool fusable(const hs_ctx* ctx, std::initializer_list<const Ct*> cts) {
@@ -331,10 +335,13 @@ class PB {
     std::vector<double> all;
     std::map<std::string, int> seen;
     for (size_t i = 0; i < chebs_.size(); ++i) {
-      // range precondition of the magic-rounding core: 1.001 * sum|c| < 2^11
+      // range precondition of the magic-rounding core (quant.cuh): every leaf, product and
+      // partial sum below 2^51 grid units, i.e. 1.001 * sum|c| < 2^(51 - scale_bits) real units;
+      // capped at 2^11 (the bound the |T_k| <= 1 + 2^-20 argument was made for, scale_bits = 40)
       double mag = 0.0;
       for (double c : cheb_table(chebs_[i].second.coeffs, QSpec{QMode::None, q_.bits})) mag += std::abs(c);
-      ts.fast.push_back(std::isfinite(mag) && 1.001 * mag < 2048.0 ? 1 : 0);
+      const double lim = std::ldexp(1.0, std::min(11, 51 - q_.bits));
+      ts.fast.push_back(std::isfinite(mag) && 1.001 * mag < lim ? 1 : 0);
       auto f = seen.find(ids[i]);
       if (f != seen.end()) {
         ts.off.push_back(f->second);
@@ -349,11 +356,13 @@ class PB {
     }
     ts.n = static_cast<int>(all.size());
     Runtime& rt = Runtime::get();
-    ts.dev = rt.alloc(all.size());
-    cuda_ok(cudaMemcpyAsync(ts.dev.get(), all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice,
-                            rt.stream()),
+    // on the upload stream, waited for here: legal (and not recorded) while the compute stream
+    // is being captured into a graph, so a series' first use may happen inside a capture
+    cudaStream_t up = rt.upload_stream();
+    ts.dev = rt.alloc_on(all.size(), up);
+    cuda_ok(cudaMemcpyAsync(ts.dev.get(), all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice, up),
             "series table upload");
-    rt.sync();
+    cuda_ok(cudaStreamSynchronize(up), "series table upload");
     if (cache.size() > 512) cache.clear();  // in-flight users hold no reference: frees are stream-ordered
     return cache.emplace(key, std::move(ts)).first->second;
   }

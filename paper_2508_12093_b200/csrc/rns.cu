@@ -22,6 +22,7 @@
 #include "rns.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -615,58 +616,13 @@ struct PassEpi {
   KsSrc ks;
 };
 
-struct CgLoad {  // L2-coherent load (skips L1): the second pass of the fused NTT reads rows another block just wrote
-  const uint64_t* g;
-  __device__ uint64_t operator()(size_t off) const { return __ldcg(g + off); }
-};
-
-// The pass tile staged in shared memory.  Row tiles keep their global layout (contiguous);
-// column tiles are stored row by row with stride TPB (the global layout's stride 2^logC
-// would put every row of a warp's access on the same banks).
-template <int LOGN, bool ROWS>
-struct StageLoad {
-  const uint64_t* s;
-  __device__ uint64_t operator()(size_t off) const {
-    using G = NttGeom<LOGN, ROWS>;
-    if constexpr (ROWS) return s[off];
-    else return s[((off >> G::logC) << G::logTPB) | (off & ((1u << G::logTPB) - 1))];
-  }
-};
-
 template <class L>
-__device__ __forceinline__ L mk_ld(const uint64_t* g, const uint64_t* stage) {
-  if constexpr (std::is_same_v<L, PlainLoad> || std::is_same_v<L, CgLoad>) return L{g};
-  else return L{stage};
+__device__ __forceinline__ L mk_ld(const uint64_t* g) {
+  return L{g};
 }
 
-// Issue the asynchronous copy of one pass tile (global -> shared, 16 B per cp.async).
-template <int LOGN, bool ROWS>
-__device__ __forceinline__ void stage_tile(uint64_t* st, const uint64_t* g) {
-  using G = NttGeom<LOGN, ROWS>;
-  constexpr uint32_t words = 1u << (G::logR + G::logTPB);
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(st));
-  for (uint32_t c = threadIdx.x; c < words / 2; c += kNT) {
-    size_t src;
-    uint32_t dst;
-    if constexpr (ROWS) {
-      src = 2 * size_t(c);
-      dst = 2 * c;
-    } else {  // row r of the column tile: TPB consecutive words at r * 2^logC
-      constexpr uint32_t per = (1u << G::logTPB) / 2;  // 16-byte chunks per row
-      const uint32_t r = c / per, k = c % per;
-      src = (size_t(r) << G::logC) + 2 * k;
-      dst = (r << G::logTPB) + 2 * k;
-    }
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + dst * 8), "l"(g + src) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// One pass over tile bx of row-map entry by, batch item bz (the body of k_ntt_pass and
-// of both phases of k_ntt_fused).  CG: plain loads of the pass input go through L2 only.
+// One pass over tile bx of row-map entry by, batch item bz (the body of k_ntt_pass).
 // sm: kNTile words for the tile, plus (row passes) RowTw<LOGN>::words doubles of staged twiddles.
-// LDK: how a plain pass input is read -- 0 global, 1 global through L2 only (fused NTT's
-// second pass), 2 from the tile staged in shared memory by the persistent kernel.
 template <bool INV, bool ROWS, int LOGN, int MODE, int LDK, class PF = NoPf>
 __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t bz, uint64_t* sm, const uint64_t* in,
                                              size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
@@ -674,7 +630,7 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
                                              const PassEpi& epi, bool use_row_tw = true,
                                              const uint64_t* stage = nullptr, const PF& pf = PF{}) {
   using G = NttGeom<LOGN, ROWS>;
-  using PlainLd = std::conditional_t<LDK == 2, StageLoad<LOGN, ROWS>, std::conditional_t<LDK == 1, CgLoad, PlainLoad>>;
+  using PlainLd = PlainLoad;
   constexpr uint32_t N = 1u << LOGN;
   const uint32_t pi = rm.prime[by];
   const PrimeC& P = pcs[pi];
@@ -708,23 +664,23 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
     uint64_t* o = e.out + bz * e.out_stride + (size_t(w * e.nl + i) << LOGN) + toff;
     if constexpr (MODE == 8) {
       const uint64_t* ad = (w == 0 ? e.add0 : e.add1) + bz * e.add_stride + (size_t(i) << LOGN) + toff;
-      run(mk_ld<PlainLd>(gi, stage), MdStore<AddRowScaled>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi), MdStore<AddRowScaled>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                                            AddRowScaled{ad, e.ascale[i], e.ascale_sh[i]}});
     } else if constexpr (MODE == 1) {
       const uint64_t* ad = w == 0 ? e.add0 : e.add1;
-      run(mk_ld<PlainLd>(gi, stage), MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi), MdStore<AddRow>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                          AddRow{ad ? ad + bz * e.add_stride + (size_t(i) << LOGN) + toff : nullptr}});
     } else if constexpr (MODE == 6) {
       const KsSrc& k = epi.ks;
       const uint64_t* a0 = k.a + bz * k.stride + (size_t(i) << LOGN) + toff;
       const uint64_t* b0 = k.b + bz * k.stride + (size_t(i) << LOGN) + toff;
       const size_t h = size_t(k.nl) << LOGN;
-      run(mk_ld<PlainLd>(gi, stage), MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi), MdStore<AddTensor>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                             AddTensor{a0, a0 + h, b0, b0 + h, P, int(w)}});
     } else {
       const KsSrc& k = epi.ks;
       const uint64_t* c0 = w == 0 ? k.a + bz * k.stride + (size_t(i) << LOGN) : nullptr;
-      run(mk_ld<PlainLd>(gi, stage), MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
+      run(mk_ld<PlainLd>(gi), MdStore<AddPerm<LOGN>>{acc, o, P.q, e.pinv[i], e.pinv_sh[i],
                                                 AddPerm<LOGN>{c0, k.g, uint32_t(toff)}});
     }
   } else if constexpr (MODE == 4 || MODE == 5) {  // inverse row pass of d = a1 b1 / sigma(c1), limb irow
@@ -748,9 +704,9 @@ __device__ __forceinline__ void ntt_pass_dev(uint32_t bx, uint32_t by, uint32_t 
                      e.out + bz * e.out_stride + (size_t(p * e.level + i) << LOGN) + toff, P.q, e.qinv[i],
                      e.qinv_sh[i], e.kon, e.kk(bz, i), e.kk_sh(bz, i),
                      (e.aitems && p == 0) ? e.aitems[size_t(bz) * e.level + i] : 0};
-    run(mk_ld<PlainLd>(gi, stage), st);
+    run(mk_ld<PlainLd>(gi), st);
   } else {
-    run(mk_ld<PlainLd>(gi, stage), PlainStore{go});
+    run(mk_ld<PlainLd>(gi), PlainStore{go});
   }
 }
 
@@ -773,321 +729,12 @@ __global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_pass(const uint64_t* i
                                              pcs, tw, twd, epi, row_tw_on);
 }
 
-// ---- persistent pass with the next tile's load in flight ------------------------------
-// ncu on the one-tile-per-block passes: half the issue slots idle, the top stall
-// long_scoreboard (every block waits for its own tile from HBM before any arithmetic).
-// Here a block walks tiles t, t + grid, ... and copies tile t + grid into shared memory
-// (cp.async) as soon as tile t's first register step has read its inputs, so the HBM
-// latency of the next tile hides behind the remaining radix steps and the stores of the
-// current one.  Passes whose input is plain words only (modes 0, 1, 3, 6, 7).
-template <bool INV, bool ROWS, int LOGN, int MODE = 0>
-#ifndef HS_NTT_DB_MINB
-#define HS_NTT_DB_MINB 4
-#endif
-__global__ void __launch_bounds__(kNT, HS_NTT_DB_MINB) k_ntt_pass_db(const uint64_t* in, size_t in_stride, uint64_t* out,
-                                                     size_t out_stride, const __grid_constant__ RowMap rm,
-                                                     const PrimeC* pcs, const uint64_t* tw, const double* twd,
-                                                     const __grid_constant__ PassEpi epi, uint32_t ntx, uint32_t ny,
-                                                     uint32_t total) {
-  using G = NttGeom<LOGN, ROWS>;
-  __shared__ uint64_t sm[kNTile];
-  __shared__ __align__(16) uint64_t stage[1u << (G::logR + G::logTPB)];
-  auto src = [&](uint32_t t) {
-    const uint32_t bx = t % ntx, rest = t / ntx, by = rest % ny, bz = rest / ny;
-    const uint32_t tile0 = bx << G::logTPB;
-    const size_t toff = ROWS ? (size_t(tile0) << G::logC) : size_t(tile0);
-    return in + bz * in_stride + (size_t(rm.irow[by]) << LOGN) + toff;
-  };
-  uint32_t t = blockIdx.x;
-  if (t < total) stage_tile<LOGN, ROWS>(stage, src(t));
-  for (; t < total; t += gridDim.x) {
-    const uint32_t bx = t % ntx, rest = t / ntx, by = rest % ny, bz = rest / ny;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    const uint32_t nt = t + gridDim.x;
-    auto pf = [&]() {
-      if (nt < total) stage_tile<LOGN, ROWS>(stage, src(nt));
-    };
-    ntt_pass_dev<INV, ROWS, LOGN, MODE, 2>(bx, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi,
-                                           row_tw_on, stage, pf);
-  }
-}
-
-// ---- both passes in one launch, the intermediate kept in L2 ---------------------------
-// The two-launch NTT writes every limb's first-pass output to HBM and reads it back.  Here
-// blocks take tickets in order: ticket block s holds the first-pass tiles of limb s and the
-// second-pass tiles of limb s - lag.  A second-pass block waits (acquire) until all first-
-// pass tiles of its limb have signalled; those hold smaller tickets, so they are already
-// resident and never wait themselves (no deadlock for any grid size).  With lag ~ 2x the
-// resident blocks, the limb's first-pass output (written in place into `out`) is still in
-// L2 when the second pass reads and overwrites it, so HBM sees one read and one write per
-// word.  Counters self-reset: the last block to finish zeroes them for the next launch
-// (CUDA-graph safe).
-struct FuseCtl {
-  uint32_t* ctr;  // [0] ticket, [1] finished blocks, [2 + limb] first-pass tiles done
-  uint32_t ny, nlimb, lag, total, bz0;  // bz0: first batch item of this launch
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <bool INV, int LOGN, int M1, int M2>
-__global__ void __launch_bounds__(kNT, HS_NTT_MINB) k_ntt_fused(const uint64_t* in, size_t in_stride, uint64_t* out,
-                                                   size_t out_stride, const __grid_constant__ RowMap rm,
-                                                   const __grid_constant__ RowMap rm2, const PrimeC* pcs,
-                                                   const uint64_t* tw, const double* twd,
-                                                   const __grid_constant__ PassEpi epi,
-                                                   const __grid_constant__ FuseCtl ctl) {
-  constexpr bool R1 = INV, R2 = !INV;  // forward: columns then rows; inverse: rows then columns
-  using G1 = NttGeom<LOGN, R1>;
-  using G2 = NttGeom<LOGN, R2>;
-  constexpr uint32_t nt1 = R1 ? 1u << (G1::logR1 - G1::logTPB) : 1u << (G1::logC - G1::logTPB);
-  constexpr uint32_t nt2 = R2 ? 1u << (G2::logR1 - G2::logTPB) : 1u << (G2::logC - G2::logTPB);
-  __shared__ uint64_t sm[kNTile + (row_tw_on ? RowTw<LOGN>::words : 0)];
-  __shared__ uint32_t s_t;
-  if (threadIdx.x == 0) s_t = atomicAdd(&ctl.ctr[0], 1u);
-  __syncthreads();
-  const uint32_t t = s_t, s = t / (nt1 + nt2), r = t - s * (nt1 + nt2);
-  uint32_t* cnt = ctl.ctr + 2;
-  if (r < nt1) {
-    if (s < ctl.nlimb) {
-      const uint32_t by = s % ctl.ny, bz = s / ctl.ny + ctl.bz0;
-      ntt_pass_dev<INV, R1, LOGN, M1, 0>(r, by, bz, sm, in, in_stride, out, out_stride, rm, pcs, tw, twd, epi,
-                                             row_tw_on);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(&cnt[s], 1u);
-      }
-    }
-  } else if (s >= ctl.lag) {
-    const uint32_t limb = s - ctl.lag, by = limb % ctl.ny, bz = limb / ctl.ny + ctl.bz0;
-    if (threadIdx.x == 0) {
-      while (ld_acquire_u32(&cnt[limb]) < nt1) __nanosleep(64);
-    }
-    __syncthreads();
-    ntt_pass_dev<INV, R2, LOGN, M2, 1>(r - nt1, by, bz, sm, out, out_stride, out, out_stride, rm2, pcs, tw, twd,
-                                          epi, row_tw_on);
-  }
-  // the last block out resets the counters for the next launch
-  __shared__ bool s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctl.ctr[1], 1u) == ctl.total - 1;
-  __syncthreads();
-  if (s_last) {
-    for (uint32_t i = threadIdx.x; i < ctl.nlimb; i += blockDim.x) cnt[i] = 0;
-    if (threadIdx.x == 0) ctl.ctr[0] = ctl.ctr[1] = 0;
-  }
-}
-
-// ---- ModUp's last NTT pass fused with the key-switch inner product -------------------
-// One block = one tile of extended limb x (blockIdx.z) of one batch item (blockIdx.x,
-// fastest, so the blocks that share a key tile run together and read it from L2).  For
-// every digit j: the row pass of ext_j[x] (its column pass already ran) or, on the
-// digit's own limbs, the NTT-form input itself; the last NTT step multiplies by the
-// key words and accumulates into shared memory (the same thread owns the same words in
-// every digit).  acc_w[x] = sum_j e_j[x] key_w[j][x] is written once: the extended
-// rows never go back to HBM after their NTT and k_ks_inner disappears.
-struct InnerArgs {
-  const uint64_t* ext;  // [nd][nx][N] per batch item, after the column pass
-  size_t ext_stride;
-  const uint64_t* d;    // own limbs (NTT form) [nl][N], unless src says otherwise
-  size_t d_stride;
-  KsSrc src;
-  const uint64_t* kb;   // keys [dnum][np][N]
-  const uint64_t* ka;
-  uint64_t* acc;        // [2][nx][N] per batch item
-  size_t acc_stride;
-  uint32_t nx, nl, nd, alpha, np, nq;
-};
-
-struct SmStore {  // last NTT step: back into the tile, in place (a group's outputs are its inputs' words)
-  uint64_t* sm;
-  __device__ void operator()(size_t off, uint64_t v) const { sm[swz(uint32_t(off))] = v; }
-};
-
-template <int LOGN>
-__global__ void __launch_bounds__(kNT, 4) k_ntt_rows_inner(const __grid_constant__ InnerArgs A, const PrimeC* pcs,
-                                                          const uint64_t* tw, const double* twd) {
-  using G = NttGeom<LOGN, true>;
-  constexpr uint32_t N = 1u << LOGN;
-  constexpr uint32_t TILE = 1u << (G::logTPB + G::logC);
-  constexpr uint32_t PER = (TILE + kNT - 1) / kNT;  // words per thread in the MAC phase
-  __shared__ uint64_t sm[kNTile];
-  __shared__ double acc_s[2][kNTile];  // thread t owns words t + kNT r (conflict-free)
-  const uint32_t b = blockIdx.x, x = blockIdx.z;
-  const uint32_t gi = x < A.nl ? x : A.nq + (x - A.nl);
-  const PrimeC& P = pcs[gi];
-  const uint32_t tile0 = blockIdx.y << G::logTPB;
-  const size_t toff = size_t(tile0) << G::logC;
-  const uint64_t* psi = tw + size_t(gi) * 4 * N;
-  const uint64_t* psip = psi + N;
-  const double* twp = twd + size_t(gi) * 2 * N;
-  const uint32_t own = x < A.nl ? x / A.alpha : 0xFFFFFFFFu;
-  uint64_t* accu0 = reinterpret_cast<uint64_t*>(acc_s[0]);
-  uint64_t* accu1 = reinterpret_cast<uint64_t*>(acc_s[1]);
-  for (uint32_t j = 0; j < A.nd; ++j) {
-    const size_t krow = (size_t(j * A.np + gi) << LOGN) + toff;
-    uint64_t v[PER];
-    if (j == own) {  // the digit's own limb: d itself (NTT form), no conversion
-#pragma unroll
-      for (uint32_t r = 0; r < PER; ++r) {
-        const uint32_t e = threadIdx.x + r * kNT;
-        if (TILE % kNT != 0 && e >= TILE) break;
-        const uint32_t n = uint32_t(toff) + e;
-        if (A.src.mode == KS_TENSOR) {
-          const size_t o = b * A.src.stride + (size_t(A.nl + x) << LOGN) + n;
-          v[r] = mul_mod(A.src.a[o], A.src.b[o], P);
-        } else if (A.src.mode == KS_PERM) {
-          v[r] = A.src.a[b * A.src.stride + (size_t(A.nl + x) << LOGN) + galois_src(n, A.src.g, LOGN)];
-        } else {
-          v[r] = A.d[b * A.d_stride + (size_t(x) << LOGN) + n];
-        }
-      }
-    } else {
-      const PlainLoad ld{A.ext + b * A.ext_stride + (size_t(j * A.nx + x) << LOGN) + toff};
-      __syncthreads();  // the previous digit is done with sm
-      if (P.fp)
-        ntt_steps_fp<false, true, LOGN, 0, PlainLoad, SmStore, NoPf, kRawIn>(  // ext rows after their column pass
-            ld, SmStore{sm}, reinterpret_cast<double*>(sm), twp, P.qd, P.qinvd, tile0, static_cast<double>(P.ninv));
-      else
-        ntt_steps<false, true, LOGN, 0>(ld, SmStore{sm}, sm, psi, psip, P.q, tile0, P.ninv, P.ninv_sh);
-      __syncthreads();
-#pragma unroll
-      for (uint32_t r = 0; r < PER; ++r) {
-        const uint32_t e = threadIdx.x + r * kNT;
-        if (TILE % kNT != 0 && e >= TILE) break;
-        v[r] = sm[swz(e)];
-      }
-    }
-    // acc_w += v * key_w[j]: all key words of this thread in flight at once
-    uint64_t k0[PER], k1[PER];
-#pragma unroll
-    for (uint32_t r = 0; r < PER; ++r) {
-      const uint32_t e = threadIdx.x + r * kNT;
-      if (TILE % kNT != 0 && e >= TILE) break;
-      k0[r] = __ldg(A.kb + krow + e);
-      k1[r] = __ldg(A.ka + krow + e);
-    }
-#pragma unroll
-    for (uint32_t r = 0; r < PER; ++r) {
-      const uint32_t e = threadIdx.x + r * kNT;
-      if (TILE % kNT != 0 && e >= TILE) break;
-      if (P.fp) {  // exact fp64 products (|t| < q); sums of <= 15 terms stay below 2^53
-        const double y = u2d(v[r]);
-        const double t0 = fp_mulmod(y, u2d(k0[r]), P.qd, P.qinvd);
-        const double t1 = fp_mulmod(y, u2d(k1[r]), P.qd, P.qinvd);
-        acc_s[0][e] = j == 0 ? t0 : __dadd_rn(acc_s[0][e], t0);
-        acc_s[1][e] = j == 0 ? t1 : __dadd_rn(acc_s[1][e], t1);
-      } else {
-        const uint64_t t0 = mul_mod(v[r], k0[r], P), t1 = mul_mod(v[r], k1[r], P);
-        accu0[e] = j == 0 ? t0 : add_mod(accu0[e], t0, P.q);
-        accu1[e] = j == 0 ? t1 : add_mod(accu1[e], t1, P.q);
-      }
-    }
-  }
-  uint64_t* o0 = A.acc + b * A.acc_stride + (size_t(x) << LOGN) + toff;
-  uint64_t* o1 = o0 + (size_t(A.nx) << LOGN);
-#pragma unroll
-  for (uint32_t r = 0; r < PER; ++r) {
-    const uint32_t e = threadIdx.x + r * kNT;
-    if (TILE % kNT != 0 && e >= TILE) break;
-    if (P.fp) {
-      o0[e] = fp_canon(acc_s[0][e], P.qd, P.qinvd);
-      o1[e] = fp_canon(acc_s[1][e], P.qd, P.qinvd);
-    } else {
-      o0[e] = accu0[e];
-      o1[e] = accu1[e];
-    }
-  }
-}
-
-// HS_NTT_FUSED=1: both NTT passes in one launch with the intermediate in L2 (k_ntt_fused).
-// Off by default: it does halve the DRAM traffic (ncu, N=2^16, 32 polys x 25 limbs: 838 MB
-// against 1604 MB for the two launches) but runs 30.6 against 27.9 us per ciphertext, since
-// the passes are bound by FP64-pipe issue and latency, not by HBM.  HS_NTT_LAG scales the
-// ticket lag (default 2 x the resident blocks).
-bool use_fused_ntt() {
-  static const int mode = [] {
-    const char* e = std::getenv("HS_NTT_FUSED");
-    return e ? std::atoi(e) : 0;
-  }();
-  return mode != 0;
-}
-
-constexpr uint32_t kFuseMaxLimbs = 1u << 16;  // limbs per fused launch (the counter buffer is fixed-size)
-
-uint32_t* fuse_counters() {
-  // fixed size, allocated once and zeroed: CUDA graphs captured with this pointer stay valid
-  static uint32_t* p = reinterpret_cast<uint32_t*>(Runtime::get().scratch(3, (kFuseMaxLimbs + 2) / 2 + 1, true));
-  return p;
-}
-
-template <bool INV, int LOGN, int M1, int M2>
-void launch_fused(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
-                  const RowMap& rm2, uint32_t n, uint32_t batch, const PrimeC* pcs, const uint64_t* tw,
-                  const double* twd, const PassEpi& ep, cudaStream_t s) {
-  using G1 = NttGeom<LOGN, INV>;
-  using G2 = NttGeom<LOGN, !INV>;
-  constexpr uint32_t nt1 = INV ? 1u << (G1::logR1 - G1::logTPB) : 1u << (G1::logC - G1::logTPB);
-  constexpr uint32_t nt2 = !INV ? 1u << (G2::logR1 - G2::logTPB) : 1u << (G2::logC - G2::logTPB);
-  static const uint32_t lag = [] {
-    int per_sm = 0;
-    cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ntt_fused<INV, LOGN, M1, M2>, kNT, 0),
-            "fused ntt occupancy");
-    const char* e = std::getenv("HS_NTT_LAG");
-    const double f = e ? std::atof(e) : 2.0;
-    const double resident = double(std::max(per_sm, 1)) * Runtime::get().sm_count();
-    return std::max<uint32_t>(1, static_cast<uint32_t>(f * resident / (nt1 + nt2)) + 1);
-  }();
-  uint32_t* ctr = fuse_counters();
-  const uint32_t per = std::max<uint32_t>(1, kFuseMaxLimbs / n);  // batch items per launch
-  for (uint32_t b0 = 0; b0 < batch; b0 += per) {
-    const uint32_t nb = std::min(per, batch - b0), nlimb = n * nb;
-    const uint32_t total = (nlimb + lag) * (nt1 + nt2);
-    const FuseCtl ctl{ctr, n, nlimb, lag, total, b0};
-    k_ntt_fused<INV, LOGN, M1, M2><<<total, kNT, 0, s>>>(in, in_stride, out, out_stride, rm, rm2, pcs, tw, twd, ep,
-                                                         ctl);
-  }
-}
-
-// HS_NTT_DB=1: passes with plain inputs run as the persistent k_ntt_pass_db (next tile
-// prefetched by cp.async).  Off by default: correct, but 33.0 against 27.9 us per
-// ciphertext NTT at N=2^16, L=24 (64 registers, 4 blocks/SM; 40 registers spill and run
-// 33.5) -- the long_scoreboard stalls of the one-tile blocks are covered by the other
-// resident blocks already, and the extra shared-memory tile costs occupancy.
-bool use_db_ntt() {
-  static const int mode = [] {
-    const char* e = std::getenv("HS_NTT_DB");
-    return e ? std::atoi(e) : 0;
-  }();
-  return mode != 0;
-}
-
 template <bool INV, bool ROWS, int LOGN, int MODE>
 void launch_pass(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const RowMap& rm,
                  uint32_t n, uint32_t batch, const PrimeC* pcs, const uint64_t* tw, const double* twd,
                  const PassEpi& ep, cudaStream_t s) {
   using G = NttGeom<LOGN, ROWS>;
   const uint32_t ntx = ROWS ? 1u << (G::logR1 - G::logTPB) : 1u << (G::logC - G::logTPB);
-  constexpr bool plain_in = MODE == 0 || MODE == 1 || MODE == 3 || MODE == 6 || MODE == 7 || MODE == 8;
-  if constexpr (plain_in) {
-    if (use_db_ntt()) {
-      static const uint32_t resident = [] {
-        int per_sm = 0;
-        cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ntt_pass_db<INV, ROWS, LOGN, MODE>, kNT, 0),
-                "ntt db occupancy");
-        return static_cast<uint32_t>(std::max(per_sm, 1) * Runtime::get().sm_count());
-      }();
-      const uint32_t total = ntx * n * batch;
-      k_ntt_pass_db<INV, ROWS, LOGN, MODE><<<std::min(total, resident), kNT, 0, s>>>(
-          in, in_stride, out, out_stride, rm, pcs, tw, twd, ep, ntx, n, total);
-      return;
-    }
-  }
   k_ntt_pass<INV, ROWS, LOGN, MODE><<<dim3(ntx, n, batch), kNT, 0, s>>>(in, in_stride, out, out_stride, rm, pcs, tw,
                                                                         twd, ep);
 }
@@ -1104,28 +751,6 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
   if (rs) ep.rs = *rs;
   const int ksm = ks ? ks->mode : KS_PLAIN;
   if (ks) ep.ks = *ks;
-  if (use_fused_ntt()) {
-    const PassEpi& e = (md || rs || ks) ? ep : none;
-    if (!inverse && md && ksm == KS_TENSOR)
-      launch_fused<false, LOGN, 0, 6>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (!inverse && md && ksm == KS_PERM)
-      launch_fused<false, LOGN, 0, 7>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (inverse && ksm == KS_TENSOR)
-      launch_fused<true, LOGN, 4, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (inverse && ksm == KS_PERM)
-      launch_fused<true, LOGN, 5, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (!inverse && rs)
-      launch_fused<false, LOGN, 2, 3>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (!inverse && md && md->ascale)
-      launch_fused<false, LOGN, 0, 8>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (!inverse && md)
-      launch_fused<false, LOGN, 0, 1>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else if (!inverse)
-      launch_fused<false, LOGN, 0, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    else
-      launch_fused<true, LOGN, 0, 0>(in, in_stride, out, out_stride, rm, rm2, n, batch, pcs, tw, twd, e, s);
-    return;
-  }
   const PassEpi& E = ep;
   if (!inverse && md && ksm != KS_PLAIN) {
     launch_pass<false, false, LOGN, 0>(in, in_stride, out, out_stride, rm, n, batch, pcs, tw, twd, none, s);
@@ -1166,7 +791,6 @@ void launch_ntt(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_
 }  // namespace rns
 }  // namespace hsg
 
-#include "ntt_cluster.cuh"
 
 namespace hsg {
 namespace rns {
@@ -1395,7 +1019,7 @@ constexpr int kMaxSrc = 32, kMaxTgt = 64;
 struct ConvJob {
   uint32_t nsrc, ntgt;
   uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
-  uint32_t frag_off, frag_off2;  // B fragments of k_conv_mma / k_conv_mma2 (uint2 index into the plan's table)
+  uint32_t frag_off;  // B fragments of k_conv_mma (uint2 index into the plan's table)
   uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
   uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
   uint64_t h[kMaxTgt][kMaxSrc];
@@ -1652,117 +1276,6 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
   }
 }
 
-// ---- base conversion, targets on the MMA's N dimension (HS_CONV_MMA=2) -------------------
-// The same exact byte-split product as k_conv_mma, with the roles of the two small
-// dimensions swapped: one m16n8k32 IMMA covers 8 TARGETS for one output byte b,
-//   B_b[8i + a][t] = byte b of (h[t][i] 2^(8a) mod q_t),   C_b[n][t] = sum_k A[n][k] B_b[k][t],
-// so each thread's accumulator fragment already holds whole outputs (rows g, g+8 of each
-// m16 tile, targets 2 (lane & 3) + 0..1): out_t[n] = sum_b C_b 2^(8b) is accumulated in
-// registers (lo: b < 4, hi: b >= 4, one IMAD.WIDE per byte) instead of parking C in shared
-// memory.  Groups whose targets are all < 2^45 skip bytes 6 and 7 (h' < 2^45).  Same epilogue
-// arithmetic as k_conv_mma, so the words are identical.
-template <int KS>
-#ifndef HS_CONV2_MINB
-#define HS_CONV2_MINB 6
-#endif
-__global__ void __launch_bounds__(kConvMmaRows, HS_CONV2_MINB) k_conv_mma2(const uint64_t* in, size_t in_stride, uint64_t* out,
-                                                             size_t out_stride, const ConvJob* jobs,
-                                                             const uint2* frags, const PrimeC* pcs, uint32_t logN) {
-  constexpr int RSW = KS * 8 + 4;
-  extern __shared__ uint4 dyn_smem[];
-  uint32_t* As = reinterpret_cast<uint32_t*>(dyn_smem);  // [128][RSW]
-  __shared__ PrimeC tq[kMaxTgt];
-  __shared__ ConvTgt tc[kMaxTgt];
-  __shared__ uint64_t hinv_s[4 * KS], hinvsh_s[4 * KS], qs_s[4 * KS];
-  __shared__ uint8_t gfp[kMaxTgt / 8];
-  const ConvJob& J = jobs[blockIdx.y];
-  const uint32_t nsrc = J.nsrc, ntgt = J.ntgt, ngrp = (ntgt + 7) / 8;
-  for (uint32_t k = threadIdx.x; k < ntgt; k += kConvMmaRows) {
-    const PrimeC P = pcs[J.tgt[k]];
-    tq[k] = P;
-    const uint64_t c32 = (uint64_t(1) << 32) % P.q;
-    tc[k] = ConvTgt{P.qd, P.qinvd, static_cast<double>(c32), J.out_row + J.tgt_row[k], P.fp};
-  }
-  if (threadIdx.x < nsrc) {
-    hinv_s[threadIdx.x] = J.hinv[threadIdx.x];
-    hinvsh_s[threadIdx.x] = J.hinv_sh[threadIdx.x];
-    qs_s[threadIdx.x] = pcs[J.src[threadIdx.x]].q;
-  }
-  __syncthreads();
-  if (threadIdx.x < ngrp) {
-    bool all = true;
-    for (uint32_t t = 8 * threadIdx.x; t < min(8 * threadIdx.x + 8, ntgt); ++t) all = all && tq[t].fp;
-    gfp[threadIdx.x] = all ? 1 : 0;
-  }
-  const uint32_t n0 = blockIdx.x * kConvMmaRows;
-  {  // y_i = [x_i hinv_i]_{q_i}: thread = coefficient, the u64 words are the A row's bytes
-    const uint64_t* I = in + blockIdx.z * in_stride + (size_t(J.in_row) << logN) + n0 + threadIdx.x;
-    uint2* row = reinterpret_cast<uint2*>(As + threadIdx.x * RSW);
-    uint64_t x[4 * KS];
-#pragma unroll
-    for (int i = 0; i < 4 * KS; ++i) x[i] = uint32_t(i) < nsrc ? __ldcs(I + (size_t(i) << logN)) : 0;
-#pragma unroll
-    for (int i = 0; i < 4 * KS; ++i) {
-      const uint64_t y = uint32_t(i) < nsrc ? mul_shoup(x[i], hinv_s[i], hinvsh_s[i], qs_s[i]) : 0;
-      row[i] = make_uint2(static_cast<uint32_t>(y), static_cast<uint32_t>(y >> 32));
-    }
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  uint64_t* O = out + blockIdx.z * out_stride + n0 + warp * 32 + g;
-  const uint2* F = frags + J.frag_off2 + lane;
-  // one m16 tile at a time (its A fragments from shared memory): half the accumulators in registers
-#pragma unroll 1
-  for (int m = 0; m < 2; ++m) {
-    uint32_t a[KS][4];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const uint32_t* r0 = As + (warp * 32 + m * 16 + g) * RSW + ks * 8 + t4;
-      const uint32_t* r1 = r0 + 8 * RSW;
-      a[ks][0] = r0[0];
-      a[ks][1] = r1[0];
-      a[ks][2] = r0[4];
-      a[ks][3] = r1[4];
-    }
-#pragma unroll 1
-    for (uint32_t grp = 0; grp < ngrp; ++grp) {
-      uint64_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
-      const int nb = gfp[grp] ? 6 : 8;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        if (b >= nb) break;
-        uint2 bf[KS];
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) bf[ks] = __ldg(F + ((grp * 8 + b) * KS + ks) * 32);
-        int c[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) imma_u8(c, a[ks], bf[ks]);
-        const uint32_t mulb = 1u << (8 * (b & 3));
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint64_t v = uint64_t(static_cast<uint32_t>(c[r])) * mulb;
-          if (b < 4) lo[r] += v;
-          else hi[r] += v;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t t = grp * 8 + 2 * t4 + (r & 1);
-        if (t >= ntgt) continue;
-        const ConvTgt T = tc[t];
-        uint64_t v;
-        if (T.fp) {
-          const double h = fp_mulmod(u2d(hi[r]), T.c32d, T.qd, T.qinvd);
-          v = fp_canon(__dadd_rn(h, u2d(lo[r])), T.qd, T.qinvd);
-        } else {
-          v = reduce128((static_cast<u128>(hi[r]) << 32) + lo[r], tq[t]);
-        }
-        O[(size_t(T.orow) << logN) + m * 16 + (r >= 2 ? 8 : 0)] = v;
-      }
-    }
-  }
-}
-
 // acc_w[x] = sum_j e_j[x] * key_w[j][prime(x)] over the nx extended rows, w = 0 (b), 1 (a);
 // e_j[x] = d[x] on digit j's own rows (NTT form, never converted), ext_j[x] elsewhere.
 // Each thread holds its key words and walks the whole batch.
@@ -1890,16 +1403,6 @@ std::vector<uint32_t> iota_rows(uint32_t n, uint32_t first = 0) {
 
 // ================================================================== NTT launch
 namespace {
-// The single-pass cluster NTT (ntt_cluster.cuh) halves HBM traffic but measured slower
-// than the two-pass kernels (38 vs 31 us per ciphertext NTT at N=2^16, L=24: cluster
-// barriers and DSMEM latency, 33 co-resident clusters); opt-in with HS_NTT_CLUSTER=1.
-bool use_cluster_ntt(uint32_t logN) {
-  static const int mode = [] {
-    const char* e = std::getenv("HS_NTT_CLUSTER");
-    return e ? std::atoi(e) : 0;
-  }();
-  return mode != 0 && logN >= 14 && logN <= 16;
-}
 }  // namespace
 
 void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride,
@@ -1923,15 +1426,6 @@ void ntt_rows(const Ctx& c, const uint64_t* in, size_t in_stride, uint64_t* out,
       rm.irow[i] = static_cast<uint16_t>(irows[base + i]);
       rm.orow[i] = rm2.irow[i] = rm2.orow[i] = static_cast<uint16_t>(orows[base + i]);
       rm.prime[i] = rm2.prime[i] = static_cast<uint8_t>(primes[base + i]);
-    }
-    if (use_cluster_ntt(logN) && !epi && !rs && !ks) {  // single pass: one 8-CTA cluster per limb (ntt_cluster.cuh)
-      switch (logN) {
-        case 14: launch_ntt_cluster<14>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
-        case 15: launch_ntt_cluster<15>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
-        default: launch_ntt_cluster<16>(in, in_stride, out, out_stride, rm, n, batch, inverse, c.dpc(), tw, twd, s); break;
-      }
-      rt.note_launch(1);
-      continue;
     }
     switch (logN) {
 #define HS_NTT_CASE(L) \
@@ -1991,6 +1485,22 @@ Ctx::Ctx(const Spec& s) : spec(s) {
       }
       c -= twoN;
     }
+  }
+  // Hybrid key switching is only correct when P = prod p_j exceeds every digit modulus
+  // Q_j = prod_{i in digit j} q_i: ModDown divides the digit's ModUp error (~ Q_j) by P.  An
+  // undersized P decrypts to garbage without any other symptom, so it is refused here.
+  {
+    long double logP = 0.0L, worst = 0.0L;
+    for (uint32_t k = 0; k < s.K; ++k) logP += std::log2(static_cast<long double>(primes[nq + k]));
+    for (uint32_t lo = 0; lo < nq; lo += alpha) {
+      long double lq = 0.0L;
+      for (uint32_t i = lo; i < std::min(lo + alpha, nq); ++i) lq += std::log2(static_cast<long double>(primes[i]));
+      worst = std::max(worst, lq);
+    }
+    if (!(logP > worst))
+      fail(HS_E_INVALID_ARG, "rns: the special modulus P (" + std::to_string(static_cast<double>(logP)) +
+                                 " bits) must exceed every key-switching digit modulus (" +
+                                 std::to_string(static_cast<double>(worst)) + " bits): raise K or logp");
   }
   // per-prime constants and twiddle tables
   std::vector<uint64_t> tw(size_t(np) * 4 * N);
@@ -2357,42 +1867,10 @@ void conv_frags(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
   }
 }
 
-// k_conv_mma2's B operand: [target group of 8][output byte b][k-step][lane] -> (b0, b1) = bytes
-// B_b[32 ks + 4 (lane & 3) + 0..3][lane >> 2] and the same at k + 16, B_b[8i + a][t'] = byte b of
-// (h[8 group + t'][i] 2^(8a) mod q_t) (0 beyond the job's targets).
-void conv_frags2(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
-  const uint32_t KS = conv_ks(J.nsrc), K = 32 * KS, ngrp = (J.ntgt + 7) / 8;
-  std::vector<uint8_t> hb(size_t(8) * 8 * K);  // [byte][t'][k]
-  for (uint32_t grp = 0; grp < ngrp; ++grp) {
-    std::fill(hb.begin(), hb.end(), 0);
-    for (uint32_t tp = 0; tp < 8; ++tp) {
-      const uint32_t t = 8 * grp + tp;
-      if (t >= J.ntgt) break;
-      const uint64_t qt = c.primes[J.tgt[t]];
-      for (uint32_t i = 0; i < J.nsrc; ++i)
-        for (uint32_t a = 0; a < 8; ++a) {
-          const uint64_t v = h_mulmod(J.h[t][i] % qt, h_pow(2, 8 * a, qt), qt);
-          for (uint32_t b = 0; b < 8; ++b) hb[(size_t(b) * 8 + tp) * K + 8 * i + a] = static_cast<uint8_t>(v >> (8 * b));
-        }
-    }
-    for (uint32_t b = 0; b < 8; ++b)
-      for (uint32_t ks = 0; ks < KS; ++ks)
-        for (uint32_t lane = 0; lane < 32; ++lane) {
-          const uint8_t* col = hb.data() + (size_t(b) * 8 + (lane >> 2)) * K + 32 * ks + 4 * (lane & 3);
-          auto pack = [](const uint8_t* p) {
-            return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
-          };
-          f->push_back(make_uint2(pack(col), pack(col + 16)));
-        }
-  }
-}
-
 void attach_frags(const Ctx& c, std::vector<ConvJob>* jobs, std::vector<uint2>* f) {
   for (ConvJob& J : *jobs) {
     J.frag_off = static_cast<uint32_t>(f->size());
     conv_frags(c, J, f);
-    J.frag_off2 = static_cast<uint32_t>(f->size());
-    conv_frags2(c, J, f);
   }
 }
 
@@ -2543,59 +2021,6 @@ void launch_conv_a(const uint64_t* in, size_t in_stride, uint64_t* out, size_t o
 // HS_KS_FUSION bit 0: rotate's automorphism inside the key switch (default on: 184 -> 176 us
 // per ciphertext at N=2^16, L=24); bit 1: mul_relin's tensor product inside it (default off:
 // the extra loads and products in the register-capped ModDown pass cost more than k_tensor).
-// HS_KS_INNER=1: ModUp's row pass fused with the key inner product (k_ntt_rows_inner).  Off by
-// default: correct, but 892 us per 16 ciphertexts against 404 + 362 us for the row pass plus
-// k_ks_inner (three dependent load/NTT/MAC phases per block at 4 blocks/SM expose the load
-// latency that six independent row-pass blocks hide).
-bool use_inner_fusion() {
-  static const int mode = [] {
-    const char* e = std::getenv("HS_KS_INNER");
-    return e ? std::atoi(e) : 0;
-  }();
-  return mode != 0;
-}
-
-template <int LOGN>
-void launch_cols_and_inner(const Ctx& c, uint64_t* ext, size_t ext_stride, const std::vector<uint32_t>& rows,
-                           const std::vector<uint32_t>& primes, const InnerArgs& ia, uint32_t batch, cudaStream_t s) {
-  using Gc = NttGeom<LOGN, false>;
-  using Gr = NttGeom<LOGN, true>;
-  const uint64_t* tw = dptr<const uint64_t>(c.d_tw);
-  const double* twd = dptr<const double>(c.d_twd);
-  PassEpi none{};
-  for (size_t base = 0; base < rows.size(); base += kMaxRows) {  // column passes of the converted rows, in place
-    const uint32_t n = static_cast<uint32_t>(std::min<size_t>(kMaxRows, rows.size() - base));
-    RowMap rm{};
-    for (uint32_t i = 0; i < n; ++i) {
-      rm.irow[i] = rm.orow[i] = static_cast<uint16_t>(rows[base + i]);
-      rm.prime[i] = static_cast<uint8_t>(primes[base + i]);
-    }
-    const dim3 gc(1u << (Gc::logC - Gc::logTPB), n, batch);
-    k_ntt_pass<false, false, LOGN><<<gc, kNT, 0, s>>>(ext, ext_stride, ext, ext_stride, rm, c.dpc(), tw, twd, none);
-    Runtime::get().note_launch();
-  }
-  const dim3 g(batch, 1u << (Gr::logR1 - Gr::logTPB), ia.nx);
-  k_ntt_rows_inner<LOGN><<<g, kNT, 0, s>>>(ia, c.dpc(), tw, twd);
-  Runtime::get().note_launch();
-}
-
-void cols_and_inner(const Ctx& c, uint64_t* ext, size_t ext_stride, const std::vector<uint32_t>& rows,
-                    const std::vector<uint32_t>& primes, const InnerArgs& ia, uint32_t batch) {
-  cudaStream_t s = Runtime::get().stream();
-  switch (c.spec.logN) {
-#define HS_CI_CASE(L) \
-  case L:             \
-    launch_cols_and_inner<L>(c, ext, ext_stride, rows, primes, ia, batch, s); \
-    break;
-    HS_CI_CASE(9) HS_CI_CASE(10) HS_CI_CASE(11) HS_CI_CASE(12) HS_CI_CASE(13) HS_CI_CASE(14) HS_CI_CASE(15)
-    HS_CI_CASE(16) HS_CI_CASE(17)
-#undef HS_CI_CASE
-    default:
-      fail(HS_E_INVALID_ARG, "ntt: unsupported ring degree");
-  }
-  cuda_ok(cudaGetLastError(), "modup ntt + inner product");
-}
-
 bool use_ks_fusion(int mode_bit) {
   static const int mode = [] {
     const char* e = std::getenv("HS_KS_FUSION");
@@ -2604,7 +2029,7 @@ bool use_ks_fusion(int mode_bit) {
   return (mode & mode_bit) != 0;
 }
 
-// HS_CONV_MMA: 1 = k_conv_mma (C parked in shared memory per target), 2 = k_conv_mma2 (targets
+// HS_CONV_MMA: 1 = k_conv_mma (C parked in shared memory per target), 0 = the ALU/FP64 k_conv
 // on the MMA's N dimension), 0 = the ALU/FP64 k_conv
 int use_conv_mma() {
   static const int mode = [] {
@@ -2615,20 +2040,8 @@ int use_conv_mma() {
 }
 
 template <int KS>
-void launch_conv_mma2(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
-                      const uint2* frags, uint32_t njobs, const Ctx& c, uint32_t batch, cudaStream_t s) {
-  constexpr size_t smem = size_t(kConvMmaRows) * (KS * 8 + 4) * 4;
-  const dim3 g(c.N / kConvMmaRows, njobs, batch);
-  k_conv_mma2<KS><<<g, kConvMmaRows, smem, s>>>(in, in_stride, out, out_stride, jobs, frags, c.dpc(), c.spec.logN);
-}
-
-template <int KS>
 void launch_conv_mma(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
                      const uint2* frags, uint32_t njobs, uint32_t ntgt, const Ctx& c, uint32_t batch, cudaStream_t s) {
-  if (use_conv_mma() == 2) {
-    launch_conv_mma2<KS>(in, in_stride, out, out_stride, jobs, frags, njobs, c, batch, s);
-    return;
-  }
   static const bool attr = [] {
     cuda_ok(cudaFuncSetAttribute(k_conv_mma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(conv_mma_smem<KS>())),
@@ -2723,13 +2136,6 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
     launch_conv(rest, nx - rest, DC, dc_stride, EXT, ext_stride, up + P.n_full, FR, nd - P.n_full, c, batch);
   }
   const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
-  if (use_inner_fusion() && nd <= 15) {
-    // column pass of the converted rows, then their row pass with the key inner product
-    // as its store (acc_w written once, the NTT'd extended rows never stored)
-    const InnerArgs ia{EXT, ext_stride, d, d_stride, src ? *src : KsSrc{}, KB, KA, ACC, acc_stride,
-                       nx, nl, nd, c.alpha, c.np, c.nq};
-    cols_and_inner(c, EXT, ext_stride, P.up_rows, P.up_primes, ia, batch);
-  } else {
   ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
   // inner product with the key (each key word read once per call)
   {
@@ -2748,7 +2154,6 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
       default:
         fail(HS_E_INVALID_ARG, "key switch: more than 15 digits");
     }
-  }
   }
   if (rescale) {
     const uint32_t lv = level;
@@ -2942,6 +2347,14 @@ void rotate(Ctx& c, uint32_t level, int64_t k, const uint64_t* in, uint64_t* out
 void prepare_level(Ctx& c, uint32_t level) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns: level > L");
   ks_plan(c, level);
+}
+
+Ctx::~Ctx() {
+  try {
+    Runtime::get().sync();
+  } catch (...) {
+  }
+  forget(*this);
 }
 
 void forget(const Ctx& c) {

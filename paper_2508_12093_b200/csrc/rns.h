@@ -99,6 +99,9 @@ __device__ __forceinline__ uint64_t reduce128(u128 x, const PrimeC& p) {
 class Ctx {
  public:
   explicit Ctx(const Spec& s);
+  ~Ctx();  // drops this context's cached key-switching plans
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
   const Spec spec;
   uint32_t N, nq, np, alpha;
   std::vector<uint64_t> primes;   // q_0..q_L, p_0..p_{K-1}

@@ -21,7 +21,9 @@
 namespace hsg {
 namespace rns {
 
-RnsB::RnsB(Ctx& c, const Params& p, Meter& m) : LedgerBase(p, m), c_(c) {
+RnsB::RnsB(Ctx& c, const Params& p, Meter& m, Boot boot) : LedgerBase(p, m), c_(c), boot_(boot) {
+  if (boot == Boot::Refresh && static_cast<int>(c.spec.L) < p.max_level + 1)
+    fail(HS_E_INVALID_ARG, "rns eval: refresh bootstrapping needs a chain of at least max_level + 1 primes");
   if (p.S != c.N / 2) fail(HS_E_INVALID_ARG, "rns eval: slot_count must be N/2 of the RNS context");
   sigma_.resize(c.spec.L + 1);
   sigma_[0] = std::ldexp(1.0, static_cast<int>(c.spec.logq));  // CKKS scale ~ the rescaling primes
@@ -153,10 +155,57 @@ RCt RnsB::add_pt(const RCt& a, double c) {  // ckks.hpp:137-144
   return make(o, a->phys, a->level);
 }
 
-RCt RnsB::bootstrap(const RCt& a) {  // ckks.hpp:207-213: logical level reset (deep chain)
+RCt RnsB::bootstrap(const RCt& a) {  // ckks.hpp:207-213
   check_shape(sz(a));
   ++m_.bootstrap;
-  return make(a->buf, a->phys, p_.max_level, a->off);
+  if (boot_ == Boot::Refresh) return refresh(a);
+  return make(a->buf, a->phys, p_.max_level, a->off);  // logical level reset (deep chain)
+}
+
+// decrypt (CRT through q_0 q_1) -> coefficients at sigma_phys -> rescaled to sigma_L -> encrypted
+// at the top of the chain with a fresh tag: same slots, fresh noise, logical level max_level
+RCt RnsB::refresh(const RCt& a) {
+  if (a->phys < 1) fail(HS_E_LEVEL_EXHAUSTED, "rns refresh: ciphertext at the last RNS limb");
+  const int L = static_cast<int>(c_.spec.L);
+  std::vector<double> co(c_.N);
+  decrypt_crt(c_, a->phys, a->ptr(), co.data());
+  const double r = sigma_[L] / sigma_[a->phys];
+  for (double& v : co) v = std::nearbyint(v * r);
+  DevBuf b = Runtime::get().alloc(words(L));
+  encrypt_real(c_, L, co.data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
+  RCt o = make(b, L, p_.max_level);
+  const_cast<RCtData*>(o.get())->n = a->n;
+  return o;
+}
+
+RCt Home::adopt(const Ct& x) {
+  if (!x || x->n == 0) return nullptr;  // Ciphertext(): the reference's empty accumulator (size 0, level 0)
+  const std::vector<double>& v = x->host_slots();
+  std::vector<double> pad(p.S, 0.0);
+  std::copy(v.begin(), v.begin() + std::min(v.size(), p.S), pad.begin());
+  RCt e = b->encrypt(pad.data(), pad.size());
+  auto d = std::make_shared<RCtData>(*e);
+  d->level = x->level;
+  d->n = x->n;  // a size other than slot_count keeps failing shape checks, as in the reference
+  return d;
+}
+
+Spec default_spec(const Params& p, Boot boot, uint32_t depth, uint64_t seed) {
+  Spec s;
+  uint32_t logN = 1;
+  while ((size_t(1) << logN) < 2 * p.S) ++logN;
+  if ((size_t(1) << logN) != 2 * p.S) fail(HS_E_INVALID_ARG, "rns: slot_count must be a power of two");
+  s.logN = logN;
+  s.L = boot == Boot::Refresh ? static_cast<uint32_t>(p.max_level) + 1 : depth + 1;
+  s.logq0 = 61;
+  s.logq = 60;
+  s.logp = 61;
+  s.dnum = std::min<uint32_t>(3, s.L + 1);
+  const uint32_t alpha = (s.L + 1 + s.dnum - 1) / s.dnum;
+  s.K = (s.logq0 + (alpha - 1) * s.logq + 1 + s.logp - 1) / s.logp;  // P above every digit modulus
+  s.h = 0;
+  s.seed = seed;
+  return s;
 }
 
 RCt RnsB::mul_ct(RCt a, RCt b) {  // ckks.hpp:149-164

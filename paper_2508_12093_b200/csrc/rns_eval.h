@@ -38,10 +38,20 @@ struct RCtData {
 };
 using RCt = std::shared_ptr<const RCtData>;
 
+// How bootstrap() (ckks.hpp:207-213, a value-preserving level reset in the reference) is realised:
+//   Logical  the logical level is reset, the physical chain is not: the chain must be at least the
+//            statistic's whole no-bootstrap depth (deep chain, no secret key during evaluation);
+//   Refresh  the ciphertext is refreshed to the top of the chain with the context's secret key
+//            (decrypt + re-encrypt on the device, fresh noise): a trusted-refresh stand-in for CKKS
+//            bootstrapping, which the reference does not implement either.  Physical level =
+//            logical level + 1 at all times, so a chain of max_level + 1 primes suffices.
+enum class Boot { Logical = 0, Refresh = 1 };
+
 class RnsB : public LedgerBase<RnsB, RCt> {
  public:
   using C = RCt;
-  RnsB(Ctx& c, const Params& p, Meter& m);
+  RnsB(Ctx& c, const Params& p, Meter& m, Boot boot = Boot::Logical);
+  Boot boot_mode() const { return boot_; }
 
   int level(const C& c) const { return c ? c->level : 0; }
   C encrypt(const double* v, size_t n);
@@ -98,12 +108,37 @@ class RnsB : public LedgerBase<RnsB, RCt> {
   C prepare_mul_pt(C a);
   C align(const C& x, int p);  // same value at physical level p (<= x->phys), scale sigma_p
   C make(DevBuf b, int phys, int level, size_t off = 0) const;
+  C refresh(const C& a);  // Boot::Refresh: the same slots at the top of the chain, fresh noise
   size_t words(int phys) const { return size_t(2) * (phys + 1) * c_.N; }
   size_t sz(const C& c) const { return c ? c->n : 0; }
   Ctx& c_;
+  Boot boot_ = Boot::Logical;
   std::vector<double> sigma_;
   uint64_t tag_ = 1;
 };
+
+// An RNS-backed EvalContext (hs_ctx::rns): the RNS context with its keys, the EvalContext's
+// parameters and meter, and the backend bound to them.  Ciphertext handles share it, so
+// Ciphertext::slots() can decrypt a handle that outlives its context.
+struct Home {
+  std::shared_ptr<Ctx> c;
+  Params p;
+  Meter m;
+  std::unique_ptr<RnsB> b;
+  Home(std::shared_ptr<Ctx> ctx, const Params& params, Boot boot) : c(std::move(ctx)), p(params) {
+    b = std::make_unique<RnsB>(*c, p, m, boot);
+  }
+  // a Tier-E handle (Ciphertext(std::vector<double>, int) or another context's output) as an RNS
+  // ciphertext of this context: its slots encrypted at the top of the chain, its level and size kept
+  RCt adopt(const Ct& x);
+};
+
+// The RNS parameter set an RNS-backed EvalContext uses for CkksParams p (N = 2 slot_count):
+//   Refresh: L = max_level + 1 (physical = logical + 1), logq0 = 61, logq = 60, dnum = 3, K so that
+//            P exceeds every digit modulus, dense ternary secret (logQP ~1100 bits at max_level 11:
+//            inside the 128-bit budget of N = 2^16, ~1760 bits);
+//   Logical: L = depth + 1 for a caller-given depth (deep chain), same primes.
+Spec default_spec(const Params& p, Boot boot, uint32_t depth, uint64_t seed);
 
 }  // namespace rns
 }  // namespace hsg

@@ -170,12 +170,36 @@ def _out(fn, *args) -> Ciphertext:
     return Ciphertext._own(h)
 
 
+BOOT_REFRESH, BOOT_LOGICAL = 0, 1  # hestat_rns.h HS_RNS_BOOT_*
+
+
 class EvalContext:  # ckks.hpp:83-257
-    def __init__(self, params: Optional[CkksParams] = None, rng_seed: int = 0):
+    """backend=None: the emulator-semantics GPU backend (Tier E; RNS when the process has
+    HESTAT_BACKEND=rns); backend="rns": every op on RNS-CKKS ciphertexts (Tier R), with
+    `boot` BOOT_REFRESH (secret-key refresh at the reference's bootstraps, chain max_level + 1)
+    or BOOT_LOGICAL (deep chain), and `rns_spec` an explicit RnsSpec (rns.py) or None."""
+
+    def __init__(self, params: Optional[CkksParams] = None, rng_seed: int = 0, backend: Optional[str] = None,
+                 boot: int = BOOT_REFRESH, rns_spec=None):
         self._p = CkksParams(**vars(params)) if params is not None else CkksParams()
         h = C.c_void_p()
-        _check(_abi.lib().hs_ctx_create(C.byref(self._p._c()), int(rng_seed), C.byref(h)))
+        if backend == "rns":
+            sp = C.byref(rns_spec.c()) if rns_spec is not None else None
+            _check(_abi.lib().hs_ctx_create_rns(C.byref(self._p._c()), int(rng_seed), sp, int(boot), C.byref(h)))
+        elif backend is None:
+            _check(_abi.lib().hs_ctx_create(C.byref(self._p._c()), int(rng_seed), C.byref(h)))
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
         self._h = h
+
+    def rns_backed(self) -> bool:
+        return _abi.lib().hs_ctx_backend(self._h) == 1
+
+    def rns_spec(self):
+        """(hs_rns_spec, boot mode) of an RNS-backed context."""
+        s, b = _abi.hs_rns_spec(), C.c_int()
+        _check(_abi.lib().hs_ctx_rns_spec(self._h, C.byref(s), C.byref(b)))
+        return s, b.value
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -81,7 +81,16 @@ class DeviceBuffer:
     def offset(self, words: int) -> int:
         return self.ptr + 8 * words
 
+    def sub(self, words: int) -> "DeviceBuffer":
+        """Non-owning view starting `words` words into this buffer."""
+        v = object.__new__(DeviceBuffer)
+        v.ptr, v.words, v._owner = self.ptr + 8 * words, self.words - words, self
+        return v
+
     def free(self):
+        if getattr(self, "_owner", None) is not None:  # a view owns nothing
+            self.ptr = None
+            return
         if self.ptr:
             _abi.lib().hs_rns_free(self.ptr)
             self.ptr = None

@@ -43,3 +43,19 @@ def test_reference_acceptance_runner():
     assert "[FAIL] C2 baseline dominance" in out, out
     assert "MRE 4.256e-11" in out, out  # same C1 MRE as proj/test_output.txt:14
     assert r.returncode == 1, out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("crit,name", [(1, "C1 grid accuracy"), (3, "C3 measures at 100k scale"),
+                                       (5, "C5 depth ledger")])
+def test_reference_acceptance_runner_on_rns(crit, name):
+    """The same unmodified acceptance binary with HESTAT_BACKEND=rns: every EvalContext it creates
+    is RNS-CKKS (RLWE ciphertexts, key switching, rescale; bootstrap = secret-key refresh at the
+    reference's bootstrap points), and the tolerance criteria still pass -- C1 (inverse-sqrt grid
+    MRE <= 1e-4, 2 bootstraps, < 30 s), C3 (znorm, skewness, kurtosis, CV, Pearson at 100k rows:
+    accuracy bounds and bootstrap counts, < 120 s) and C5 (depth ledger)."""
+    env = {**os.environ, "HESTAT_BACKEND": "rns"}
+    r = subprocess.run([_bin("acceptance_gpu"), "--criterion", str(crit)], capture_output=True, text=True,
+                       timeout=900, cwd=FIXTURE_CWD, env=env)
+    assert f"[PASS] {name}" in r.stdout, r.stdout + r.stderr[-2000:]
+    assert r.returncode == 0, r.stdout
