@@ -169,9 +169,10 @@ def test_errors_match_reference():
         RnsEval(_rns(LOGN, L), H.CkksParams(slot_count=S // 2))  # slot_count != N/2
 
 
-@pytest.mark.parametrize("which", ["kurt", "skew", "pearson"])
+@pytest.mark.parametrize("which", ["kurt", "skew", "pearson", "kurt_normal", "skew_normal"])
 def test_full_size_c3_c4(which):
-    """N = 2^16: the cancellation-prone statistics at full size, within 1e-6."""
+    """N = 2^16: the cancellation-prone statistics at full size, within 1e-6 (C3's two datasets:
+    LogNormal(0, 0.5) and N(0,1), whose skewness ~1e-2 is the cancellation-prone case)."""
     from paper_2508_12093_b200 import rns as R
     rng = np.random.default_rng(12)
     Sf = 32768
@@ -181,8 +182,9 @@ def test_full_size_c3_c4(which):
         y = np.sqrt(0.6) * z + np.sqrt(0.4) * rng.standard_normal(Sf)
         code, ow = R.PEARSON, ST_PEARSON
     else:
-        x, y = np.exp(0.5 * rng.standard_normal(Sf)), None
-        code, ow = (R.KURTOSIS, ST_KURT) if which == "kurt" else (R.SKEWNESS, ST_SKEW)
+        x = rng.standard_normal(Sf) if which.endswith("_normal") else np.exp(0.5 * rng.standard_normal(Sf))
+        y = None
+        code, ow = (R.KURTOSIS, ST_KURT) if which.startswith("kurt") else (R.SKEWNESS, ST_SKEW)
     e = _eval(16, 28)
     out, lv = e.stat(code, x, 20.0, y=y)
     ref = oracle().stat(Params(slot_count=Sf), ow, x, 20.0, y=y)
