@@ -1020,6 +1020,7 @@ struct ConvJob {
   uint32_t nsrc, ntgt;
   uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
   uint32_t frag_off;  // B fragments of k_conv_mma (uint2 index into the plan's table)
+  uint32_t img_off;   // B image of k_conv_tc (byte offset into the plan's image table)
   uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
   uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
   uint64_t h[kMaxTgt][kMaxSrc];
@@ -1275,6 +1276,8 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
     __syncwarp();
   }
 }
+
+#include "conv_tc.cuh"
 
 // acc_w[x] = sum_j e_j[x] * key_w[j][prime(x)] over the nx extended rows, w = 0 (b), 1 (a);
 // e_j[x] = d[x] on digit j's own rows (NTT form, never converted), ext_j[x] elsewhere.
@@ -1867,10 +1870,32 @@ void conv_frags(const Ctx& c, const ConvJob& J, std::vector<uint2>* f) {
   }
 }
 
-void attach_frags(const Ctx& c, std::vector<ConvJob>* jobs, std::vector<uint2>* f) {
+// k_conv_tc's B operand for one job: the shared-memory image [KC][NR][16] (K-major,
+// SWIZZLE_NONE core matrices) of B[8t + b][8i + a] = byte b of (h[t][i] 2^(8a) mod q_t);
+// chunk kc holds K bytes 16 kc .. 16 kc + 15 (sources 2 kc, 2 kc + 1), rows past 8 ntgt
+// and sources past nsrc are zero.
+void conv_tc_image(const Ctx& c, const ConvJob& J, std::vector<uint8_t>* img) {
+  const uint32_t KC = 2 * conv_ks(J.nsrc), NR = tc_rows(J.ntgt);
+  const size_t base = img->size();
+  img->resize(base + size_t(KC) * NR * 16, 0);
+  for (uint32_t t = 0; t < J.ntgt; ++t) {
+    const uint64_t qt = c.primes[J.tgt[t]];
+    for (uint32_t i = 0; i < J.nsrc; ++i)
+      for (uint32_t a = 0; a < 8; ++a) {
+        const uint64_t v = h_mulmod(J.h[t][i] % qt, h_pow(2, 8 * a, qt), qt);
+        const uint32_t k = 8 * i + a, kc = k / 16, j = k % 16;
+        for (uint32_t b = 0; b < 8; ++b)
+          (*img)[base + (size_t(kc) * NR + 8 * t + b) * 16 + j] = static_cast<uint8_t>(v >> (8 * b));
+      }
+  }
+}
+
+void attach_frags(const Ctx& c, std::vector<ConvJob>* jobs, std::vector<uint2>* f, std::vector<uint8_t>* img) {
   for (ConvJob& J : *jobs) {
     J.frag_off = static_cast<uint32_t>(f->size());
     conv_frags(c, J, f);
+    J.img_off = static_cast<uint32_t>(img->size());
+    conv_tc_image(c, J, img);
   }
 }
 
@@ -1885,6 +1910,7 @@ struct KsPlan {
   std::vector<uint32_t> p_rows, p_primes;    // acc P rows (both halves) for the iNTT
   std::vector<uint32_t> cv_rows, cv_primes;  // conv rows (both halves) for the NTT
   DevBuf frags;                       // k_conv_mma B fragments of every job above
+  DevBuf tc_img;                      // k_conv_tc B images of every job above
   DevBuf pinv, pinv_sh;               // [nl] P^-1 mod q_i
   DevBuf qinv, qinv_sh;               // [level] q_level^-1 mod q_i (rescale)
   // ModDown by P q_level (HMult's rescale merged into the key switch), level >= 1:
@@ -1922,7 +1948,8 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
     fill_conv(c, src, tgt, row, lo, j * p->nx, &up[j]);
   }
   std::vector<uint2> frags;
-  attach_frags(c, &up, &frags);
+  std::vector<uint8_t> img;
+  attach_frags(c, &up, &frags, &img);
   std::vector<ConvJob> down(2);
   std::vector<uint32_t> src, tgt, row;
   for (uint32_t k = 0; k < K; ++k) src.push_back(c.nq + k);
@@ -1941,7 +1968,7 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
       p->cv_primes.push_back(i);
     }
   }
-  attach_frags(c, &down, &frags);
+  attach_frags(c, &down, &frags, &img);
   std::vector<ConvJob> rdown;
   if (level >= 1) {
     rdown.resize(2);
@@ -1962,7 +1989,7 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
         p->cv2_primes.push_back(i);
       }
     }
-    attach_frags(c, &rdown, &frags);
+    attach_frags(c, &rdown, &frags, &img);
     const uint64_t ql = c.primes[level];
     uint64_t v = 1;
     for (uint32_t k = 0; k < K; ++k) v = h_mulmod(v, c.primes[c.nq + k] % ql, ql);
@@ -1983,6 +2010,7 @@ std::unique_ptr<KsPlan> build_plan(const Ctx& c, uint32_t level) {
   p->up_jobs = upload(up);
   p->down_jobs = upload(down);
   p->frags = upload(frags);
+  p->tc_img = upload(img);
   std::vector<uint64_t> pinv(nl), pinv_sh(nl);
   for (uint32_t i = 0; i < nl; ++i) {
     const uint64_t q = c.primes[i];
@@ -2029,12 +2057,13 @@ bool use_ks_fusion(int mode_bit) {
   return (mode & mode_bit) != 0;
 }
 
-// HS_CONV_MMA: 1 = k_conv_mma (C parked in shared memory per target), 0 = the ALU/FP64 k_conv
-// on the MMA's N dimension), 0 = the ALU/FP64 k_conv
+// HS_CONV_MMA: 2 (default) = k_conv_tc (tcgen05.mma, accumulators in TMEM), 1 = k_conv_mma
+// (legacy warp-level mma.sync IMMA, C parked in shared memory per target), 0 = the ALU/FP64
+// k_conv
 int use_conv_mma() {
   static const int mode = [] {
     const char* e = std::getenv("HS_CONV_MMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return mode;
 }
@@ -2055,13 +2084,48 @@ void launch_conv_mma(const uint64_t* in, size_t in_stride, uint64_t* out, size_t
                                                                    c.dpc(), c.spec.logN);
 }
 
+// k_conv_tc: persistent, one CTA per SM (the dynamic shared memory request keeps a second
+// CTA off the SM, so no CTA waits in tcgen05.alloc); the SMs are split evenly between the
+// jobs of the call, each CTA taking a contiguous run of its job's (batch item, tile) pairs.
+template <int KS>
+void launch_conv_tc(const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, const ConvJob* jobs,
+                    const uint8_t* img, uint32_t njobs, uint32_t ntgt, const Ctx& c, uint32_t batch, cudaStream_t s) {
+  static const bool attr = [] {
+    cuda_ok(cudaFuncSetAttribute(k_conv_tc<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+            "conv_tc smem");
+    return true;
+  }();
+  (void)attr;
+  const uint32_t NR = tc_rows(ntgt);
+  const size_t smem = std::max<size_t>(2 * tc_smem_a<KS>() + size_t(2 * KS) * NR * 16, 120 * 1024);
+  const uint32_t ntiles = batch * (c.N / kTcRows);
+  const uint32_t sms = static_cast<uint32_t>(Runtime::get().sm_count());
+  const uint32_t want = std::max<uint32_t>(1, sms / njobs);
+  const uint32_t per = (ntiles + want - 1) / want, nblk = (ntiles + per - 1) / per;
+  k_conv_tc<KS><<<dim3(nblk, njobs), kTcThreads, smem, s>>>(in, in_stride, out, out_stride, jobs, img, c.dpc(),
+                                                              c.spec.logN, ntiles, per);
+}
+
 // nsrc sources per job (all jobs of a call alike), ntgt targets at most per job.
 void launch_conv(uint32_t nsrc, uint32_t ntgt, const uint64_t* in, size_t in_stride, uint64_t* out,
-                 size_t out_stride, const ConvJob* jobs, const uint2* frags, uint32_t njobs, const Ctx& c,
+                 size_t out_stride, const ConvJob* jobs, const KsPlan& P, uint32_t njobs, const Ctx& c,
                  uint32_t batch) {
   if (njobs == 0) return;
   cudaStream_t s = Runtime::get().stream();
-  if (frags && use_conv_mma() && conv_ks(nsrc) <= 4 && c.N % kConvMmaRows == 0) {
+  const uint2* frags = dptr<const uint2>(P.frags);
+  if (use_conv_mma() == 2 && conv_ks(nsrc) <= 4 && ntgt <= 64 && c.N % kTcRows == 0) {
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(P.tc_img.get());
+    switch (conv_ks(nsrc)) {
+      case 1: launch_conv_tc<1>(in, in_stride, out, out_stride, jobs, img, njobs, ntgt, c, batch, s); break;
+      case 2: launch_conv_tc<2>(in, in_stride, out, out_stride, jobs, img, njobs, ntgt, c, batch, s); break;
+      case 3: launch_conv_tc<3>(in, in_stride, out, out_stride, jobs, img, njobs, ntgt, c, batch, s); break;
+      default: launch_conv_tc<4>(in, in_stride, out, out_stride, jobs, img, njobs, ntgt, c, batch, s);
+    }
+    cuda_ok(cudaGetLastError(), "conv_tc launch");
+    Runtime::get().note_launch();
+    return;
+  }
+  if (use_conv_mma() != 0 && conv_ks(nsrc) <= 4 && c.N % kConvMmaRows == 0) {
     switch (conv_ks(nsrc)) {
       case 1: launch_conv_mma<1>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s); break;
       case 2: launch_conv_mma<2>(in, in_stride, out, out_stride, jobs, frags, njobs, ntgt, c, batch, s); break;
@@ -2129,11 +2193,10 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   // ModUp: d -> coefficient form (out of place), convert every digit, NTT the new rows
   ntt_rows(c, d, d_stride, DC, dc_stride, qrows, qrows, qrows, batch, true, nullptr, nullptr, src);
   const ConvJob* up = dptr<const ConvJob>(P.up_jobs);
-  const uint2* FR = dptr<const uint2>(P.frags);
-  launch_conv(c.alpha, nx - c.alpha, DC, dc_stride, EXT, ext_stride, up, FR, P.n_full, c, batch);
+  launch_conv(c.alpha, nx - c.alpha, DC, dc_stride, EXT, ext_stride, up, P, P.n_full, c, batch);
   if (P.n_full < nd) {
     const uint32_t rest = nl - P.n_full * c.alpha;
-    launch_conv(rest, nx - rest, DC, dc_stride, EXT, ext_stride, up + P.n_full, FR, nd - P.n_full, c, batch);
+    launch_conv(rest, nx - rest, DC, dc_stride, EXT, ext_stride, up + P.n_full, P, nd - P.n_full, c, batch);
   }
   const uint64_t *KB = dptr<const uint64_t>(kk.b), *KA = dptr<const uint64_t>(kk.a);
   ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
@@ -2161,7 +2224,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
                                                                  P.pql, P.pql_sh, c.primes[lv]);
     rt.note_launch();
     ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.r_rows, P.r_rows, P.r_primes, batch, true);
-    launch_conv(c.spec.K + 1, lv, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.rd_jobs), FR, 2, c, batch);
+    launch_conv(c.spec.K + 1, lv, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.rd_jobs), P, 2, c, batch);
     MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pqinv), dptr<const uint64_t>(P.pqinv_sh),
               acc_stride, add_stride, out_stride, lv, nx};
     epi.ascale = dptr<const uint64_t>(P.qinv);
@@ -2172,7 +2235,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   }
   // ModDown: P rows -> coefficient form (in place), convert into Q_l, NTT, combine
   ntt_rows(c, ACC, acc_stride, ACC, acc_stride, P.p_rows, P.p_rows, P.p_primes, batch, true);
-  launch_conv(c.spec.K, nl, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), FR, 2, c, batch);
+  launch_conv(c.spec.K, nl, ACC, acc_stride, CV, cv_stride, dptr<const ConvJob>(P.down_jobs), P, 2, c, batch);
   // NTT of the converted rows with the ModDown combine fused into its last pass:
   // out_w = (acc_w - conv_w) * P^-1 (+ add_w), conv_w never stored
   const MdEpi epi{ACC, add0, add1, out, dptr<const uint64_t>(P.pinv), dptr<const uint64_t>(P.pinv_sh),

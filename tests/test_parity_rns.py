@@ -256,9 +256,10 @@ def test_conv_widths_mul_relin_and_rotate(s):
         assert np.array_equal(c.rotate(level, 3, _buf(a)).download(), O.rotate(s, level, 3, a)), level
 
 
-@pytest.mark.parametrize("mode", ["0"])
+@pytest.mark.parametrize("mode", ["0", "1"])
 def test_alu_conversion_option_matches_oracle(mode):
-    """HS_CONV_MMA=0 (the ALU/FP64 base conversion instead of the tensor-core one) gives the same limbs."""
+    """HS_CONV_MMA=0 (the ALU/FP64 base conversion) and =1 (the legacy mma.sync IMMA kernel) give the
+    same limbs as the default tcgen05 conversion and the oracle."""
     import os
     import subprocess
     import sys
