@@ -20,9 +20,11 @@
 //     thread owns one coefficient and gets a target's 8 byte-column sums in 8
 //     consecutive registers, so the recombination and the modular reduction run in
 //     registers and the store is a coalesced row segment.
-// Software pipeline, iteration j: store A(j+1) from the registers loaded during
-// iteration j-1, issue the global loads of tile j+2, barrier, MMA(j+1) (runs under
-// the epilogue), wait MMA(j), epilogue(j).  One __syncthreads per tile.
+// Warp roles: 16 compute warps and one MMA warp.  Compute warps, iteration j: store
+// A(j+1) from the registers loaded during iteration j-1, issue the global loads of
+// tile j+2, arrive on ready[(j+1) & 1]; wait full[j & 1]; epilogue(j).  The MMA warp:
+// wait ready[j & 1] (A(j) stored, and every epilogue of tile j-2 done with that
+// accumulator), issue MMA(j), commit to full[j & 1].  No CTA-wide barrier per tile.
 // The output is canonical, so it equals k_conv's / k_conv_mma's word for word.
 #pragma once
 
@@ -37,6 +39,24 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// polling with a back-off: a spinning warp would take issue slots from the compute warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase, uint32_t ns) {
+  while (!mbar_test(bar, phase)) __nanosleep(ns);
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   uint32_t ok = 0;
@@ -104,8 +124,15 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 }  // namespace tc
 
 constexpr int kTcRows = 128;      // coefficients per tile (MMA M)
-constexpr int kTcThreads = 512;   // 16 warps: 4 per TMEM lane quarter, 4 threads per A row
-constexpr int kTcParts = kTcThreads / kTcRows;
+constexpr int kTcCompute = 512;  // 16 compute warps: 4 per TMEM lane quarter, 4 threads per A row
+constexpr int kTcThreads = kTcCompute + 32;  // + the MMA-issuing warp
+constexpr int kTcParts = kTcCompute / kTcRows;
+
+struct TcTgt {
+  double qd, qinvd, c32d;  // fp targets: q, 1/q, 2^32 mod q
+  uint64_t off;            // output row offset (words) inside a batch item
+  uint32_t fp;
+};
 
 __host__ __device__ constexpr uint32_t tc_rows(uint32_t ntgt) { return (8 * ntgt + 15) / 16 * 16; }
 // two accumulators when they fit in TMEM's 512 columns (targets <= 32), else one (the next
@@ -131,9 +158,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
   extern __shared__ __align__(128) uint8_t tc_smem[];
   uint8_t* As = tc_smem;                            // [2][KC][128 rows][16 B]
   uint8_t* Bs = tc_smem + 2 * tc_smem_a<KS>();      // [KC][NR rows][16 B]
-  __shared__ __align__(8) uint64_t bars[3];          // 0: B landed; 1, 2: MMAs into accumulator 0, 1 done
+  __shared__ __align__(8) uint64_t bars[5];  // 0: B landed; 1, 2: full (MMAs done); 3, 4: ready (A stored)
   __shared__ uint32_t tslot;
-  __shared__ ConvTgt tgs[kMaxTgt];
+  __shared__ TcTgt tgs[kMaxTgt];
   __shared__ PrimeC tq[kMaxTgt];
   __shared__ uint64_t hinv_s[4 * KS], hinvsh_s[4 * KS], qs_s[4 * KS];
   const ConvJob& J = jobs[blockIdx.y];
@@ -143,10 +170,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
   if (t0 >= t1) return;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_b = tc::smem_u32(&bars[0]);
+  auto full = [&](uint32_t b) { return tc::smem_u32(&bars[1 + b]); };
+  auto ready = [&](uint32_t b) { return tc::smem_u32(&bars[3 + b]); };
   if (threadIdx.x == 0) {
     tc::mbar_init(bar_b, 1);
-    tc::mbar_init(tc::smem_u32(&bars[1]), 1);
-    tc::mbar_init(tc::smem_u32(&bars[2]), 1);
+    tc::mbar_init(full(0), 1);
+    tc::mbar_init(full(1), 1);
+    tc::mbar_init(ready(0), kTcCompute / 32);
+    tc::mbar_init(ready(1), kTcCompute / 32);
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(tc::smem_u32(&tslot), ncols);
@@ -154,7 +185,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
     const PrimeC P = pcs[J.tgt[k]];
     tq[k] = P;
     const uint64_t c32 = (uint64_t(1) << 32) % P.q;
-    tgs[k] = ConvTgt{P.qd, P.qinvd, static_cast<double>(c32), J.out_row + J.tgt_row[k], P.fp};
+    tgs[k] = TcTgt{P.qd, P.qinvd, static_cast<double>(c32), uint64_t(J.out_row + J.tgt_row[k]) << logN, P.fp};
   }
   if (threadIdx.x < nsrc) {
     hinv_s[threadIdx.x] = J.hinv[threadIdx.x];
@@ -165,12 +196,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tslot;
-  if (threadIdx.x == 0) {  // the job's B image: one bulk copy
-    const uint32_t bytes = KC * NR * 16;
-    tc::mbar_expect_tx(bar_b, bytes);
-    tc::bulk_g2s(tc::smem_u32(Bs), img + J.img_off, bytes, bar_b);
-  }
   const uint32_t tiles_per_item = 1u << (logN - 7);
+  auto issue = [&](uint32_t buf) {  // one thread: the tile's MMAs into accumulator `buf`
+    const uint32_t a0 = tc::smem_u32(As + buf * tc_smem_a<KS>()), b0 = tc::smem_u32(Bs);
+    for (uint32_t nb = 0; nb < NR; nb += 256) {
+      const uint32_t n = NR - nb < 256 ? NR - nb : 256;
+      const uint32_t id = tc::idesc_u8(n);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint64_t ad = tc::sdesc(a0 + 2 * ks * kTcRows * 16, kTcRows * 16, 128);
+        const uint64_t bd = tc::sdesc(b0 + 2 * ks * NR * 16 + nb * 16, NR * 16, 128);
+        tc::mma_u8(tmem + (dbuf ? buf * NR : 0) + nb, ad, bd, id, ks > 0 ? 1u : 0u);
+      }
+    }
+    tc::mma_commit(full(buf));
+  };
+  if (warp == kTcCompute / 32) {  // ---- the MMA warp ----
+    if (lane == 0) {
+      const uint32_t bytes = KC * NR * 16;  // the job's B image: one bulk copy
+      tc::mbar_expect_tx(bar_b, bytes);
+      tc::bulk_g2s(tc::smem_u32(Bs), img + J.img_off, bytes, bar_b);
+      tc::mbar_wait(bar_b, 0);
+      for (uint32_t j = 0; j < t1 - t0; ++j) {
+        tc::mbar_wait_sleep(ready(j & 1), (j >> 1) & 1, 32);
+        tc::fence_after();
+        issue(j & 1);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- compute warps ----
   // A rows: thread (row m, part p) owns chunks p, p + 4, ... of row m
   const uint32_t m = threadIdx.x & (kTcRows - 1), part = threadIdx.x / kTcRows;
   uint64_t x[CPT][2];
@@ -184,7 +238,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
       x[c][1] = kc < KC && i1 < nsrc ? __ldcs(I + (size_t(i1) << logN)) : 0;
     }
   };
-  auto store_a = [&](uint32_t buf) {
+  auto store_a = [&](uint32_t buf) {  // then this warp's arrival on ready[buf]
     uint8_t* A = As + buf * tc_smem_a<KS>();
 #pragma unroll
     for (uint32_t c = 0; c < CPT; ++c) {
@@ -196,91 +250,84 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(const uint64_t* in, s
           make_uint4(uint32_t(y0), uint32_t(y0 >> 32), uint32_t(y1), uint32_t(y1 >> 32));
     }
     tc::fence_async_smem();
-  };
-  auto issue = [&](uint32_t buf) {  // one thread: the tile's MMAs into accumulator `buf`
-    const uint32_t a0 = tc::smem_u32(As + buf * tc_smem_a<KS>()), b0 = tc::smem_u32(Bs);
-    for (uint32_t nb = 0; nb < NR; nb += 256) {
-      const uint32_t n = NR - nb < 256 ? NR - nb : 256;
-      const uint32_t id = tc::idesc_u8(n);
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const uint64_t ad = tc::sdesc(a0 + 2 * ks * kTcRows * 16, kTcRows * 16, 128);
-        const uint64_t bd = tc::sdesc(b0 + 2 * ks * NR * 16 + nb * 16, NR * 16, 128);
-        tc::mma_u8(tmem + (dbuf ? buf * NR : 0) + nb, ad, bd, id, ks > 0 ? 1u : 0u);
-      }
-    }
-    tc::mma_commit(tc::smem_u32(&bars[1 + buf]));
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(ready(buf));
   };
   // epilogue mapping: warp w reads TMEM lanes 32 (w & 3) .. + 31; the four warps of a lane
   // quarter take targets g, g + 4, ... (g = w >> 2)
   const uint32_t q4 = warp & 3, grp = warp >> 2;
-  auto finish = [&](uint64_t* O, uint32_t t, const uint32_t (&v)[8]) {
-    const uint64_t lo = uint64_t(v[0]) + (uint64_t(v[1]) << 8) + (uint64_t(v[2]) << 16) + (uint64_t(v[3]) << 24);
-    const uint64_t hi = uint64_t(v[4]) + (uint64_t(v[5]) << 8) + (uint64_t(v[6]) << 16) + (uint64_t(v[7]) << 24);
-    const ConvTgt T = tgs[t];
-    uint64_t r;
-    if (T.fp) {  // lo + hi (2^32 mod q) on the FP64 pipe: lo, hi < 2^47, every step exact
-      const double hh = fp_mulmod(u2d(hi), T.c32d, T.qd, T.qinvd);
-      r = fp_canon(__dadd_rn(hh, u2d(lo)), T.qd, T.qinvd);
-    } else {
-      r = reduce128((static_cast<u128>(hi) << 32) + lo, tq[t]);
-    }
-    __stcs(O + (size_t(T.orow) << logN), r);
+  // lo = sum_{b<4} v_b 2^(8b), hi = sum_{b>=4} v_b 2^(8(b-4)), each < 2^47 (v_b < 2^23)
+  auto lohi = [](const uint32_t (&v)[8], uint64_t& lo, uint64_t& hi) {
+    lo = (uint64_t(v[2] + (v[3] << 8)) << 16) + (v[0] + (v[1] << 8));
+    hi = (uint64_t(v[6] + (v[7] << 8)) << 16) + (v[4] + (v[5] << 8));
   };
-  // prologue: A(t0) stored, MMA(t0) issued, loads of t0 + 1 in flight
+  auto fin_int = [&](uint64_t* O, uint32_t t, const uint32_t (&v)[8]) {
+    uint64_t lo, hi;
+    lohi(v, lo, hi);
+    __stcs(O + tgs[t].off, reduce128((static_cast<u128>(hi) << 32) + lo, tq[t]));
+  };
+  // targets < 2^45: lo + hi (2^32 mod q) on the FP64 pipe, every step exact
+  auto fin_fp = [&](uint64_t* O, uint32_t t, const uint32_t (&v)[8]) {
+    uint64_t lo, hi;
+    lohi(v, lo, hi);
+    const TcTgt T = tgs[t];
+    const double hh = fp_mulmod(u2d(hi), T.c32d, T.qd, T.qinvd);
+    __stcs(O + T.off, fp_canon(__dadd_rn(hh, u2d(lo)), T.qd, T.qinvd));
+  };
+  const uint32_t nint = J.nint;
+  // prologue: A(t0) stored (ready[0]), loads of t0 + 1 in flight
   load(t0);
   store_a(0);
   if (t0 + 1 < t1) load(t0 + 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tc::mbar_wait(bar_b, 0);
-    tc::fence_after();
-    issue(0);
-  }
 #pragma unroll 1
   for (uint32_t tile = t0, j = 0; tile < t1; ++tile, ++j) {
     const uint32_t buf = j & 1;
-    if (tile + 1 < t1) {
+    if (tile + 1 < t1 && dbuf) {
       store_a(buf ^ 1);                  // the loads issued one iteration ago
       if (tile + 2 < t1) load(tile + 2);  // in flight during this epilogue
     }
-    tc::fence_before();
-    __syncthreads();  // A(j+1) complete; epilogue(j-1)'s TMEM reads of accumulator buf ^ 1 done
-    if (dbuf && threadIdx.x == 0 && tile + 1 < t1) {
-      tc::fence_after();
-      issue(buf ^ 1);
-    }
-    __syncwarp();
-    tc::mbar_wait(tc::smem_u32(&bars[1 + buf]), (j >> 1) & 1);
+    tc::mbar_wait_sleep(full(buf), (j >> 1) & 1, 64);
     tc::fence_after();
     const uint32_t item = tile / tiles_per_item, n0 = (tile % tiles_per_item) * kTcRows;
     uint64_t* O = out + item * out_stride + n0 + 32 * q4 + lane;
     const uint32_t taddr = tmem + ((32 * q4) << 16) + (dbuf ? buf * NR : 0);
+    // integer targets first (at most a few), then the FP64 ones four at a time, branch-free
     uint32_t t = grp;
 #pragma unroll 1
-    for (; t + 4 < ntgt; t += 8) {  // two targets' loads in flight per wait
-      uint32_t v0[8], v1[8];
-      tc::tmem_ld8(taddr + 8 * t, v0);
-      tc::tmem_ld8(taddr + 8 * (t + 4), v1);
-      tc::tmem_wait_ld();
-      finish(O, t, v0);
-      finish(O, t + 4, v1);
-    }
-    if (t < ntgt) {
+    for (; t < nint; t += 4) {
       uint32_t v0[8];
       tc::tmem_ld8(taddr + 8 * t, v0);
       tc::tmem_wait_ld();
-      finish(O, t, v0);
+      fin_int(O, t, v0);
     }
-    if (!dbuf && tile + 1 < t1) {  // one accumulator: the next MMAs after this epilogue
-      tc::fence_before();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tc::fence_after();
-        issue(buf ^ 1);
-      }
+    t = nint + grp;
+#pragma unroll 1
+    for (; t + 12 < ntgt; t += 16) {
+      uint32_t v0[8], v1[8], v2[8], v3[8];
+      tc::tmem_ld8(taddr + 8 * t, v0);
+      tc::tmem_ld8(taddr + 8 * (t + 4), v1);
+      tc::tmem_ld8(taddr + 8 * (t + 8), v2);
+      tc::tmem_ld8(taddr + 8 * (t + 12), v3);
+      tc::tmem_wait_ld();
+      fin_fp(O, t, v0);
+      fin_fp(O, t + 4, v1);
+      fin_fp(O, t + 8, v2);
+      fin_fp(O, t + 12, v3);
+    }
+#pragma unroll 1
+    for (; t < ntgt; t += 4) {
+      uint32_t v0[8];
+      tc::tmem_ld8(taddr + 8 * t, v0);
+      tc::tmem_wait_ld();
+      fin_fp(O, t, v0);
+    }
+    if (tile + 1 < t1 && !dbuf) {  // one accumulator: A(j+1) and its MMAs after this epilogue
+      store_a(buf ^ 1);
+      if (tile + 2 < t1) load(tile + 2);
     }
   }
+  }  // compute warps
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);

@@ -1021,6 +1021,7 @@ struct ConvJob {
   uint32_t in_row, out_row;  // first source row / row base of the outputs, per batch item
   uint32_t frag_off;  // B fragments of k_conv_mma (uint2 index into the plan's table)
   uint32_t img_off;   // B image of k_conv_tc (byte offset into the plan's image table)
+  uint32_t nint;      // targets [0, nint) are >= 2^45 (integer reduction), the rest take the FP64 path
   uint8_t src[kMaxSrc], tgt[kMaxTgt], tgt_row[kMaxTgt];
   uint64_t hinv[kMaxSrc], hinv_sh[kMaxSrc];
   uint64_t h[kMaxTgt][kMaxSrc];
@@ -1814,9 +1815,19 @@ void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out) {
 
 namespace {
 
-void fill_conv(const Ctx& c, const std::vector<uint32_t>& src, const std::vector<uint32_t>& tgt,
-               const std::vector<uint32_t>& tgt_row, uint32_t in_row, uint32_t out_row, ConvJob* cv) {
+void fill_conv(const Ctx& c, const std::vector<uint32_t>& src, const std::vector<uint32_t>& tgt_in,
+               const std::vector<uint32_t>& tgt_row_in, uint32_t in_row, uint32_t out_row, ConvJob* cv) {
   std::memset(cv, 0, sizeof *cv);
+  // targets >= 2^45 first (k_conv_tc's epilogue runs the two reductions as separate
+  // branch-free loops); tgt_row keeps every output where it belongs
+  std::vector<uint32_t> tgt, tgt_row;
+  for (int pass = 0; pass < 2; ++pass)
+    for (size_t t = 0; t < tgt_in.size(); ++t)
+      if ((c.pc[tgt_in[t]].fp == 0) == (pass == 0)) {
+        tgt.push_back(tgt_in[t]);
+        tgt_row.push_back(tgt_row_in[t]);
+        if (pass == 0) ++cv->nint;
+      }
   cv->nsrc = static_cast<uint32_t>(src.size());
   cv->ntgt = static_cast<uint32_t>(tgt.size());
   cv->in_row = in_row;
