@@ -1284,8 +1284,15 @@ __global__ void __launch_bounds__(kConvMmaRows, 6) k_conv_mma(const uint64_t* in
 // e_j[x] = d[x] on digit j's own rows (NTT form, never converted), ext_j[x] elsewhere.
 // Each thread holds its key words and walks the whole batch.
 constexpr int kMaxDigits = 15;
+#ifndef HS_INNER_MINB
+#define HS_INNER_MINB 4  // 64 registers, 4 blocks per SM (3 at 80 registers: 5 % slower HMult)
+#endif
+#ifndef HS_INNER_UNROLL
+#define HS_INNER_UNROLL 2
+#endif
+constexpr int kInnerUnroll = HS_INNER_UNROLL;  // batch items in flight per thread
 template <int ND>
-__global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext_stride, const uint64_t* d,
+__global__ void __launch_bounds__(kT, HS_INNER_MINB) k_ks_inner(const uint64_t* ext, size_t ext_stride, const uint64_t* d,
                                                  size_t d_stride, uint64_t* acc, size_t acc_stride,
                                                  const uint64_t* kb, const uint64_t* ka, const PrimeC* pcs,
                                                  uint32_t nx, uint32_t nl, uint32_t np, uint32_t nq, uint32_t alpha,
@@ -1313,7 +1320,7 @@ __global__ void __launch_bounds__(kT) k_ks_inner(const uint64_t* ext, size_t ext
     if (src.mode == KS_PERM) return src.a[b * src.stride + (size_t(nl + row) << logN) + galois_src(n, src.g, logN)];
     return d[b * d_stride + x];
   };
-#pragma unroll 2
+#pragma unroll(kInnerUnroll)
   for (uint32_t b = 0; b < batch; ++b) {
     const uint64_t* E = ext + b * ext_stride + x;
     uint64_t e[ND];
