@@ -726,6 +726,68 @@ def main():
     _abi.lib().hs_diag_fp64_rate(0, ctypes.byref(rate))
     peak = rate.value / 1e12
 
+    # ---- debug_checks = true (the reference CLI's / acceptance runner's default): checked fusion ----
+    # (device predicates + one 4-byte flag read per call) vs the op-by-op debug path (set_fused(False))
+    ctxd = H.EvalContext(H.CkksParams(slot_count=S, debug_checks=True), rng_seed=rank)
+    refd = oracle().stat(Params(slot_count=S, debug_checks=True), ST_ZNORM, x, B)
+
+    def debug_loop(reps):
+        for i in range(2):
+            H.znorm(ctxd, pool[i % POOL], B)
+        barrier_sync()
+        l0 = H.kernel_launches()
+        t0_ = time.perf_counter()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for i in range(reps):
+            zc = H.znorm(ctxd, pool[i % POOL], B)
+        d1.record(stream)
+        barrier_sync()
+        zz = H.decode_column(ctxd, H.znorm(ctxd, pool[0], B))
+        return (1e3 * (time.perf_counter() - t0_) / reps, d0.elapsed_time(d1) / reps,
+                (H.kernel_launches() - l0) / (reps + 1), bool(np.array_equal(bits(zz), bits(refd.out))))
+
+    dbg_wall, dbg_dev, dbg_launch, dbg_ok = debug_loop(50)
+    H.set_fused(False)
+    obo_wall, obo_dev, obo_launch, obo_ok = debug_loop(3)
+    H.set_fused(True)
+    debug_line = {"metric": "C2 znorm with debug_checks=true, ms per call (public API, host-timed)",
+                  "checked_fusion": {"wall_ms": dbg_wall, "device_ms": dbg_dev, "launches_per_call": dbg_launch,
+                                     "matches_oracle": dbg_ok},
+                  "op_by_op": {"wall_ms": obo_wall, "device_ms": obo_dev, "launches_per_call": obo_launch,
+                               "matches_oracle": obo_ok},
+                  "note": "checked fusion: the reference's value checks as device predicates in the one "
+                          "statistics kernel, one 4-byte flag read per call; a failing check replays the call op "
+                          "by op (the reference's error and meter)"}
+
+    # ---- C4: all 28 Pearson pairs of 8 columns (reference semantics: 28 pearson calls) ----------
+    cols8 = W.c4_table(H.synthetic_uniform)  # 8 x 32768, pairwise rho 0.6 (seeded)
+    c4_line = None
+    if True:
+        ctx4 = H.EvalContext(H.CkksParams(slot_count=S), rng_seed=rank)
+        enc8 = [H.encode_column(ctx4, c) for c in cols8]
+        pairs = [(i, j) for i in range(8) for j in range(i + 1, 8)]
+        for i, j in pairs[:3]:
+            H.pearson(ctx4, enc8[i], enc8[j], 20.0)
+        H.sync()
+        with H.Graph() as g4:  # outputs freed inside the graph (a graph's live allocations block a relaunch)
+            for i, j in pairs:
+                r4 = H.pearson(ctx4, enc8[i], enc8[j], 20.0)
+                del r4
+        g4.launch()
+        barrier_sync()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        g4.launch()
+        c1.record(stream)
+        barrier_sync()
+        r01 = float(ctx4.decrypt(H.pearson(ctx4, enc8[0], enc8[1], 20.0), 1)[0])
+        from oracle_abi import ST_PEARSON
+        refp = oracle().stat(Params(slot_count=S), ST_PEARSON, cols8[0], 20.0, y=cols8[1])
+        c4_line = {"metric": "C4: 28 Pearson pairs of 8 x 32768 columns, device ms per table (graph replay)",
+                   "value": c0.elapsed_time(c1), "unit": "ms", "B": 20.0, "rho": 0.6,
+                   "pair01_matches_oracle": bool(np.array_equal(bits(np.array([r01])), bits(refp.out[:1])))}
+
     # ---- max over ranks ---------------------------------------------------------------------------
     t = torch.tensor([dev_ms, e2e_ms, seq_ms], dtype=torch.float64, device="cuda")
     if ws > 1:
@@ -769,7 +831,10 @@ def main():
             "kernels_us": {"moments_stat_kernel": mom_us, "invsqrt_prog_kernel": prog_us,
                            "note": "graph replay per call, includes ~1-2 us node overhead"},
             "clocks": clk.summary(),
+            "debug_checks": debug_line,
         }
+        if c4_line is not None:
+            line["c4_pearson_table"] = c4_line
         c5 = c5_tier_e(torch, stream, S, args.batch, ops=("mul_ct", "add", "mul_pt", "rotate_1"))
         line["c5_tier_e"] = {"metric": "mul_ct/s (batch of 64 x 2^15 slots)", "value": c5["mul_ct"]["ops_per_s"],
                              "unit": "mul_ct/s", "ops": c5,

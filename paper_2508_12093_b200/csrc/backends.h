@@ -98,8 +98,10 @@ class SymB : public LedgerBase<SymB, SymCt> {
     for (size_t step = 1; step < p_.S; step <<= 1) acc = add_ct(acc, rotate(acc, static_cast<long>(step)));
     return acc;
   }
-  // value checks never run symbolically (debug mode executes on DevB)
-  double first_slot(const C&) { fail(HS_E_ERROR, "internal: value peek on the symbolic ledger"); }
+  // value checks never run symbolically: with debug_checks the fused kernels evaluate them on
+  // the device (pipelines.cu checked()); the ledger assumes they pass (1.0 passes every
+  // first-slot predicate for B >= 2^-15; a failing one throws and the call replays op by op)
+  double first_slot(const C&) { return 1.0; }
   void check_open_domain(const C&, size_t, double, double, const char*) {}
   void check_eval_domain(const C&, double, double) {}
   void check_divergence(const C&, size_t) {}

@@ -60,11 +60,23 @@ enum MOp : int {
   M_CHEB,     // r[dst] = ChebEncryptedEval(table @ i0, degree i1) on r[a]
   M_NEWTON,   // r[dst] = newton_loop(x_op = r[a], y = r[b], n = i0, iters = i1, (n+1)/n = c)
   M_ZAPPLY,   // for every chunk: zout[c][slot] = out(mul(sub(in(zin[c][slot]), r[a]), r[b]))
-  M_LDR       // r[dst] = per-slot statistic value i0 (stat.cu: 0 mu_x, 1 var_x, 2 mu_y, 3 var_y, 4 num)
+  M_LDR,      // r[dst] = per-slot statistic value i0 (stat.cu: 0 mu_x, 1 var_x, 2 mu_y, 3 var_y, 4 num)
+  M_CHK       // debug_checks value check of r[a] (real units) on slots < i1, kind i0, constants c, c2:
+              // a failing slot sets *Prog::flags (the host then replays the call op by op)
+};
+// M_CHK kinds: the reference's debug predicates, evaluated with the same fp64 operations
+enum ChkKind : int {
+  CK_OPEN = 0,       // fail if !(v > c) || !(v <= c2)          check_open_domain, primitives.hpp:134-144
+  CK_RANGE = 1,      // fail if v < c || v > c2                  eval_encrypted / sqrt / sign domains
+  CK_LT = 2,         // fail if v < c                            moments: negative variance, stats.hpp:144
+  CK_SCALED_LT = 3,  // fail if (v * c) * c < c2                 variance below 1e-9 (B^2-scaled), stats.hpp:156
+  CK_ABS_LT = 4      // fail if |v| < c                          coeff_variation near-zero mean, stats.hpp:221
 };
 struct MInst {
   int op, dst, a, b, i0, i1;
   double c;
+  int i2 = 0;      // M_NEWTON: divergence check on slots < i2 after every iteration (0 = none)
+  double c2 = 0.0;
 };
 constexpr int kMaxInst = 40;
 constexpr int kMaxArr = 6;
@@ -82,6 +94,7 @@ struct Prog {
   unsigned S = 0;
   int ntab = 0;                  // doubles of coefficient tables, staged into shared memory
   const double* tabs = nullptr;  // coefficient tables (device); M_CHEB i0 = offset, b = lane-split
+  unsigned* flags = nullptr;     // debug_checks: set nonzero by any failing M_CHK / Newton guard
   MInst ins[kMaxInst];
   const double* in[kMaxArr];
   double* out[kMaxArr];

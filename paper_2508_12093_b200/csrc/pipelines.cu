@@ -4,6 +4,7 @@
 #include "pipelines.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 #include <cstring>
 #include <map>
@@ -34,9 +35,28 @@ bool ct_ok(const Params& p, const Ct& c) {
   return c && c->n == p.S && (!p.quantize || (c->grid == p.scale_bits && p.scale_bits <= kMaxFusedScaleBits));
 }
 
+// debug_checks (HS_DEBUG_FUSED, default 1): "checked fusion" -- the fused kernels evaluate the
+// reference's value checks as device predicates (M_CHK, the Newton guard); when any fails, the
+// call is replayed op by op (DevB), which raises the reference's error at the reference's op with
+// the reference's meter.  The checks never steer the computation, so a clean run's outputs,
+// levels and meter are exactly the op-by-op ones.  Graph capture cannot read the flags back: a
+// debug call while capturing takes the op-by-op path as before.
+bool debug_fused() {
+  static const bool on = [] {
+    const char* e = std::getenv("HS_DEBUG_FUSED");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+bool mode_ok(const Params& p) {
+  Runtime& rt = Runtime::get();
+  if (!rt.fused) return false;
+  return !p.debug || (debug_fused() && !rt.capturing());
+}
+
 bool fusable(const hs_ctx* ctx, std::initializer_list<const Ct*> cts) {
   const Params& p = ctx->p;
-  if (p.debug || !Runtime::get().fused) return false;
+  if (!mode_ok(p)) return false;
   if (p.S > (1u << 30)) return false;
   for (const Ct* c : cts)
     if (!ct_ok(p, *c)) return false;
@@ -45,7 +65,7 @@ bool fusable(const hs_ctx* ctx, std::initializer_list<const Ct*> cts) {
 
 bool col_ok(const hs_ctx* ctx, const ColC& col) {
   const Params& p = ctx->p;
-  if (p.debug || !Runtime::get().fused) return false;
+  if (!mode_ok(p)) return false;
   if (col.chunks.empty() || col.chunks.size() > static_cast<size_t>(k::kMaxChunks)) return false;
   if (p.S > (1u << 24)) return false;
   for (const Ct& c : col.chunks)
@@ -178,6 +198,34 @@ auto ledger(hs_ctx* ctx, const Key& key, F&& f) {
   }
 }
 
+// ---- checked fusion (debug_checks) -------------------------------------------------
+unsigned* debug_flag_word() { return reinterpret_cast<unsigned*>(Runtime::get().scratch(2, 1)); }
+
+bool checks_failed() {
+  Runtime& rt = Runtime::get();
+  unsigned h = 0;
+  cuda_ok(cudaMemcpyAsync(&h, debug_flag_word(), sizeof h, cudaMemcpyDeviceToHost, rt.stream()), "debug flags");
+  cuda_ok(cudaStreamSynchronize(rt.stream()), "debug flags");
+  return h != 0;
+}
+
+// Run the fused body; with debug_checks on, a failed device check (or a ledger error, whose
+// place relative to the value checks only the op-by-op order decides) restores the meter and
+// replays the call op by op, which raises exactly where the reference raises.
+template <class Body, class Fallback>
+auto checked(hs_ctx* ctx, Body&& body, Fallback&& fallback) -> decltype(body()) {
+  if (!ctx->p.debug) return body();
+  const Meter m0 = ctx->m;
+  try {
+    auto out = body();
+    if (!checks_failed()) return out;
+  } catch (const Error& e) {
+    if (e.code == HS_E_CUDA) throw;
+  }
+  ctx->m = m0;
+  return fallback();
+}
+
 // ---- per-slot program builder ---------------------------------------------------
 class PB {
  public:
@@ -200,6 +248,10 @@ class PB {
     return emit(k::M_CONST, reg(), 0, 0, 0, 0, u);
   }
   int ldr(int k) { return emit(k::M_LDR, reg(), 0, 0, k, 0, 0.0); }  // per-slot statistic value
+  // debug_checks: the reference's value check of register r on slots [0, n_valid) (no-op otherwise)
+  void check(int r, k::ChkKind kind, size_t n_valid, double c, double c2 = 0.0) {
+    if (p_.debug) emit(k::M_CHK, -1, r, 0, kind, lim(n_valid), c, 0, c2);
+  }
   int add(int a, int b) { return emit(k::M_ADD, reg(), a, b, 0, 0, 0.0); }
   int sub(int a, int b) { return emit(k::M_SUB, reg(), a, b, 0, 0, 0.0); }
   int mul(int a, int b) { return emit(k::M_MUL, reg(), a, b, 0, 0, 0.0); }
@@ -211,6 +263,7 @@ class PB {
   // eval_encrypted (chebyshev.hpp:171-189); bootstraps are value-identities here.
   // The table offset (i0) and lane-split flag (b) are patched in launch().
   int cheb(int x, const Series& s) {
+    check(x, k::CK_RANGE, p_.S, s.lo - 1e-9, s.hi + 1e-9);  // chebyshev.hpp:174-179 (every slot)
     if (!s.native()) {
       const double span = s.hi - s.lo;
       x = addc(mulc(x, 2.0 / span), -(s.lo + s.hi) / span);
@@ -220,9 +273,9 @@ class PB {
     return emit(k::M_CHEB, reg(), x, 0, 0, s.degree(), 0.0);
   }
   // newton_loop (primitives.hpp:105-132)
-  int newton(int x, int y, int n, int iters) {
+  int newton(int x, int y, int n, int iters, size_t n_valid = flow::kAllSlots) {
     if (iters <= 0) return y;
-    return emit(k::M_NEWTON, reg(), x, y, n, iters, (n + 1.0) / n);
+    return emit(k::M_NEWTON, reg(), x, y, n, iters, (n + 1.0) / n, p_.debug ? lim(n_valid) : 0);
   }
   void zapply(int mu, int inv, const std::vector<Ct>& in, const std::vector<DevBuf>& out) {
     prog_.nchunks = static_cast<int>(in.size());
@@ -234,27 +287,31 @@ class PB {
   }
 
   // ---- composite primitives -------------------------------------------------------
-  int baseline(int t, double S, int iters) {  // primitives.hpp:173-184
+  int baseline(int t, double S, int iters, size_t nv = flow::kAllSlots) {  // primitives.hpp:173-184
+    check(t, k::CK_OPEN, nv, 0.0, 1.0);
     int y = cnst(1.0);
-    if (iters > 0) y = newton(mulc(t, 0.5), y, 2, iters);
+    if (iters > 0) y = newton(mulc(t, 0.5), y, 2, iters, nv);
     return mulc(y, 1.0 / std::sqrt(S));
   }
-  int invsqrt(int t, double S, const InvCfg& cfg) {  // primitives.hpp:186-208
-    if (cfg.baseline_mode) return baseline(t, S, cfg.effective_baseline_iters());
+  int invsqrt(int t, double S, const InvCfg& cfg, size_t nv = flow::kAllSlots) {  // primitives.hpp:186-208
+    if (cfg.baseline_mode) return baseline(t, S, cfg.effective_baseline_iters(), nv);
+    check(t, k::CK_OPEN, nv, 0.0, 2.0);
     const Series seed = fit_scaled(TargetKind::InvSqrtShifted, S, cfg.cheb_degree);
     int y = cheb(addc(t, -1.0), seed);
-    if (cfg.newton_iters > 0) y = newton(mulc(t, S / 2.0), y, 2, cfg.newton_iters);
+    if (cfg.newton_iters > 0) y = newton(mulc(t, S / 2.0), y, 2, cfg.newton_iters, nv);
     return y;
   }
-  int inv(int t, double S, const InvCfg& cfg) {  // primitives.hpp:211-217
-    const int y = invsqrt(t, S, cfg);
+  int inv(int t, double S, const InvCfg& cfg, size_t nv = flow::kAllSlots) {  // primitives.hpp:211-217
+    const int y = invsqrt(t, S, cfg, nv);
     return mul(y, y);
   }
-  int sqrt_(int t, double S, int degree) {  // primitives.hpp:222-238
+  int sqrt_(int t, double S, int degree, size_t nv = flow::kAllSlots) {  // primitives.hpp:222-238
+    check(t, k::CK_RANGE, nv, -1e-9, 2.0 + 1e-9);
     const Series s = fit_scaled(TargetKind::SqrtShifted, S, degree);
     return cheb(addc(t, -1.0), s);
   }
   int sign(int x, const SignCfg& cfg) {  // primitives.hpp:279-300
+    check(x, k::CK_RANGE, p_.S, -1.0 - 1e-9, 1.0 + 1e-9);
     const std::vector<Series> st = sign_stages(cfg.mode, cfg.custom_polys);
     int y = x;
     for (int f = 0; f < cfg.folds; ++f) y = cheb(y, st[static_cast<size_t>(f) % st.size()]);
@@ -301,6 +358,10 @@ class PB {
     static int nl = 0;
     auto l0 = std::chrono::steady_clock::now();
 #endif
+    if (p_.debug) {  // checked fusion: arm the flag word (read back by checks_failed())
+      prog_.flags = debug_flag_word();
+      cuda_ok(cudaMemsetAsync(prog_.flags, 0, sizeof(unsigned), rt.stream()), "debug flags");
+    }
     if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
     else k::run_prog(q_, prog_, lanes, rt.stream());
 #ifdef HS_HOST_PROFILE
@@ -313,11 +374,12 @@ class PB {
     if (nreg_ >= k::kRegs) fail(HS_E_ERROR, "fused program: register file exhausted");
     return nreg_++;
   }
-  int emit(int op, int dst, int a, int b, int i0, int i1, double c) {
+  int emit(int op, int dst, int a, int b, int i0, int i1, double c, int i2 = 0, double c2 = 0.0) {
     if (prog_.n >= k::kMaxInst) fail(HS_E_ERROR, "fused program: too many instructions");
-    prog_.ins[prog_.n++] = k::MInst{op, dst, a, b, i0, i1, c};
+    prog_.ins[prog_.n++] = k::MInst{op, dst, a, b, i0, i1, c, i2, c2};
     return dst;
   }
+  int lim(size_t n_valid) const { return static_cast<int>(std::min(n_valid, p_.S)); }
 
   struct TableSet {
     DevBuf dev;
@@ -405,135 +467,179 @@ Ct make_out(hs_ctx* ctx, const DevBuf& b, int level) { return ct_device(b, ctx->
 }  // namespace
 
 // =====================================================================================
+// Every entry point: the op-by-op path `dev` when the call is not fusable, else the fused
+// launch, wrapped by checked() (debug_checks: device predicates + op-by-op replay on failure).
 Ct eval_encrypted(hs_ctx* ctx, const Series& s, const Ct& ct) {
-  if (!fusable(ctx, {&ct}) || s.coeffs.empty() || !degree_ok(s.degree())) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::eval_encrypted(db, s, ct);
-  }
-  auto [r, m] = ledger(ctx, Key("eval", ctx->p).ct(ct).add(s.degree()).add(s.lo).add(s.hi), [&](SymB& sb) { return flow::eval_encrypted(sb, s, sym(ct)); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.cheb(pb.ld(ct), s), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct}) || s.coeffs.empty() || !degree_ok(s.degree())) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("eval", ctx->p).ct(ct).add(s.degree()).add(s.lo).add(s.hi),
+                         [&](SymB& sb) { return flow::eval_encrypted(sb, s, sym(ct)); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.cheb(pb.ld(ct), s), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct newton_loop(hs_ctx* ctx, const Ct& x_op, const Ct& y, int n, int iters, size_t n_valid) {
-  if (!fusable(ctx, {&x_op, &y}) || n < 1 || n > k::kMaxFusedNewtonN) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::newton_loop(db, x_op, y, n, iters, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("newton_loop", ctx->p).ct(x_op).ct(y).add(n).add(iters).add(n_valid), [&](SymB& sb) { return flow::newton_loop(sb, sym(x_op), sym(y), n, iters, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  const int xr = pb.ld(x_op);
-  pb.st(pb.newton(xr, pb.ld(y), n, iters), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&x_op, &y}) || n < 1 || n > k::kMaxFusedNewtonN) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("newton_loop", ctx->p).ct(x_op).ct(y).add(n).add(iters).add(n_valid),
+                         [&](SymB& sb) { return flow::newton_loop(sb, sym(x_op), sym(y), n, iters, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    const int xr = pb.ld(x_op);
+    pb.st(pb.newton(xr, pb.ld(y), n, iters, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct newton_refine(hs_ctx* ctx, const Ct& x, const Ct& y0, int n, int iters, size_t n_valid) {
-  if (!fusable(ctx, {&x, &y0}) || n < 1 || n > k::kMaxFusedNewtonN) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::newton_refine(db, x, y0, n, iters, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("newton_refine", ctx->p).ct(x).ct(y0).add(n).add(iters).add(n_valid), [&](SymB& sb) { return flow::newton_refine(sb, sym(x), sym(y0), n, iters, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  int xr = pb.ld(x);
-  const int yr = pb.ld(y0);
-  if (n >= 2) xr = pb.mulc(xr, 1.0 / n);
-  pb.st(pb.newton(xr, yr, n, iters), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&x, &y0}) || n < 1 || n > k::kMaxFusedNewtonN) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("newton_refine", ctx->p).ct(x).ct(y0).add(n).add(iters).add(n_valid),
+                         [&](SymB& sb) { return flow::newton_refine(sb, sym(x), sym(y0), n, iters, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    int xr = pb.ld(x);
+    const int yr = pb.ld(y0);
+    if (n >= 2) xr = pb.mulc(xr, 1.0 / n);
+    pb.st(pb.newton(xr, yr, n, iters, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct crypto_invsqrt(hs_ctx* ctx, const Ct& ct, double S, const InvCfg& cfg, size_t n_valid) {
-  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::crypto_invsqrt(db, ct, S, cfg, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("invsqrt", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid), [&](SymB& sb) { return flow::crypto_invsqrt(sb, sym(ct), S, cfg, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.invsqrt(pb.ld(ct), S, cfg), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("invsqrt", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid),
+                         [&](SymB& sb) { return flow::crypto_invsqrt(sb, sym(ct), S, cfg, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.invsqrt(pb.ld(ct), S, cfg, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct baseline_invsqrt(hs_ctx* ctx, const Ct& ct, double S, int iters, size_t n_valid) {
-  if (!fusable(ctx, {&ct})) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::baseline_invsqrt(db, ct, S, iters, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("baseline", ctx->p).ct(ct).add(S).add(iters).add(n_valid), [&](SymB& sb) { return flow::baseline_invsqrt(sb, sym(ct), S, iters, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.baseline(pb.ld(ct), S, iters), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct})) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("baseline", ctx->p).ct(ct).add(S).add(iters).add(n_valid),
+                         [&](SymB& sb) { return flow::baseline_invsqrt(sb, sym(ct), S, iters, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.baseline(pb.ld(ct), S, iters, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct crypto_inv(hs_ctx* ctx, const Ct& ct, double S, const InvCfg& cfg, size_t n_valid) {
-  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::crypto_inv(db, ct, S, cfg, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("inv", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid), [&](SymB& sb) { return flow::crypto_inv(sb, sym(ct), S, cfg, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.inv(pb.ld(ct), S, cfg), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct}) || !cfg_ok(cfg)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("inv", ctx->p).ct(ct).add(S).cfg(cfg).add(n_valid),
+                         [&](SymB& sb) { return flow::crypto_inv(sb, sym(ct), S, cfg, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.inv(pb.ld(ct), S, cfg, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct crypto_sqrt(hs_ctx* ctx, const Ct& ct, double S, int degree, size_t n_valid) {
-  if (!fusable(ctx, {&ct}) || !degree_ok(degree)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::crypto_sqrt(db, ct, S, degree, n_valid);
-  }
-  auto [r, m] = ledger(ctx, Key("sqrt", ctx->p).ct(ct).add(S).add(degree).add(n_valid), [&](SymB& sb) { return flow::crypto_sqrt(sb, sym(ct), S, degree, n_valid); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.sqrt_(pb.ld(ct), S, degree), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct}) || !degree_ok(degree)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("sqrt", ctx->p).ct(ct).add(S).add(degree).add(n_valid),
+                         [&](SymB& sb) { return flow::crypto_sqrt(sb, sym(ct), S, degree, n_valid); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.sqrt_(pb.ld(ct), S, degree, n_valid), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct crypto_sign(hs_ctx* ctx, const Ct& ct, const SignCfg& cfg) {
-  if (!fusable(ctx, {&ct}) || !sign_ok(cfg) || cfg.folds > 24) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::crypto_sign(db, ct, cfg);
-  }
-  auto [r, m] = ledger(ctx, Key("sign", ctx->p).ct(ct).sign(cfg), [&](SymB& sb) { return flow::crypto_sign(sb, sym(ct), cfg); });
-  PB pb(ctx->p);
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  pb.st(pb.sign(pb.ld(ct), cfg), out.get());
-  pb.launch();
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!fusable(ctx, {&ct}) || !sign_ok(cfg) || cfg.folds > 24) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("sign", ctx->p).ct(ct).sign(cfg),
+                         [&](SymB& sb) { return flow::crypto_sign(sb, sym(ct), cfg); });
+    PB pb(ctx->p);
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    pb.st(pb.sign(pb.ld(ct), cfg), out.get());
+    pb.launch();
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 // ---- statistics ---------------------------------------------------------------------------
+// moments() debug checks (stats.hpp:144-146, 156-158, ...): slot 0 of the scaled variance
+void check_var(PB& pb, int var, double B, bool scaled_check) {
+  pb.check(var, k::CK_LT, 1, -1e-9);                        // moments: negative scaled variance
+  if (scaled_check) pb.check(var, k::CK_SCALED_LT, 1, B, 1e-9);  // (var * B) * B < 1e-9
+}
+
 Ct mean_scaled(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::mean_scaled(db, col, B);
-  }
-  auto [r, m] = ledger(ctx, Key("mean", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::mean_scaled(sb, sym(col), B); });
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  PB pb(ctx->p);
-  pb.st(pb.ldr(0), out.get());
-  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_MEAN, B, 1.0));
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!col_ok(ctx, col)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("mean", ctx->p).col(col).add(B),
+                         [&](SymB& sb) { return flow::mean_scaled(sb, sym(col), B); });
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    PB pb(ctx->p);
+    pb.st(pb.ldr(0), out.get());
+    pb.launch_stat(stat_args(ctx, {&col}, k::MOM_MEAN, B, 1.0));
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 static Ct variance_impl(hs_ctx* ctx, const ColC& col, double S, const Key& key, bool scaled, double B) {
@@ -549,141 +655,151 @@ static Ct variance_impl(hs_ctx* ctx, const ColC& col, double S, const Key& key, 
 }
 
 Ct variance_to_scale(hs_ctx* ctx, const ColC& col, double S) {
-  if (!col_ok(ctx, col)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::variance_to_scale(db, col, S);
-  }
-  return variance_impl(ctx, col, S, Key("var_to_scale", ctx->p).col(col).add(S), false, 0.0);
+  };
+  if (!col_ok(ctx, col)) return dev();
+  return checked(ctx, [&] { return variance_impl(ctx, col, S, Key("var_to_scale", ctx->p).col(col).add(S), false, 0.0); },
+                 dev);
 }
 
 Ct variance_scaled(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::variance_scaled(db, col, B);
-  }
-  return variance_impl(ctx, col, B * B, Key("var_scaled", ctx->p).col(col).add(B), true, B);
+  };
+  if (!col_ok(ctx, col)) return dev();
+  return checked(ctx, [&] { return variance_impl(ctx, col, B * B, Key("var_scaled", ctx->p).col(col).add(B), true, B); },
+                 dev);
 }
 
 flow::Moments<Ct> moments(hs_ctx* ctx, const ColC& col, double B) {
-  if (!col_ok(ctx, col)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::moments(db, col, B);
-  }
-  auto [r, m] = ledger(ctx, Key("moments", ctx->p).col(col).add(B), [&](SymB& sb) { return flow::moments(sb, sym(col), B); });
-  Runtime& rt = Runtime::get();
-  DevBuf mu = rt.alloc(ctx->p.S), var = rt.alloc(ctx->p.S);
-  PB pb(ctx->p);
-  pb.st(pb.ldr(0), mu.get());
-  pb.st(pb.ldr(1), var.get());
-  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
-  ctx->m = m;
-  flow::Moments<Ct> out;
-  out.mu = make_out(ctx, mu, r.mu.level);
-  out.var = make_out(ctx, var, r.var.level);
-  out.n_valid = col.n_valid;
-  return out;
+  };
+  if (!col_ok(ctx, col)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("moments", ctx->p).col(col).add(B),
+                         [&](SymB& sb) { return flow::moments(sb, sym(col), B); });
+    Runtime& rt = Runtime::get();
+    DevBuf mu = rt.alloc(ctx->p.S), var = rt.alloc(ctx->p.S);
+    PB pb(ctx->p);
+    pb.st(pb.ldr(0), mu.get());
+    const int v = pb.ldr(1);
+    check_var(pb, v, B, false);
+    pb.st(v, var.get());
+    pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
+    ctx->m = m;
+    flow::Moments<Ct> out;
+    out.mu = make_out(ctx, mu, r.mu.level);
+    out.var = make_out(ctx, var, r.var.level);
+    out.n_valid = col.n_valid;
+    return out;
+  }, dev);
 }
 
 ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
-  if (!col_ok(ctx, col) || !cfg_ok(cfg)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::znorm(db, col, B, cfg);
-  }
-#ifdef HS_HOST_PROFILE
-  auto T = [] { return std::chrono::steady_clock::now(); };
-  static double acc[6] = {0, 0, 0, 0, 0, 0};
-  static int calls = 0;
-  auto t0 = T();
-#define HS_HP(i) acc[i] += std::chrono::duration<double, std::micro>(T() - t0).count(), t0 = T()
-#else
-#define HS_HP(i)
-#endif
-  auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(col).add(B).cfg(cfg), [&](SymB& sb) { return flow::znorm(sb, sym(col), B, cfg); });
-  HS_HP(0);
-  Runtime& rt = Runtime::get();
-  std::vector<DevBuf> outs;
-  for (size_t c = 0; c < col.chunks.size(); ++c) outs.push_back(rt.alloc(ctx->p.S));
-  HS_HP(1);
-  PB pb(ctx->p);
-  const int inv = pb.invsqrt(pb.ldr(1), B * B, cfg);  // crypto_invsqrt(var, B^2)
-  pb.zapply(pb.ldr(0), inv, col.chunks, outs);        // mul_ct(sub_ct(chunk, mu), inv)
-  HS_HP(2);
-  const k::StatArgs sa = stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
-  HS_HP(3);
-  pb.launch_stat(sa);
-  HS_HP(4);
-  ctx->m = m;
-#ifdef HS_HOST_PROFILE
-  if (++calls % 200 == 0)
-    std::fprintf(stderr, "znorm host us/call: ledger %.2f alloc %.2f program %.2f args %.2f launch %.2f\n",
-                 acc[0] / calls, acc[1] / calls, acc[2] / calls, acc[3] / calls, acc[4] / calls);
-#endif
-#undef HS_HP
-  ColC z;
-  z.n_valid = col.n_valid;
-  for (size_t c = 0; c < outs.size(); ++c) z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level));
-  return z;
+  };
+  if (!col_ok(ctx, col) || !cfg_ok(cfg)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(col).add(B).cfg(cfg),
+                         [&](SymB& sb) { return flow::znorm(sb, sym(col), B, cfg); });
+    Runtime& rt = Runtime::get();
+    std::vector<DevBuf> outs;
+    for (size_t c = 0; c < col.chunks.size(); ++c) outs.push_back(rt.alloc(ctx->p.S));
+    PB pb(ctx->p);
+    const int var = pb.ldr(1);
+    check_var(pb, var, B, true);
+    const int inv = pb.invsqrt(var, B * B, cfg);  // crypto_invsqrt(var, B^2)
+    pb.zapply(pb.ldr(0), inv, col.chunks, outs);  // mul_ct(sub_ct(chunk, mu), inv)
+    pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B));
+    ctx->m = m;
+    ColC z;
+    z.n_valid = col.n_valid;
+    for (size_t c = 0; c < outs.size(); ++c) z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level));
+    return z;
+  }, dev);
 }
 
 static Ct std_moment(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg, int power) {
-  if (!col_ok(ctx, col) || !cfg_ok(cfg)) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::std_moment(db, col, B, cfg, power);
-  }
-  auto [r, m] = ledger(ctx, Key("std_moment", ctx->p).col(col).add(B).cfg(cfg).add(power),
-                       [&](SymB& sb) { return flow::std_moment(sb, sym(col), B, cfg, power); });
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  PB pb(ctx->p);
-  const int inv = pb.invsqrt(pb.ldr(1), B * B, cfg);
-  const int inv2 = pb.mul(inv, inv);
-  const int invp = power == 4 ? pb.mul(inv2, inv2) : pb.mul(inv2, inv);
-  pb.st(pb.mul(pb.ldr(4), invp), out.get());  // mul_ct(numerator, inv^p)
-  k::StatArgs a = stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
-  a.power = power;
-  pb.launch_stat(a);
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!col_ok(ctx, col) || !cfg_ok(cfg)) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("std_moment", ctx->p).col(col).add(B).cfg(cfg).add(power),
+                         [&](SymB& sb) { return flow::std_moment(sb, sym(col), B, cfg, power); });
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    PB pb(ctx->p);
+    const int var = pb.ldr(1);
+    check_var(pb, var, B, true);
+    const int inv = pb.invsqrt(var, B * B, cfg);
+    const int inv2 = pb.mul(inv, inv);
+    const int invp = power == 4 ? pb.mul(inv2, inv2) : pb.mul(inv2, inv);
+    pb.st(pb.mul(pb.ldr(4), invp), out.get());  // mul_ct(numerator, inv^p)
+    k::StatArgs a = stat_args(ctx, {&col}, k::MOM_BOTH, 1.0, B * B);
+    a.power = power;
+    pb.launch_stat(a);
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct kurtosis(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return std_moment(ctx, col, B, cfg, 4); }
 Ct skewness(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) { return std_moment(ctx, col, B, cfg, 3); }
 
 Ct coeff_variation(hs_ctx* ctx, const ColC& col, double B, const SignCfg& sc, const InvCfg& cfg) {
-  if (!col_ok(ctx, col) || !cfg_ok(cfg) || !degree_ok(cfg.cheb_degree) || !sign_ok(sc) || sc.folds > 24) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::coeff_variation(db, col, B, sc, cfg);
-  }
-  auto [r, m] = ledger(ctx, Key("cv", ctx->p).col(col).add(B).sign(sc).cfg(cfg),
-                       [&](SymB& sb) { return flow::coeff_variation(sb, sym(col), B, sc, cfg); });
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  PB pb(ctx->p);
-  const int mu_b = pb.ldr(0);  // mean_scaled(col, B)
-  const int sgn = pb.sign(mu_b, sc);
-  const int inv_mu = pb.inv(pb.mul(mu_b, sgn), B, cfg);
-  const int sigma = pb.sqrt_(pb.ldr(1), B * B, cfg.cheb_degree);  // variance_scaled(col, B)
-  pb.st(pb.mul(pb.mul(sigma, inv_mu), sgn), out.get());
-  pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, B, B * B));
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!col_ok(ctx, col) || !cfg_ok(cfg) || !degree_ok(cfg.cheb_degree) || !sign_ok(sc) || sc.folds > 24) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("cv", ctx->p).col(col).add(B).sign(sc).cfg(cfg),
+                         [&](SymB& sb) { return flow::coeff_variation(sb, sym(col), B, sc, cfg); });
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    PB pb(ctx->p);
+    const int mu_b = pb.ldr(0);  // mean_scaled(col, B)
+    pb.check(mu_b, k::CK_ABS_LT, 1, 0.01);  // stats.hpp:221-223
+    const int sgn = pb.sign(mu_b, sc);
+    const int inv_mu = pb.inv(pb.mul(mu_b, sgn), B, cfg);
+    const int sigma = pb.sqrt_(pb.ldr(1), B * B, cfg.cheb_degree);  // variance_scaled(col, B)
+    pb.st(pb.mul(pb.mul(sigma, inv_mu), sgn), out.get());
+    pb.launch_stat(stat_args(ctx, {&col}, k::MOM_BOTH, B, B * B));
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 Ct pearson(hs_ctx* ctx, const ColC& x, const ColC& y, double B, const InvCfg& cfg) {
-  if (!col_ok(ctx, x) || !col_ok(ctx, y) || !cfg_ok(cfg) || x.chunks.size() != y.chunks.size()) {
+  auto dev = [&] {
     DevB db(ctx->p, ctx->m);
     return flow::pearson(db, x, y, B, cfg);
-  }
-  auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(x).col(y).add(B).cfg(cfg),
-                       [&](SymB& sb) { return flow::pearson(sb, sym(x), sym(y), B, cfg); });
-  DevBuf out = Runtime::get().alloc(ctx->p.S);
-  PB pb(ctx->p);
-  const int ix = pb.invsqrt(pb.ldr(1), B * B, cfg);
-  const int iy = pb.invsqrt(pb.ldr(3), B * B, cfg);
-  pb.st(pb.mul(pb.mul(pb.ldr(4), ix), iy), out.get());  // mul_ct(mul_ct(cov, inv_x), inv_y)
-  k::StatArgs a = stat_args(ctx, {&x, &y}, k::MOM_BOTH, 1.0, B * B);
-  a.power = 2;
-  pb.launch_stat(a);
-  ctx->m = m;
-  return make_out(ctx, out, r.level);
+  };
+  if (!col_ok(ctx, x) || !col_ok(ctx, y) || !cfg_ok(cfg) || x.chunks.size() != y.chunks.size()) return dev();
+  return checked(ctx, [&] {
+    auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(x).col(y).add(B).cfg(cfg),
+                         [&](SymB& sb) { return flow::pearson(sb, sym(x), sym(y), B, cfg); });
+    DevBuf out = Runtime::get().alloc(ctx->p.S);
+    PB pb(ctx->p);
+    const int vx = pb.ldr(1), vy = pb.ldr(3);
+    check_var(pb, vx, B, true);
+    check_var(pb, vy, B, true);
+    const int ix = pb.invsqrt(vx, B * B, cfg);
+    const int iy = pb.invsqrt(vy, B * B, cfg);
+    pb.st(pb.mul(pb.mul(pb.ldr(4), ix), iy), out.get());  // mul_ct(mul_ct(cov, inv_x), inv_y)
+    k::StatArgs a = stat_args(ctx, {&x, &y}, k::MOM_BOTH, 1.0, B * B);
+    a.power = 2;
+    pb.launch_stat(a);
+    ctx->m = m;
+    return make_out(ctx, out, r.level);
+  }, dev);
 }
 
 }  // namespace pipe

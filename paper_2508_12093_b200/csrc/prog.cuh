@@ -237,8 +237,9 @@ __device__ __forceinline__ double cheb_eval(const Q& q, const double* t, int d, 
 }
 
 // ---- Newton (primitives.hpp:105-132) -----------------------------------------------
+// flag (debug_checks, this slot checked): check_divergence after every iteration
 template <class Q>
-__device__ double newton(const Q& q, double x, double y, int n, int iters, double lin) {
+__device__ double newton(const Q& q, double x, double y, int n, int iters, double lin, unsigned* flag = nullptr) {
   for (int it = 0; it < iters; ++it) {
     double prod;
     if (n == 2) {
@@ -259,8 +260,20 @@ __device__ double newton(const Q& q, double x, double y, int n, int iters, doubl
       prod = f[0];
     }
     y = q.sub(q.mulc(y, lin), prod);  // sub_ct(mul_pt(y, (n+1)/n), prod)
+    if (flag && !(fabs(q.out(y)) <= 1e6)) atomicOr(flag, 1u);  // primitives.hpp:89-96
   }
   return y;
+}
+
+// The reference's debug predicates (kernels.h ChkKind) on a slot value in real units
+__device__ __forceinline__ bool chk_fails(int kind, double v, double c, double c2) {
+  switch (kind) {
+    case CK_OPEN: return !(v > c) || !(v <= c2);
+    case CK_RANGE: return v < c || v > c2;
+    case CK_LT: return v < c;
+    case CK_SCALED_LT: return __dmul_rn(__dmul_rn(v, c), c) < c2;
+    default: return fabs(v) < c;
+  }
 }
 
 // ---- launch geometry ---------------------------------------------------------------------
@@ -318,7 +331,14 @@ __device__ __forceinline__ void exec(const Q& q, const Prog& pg, const double* s
       case M_ADDC: r[I.dst] = q.addc(r[I.a], I.c); break;
       case M_MULC: r[I.dst] = q.mulc(r[I.a], I.c); break;
       case M_CHEB: r[I.dst] = cheb_eval<Q, P>(q, stab + I.i0, I.i1, r[I.a], lane, I.b != 0, I.c != 0.0); break;
-      case M_NEWTON: r[I.dst] = newton<Q>(q, r[I.a], r[I.b], I.i0, I.i1, I.c); break;
+      case M_NEWTON:
+        r[I.dst] = newton<Q>(q, r[I.a], r[I.b], I.i0, I.i1, I.c,
+                             pg.flags && live && lane == 0 && s < static_cast<unsigned>(I.i2) ? pg.flags : nullptr);
+        break;
+      case M_CHK:
+        if (pg.flags && live && lane == 0 && s < static_cast<unsigned>(I.i1) && chk_fails(I.i0, q.out(r[I.a]), I.c, I.c2))
+          atomicOr(pg.flags, 1u);
+        break;
       case M_ZAPPLY:
         if (live)
           for (int c = lane; c < pg.nchunks; c += P)
