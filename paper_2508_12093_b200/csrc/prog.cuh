@@ -202,7 +202,8 @@ __device__ __forceinline__ double cheb_eval(const Q& q, const double* t, int d, 
       const bool left = ((lane >> r) & 1) == 0;
       v = ff.add(ff.mul(left ? v : o, tpow(Ks + r, T)), left ? o : v);
     }
-    return v;
+    // a zero result may carry the wrong zero sign (quant.cuh magic_round_nz): redo exactly
+    return v == 0.0 ? cheb_exact<Q>(q, t, d, x, P, 1) : v;
   }
   // general degree: peel the top bit repeatedly (p = q*T_g + r, r full)
   int gk[kMaxK];
@@ -233,7 +234,7 @@ __device__ __forceinline__ double cheb_eval(const Q& q, const double* t, int d, 
     c += (k == 0) ? 2 : (1 << k);
     v = ff.add(head, rest);
   }
-  return v;
+  return v == 0.0 ? cheb_exact<Q>(q, t, d, x, P, 0) : v;  // zero sign: see quant.cuh magic_round_nz
 }
 
 // ---- Newton (primitives.hpp:105-132) -----------------------------------------------

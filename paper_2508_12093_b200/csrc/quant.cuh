@@ -93,21 +93,24 @@ constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 __device__ __forceinline__ double magic_round(double s, double sign_src) {
   return copysign(__dsub_rn(s, kMagic), sign_src);
 }
+// Without the copysign the result differs from rint only in the SIGN OF A ZERO (t in
+// [-0.5, 0) gives +0 instead of -0).  Inside a Chebyshev tree a zero's sign only ever flows
+// into other zeros (x + 0 = x for x != 0; 0 * y and rint(0 + c) keep or drop it), so every
+// nonzero value of the tree, and in particular a nonzero result, is bit-identical to the
+// rint() evaluation; prog.cuh re-evaluates a slot exactly when the tree's result is zero.
+__device__ __forceinline__ double magic_round_nz(double s) { return __dsub_rn(s, kMagic); }
 
 struct QGridFast {
   double inv;
   __device__ __forceinline__ double add(double a, double b) const { return __dadd_rn(a, b); }
   __device__ __forceinline__ double mul(double a, double b) const {
-    const double p = __dmul_rn(a, b);
-    return magic_round(__fma_rn(p, inv, kMagic), p);
+    return magic_round_nz(__fma_rn(__dmul_rn(a, b), inv, kMagic));
   }
   __device__ __forceinline__ double mulc(double a, double c) const {
-    const double p = __dmul_rn(a, c);
-    return magic_round(__dadd_rn(p, kMagic), p);
+    return magic_round_nz(__dadd_rn(__dmul_rn(a, c), kMagic));
   }
   __device__ __forceinline__ double addc(double a, double cs) const {
-    const double p = __dadd_rn(a, cs);
-    return magic_round(__dadd_rn(p, kMagic), p);
+    return magic_round_nz(__dadd_rn(__dadd_rn(a, cs), kMagic));
   }
 };
 
