@@ -61,6 +61,10 @@ int hs_rns_secret(hs_rns* ctx, uint64_t* dev_out); /* [L+1+K][N] NTT form (tests
  * n <= N/2 real values -> N coefficients round(scale * m_k), and back. */
 int hs_rns_encode(uint32_t logN, const double* z, uint64_t n, double scale, int64_t* coeffs);
 int hs_rns_decode(uint32_t logN, const int64_t* coeffs, double scale, double* z, uint64_t n);
+/* the same transforms on the GPU (codec_gpu.cu; what RNS-backed EvalContexts use), host buffers
+ * in and out, coefficients as integer-valued doubles; bit-identical to the host codec */
+int hs_rns_encode_gpu(uint32_t logN, const double* z, uint64_t n, double scale, double* coeffs);
+int hs_rns_decode_gpu(uint32_t logN, const double* coeffs, double scale, double* z, uint64_t n);
 /* symmetric RLWE encryption at `level` (seeded by spec.seed and tag) of host
  * coefficients / of slot values; decryption through q_0 (|scale * value| < q_0/2) */
 int hs_rns_encrypt_coeffs(hs_rns* ctx, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* dev_out);

@@ -147,6 +147,8 @@ _SIGS.update({
     "hs_rns_random_ct": (C.c_int, [RNS, C.c_uint32, C.c_uint64, C.c_void_p]),
     "hs_rns_encode": (C.c_int, [C.c_uint32, DP, C.c_uint64, C.c_double, C.POINTER(C.c_int64)]),
     "hs_rns_decode": (C.c_int, [C.c_uint32, C.POINTER(C.c_int64), C.c_double, DP, C.c_uint64]),
+    "hs_rns_encode_gpu": (C.c_int, [C.c_uint32, DP, C.c_uint64, C.c_double, DP]),
+    "hs_rns_decode_gpu": (C.c_int, [C.c_uint32, DP, C.c_double, DP, C.c_uint64]),
     "hs_rns_add": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_sub": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "hs_rns_add_const": (C.c_int, [RNS, C.c_uint32, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32]),

@@ -1095,6 +1095,40 @@ int hs_rns_decode(uint32_t logN, const int64_t* coeffs, double scale, double* z,
   });
 }
 
+int hs_rns_encode_gpu(uint32_t logN, const double* z, uint64_t n, double scale, double* coeffs) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    if (logN < 2 || logN > 17) fail(HS_E_INVALID_ARG, "hs_rns_encode_gpu: logN out of range");
+    if (n && !z) fail(HS_E_INVALID_ARG, "null values");
+    if (n > (1u << logN) / 2) fail(HS_E_TOO_MANY_VALUES, "hs_rns_encode_gpu: more values than slots");
+    if (!(scale > 0.0) || !std::isfinite(scale)) fail(HS_E_INVALID_ARG, "hs_rns_encode_gpu: bad scale");
+    Runtime& rt = Runtime::get();
+    const size_t N = size_t(1) << logN;
+    DevBuf zd = rt.alloc(std::max<uint64_t>(n, 1)), cd = rt.alloc(N);
+    if (n) cuda_ok(cudaMemcpyAsync(zd.get(), z, n * 8, cudaMemcpyHostToDevice, rt.stream()), "encode upload");
+    rns::encode_dev(logN, zd.get(), n, scale, cd.get(), 1);
+    cuda_ok(cudaMemcpyAsync(coeffs, cd.get(), N * 8, cudaMemcpyDeviceToHost, rt.stream()), "encode read");
+    rt.sync();
+  });
+}
+
+int hs_rns_decode_gpu(uint32_t logN, const double* coeffs, double scale, double* z, uint64_t n) {
+  return guard([&] {
+    need(coeffs, "coeffs");
+    if (logN < 2 || logN > 17) fail(HS_E_INVALID_ARG, "hs_rns_decode_gpu: logN out of range");
+    if (n > (1u << logN) / 2) fail(HS_E_TOO_MANY_VALUES, "hs_rns_decode_gpu: more values than slots");
+    if (n && !z) fail(HS_E_INVALID_ARG, "null output");
+    if (!(scale > 0.0) || !std::isfinite(scale)) fail(HS_E_INVALID_ARG, "hs_rns_decode_gpu: bad scale");
+    Runtime& rt = Runtime::get();
+    const size_t N = size_t(1) << logN;
+    DevBuf cd = rt.alloc(N), zd = rt.alloc(std::max<uint64_t>(n, 1));
+    cuda_ok(cudaMemcpyAsync(cd.get(), coeffs, N * 8, cudaMemcpyHostToDevice, rt.stream()), "decode upload");
+    rns::decode_dev(logN, cd.get(), scale, zd.get(), n, n, 1);
+    if (n) cuda_ok(cudaMemcpyAsync(z, zd.get(), n * 8, cudaMemcpyDeviceToHost, rt.stream()), "decode read");
+    rt.sync();
+  });
+}
+
 int hs_rns_encrypt_coeffs(hs_rns* ctx, uint32_t level, const int64_t* coeffs, uint64_t tag, uint64_t* dev_out) {
   return guard([&] {
     need(coeffs, "coeffs");

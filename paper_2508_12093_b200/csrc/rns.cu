@@ -845,20 +845,29 @@ __global__ void k_dec(const uint64_t* ct, const uint64_t* sk, uint64_t* out, con
   }
 }
 
-// CRT of the two lowest limbs of a decryption: v = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, q0 q1),
-// as (lo, hi) words; the host centres and converts (the modular work stays off the host)
-__global__ void k_crt2(const uint64_t* m, uint64_t* v, const PrimeC* pcs, uint64_t q0inv, uint64_t q0inv_sh,
-                       uint32_t logN) {
+// decryption (phase m through q_0, or q_0 q_1 with CRT) -> centred coefficients as doubles
+// (the value nearest to the exact integer, as the host conversion of the same integer gives)
+__global__ void k_center(const uint64_t* m, double* co, const PrimeC* pcs, uint64_t q0inv, uint64_t q0inv_sh,
+                         uint32_t use, uint32_t logN) {
   const uint32_t N = 1u << logN;
-  const uint64_t q0 = pcs[0].q, q1 = pcs[1].q;
+  const uint64_t q0 = pcs[0].q;
   for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    if (use == 1) {
+      const uint64_t h = m[n];
+      co[n] = h > q0 / 2 ? -static_cast<double>(q0 - h) : static_cast<double>(h);
+      continue;
+    }
+    const uint64_t q1 = pcs[1].q;
     const uint64_t a0 = m[n], a1 = m[N + n];
-    const uint64_t d = sub_mod(a1, a0 % q1, q1);
-    const uint64_t t = mul_shoup(d, q0inv, q0inv_sh, q1);
-    const u128 r = static_cast<u128>(q0) * t + a0;
-    v[2 * size_t(n)] = static_cast<uint64_t>(r);
-    v[2 * size_t(n) + 1] = static_cast<uint64_t>(r >> 64);
+    const uint64_t t = mul_shoup(sub_mod(a1, a0 % q1, q1), q0inv, q0inv_sh, q1);
+    const u128 r = static_cast<u128>(q0) * t + a0, Q = static_cast<u128>(q0) * q1;
+    co[n] = r > Q / 2 ? -static_cast<double>(Q - r) : static_cast<double>(r);
   }
+}
+
+__global__ void k_scale_round(double* co, double r, uint32_t N) {  // refresh: co = rint(co * r)
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+    co[n] = rint(__dmul_rn(co[n], r));
 }
 
 __global__ void k_enc_as(uint64_t* ct, const uint64_t* sk, const PrimeC* pcs, uint32_t nl, uint32_t logN) {
@@ -1747,38 +1756,47 @@ void const_op_big(const Ctx& c, uint32_t level, const uint64_t* a, double k, uin
   const_op_res(c, level, a, res, out, batch, mul);
 }
 
-void encrypt_real(const Ctx& c, uint32_t level, const double* co, uint64_t tag, uint64_t* out) {
+void encrypt_real_dev(const Ctx& c, uint32_t level, const double* dco, uint64_t tag, uint64_t* out) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns encrypt: level > L");
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1, logN = c.spec.logN;
-  DevBuf d = rt.alloc(c.N);
-  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
-  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const double>(d), out, c.dpc(), nl, logN);
+  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dco, out, c.dpc(), nl, logN);
   k_enc_res<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, c.dpc(), c.spec.seed, tag, nl, logN);
   ntt(c, out, iota_rows(nl), 1, 0, false);
   k_enc_as<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(out, dptr<const uint64_t>(c.d_sk), c.dpc(), nl, logN);
   cuda_ok(cudaGetLastError(), "encrypt");
   rt.note_launch(3);
+}
+
+void encrypt_real(const Ctx& c, uint32_t level, const double* co, uint64_t tag, uint64_t* out) {
+  Runtime& rt = Runtime::get();
+  DevBuf d = rt.alloc(c.N);
+  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "encrypt upload");
+  encrypt_real_dev(c, level, dptr<const double>(d), tag, out);
   rt.sync();  // the caller's coefficient buffer may be released on return
 }
 
-void mul_plain_real(const Ctx& c, uint32_t level, const uint64_t* a, const double* co, uint64_t* out) {
+void mul_plain_real_dev(const Ctx& c, uint32_t level, const uint64_t* a, const double* dco, uint64_t* out) {
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1, logN = c.spec.logN;
-  DevBuf d = rt.alloc(c.N);
   DevBuf pt = rt.alloc(size_t(nl) * c.N);
-  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
-  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dptr<const double>(d), dptr<uint64_t>(pt), c.dpc(), nl,
-                                                                logN);
+  k_residues<<<grid_of(size_t(nl) * c.N), kT, 0, rt.stream()>>>(dco, dptr<uint64_t>(pt), c.dpc(), nl, logN);
   ntt(c, dptr<uint64_t>(pt), iota_rows(nl), 1, 0, false);
   k_mul_plain<<<grid_of(size_t(2) * nl * c.N), kT, 0, rt.stream()>>>(a, dptr<const uint64_t>(pt), out, c.dpc(), nl,
                                                                      logN);
   cuda_ok(cudaGetLastError(), "mul_plain");
   rt.note_launch(2);
+}
+
+void mul_plain_real(const Ctx& c, uint32_t level, const uint64_t* a, const double* co, uint64_t* out) {
+  Runtime& rt = Runtime::get();
+  DevBuf d = rt.alloc(c.N);
+  cuda_ok(cudaMemcpyAsync(d.get(), co, size_t(c.N) * 8, cudaMemcpyHostToDevice, rt.stream()), "pt upload");
+  mul_plain_real_dev(c, level, a, dptr<const double>(d), out);
   rt.sync();
 }
 
-void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeffs) {
+void decrypt_crt_dev(const Ctx& c, uint32_t level, const uint64_t* ct, double* dco) {
   if (level > c.spec.L) fail(HS_E_INVALID_ARG, "rns decrypt: level > L");
   Runtime& rt = Runtime::get();
   const uint32_t nl = level + 1, use = level >= 1 ? 2 : 1;
@@ -1786,30 +1804,30 @@ void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeff
   k_dec<<<grid_of(size_t(use) * c.N), kT, 0, rt.stream()>>>(ct, dptr<const uint64_t>(c.d_sk), dptr<uint64_t>(m),
                                                              c.dpc(), nl, use, c.spec.logN);
   ntt(c, dptr<uint64_t>(m), iota_rows(use), 1, 0, true);
-  const uint64_t q0 = c.primes[0];
-  if (use == 1) {
-    std::vector<uint64_t> h(c.N);
-    cuda_ok(cudaMemcpyAsync(h.data(), m.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
-    rt.sync();
-    rt.note_launch();
-    for (uint32_t n = 0; n < c.N; ++n)
-      coeffs[n] = h[n] > q0 / 2 ? -static_cast<double>(q0 - h[n]) : static_cast<double>(h[n]);
-    return;
+  uint64_t q0inv = 0, q0inv_sh = 0;
+  if (use == 2) {
+    q0inv = h_inv(c.primes[0] % c.primes[1], c.primes[1]);
+    q0inv_sh = shoup_of(q0inv, c.primes[1]);
   }
-  const uint64_t q1 = c.primes[1];
-  const uint64_t q0inv = h_inv(q0 % q1, q1);
-  DevBuf v = rt.alloc(size_t(2) * c.N);
-  k_crt2<<<grid_of(c.N), kT, 0, rt.stream()>>>(dptr<const uint64_t>(m), dptr<uint64_t>(v), c.dpc(), q0inv,
-                                                shoup_of(q0inv, q1), c.spec.logN);
-  std::vector<uint64_t> h(size_t(2) * c.N);
-  cuda_ok(cudaMemcpyAsync(h.data(), v.get(), h.size() * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
-  rt.sync();
+  k_center<<<grid_of(c.N), kT, 0, rt.stream()>>>(dptr<const uint64_t>(m), dco, c.dpc(), q0inv, q0inv_sh, use,
+                                                  c.spec.logN);
+  cuda_ok(cudaGetLastError(), "decrypt");
   rt.note_launch(2);
-  const unsigned __int128 Q = static_cast<unsigned __int128>(q0) * q1;
-  for (uint32_t n = 0; n < c.N; ++n) {  // CRT value in [0, q0 q1), centred
-    const unsigned __int128 r = (static_cast<unsigned __int128>(h[2 * size_t(n) + 1]) << 64) | h[2 * size_t(n)];
-    coeffs[n] = r > Q / 2 ? -static_cast<double>(Q - r) : static_cast<double>(r);
-  }
+}
+
+void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeffs) {
+  Runtime& rt = Runtime::get();
+  DevBuf d = rt.alloc(c.N);
+  decrypt_crt_dev(c, level, ct, dptr<double>(d));
+  cuda_ok(cudaMemcpyAsync(coeffs, d.get(), size_t(c.N) * 8, cudaMemcpyDeviceToHost, rt.stream()), "decrypt read");
+  rt.sync();
+}
+
+void scale_round_dev(const Ctx& c, double* dco, double r) {
+  Runtime& rt = Runtime::get();
+  k_scale_round<<<grid_of(c.N), kT, 0, rt.stream()>>>(dco, r, c.N);
+  cuda_ok(cudaGetLastError(), "refresh scale");
+  rt.note_launch();
 }
 
 void random_ct(const Ctx& c, uint32_t level, uint64_t tag, uint64_t* out) {

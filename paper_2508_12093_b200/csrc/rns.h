@@ -157,6 +157,16 @@ void encrypt_real(const Ctx& c, uint32_t level, const double* co, uint64_t tag, 
 void mul_plain_real(const Ctx& c, uint32_t level, const uint64_t* a, const double* co, uint64_t* out);
 // decryption through q_0 q_1 (CRT; q_0 alone at level 0): centred coefficients as doubles
 void decrypt_crt(const Ctx& c, uint32_t level, const uint64_t* ct, double* coeffs);
+// device-resident forms (dco: N device doubles; no host round trip, no synchronisation)
+void decrypt_crt_dev(const Ctx& c, uint32_t level, const uint64_t* ct, double* dco);
+void encrypt_real_dev(const Ctx& c, uint32_t level, const double* dco, uint64_t tag, uint64_t* out);
+void mul_plain_real_dev(const Ctx& c, uint32_t level, const uint64_t* a, const double* dco, uint64_t* out);
+void scale_round_dev(const Ctx& c, double* dco, double r);  // dco = rint(dco * r)
+// CKKS canonical-embedding codec on the device (codec_gpu.cu; bit-identical to rns_codec.cpp):
+// encode: item k of `batch` takes z[k N/2 .. min(n, (k+1) N/2)) (device) -> co + k N (device)
+void encode_dev(uint32_t logN, const double* z, size_t n, double scale, double* co, uint32_t batch);
+// decode: item k's N coefficients co + k N at `scale` -> its first n slots at z + k z_stride (device)
+void decode_dev(uint32_t logN, const double* co, double scale, double* z, size_t n, size_t z_stride, uint32_t batch);
 // out = a +- b (limb-wise), batch ciphertexts at `level`
 void add_sub(const Ctx& c, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out, uint32_t batch,
              bool sub);

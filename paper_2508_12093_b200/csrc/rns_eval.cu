@@ -40,67 +40,49 @@ RCt RnsB::make(DevBuf b, int phys, int level, size_t off) const {
   return d;
 }
 
+// host slot values -> device (the canonical-embedding encoding runs on the device, codec_gpu.cu)
+static DevBuf upload_values(const double* v, size_t n) {
+  Runtime& rt = Runtime::get();
+  DevBuf d = rt.alloc(std::max<size_t>(n, 1));
+  if (n) cuda_ok(cudaMemcpyAsync(d.get(), v, n * 8, cudaMemcpyHostToDevice, rt.stream()), "encode upload");
+  return d;
+}
+
 RCt RnsB::encrypt(const double* v, size_t n) {  // ckks.hpp:97-104
   if (n > p_.S) fail(HS_E_TOO_MANY_VALUES, "encrypt: more values than slots");
   const int L = static_cast<int>(c_.spec.L);
-  std::vector<double> co(c_.N);
-  encode_real(c_.spec.logN, v, n, sigma_[L], co.data());
-  DevBuf b = Runtime::get().alloc(words(L));
-  encrypt_real(c_, L, co.data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
+  Runtime& rt = Runtime::get();
+  DevBuf z = upload_values(v, n), co = rt.alloc(c_.N);
+  encode_dev(c_.spec.logN, reinterpret_cast<const double*>(z.get()), n, sigma_[L], co.get(), 1);
+  DevBuf b = rt.alloc(words(L));
+  encrypt_real_dev(c_, L, co.get(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
   return make(b, L, p_.max_level);
-}
-
-// Run f(i) for i < n on up to `hw` host threads (the chunks' host FFTs are independent).
-template <class F>
-static void parallel_chunks(size_t n, F&& f) {
-  const size_t hw = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), 16));
-  if (n <= 1 || hw == 1) {
-    for (size_t i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::atomic<size_t> next{0};
-  std::vector<std::thread> ts;
-  std::exception_ptr err;
-  std::mutex em;
-  for (size_t t = 0; t < std::min(hw, n); ++t)
-    ts.emplace_back([&] {
-      for (size_t i; (i = next.fetch_add(1)) < n;) {
-        try {
-          f(i);
-        } catch (...) {
-          std::lock_guard<std::mutex> g(em);
-          if (!err) err = std::current_exception();
-        }
-      }
-    });
-  for (auto& t : ts) t.join();
-  if (err) std::rethrow_exception(err);
 }
 
 std::vector<RCt> RnsB::encrypt_column(const double* v, size_t n) {  // column.hpp:25-39
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(v[i])) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
-  // the chunks' canonical-embedding encodings on host threads, then the encryptions in order
-  // (the per-chunk randomness tags follow the chunk order, as in encrypt())
+  // one upload, the chunks' canonical-embedding encodings as one batched device transform, then
+  // the encryptions in order (the per-chunk randomness tags follow the chunk order, as in encrypt())
   const size_t nch = (n + p_.S - 1) / p_.S;
   const int L = static_cast<int>(c_.spec.L);
-  std::vector<std::vector<double>> co(nch, std::vector<double>(c_.N));
-  parallel_chunks(nch, [&](size_t k) {
-    const size_t off = k * p_.S;
-    encode_real(c_.spec.logN, v + off, std::min(p_.S, n - off), sigma_[L], co[k].data());
-  });
+  Runtime& rt = Runtime::get();
+  DevBuf z = upload_values(v, n), co = rt.alloc(nch * c_.N);
+  encode_dev(c_.spec.logN, reinterpret_cast<const double*>(z.get()), n, sigma_[L], co.get(),
+             static_cast<uint32_t>(nch));
   std::vector<RCt> out;
-  DevBuf b = Runtime::get().alloc(nch * words(L));  // one contiguous buffer: chunk ops batch without copies
+  DevBuf b = rt.alloc(nch * words(L));  // one contiguous buffer: chunk ops batch without copies
   for (size_t k = 0; k < nch; ++k) {
-    encrypt_real(c_, L, co[k].data(), tag_++, reinterpret_cast<uint64_t*>(b.get()) + k * words(L));
+    encrypt_real_dev(c_, L, co.get() + k * c_.N, tag_++, reinterpret_cast<uint64_t*>(b.get()) + k * words(L));
     out.push_back(make(b, L, p_.max_level, k * words(L)));
   }
+  rt.sync();  // the caller's values may be released on return
   return out;
 }
 
 std::vector<std::vector<double>> RnsB::decrypt_many(const std::vector<RCt>& cts, const std::vector<size_t>& ns) {
   std::vector<std::vector<double>> out(cts.size());
-  parallel_chunks(cts.size(), [&](size_t k) { out[k] = decrypt(cts[k], ns[k]); });
+  for (size_t k = 0; k < cts.size(); ++k) out[k] = decrypt(cts[k], ns[k]);
   return out;
 }
 
@@ -167,12 +149,12 @@ RCt RnsB::bootstrap(const RCt& a) {  // ckks.hpp:207-213
 RCt RnsB::refresh(const RCt& a) {
   if (a->phys < 1) fail(HS_E_LEVEL_EXHAUSTED, "rns refresh: ciphertext at the last RNS limb");
   const int L = static_cast<int>(c_.spec.L);
-  std::vector<double> co(c_.N);
-  decrypt_crt(c_, a->phys, a->ptr(), co.data());
-  const double r = sigma_[L] / sigma_[a->phys];
-  for (double& v : co) v = std::nearbyint(v * r);
-  DevBuf b = Runtime::get().alloc(words(L));
-  encrypt_real(c_, L, co.data(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
+  Runtime& rt = Runtime::get();
+  DevBuf co = rt.alloc(c_.N);  // the refresh stays on the device: decrypt, rescale, re-encrypt
+  decrypt_crt_dev(c_, a->phys, a->ptr(), co.get());
+  scale_round_dev(c_, co.get(), sigma_[L] / sigma_[a->phys]);
+  DevBuf b = rt.alloc(words(L));
+  encrypt_real_dev(c_, L, co.get(), tag_++, reinterpret_cast<uint64_t*>(b.get()));
   RCt o = make(b, L, p_.max_level);
   const_cast<RCtData*>(o.get())->n = a->n;
   return o;
@@ -253,12 +235,12 @@ RCt RnsB::mul_pt_vec(RCt a, const std::vector<double>& v) {  // ckks.hpp:179-189
   a = prepare_mul_pt(a);
   const int p = a->phys;
   if (p < 1) fail(HS_E_LEVEL_EXHAUSTED, "mul_pt: RNS modulus chain exhausted (deep chain too short)");
-  std::vector<double> co(c_.N);
-  encode_real(c_.spec.logN, v.data(), v.size(), sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p],
-              co.data());
   Runtime& rt = Runtime::get();
+  DevBuf z = upload_values(v.data(), v.size()), co = rt.alloc(c_.N);
+  encode_dev(c_.spec.logN, reinterpret_cast<const double*>(z.get()), v.size(),
+             sigma_[p - 1] * static_cast<double>(c_.primes[p]) / sigma_[p], co.get(), 1);
   DevBuf m = rt.alloc(words(p));
-  mul_plain_real(c_, p, a->ptr(), co.data(), reinterpret_cast<uint64_t*>(m.get()));
+  mul_plain_real_dev(c_, p, a->ptr(), co.get(), reinterpret_cast<uint64_t*>(m.get()));
   DevBuf o = rt.alloc(words(p - 1));
   rescale(c_, p, reinterpret_cast<const uint64_t*>(m.get()), reinterpret_cast<uint64_t*>(o.get()), 1);
   ++m_.mul_pt;
@@ -499,10 +481,13 @@ std::vector<double> RnsB::decrypt(const RCt& c, size_t n) {
   // q_0 alone cannot hold sigma_0 * value for |value| >= 2^(log q_0 - log sigma_0 - 1): decrypt through two limbs
   if (c->phys < 1)
     fail(HS_E_LEVEL_EXHAUSTED, "rns decrypt: result at the last RNS limb (chain must exceed the statistic's depth)");
-  std::vector<double> co(c_.N);
-  decrypt_crt(c_, c->phys, c->ptr(), co.data());
+  Runtime& rt = Runtime::get();
+  DevBuf co = rt.alloc(c_.N), zd = rt.alloc(std::max<size_t>(n, 1));
+  decrypt_crt_dev(c_, c->phys, c->ptr(), co.get());
+  decode_dev(c_.spec.logN, co.get(), sigma_[c->phys], zd.get(), n, n, 1);
   std::vector<double> z(n);
-  decode_real(c_.spec.logN, co.data(), sigma_[c->phys], z.data(), n);
+  if (n) cuda_ok(cudaMemcpyAsync(z.data(), zd.get(), n * 8, cudaMemcpyDeviceToHost, rt.stream()), "decode read");
+  rt.sync();
   return z;
 }
 

@@ -57,6 +57,24 @@ def decode(logN: int, coeffs: np.ndarray, scale: float, n: int | None = None) ->
     return out
 
 
+def encode_gpu(logN: int, z, scale: float) -> np.ndarray:
+    """The device codec (what RNS-backed contexts use): N integer-valued float64 coefficients."""
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
+    out = np.zeros(1 << logN, dtype=np.float64)
+    _check(_abi.lib().hs_rns_encode_gpu(logN, z.ctypes.data_as(C.POINTER(C.c_double)), z.size, scale,
+                                        out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def decode_gpu(logN: int, coeffs: np.ndarray, scale: float, n: int | None = None) -> np.ndarray:
+    co = np.ascontiguousarray(coeffs, dtype=np.float64)
+    n = (1 << logN) // 2 if n is None else n
+    out = np.zeros(n, dtype=np.float64)
+    _check(_abi.lib().hs_rns_decode_gpu(logN, co.ctypes.data_as(C.POINTER(C.c_double)), scale,
+                                        out.ctypes.data_as(C.POINTER(C.c_double)), n))
+    return out
+
+
 class DeviceBuffer:
     """`words` u64 words of device memory (freed stream-ordered on release)."""
 

@@ -117,3 +117,21 @@ def test_full_size_round_trip():
     assert np.max(np.abs(c.decrypt(s.L - 1, p, s1) - x * y)) < 1e-5
     r = c.rotate(s.L, 7, a)
     assert np.max(np.abs(c.decrypt(s.L, r, DELTA) - np.roll(x, -7))) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("logN", [4, 10, 12, 16])
+def test_device_codec_bit_identical_to_host(logN):
+    """codec_gpu.cu (used by RNS-backed EvalContexts) vs rns_codec.cpp: same FFT, same roundings."""
+    from paper_2508_12093_b200 import rns as R
+    rng = np.random.default_rng(logN)
+    S = 1 << (logN - 1)
+    for n, scale in ((S, 2.0 ** 40), (S // 2 + 1, 2.0 ** 30), (1, 2.0 ** 20)):
+        z = rng.uniform(-3.0, 3.0, n)
+        host = R.encode(logN, z, scale)  # int64 (no signed zero); the device gives integral doubles
+        dev = R.encode_gpu(logN, z, scale)
+        assert np.array_equal(host.astype(np.float64), dev) and np.array_equal(np.rint(dev), dev), (logN, n)
+        back_h = R.decode(logN, host, scale, n)
+        back_d = R.decode_gpu(logN, dev, scale, n)
+        assert np.array_equal(back_h.view(np.int64), back_d.view(np.int64)), (logN, n)
+        assert np.max(np.abs(back_d - z)) < (1 << logN) / scale
