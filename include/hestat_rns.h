@@ -73,7 +73,13 @@ int hs_rns_encrypt(hs_rns* ctx, uint32_t level, const double* z, uint64_t n, dou
 int hs_rns_decrypt_coeffs(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, int64_t* coeffs);
 int hs_rns_decrypt(hs_rns* ctx, uint32_t level, const uint64_t* dev_ct, double scale, double* z, uint64_t n);
 
-/* ops; `batch` ciphertexts per call, consecutive in memory */
+/* ops; `batch` ciphertexts per call, consecutive in memory.  Device pointers are raw: a
+ * ciphertext at level l is 2 (l+1) N words, so every input and output must cover
+ * batch * 2 (l+1) N words (out of rescale / mul_relin_rescale: batch * 2 l N); the library does
+ * not know the allocations behind the pointers (the Python binding, rns.py, checks its
+ * DeviceBuffer sizes before every call).  Tier R is an evaluation / parity / benchmark engine:
+ * keys and encryption randomness are a deterministic hash of spec.seed (so the device and the
+ * oracle produce identical limbs) and hs_rns_secret exports the secret key for the tests. */
 int hs_rns_random_ct(hs_rns* ctx, uint32_t level, uint64_t tag, uint64_t* dev_out);
 /* in-place NTT (inverse != 0: iNTT) of `batch` groups of `nlimbs` limbs, limb i
  * of each group taken mod prime first_prime + i, groups `nlimbs*N` words apart */

@@ -120,6 +120,13 @@ class DeviceBuffer:
             pass
 
 
+def _need(buf: "DeviceBuffer", words: int, what: str) -> "DeviceBuffer":
+    """The hs_rns_* ops take raw device pointers: check the buffer covers what the op touches."""
+    if buf.words < words:
+        raise ValueError(f"{what}: device buffer of {buf.words} words, the op needs {words}")
+    return buf
+
+
 class RnsContext:
     """hs_rns: primes, twiddles and (lazily) keys for one parameter set."""
 
@@ -160,6 +167,7 @@ class RnsContext:
 
     def random_ct(self, level: int, tag: int, out: DeviceBuffer | None = None, offset: int = 0) -> DeviceBuffer:
         out = out or DeviceBuffer(self.spec.ct_words(level))
+        _need(out, offset + self.spec.ct_words(level), "random_ct out")
         _check(_abi.lib().hs_rns_random_ct(self.h, level, tag, out.offset(offset)))
         return out
 
@@ -172,77 +180,99 @@ class RnsContext:
 
     def add(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
             batch: int = 1, sub: bool = False) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(w), w, "add out")
+        _need(a, w, "add a"), _need(b, w, "add b")
         f = _abi.lib().hs_rns_sub if sub else _abi.lib().hs_rns_add
         _check(f(self.h, level, a.ptr, b.ptr, out.ptr, batch))
         return out
 
     def add_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
                   batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(w), w, "add_const out")
+        _need(a, w, "add_const a")
         _check(_abi.lib().hs_rns_add_const(self.h, level, a.ptr, int(c), out.ptr, batch))
         return out
 
     def mul_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
                   batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(w), w, "mul_const out")
+        _need(a, w, "mul_const a")
         _check(_abi.lib().hs_rns_mul_const(self.h, level, a.ptr, int(c), out.ptr, batch))
         return out
 
     def encrypt_coeffs(self, level: int, coeffs: np.ndarray, tag: int, out: DeviceBuffer | None = None) -> DeviceBuffer:
         co = np.ascontiguousarray(coeffs, dtype=np.int64)
-        out = out or DeviceBuffer(self.spec.ct_words(level))
+        out = _need(out or DeviceBuffer(self.spec.ct_words(level)), self.spec.ct_words(level), "encrypt out")
+        if co.size != self.spec.N:
+            raise ValueError(f"encrypt_coeffs: {co.size} coefficients, N = {self.spec.N}")
         _check(_abi.lib().hs_rns_encrypt_coeffs(self.h, level, co.ctypes.data_as(C.POINTER(C.c_int64)), tag, out.ptr))
         return out
 
     def encrypt(self, level: int, z, scale: float, tag: int, out: DeviceBuffer | None = None) -> DeviceBuffer:
         z = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
-        out = out or DeviceBuffer(self.spec.ct_words(level))
+        out = _need(out or DeviceBuffer(self.spec.ct_words(level)), self.spec.ct_words(level), "encrypt out")
         _check(_abi.lib().hs_rns_encrypt(self.h, level, z.ctypes.data_as(C.POINTER(C.c_double)), z.size, scale, tag,
                                          out.ptr))
         return out
 
     def decrypt_coeffs(self, level: int, ct: DeviceBuffer) -> np.ndarray:
+        _need(ct, self.spec.ct_words(level), "decrypt ct")
         out = np.zeros(self.spec.N, dtype=np.int64)
         _check(_abi.lib().hs_rns_decrypt_coeffs(self.h, level, ct.ptr, out.ctypes.data_as(C.POINTER(C.c_int64))))
         return out
 
     def decrypt(self, level: int, ct: DeviceBuffer, scale: float, n: int | None = None) -> np.ndarray:
         n = self.spec.N // 2 if n is None else n
+        _need(ct, self.spec.ct_words(level), "decrypt ct")
         out = np.zeros(n, dtype=np.float64)
         _check(_abi.lib().hs_rns_decrypt(self.h, level, ct.ptr, scale, out.ctypes.data_as(C.POINTER(C.c_double)), n))
         return out
 
     def ntt(self, buf: DeviceBuffer, first_prime: int, nlimbs: int, batch: int = 1, inverse: bool = False):
+        _need(buf, batch * nlimbs * self.spec.N, "ntt buffer")
         _check(_abi.lib().hs_rns_ntt(self.h, buf.ptr, first_prime, nlimbs, batch, int(inverse)))
 
     def mul_relin(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
                   batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(w), w, "mul_relin out")
+        _need(a, w, "mul_relin a"), _need(b, w, "mul_relin b")
         _check(_abi.lib().hs_rns_mul_relin(self.h, level, a.ptr, b.ptr, out.ptr, batch))
         return out
 
     def mul_relin_rescale(self, level: int, a: DeviceBuffer, b: DeviceBuffer, out: DeviceBuffer | None = None,
                           batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(batch * self.spec.ct_words(level - 1)), batch * self.spec.ct_words(level - 1),
+                    "mul_relin_rescale out")
+        _need(a, w, "mul_relin_rescale a"), _need(b, w, "mul_relin_rescale b")
         _check(_abi.lib().hs_rns_mul_relin_rescale(self.h, level, a.ptr, b.ptr, out.ptr, batch))
         return out
 
     def rescale(self, level: int, a: DeviceBuffer, out: DeviceBuffer | None = None, batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        out = _need(out or DeviceBuffer(batch * self.spec.ct_words(level - 1)), batch * self.spec.ct_words(level - 1),
+                    "rescale out")
+        _need(a, batch * self.spec.ct_words(level), "rescale a")
         _check(_abi.lib().hs_rns_rescale(self.h, level, a.ptr, out.ptr, batch))
         return out
 
     def rescale_mul_const(self, level: int, a: DeviceBuffer, c: int, out: DeviceBuffer | None = None,
                           batch: int = 1) -> DeviceBuffer:
         """rescale(c * a) without materialising c * a (|c| < 2^53: passed exactly as a double)."""
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level - 1))
+        out = _need(out or DeviceBuffer(batch * self.spec.ct_words(level - 1)), batch * self.spec.ct_words(level - 1),
+                    "rescale_mul_const out")
+        _need(a, batch * self.spec.ct_words(level), "rescale_mul_const a")
         _check(_abi.lib().hs_rns_rescale_mul_const(self.h, level, a.ptr, int(c), out.ptr, batch))
         return out
 
     def rotate(self, level: int, k: int, a: DeviceBuffer, out: DeviceBuffer | None = None,
                batch: int = 1) -> DeviceBuffer:
-        out = out or DeviceBuffer(batch * self.spec.ct_words(level))
+        w = batch * self.spec.ct_words(level)
+        out = _need(out or DeviceBuffer(w), w, "rotate out")
+        _need(a, w, "rotate a")
         _check(_abi.lib().hs_rns_rotate(self.h, level, k, a.ptr, out.ptr, batch))
         return out
 

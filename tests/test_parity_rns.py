@@ -217,8 +217,14 @@ def test_errors():
     a = c.random_ct(1, 1)
     with pytest.raises(H.error):
         c.rescale(0, a)
-    with pytest.raises(H.error):
+    with pytest.raises((H.error, ValueError)):  # level > L (the buffer check fires first)
         c.mul_relin(SHAPES[0].L + 1, a, a)
+    # raw-pointer ops: an undersized device buffer is refused before the call (no OOB access)
+    top = c.random_ct(SHAPES[0].L, 2)
+    with pytest.raises(ValueError):
+        c.mul_relin(SHAPES[0].L, top, a)
+    with pytest.raises(ValueError):
+        c.rotate(SHAPES[0].L, 1, top, out=a)
 
 
 def test_full_size_north_star():
