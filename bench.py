@@ -377,7 +377,9 @@ def rns_znorm(torch, stream, reps=3):
 
 
 def tier_r_section(torch, stream, batch=64, with_cpu=True):
-    logN, L, dnum, logp = 16, 24, 3, 44
+    # dnum = 2 (K = 13 x 44-bit so P exceeds the 13-prime digits): HMult 154 vs 168 us at dnum = 3
+    # (K = 9) and 183 us at dnum = 4 with the round-2 kernels (profiles/r2_summary.md)
+    logN, L, dnum, logp = 16, 24, 2, 44
     K = special_primes(L, dnum, logp=logp)
     peak, src = hbm_peak_gbs()
     us, launches = rns_measure(torch, stream, logN, L, K, dnum, batch)
@@ -405,11 +407,12 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
                         "achieved": ops["mul_relin"]["achieved_gbs"], "peak": peak, "unit": "GB/s",
                         "frac": ops["mul_relin"]["hbm_frac"], "traffic": rns_traffic("mul_relin", logN, L, K),
                         "peak_source": src,
-                        "traffic_source": "profiles/r1_tier_r_traffic.json (ncu dram bytes per ciphertext, "
+                        "traffic_source": "profiles/r2_tier_r_traffic.json (ncu dram bytes per ciphertext, "
                                           "tools/rns_traffic.py, batch 16)",
                         "note": "the key switch's intermediates and the two-pass NTTs go through HBM (real traffic "
                                 "~3.5x the algorithmic bytes); the NTT passes are FP64-issue/latency bound "
-                                "(ncu: FP64 pipe 40-56%, issue 47-51%), see profiles/r1_tier_r.md"},
+                                "(ncu: FP64 pipe 42-54%, issue 46-51%); base conversion on tcgen05 (k_conv_tc), "
+                                "see profiles/r2_summary.md"},
            "parity_vs_oracle": rns_parity_small(),
            "znorm": rns_znorm(torch, stream)}
     if with_cpu:
@@ -418,18 +421,19 @@ def tier_r_section(torch, stream, batch=64, with_cpu=True):
 
 
 def rns_traffic(op, logN, L, K):
-    """DRAM bytes per ciphertext of a Tier-R op from profiles/r1_tier_r_traffic.json (None if absent
-    or captured at another shape)."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_tier_r_traffic.json")
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        sh = d["shape"]
-        if (sh["logN"], sh["L"], sh["K"]) != (logN, L, K):
-            return None
-        return d["ops"][op]["dram_bytes_per_ct"]
-    except (OSError, KeyError, ValueError):
-        return None
+    """DRAM bytes per ciphertext of a Tier-R op from profiles/r2_tier_r_traffic.json (or round 1's),
+    None if absent or captured at another shape."""
+    for name in ("r2_tier_r_traffic.json", "r1_tier_r_traffic.json"):
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            sh = d["shape"]
+            if (sh["logN"], sh["L"], sh["K"]) == (logN, L, K):
+                return d["ops"][op]["dram_bytes_per_ct"]
+        except (OSError, KeyError, ValueError):
+            pass
+    return None
 
 
 def kstat_traffic():

@@ -1,9 +1,9 @@
 """Per-op DRAM traffic of the Tier-R primitives (run on the GPU box; needs ncu).
 
-  python tools/rns_traffic.py OUT.json [--batch 16]
+  python tools/rns_traffic.py OUT.json [--batch 16] [--dnum 2 --K 13]
 
-For each op, one eager call on `batch` ciphertexts (N=2^16, L=24, K=9, dnum=3, 44-bit special
-primes: the bench shape) under ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+For each op, one eager call on `batch` ciphertexts (N=2^16, L=24, 44-bit special primes; dnum/K as
+given, default the bench shape dnum=2, K=13) under ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
 gpu__time_duration.sum; the kernels of the call are summed and divided by the batch.  ncu
 serialises launches and flushes caches between them, so traffic is an upper bound of what the
 graph-replayed bench sees; times here are NOT bench values."""
@@ -17,7 +17,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out_path = sys.argv[1]
 batch = int(sys.argv[sys.argv.index("--batch") + 1]) if "--batch" in sys.argv else 16
-N, l, K, dnum = 1 << 16, 24, 9, 3
+def _arg(name, default):
+    return int(sys.argv[sys.argv.index(name) + 1]) if name in sys.argv else default
+
+
+N, l = 1 << 16, 24
+K, dnum = _arg("--K", 13), _arg("--dnum", 2)
 key = 2 * dnum * (l + 1 + K) * N * 8
 alg = {"ntt": 2 * 2 * (l + 1) * N * 8, "mul_relin": 4 * (l + 1) * N * 8 + key + 2 * (l + 1) * N * 8,
        "mul_relin_rescale": 4 * (l + 1) * N * 8 + key + 2 * l * N * 8,
@@ -29,7 +34,8 @@ res = {"shape": {"logN": 16, "L": l, "K": K, "dnum": dnum, "logp": 44, "batch": 
 for op in ("ntt", "mul_relin", "mul_relin_rescale", "rescale", "rotate"):
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "--profile-from-start", "off", "--csv",
-           sys.executable, os.path.join(ROOT, "tools", "rns_prof.py"), op, "--batch", str(batch), "--reps", "1"]
+           sys.executable, os.path.join(ROOT, "tools", "rns_prof.py"), op, "--batch", str(batch), "--reps", "1",
+           "--K", str(K), "--dnum", str(dnum)]
     txt = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT).stdout
     lines = [x for x in txt.splitlines() if x.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("\n".join(lines))))
