@@ -785,12 +785,33 @@ def main():
         g4.launch()
         c1.record(stream)
         barrier_sync()
+        c0_c1_graph = c0.elapsed_time(c1)
         r01 = float(ctx4.decrypt(H.pearson(ctx4, enc8[0], enc8[1], 20.0), 1)[0])
         from oracle_abi import ST_PEARSON
         refp = oracle().stat(Params(slot_count=S), ST_PEARSON, cols8[0], 20.0, y=cols8[1])
+        # the same table through hs_pearson_table: one launch, one inverse square root per column
+        tab = H.pearson_table(ctx4, enc8, 20.0)
+        tab_ok = bool(np.array_equal(bits(np.array([float(ctx4.decrypt(tab[0], 1)[0])])), bits(refp.out[:1])))
+        del tab
+        best = None
+        for _ in range(5):
+            barrier_sync()
+            t0_ = time.perf_counter()
+            c0.record(stream)
+            tab = H.pearson_table(ctx4, enc8, 20.0)
+            c1.record(stream)
+            c1.synchronize()
+            w_ = 1e3 * (time.perf_counter() - t0_)
+            if best is None or w_ < best[0]:
+                best = (w_, c0.elapsed_time(c1))
+            del tab
         c4_line = {"metric": "C4: 28 Pearson pairs of 8 x 32768 columns, device ms per table (graph replay)",
-                   "value": c0.elapsed_time(c1), "unit": "ms", "B": 20.0, "rho": 0.6,
-                   "pair01_matches_oracle": bool(np.array_equal(bits(np.array([r01])), bits(refp.out[:1])))}
+                   "value": c0_c1_graph, "unit": "ms", "B": 20.0, "rho": 0.6,
+                   "pair01_matches_oracle": bool(np.array_equal(bits(np.array([r01])), bits(refp.out[:1]))),
+                   "pearson_table": {"wall_ms": best[0], "device_ms": best[1], "pair01_matches_oracle": tab_ok,
+                                     "note": "hs_pearson_table: one cooperative launch (8 inverse square roots "
+                                             "instead of 56) + a 4-byte flag read; same slots, levels and meter "
+                                             "as the 28 calls"}}
 
     # ---- max over ranks ---------------------------------------------------------------------------
     t = torch.tensor([dev_ms, e2e_ms, seq_ms], dtype=torch.float64, device="cuda")

@@ -106,4 +106,21 @@ inline Ciphertext pearson(EvalContext& ctx, const EncryptedColumn& col_x, const 
   return ctx.run([&](hs_ct** o) { return hs_pearson(ctx.raw(), &vx.c, &vy.c, B, &c, o); });
 }
 
+// Extension: pearson(cols[i], cols[j]) for every pair i < j, in that order (hs_pearson_table).
+inline std::vector<Ciphertext> pearson_table(EvalContext& ctx, const std::vector<EncryptedColumn>& cols, double B,
+                                             const InvRootConfig& cfg = {}) {
+  std::vector<EncryptedColumn::CView> views;
+  views.reserve(cols.size());
+  for (const EncryptedColumn& c : cols) views.push_back(c.to_c());
+  std::vector<const hs_column*> ptrs;
+  for (const auto& v : views) ptrs.push_back(&v.c);
+  const hs_invroot_cfg c = cfg.to_c();
+  const size_t np = cols.size() * (cols.empty() ? 0 : cols.size() - 1) / 2;
+  std::vector<hs_ct*> hs(np ? np : 1, nullptr);
+  gpu::check(hs_pearson_table(ctx.raw(), ptrs.data(), static_cast<uint32_t>(cols.size()), B, &c, hs.data()));
+  std::vector<Ciphertext> out;
+  for (size_t k = 0; k < np; ++k) out.push_back(Ciphertext::adopt(hs[k]));
+  return out;
+}
+
 }  // namespace hestat

@@ -209,6 +209,13 @@ int hs_coeff_variation(hs_ctx* ctx, const hs_column* col, double B, const hs_sig
                        const hs_invroot_cfg* cfg, hs_ct** out);                       /* :216 */
 int hs_pearson(hs_ctx* ctx, const hs_column* x, const hs_column* y, double B,
                const hs_invroot_cfg* cfg, hs_ct** out);                               /* :239 */
+/* Extension (SURVEY 8(d) C4's "deduplicated batched variant"): pearson(cols[i], cols[j]) for
+ * every pair i < j of ncols columns, in that order, into out[ncols (ncols - 1) / 2]: the same
+ * slots, levels and meter as the sequential calls; one launch for up to 8 single-chunk columns
+ * of equal length (one inverse square root per column), the sequential calls otherwise.  An
+ * error leaves no output (the meter is the sequential calls' at the error). */
+int hs_pearson_table(hs_ctx* ctx, const hs_column* const* cols, uint32_t ncols, double B,
+                     const hs_invroot_cfg* cfg, hs_ct** out);
 
 /* ---- host-side data helpers (data.hpp / plain.hpp; CPU, not the hot path) ------ */
 int hs_synthetic_uniform(uint64_t seed, uint64_t n, double lo, double hi, double* out); /* data.hpp:148 */

@@ -759,6 +759,37 @@ int hs_pearson(hs_ctx* c, const hs_column* x, const hs_column* y, double B, cons
   });
 }
 
+int hs_pearson_table(hs_ctx* c, const hs_column* const* cols, uint32_t ncols, double B, const hs_invroot_cfg* cfg,
+                     hs_ct** out) {
+  return guard([&] {
+    need(out, "out");
+    if (ncols && !cols) fail(HS_E_INVALID_ARG, "hs_pearson_table: null columns");
+    const size_t np = size_t(ncols) * (ncols ? ncols - 1 : 0) / 2;
+    std::vector<hs_ct*> res;
+    auto release = [&] {
+      for (hs_ct* h : res) hs_ct_release(h);
+    };
+    try {
+      if (ctxp(c)->rns) {  // RNS-backed: the sequential calls (rns_eval batches inside each)
+        hs_ctx* cc = c;
+        rns::RnsB& rb = *cc->rns->b;
+        for (uint32_t i = 0; i < ncols; ++i)
+          for (uint32_t j = i + 1; j < ncols; ++j)
+            res.push_back(rwrap(cc, flow::pearson(rb, rcol_of(cc, cols[i]), rcol_of(cc, cols[j]), B, cfg_of(cfg))));
+      } else {
+        std::vector<pipe::ColC> cs;
+        for (uint32_t i = 0; i < ncols; ++i) cs.push_back(col_of(cols[i]));
+        for (Ct& r : pipe::pearson_table(ctxp(c), cs, B, cfg_of(cfg))) res.push_back(wrap(std::move(r)));
+      }
+    } catch (...) {
+      release();
+      throw;
+    }
+    if (res.size() != np) fail(HS_E_ERROR, "hs_pearson_table: internal pair count");
+    std::copy(res.begin(), res.end(), out);
+  });
+}
+
 // ---- host-side data helpers (data.hpp:148-208, plain.hpp:18-92) -------------------------------
 int hs_synthetic_uniform(uint64_t seed, uint64_t n, double lo, double hi, double* out) {
   return guard([&] {

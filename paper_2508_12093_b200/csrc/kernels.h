@@ -131,6 +131,28 @@ struct StatArgs {
   double* scratch = nullptr;  // >= 2 * 6 * S doubles (butterfly fallback)
 };
 void run_stat(QSpec q, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s);
+
+// ---- stat.cu: the C4 Pearson table in one cooperative kernel -----------------------------
+// All ncols (<= 8) single-chunk columns' moments (phase A), every pair's centred product sum
+// (phase B: pair p = (pi[p], pj[p]), the x side masked past n_valid as centered_chunks does),
+// one inverse square root per COLUMN (phase C: the program `p`, M_LDR 0/1 = mu/var of the
+// item's column, its M_ST writes inv + col * S), and per pair out[p] = (cov_p inv_i) inv_j
+// (phase D, block-local).  Requires exact grid sums (QGrid): when a sum is not provably exact the
+// kernel sets *inexact and writes nothing (the host replays the pairs one by one).
+constexpr int kMaxTableCols = 8, kMaxTablePairs = kMaxTableCols * (kMaxTableCols - 1) / 2;
+struct PTableArgs {
+  int ncols = 0, npairs = 0;
+  const double* x[kMaxTableCols];
+  uint64_t valid = 0;            // n_valid (< S: the x side of every product is masked)
+  double cm = 0, ca = 0, cmp = 0;  // mean_scaled(B = 1), variance_to_scale(B^2) constants
+  double inv_n = 0;
+  uint8_t pi[kMaxTablePairs], pj[kMaxTablePairs];
+  double* out[kMaxTablePairs];
+  double* partial = nullptr;     // ptable_partial_doubles(), zero between launches
+  unsigned* inexact = nullptr;
+};
+size_t ptable_partial_doubles();
+void run_ptable(QSpec q, const PTableArgs& a, const Prog& p, int lanes, cudaStream_t s);
 size_t stat_partial_doubles();  // scratch sizing for StatArgs::partial
 
 }  // namespace k

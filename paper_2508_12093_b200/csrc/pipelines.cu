@@ -320,6 +320,10 @@ class PB {
 
   void launch() { finish(false, nullptr); }
   void launch_stat(const k::StatArgs& a) { finish(true, &a); }
+  void launch_table(const k::PTableArgs& a) {
+    table_ = &a;
+    finish(false, nullptr);
+  }
 
  private:
   void finish(bool stat, const k::StatArgs* a) {
@@ -362,7 +366,8 @@ class PB {
       prog_.flags = debug_flag_word();
       cuda_ok(cudaMemsetAsync(prog_.flags, 0, sizeof(unsigned), rt.stream()), "debug flags");
     }
-    if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
+    if (table_) k::run_ptable(q_, *table_, prog_, lanes, rt.stream());
+    else if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
     else k::run_prog(q_, prog_, lanes, rt.stream());
 #ifdef HS_HOST_PROFILE
     tl += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - l0).count();
@@ -435,6 +440,7 @@ class PB {
   int nreg_ = 0, nin_ = 0, nout_ = 0;
   bool big_cheb_ = false;
   std::vector<std::pair<int, Series>> chebs_;
+  const k::PTableArgs* table_ = nullptr;
 };
 
 // ---- statistics: one cooperative launch per call (stat.cu) ------------------------------
@@ -800,6 +806,83 @@ Ct pearson(hs_ctx* ctx, const ColC& x, const ColC& y, double B, const InvCfg& cf
     ctx->m = m;
     return make_out(ctx, out, r.level);
   }, dev);
+}
+
+// C4's table: pearson(cols[i], cols[j]) for every pair i < j, in that order, in one launch
+// (kernels.h PTableArgs).  Reference semantics: the same values, levels and meter as the
+// sequential calls (each pair's ledger replayed in order); one inverse square root per column
+// instead of two per pair, since pearson(x, y) evaluates crypto_invsqrt of the same var_x ciphertext
+// for every y (identical inputs, identical ops: identical slots).  Cases the kernel does not take
+// (debug_checks, more than 8 or multi-chunk columns, unequal lengths, quantize off, a ledger error,
+// or a sum that is not provably exact) run the pairs one by one.
+std::vector<Ct> pearson_table(hs_ctx* ctx, const std::vector<ColC>& cols, double B, const InvCfg& cfg) {
+  const size_t n = cols.size();
+  auto sequential = [&] {
+    std::vector<Ct> out;
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = i + 1; j < n; ++j) out.push_back(pearson(ctx, cols[i], cols[j], B, cfg));
+    return out;
+  };
+  const Params& p = ctx->p;
+  bool ok = n >= 2 && n <= static_cast<size_t>(k::kMaxTableCols) && !p.debug && p.quantize && cfg_ok(cfg) &&
+            Runtime::get().fused;
+  for (const ColC& c : cols) ok = ok && col_ok(ctx, c) && c.chunks.size() == 1 && c.n_valid == cols[0].n_valid;
+  if (!ok) return sequential();
+  const Meter m0 = ctx->m;
+  std::vector<int> levels;
+  try {
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = i + 1; j < n; ++j) {
+        auto [r, m] = ledger(ctx, Key("pearson", ctx->p).col(cols[i]).col(cols[j]).add(B).cfg(cfg),
+                             [&](SymB& sb) { return flow::pearson(sb, sym(cols[i]), sym(cols[j]), B, cfg); });
+        ctx->m = m;
+        levels.push_back(r.level);
+      }
+  } catch (const Error& e) {
+    if (e.code == HS_E_CUDA) throw;
+    ctx->m = m0;
+    return sequential();
+  }
+  const Meter m_all = ctx->m;
+  Runtime& rt = Runtime::get();
+  const size_t S = p.S;
+  k::PTableArgs a{};
+  a.ncols = static_cast<int>(n);
+  const double nv = static_cast<double>(cols[0].n_valid), Sv = B * B;
+  a.valid = cols[0].n_valid;
+  a.cm = 1.0 / (1.0 * nv);               // mean_scaled(col, 1), stats.hpp:101
+  a.ca = 1.0 / std::sqrt(Sv * nv);       // variance_to_scale(col, B^2), stats.hpp:117
+  a.cmp = 1.0 / (nv * std::sqrt(Sv));    // stats.hpp:123
+  a.inv_n = 1.0 / nv;                    // mean_of_chunks, stats.hpp:83
+  for (size_t c = 0; c < n; ++c) a.x[c] = cols[c].chunks[0]->device();
+  std::vector<DevBuf> outs;
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = i + 1; j < n; ++j) {
+      a.pi[a.npairs] = static_cast<uint8_t>(i);
+      a.pj[a.npairs] = static_cast<uint8_t>(j);
+      outs.push_back(rt.alloc(S));
+      a.out[a.npairs] = outs.back().get();
+      ++a.npairs;
+    }
+  a.partial = rt.scratch(3, k::ptable_partial_doubles(), true);
+  DevBuf inexact = rt.alloc(1);
+  a.inexact = reinterpret_cast<unsigned*>(inexact.get());
+  cuda_ok(cudaMemsetAsync(a.inexact, 0, sizeof(unsigned), rt.stream()), "pearson table flag");
+  DevBuf inv = rt.alloc(n * S);
+  PB pb(p);
+  pb.st(pb.invsqrt(pb.ldr(1), B * B, cfg), inv.get());  // crypto_invsqrt(var, B^2), pearson's inv_x / inv_y
+  pb.launch_table(a);
+  unsigned flag = 0;
+  cuda_ok(cudaMemcpyAsync(&flag, a.inexact, sizeof flag, cudaMemcpyDeviceToHost, rt.stream()), "pearson table flag");
+  cuda_ok(cudaStreamSynchronize(rt.stream()), "pearson table flag");
+  if (flag) {  // a sum beyond the exact-sum bound: the literal butterflies, pair by pair
+    ctx->m = m0;
+    return sequential();
+  }
+  ctx->m = m_all;
+  std::vector<Ct> out;
+  for (size_t k = 0; k < outs.size(); ++k) out.push_back(make_out(ctx, outs[k], levels[k]));
+  return out;
 }
 
 }  // namespace pipe

@@ -279,6 +279,129 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
   stamp(4);
 }
 
+// ---- the C4 Pearson table (kernels.h PTableArgs) ----------------------------------------------
+constexpr int kTA = 3 * kMaxTableCols, kTB = kMaxTablePairs;  // phase A / B arrays
+constexpr int kTChunk = 8;                                      // arrays reduced per pass
+
+// Block sums (and |sums|) of arrays [a0, a0 + n) (n <= kTChunk) into the grid-wide totals.
+template <class TermFn>
+__device__ void table_accumulate(TermFn term, int a0, int n, const Range& BR, double* accum) {
+  __shared__ double red[kMaxWarps][2 * kTChunk];
+  double acc[2 * kTChunk];
+#pragma unroll
+  for (int k = 0; k < 2 * kTChunk; ++k) acc[k] = 0.0;
+  for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < kTChunk; ++k)
+      if (k < n) {
+        const double t = term(a0 + k, i);
+        acc[2 * k] += t;
+        acc[2 * k + 1] += fabs(t);
+      }
+  }
+#pragma unroll
+  for (int k = 0; k < 2 * kTChunk; ++k)
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 2 * kTChunk; ++k) red[threadIdx.x >> 5][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < 2 * n) {
+    double s = 0.0;
+    for (unsigned w = 0; w < blockDim.x / 32; ++w) s += red[w][threadIdx.x];
+    // integer terms, checked bound below: exact in any order (grid_sum's argument)
+    atomicAdd(accum + 2 * a0 + threadIdx.x, s);
+  }
+  __syncthreads();
+}
+
+// Grid barrier, then the totals of arrays [0, n) into tot[] (shared); false when a sum is not
+// provably exact.  The last block to read zeroes the totals and its counter for the next launch.
+__device__ bool table_totals(const GridBar& grid, double* accum, unsigned* count, int n, double* tot) {
+  grid.sync();
+  for (int k = threadIdx.x; k < 2 * n; k += blockDim.x) tot[k] = __ldcg(accum + k);
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(count, 1u) == gridDim.x - 1) {
+    for (int k = 0; k < 2 * n; ++k) accum[k] = 0.0;
+    *count = 0u;
+  }
+  bool exact = true;
+  for (int k = 0; k < n; ++k) exact = exact && tot[2 * k + 1] < 4503599627370496.0;  // 2^52
+  return exact;
+}
+
+template <class Q, int P>
+__global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const __grid_constant__ PTableArgs a,
+                                                         const __grid_constant__ Prog pg) {
+  extern __shared__ double stab[];
+  __shared__ double totA[2 * kTA], totB[2 * kTB];
+  double* accA = a.partial;
+  double* accB = a.partial + 2 * kTA;
+  unsigned* counts = reinterpret_cast<unsigned*>(a.partial + 2 * (kTA + kTB));
+  const GridBar grid{counts + 2};
+  const unsigned S = pg.S;
+  const Range BR = block_range(S);
+  for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
+  // ---- phase A: per column mean_scaled(B = 1) and variance_to_scale(B^2) terms ----
+  const int NA = 3 * a.ncols;
+  auto termA = [&](int k, unsigned i) -> double {
+    const int c = k / 3, t = k - 3 * c;
+    const double X = q.in(__ldg(a.x[c] + i));
+    if (t == 0) return q.mulc(X, a.cm);                       // mul_pt(chunk, 1/(B n))
+    if (t == 1) {
+      const double sx = q.mulc(X, a.ca);                      // mul_pt(chunk, 1/sqrt(S n))
+      return q.mul(sx, sx);                                   // mul_ct(a, a)
+    }
+    return q.mulc(X, a.cmp);                                  // mul_pt(chunk, 1/(n sqrt(S)))
+  };
+  for (int a0 = 0; a0 < NA; a0 += kTChunk) table_accumulate(termA, a0, min(kTChunk, NA - a0), BR, accA);
+  if (!table_totals(grid, accA, counts, NA, totA)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.inexact = 1u;
+    return;
+  }
+  // per-column mu, var (every slot holds the exact totals)
+  auto mu = [&](int c) { return totA[2 * (3 * c)]; };
+  auto var = [&](int c) {
+    const double sq = totA[2 * (3 * c + 1)], mp = totA[2 * (3 * c + 2)];
+    return q.sub(sq, q.mul(mp, mp));                          // sub_ct(sq_sum, mul_ct(mp, mp))
+  };
+  // ---- phase B: every pair's centred product, mean_of_chunks(1/n) ----
+  auto termB = [&](int p, unsigned i) -> double {
+    const int ci = a.pi[p], cj = a.pj[p];
+    const double mi = mu(ci);
+    const double mm = a.valid < S ? q.mulc(mi, i < a.valid ? 1.0 : 0.0) : mi;  // mul_pt(mu, mask)
+    const double cx = q.sub(q.in(__ldg(a.x[ci] + i)), mm);
+    const double cy = q.sub(q.in(__ldg(a.x[cj] + i)), mu(cj));
+    return q.mulc(q.mul(cx, cy), a.inv_n);
+  };
+  for (int b0 = 0; b0 < a.npairs; b0 += kTChunk) table_accumulate(termB, b0, min(kTChunk, a.npairs - b0), BR, accB);
+  if (!table_totals(grid, accB, counts + 1, a.npairs, totB)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.inexact = 1u;
+    return;
+  }
+  if (BR.lo >= BR.hi) return;
+  // ---- phase C: the inverse square root of every column's variance, this block's slots ----
+  const unsigned items = (BR.hi - BR.lo) * static_cast<unsigned>(a.ncols);
+  const unsigned iters = (items * P + blockDim.x - 1) / blockDim.x;
+  for (unsigned it = 0; it < iters; ++it) {
+    const unsigned g = threadIdx.x + it * blockDim.x, item = g / P;
+    const bool live = item < items;
+    const unsigned it2 = live ? item : items - 1;
+    const unsigned c = it2 / (BR.hi - BR.lo), s = BR.lo + it2 % (BR.hi - BR.lo);
+    double sv[5] = {mu(static_cast<int>(c)), var(static_cast<int>(c)), 0.0, 0.0, 0.0};
+    exec<Q, P>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
+  }
+  __syncthreads();  // the block's inverse roots (global, this block's slots) are visible to it
+  // ---- phase D: pearson's epilogue per pair, mul_ct(mul_ct(cov, inv_x), inv_y) ----
+  const double* inv = pg.out[0];
+  const unsigned pitems = (BR.hi - BR.lo) * static_cast<unsigned>(a.npairs);
+  for (unsigned g = threadIdx.x; g < pitems; g += blockDim.x) {
+    const unsigned p = g / (BR.hi - BR.lo), s = BR.lo + g % (BR.hi - BR.lo);
+    const double ix = q.in(__ldcg(inv + a.pi[p] * S + s)), iy = q.in(__ldcg(inv + a.pj[p] * S + s));
+    a.out[p][s] = q.out(q.mul(q.mul(totB[2 * p], ix), iy));
+  }
+}
+
 template <class F>
 void with_q(QSpec qs, F&& f) {
   const double s = ldexp(1.0, qs.bits), inv = ldexp(1.0, -qs.bits);
@@ -327,6 +450,32 @@ int max_blocks(K kern, size_t smem, int threads) {
 
 // two sets of 2 kNK totals, two block counters, the grid barrier's two words
 size_t stat_partial_doubles() { return 4 * kNK + 2; }
+// the table's 2 (kTA + kTB) totals, two block counters and its grid barrier word
+size_t ptable_partial_doubles() { return 2 * (kTA + kTB) + 2; }
+
+void run_ptable(QSpec qs, const PTableArgs& a, const Prog& p, int lanes, cudaStream_t s) {
+  if (p.S == 0) return;
+  if (qs.mode != QMode::Grid) fail(HS_E_ERROR, "pearson table: exact grid sums need quantize = true");
+  const QGrid Q{ldexp(1.0, qs.bits), ldexp(1.0, -qs.bits)};
+  const size_t smem = static_cast<size_t>(p.ntab) * sizeof(double);
+  auto go = [&](auto kern, int P) {
+    const int maxt = P == 1 ? prog_max_threads<1>() : (P == 2 ? prog_max_threads<2>() : prog_max_threads<4>());
+    const Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+    const int cap = max_blocks(kern, smem, static_cast<int>(geo.threads));
+    if (cap < static_cast<int>(geo.blocks)) fail(HS_E_CUDA, "pearson table kernel: grid not co-resident");
+    QGrid qv = Q;
+    PTableArgs av = a;
+    Prog pv = p;
+    void* args[] = {&qv, &av, &pv};
+    cuda_ok(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(geo.blocks), dim3(geo.threads), args,
+                                        smem, s),
+            "pearson table launch");
+  };
+  if (lanes == 4) go(k_ptable<QGrid, 4>, 4);
+  else if (lanes == 2) go(k_ptable<QGrid, 2>, 2);
+  else go(k_ptable<QGrid, 1>, 1);
+  Runtime::get().note_launch();
+}
 
 void run_stat(QSpec qs, const StatArgs& a, const Prog& p, int lanes, cudaStream_t s) {
   if (p.S == 0) return;

@@ -600,6 +600,24 @@ def pearson(ctx: EvalContext, col_x: EncryptedColumn, col_y: EncryptedColumn, B:
     return r
 
 
+def pearson_table(ctx: EvalContext, cols: Sequence[EncryptedColumn], B: float,
+                  cfg: Optional[InvRootConfig] = None) -> List[Ciphertext]:
+    """pearson(cols[i], cols[j]) for every pair i < j, in that order (hs_pearson_table: one
+    launch for up to 8 single-chunk columns; same slots, levels and meter as the calls)."""
+    cs, keep = [], []
+    for col in cols:
+        c, k = col._c()
+        cs.append(c)
+        keep.append(k)
+    arr = (C.POINTER(_abi.hs_column) * max(len(cs), 1))(*[C.pointer(c) for c in cs])
+    npairs = len(cs) * (len(cs) - 1) // 2
+    hs = (C.c_void_p * max(npairs, 1))()
+    _check(_abi.lib().hs_pearson_table(ctx._h, arr, len(cs), float(B), _cfg(cfg),
+                                       C.cast(hs, C.POINTER(C.c_void_p))))
+    del keep
+    return [Ciphertext._own(C.c_void_p(hs[k])) for k in range(npairs)]
+
+
 # ---- data.hpp / plain.hpp (host) --------------------------------------------------------------------
 def synthetic_uniform(seed: int, n: int, lo: float, hi: float) -> np.ndarray:  # data.hpp:148-160
     out = np.empty(max(int(n), 1))
