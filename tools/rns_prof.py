@@ -17,8 +17,10 @@ ap.add_argument("--dnum", type=int, default=3)
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--logp", type=int, default=44)
+ap.add_argument("--logq", type=int, default=40)
+ap.add_argument("--logq0", type=int, default=60)
 a = ap.parse_args()
-spec = RnsSpec(a.logN, a.L, a.K, a.dnum, logp=a.logp, seed=1)
+spec = RnsSpec(a.logN, a.L, a.K, a.dnum, logq0=a.logq0, logq=a.logq, logp=a.logp, seed=1)
 c = RnsContext(spec)
 c.prepare_relin()
 c.prepare_rotation(1)
