@@ -1306,44 +1306,54 @@ __global__ void __launch_bounds__(kT, HS_INNER_MINB) k_ks_inner(const uint64_t* 
                                                  const uint64_t* kb, const uint64_t* ka, const PrimeC* pcs,
                                                  uint32_t nx, uint32_t nl, uint32_t np, uint32_t nq, uint32_t alpha,
                                                  uint32_t logN, uint32_t batch, const KsSrc src) {
-  const size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  // two adjacent coefficients per thread: 16-byte loads and stores (twice the bytes in flight per
+  // instruction; the kernel streams ext/acc once per batch item)
+  const size_t x = 2 * (blockIdx.x * size_t(blockDim.x) + threadIdx.x);
   const uint32_t row = x >> logN, n = x & ((1u << logN) - 1);
   if (row >= nx) return;
   const uint32_t gi = row < nl ? row : nq + (row - nl);
   const PrimeC P = pcs[gi];
-  uint64_t kbr[ND], kar[ND];
+  ulonglong2 kbr[ND], kar[ND];
 #pragma unroll
   for (int j = 0; j < ND; ++j) {
     const size_t kx = (size_t(j * np + gi) << logN) + n;
-    kbr[j] = __ldg(kb + kx);
-    kar[j] = __ldg(ka + kx);
+    kbr[j] = __ldg(reinterpret_cast<const ulonglong2*>(kb + kx));
+    kar[j] = __ldg(reinterpret_cast<const ulonglong2*>(ka + kx));
   }
   const uint32_t own = row < nl ? row / alpha : 0xFFFFFFFFu;
   const size_t rowsN = size_t(nx) << logN;
   // d on the digit's own rows: materialised, or the tensor / automorphism of the inputs
-  auto own_word = [&](uint32_t b) -> uint64_t {
+  auto own_word = [&](uint32_t b) -> ulonglong2 {
     if (src.mode == KS_TENSOR) {
       const size_t o = b * src.stride + (size_t(nl + row) << logN) + n;
-      return mul_mod(src.a[o], src.b[o], P);
+      const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(src.a + o);
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src.b + o);
+      return make_ulonglong2(mul_mod(u.x, v.x, P), mul_mod(u.y, v.y, P));
     }
-    if (src.mode == KS_PERM) return src.a[b * src.stride + (size_t(nl + row) << logN) + galois_src(n, src.g, logN)];
-    return d[b * d_stride + x];
+    if (src.mode == KS_PERM) {
+      const uint64_t* r = src.a + b * src.stride + (size_t(nl + row) << logN);
+      return make_ulonglong2(r[galois_src(n, src.g, logN)], r[galois_src(n + 1, src.g, logN)]);
+    }
+    return *reinterpret_cast<const ulonglong2*>(d + b * d_stride + x);
   };
 #pragma unroll(kInnerUnroll)
   for (uint32_t b = 0; b < batch; ++b) {
     const uint64_t* E = ext + b * ext_stride + x;
-    uint64_t e[ND];
+    ulonglong2 e[ND];
 #pragma unroll
-    for (int j = 0; j < ND; ++j) e[j] = uint32_t(j) == own ? own_word(b) : E[j * rowsN];
-    u128 s0 = 0, s1 = 0;
+    for (int j = 0; j < ND; ++j)
+      e[j] = uint32_t(j) == own ? own_word(b) : *reinterpret_cast<const ulonglong2*>(E + j * rowsN);
+    u128 s0 = 0, s1 = 0, t0 = 0, t1 = 0;
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
-      s0 += static_cast<u128>(e[j]) * kbr[j];
-      s1 += static_cast<u128>(e[j]) * kar[j];
+      s0 += static_cast<u128>(e[j].x) * kbr[j].x;
+      s1 += static_cast<u128>(e[j].x) * kar[j].x;
+      t0 += static_cast<u128>(e[j].y) * kbr[j].y;
+      t1 += static_cast<u128>(e[j].y) * kar[j].y;
     }
     uint64_t* Ac = acc + b * acc_stride + x;
-    Ac[0] = reduce128(s0, P);
-    Ac[rowsN] = reduce128(s1, P);
+    *reinterpret_cast<ulonglong2*>(Ac) = make_ulonglong2(reduce128(s0, P), reduce128(t0, P));
+    *reinterpret_cast<ulonglong2*>(Ac + rowsN) = make_ulonglong2(reduce128(s1, P), reduce128(t1, P));
   }
 }
 
@@ -2238,7 +2248,7 @@ void key_switch(Ctx& c, uint32_t level, const uint64_t* d, size_t d_stride, cons
   ntt_rows(c, EXT, ext_stride, EXT, ext_stride, P.up_rows, P.up_rows, P.up_primes, batch, false);
   // inner product with the key (each key word read once per call)
   {
-    const unsigned g = (unsigned)((size_t(nx) * N + kT - 1) / kT);
+    const unsigned g = (unsigned)((size_t(nx) * N / 2 + kT - 1) / kT);  // two coefficients per thread
     const KsSrc ksrc = src ? *src : KsSrc{};
     switch (nd) {
 #define HS_INNER_CASE(D)                                                                                          \
