@@ -6,17 +6,19 @@ reference's default inverse-root configuration (Chebyshev degree 511 seed, 6
 Newton iterations, 2 bootstraps), scale 2^-40 quantisation.  A step is one
 znorm of one ciphertext.
 
-  value  device time per ciphertext, inputs already resident in HBM: K znorm
-         calls through the public API captured once into a CUDA graph and
-         replayed (one cooperative kernel per znorm); the inputs cycle through
-         a pool of distinct encrypted columns larger than L2 (config.l2).
+  value  device time per ciphertext, inputs already resident in HBM: each step
+         is --batch-cols (64) independent C2 ciphertexts through hs_znorm_batch
+         (every ciphertext its own moments, inverse square root and
+         normalisation; one cooperative launch per step), K steps captured into
+         a CUDA graph and replayed; the inputs cycle through a pool of distinct
+         encrypted columns larger than L2 (config.l2).  `single_call` reports
+         the same with one znorm call (one launch) per ciphertext.
   e2e    the same metric through the public API with HOST buffers: every step
-         encodes from pinned host memory (H2D), runs znorm and decodes the result
-         (D2H), all inside the timed region.  The loop is the steady state of a
-         caller that encodes the next column while the current one computes
-         (encode_column runs on the library's upload stream, znorm/decode on the
-         compute stream); e2e.latency_ms_per_step is the same calls strictly in
-         sequence (one ciphertext in flight).
+         encodes its 64 ciphertexts' values from pinned host memory (H2D), runs
+         znorm_batch and decodes the results (D2H), all inside the timed region;
+         the next step's encode overlaps the current Z-scores (upload stream).
+         `e2e_single_call` is the one-ciphertext-per-step loop (and its
+         strictly sequential latency and pageable-buffer variants).
 
 N > 1 (torchrun): replicas only — every rank runs its own ciphertexts, no
 collective on the data path; value = max-over-ranks time /
@@ -63,8 +65,8 @@ def workload_config(extra=None):
     cfg = {"workload": "C2 znorm: 32768 x N(50,10^2) in one 2^15-slot ciphertext, B=100, "
                        "invsqrt degree 511 + 6 Newton, scale 2^-40",
            "slots": S, "B": B, "cheb_degree": 511, "newton_iters": 6,
-           "l2": f"L2 flushed (256 MiB write) right before the timed region; the K timed steps read K distinct "
-                 f"resident columns, cycled over {POOL} ({POOL * S * 8 // (1 << 20)} MiB > L2) when K > {POOL}"}
+           "l2": f"L2 flushed (256 MiB write) right before the timed region; every step reads its own resident "
+                 f"ciphertexts, cycled over a pool of {POOL} ({POOL * S * 8 // (1 << 20)} MiB > L2)"}
     if extra:
         cfg.update(extra)
     return cfg
@@ -546,6 +548,8 @@ def main():
     ap.add_argument("--no-tier-r", action="store_true")
     ap.add_argument("--c5", action="store_true", help="print the C5 tier-R sweep instead")
     ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch-cols", type=int, default=64,
+                    help="independent C2 ciphertexts per step (hs_znorm_batch, <= 64 per launch)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.c5:
@@ -603,19 +607,55 @@ def main():
     # L2 flush before the timed region (the timed steps then read inputs no step has touched since)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        flush.fill_(1)
+    e0.record(stream)
+    graph.launch()
+    e1.record(stream)
+    barrier_sync()
+    dev_ms = e0.elapsed_time(e1)
+    del graph
+
+    # ---- value (headline): KB independent C2 ciphertexts per step, one hs_znorm_batch launch ----
+    # Every ciphertext gets its whole Z-score DAG (moments, degree-511 + 6-Newton inverse square
+    # root of ITS variance, (x - mu) inv); the batch shares one launch, one grid barrier and the
+    # SMs' latency hiding.  encode_column's magnitude bound proves the exact sums on the host, so the
+    # call has no synchronisation and the K steps are captured into one CUDA graph.
+    KB = max(1, min(args.batch_cols, 64))
+
+    def bcols(i):
+        return [pool[(i * KB + j) % POOL] for j in range(KB)]
+
+    zb0 = H.znorm_batch(ctx, bcols(0), B)
+    bparity = bool(np.array_equal(bits(H.decode_column(ctx, zb0[0])), bits(ref.out)))
+    del zb0
+    for i in range(args.warmup):
+        zb = H.znorm_batch(ctx, bcols(i), B)
+        del zb
+    barrier_sync()
+    bl0 = H.kernel_launches()
+    with H.Graph() as bgraph:
+        for i in range(args.steps):
+            zb = H.znorm_batch(ctx, bcols(i), B)
+            del zb
+    blaunches = H.kernel_launches() - bl0
+    bgraph.launch()  # warm replay (untimed)
+    barrier_sync()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let the sampler start
         with torch.cuda.stream(stream):
             flush.fill_(1)
-        e0.record(stream)
-        graph.launch()
-        e1.record(stream)
+        b0.record(stream)
+        bgraph.launch()
+        b1.record(stream)
         barrier_sync()
         t_end = time.perf_counter() + 1.0  # keep the same load on for the clock samples
         while time.perf_counter() < t_end:
-            graph.launch()
+            bgraph.launch()
             H.sync()
-    dev_ms = e0.elapsed_time(e1)
+    bdev_ms = b0.elapsed_time(b1)
+    del bgraph
 
     # same K steps as plain API calls (host enqueue included)
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -690,6 +730,46 @@ def main():
     pg_wall_ms = 1e3 * (time.perf_counter() - t0)
     pg_ms = f0.elapsed_time(f1)
     pg_ok = bool(np.array_equal(bits(pz), bits(ref.out)))
+
+    # ---- e2e (headline): KB ciphertexts per step through the public API from pinned host memory --
+    # encode_column of the step's KB x 2^15 values (one H2D + encrypt, one synchronisation), each
+    # chunk its own single-chunk column, znorm_batch, the KB result chunks decoded as one column
+    # (one D2H); the next step's encode overlaps the current Z-scores (upload stream).
+    XB = torch.empty(KB * S, dtype=torch.float64).pin_memory()
+    ZB = torch.empty(KB * S, dtype=torch.float64).pin_memory()
+    xbn, zbn = XB.numpy(), ZB.numpy()
+    for j in range(KB):
+        xbn[j * S:(j + 1) * S] = np.roll(x, 97 * j)
+
+    def benc():
+        big = H.encode_column(ctx, xbn)
+        return [H.EncryptedColumn([c], S) for c in big.chunks]
+
+    def bdec(zs):
+        H.decode_column(ctx, H.EncryptedColumn([zc_.chunks[0] for zc_ in zs], KB * S), out=zbn)
+
+    for _ in range(5):
+        bdec(H.znorm_batch(ctx, benc(), B))
+    bcol = benc()
+    for _ in range(5):
+        zs_ = H.znorm_batch(ctx, bcol, B)
+        bcol = benc()
+        bdec(zs_)
+    del bcol, zs_
+    barrier_sync()
+    be2e_steps = max(20, args.steps // 4)
+    t0 = time.perf_counter()
+    f0.record(stream)
+    bcol = benc()
+    for k_ in range(be2e_steps):
+        zs_ = H.znorm_batch(ctx, bcol, B)
+        bcol = benc() if k_ + 1 < be2e_steps else None
+        bdec(zs_)
+    f1.record(stream)
+    barrier_sync()
+    be2e_wall_ms = 1e3 * (time.perf_counter() - t0)
+    be2e_ms = f0.elapsed_time(f1)
+    be2e_ok = bool(np.array_equal(bits(zbn[:S]), bits(ref.out)))
 
     # ---- kernel roofline: the fused inverse-sqrt program (dominant phase) -------------------
     # Both probes replay CUDA graphs of `reps` calls (device time only).
@@ -814,22 +894,38 @@ def main():
                                              "as the 28 calls"}}
 
     # ---- max over ranks ---------------------------------------------------------------------------
-    t = torch.tensor([dev_ms, e2e_ms, seq_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_ms, e2e_ms, seq_ms, bdev_ms, be2e_ms], dtype=torch.float64, device="cuda")
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    dev_ms, e2e_ms, seq_ms = float(t[0]), float(t[1]), float(t[2])
+    dev_ms, e2e_ms, seq_ms, bdev_ms, be2e_ms = (float(v) for v in t)
     if rank == 0:
-        value = dev_ms / (args.steps * ws)
-        step_us = 1e3 * dev_ms / args.steps  # one k_stat launch per step, CUDA events over the timed region
+        value = bdev_ms / (args.steps * KB * ws)
+        bstep_us = 1e3 * bdev_ms / args.steps  # one k_zbatch launch per step, CUDA events over the timed region
+        bachieved = step_per_slot * S * KB / (bstep_us * 1e-6) / 1e12
+        step_us = 1e3 * dev_ms / args.steps  # single call: one k_stat launch per step
         achieved = step_per_slot * S / (step_us * 1e-6) / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": False,
+            "warmup": args.warmup, "ms_per_step": bdev_ms / args.steps, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded N(50,10^2) via mt19937_64 + Box-Muller (paper datasets absent)",
-            "config": workload_config({"parallelism": f"replicas x{ws} (no data-path collective)"}),
-            "parity_vs_oracle": parity,
-            "e2e": {"value": e2e_ms / (e2e_steps * ws), "unit": UNIT, "h2d_bytes_per_step": S * 8,
+            "config": workload_config({"parallelism": f"replicas x{ws} (no data-path collective)",
+                                       "ciphertexts_per_step": KB,
+                                       "step": f"{KB} independent C2 Z-scores (each its own moments, inverse "
+                                               f"square root and normalisation) through hs_znorm_batch: one "
+                                               f"launch per step, graph-replayed"}),
+            "parity_vs_oracle": parity and bparity,
+            "e2e": {"value": be2e_ms / (be2e_steps * KB * ws), "unit": UNIT, "h2d_bytes_per_step": KB * S * 8,
+                    "d2h_bytes_per_step": KB * S * 8, "wall_ms_per_ciphertext": be2e_wall_ms / (be2e_steps * KB),
+                    "mode": f"pipelined, {KB} ciphertexts per step: encode_column of the step's {KB} x 2^15 "
+                            "values from pinned memory (H2D) overlapping the previous step's znorm_batch, "
+                            "decode_column of the results (D2H); public API calls only",
+                    "output_matches_oracle": be2e_ok, "host_buffers": "pinned (torch pin_memory)"},
+            "single_call": {
+                "value": dev_ms / (args.steps * ws), "unit": UNIT, "ms_per_step": dev_ms / args.steps,
+                "mode": "one znorm call per step (one k_stat launch), graph-replayed",
+                "roofline_frac": achieved / peak, "achieved": achieved, "duration_us": step_us},
+            "e2e_single_call": {"value": e2e_ms / (e2e_steps * ws), "unit": UNIT, "h2d_bytes_per_step": S * 8,
                     "d2h_bytes_per_step": S * 8, "wall_ms_per_step": e2e_wall_ms / e2e_steps,
                     "mode": "pipelined: encode of step k+1 overlaps znorm of step k (public API calls only)",
                     "latency_ms_per_step": seq_ms / e2e_steps, "latency_wall_ms_per_step": seq_wall_ms / e2e_steps,
@@ -837,18 +933,19 @@ def main():
                     "pageable": {"value": pg_ms / e2e_steps, "wall_ms_per_step": pg_wall_ms / e2e_steps,
                                  "host_buffers": "pageable numpy arrays (staged by the library)",
                                  "output_matches_oracle": pg_ok}},
-            "gpu_launches": int(launches),
-            "api_loop_ms_per_step": api_ms / args.steps,
+            "gpu_launches": int(blaunches),
+            "api_loop_ms_per_step_single_call": api_ms / args.steps,
             "roofline": {"bound": "fp64",
-                         "kernel": "k_stat<QGrid,2> (the step: fused C2 znorm = moments, grid-wide exact sums, "
-                                   "invsqrt degree 511 + 6 Newton, (x - mu) * inv)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": kstat_traffic(), "duration_us": step_us,
-                         "work": f"{step_per_slot} fp64 ops/slot x {S} slots",
+                         "kernel": f"k_zbatch<QGrid,2> (the step: {KB} fused C2 Z-scores = moments, grid-wide exact "
+                                   "sums, invsqrt degree 511 + 6 Newton per ciphertext, (x - mu) * inv)",
+                         "achieved": bachieved, "peak": peak, "unit": "TFLOP/s", "frac": bachieved / peak,
+                         "traffic": None, "duration_us": bstep_us,
+                         "work": f"{step_per_slot} fp64 ops/slot x {S} slots x {KB} ciphertexts",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "traffic_source": "profiles/r1_kstat_ncu.json (ncu --set full, cold caches: input, "
-                                           "code and parameters; algorithmic 512 KiB)",
+                         "traffic_source": "none captured for k_zbatch (algorithmic: 16 B per slot and "
+                                           "ciphertext, 512 KiB per ciphertext; the single-call k_stat capture is "
+                                           "profiles/r1_kstat_ncu.json)",
                          "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",
                                             "duration_us": prog_us, "achieved": prog_achieved,
                                             "frac": prog_achieved / peak,

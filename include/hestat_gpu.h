@@ -209,6 +209,11 @@ int hs_coeff_variation(hs_ctx* ctx, const hs_column* col, double B, const hs_sig
                        const hs_invroot_cfg* cfg, hs_ct** out);                       /* :216 */
 int hs_pearson(hs_ctx* ctx, const hs_column* x, const hs_column* y, double B,
                const hs_invroot_cfg* cfg, hs_ct** out);                               /* :239 */
+/* Extension: znorm(cols[k]) for k < ncols, in that order, into out_chunks (the result columns'
+ * chunks concatenated: sum of the inputs' chunk counts): the same slots, levels and meter as the
+ * calls; one launch per 64 single-chunk columns, the calls one by one otherwise. */
+int hs_znorm_batch(hs_ctx* ctx, const hs_column* const* cols, uint32_t ncols, double B,
+                   const hs_invroot_cfg* cfg, hs_ct** out_chunks);
 /* Extension (SURVEY 8(d) C4's "deduplicated batched variant"): pearson(cols[i], cols[j]) for
  * every pair i < j of ncols columns, in that order, into out[ncols (ncols - 1) / 2]: the same
  * slots, levels and meter as the sequential calls; one launch for up to 8 single-chunk columns

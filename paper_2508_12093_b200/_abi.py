@@ -117,6 +117,8 @@ _SIGS = {
                              C.POINTER(hs_invroot_cfg), PCT]),
     "hs_pearson_table": (C.c_int, [CTX, C.POINTER(C.POINTER(hs_column)), C.c_uint32, C.c_double,
                                    C.POINTER(hs_invroot_cfg), PCT]),
+    "hs_znorm_batch": (C.c_int, [CTX, C.POINTER(C.POINTER(hs_column)), C.c_uint32, C.c_double,
+                                 C.POINTER(hs_invroot_cfg), PCT]),
     "hs_synthetic_uniform": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_double, DP]),
     "hs_synthetic_grid": (C.c_int, [C.c_uint64, C.c_double, C.c_double, DP]),
     "hs_two_subrange_grid": (C.c_int, [C.c_uint64, C.c_double, C.c_double, DP]),

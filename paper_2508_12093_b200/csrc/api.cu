@@ -759,6 +759,32 @@ int hs_pearson(hs_ctx* c, const hs_column* x, const hs_column* y, double B, cons
   });
 }
 
+int hs_znorm_batch(hs_ctx* c, const hs_column* const* cols, uint32_t ncols, double B, const hs_invroot_cfg* cfg,
+                   hs_ct** out) {
+  return guard([&] {
+    if (ncols && !cols) fail(HS_E_INVALID_ARG, "hs_znorm_batch: null columns");
+    std::vector<hs_ct*> res;
+    try {
+      if (ctxp(c)->rns) {
+        hs_ctx* cc = c;
+        rns::RnsB& rb = *cc->rns->b;
+        for (uint32_t i = 0; i < ncols; ++i)
+          for (auto& z : flow::znorm(rb, rcol_of(cc, cols[i]), B, cfg_of(cfg)).chunks) res.push_back(rwrap(cc, z));
+      } else {
+        std::vector<pipe::ColC> cs;
+        for (uint32_t i = 0; i < ncols; ++i) cs.push_back(col_of(cols[i]));
+        for (auto& z : pipe::znorm_batch(ctxp(c), cs, B, cfg_of(cfg)))
+          for (Ct& ch : z.chunks) res.push_back(wrap(std::move(ch)));
+      }
+    } catch (...) {
+      for (hs_ct* h : res) hs_ct_release(h);
+      throw;
+    }
+    if (!res.empty()) need(out, "out_chunks");
+    std::copy(res.begin(), res.end(), out);
+  });
+}
+
 int hs_pearson_table(hs_ctx* c, const hs_column* const* cols, uint32_t ncols, double B, const hs_invroot_cfg* cfg,
                      hs_ct** out) {
   return guard([&] {

@@ -90,8 +90,8 @@ class Runtime {
   cudaStream_t upload_ = nullptr;
   std::atomic<uint64_t> launches_{0};
   std::mutex scratch_mu_;
-  DevBuf scratch_[4];
-  size_t scratch_n_[4] = {0, 0, 0, 0};
+  DevBuf scratch_[6];
+  size_t scratch_n_[6] = {0, 0, 0, 0, 0, 0};
 };
 
 // L1/shared carveout (percent of the unified 228 KB) shared by the statistics kernels and

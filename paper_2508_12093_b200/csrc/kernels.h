@@ -153,6 +153,23 @@ struct PTableArgs {
 };
 size_t ptable_partial_doubles();
 void run_ptable(QSpec q, const PTableArgs& a, const Prog& p, int lanes, cudaStream_t s);
+
+// ---- stat.cu: many independent single-chunk Z-scores in one cooperative kernel -----------
+// Column k: moments (phase A: mean_scaled(B = 1) and variance_scaled(B) terms), the program `p`
+// (M_LDR 0/1 = the column's mu/var; its M_ST writes inv + k S: crypto_invsqrt(var, B^2)), then
+// z_k = (x_k - mu_k) inv_k (block-local).  A column whose sums are not provably exact takes the
+// literal rotate-and-add butterfly in the same launch (scratch: 2 x 3 ncols x S doubles).
+constexpr int kMaxZBatch = 64;
+struct ZBatchArgs {
+  int ncols = 0;
+  const double* x[kMaxZBatch];
+  double* z[kMaxZBatch];
+  double cm[kMaxZBatch], ca[kMaxZBatch], cmp[kMaxZBatch];
+  double* partial = nullptr;  // zbatch_partial_doubles(), zero between launches
+  double* scratch = nullptr;  // butterfly fallback
+};
+size_t zbatch_partial_doubles();
+void run_zbatch(QSpec q, const ZBatchArgs& a, const Prog& p, int lanes, cudaStream_t s);
 size_t stat_partial_doubles();  // scratch sizing for StatArgs::partial
 
 }  // namespace k

@@ -324,6 +324,10 @@ class PB {
     table_ = &a;
     finish(false, nullptr);
   }
+  void launch_zbatch(const k::ZBatchArgs& a) {
+    zbatch_ = &a;
+    finish(false, nullptr);
+  }
 
  private:
   void finish(bool stat, const k::StatArgs* a) {
@@ -366,7 +370,8 @@ class PB {
       prog_.flags = debug_flag_word();
       cuda_ok(cudaMemsetAsync(prog_.flags, 0, sizeof(unsigned), rt.stream()), "debug flags");
     }
-    if (table_) k::run_ptable(q_, *table_, prog_, lanes, rt.stream());
+    if (zbatch_) k::run_zbatch(q_, *zbatch_, prog_, lanes, rt.stream());
+    else if (table_) k::run_ptable(q_, *table_, prog_, lanes, rt.stream());
     else if (stat) k::run_stat(q_, *a, prog_, lanes, rt.stream());
     else k::run_prog(q_, prog_, lanes, rt.stream());
 #ifdef HS_HOST_PROFILE
@@ -441,6 +446,7 @@ class PB {
   bool big_cheb_ = false;
   std::vector<std::pair<int, Series>> chebs_;
   const k::PTableArgs* table_ = nullptr;
+  const k::ZBatchArgs* zbatch_ = nullptr;
 };
 
 // ---- statistics: one cooperative launch per call (stat.cu) ------------------------------
@@ -856,11 +862,12 @@ std::vector<Ct> pearson_table(hs_ctx* ctx, const std::vector<ColC>& cols, double
   a.inv_n = 1.0 / nv;                    // mean_of_chunks, stats.hpp:83
   for (size_t c = 0; c < n; ++c) a.x[c] = cols[c].chunks[0]->device();
   std::vector<DevBuf> outs;
+  const DevBuf block = rt.alloc(n * (n - 1) / 2 * S);  // one allocation; each output aliases its slice
   for (size_t i = 0; i < n; ++i)
     for (size_t j = i + 1; j < n; ++j) {
       a.pi[a.npairs] = static_cast<uint8_t>(i);
       a.pj[a.npairs] = static_cast<uint8_t>(j);
-      outs.push_back(rt.alloc(S));
+      outs.push_back(DevBuf(block, block.get() + a.npairs * S));
       a.out[a.npairs] = outs.back().get();
       ++a.npairs;
     }
@@ -882,6 +889,72 @@ std::vector<Ct> pearson_table(hs_ctx* ctx, const std::vector<ColC>& cols, double
   ctx->m = m_all;
   std::vector<Ct> out;
   for (size_t k = 0; k < outs.size(); ++k) out.push_back(make_out(ctx, outs[k], levels[k]));
+  return out;
+}
+
+// znorm of many independent columns in one launch (kernels.h ZBatchArgs): the same chunks,
+// levels and meter as znorm(cols[0]), znorm(cols[1]), ... in order.  Columns must be single-chunk
+// for the fused path (up to 64 per launch); debug_checks, quantize off, multi-chunk columns or a
+// ledger error run the calls one by one.  No host synchronisation: capturable into a graph.
+std::vector<ColC> znorm_batch(hs_ctx* ctx, const std::vector<ColC>& cols, double B, const InvCfg& cfg) {
+  auto sequential = [&] {
+    std::vector<ColC> out;
+    for (const ColC& c : cols) out.push_back(znorm(ctx, c, B, cfg));
+    return out;
+  };
+  const Params& p = ctx->p;
+  bool ok = !cols.empty() && !p.debug && p.quantize && cfg_ok(cfg) && Runtime::get().fused;
+  for (const ColC& c : cols) ok = ok && col_ok(ctx, c) && c.chunks.size() == 1;
+  if (!ok) return sequential();
+  std::vector<ColC> out;
+  const Meter m0 = ctx->m;
+  std::vector<int> levels;
+  try {
+    for (const ColC& c : cols) {
+      auto [r, m] = ledger(ctx, Key("znorm", ctx->p).col(c).add(B).cfg(cfg),
+                           [&](SymB& sb) { return flow::znorm(sb, sym(c), B, cfg); });
+      ctx->m = m;
+      levels.push_back(r.chunks.at(0).level);
+    }
+  } catch (const Error& e) {
+    if (e.code == HS_E_CUDA) throw;
+    ctx->m = m0;
+    return sequential();
+  }
+  const Meter m_all = ctx->m;
+  Runtime& rt = Runtime::get();
+  const size_t S = p.S;
+  const size_t nmax = std::min(cols.size(), size_t(k::kMaxZBatch));
+  DevBuf inv = rt.alloc(nmax * S);
+  for (size_t b0 = 0; b0 < cols.size(); b0 += k::kMaxZBatch) {
+    const size_t nb = std::min(cols.size() - b0, size_t(k::kMaxZBatch));
+    k::ZBatchArgs a{};
+    a.ncols = static_cast<int>(nb);
+    std::vector<DevBuf> zs;
+    const DevBuf block = rt.alloc(nb * S);  // one allocation; each output aliases its slice
+    for (size_t k = 0; k < nb; ++k) {
+      const ColC& c = cols[b0 + k];
+      const double nv = static_cast<double>(c.n_valid);
+      a.x[k] = c.chunks[0]->device();
+      zs.push_back(DevBuf(block, block.get() + k * S));
+      a.z[k] = zs.back().get();
+      a.cm[k] = 1.0 / (1.0 * nv);                 // mean_scaled(col, 1), stats.hpp:101
+      a.ca[k] = 1.0 / std::sqrt(B * B * nv);      // variance_to_scale(col, B^2), stats.hpp:117
+      a.cmp[k] = 1.0 / (nv * std::sqrt(B * B));   // stats.hpp:123
+    }
+    a.partial = rt.scratch(4, k::zbatch_partial_doubles(), true);
+    a.scratch = rt.scratch(5, 2 * 3 * nmax * S);  // butterfly fallback (never read on the exact path)
+    PB pb(p);
+    pb.st(pb.invsqrt(pb.ldr(1), B * B, cfg), inv.get());  // crypto_invsqrt(var, B^2), stats.hpp:159
+    pb.launch_zbatch(a);
+    for (size_t k = 0; k < nb; ++k) {
+      ColC z;
+      z.n_valid = cols[b0 + k].n_valid;
+      z.chunks.push_back(make_out(ctx, zs[k], levels[b0 + k]));
+      out.push_back(std::move(z));
+    }
+  }
+  ctx->m = m_all;
   return out;
 }
 

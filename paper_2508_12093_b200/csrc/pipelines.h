@@ -38,6 +38,8 @@ Ct kurtosis(hs_ctx* ctx, const ColC& col, double B, const flow::InvCfg& cfg);
 Ct skewness(hs_ctx* ctx, const ColC& col, double B, const flow::InvCfg& cfg);
 Ct coeff_variation(hs_ctx* ctx, const ColC& col, double B, const flow::SignCfg& sc, const flow::InvCfg& cfg);
 Ct pearson(hs_ctx* ctx, const ColC& x, const ColC& y, double B, const flow::InvCfg& cfg);
+// znorm(cols[k]) for every k, in order; one launch per 64 single-chunk columns where possible
+std::vector<ColC> znorm_batch(hs_ctx* ctx, const std::vector<ColC>& cols, double B, const flow::InvCfg& cfg);
 // pearson(cols[i], cols[j]) for every pair i < j in order, one launch where possible
 std::vector<Ct> pearson_table(hs_ctx* ctx, const std::vector<ColC>& cols, double B, const flow::InvCfg& cfg);
 

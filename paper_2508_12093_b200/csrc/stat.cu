@@ -281,38 +281,35 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_stat(Q q, const __
 
 // ---- the C4 Pearson table (kernels.h PTableArgs) ----------------------------------------------
 constexpr int kTA = 3 * kMaxTableCols, kTB = kMaxTablePairs;  // phase A / B arrays
-constexpr int kTChunk = 8;                                      // arrays reduced per pass
 
-// Block sums (and |sums|) of arrays [a0, a0 + n) (n <= kTChunk) into the grid-wide totals.
+// The same totals with one warp per array: warp w sums arrays w, w + warps, ... over the block's
+// slots (coalesced loads, shuffles, one pair of atomics per array and block; no block barrier per
+// array group).  Used when many arrays are summed (the batched statistics).
 template <class TermFn>
-__device__ void table_accumulate(TermFn term, int a0, int n, const Range& BR, double* accum) {
-  __shared__ double red[kMaxWarps][2 * kTChunk];
-  double acc[2 * kTChunk];
+__device__ void warp_accumulate(TermFn term, int n, const Range& BR, double* accum) {
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  for (int k = warp; k < n; k += nw) {
+    double sm = 0.0, ab = 0.0;
+    for (unsigned i0 = BR.lo + lane; i0 < BR.hi; i0 += 8 * 32) {
+      double t[8];  // eight slots' loads in flight per lane
 #pragma unroll
-  for (int k = 0; k < 2 * kTChunk; ++k) acc[k] = 0.0;
-  for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) {
+      for (int u = 0; u < 8; ++u) t[u] = i0 + 32 * u < BR.hi ? term(k, i0 + 32 * u) : 0.0;
 #pragma unroll
-    for (int k = 0; k < kTChunk; ++k)
-      if (k < n) {
-        const double t = term(a0 + k, i);
-        acc[2 * k] += t;
-        acc[2 * k + 1] += fabs(t);
+      for (int u = 0; u < 8; ++u) {
+        sm += t[u];
+        ab += fabs(t[u]);
       }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      ab += __shfl_xor_sync(0xffffffffu, ab, o);
+    }
+    if (lane == 0) {  // integer terms, checked bound: exact in any order
+      atomicAdd(accum + 2 * k, sm);
+      atomicAdd(accum + 2 * k + 1, ab);
+    }
   }
-#pragma unroll
-  for (int k = 0; k < 2 * kTChunk; ++k)
-    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-  if ((threadIdx.x & 31) == 0)
-#pragma unroll
-    for (int k = 0; k < 2 * kTChunk; ++k) red[threadIdx.x >> 5][k] = acc[k];
-  __syncthreads();
-  if (threadIdx.x < 2 * n) {
-    double s = 0.0;
-    for (unsigned w = 0; w < blockDim.x / 32; ++w) s += red[w][threadIdx.x];
-    // integer terms, checked bound below: exact in any order (grid_sum's argument)
-    atomicAdd(accum + 2 * a0 + threadIdx.x, s);
-  }
-  __syncthreads();
 }
 
 // Grid barrier, then the totals of arrays [0, n) into tot[] (shared); false when a sum is not
@@ -354,7 +351,7 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const 
     }
     return q.mulc(X, a.cmp);                                  // mul_pt(chunk, 1/(n sqrt(S)))
   };
-  for (int a0 = 0; a0 < NA; a0 += kTChunk) table_accumulate(termA, a0, min(kTChunk, NA - a0), BR, accA);
+  warp_accumulate(termA, NA, BR, accA);
   if (!table_totals(grid, accA, counts, NA, totA)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.inexact = 1u;
     return;
@@ -374,7 +371,7 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const 
     const double cy = q.sub(q.in(__ldg(a.x[cj] + i)), mu(cj));
     return q.mulc(q.mul(cx, cy), a.inv_n);
   };
-  for (int b0 = 0; b0 < a.npairs; b0 += kTChunk) table_accumulate(termB, b0, min(kTChunk, a.npairs - b0), BR, accB);
+  warp_accumulate(termB, a.npairs, BR, accB);
   if (!table_totals(grid, accB, counts + 1, a.npairs, totB)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.inexact = 1u;
     return;
@@ -400,6 +397,100 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const 
     const double ix = q.in(__ldcg(inv + a.pi[p] * S + s)), iy = q.in(__ldcg(inv + a.pj[p] * S + s));
     a.out[p][s] = q.out(q.mul(q.mul(totB[2 * p], ix), iy));
   }
+}
+
+// ---- many independent Z-scores (kernels.h ZBatchArgs) ----------------------------------------
+constexpr int kZA = 3 * kMaxZBatch;
+
+template <class Q, int P>
+__global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_zbatch(Q q, const __grid_constant__ ZBatchArgs a,
+                                                         const __grid_constant__ Prog pg) {
+  extern __shared__ double stab[];
+  __shared__ double tot[2 * kZA];
+  __shared__ unsigned char exact[kMaxZBatch];
+  __shared__ int any_inexact;
+  unsigned* counts = reinterpret_cast<unsigned*>(a.partial + 2 * kZA);
+  const GridBar grid{counts + 1};
+  const unsigned S = pg.S;
+  const Range BR = block_range(S);
+  stamp(0);
+  for (int i = threadIdx.x; i < pg.ntab; i += blockDim.x) stab[i] = __ldg(pg.tabs + i);
+  // ---- phase A: every column's moment terms (stats.hpp:41-51, 110-126) ----
+  const int NA = 3 * a.ncols;
+  auto termA = [&](int k, unsigned i) -> double {
+    const int c = k / 3, t = k - 3 * c;
+    const double X = q.in(__ldg(a.x[c] + i));
+    if (t == 0) return q.mulc(X, a.cm[c]);                    // mul_pt(chunk, 1/(B n)), B = 1
+    if (t == 1) {
+      const double sx = q.mulc(X, a.ca[c]);                   // mul_pt(chunk, 1/sqrt(B^2 n))
+      return q.mul(sx, sx);                                   // mul_ct(a, a)
+    }
+    return q.mulc(X, a.cmp[c]);                               // mul_pt(chunk, 1/(n sqrt(B^2)))
+  };
+  warp_accumulate(termA, NA, BR, a.partial);
+  stamp(1);
+  table_totals(grid, a.partial, counts, NA, tot);
+  // exact-sum per column (uniform across blocks: every block reads the same totals)
+  if (threadIdx.x == 0) any_inexact = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < a.ncols; c += blockDim.x) {
+    bool e = true;
+    for (int t = 0; t < 3; ++t) e = e && tot[2 * (3 * c + t) + 1] < 4503599627370496.0;  // 2^52
+    exact[c] = e ? 1 : 0;
+    if (!e) any_inexact = 1;
+  }
+  __syncthreads();
+  // ---- a column with a sum beyond the exact bound: the literal butterfly (ckks.hpp:218-230) ----
+  double* cur = a.scratch;
+  if (any_inexact) {  // uniform
+    double* nxt = a.scratch + size_t(NA) * S;
+    for (int k = 0; k < NA; ++k)
+      if (!exact[k / 3])
+        for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x) cur[size_t(k) * S + i] = termA(k, i);
+    grid.sync();
+    for (unsigned d = 1; d < S; d <<= 1) {
+      for (int k = 0; k < NA; ++k)
+        if (!exact[k / 3])
+          for (unsigned i = BR.lo + threadIdx.x; i < BR.hi; i += blockDim.x)
+            nxt[size_t(k) * S + i] = q.add(__ldcg(cur + size_t(k) * S + i), __ldcg(cur + size_t(k) * S + ((i + d) & (S - 1))));
+      grid.sync();
+      double* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+  }
+  stamp(2);
+  if (BR.lo >= BR.hi) return;
+  // per (column, slot): the reduced array values (uniform totals, or the butterfly's slots)
+  auto val = [&](int c, int t, unsigned s) {
+    return exact[c] ? tot[2 * (3 * c + t)] : __ldcg(cur + size_t(3 * c + t) * S + s);
+  };
+  auto mu = [&](int c, unsigned s) { return val(c, 0, s); };
+  auto var = [&](int c, unsigned s) {
+    const double mp = val(c, 2, s);
+    return q.sub(val(c, 1, s), q.mul(mp, mp));                // sub_ct(sq_sum, mul_ct(mp, mp))
+  };
+  // ---- phase C: crypto_invsqrt(var_k, B^2) for every column on this block's slots ----
+  const unsigned w = BR.hi - BR.lo, items = w * static_cast<unsigned>(a.ncols);
+  const unsigned iters = (items * P + blockDim.x - 1) / blockDim.x;
+  for (unsigned it = 0; it < iters; ++it) {
+    const unsigned g = threadIdx.x + it * blockDim.x, item = g / P;
+    const bool live = item < items;
+    const unsigned it2 = live ? item : items - 1;
+    const unsigned c = it2 / w, s = BR.lo + it2 % w;
+    double sv[5] = {mu(static_cast<int>(c), s), var(static_cast<int>(c), s), 0.0, 0.0, 0.0};
+    exec<Q, P>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
+  }
+  __syncthreads();
+  stamp(3);
+  // ---- z = mul_ct(sub_ct(x, mu), inv) (stats.hpp:160-165) ----
+  const double* inv = pg.out[0];
+  for (unsigned g = threadIdx.x; g < items; g += blockDim.x) {
+    const unsigned c = g / w, s = BR.lo + g % w;
+    const double ix = q.in(__ldcg(inv + c * S + s));
+    a.z[c][s] = q.out(q.mul(q.sub(q.in(__ldg(a.x[c] + s)), mu(static_cast<int>(c), s)), ix));
+  }
+  stamp(4);
 }
 
 template <class F>
@@ -452,6 +543,32 @@ int max_blocks(K kern, size_t smem, int threads) {
 size_t stat_partial_doubles() { return 4 * kNK + 2; }
 // the table's 2 (kTA + kTB) totals, two block counters and its grid barrier word
 size_t ptable_partial_doubles() { return 2 * (kTA + kTB) + 2; }
+
+size_t zbatch_partial_doubles() { return 2 * kZA + 2; }
+
+void run_zbatch(QSpec qs, const ZBatchArgs& a, const Prog& p, int lanes, cudaStream_t s) {
+  if (p.S == 0 || a.ncols == 0) return;
+  if (qs.mode != QMode::Grid) fail(HS_E_ERROR, "znorm batch: exact grid sums need quantize = true");
+  const QGrid Q{ldexp(1.0, qs.bits), ldexp(1.0, -qs.bits)};
+  const size_t smem = static_cast<size_t>(p.ntab) * sizeof(double);
+  auto go = [&](auto kern, int P) {
+    const int maxt = P == 1 ? prog_max_threads<1>() : (P == 2 ? prog_max_threads<2>() : prog_max_threads<4>());
+    const Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+    const int cap = max_blocks(kern, smem, static_cast<int>(geo.threads));
+    if (cap < static_cast<int>(geo.blocks)) fail(HS_E_CUDA, "znorm batch kernel: grid not co-resident");
+    QGrid qv = Q;
+    ZBatchArgs av = a;
+    Prog pv = p;
+    void* args[] = {&qv, &av, &pv};
+    cuda_ok(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(geo.blocks), dim3(geo.threads), args,
+                                        smem, s),
+            "znorm batch launch");
+  };
+  if (lanes == 4) go(k_zbatch<QGrid, 4>, 4);
+  else if (lanes == 2) go(k_zbatch<QGrid, 2>, 2);
+  else go(k_zbatch<QGrid, 1>, 1);
+  Runtime::get().note_launch();
+}
 
 void run_ptable(QSpec qs, const PTableArgs& a, const Prog& p, int lanes, cudaStream_t s) {
   if (p.S == 0) return;

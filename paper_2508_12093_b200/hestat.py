@@ -600,6 +600,29 @@ def pearson(ctx: EvalContext, col_x: EncryptedColumn, col_y: EncryptedColumn, B:
     return r
 
 
+def znorm_batch(ctx: EvalContext, cols: Sequence[EncryptedColumn], B: float,
+                cfg: Optional[InvRootConfig] = None) -> List[EncryptedColumn]:
+    """znorm(col) for every column, in order (hs_znorm_batch: one launch per 64 single-chunk
+    columns; same slots, levels and meter as the calls)."""
+    cs, keep = [], []
+    for col in cols:
+        c, k = col._c()
+        cs.append(c)
+        keep.append(k)
+    arr = (C.POINTER(_abi.hs_column) * max(len(cs), 1))(*[C.pointer(c) for c in cs])
+    total = sum(len(c.chunks) for c in cols)
+    out = _ptr_array(max(total, 1))()
+    _check(_abi.lib().hs_znorm_batch(ctx._h, arr, len(cs), float(B), _cfg(cfg), out))
+    del keep
+    res, off = [], 0
+    for col in cols:
+        n = len(col.chunks)
+        chunks = [Ciphertext._own(C.c_void_p(out[off + i])) for i in range(n)]
+        res.append(EncryptedColumn(chunks, col.n_valid, col.name))
+        off += n
+    return res
+
+
 def pearson_table(ctx: EvalContext, cols: Sequence[EncryptedColumn], B: float,
                   cfg: Optional[InvRootConfig] = None) -> List[Ciphertext]:
     """pearson(cols[i], cols[j]) for every pair i < j, in that order (hs_pearson_table: one
