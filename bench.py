@@ -178,7 +178,11 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "config": workload_config({"parallelism": f"replicas x{max(args.gpus, 1)} (no data-path collective)"}),
+            "config": workload_config({"parallelism": f"replicas x{max(args.gpus, 1)} (no data-path collective)",
+                                       "ciphertexts_per_step": max(1, min(args.batch_cols, 64)),
+                                       "step": "independent C2 Z-scores, each its own EvalContext on a host thread "
+                                               "(the reference's sanctioned concurrency, SPEC.md:141); value per "
+                                               "ciphertext"}),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                              "sample": f"per step: {threads} independent C2 znorm runs on {threads} threads"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
