@@ -332,7 +332,7 @@ class PB {
  private:
   void finish(bool stat, const k::StatArgs* a) {
     Runtime& rt = Runtime::get();
-    const int lanes = big_cheb_ ? rt.prog_lanes : 1;
+    const int lanes = !big_cheb_ ? 1 : (zbatch_ ? rt.batch_lanes : rt.prog_lanes);
     int p = 0;
     while ((1 << p) < lanes) ++p;
     // one concatenated table per distinct series (deduplicated), cached on the

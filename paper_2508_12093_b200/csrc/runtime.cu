@@ -64,6 +64,10 @@ Runtime::Runtime(int device) {
     const int l = std::atoi(e);
     if (l == 1 || l == 2 || l == 4 || l == 8) prog_lanes = l;
   }
+  if (const char* e = std::getenv("HESTAT_BATCH_LANES")) {  // batched Z-score: 4 measured 3 % over 2
+    const int l = std::atoi(e);
+    if (l == 1 || l == 2 || l == 4) batch_lanes = l;
+  }
   cuda_ok(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_ok(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking), "cudaStreamCreate (upload)");
   // Keep freed blocks in the stream-ordered pool: ciphertexts are churned per op.
