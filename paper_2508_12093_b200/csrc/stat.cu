@@ -312,6 +312,50 @@ __device__ void warp_accumulate(TermFn term, int n, const Range& BR, double* acc
   }
 }
 
+// The same with NT arrays per group computed together (group g = arrays NT g .. NT g + NT - 1,
+// term(g, i, t[NT])): one load serves the group's terms, NT sums in flight per warp.
+template <int NT, class TermFn>
+__device__ void warp_accumulate_groups(TermFn term, int ngroups, const Range& BR, double* accum) {
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  for (int g = warp; g < ngroups; g += nw) {
+    double sm[NT], ab[NT];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) sm[k] = ab[k] = 0.0;
+    for (unsigned i0 = BR.lo + lane; i0 < BR.hi; i0 += 4 * 32) {
+      double t[4][NT];  // four slots' loads in flight per lane
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + 32 * u < BR.hi) {
+          term(g, i0 + 32 * u, t[u]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < NT; ++k) t[u][k] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          sm[k] += t[u][k];
+          ab[k] += fabs(t[u][k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      for (int o = 16; o > 0; o >>= 1) {
+        sm[k] += __shfl_xor_sync(0xffffffffu, sm[k], o);
+        ab[k] += __shfl_xor_sync(0xffffffffu, ab[k], o);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        atomicAdd(accum + 2 * (NT * g + k), sm[k]);
+        atomicAdd(accum + 2 * (NT * g + k) + 1, ab[k]);
+      }
+  }
+}
+
 // Grid barrier, then the totals of arrays [0, n) into tot[] (shared); false when a sum is not
 // provably exact.  The last block to read zeroes the totals and its counter for the next launch.
 __device__ bool table_totals(const GridBar& grid, double* accum, unsigned* count, int n, double* tot) {
@@ -427,7 +471,15 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_zbatch(Q q, const 
     }
     return q.mulc(X, a.cmp[c]);                               // mul_pt(chunk, 1/(n sqrt(B^2)))
   };
-  warp_accumulate(termA, NA, BR, a.partial);
+  // the column's three terms from one load of each slot
+  auto termCol = [&](int c, unsigned i, double (&t)[3]) {
+    const double X = q.in(__ldg(a.x[c] + i));
+    t[0] = q.mulc(X, a.cm[c]);
+    const double sx = q.mulc(X, a.ca[c]);
+    t[1] = q.mul(sx, sx);
+    t[2] = q.mulc(X, a.cmp[c]);
+  };
+  warp_accumulate_groups<3>(termCol, a.ncols, BR, a.partial);
   stamp(1);
   table_totals(grid, a.partial, counts, NA, tot);
   // exact-sum per column (uniform across blocks: every block reads the same totals)
@@ -485,10 +537,25 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_zbatch(Q q, const 
   stamp(3);
   // ---- z = mul_ct(sub_ct(x, mu), inv) (stats.hpp:160-165) ----
   const double* inv = pg.out[0];
-  for (unsigned g = threadIdx.x; g < items; g += blockDim.x) {
-    const unsigned c = g / w, s = BR.lo + g % w;
-    const double ix = q.in(__ldcg(inv + c * S + s));
-    a.z[c][s] = q.out(q.mul(q.sub(q.in(__ldg(a.x[c] + s)), mu(static_cast<int>(c), s)), ix));
+  for (unsigned g0 = threadIdx.x; g0 < items; g0 += 4 * blockDim.x) {  // four items' loads in flight
+    double xv[4], iv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned g = g0 + u * blockDim.x;
+      if (g < items) {
+        const unsigned c = g / w, s = BR.lo + g % w;
+        iv[u] = __ldcg(inv + c * S + s);
+        xv[u] = __ldg(a.x[c] + s);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned g = g0 + u * blockDim.x;
+      if (g < items) {
+        const unsigned c = g / w, s = BR.lo + g % w;
+        a.z[c][s] = q.out(q.mul(q.sub(q.in(xv[u]), mu(static_cast<int>(c), s)), q.in(iv[u])));
+      }
+    }
   }
   stamp(4);
 }
