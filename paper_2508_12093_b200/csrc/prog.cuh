@@ -280,9 +280,12 @@ __device__ __forceinline__ bool chk_fails(int kind, double v, double c, double c
 // ---- launch geometry ---------------------------------------------------------------------
 // One block per SM (148 on B200), each owning a contiguous, equal range of slots,
 // P threads per slot: every SM gets the same amount of FP64 work.
+#ifndef HS_P1_THREADS
+#define HS_P1_THREADS 256
+#endif
 template <int P>
 constexpr int prog_max_threads() {
-  return P == 1 ? 256 : (P == 2 ? 512 : 1024);
+  return P == 1 ? HS_P1_THREADS : (P == 2 ? 512 : 1024);
 }
 
 struct Geo {

@@ -6,6 +6,9 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+from paper_2508_12093_b200 import _abi  # noqa: E402
+if os.environ.get("HESTAT_LIB"):  # A/B a variant build of the library
+    _abi.LIB_PATH = os.path.abspath(os.environ["HESTAT_LIB"])
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from paper_2508_12093_b200 import hestat as H  # noqa: E402
@@ -38,4 +41,4 @@ for K in (1, 8, 16, 32, 64, 128):
         if best is None or w < best[0]:
             best = (w, e0.elapsed_time(e1))
         del z
-    print(f"K={K}: wall {1e3 * best[0] / K:.2f} us/ct, device {1e3 * best[1] / K:.2f} us/ct, parity {ok}")
+    print(f"K={K}: wall {1e6 * best[0] / K:.2f} us/ct, device {1e3 * best[1] / K:.2f} us/ct, parity {ok}")
