@@ -442,6 +442,25 @@ def rns_traffic(op, logN, L, K):
     return None
 
 
+def zbatch_lanes():
+    """Threads per slot of the batched Z-score kernel (the library's default, or HESTAT_BATCH_LANES)."""
+    v = os.environ.get("HESTAT_BATCH_LANES", "4")
+    return int(v) if v in ("1", "2", "4") else 4
+
+
+def zbatch_traffic(kb):
+    """DRAM bytes per k_zbatch launch of kb ciphertexts from the committed ncu --set full summary."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d["ciphertexts"] != kb:
+            return None
+        return d["dram_bytes_read"] + d["dram_bytes_write"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def kstat_traffic():
     """DRAM bytes per k_stat launch from the committed ncu --set full summary (None if absent)."""
     p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_kstat_ncu.json")
@@ -940,16 +959,16 @@ def main():
             "gpu_launches": int(blaunches),
             "api_loop_ms_per_step_single_call": api_ms / args.steps,
             "roofline": {"bound": "fp64",
-                         "kernel": f"k_zbatch<QGrid,2> (the step: {KB} fused C2 Z-scores = moments, grid-wide exact "
+                         "kernel": f"k_zbatch<QGrid,{zbatch_lanes()}> (the step: {KB} fused C2 Z-scores = moments, grid-wide exact "
                                    "sums, invsqrt degree 511 + 6 Newton per ciphertext, (x - mu) * inv)",
                          "achieved": bachieved, "peak": peak, "unit": "TFLOP/s", "frac": bachieved / peak,
-                         "traffic": None, "duration_us": bstep_us,
+                         "traffic": zbatch_traffic(KB), "duration_us": bstep_us,
                          "work": f"{step_per_slot} fp64 ops/slot x {S} slots x {KB} ciphertexts",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "traffic_source": "none captured for k_zbatch (algorithmic: 16 B per slot and "
-                                           "ciphertext, 512 KiB per ciphertext; the single-call k_stat capture is "
-                                           "profiles/r1_kstat_ncu.json)",
+                         "traffic_source": "profiles/r2_zbatch_ncu.json (ncu --set full, one k_zbatch launch of "
+                                           "64 ciphertexts, dram read+write; algorithmic: 16 B per slot and "
+                                           "ciphertext, 32 MiB per launch)",
                          "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",
                                             "duration_us": prog_us, "achieved": prog_achieved,
                                             "frac": prog_achieved / peak,
