@@ -14,9 +14,11 @@ znorm of one ciphertext.
          encrypted columns larger than L2 (config.l2).  `single_call` reports
          the same with one znorm call (one launch) per ciphertext.
   e2e    the same metric through the public API with HOST buffers: every step
-         encodes its 64 ciphertexts' values from pinned host memory (H2D), runs
-         znorm_batch and decodes the results (D2H), all inside the timed region;
-         the next step's encode overlaps the current Z-scores (upload stream).
+         encodes its 64 ciphertexts' values from pinned host memory (16 MiB H2D),
+         runs znorm_batch and decodes the results (16 MiB D2H), all inside the
+         timed region, as a one-thread software pipeline over the asynchronous
+         calls (encode_column_async k+1 | znorm_batch k | decode_column_async k,
+         then the waits for k's verdict and k-1's results).
          `e2e_single_call` is the one-ciphertext-per-step loop (and its
          strictly sequential latency and pageable-buffer variants).
 
@@ -755,44 +757,77 @@ def main():
     pg_ok = bool(np.array_equal(bits(pz), bits(ref.out)))
 
     # ---- e2e (headline): KB ciphertexts per step through the public API from pinned host memory --
-    # encode_column of the step's KB x 2^15 values (one H2D + encrypt, one synchronisation), each
-    # chunk its own single-chunk column, znorm_batch, the KB result chunks decoded as one column
-    # (one D2H); the next step's encode overlaps the current Z-scores (upload stream).
-    XB = torch.empty(KB * S, dtype=torch.float64).pin_memory()
-    ZB = torch.empty(KB * S, dtype=torch.float64).pin_memory()
-    xbn, zbn = XB.numpy(), ZB.numpy()
-    for j in range(KB):
-        xbn[j * S:(j + 1) * S] = np.roll(x, 97 * j)
+    # Per step: encode_column_async of the step's KB x 2^15 values (one 16 MiB H2D DMA + one encrypt
+    # launch on an upload stream), each chunk its own single-chunk column, znorm_batch (ordered
+    # behind the upload on the device), decode_column_async of the KB result chunks as one column
+    # (one 16 MiB D2H DMA on the download stream); the host waits for step k's finiteness verdict
+    # and step k-1's results while step k computes, so both copy engines and the SMs stay busy.
+    # Every step's input is copied H2D and its whole result D2H inside the timed region; host
+    # buffers rotate over NBUF pinned pairs.
+    NBUF = 4
+    XB = [torch.empty(KB * S, dtype=torch.float64).pin_memory() for _ in range(NBUF)]
+    ZB = [torch.empty(KB * S, dtype=torch.float64).pin_memory() for _ in range(NBUF)]
+    xbn, zbn = [t_.numpy() for t_ in XB], [t_.numpy() for t_ in ZB]
+    for b_ in xbn:
+        for j in range(KB):
+            b_[j * S:(j + 1) * S] = np.roll(x, 97 * j)
 
-    def benc():
-        big = H.encode_column(ctx, xbn)
-        return [H.EncryptedColumn([c], S) for c in big.chunks]
+    def benc(i):
+        big, pend = H.encode_column_async(ctx, xbn[i % NBUF])
+        return [H.EncryptedColumn([c], S) for c in big.chunks], pend
 
-    def bdec(zs):
-        H.decode_column(ctx, H.EncryptedColumn([zc_.chunks[0] for zc_ in zs], KB * S), out=zbn)
+    def bdec(zs, i):
+        return H.decode_column_async(ctx, H.EncryptedColumn([zc_.chunks[0] for zc_ in zs], KB * S), zbn[i % NBUF])
 
-    for _ in range(5):
-        bdec(H.znorm_batch(ctx, benc(), B))
-    bcol = benc()
-    for _ in range(5):
-        zs_ = H.znorm_batch(ctx, bcol, B)
-        bcol = benc()
-        bdec(zs_)
-    del bcol, zs_
+    def e2e_loop(steps):
+        col_, pe = benc(0)
+        dq = []
+        for k_ in range(steps):
+            zs_ = H.znorm_batch(ctx, col_, B)  # ordered behind encode k on the device
+            pk = pe
+            if k_ + 1 < steps:
+                col_, pe = benc(k_ + 1)
+            dq.append(bdec(zs_, k_))
+            pk.wait()  # encode k's finiteness verdict
+            while len(dq) > 1:
+                dq.pop(0).wait()  # step k-1's results are in host memory
+        dq.pop(0).wait()
+
+    e2e_loop(max(args.warmup, 8))
+    for b_ in zbn:
+        b_[:] = 0.0
     barrier_sync()
     be2e_steps = max(20, args.steps // 4)
     t0 = time.perf_counter()
     f0.record(stream)
-    bcol = benc()
-    for k_ in range(be2e_steps):
-        zs_ = H.znorm_batch(ctx, bcol, B)
-        bcol = benc() if k_ + 1 < be2e_steps else None
-        bdec(zs_)
+    e2e_loop(be2e_steps)
     f1.record(stream)
     barrier_sync()
     be2e_wall_ms = 1e3 * (time.perf_counter() - t0)
-    be2e_ms = f0.elapsed_time(f1)
-    be2e_ok = bool(np.array_equal(bits(zbn[:S]), bits(ref.out)))
+    be2e_ms = max(f0.elapsed_time(f1), be2e_wall_ms)  # events bracket the loop on the compute stream; the
+    # last results land on the download stream, which the final wait() has already drained
+    be2e_ok = all(bool(np.array_equal(bits(b_[:S]), bits(ref.out))) for b_ in zbn)
+    # the round-2 synchronous loop for comparison (encode k+1 beside znorm_batch k, decode k serial)
+    def benc_sync():
+        return [H.EncryptedColumn([c], S) for c in H.encode_column(ctx, xbn[0]).chunks]
+
+    def bdec_sync(zs):
+        H.decode_column(ctx, H.EncryptedColumn([zc_.chunks[0] for zc_ in zs], KB * S), out=zbn[0])
+
+    bcol = benc_sync()
+    for _ in range(5):
+        zs_ = H.znorm_batch(ctx, bcol, B)
+        bcol = benc_sync()
+        bdec_sync(zs_)
+    barrier_sync()
+    t0 = time.perf_counter()
+    for k_ in range(be2e_steps):
+        zs_ = H.znorm_batch(ctx, bcol, B)
+        bcol = benc_sync()
+        bdec_sync(zs_)
+    barrier_sync()
+    be2e_sync_wall_ms = 1e3 * (time.perf_counter() - t0)
+    del bcol, zs_
 
     # ---- kernel roofline: the fused inverse-sqrt program (dominant phase) -------------------
     # Both probes replay CUDA graphs of `reps` calls (device time only).
@@ -940,10 +975,15 @@ def main():
             "parity_vs_oracle": parity and bparity,
             "e2e": {"value": be2e_ms / (be2e_steps * KB * ws), "unit": UNIT, "h2d_bytes_per_step": KB * S * 8,
                     "d2h_bytes_per_step": KB * S * 8, "wall_ms_per_ciphertext": be2e_wall_ms / (be2e_steps * KB),
-                    "mode": f"pipelined, {KB} ciphertexts per step: encode_column of the step's {KB} x 2^15 "
-                            "values from pinned memory (H2D) overlapping the previous step's znorm_batch, "
-                            "decode_column of the results (D2H); public API calls only",
-                    "output_matches_oracle": be2e_ok, "host_buffers": "pinned (torch pin_memory)"},
+                    "mode": f"pipelined, {KB} ciphertexts per step, one host thread: encode_column_async of step "
+                            f"k+1's {KB} x 2^15 values (16 MiB H2D DMA + encrypt on an upload stream), znorm_batch "
+                            "of step k, decode_column_async of its results (16 MiB D2H DMA on the download "
+                            "stream), then the waits for step k's finiteness verdict and step k-1's results; "
+                            "public API calls only",
+                    "synchronous_calls_wall_ms_per_ciphertext": be2e_sync_wall_ms / (be2e_steps * KB),
+                    "synchronous_calls_mode": "the same step with the reference-shaped blocking calls "
+                                              "(encode_column k+1 beside znorm_batch k, decode_column k)",
+                    "output_matches_oracle": be2e_ok, "host_buffers": f"pinned (torch pin_memory), {NBUF} rotating pairs"},
             "single_call": {
                 "value": dev_ms / (args.steps * ws), "unit": UNIT, "ms_per_step": dev_ms / args.steps,
                 "mode": "one znorm call per step (one k_stat launch), graph-replayed",

@@ -193,6 +193,21 @@ int hs_encode_column(hs_ctx* ctx, const double* v, uint64_t n, hs_ct** chunks_ou
                      uint64_t* n_chunks);                                             /* :25 */
 int hs_decode_column(const hs_ctx* ctx, const hs_column* col, double* out);           /* :41 */
 
+/* Asynchronous forms (extension: the reference's calls are synchronous).  They enqueue the
+ * transfer and return; hs_pending_wait blocks until it has completed and returns the deferred
+ * status (HS_E_NON_FINITE_VALUE for an encode whose input held a NaN or infinity: discard its
+ * chunks).  Until then the caller must not touch `v` / `out`.  Chunks of a pending encode can be
+ * passed to any op at once: the library orders its streams behind the upload.  A host loop
+ * "encode k+1, compute k, decode k, wait k-1" keeps the copy engines and the SMs busy together.
+ * Every hs_pending is released with hs_pending_release (which waits first if needed). */
+typedef struct hs_pending hs_pending;
+int hs_encode_column_async(hs_ctx* ctx, const double* v, uint64_t n, hs_ct** chunks_out,
+                           uint64_t* n_chunks, hs_pending** pending);
+int hs_decode_column_async(const hs_ctx* ctx, const hs_column* col, double* out,
+                           hs_pending** pending);
+int hs_pending_wait(hs_pending* pending);
+void hs_pending_release(hs_pending* pending);
+
 /* ---- statistics (stats.hpp) ------------------------------------------------------ */
 int hs_mean_scaled(hs_ctx* ctx, const hs_column* col, double B, hs_ct** out);         /* :97  */
 int hs_variance_to_scale(hs_ctx* ctx, const hs_column* col, double S, hs_ct** out);   /* :110 */

@@ -104,6 +104,10 @@ _SIGS = {
     "hs_crypto_sign": (C.c_int, [CTX, CT, C.POINTER(hs_sign_cfg), PCT]),
     "hs_encode_column": (C.c_int, [CTX, DP, C.c_uint64, PCT, C.POINTER(C.c_uint64)]),
     "hs_decode_column": (C.c_int, [CTX, C.POINTER(hs_column), DP]),
+    "hs_encode_column_async": (C.c_int, [CTX, DP, C.c_uint64, PCT, C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]),
+    "hs_decode_column_async": (C.c_int, [CTX, C.POINTER(hs_column), DP, C.POINTER(C.c_void_p)]),
+    "hs_pending_wait": (C.c_int, [C.c_void_p]),
+    "hs_pending_release": (None, [C.c_void_p]),
     "hs_mean_scaled": (C.c_int, [CTX, C.POINTER(hs_column), C.c_double, PCT]),
     "hs_variance_to_scale": (C.c_int, [CTX, C.POINTER(hs_column), C.c_double, PCT]),
     "hs_variance_scaled": (C.c_int, [CTX, C.POINTER(hs_column), C.c_double, PCT]),

@@ -32,9 +32,27 @@ thread_local std::string g_err;
 std::recursive_mutex g_api_mu;
 thread_local int g_capture_depth = 0;
 
+thread_local int g_guard_depth = 0;  // guard() nesting on this thread
+
+// Runtime::wait: the blocking waits of hs_encode_column / hs_decode_column give the API lock up
+// while they sleep (their enqueues are complete, what remains touches only the caller's state),
+// unless this thread holds it more than once (a nested call, or a graph capture in progress).
+void wait_unlocked(cudaStream_t s) {
+  const bool drop = g_guard_depth == 1 && g_capture_depth == 0;
+  if (drop) g_api_mu.unlock();
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (drop) g_api_mu.lock();
+  cuda_ok(e, "cudaStreamSynchronize");
+}
+const bool g_wait_hook_set = (Runtime::set_wait_hook(&wait_unlocked), true);
+
 template <class F>
 int guard(F&& f) {
   std::lock_guard<std::recursive_mutex> lk(g_api_mu);
+  struct Depth {
+    Depth() { ++g_guard_depth; }
+    ~Depth() { --g_guard_depth; }
+  } depth;
   try {
     f();
     return HS_OK;
@@ -613,6 +631,67 @@ int hs_crypto_sign(hs_ctx* c, const hs_ct* ct, const hs_sign_cfg* cfg, hs_ct** o
   });
 }
 
+// hs_decode_column's Tier-E body: enqueue the D2H copies of the column's chunks and either wait
+// for them (releasing the API lock, Runtime::wait) or return the stream they were enqueued on.
+// One copy per run of chunks that is contiguous on both sides (the outputs of hs_znorm_batch are
+// slices of one allocation: a 64-chunk column is one 16 MiB copy).  Chunks that carry a completion
+// event (fused statistics) are copied on the download stream after that event, beside whatever the
+// compute stream runs next; anything else keeps the compute stream's order.
+cudaStream_t decode_enqueue(size_t S, const hs_column* col, double* out, size_t remaining, bool wait) {
+  Runtime& rt = Runtime::get();
+  struct Run {
+    const double* src;
+    double* dst;
+    size_t n;
+    const DevBuf* owner;  // runs only grow inside one allocation (slices share its ownership)
+  };
+  std::vector<Run> runs;
+  std::vector<cudaEvent_t> evs;
+  bool all_ready = true, any_dev = false;
+  size_t o = 0;
+  for (uint64_t i = 0; i < col->n_chunks; ++i) {
+    const size_t take = std::min(S, remaining);
+    const Ct& x = get(col->chunks[i]);
+    if (take > x->n) fail(HS_E_LENGTH_MISMATCH, "decode_column: chunk shorter than slot count");
+    if (take) {
+      bool on_host, filling;
+      {
+        std::lock_guard<std::mutex> g(x->mu);
+        on_host = x->host_ok;
+        filling = static_cast<bool>(x->filling);
+      }
+      if (on_host || !x->dev) {
+        x->read_async(out + o, take, 0);  // host mirror: a memcpy
+      } else {
+        any_dev = true;
+        if (filling) x->device();  // an asynchronous encode in flight: the compute stream waits for it
+        if (x->ready && !filling) {
+          if (evs.empty() || evs.back() != x->ready->e) evs.push_back(x->ready->e);
+        } else {
+          all_ready = false;
+        }
+        const double* src = x->dev.get();
+        if (!runs.empty() && runs.back().src + runs.back().n == src && runs.back().dst + runs.back().n == out + o &&
+            !runs.back().owner->owner_before(x->dev) && !x->dev.owner_before(*runs.back().owner))
+          runs.back().n += take;
+        else
+          runs.push_back(Run{src, out + o, take, &x->dev});
+      }
+    }
+    o += take;
+    remaining -= take;
+  }
+  if (!any_dev) return nullptr;
+  const bool side = all_ready && !rt.capturing();
+  cudaStream_t st = side ? rt.download_stream() : rt.stream();
+  if (side)
+    for (cudaEvent_t e : evs) cuda_ok(cudaStreamWaitEvent(st, e, 0), "decode_column wait");
+  for (const Run& r : runs)
+    cuda_ok(cudaMemcpyAsync(r.dst, r.src, r.n * sizeof(double), cudaMemcpyDeviceToHost, st), "decode_column read");
+  if (wait) rt.wait(st);
+  return st;
+}
+
 // ---- columns ----------------------------------------------------------------------------------
 int hs_encode_column(hs_ctx* c, const double* v, uint64_t n, hs_ct** chunks_out, uint64_t* n_chunks) {
   return guard([&] {  // column.hpp:25-39
@@ -660,16 +739,101 @@ int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
       }
       return;
     }
-    for (uint64_t i = 0; i < col->n_chunks; ++i) {
-      const size_t take = std::min(S, remaining);
-      const Ct& x = get(col->chunks[i]);
-      if (take > x->n) fail(HS_E_LENGTH_MISMATCH, "decode_column: chunk shorter than slot count");
-      if (take) x->read_async(out + o, take, 0);
-      o += take;
-      remaining -= take;
-    }
-    Runtime::get().sync();
+    decode_enqueue(S, col, out, remaining, true);
   });
+}
+
+// ---- asynchronous column transfers (extension; the reference's encode_column / decode_column
+// are the synchronous calls above) --------------------------------------------------------------
+struct hs_pending {
+  std::shared_ptr<ReadyEv> done;      // fires when the enqueued work has completed (null: nothing to wait for)
+  std::unique_ptr<EncodePending> enc;  // encode: deferred finiteness verdict + staging buffer
+  bool settled = false;
+  int rc = HS_OK;
+  std::string err;
+};
+
+int hs_encode_column_async(hs_ctx* c, const double* v, uint64_t n, hs_ct** chunks_out, uint64_t* n_chunks,
+                           hs_pending** pending) {
+  return guard([&] {
+    hs_ctx* cc = ctxp(c);
+    need(n_chunks, "n_chunks");
+    need(pending, "pending");
+    if (n) {
+      need(v, "values");
+      need(chunks_out, "chunks_out");
+    }
+    auto p = std::make_unique<hs_pending>();
+    if (cc->rns || n == 0) {  // RNS contexts (host-side encoding) and empty columns: the synchronous call
+      const int rc = hs_encode_column(c, v, n, chunks_out, n_chunks);
+      if (rc != HS_OK) throw Error(rc, g_err);
+      p->settled = true;
+      *pending = p.release();
+      return;
+    }
+    p->enc = std::make_unique<EncodePending>();
+    DevB db(cc->p, cc->m);
+    std::vector<Ct> chunks = db.encrypt_column(v, static_cast<size_t>(n), p->enc.get());
+    p->done = p->enc->done;
+    for (size_t i = 0; i < chunks.size(); ++i) chunks_out[i] = wrap(chunks[i]);
+    *n_chunks = chunks.size();
+    *pending = p.release();
+  });
+}
+
+int hs_decode_column_async(const hs_ctx* c, const hs_column* col, double* out, hs_pending** pending) {
+  return guard([&] {
+    need(pending, "pending");
+    need(col, "column");
+    auto p = std::make_unique<hs_pending>();
+    if (ctxp(c)->rns) {
+      const int rc = hs_decode_column(c, col, out);
+      if (rc != HS_OK) throw Error(rc, g_err);
+      p->settled = true;
+      *pending = p.release();
+      return;
+    }
+    const size_t S = ctxp(c)->p.S;
+    if (col->n_valid > col->n_chunks * S) fail(HS_E_LENGTH_MISMATCH, "decode_column: n_valid exceeds packed capacity");
+    if (col->n_valid) need(out, "out");
+    cudaStream_t st = decode_enqueue(S, col, out, col->n_valid, false);
+    if (st)
+      p->done = Runtime::get().mark_on(st);
+    else
+      p->settled = true;
+    *pending = p.release();
+  });
+}
+
+// Blocks until the transfer has completed (the API lock is not held while waiting); returns the
+// call's deferred status: HS_E_NON_FINITE_VALUE for an encode whose input held a NaN or infinity
+// (its chunks must then be discarded), HS_OK otherwise.  Idempotent.
+int hs_pending_wait(hs_pending* p) {
+  if (!p) return HS_E_INVALID_ARG;
+  if (!p->settled) {
+    if (p->done) {
+      const cudaError_t e = cudaEventSynchronize(p->done->e);
+      if (e != cudaSuccess) {
+        g_err = std::string("hs_pending_wait: ") + cudaGetErrorString(e);
+        return HS_E_CUDA;
+      }
+    }
+    p->rc = guard([&] {
+      if (p->enc) p->enc->finish();
+    });
+    if (p->rc != HS_OK) p->err = g_err;
+    p->settled = true;
+  } else if (p->rc != HS_OK) {
+    g_err = p->err;
+  }
+  return p->rc;
+}
+
+void hs_pending_release(hs_pending* p) {
+  if (!p) return;
+  if (!p->settled) hs_pending_wait(p);  // the staging buffer and the caller's buffers are in use until then
+  std::lock_guard<std::recursive_mutex> lk(g_api_mu);
+  delete p;
 }
 
 // ---- statistics ---------------------------------------------------------------------------------

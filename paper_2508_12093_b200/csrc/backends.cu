@@ -2,6 +2,8 @@
 #include "backends.h"
 
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <string>
 
 namespace hsg {
@@ -15,12 +17,18 @@ namespace {
 // Where the device can read the caller's buffer directly (pinned, host-mapped
 // under UVA) the encrypt kernel reads it zero-copy; otherwise stage it through
 // a device buffer.  Returns the device-visible source pointer.
+// Large pinned inputs (>= kDmaBytes) go through the copy engine into a staging buffer
+// instead: the DMA runs at PCIe rate beside a statistics kernel that fills every SM (a
+// zero-copy k_encrypt would queue behind it, and reads host memory at less than half that
+// rate), and the encrypt kernel then reads HBM.
+constexpr size_t kDmaBytes = size_t(2) << 20;
 const double* device_source(const double* v, size_t n, DevBuf* stage, bool* pinned, cudaStream_t s) {
   Runtime& rt = Runtime::get();
   cudaPointerAttributes at{};
   *pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  if (*pinned && at.devicePointer) return static_cast<const double*>(at.devicePointer);
+  if (*pinned && at.devicePointer && n * sizeof(double) < kDmaBytes)
+    return static_cast<const double*>(at.devicePointer);
   if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return v;
   *stage = s == rt.stream() ? rt.alloc(n) : rt.alloc_on(n, s);
   cuda_ok(cudaMemcpyAsync(stage->get(), v, n * sizeof(double), cudaMemcpyHostToDevice, s), "encrypt upload");
@@ -32,7 +40,39 @@ int* bad_flag() {  // host-mapped pinned flag word, one per thread
   if (!f) cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&f), sizeof(int), cudaHostAllocMapped), "flag alloc");
   return f;
 }
+
+// flag words of asynchronous encodes (one per call in flight), recycled
+std::mutex g_flag_mu;
+std::vector<int*> g_flags;
+int* take_flag() {
+  {
+    std::lock_guard<std::mutex> g(g_flag_mu);
+    if (!g_flags.empty()) {
+      int* f = g_flags.back();
+      g_flags.pop_back();
+      return f;
+    }
+  }
+  int* f = nullptr;
+  cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&f), sizeof(int), cudaHostAllocMapped), "flag alloc");
+  return f;
+}
+void give_flag(int* f) {
+  std::lock_guard<std::mutex> g(g_flag_mu);
+  g_flags.push_back(f);
+}
 }  // namespace
+
+void EncodePending::finish() {
+  const bool nf = bad && *bad;
+  if (bad) give_flag(bad);
+  bad = nullptr;
+  stage.reset();
+  if (nf) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
+}
+EncodePending::~EncodePending() {
+  if (bad) give_flag(bad);
+}
 
 Ct DevB::encrypt(const double* v, size_t n) const {
   if (n > p_.S) fail(HS_E_TOO_MANY_VALUES, "encrypt: more values than slots");
@@ -48,7 +88,7 @@ Ct DevB::encrypt(const double* v, size_t n) const {
   return ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0);
 }
 
-std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
+std::vector<Ct> DevB::encrypt_column(const double* v, size_t n, EncodePending* pend) const {
   Runtime& rt = Runtime::get();
   std::vector<Ct> out;
   if (n == 0) return out;
@@ -63,17 +103,27 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n) const {
   DevBuf stage;
   bool pinned = false;
   const double* src = device_source(v, n, &stage, &pinned, s);
-  int* bad = bad_flag();
+  int* bad = pend ? take_flag() : bad_flag();
   *bad = 0;
-  for (size_t off = 0; off < n; off += p_.S) {
-    const size_t take = std::min(p_.S, n - off);
-    DevBuf d = rt.alloc_on(p_.S, s);
-    k::encrypt(qs_, src + off, take, d.get(), p_.S, bad, s);
-    out.push_back(ct_device(d, p_.S, p_.max_level, p_.quantize ? p_.scale_bits : 0));
-  }
+  // One allocation and one launch for the whole column: chunk c is the slice [c S, (c + 1) S) of
+  // the block (zero padding behind the last value included), so the kernel is the single-chunk
+  // one over n values and nch * S slots.
+  const size_t nch = (n + p_.S - 1) / p_.S;
+  const DevBuf block = rt.alloc_on(nch * p_.S, s);
+  k::encrypt(qs_, src, n, block.get(), nch * p_.S, bad, s);
+  for (size_t c = 0; c < nch; ++c)
+    out.push_back(ct_device(DevBuf(block, block.get() + c * p_.S), p_.S, p_.max_level,
+                            p_.quantize ? p_.scale_bits : 0));
   // the finiteness verdict (and the caller's buffer) must be settled before returning; the
   // outputs are then complete for any later compute-stream work
-  cuda_ok(cudaStreamSynchronize(s), "encode_column sync");
+  if (pend) {  // asynchronous: consumers order themselves behind `done` (CtData::device)
+    pend->done = rt.mark_on(s);
+    pend->bad = bad;
+    pend->stage = std::move(stage);
+    for (const Ct& c : out) c->filling = pend->done;
+    return out;
+  }
+  rt.wait(s);  // releases the API lock while this thread sleeps (api.cu wait_unlocked)
   if (*bad) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
   return out;
 }

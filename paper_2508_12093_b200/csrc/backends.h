@@ -119,6 +119,16 @@ class SymB : public LedgerBase<SymB, SymCt> {
 };
 
 // ---------------------------------------------------------------------------
+// The unsettled part of an asynchronous encode_column: completion event of its upload-stream
+// work, the finiteness flag that work writes, and the staging buffer it reads.
+struct EncodePending {
+  std::shared_ptr<ReadyEv> done;
+  int* bad = nullptr;
+  DevBuf stage;
+  void finish();  // after `done` has fired: returns the flag, frees the stage; throws non_finite_value
+  ~EncodePending();
+};
+
 class DevB : public LedgerBase<DevB, Ct> {
  public:
   using C = Ct;
@@ -127,7 +137,9 @@ class DevB : public LedgerBase<DevB, Ct> {
   int level(const C& c) const { return c ? c->level : 0; }
   C encrypt(const double* v, size_t n) const;  // ckks.hpp:97-104 (const: no meter)
   // encode_column's chunks (column.hpp:25-39) with the non-finite check on device
-  std::vector<C> encrypt_column(const double* v, size_t n) const;
+  // With `pend`, nothing is waited for: the chunks are marked `filling`, and the caller settles
+  // the finiteness verdict later (EncodePending::finish).
+  std::vector<C> encrypt_column(const double* v, size_t n, struct EncodePending* pend = nullptr) const;
   C encrypt_const(double c) const;
   C add_ct(const C& a, const C& b) { return addsub(a, b, k::B_ADD); }
   C sub_ct(const C& a, const C& b) { return addsub(a, b, k::B_SUB); }

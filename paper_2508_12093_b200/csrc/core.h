@@ -64,7 +64,25 @@ class Runtime {
   // stream's kernels (a caller can encode the next column while the current one computes).
   // encode_column synchronises it before returning, so its outputs are complete for any
   // later work on the compute stream without an event.
-  cudaStream_t upload_stream() const { return upload_; }
+  // One of kUploadStreams, round-robin per call: consecutive encode_column calls (host threads
+  // encoding ahead) do not order one column's copy behind the previous column's encrypt kernel,
+  // which may be waiting for SMs.  A caller keeps the stream it got for its whole operation.
+  cudaStream_t upload_stream() { return upload_[up_next_.fetch_add(1) % kUploadStreams]; }
+  // Result stream of decode_column: the D2H copies of ciphertexts that carry a `ready` event
+  // (outputs of the fused statistics) run here, beside the compute stream's next kernels.
+  cudaStream_t download_stream() const { return download_; }
+  // Block the calling thread until `s` has drained.  api.cu installs a hook that releases the
+  // API lock for the duration (hs_encode_column / hs_decode_column of one thread then overlap
+  // another thread's calls: PCIe is full duplex and the copy engines are independent).
+  void wait(cudaStream_t s) const;
+  static void set_wait_hook(void (*hook)(cudaStream_t));
+  // An event recorded on the compute stream now (null while the stream is being captured):
+  // the completion marker a fused statistic attaches to its outputs.
+  std::shared_ptr<struct ReadyEv> mark_ready();
+  std::shared_ptr<struct ReadyEv> mark_on(cudaStream_t s);  // the same on any stream
+  void compute_waits(const std::shared_ptr<struct ReadyEv>& ev);  // compute stream waits (deduplicated)
+  cudaEvent_t take_event();
+  void give_event(cudaEvent_t e);
   bool capturing() const;                   // the compute stream is being captured into a graph
   int device() const { return device_; }
   int sm_count() const { return sms_; }
@@ -88,7 +106,14 @@ class Runtime {
   int device_ = 0;
   int sms_ = 148;
   cudaStream_t stream_ = nullptr;
-  cudaStream_t upload_ = nullptr;
+  static constexpr unsigned kUploadStreams = 3;
+  cudaStream_t upload_[kUploadStreams] = {nullptr, nullptr, nullptr};
+  std::atomic<unsigned> up_next_{0};
+  cudaStream_t download_ = nullptr;
+  std::mutex ev_mu_;
+  std::atomic<uint64_t> ev_serial_{0};
+  uint64_t last_waited_ = 0;
+  std::vector<cudaEvent_t> ev_free_;
   std::atomic<uint64_t> launches_{0};
   std::mutex scratch_mu_;
   DevBuf scratch_[6];
@@ -110,11 +135,21 @@ inline int carveout_pct() {
 // grid > 0 records that every slot is a multiple of 2^-grid (the output of a
 // quantising op under scale_bits == grid); fused kernels rely on it to carry
 // values in exact integer grid units.
+struct ReadyEv {  // pooled event, returned to the runtime when the last holder drops it
+  cudaEvent_t e = nullptr;
+  uint64_t serial = 0;  // unique per recording (events are recycled)
+  ~ReadyEv();
+};
+
 struct CtData {
   size_t n = 0;
   int level = 0;
   int grid = 0;
   DevBuf dev;  // null for host-constructed ciphertexts until first device use
+  std::shared_ptr<ReadyEv> ready;  // set by the fused statistics: `dev` is complete once it has fired
+  // set by an asynchronous encode_column: `dev` is being written on an upload stream; the first
+  // device() use makes the compute stream wait for it
+  mutable std::shared_ptr<ReadyEv> filling;
   mutable std::mutex mu;
   mutable std::vector<double> host;
   mutable bool host_ok = false;
@@ -126,7 +161,7 @@ struct CtData {
 };
 using Ct = std::shared_ptr<const CtData>;
 
-Ct ct_device(DevBuf buf, size_t n, int level, int grid);
+Ct ct_device(DevBuf buf, size_t n, int level, int grid, std::shared_ptr<ReadyEv> ready = nullptr);
 Ct ct_host(std::vector<double> v, int level);  // Ciphertext(std::vector<double>, int)
 Ct ct_empty();                                 // Ciphertext()
 

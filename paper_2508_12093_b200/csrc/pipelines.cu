@@ -474,7 +474,9 @@ k::StatArgs stat_args(hs_ctx* ctx, const std::vector<const ColC*>& cols, int mod
   return a;
 }
 
-Ct make_out(hs_ctx* ctx, const DevBuf& b, int level) { return ct_device(b, ctx->p.S, level, out_grid(ctx->p)); }
+Ct make_out(hs_ctx* ctx, const DevBuf& b, int level, std::shared_ptr<ReadyEv> ready = nullptr) {
+  return ct_device(b, ctx->p.S, level, out_grid(ctx->p), std::move(ready));
+}
 
 }  // namespace
 
@@ -733,7 +735,9 @@ ColC znorm(hs_ctx* ctx, const ColC& col, double B, const InvCfg& cfg) {
     ctx->m = m;
     ColC z;
     z.n_valid = col.n_valid;
-    for (size_t c = 0; c < outs.size(); ++c) z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level));
+    const auto ready = rt.mark_ready();  // decode_column may fetch the result beside later compute work
+    for (size_t c = 0; c < outs.size(); ++c)
+      z.chunks.push_back(make_out(ctx, outs[c], r.chunks[c].level, ready));
     return z;
   }, dev);
 }
@@ -947,10 +951,11 @@ std::vector<ColC> znorm_batch(hs_ctx* ctx, const std::vector<ColC>& cols, double
     PB pb(p);
     pb.st(pb.invsqrt(pb.ldr(1), B * B, cfg), inv.get());  // crypto_invsqrt(var, B^2), stats.hpp:159
     pb.launch_zbatch(a);
+    const auto ready = rt.mark_ready();
     for (size_t k = 0; k < nb; ++k) {
       ColC z;
       z.n_valid = cols[b0 + k].n_valid;
-      z.chunks.push_back(make_out(ctx, zs[k], levels[b0 + k]));
+      z.chunks.push_back(make_out(ctx, zs[k], levels[b0 + k], ready));
       out.push_back(std::move(z));
     }
   }

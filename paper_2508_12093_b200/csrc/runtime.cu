@@ -69,7 +69,14 @@ Runtime::Runtime(int device) {
     if (l == 1 || l == 2 || l == 4) batch_lanes = l;
   }
   cuda_ok(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-  cuda_ok(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking), "cudaStreamCreate (upload)");
+  // The side streams carry short work that a caller is blocked on (encode_column's encrypt kernel,
+  // decode_column's copies): highest priority, so their blocks are placed before the next queued
+  // statistics launch when SMs free up.
+  int prio_lo = 0, prio_hi = 0;
+  cuda_ok(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "cudaDeviceGetStreamPriorityRange");
+  for (cudaStream_t& u : upload_)
+    cuda_ok(cudaStreamCreateWithPriority(&u, cudaStreamNonBlocking, prio_hi), "cudaStreamCreate (upload)");
+  cuda_ok(cudaStreamCreateWithPriority(&download_, cudaStreamNonBlocking, prio_hi), "cudaStreamCreate (download)");
   // Keep freed blocks in the stream-ordered pool: ciphertexts are churned per op.
   cudaMemPool_t pool;
   cuda_ok(cudaDeviceGetDefaultMemPool(&pool, device_), "cudaDeviceGetDefaultMemPool");
@@ -126,6 +133,56 @@ bool Runtime::capturing() const {
 
 void Runtime::sync() { cuda_ok(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
+namespace {
+void (*g_wait_hook)(cudaStream_t) = nullptr;
+}
+void Runtime::set_wait_hook(void (*hook)(cudaStream_t)) { g_wait_hook = hook; }
+void Runtime::wait(cudaStream_t s) const {
+  if (g_wait_hook)
+    g_wait_hook(s);
+  else
+    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+cudaEvent_t Runtime::take_event() {
+  {
+    std::lock_guard<std::mutex> g(ev_mu_);
+    if (!ev_free_.empty()) {
+      cudaEvent_t e = ev_free_.back();
+      ev_free_.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  return e;
+}
+void Runtime::give_event(cudaEvent_t e) {
+  std::lock_guard<std::mutex> g(ev_mu_);
+  ev_free_.push_back(e);
+}
+ReadyEv::~ReadyEv() {
+  if (e) Runtime::get().give_event(e);
+}
+std::shared_ptr<ReadyEv> Runtime::mark_ready() {
+  if (capturing()) return nullptr;
+  return mark_on(stream_);
+}
+std::shared_ptr<ReadyEv> Runtime::mark_on(cudaStream_t s) {
+  auto r = std::make_shared<ReadyEv>();
+  r->e = take_event();
+  r->serial = ++ev_serial_;
+  cuda_ok(cudaEventRecord(r->e, s), "cudaEventRecord (ready)");
+  return r;
+}
+void Runtime::compute_waits(const std::shared_ptr<ReadyEv>& ev) {
+  if (!ev) return;
+  std::lock_guard<std::mutex> g(ev_mu_);
+  if (last_waited_ == ev->serial) return;  // the chunks of one column share one event
+  cuda_ok(cudaStreamWaitEvent(stream_, ev->e, 0), "cudaStreamWaitEvent (upload)");
+  last_waited_ = ev->serial;
+}
+
 double* Runtime::scratch(int slot, size_t n, bool zero) {
   std::lock_guard<std::mutex> g(scratch_mu_);
   if (scratch_n_[slot] < n) {
@@ -139,6 +196,10 @@ double* Runtime::scratch(int slot, size_t n, bool zero) {
 // ---- ciphertext storage -----------------------------------------------------------
 const double* CtData::device() const {
   std::lock_guard<std::mutex> g(mu);
+  if (filling) {  // asynchronous encode_column still in flight: order the compute stream behind it
+    Runtime::get().compute_waits(filling);
+    filling.reset();
+  }
   if (!dev) {
     Runtime& rt = Runtime::get();
     DevBuf d = rt.alloc(n);
@@ -153,6 +214,10 @@ const double* CtData::device() const {
 
 const std::vector<double>& CtData::host_slots() const {
   std::lock_guard<std::mutex> g(mu);
+  if (filling) {
+    Runtime::get().compute_waits(filling);
+    filling.reset();
+  }
   if (!host_ok) {
     host.resize(n);
     if (n) {
@@ -182,6 +247,10 @@ void CtData::read_async(double* out, size_t count, size_t) const {
       std::memcpy(out, host.data(), count * sizeof(double));
       return;
     }
+    if (filling) {
+      Runtime::get().compute_waits(filling);
+      filling.reset();
+    }
   }
   Runtime& rt = Runtime::get();
   // copy-engine DMA straight into the caller's buffer (measured faster than SM stores
@@ -190,8 +259,9 @@ void CtData::read_async(double* out, size_t count, size_t) const {
           "ciphertext read");
 }
 
-Ct ct_device(DevBuf buf, size_t n, int level, int grid) {
+Ct ct_device(DevBuf buf, size_t n, int level, int grid, std::shared_ptr<ReadyEv> ready) {
   auto c = std::make_shared<CtData>();
+  c->ready = std::move(ready);
   c->n = n;
   c->level = level;
   c->grid = grid;

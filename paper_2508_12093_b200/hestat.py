@@ -528,6 +528,58 @@ def decode_column(ctx: EvalContext, col: EncryptedColumn, out: Optional[np.ndarr
     return out
 
 
+class Pending:
+    """An asynchronous transfer in flight (hs_pending).  ``wait()`` blocks until it has completed
+    and raises the call's deferred error (non_finite_value for an encode whose input held a NaN or
+    infinity).  The host buffer handed to the call must not be touched until then."""
+
+    __slots__ = ("_h", "_keep")
+
+    def __init__(self, h: C.c_void_p, keep=None):
+        self._h = h
+        self._keep = keep  # host arrays and ctypes views the transfer still uses
+
+    def wait(self) -> None:
+        _check(_abi.lib().hs_pending_wait(self._h))
+        self._keep = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        try:
+            if h is not None and h.value and _abi._lib is not None:
+                _abi._lib.hs_pending_release(h)
+        except Exception:  # interpreter teardown
+            pass
+        self._h = None
+
+
+def encode_column_async(ctx: EvalContext, values, name: str = ""):
+    """encode_column without the wait: returns (column, Pending).  The column can be passed to
+    any op at once (the library orders its streams behind the upload); ``Pending.wait()`` delivers
+    the finiteness verdict.  ``values`` (pinned for a DMA at PCIe rate) must stay untouched until
+    then."""
+    v = values if (isinstance(values, np.ndarray) and values.dtype == np.float64 and values.ndim == 1
+                   and values.flags.c_contiguous) else _arr(values)
+    S = ctx._p.slot_count
+    nch = (len(v) + S - 1) // S
+    arr = _ptr_array(nch)()
+    got = C.c_uint64(0)
+    h = C.c_void_p()
+    _check(_abi.lib().hs_encode_column_async(ctx._h, _dp(v), len(v), arr, C.byref(got), C.byref(h)))
+    return EncryptedColumn._from_handles(arr, got.value, len(v), name), Pending(h, v)
+
+
+def decode_column_async(ctx: EvalContext, col: EncryptedColumn, out: np.ndarray) -> Pending:
+    """decode_column without the wait: ``out`` (a contiguous float64 array of n_valid elements,
+    pinned for direct DMA) holds the slots once ``Pending.wait()`` returns."""
+    if out.dtype != np.float64 or not out.flags.c_contiguous or out.size < col.n_valid:
+        raise length_mismatch("decode_column: out must be a contiguous float64 array of n_valid elements")
+    c, keep = col._c()
+    h = C.c_void_p()
+    _check(_abi.lib().hs_decode_column_async(ctx._h, C.byref(c), _dp(out) if len(out) else None, C.byref(h)))
+    return Pending(h, (out, col, keep))
+
+
 # ---- stats.hpp ------------------------------------------------------------------------------------
 @dataclass
 class MomentSet:  # stats.hpp:18-22
