@@ -446,8 +446,8 @@ def rns_traffic(op, logN, L, K):
 
 def zbatch_lanes():
     """Threads per slot of the batched Z-score kernel (the library's default, or HESTAT_BATCH_LANES)."""
-    v = os.environ.get("HESTAT_BATCH_LANES", "4")
-    return int(v) if v in ("1", "2", "4") else 4
+    v = os.environ.get("HESTAT_BATCH_LANES", "")
+    return int(v) if v in ("1", "2", "4") else 1  # the library's choice for a 64-ciphertext step
 
 
 def zbatch_traffic(kb):

@@ -94,7 +94,9 @@ class Runtime {
   uint64_t launches() const { return launches_.load(); }
   bool fused = true;
   int prog_lanes = 2;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
-  int batch_lanes = 4;  // the same for the batched Z-score kernel (HESTAT_BATCH_LANES: 1, 2, 4)
+  // the same for the batched Z-score kernel (HESTAT_BATCH_LANES: 1, 2, 4); 0 = by batch size: one
+  // thread per slot once a block has two full rounds of items (no work is repeated across lanes)
+  int batch_lanes = 0;
 
   // Persistent device scratch buffer `slot` of at least n doubles (grown on
   // demand; zero-filled when (re)allocated if `zero`).  All device work is ordered

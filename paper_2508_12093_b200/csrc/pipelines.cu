@@ -332,7 +332,11 @@ class PB {
  private:
   void finish(bool stat, const k::StatArgs* a) {
     Runtime& rt = Runtime::get();
-    const int lanes = !big_cheb_ ? 1 : (zbatch_ ? rt.batch_lanes : rt.prog_lanes);
+    int lanes = !big_cheb_ ? 1 : (zbatch_ ? rt.batch_lanes : rt.prog_lanes);
+    if (big_cheb_ && zbatch_ && lanes == 0) {
+      const size_t items = (p_.S + rt.sm_count() - 1) / rt.sm_count() * static_cast<size_t>(zbatch_->ncols);
+      lanes = items >= 2048 ? 1 : (items >= 1024 ? 2 : 4);
+    }
     int p = 0;
     while ((1 << p) < lanes) ++p;
     // one concatenated table per distinct series (deduplicated), cached on the

@@ -446,8 +446,15 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const 
 // ---- many independent Z-scores (kernels.h ZBatchArgs) ----------------------------------------
 constexpr int kZA = 3 * kMaxZBatch;
 
+// The batch has thousands of (column, slot) items per block whatever P is: every lane count runs
+// the largest block (64 registers per thread).
+#ifndef HS_ZB_THREADS
+#define HS_ZB_THREADS 1024
+#endif
+constexpr int kZbThreads = HS_ZB_THREADS;
+
 template <class Q, int P>
-__global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_zbatch(Q q, const __grid_constant__ ZBatchArgs a,
+__global__ void __launch_bounds__(kZbThreads, 1) k_zbatch(Q q, const __grid_constant__ ZBatchArgs a,
                                                          const __grid_constant__ Prog pg) {
   extern __shared__ double stab[];
   __shared__ double tot[2 * kZA];
@@ -619,8 +626,13 @@ void run_zbatch(QSpec qs, const ZBatchArgs& a, const Prog& p, int lanes, cudaStr
   const QGrid Q{ldexp(1.0, qs.bits), ldexp(1.0, -qs.bits)};
   const size_t smem = static_cast<size_t>(p.ntab) * sizeof(double);
   auto go = [&](auto kern, int P) {
-    const int maxt = P == 1 ? prog_max_threads<1>() : (P == 2 ? prog_max_threads<2>() : prog_max_threads<4>());
-    const Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+    const int maxt = kZbThreads;
+    Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+    {  // a block's items are its slots of EVERY column: size the block for them, not for one column
+      const size_t spb = (p.S + geo.blocks - 1) / geo.blocks;
+      const size_t want = ((spb * static_cast<size_t>(a.ncols) * P + 31) / 32) * 32;
+      geo.threads = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(maxt)));
+    }
     const int cap = max_blocks(kern, smem, static_cast<int>(geo.threads));
     if (cap < static_cast<int>(geo.blocks)) fail(HS_E_CUDA, "znorm batch kernel: grid not co-resident");
     QGrid qv = Q;
