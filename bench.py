@@ -18,7 +18,7 @@ znorm of one ciphertext.
          runs znorm_batch and decodes the results (16 MiB D2H), all inside the
          timed region, as a one-thread software pipeline over the asynchronous
          calls (encode_column_async k+1 | znorm_batch k | decode_column_async k,
-         then the waits for k's verdict and k-1's results).
+         then the waits for k's verdict and k-2's results).
          `e2e_single_call` is the one-ciphertext-per-step loop (and its
          strictly sequential latency and pageable-buffer variants).
 
@@ -452,7 +452,7 @@ def zbatch_lanes():
 
 def zbatch_traffic(kb):
     """DRAM bytes per k_zbatch launch of kb ciphertexts from the committed ncu --set full summary."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_ncu.json")
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_p1_ncu.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -761,7 +761,7 @@ def main():
     # launch on an upload stream), each chunk its own single-chunk column, znorm_batch (ordered
     # behind the upload on the device), decode_column_async of the KB result chunks as one column
     # (one 16 MiB D2H DMA on the download stream); the host waits for step k's finiteness verdict
-    # and step k-1's results while step k computes, so both copy engines and the SMs stay busy.
+    # and step k-2's results while step k computes, so both copy engines and the SMs stay busy.
     # Every step's input is copied H2D and its whole result D2H inside the timed region; host
     # buffers rotate over NBUF pinned pairs.
     NBUF = 4
@@ -789,9 +789,10 @@ def main():
                 col_, pe = benc(k_ + 1)
             dq.append(bdec(zs_, k_))
             pk.wait()  # encode k's finiteness verdict
-            while len(dq) > 1:
-                dq.pop(0).wait()  # step k-1's results are in host memory
-        dq.pop(0).wait()
+            while len(dq) > 2:
+                dq.pop(0).wait()  # step k-2's results are in host memory
+        while dq:
+            dq.pop(0).wait()
 
     e2e_loop(max(args.warmup, 8))
     for b_ in zbn:
@@ -978,7 +979,7 @@ def main():
                     "mode": f"pipelined, {KB} ciphertexts per step, one host thread: encode_column_async of step "
                             f"k+1's {KB} x 2^15 values (16 MiB H2D DMA + encrypt on an upload stream), znorm_batch "
                             "of step k, decode_column_async of its results (16 MiB D2H DMA on the download "
-                            "stream), then the waits for step k's finiteness verdict and step k-1's results; "
+                            "stream), then the waits for step k's finiteness verdict and step k-2's results; "
                             "public API calls only",
                     "synchronous_calls_wall_ms_per_ciphertext": be2e_sync_wall_ms / (be2e_steps * KB),
                     "synchronous_calls_mode": "the same step with the reference-shaped blocking calls "
@@ -1006,7 +1007,7 @@ def main():
                          "work": f"{step_per_slot} fp64 ops/slot x {S} slots x {KB} ciphertexts",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "traffic_source": "profiles/r2_zbatch_ncu.json (ncu --set full, one k_zbatch launch of "
+                         "traffic_source": "profiles/r2_zbatch_p1_ncu.json (ncu --set full, one k_zbatch launch of "
                                            "64 ciphertexts, dram read+write; algorithmic: 16 B per slot and "
                                            "ciphertext, 32 MiB per launch)",
                          "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",

@@ -97,19 +97,38 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n, EncodePending* p
   if (rt.capturing())
     fail(HS_E_INVALID_ARG, "encode_column cannot run inside hs_graph_begin/hs_graph_end: encode the "
                            "columns first and capture the computation on them");
-  // On the upload stream: the host input is read and encrypted beside whatever the compute
+  // On an upload stream: the host input is read and encrypted beside whatever the compute
   // stream is running, and only this work is waited for below.
-  cudaStream_t s = rt.upload_stream();
-  DevBuf stage;
-  bool pinned = false;
-  const double* src = device_source(v, n, &stage, &pinned, s);
+  const unsigned ui = rt.next_upload();
+  cudaStream_t s = rt.upload_stream_at(ui);
+  const size_t nch = (n + p_.S - 1) / p_.S;
   int* bad = pend ? take_flag() : bad_flag();
   *bad = 0;
+  DevBuf stage, block;
+  bool pinned = false;
+  cudaPointerAttributes at{};
+  const bool host_pinned = cudaPointerGetAttributes(&at, v) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const double* src;
+  if (host_pinned && n * sizeof(double) >= kDmaBytes) {
+    // Large pinned column: copy-engine DMA into the stream's persistent staging buffer, output
+    // block from the compute stream's pool (whose freed blocks are reusable at once; an
+    // upload-stream allocation would have to map new memory whenever the pool's free blocks still
+    // wait on compute-stream work), the encrypt kernel ordered behind the allocation point.
+    double* st = rt.upload_stage(ui, n);
+    cuda_ok(cudaMemcpyAsync(st, v, n * sizeof(double), cudaMemcpyHostToDevice, s), "encrypt upload");
+    block = rt.alloc(nch * p_.S);
+    const auto here = rt.mark_on(rt.stream());
+    cuda_ok(cudaStreamWaitEvent(s, here->e, 0), "encode_column order");
+    src = st;
+    pinned = true;
+  } else {
+    src = device_source(v, n, &stage, &pinned, s);
+    block = rt.alloc_on(nch * p_.S, s);
+  }
   // One allocation and one launch for the whole column: chunk c is the slice [c S, (c + 1) S) of
   // the block (zero padding behind the last value included), so the kernel is the single-chunk
   // one over n values and nch * S slots.
-  const size_t nch = (n + p_.S - 1) / p_.S;
-  const DevBuf block = rt.alloc_on(nch * p_.S, s);
   k::encrypt(qs_, src, n, block.get(), nch * p_.S, bad, s);
   for (size_t c = 0; c < nch; ++c)
     out.push_back(ct_device(DevBuf(block, block.get() + c * p_.S), p_.S, p_.max_level,

@@ -67,7 +67,13 @@ class Runtime {
   // One of kUploadStreams, round-robin per call: consecutive encode_column calls (host threads
   // encoding ahead) do not order one column's copy behind the previous column's encrypt kernel,
   // which may be waiting for SMs.  A caller keeps the stream it got for its whole operation.
-  cudaStream_t upload_stream() { return upload_[up_next_.fetch_add(1) % kUploadStreams]; }
+  cudaStream_t upload_stream() { return upload_[next_upload()]; }
+  unsigned next_upload() { return up_next_.fetch_add(1) % kUploadStreams; }
+  cudaStream_t upload_stream_at(unsigned i) const { return upload_[i]; }
+  // Upload stream i's persistent staging buffer of at least n doubles (grown on demand, which
+  // synchronises that stream; steady state allocates nothing).  Work that uses it is ordered by
+  // the stream, so consecutive encodes on one stream reuse it safely.
+  double* upload_stage(unsigned i, size_t n);
   // Result stream of decode_column: the D2H copies of ciphertexts that carry a `ready` event
   // (outputs of the fused statistics) run here, beside the compute stream's next kernels.
   cudaStream_t download_stream() const { return download_; }
@@ -111,6 +117,9 @@ class Runtime {
   static constexpr unsigned kUploadStreams = 3;
   cudaStream_t upload_[kUploadStreams] = {nullptr, nullptr, nullptr};
   std::atomic<unsigned> up_next_{0};
+  std::mutex stage_mu_;
+  double* stage_[kUploadStreams] = {nullptr, nullptr, nullptr};
+  size_t stage_n_[kUploadStreams] = {0, 0, 0};
   cudaStream_t download_ = nullptr;
   std::mutex ev_mu_;
   std::atomic<uint64_t> ev_serial_{0};

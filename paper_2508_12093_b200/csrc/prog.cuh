@@ -21,15 +21,33 @@ constexpr int kMaxK = 10;  // T_{2^0} .. T_{2^9}; degree <= 1023
 //
 // F_K: full tree of degree 2^K - 1 (K >= 1) or a degree-0 leaf (K == 0).
 // Table layout [F_{K-1}(q) | F_{K-1}(r)], leaves (c1, c0).  chebyshev.hpp:140-158.
-template <int K, int ST, class F>
+//
+// Pipe balance (sm_100a, ncu of k_zbatch): a magic-constant rounding is two FP64-pipe
+// instructions (add M, subtract M; the add folds into an FMA for products), FRND.F64 is one XU
+// instruction at a quarter of the FP64 rate, and the two pipes issue side by side.  All-magic
+// leaves the XU pipe idle with the FP64 pipe at 81 %; all-FRND is XU bound.  The leaves
+// (mul_pt + add_pt, two roundings each, two thirds of the tree's roundings) therefore round with
+// FRND on the leaf positions selected by kLeafMulX / kLeafAddX (bit j: leaves with index = j
+// mod 8), everything else with the magic constant: both forms give the same bits (quant.cuh).
+#ifndef HS_LEAF_MULX
+#define HS_LEAF_MULX 0xFF
+#endif
+#ifndef HS_LEAF_ADDX
+#define HS_LEAF_ADDX 0x55
+#endif
+constexpr unsigned kLeafMulX = HS_LEAF_MULX, kLeafAddX = HS_LEAF_ADDX;
+
+template <int K, int ST, int J = 0, class F>
 __device__ __forceinline__ double ffull(const F& f, const double* t, const double (&T)[kMaxK]) {
-  if constexpr (K <= 1) {
-    return f.addc(f.mulc(T[0], t[0]), t[ST]);  // add_pt(mul_pt(x, c1), c0)
+  if constexpr (K <= 1) {  // add_pt(mul_pt(x, c1), c0)
+    constexpr bool mx = (kLeafMulX >> (J & 7)) & 1u, ax = (kLeafAddX >> (J & 7)) & 1u;
+    const double m = mx ? f.mulc_x(T[0], t[0]) : f.mulc(T[0], t[0]);
+    return ax ? f.addc_x(m, t[ST]) : f.addc(m, t[ST]);
   } else {
     constexpr int H = (1 << (K - 1)) * ST;
-    const double head = f.mul(ffull<K - 1, ST>(f, t, T), T[K - 1]);  // mul_ct(eval(q), T_g)
-    const double rest = ffull<K - 1, ST>(f, t + H, T);
-    return f.add(head, rest);                                       // add_ct(head, eval(r))
+    const double head = f.mul(ffull<K - 1, ST, 2 * J>(f, t, T), T[K - 1]);  // mul_ct(eval(q), T_g)
+    const double rest = ffull<K - 1, ST, 2 * J + 1>(f, t + H, T);
+    return f.add(head, rest);                                              // add_ct(head, eval(r))
   }
 }
 

@@ -38,6 +38,8 @@ struct QNone {
   __device__ __forceinline__ double mul(double a, double b) const { return __dmul_rn(a, b); }
   __device__ __forceinline__ double mulc(double a, double c) const { return __dmul_rn(a, c); }
   __device__ __forceinline__ double addc(double a, double c) const { return __dadd_rn(a, c); }
+  __device__ __forceinline__ double mulc_x(double a, double c) const { return __dmul_rn(a, c); }
+  __device__ __forceinline__ double addc_x(double a, double c) const { return __dadd_rn(a, c); }
   __device__ __forceinline__ double req(double a) const { return a; }
 };
 
@@ -112,6 +114,9 @@ struct QGridFast {
   __device__ __forceinline__ double addc(double a, double cs) const {
     return magic_round_nz(__dadd_rn(__dadd_rn(a, cs), kMagic));
   }
+  // the same roundings on the XU pipe (FRND.F64): QGrid's own forms, valid for any magnitude
+  __device__ __forceinline__ double mulc_x(double a, double c) const { return rint(__dmul_rn(a, c)); }
+  __device__ __forceinline__ double addc_x(double a, double cs) const { return rint(__dadd_rn(a, cs)); }
 };
 
 template <class Q>

@@ -144,6 +144,19 @@ void Runtime::wait(cudaStream_t s) const {
     cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
+double* Runtime::upload_stage(unsigned i, size_t n) {
+  std::lock_guard<std::mutex> g(stage_mu_);
+  if (stage_n_[i] < n) {
+    cuda_ok(cudaStreamSynchronize(upload_[i]), "upload stage sync");
+    if (stage_[i]) cuda_ok(cudaFree(stage_[i]), "upload stage free");
+    stage_[i] = nullptr;
+    stage_n_[i] = 0;
+    cuda_ok(cudaMalloc(reinterpret_cast<void**>(&stage_[i]), n * sizeof(double)), "upload stage alloc");
+    stage_n_[i] = n;
+  }
+  return stage_[i];
+}
+
 cudaEvent_t Runtime::take_event() {
   {
     std::lock_guard<std::mutex> g(ev_mu_);

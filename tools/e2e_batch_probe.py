@@ -118,17 +118,29 @@ def main():
         t0 = time.perf_counter()
         col, pe = aenc(0)
         dq = collections.deque()
+        ht = {"znorm_batch": 0.0, "encode_async": 0.0, "decode_async": 0.0, "wait_enc": 0.0, "wait_dec": 0.0}
+        pc = time.perf_counter
         for k in range(steps):
+            a0 = pc()
             zs = H.znorm_batch(ctx, col, B)  # ordered behind encode k on the device
+            a1 = pc()
             pk = pe
             if k + 1 < steps:
                 col, pe = aenc(k + 1)
+            a2 = pc()
             dq.append(adec(zs, k))
+            a3 = pc()
             pk.wait()  # encode k's finiteness verdict
+            a4 = pc()
             while len(dq) > args.lag - 1:
                 dq.popleft().wait()
+            a5 = pc()
+            for n_, v_ in zip(ht, (a1 - a0, a2 - a1, a3 - a2, a4 - a3, a5 - a4)):
+                ht[n_] += v_
         while dq:
             dq.popleft().wait()
+        if rep:
+            print("async loop host time per step (ms):", {n_: round(1e3 * v_ / steps, 3) for n_, v_ in ht.items()})
         H.sync()
         t_async = 1e3 * (time.perf_counter() - t0) / steps
     ok2 = all(np.array_equal(bits(zb[i][:S]), bits(ref.out)) for i in range(nbuf))
