@@ -452,7 +452,7 @@ def zbatch_lanes():
 
 def zbatch_traffic(kb):
     """DRAM bytes per k_zbatch launch of kb ciphertexts from the committed ncu --set full summary."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_p1_ncu.json")
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_mix_ncu.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -829,6 +829,19 @@ def main():
     barrier_sync()
     be2e_sync_wall_ms = 1e3 * (time.perf_counter() - t0)
     del bcol, zs_
+    # the same pipeline from a C++ host over the drop-in headers (tests/dropin/ext_pipeline.cpp,
+    # built by build(); it checks its results against decode_column(znorm(encode_column(x))))
+    cpp_e2e = None
+    cpp_bin = os.path.join(ROOT, "build", "ext_pipeline_gpu")
+    if ws == 1 and os.path.exists(cpp_bin):
+        barrier_sync()
+        try:
+            r_ = subprocess.run([cpp_bin, str(S), str(KB), str(max(be2e_steps, 40))], capture_output=True, text=True,
+                                timeout=300)
+            if r_.returncode == 0 and "ext_pipeline ok" in r_.stdout:
+                cpp_e2e = float(r_.stdout.split("steps,")[1].split("us/ciphertext")[0]) / 1e3
+        except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+            cpp_e2e = None
 
     # ---- kernel roofline: the fused inverse-sqrt program (dominant phase) -------------------
     # Both probes replay CUDA graphs of `reps` calls (device time only).
@@ -981,6 +994,9 @@ def main():
                             "of step k, decode_column_async of its results (16 MiB D2H DMA on the download "
                             "stream), then the waits for step k's finiteness verdict and step k-2's results; "
                             "public API calls only",
+                    "cpp_host_ms_per_ciphertext": cpp_e2e,
+                    "cpp_host": "the same pipeline from a C++ host over include/hestat/*.hpp "
+                                "(build/ext_pipeline_gpu, own process, bit-checked against the blocking calls)",
                     "synchronous_calls_wall_ms_per_ciphertext": be2e_sync_wall_ms / (be2e_steps * KB),
                     "synchronous_calls_mode": "the same step with the reference-shaped blocking calls "
                                               "(encode_column k+1 beside znorm_batch k, decode_column k)",
@@ -1007,7 +1023,7 @@ def main():
                          "work": f"{step_per_slot} fp64 ops/slot x {S} slots x {KB} ciphertexts",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "traffic_source": "profiles/r2_zbatch_p1_ncu.json (ncu --set full, one k_zbatch launch of "
+                         "traffic_source": "profiles/r2_zbatch_mix_ncu.json (ncu --set full, one k_zbatch launch of "
                                            "64 ciphertexts, dram read+write; algorithmic: 16 B per slot and "
                                            "ciphertext, 32 MiB per launch)",
                          "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",

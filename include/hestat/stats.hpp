@@ -106,6 +106,35 @@ inline Ciphertext pearson(EvalContext& ctx, const EncryptedColumn& col_x, const 
   return ctx.run([&](hs_ct** o) { return hs_pearson(ctx.raw(), &vx.c, &vy.c, B, &c, o); });
 }
 
+// Extension: znorm(cols[k], B) for every column, in order (hs_znorm_batch: one launch per 64
+// single-chunk columns; same slots, levels and meter as the calls).
+inline std::vector<EncryptedColumn> znorm_batch(EvalContext& ctx, const std::vector<EncryptedColumn>& cols, double B,
+                                                const InvRootConfig& cfg = {}) {
+  std::vector<EncryptedColumn::CView> views;
+  views.reserve(cols.size());
+  size_t total = 0;
+  for (const EncryptedColumn& c : cols) {
+    views.push_back(c.to_c());
+    total += c.chunks.size();
+  }
+  std::vector<const hs_column*> ptrs;
+  for (const auto& v : views) ptrs.push_back(&v.c);
+  const hs_invroot_cfg c = cfg.to_c();
+  std::vector<hs_ct*> hs(total ? total : 1, nullptr);
+  gpu::check(hs_znorm_batch(ctx.raw(), ptrs.data(), static_cast<uint32_t>(cols.size()), B, &c, hs.data()));
+  std::vector<EncryptedColumn> out;
+  size_t off = 0;
+  for (const EncryptedColumn& col : cols) {
+    EncryptedColumn z;
+    z.n_valid = col.n_valid;
+    z.name = col.name;
+    for (size_t i = 0; i < col.chunks.size(); ++i) z.chunks.push_back(Ciphertext::adopt(hs[off + i]));
+    off += col.chunks.size();
+    out.push_back(std::move(z));
+  }
+  return out;
+}
+
 // Extension: pearson(cols[i], cols[j]) for every pair i < j, in that order (hs_pearson_table).
 inline std::vector<Ciphertext> pearson_table(EvalContext& ctx, const std::vector<EncryptedColumn>& cols, double B,
                                              const InvRootConfig& cfg = {}) {

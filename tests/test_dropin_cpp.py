@@ -59,3 +59,14 @@ def test_reference_acceptance_runner_on_rns(crit, name):
                        timeout=900, cwd=FIXTURE_CWD, env=env)
     assert f"[PASS] {name}" in r.stdout, r.stdout + r.stderr[-2000:]
     assert r.returncode == 0, r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [("4096", "8", "6"), ("32768", "64", "12")])
+def test_cpp_extension_pipeline(args):
+    """tests/dropin/ext_pipeline.cpp (our own program over the drop-in headers): znorm_batch and
+    the asynchronous encode_column / decode_column pipeline from pinned memory reproduce
+    decode_column(znorm(encode_column(x))) bit for bit, and a NaN input is reported by wait()."""
+    r = subprocess.run([_bin("ext_pipeline_gpu"), *args], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-2000:]
+    assert "ext_pipeline ok" in r.stdout, r.stdout
