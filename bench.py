@@ -219,7 +219,7 @@ def special_primes(L, dnum, logq0=60, logq=40, logp=44):
     return -(-(logq0 + (alpha - 1) * logq) // logp)
 
 
-def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None, logp=44):
+def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None, logp=44, rot_steps=()):
     """Device time per ciphertext of each Tier-R op (CUDA-graph replay of `reps`
     batched calls), inputs resident; returns {op: us_per_ct}, launches per op."""
     from paper_2508_12093_b200 import _abi
@@ -243,6 +243,9 @@ def rns_measure(torch, stream, logN, L, K, dnum, batch, reps=3, ops=None, logp=4
         "rescale": lambda: c.rescale(L, x, out, batch=batch),
         "rotate": lambda: c.rotate(L, 1, x, out, batch=batch),
     }
+    for st_ in rot_steps:  # C5: rotation steps 1, 2, 4 ... 2^14 (each its own Galois key)
+        c.prepare_rotation(st_)
+        fns[f"rotate_{st_}"] = (lambda st__: lambda: c.rotate(L, st__, x, out, batch=batch))(st_)
     res, launches = {}, {}
     for name, fn in fns.items():
         if ops and name not in ops:
@@ -549,11 +552,16 @@ def c5_sweep(args):
     peak, src = hbm_peak_gbs()
     for logN in (14, 15, 16):
         for L in (8, 16, 24, 32):
-            dnum = 3
+            # dnum = 2 measured fastest with the round-2 kernels (profiles/r2_summary.md; the bench shape); the
+            # tensor-core base conversion takes digits of up to 16 primes, so L = 32 runs dnum = 3
+            dnum = 2 if (L + 2) // 2 <= 16 else 3
             K = special_primes(L, dnum)
-            us, launches = rns_measure(torch, stream, logN, L, K, dnum, args.batch)
+            steps_ = tuple(1 << j for j in range(1, logN - 1)) if (logN, L) == (16, 24) else ()
+            us, launches = rns_measure(torch, stream, logN, L, K, dnum, args.batch, rot_steps=steps_)
             ab = rns_alg_bytes(logN, L, K, dnum, L)
             ab["intt"] = ab["ntt"]
+            for st_ in steps_:
+                ab[f"rotate_{st_}"] = ab["rotate"]
             line = {"sweep": "C5 tier R", "logN": logN, "L": L, "K": K, "dnum": dnum, "logp": 44, "batch": args.batch,
                     "peak_gbs": peak, "ops": {k: {"us_per_ct": round(v, 2), "ops_per_s": round(1e6 / v, 1),
                                                   "hbm_frac": round(ab[k] / (v * 1e-6) / 1e9 / peak, 4)}
