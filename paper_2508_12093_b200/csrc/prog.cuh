@@ -71,7 +71,8 @@ __device__ __forceinline__ double ffull_small(int K, const F& f, const double* t
     case 2: return ffull<2, ST>(f, t, T);
     case 3: return ffull<3, ST>(f, t, T);
     case 4: return ffull<4, ST>(f, t, T);
-    default: return ffull<5, ST>(f, t, T);
+    case 5: return ffull<5, ST>(f, t, T);
+    default: return ffull<(kBK > 5 ? kBK : 5), ST>(f, t, T);
   }
 }
 
