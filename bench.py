@@ -581,6 +581,9 @@ def main():
     ap.add_argument("--no-tier-r", action="store_true")
     ap.add_argument("--c5", action="store_true", help="print the C5 tier-R sweep instead")
     ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--profile-step", action="store_true",
+                    help="only the timed step, eagerly, between cudaProfilerStart/Stop (for ncu "
+                         "--profile-from-start off: the launch list of exactly the K timed steps)")
     ap.add_argument("--batch-cols", type=int, default=64,
                     help="independent C2 ciphertexts per step (hs_znorm_batch, <= 64 per launch)")
     args = ap.parse_args()
@@ -666,6 +669,15 @@ def main():
         zb = H.znorm_batch(ctx, bcols(i), B)
         del zb
     barrier_sync()
+    if args.profile_step:  # the K steps of the timed region, eager, inside the profiler range
+        torch.cuda.cudart().cudaProfilerStart()
+        for i in range(args.steps):
+            zb = H.znorm_batch(ctx, bcols(i), B)
+            del zb
+        barrier_sync()
+        torch.cuda.cudart().cudaProfilerStop()
+        print(json.dumps({"profile_step": True, "steps": args.steps, "parity_vs_oracle": parity and bparity}))
+        return 0
     bl0 = H.kernel_launches()
     with H.Graph() as bgraph:
         for i in range(args.steps):
