@@ -332,9 +332,10 @@ class PB {
  private:
   void finish(bool stat, const k::StatArgs* a) {
     Runtime& rt = Runtime::get();
-    int lanes = !big_cheb_ ? 1 : (zbatch_ ? rt.batch_lanes : rt.prog_lanes);
-    if (big_cheb_ && zbatch_ && lanes == 0) {
-      const size_t items = (p_.S + rt.sm_count() - 1) / rt.sm_count() * static_cast<size_t>(zbatch_->ncols);
+    int lanes = !big_cheb_ ? 1 : ((zbatch_ || table_) ? rt.batch_lanes : rt.prog_lanes);
+    if (big_cheb_ && (zbatch_ || table_) && lanes == 0) {
+      const size_t ncols = zbatch_ ? zbatch_->ncols : table_->ncols;
+      const size_t items = (p_.S + rt.sm_count() - 1) / rt.sm_count() * ncols;
       lanes = items >= 2048 ? 1 : (items >= 1024 ? 2 : 4);
     }
     int p = 0;

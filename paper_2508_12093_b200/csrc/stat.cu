@@ -371,8 +371,15 @@ __device__ bool table_totals(const GridBar& grid, double* accum, unsigned* count
   return exact;
 }
 
+// The batched kernels (Pearson table, Z-score batch) have hundreds to thousands of (column, slot)
+// items per block whatever P is: every lane count may run the largest block (64 registers per thread).
+#ifndef HS_ZB_THREADS
+#define HS_ZB_THREADS 1024
+#endif
+constexpr int kZbThreads = HS_ZB_THREADS;
+
 template <class Q, int P>
-__global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const __grid_constant__ PTableArgs a,
+__global__ void __launch_bounds__(kZbThreads, 1) k_ptable(Q q, const __grid_constant__ PTableArgs a,
                                                          const __grid_constant__ Prog pg) {
   extern __shared__ double stab[];
   __shared__ double totA[2 * kTA], totB[2 * kTB];
@@ -445,13 +452,6 @@ __global__ void __launch_bounds__(prog_max_threads<P>(), 1) k_ptable(Q q, const 
 
 // ---- many independent Z-scores (kernels.h ZBatchArgs) ----------------------------------------
 constexpr int kZA = 3 * kMaxZBatch;
-
-// The batch has thousands of (column, slot) items per block whatever P is: every lane count runs
-// the largest block (64 registers per thread).
-#ifndef HS_ZB_THREADS
-#define HS_ZB_THREADS 1024
-#endif
-constexpr int kZbThreads = HS_ZB_THREADS;
 
 template <class Q, int P>
 __global__ void __launch_bounds__(kZbThreads, 1) k_zbatch(Q q, const __grid_constant__ ZBatchArgs a,
@@ -655,8 +655,12 @@ void run_ptable(QSpec qs, const PTableArgs& a, const Prog& p, int lanes, cudaStr
   const QGrid Q{ldexp(1.0, qs.bits), ldexp(1.0, -qs.bits)};
   const size_t smem = static_cast<size_t>(p.ntab) * sizeof(double);
   auto go = [&](auto kern, int P) {
-    const int maxt = P == 1 ? prog_max_threads<1>() : (P == 2 ? prog_max_threads<2>() : prog_max_threads<4>());
-    const Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), maxt);
+    Geo geo = prog_geometry(p.S, P, Runtime::get().sm_count(), kZbThreads);
+    {  // a block's program items are its slots of every column
+      const size_t spb = (p.S + geo.blocks - 1) / geo.blocks;
+      const size_t want = ((spb * static_cast<size_t>(a.ncols) * P + 31) / 32) * 32;
+      geo.threads = static_cast<unsigned>(std::min<size_t>(want, static_cast<size_t>(kZbThreads)));
+    }
     const int cap = max_blocks(kern, smem, static_cast<int>(geo.threads));
     if (cap < static_cast<int>(geo.blocks)) fail(HS_E_CUDA, "pearson table kernel: grid not co-resident");
     QGrid qv = Q;
