@@ -753,6 +753,33 @@ def main():
     e2e_wall_ms = 1e3 * (time.perf_counter() - t0)
     e2e_ms = f0.elapsed_time(f1)
     e2e_ok = bool(np.array_equal(bits(hzn), bits(ref.out)))
+    # one ciphertext per step over the asynchronous calls (encode k+1 | znorm k | decode k, waits for k's
+    # verdict and k-2's slots); four pinned buffer pairs rotate
+    hxs = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for _ in range(4)]
+    hzs = [torch.zeros(S, dtype=torch.float64).pin_memory().numpy() for _ in range(4)]
+
+    def single_async(steps):
+        col_, pe_ = H.encode_column_async(ctx, hxs[0])
+        dq_ = []
+        for k_ in range(steps):
+            zc_ = H.znorm(ctx, col_, B)
+            pk_ = pe_
+            if k_ + 1 < steps:
+                col_, pe_ = H.encode_column_async(ctx, hxs[(k_ + 1) % 4])
+            dq_.append(H.decode_column_async(ctx, zc_, hzs[k_ % 4]))
+            pk_.wait()
+            while len(dq_) > 2:
+                dq_.pop(0).wait()
+        while dq_:
+            dq_.pop(0).wait()
+
+    single_async(50)
+    barrier_sync()
+    t0 = time.perf_counter()
+    single_async(e2e_steps)
+    barrier_sync()
+    sa_wall_ms = 1e3 * (time.perf_counter() - t0)
+    sa_ok = all(bool(np.array_equal(bits(b_), bits(ref.out))) for b_ in hzs)
     # the same pipelined loop from pageable (ordinary numpy) host buffers: the library stages them
     px = np.array(x)
     pz = np.empty(S)
@@ -1030,6 +1057,9 @@ def main():
                     "mode": "pipelined: encode of step k+1 overlaps znorm of step k (public API calls only)",
                     "latency_ms_per_step": seq_ms / e2e_steps, "latency_wall_ms_per_step": seq_wall_ms / e2e_steps,
                     "output_matches_oracle": e2e_ok, "host_buffers": "pinned (torch pin_memory)",
+                    "async_pipeline": {"value": sa_wall_ms / e2e_steps, "output_matches_oracle": sa_ok,
+                                       "mode": "encode_column_async k+1 | znorm k | decode_column_async k, waits "
+                                               "for k's verdict and k-2's slots (wall clock)"},
                     "pageable": {"value": pg_ms / e2e_steps, "wall_ms_per_step": pg_wall_ms / e2e_steps,
                                  "host_buffers": "pageable numpy arrays (staged by the library)",
                                  "output_matches_oracle": pg_ok}},
