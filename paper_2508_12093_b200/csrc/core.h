@@ -169,6 +169,9 @@ struct CtData {
   void read(double* out, size_t count) const;   // synchronous D2H into the caller's buffer
   void read_async(double* out, size_t count, size_t) const;  // enqueue only
   const std::vector<double>& host_slots() const;
+
+ private:
+  void settle_locked() const;  // caller holds mu
 };
 using Ct = std::shared_ptr<const CtData>;
 

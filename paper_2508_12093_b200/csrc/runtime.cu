@@ -207,12 +207,22 @@ double* Runtime::scratch(int slot, size_t n, bool zero) {
 }
 
 // ---- ciphertext storage -----------------------------------------------------------
+// An asynchronous encode_column may still be writing `dev` on an upload stream: order the compute
+// stream behind it.  While the compute stream is being captured into a graph an outside event
+// cannot become a dependency of the capture, so the host waits for the upload instead.
+void CtData::settle_locked() const {
+  if (!filling) return;
+  Runtime& rt = Runtime::get();
+  if (rt.capturing())
+    cuda_ok(cudaEventSynchronize(filling->e), "cudaEventSynchronize (upload)");
+  else
+    rt.compute_waits(filling);
+  filling.reset();
+}
+
 const double* CtData::device() const {
   std::lock_guard<std::mutex> g(mu);
-  if (filling) {  // asynchronous encode_column still in flight: order the compute stream behind it
-    Runtime::get().compute_waits(filling);
-    filling.reset();
-  }
+  settle_locked();
   if (!dev) {
     Runtime& rt = Runtime::get();
     DevBuf d = rt.alloc(n);
@@ -227,10 +237,7 @@ const double* CtData::device() const {
 
 const std::vector<double>& CtData::host_slots() const {
   std::lock_guard<std::mutex> g(mu);
-  if (filling) {
-    Runtime::get().compute_waits(filling);
-    filling.reset();
-  }
+  settle_locked();
   if (!host_ok) {
     host.resize(n);
     if (n) {
@@ -260,10 +267,7 @@ void CtData::read_async(double* out, size_t count, size_t) const {
       std::memcpy(out, host.data(), count * sizeof(double));
       return;
     }
-    if (filling) {
-      Runtime::get().compute_waits(filling);
-      filling.reset();
-    }
+    settle_locked();
   }
   Runtime& rt = Runtime::get();
   // copy-engine DMA straight into the caller's buffer (measured faster than SM stores

@@ -106,3 +106,20 @@ def test_rns_context_async_calls_complete_synchronously():
     out = np.empty(300)
     H.decode_column_async(ctx, col, out).wait()
     assert np.allclose(out, x, rtol=0, atol=1e-6)
+
+
+def test_pending_column_used_inside_graph_capture():
+    """A column whose upload is still in flight can be the input of captured work: the library
+    settles the upload on the host instead of making an outside event a capture dependency."""
+    from paper_2508_12093_b200 import hestat as H
+    S = 4096
+    ctx = H.EvalContext(H.CkksParams(slot_count=S))
+    x = _x(S, seed=31)
+    col, pend = H.encode_column_async(ctx, x)
+    with H.Graph() as g:
+        z = H.znorm(ctx, col, 100.0)
+    pend.wait()
+    g.launch()
+    H.sync()
+    ref = oracle().stat(Params(slot_count=S), ST_ZNORM, x, 100.0)
+    assert np.array_equal(bits(H.decode_column(ctx, z)), bits(ref.out))
