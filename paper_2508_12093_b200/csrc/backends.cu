@@ -17,10 +17,10 @@ namespace {
 // Where the device can read the caller's buffer directly (pinned, host-mapped
 // under UVA) the encrypt kernel reads it zero-copy; otherwise stage it through
 // a device buffer.  Returns the device-visible source pointer.
-// Large pinned inputs (>= kDmaBytes) go through the copy engine into a staging buffer
-// instead: the DMA runs at PCIe rate beside a statistics kernel that fills every SM (a
-// zero-copy k_encrypt would queue behind it, and reads host memory at less than half that
-// rate), and the encrypt kernel then reads HBM.
+// Large pinned inputs (>= kDmaBytes) go through the copy engine instead (encrypt_column's own
+// branch, or the staged copy below for a single ciphertext): the DMA runs at PCIe rate beside a
+// statistics kernel that fills every SM (a zero-copy k_encrypt would queue behind it, and reads
+// host memory at less than half that rate), and the encrypt kernel then reads HBM.
 constexpr size_t kDmaBytes = size_t(2) << 20;
 const double* device_source(const double* v, size_t n, DevBuf* stage, bool* pinned, cudaStream_t s) {
   Runtime& rt = Runtime::get();

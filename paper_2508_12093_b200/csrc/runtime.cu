@@ -64,7 +64,7 @@ Runtime::Runtime(int device) {
     const int l = std::atoi(e);
     if (l == 1 || l == 2 || l == 4 || l == 8) prog_lanes = l;
   }
-  if (const char* e = std::getenv("HESTAT_BATCH_LANES")) {  // batched Z-score: 4 measured 3 % over 2
+  if (const char* e = std::getenv("HESTAT_BATCH_LANES")) {  // batched kernels: default by batch size (core.h)
     const int l = std::atoi(e);
     if (l == 1 || l == 2 || l == 4) batch_lanes = l;
   }
