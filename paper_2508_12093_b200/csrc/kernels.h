@@ -104,6 +104,8 @@ struct Prog {
 
 // Launch one per-slot program over S slots.  lanes = 1, 2, 4 or 8 threads per slot.
 void run_prog(QSpec q, const Prog& p, int lanes, cudaStream_t s);
+// copies a degree-511 coefficient table (512 doubles, device) into stat.cu's constant-bank copy
+void upload_const_table(const double* dev_table, cudaStream_t s);
 
 // moment modes of the statistics kernel (stats.hpp:97-126): mean_scaled terms,
 // variance_to_scale terms (squares + mean part), or both

@@ -74,6 +74,13 @@ bool col_ok(const hs_ctx* ctx, const ColC& col) {
 }
 
 bool degree_ok(int d) { return d <= k::kMaxFusedDegree; }
+bool const_tree_on() {  // HS_CONST_TREE=0: the shared-memory table walk for every series
+  static const bool on = [] {
+    const char* e = std::getenv("HS_CONST_TREE");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 bool cfg_ok(const InvCfg& c) {
   return c.baseline_mode ? true : degree_ok(c.cheb_degree);
 }
@@ -374,6 +381,15 @@ class PB {
     if (p_.debug) {  // checked fusion: arm the flag word (read back by checks_failed())
       prog_.flags = debug_flag_word();
       cuda_ok(cudaMemsetAsync(prog_.flags, 0, sizeof(unsigned), rt.stream()), "debug flags");
+    }
+    if (zbatch_ && lanes == 1 && const_tree_on()) {
+      // a fast-path degree-511 series of a one-lane batch: its table also goes to the constant bank
+      for (auto& [ins, s] : chebs_)
+        if (s.degree() == 511 && prog_.ins[ins].c != 0.0 && prog_.ins[ins].b == 0) {
+          k::upload_const_table(prog_.tabs + prog_.ins[ins].i0, rt.stream());
+          prog_.ins[ins].i2 = 1;
+          break;  // one table in the bank
+        }
     }
     if (zbatch_) k::run_zbatch(q_, *zbatch_, prog_, lanes, rt.stream());
     else if (table_) k::run_ptable(q_, *table_, prog_, lanes, rt.stream());

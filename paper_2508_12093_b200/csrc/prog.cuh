@@ -118,6 +118,39 @@ __device__ __forceinline__ double tpow(int k, const double (&T)[kMaxK]) {
   }
 }
 
+// ---- degree-511 tree with its table in the constant bank (batched Z-score, one lane per slot) ----
+// The coefficients are operands of the FP64 instructions themselves (c[bank][immediate]): no
+// coefficient loads, no table addressing and no block loop, at the price of a fully unrolled tree.
+// Each translation unit that includes this header has its own copy of the table; only stat.cu's is
+// ever filled (upload_const_table) and read (k_zbatch with CT = true).
+__constant__ double c_cheb511[512];
+
+template <int K, int OFF, int J, class F>
+__device__ __forceinline__ double ffull_c(const F& f, const double (&T)[kMaxK]) {
+  if constexpr (K <= 1) {
+    constexpr bool mx = (kLeafMulX >> (J & 7)) & 1u, ax = (kLeafAddX >> (J & 7)) & 1u;
+    const double m = mx ? f.mulc_x(T[0], c_cheb511[OFF]) : f.mulc(T[0], c_cheb511[OFF]);
+    return ax ? f.addc_x(m, c_cheb511[OFF + 1]) : f.addc(m, c_cheb511[OFF + 1]);
+  } else {
+    constexpr int H = 1 << (K - 1);
+    const double head = f.mul(ffull_c<K - 1, OFF, 2 * J>(f, T), T[K - 1]);
+    const double rest = ffull_c<K - 1, OFF + H, 2 * J + 1>(f, T);
+    return f.add(head, rest);
+  }
+}
+
+// the d = 511 instance of cheb_eval's peel-the-top-bit loop: leaf (c[0], c[1]), then F_k at c[2^k]
+template <int KK, class F>
+__device__ __forceinline__ double cheb511_c(const F& f, double v, const double (&T)[kMaxK]) {
+  if constexpr (KK > 8) {
+    return v;
+  } else {
+    const double head = f.mul(v, T[KK]);
+    const double rest = ffull_c<KK, (1 << KK), 0>(f, T);
+    return cheb511_c<KK + 1>(f, f.add(head, rest), T);
+  }
+}
+
 // Exact iterative evaluation of F_k (post-order with an explicit stack):
 // compact code for slots outside the fast path's range.
 template <class Q>
@@ -188,9 +221,9 @@ __device__ __noinline__ double cheb_exact(Q q, const double* t, int d, double x,
 }
 
 // ChebEncryptedEval::run (chebyshev.hpp:117-125) for degree d <= 1023; t in smem.
-template <class Q, int P>
+template <class Q, int P, bool CT = false>
 __device__ __forceinline__ double cheb_eval(const Q& q, const double* t, int d, double x, int lane, bool split,
-                                            bool fast_ok) {
+                                            bool fast_ok, bool in_const = false) {
   if (d <= 0) return q.addc(q.sub(x, x), t[0]);        // add_pt(sub_ct(x, x), c0)
   if (d == 1) return q.addc(q.mulc(x, t[0]), t[1]);     // a single leaf
   if (!(fast_ok && FastOf<Q>::in_range(q, x))) return cheb_exact<Q>(q, t, d, x, P, split ? 1 : 0);
@@ -223,6 +256,13 @@ __device__ __forceinline__ double cheb_eval(const Q& q, const double* t, int d, 
     }
     // a zero result may carry the wrong zero sign (quant.cuh magic_round_nz): redo exactly
     return v == 0.0 ? cheb_exact<Q>(q, t, d, x, P, 1) : v;
+  }
+  if constexpr (CT && P == 1) {
+    if (in_const && d == 511) {  // uniform: the table of this series is also in the constant bank
+      const double v0 = ff.addc(ff.mulc(x, c_cheb511[0]), c_cheb511[1]);
+      const double v = cheb511_c<1>(ff, v0, T);
+      return v == 0.0 ? cheb_exact<Q>(q, t, d, x, P, 0) : v;
+    }
   }
   // general degree: peel the top bit repeatedly (p = q*T_g + r, r full)
   int gk[kMaxK];
@@ -334,7 +374,7 @@ __device__ __forceinline__ Range block_range(unsigned S) {
 
 // ---- one slot's program ------------------------------------------------------------
 // r: the slot's register file; sv: per-slot statistic values (M_LDR), if any.
-template <class Q, int P>
+template <class Q, int P, bool CT = false>
 __device__ __forceinline__ void exec(const Q& q, const Prog& pg, const double* stab, unsigned s, int lane,
                                      bool live, const double* sv) {
   double r[kRegs];
@@ -353,7 +393,9 @@ __device__ __forceinline__ void exec(const Q& q, const Prog& pg, const double* s
       case M_MUL: r[I.dst] = q.mul(r[I.a], r[I.b]); break;
       case M_ADDC: r[I.dst] = q.addc(r[I.a], I.c); break;
       case M_MULC: r[I.dst] = q.mulc(r[I.a], I.c); break;
-      case M_CHEB: r[I.dst] = cheb_eval<Q, P>(q, stab + I.i0, I.i1, r[I.a], lane, I.b != 0, I.c != 0.0); break;
+      case M_CHEB:
+        r[I.dst] = cheb_eval<Q, P, CT>(q, stab + I.i0, I.i1, r[I.a], lane, I.b != 0, I.c != 0.0, I.i2 != 0);
+        break;
       case M_NEWTON:
         r[I.dst] = newton<Q>(q, r[I.a], r[I.b], I.i0, I.i1, I.c,
                              pg.flags && live && lane == 0 && s < static_cast<unsigned>(I.i2) ? pg.flags : nullptr);

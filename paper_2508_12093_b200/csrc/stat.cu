@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kZbThreads, 1) k_zbatch(Q q, const __grid_cons
     const unsigned it2 = live ? item : items - 1;
     const unsigned c = it2 / w, s = BR.lo + it2 % w;
     double sv[5] = {mu(static_cast<int>(c), s), var(static_cast<int>(c), s), 0.0, 0.0, 0.0};
-    exec<Q, P>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
+    exec<Q, P, P == 1>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
   }
   __syncthreads();
   stamp(3);
@@ -619,6 +619,13 @@ size_t stat_partial_doubles() { return 4 * kNK + 2; }
 size_t ptable_partial_doubles() { return 2 * (kTA + kTB) + 2; }
 
 size_t zbatch_partial_doubles() { return 2 * kZA + 2; }
+
+// The degree-511 table of the next k_zbatch launch into the constant bank (prog.cuh c_cheb511),
+// stream-ordered (and captured as a copy node inside a graph capture).
+void upload_const_table(const double* dev_table, cudaStream_t s) {
+  cuda_ok(cudaMemcpyToSymbolAsync(c_cheb511, dev_table, 512 * sizeof(double), 0, cudaMemcpyDeviceToDevice, s),
+          "constant table upload");
+}
 
 void run_zbatch(QSpec qs, const ZBatchArgs& a, const Prog& p, int lanes, cudaStream_t s) {
   if (p.S == 0 || a.ncols == 0) return;
