@@ -382,7 +382,7 @@ class PB {
       prog_.flags = debug_flag_word();
       cuda_ok(cudaMemsetAsync(prog_.flags, 0, sizeof(unsigned), rt.stream()), "debug flags");
     }
-    if (zbatch_ && lanes == 1 && const_tree_on()) {
+    if ((zbatch_ || table_) && lanes == 1 && const_tree_on()) {
       // a fast-path degree-511 series of a one-lane batch: its table also goes to the constant bank
       for (auto& [ins, s] : chebs_)
         if (s.degree() == 511 && prog_.ins[ins].c != 0.0 && prog_.ins[ins].b == 0) {

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kZbThreads, 1) k_ptable(Q q, const __grid_cons
     const unsigned it2 = live ? item : items - 1;
     const unsigned c = it2 / (BR.hi - BR.lo), s = BR.lo + it2 % (BR.hi - BR.lo);
     double sv[5] = {mu(static_cast<int>(c)), var(static_cast<int>(c)), 0.0, 0.0, 0.0};
-    exec<Q, P>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
+    exec<Q, P, P == 1>(q, pg, stab, c * S + s, static_cast<int>(g % P), live, sv);
   }
   __syncthreads();  // the block's inverse roots (global, this block's slots) are visible to it
   // ---- phase D: pearson's epilogue per pair, mul_ct(mul_ct(cov, inv_x), inv_y) ----
