@@ -455,7 +455,7 @@ def zbatch_lanes():
 
 def zbatch_traffic(kb):
     """DRAM bytes per k_zbatch launch of kb ciphertexts from the committed ncu --set full summary."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_mix_ncu.json")
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_zbatch_ct_ncu.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -1073,7 +1073,7 @@ def main():
                          "work": f"{step_per_slot} fp64 ops/slot x {S} slots x {KB} ciphertexts",
                          "peak_source": "measured DMUL rate on this GPU (hs_diag_fp64_rate); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "traffic_source": "profiles/r2_zbatch_mix_ncu.json (ncu --set full, one k_zbatch launch of "
+                         "traffic_source": "profiles/r2_zbatch_ct_ncu.json (ncu --set full, one k_zbatch launch of "
                                            "64 ciphertexts, dram read+write; algorithmic: 16 B per slot and "
                                            "ciphertext, 32 MiB per launch)",
                          "program_kernel": {"kernel": "k_prog<QGrid,2> (crypto_invsqrt alone)",
