@@ -100,8 +100,9 @@ class Runtime {
   uint64_t launches() const { return launches_.load(); }
   bool fused = true;
   int prog_lanes = 2;  // threads per slot of the fused program kernel (HESTAT_LANES: 1, 2, 4, 8)
-  // the same for the batched Z-score kernel (HESTAT_BATCH_LANES: 1, 2, 4); 0 = by batch size: one
-  // thread per slot once a block has two full rounds of items (no work is repeated across lanes)
+  // the same for the batched kernels (HESTAT_BATCH_LANES: 1, 2, 4); 0 = by batch size: one thread
+  // per slot once a block has a full round of items (no work repeated across lanes, and the
+  // degree-511 tree then runs from the constant bank)
   int batch_lanes = 0;
 
   // Persistent device scratch buffer `slot` of at least n doubles (grown on

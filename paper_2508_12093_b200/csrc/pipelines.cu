@@ -343,7 +343,7 @@ class PB {
     if (big_cheb_ && (zbatch_ || table_) && lanes == 0) {
       const size_t ncols = zbatch_ ? zbatch_->ncols : table_->ncols;
       const size_t items = (p_.S + rt.sm_count() - 1) / rt.sm_count() * ncols;
-      lanes = items >= 2048 ? 1 : (items >= 1024 ? 2 : 4);
+      lanes = items >= 1024 ? 1 : (items >= 512 ? 2 : 4);  // one lane as soon as a block has one full round
     }
     int p = 0;
     while ((1 << p) < lanes) ++p;
