@@ -60,6 +60,9 @@ UNIT = "ms/ciphertext"
 S = 32768
 B = 100.0
 SEED = 21
+# the same wording in both arms' config (the driver compares the dictionaries)
+STEP_TEXT = ("independent C2 Z-scores (each its own moments, inverse square root and normalisation); "
+             "value per ciphertext")
 POOL = 640  # 640 x 256 KiB = 160 MiB of distinct inputs > 126 MB L2
 
 
@@ -182,9 +185,9 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
             "config": workload_config({"parallelism": f"replicas x{max(args.gpus, 1)} (no data-path collective)",
                                        "ciphertexts_per_step": max(1, min(args.batch_cols, 64)),
-                                       "step": "independent C2 Z-scores, each its own EvalContext on a host thread "
-                                               "(the reference's sanctioned concurrency, SPEC.md:141); value per "
-                                               "ciphertext"}),
+                                       "step": STEP_TEXT}),
+            "step_detail": "each Z-score its own EvalContext on a host thread (the reference's sanctioned "
+                           "concurrency, SPEC.md:141)",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                              "sample": f"per step: {threads} independent C2 znorm runs on {threads} threads"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -1030,9 +1033,8 @@ def main():
             "data": "synthetic: seeded N(50,10^2) via mt19937_64 + Box-Muller (paper datasets absent)",
             "config": workload_config({"parallelism": f"replicas x{ws} (no data-path collective)",
                                        "ciphertexts_per_step": KB,
-                                       "step": f"{KB} independent C2 Z-scores (each its own moments, inverse "
-                                               f"square root and normalisation) through hs_znorm_batch: one "
-                                               f"launch per step, graph-replayed"}),
+                                       "step": STEP_TEXT}),
+            "step_detail": f"{KB} Z-scores through hs_znorm_batch: one k_zbatch launch per step, graph-replayed",
             "parity_vs_oracle": parity and bparity,
             "e2e": {"value": be2e_ms / (be2e_steps * KB * ws), "unit": UNIT, "h2d_bytes_per_step": KB * S * 8,
                     "d2h_bytes_per_step": KB * S * 8, "wall_ms_per_ciphertext": be2e_wall_ms / (be2e_steps * KB),
