@@ -310,6 +310,10 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
     }
     const uint32_t blk0 = g >> logs;
     const uint32_t j0 = (blk0 << (logs + RB)) | (g & ((1u << logs) - 1));
+    // swz is linear over XOR and j0 has zeros in bits logs .. logs + RB - 1, so the swizzled index of
+    // element k is swz(base) ^ swz(k << logs): one swizzle per thread and step, one XOR with a
+    // compile-time constant per element
+    const uint32_t sb = ROWS ? swz((tr << logR) + j0) : 0u;
     const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
     uint64_t x[1 << RB];
 #pragma unroll
@@ -318,7 +322,7 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
       if (FIRST)
         x[k] = gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr);
       else
-        x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
+        x[k] = ROWS ? sm[sb ^ swz(uint32_t(k) << logs)] : sm[(e << logTPB) + tr];
     }
     if (!INV) {
 #pragma unroll
@@ -379,7 +383,7 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
         gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr, v);
       } else {
         if (ROWS)
-          sm[swz((tr << logR) + e)] = v;
+          sm[sb ^ swz(uint32_t(k) << logs)] = v;
         else
           sm[(e << logTPB) + tr] = v;
       }
@@ -509,6 +513,10 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
     }
     const uint32_t blk0 = g >> logs;
     const uint32_t j0 = (blk0 << (logs + RB)) | (g & ((1u << logs) - 1));
+    // swz is linear over XOR and j0 has zeros in bits logs .. logs + RB - 1, so the swizzled index of
+    // element k is swz(base) ^ swz(k << logs): one swizzle per thread and step, one XOR with a
+    // compile-time constant per element
+    const uint32_t sb = ROWS ? swz((tr << logR) + j0) : 0u;
     const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
     double x[1 << RB];
 #pragma unroll
@@ -518,7 +526,7 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
         const uint64_t g = gin(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr);
         x[k] = RAWM == 2 ? __longlong_as_double(static_cast<long long>(g)) : u2d(g);
       } else {
-        x[k] = ROWS ? sm[swz((tr << logR) + e)] : sm[(e << logTPB) + tr];
+        x[k] = ROWS ? sm[sb ^ swz(uint32_t(k) << logs)] : sm[(e << logTPB) + tr];
       }
     }
     if (!INV) {
@@ -578,7 +586,7 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
         gout(ROWS ? (size_t(tr) << logC) + e : (size_t(e) << logC) + tr, fp_canon(v, q, qinv));
       } else {
         if (ROWS)
-          sm[swz((tr << logR) + e)] = x[k];
+          sm[sb ^ swz(uint32_t(k) << logs)] = x[k];
         else
           sm[(e << logTPB) + tr] = x[k];
       }
