@@ -123,3 +123,52 @@ def test_pending_column_used_inside_graph_capture():
     H.sync()
     ref = oracle().stat(Params(slot_count=S), ST_ZNORM, x, 100.0)
     assert np.array_equal(bits(H.decode_column(ctx, z)), bits(ref.out))
+
+
+def test_edge_cases_empty_host_side_and_release_without_wait():
+    from paper_2508_12093_b200 import hestat as H
+    S = 1024
+    ctx = H.EvalContext(H.CkksParams(slot_count=S))
+    # empty column: nothing to upload, the pending is complete at once
+    col, pend = H.encode_column_async(ctx, np.empty(0))
+    pend.wait()
+    assert len(col.chunks) == 0 and col.n_valid == 0
+    H.decode_column_async(ctx, col, np.empty(0)).wait()
+    # a column of host-constructed ciphertexts (no device buffer yet): decoded by a host copy
+    v = _x(S, seed=41)
+    hc = H.EncryptedColumn([H.Ciphertext(v, 3)], S)
+    out = np.zeros(S)
+    H.decode_column_async(ctx, hc, out).wait()
+    assert np.array_equal(bits(out), bits(v))
+    # an out buffer that is too short is refused before anything is enqueued
+    with pytest.raises(H.length_mismatch):
+        H.decode_column_async(ctx, hc, np.zeros(S - 1))
+    # dropping a Pending without wait() settles it (the library waits inside hs_pending_release)
+    x = _x(5 * S, seed=42)
+    col, pend = H.encode_column_async(ctx, x)
+    del pend
+    assert np.array_equal(bits(H.decode_column(ctx, col)), bits(H.decode_column(ctx, H.encode_column(ctx, x))))
+    big = np.zeros(5 * S)
+    d = H.decode_column_async(ctx, col, big)
+    del d
+    H.sync()
+    assert np.array_equal(bits(big), bits(H.decode_column(ctx, col)))
+
+
+def test_too_many_chunks_and_mixed_readiness_decode():
+    """A column mixing a statistic's outputs (completion event), an upload still in flight and a
+    plain op result decodes to the same slots as chunk-by-chunk reads."""
+    from paper_2508_12093_b200 import hestat as H
+    S = 2048
+    ctx = H.EvalContext(H.CkksParams(slot_count=S))
+    a = H.encode_column(ctx, _x(S, seed=51))
+    z = H.znorm(ctx, a, 100.0).chunks[0]                       # fused statistic output
+    up, pend = H.encode_column_async(ctx, _x(S, seed=52))      # upload in flight
+    plain = ctx.add_pt(a.chunks[0], 1.5)                       # op-by-op result
+    mixed = H.EncryptedColumn([z, up.chunks[0], plain], 3 * S)
+    out = np.zeros(3 * S)
+    d = H.decode_column_async(ctx, mixed, out)
+    pend.wait()
+    d.wait()
+    for k, c in enumerate((z, up.chunks[0], plain)):
+        assert np.array_equal(bits(out[k * S:(k + 1) * S]), bits(c.slots()))
