@@ -493,7 +493,7 @@ template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST
 __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
                                             double* __restrict__ sm, const double* __restrict__ tw, double q,
                                             double qinv, uint32_t tile0, double ninv,
-                                            const double* __restrict__ tws) {
+                                            const double* __restrict__ tws, const double* wpre = nullptr) {
   using G = NttGeom<LOGN, ROWS>;
   constexpr uint32_t logR = G::logR, logTPB = G::logTPB, logC = G::logC;
   constexpr uint32_t logG = logR - RB;
@@ -534,7 +534,12 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << (RB - 1 - st);
         double wv[8];  // the stage's 2^st twiddles are consecutive: 16-byte loads
-        if (!(ROWS && tws)) ldg_tw(wv, tw + ((1u << (DONE + st)) * S) + (blk0 << st), 1 << st);
+        if (wpre && it == 0) {  // loaded before the barrier that precedes this step (ntt_tw_fp)
+#pragma unroll
+          for (int b = 0; b < (1 << st); ++b) wv[b] = wpre[(1 << st) - 1 + b];
+        } else if (!(ROWS && tws)) {
+          ldg_tw(wv, tw + ((1u << (DONE + st)) * S) + (blk0 << st), 1 << st);
+        }
 #pragma unroll
         for (int b = 0; b < (1 << st); ++b) {
           const double w = ROWS && tws ? tws[RowTw<LOGN>::off(DONE + st) + (tr << (DONE + st)) + (blk0 << st) + b]
@@ -555,7 +560,12 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
       for (int st = 0; st < RB; ++st) {
         const int d = 1 << st;
         double wv[8];
-        if (!(ROWS && tws)) ldg_tw(wv, tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)), 1 << (RB - 1 - st));
+        if (wpre && it == 0) {
+#pragma unroll
+          for (int b = 0; b < (1 << (RB - 1 - st)); ++b) wv[b] = wpre[(1 << RB) - (2 << (RB - 1 - st)) + b];
+        } else if (!(ROWS && tws)) {
+          ldg_tw(wv, tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)), 1 << (RB - 1 - st));
+        }
 #pragma unroll
         for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
           const double w = ROWS && tws
@@ -594,6 +604,41 @@ __device__ __forceinline__ void ntt_step_fp(const LD& gin, const ST& gout,
   }
 }
 
+// The twiddles of one radix step for this thread's first group (it = 0), issued before the barrier
+// that precedes the step: their L1/L2 latency overlaps the barrier wait and the shared-memory reads
+// instead of following them (a row pass's twiddles are distinct per row: L1 misses).  Forward: stage
+// st's 2^st values at wpre[2^st - 1 ..]; inverse: stage st's 2^(RB-1-st) values after the earlier stages'.
+// HS_NTT_PRETW: bit 0 forward rows, bit 1 forward columns, bit 2 inverse rows, bit 3 inverse columns.
+#ifndef HS_NTT_PRETW
+#define HS_NTT_PRETW 3
+#endif
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE>
+__device__ __forceinline__ void ntt_tw_fp(double (&wpre)[8], const double* __restrict__ tw, uint32_t tile0) {
+  using G = NttGeom<LOGN, ROWS>;
+  constexpr uint32_t logR = G::logR, logTPB = G::logTPB;
+  constexpr uint32_t logG = logR - RB;
+  constexpr uint32_t logs = INV ? DONE : logR - 1 - DONE - (RB - 1);
+  const uint32_t idx = threadIdx.x;
+  const uint32_t g = ROWS ? idx & ((1u << logG) - 1) : idx >> logTPB;
+  const uint32_t tr = ROWS ? idx >> logG : idx & ((1u << logTPB) - 1);
+  const uint32_t blk0 = g >> logs;
+  const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
+#pragma unroll
+  for (int st = 0; st < RB; ++st) {
+    double wv[8];
+    if (!INV) {
+      ldg_tw(wv, tw + ((1u << (DONE + st)) * S) + (blk0 << st), 1 << st);
+#pragma unroll
+      for (int b = 0; b < (1 << st); ++b) wpre[(1 << st) - 1 + b] = wv[b];
+    } else {
+      constexpr uint32_t logh0 = logR - 1 - DONE;
+      ldg_tw(wv, tw + ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st)), 1 << (RB - 1 - st));
+#pragma unroll
+      for (int b = 0; b < (1 << (RB - 1 - st)); ++b) wpre[(1 << RB) - (2 << (RB - 1 - st)) + b] = wv[b];
+    }
+  }
+}
+
 template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf, int RAWM = 0>
 __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, double* sm, const double* tw,
                                              double q, double qinv, uint32_t tile0, double ninv,
@@ -602,10 +647,15 @@ __device__ __forceinline__ void ntt_steps_fp(const LD& gin, const ST& gout, doub
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = pick_rb(rem);
+    constexpr bool pre = ((HS_NTT_PRETW >> ((INV ? 2 : 0) + (ROWS ? 0 : 1))) & 1) != 0 && DONE > 0 && RB <= 3;
+    double wpre[8];
+    if constexpr (pre) {
+      if (!(ROWS && tws)) ntt_tw_fp<INV, ROWS, LOGN, RB, DONE>(wpre, tw, tile0);
+    }
     if constexpr (DONE > 0) __syncthreads();
     if constexpr (DONE > 0 && DONE == pick_rb(logR)) pf();
-    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST, RAWM>(gin, gout, sm, tw, q, qinv,
-                                                                                       tile0, ninv, tws);
+    ntt_step_fp<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST, RAWM>(
+        gin, gout, sm, tw, q, qinv, tile0, ninv, tws, pre && !(ROWS && tws) ? wpre : nullptr);
     ntt_steps_fp<INV, ROWS, LOGN, DONE + RB, LD, ST, PF, RAWM>(gin, gout, sm, tw, q, qinv, tile0, ninv, tws, pf);
   } else if constexpr (DONE == pick_rb(logR) && !std::is_same_v<PF, NoPf>) {
     __syncthreads();
