@@ -289,7 +289,8 @@ template <bool INV, bool ROWS, int LOGN, int RB, int DONE, bool FIRST, bool LAST
 __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
                                          uint64_t* __restrict__ sm, const uint64_t* __restrict__ psi,
                                          const uint64_t* __restrict__ psip, uint64_t q, uint32_t tile0,
-                                         uint64_t ninv, uint64_t ninv_sh) {
+                                         uint64_t ninv, uint64_t ninv_sh, const uint64_t* wpre = nullptr,
+                                         const uint64_t* wppre = nullptr) {
   using G = NttGeom<LOGN, ROWS>;
   constexpr uint32_t logR = G::logR, logTPB = G::logTPB, logC = G::logC;
   constexpr uint32_t logG = logR - RB;  // groups per transform (log)
@@ -330,8 +331,16 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
         const int d = 1 << (RB - 1 - st);
         uint64_t wv[8], wpv[8];  // the stage's 2^st consecutive twiddles: 16-byte loads
         const uint32_t wi0 = ((1u << (DONE + st)) * S) + (blk0 << st);
-        ldg_tw(wv, psi + wi0, 1 << st);
-        ldg_tw(wpv, psip + wi0, 1 << st);
+        if (wpre && it == 0) {  // loaded before the barrier that precedes this step (ntt_tw_u64)
+#pragma unroll
+          for (int b = 0; b < (1 << st); ++b) {
+            wv[b] = wpre[(1 << st) - 1 + b];
+            wpv[b] = wppre[(1 << st) - 1 + b];
+          }
+        } else {
+          ldg_tw(wv, psi + wi0, 1 << st);
+          ldg_tw(wpv, psip + wi0, 1 << st);
+        }
 #pragma unroll
         for (int b = 0; b < (1 << st); ++b) {
           const uint64_t w = wv[b], wp = wpv[b];
@@ -353,8 +362,16 @@ __device__ __forceinline__ void ntt_step(const LD& gin, const ST& gout,
         constexpr uint32_t logh0 = logR - 1 - DONE;
         uint64_t wv[8], wpv[8];
         const uint32_t wi0 = ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st));
-        ldg_tw(wv, psi + wi0, 1 << (RB - 1 - st));
-        ldg_tw(wpv, psip + wi0, 1 << (RB - 1 - st));
+        if (wpre && it == 0) {
+#pragma unroll
+          for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
+            wv[b] = wpre[(1 << RB) - (2 << (RB - 1 - st)) + b];
+            wpv[b] = wppre[(1 << RB) - (2 << (RB - 1 - st)) + b];
+          }
+        } else {
+          ldg_tw(wv, psi + wi0, 1 << (RB - 1 - st));
+          ldg_tw(wpv, psip + wi0, 1 << (RB - 1 - st));
+        }
 #pragma unroll
         for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
           const uint64_t w = wv[b], wp = wpv[b];
@@ -404,6 +421,50 @@ struct NoPf {
   __device__ void operator()() const {}
 };
 
+// The twiddles (and Shoup companions) of one radix step for this thread's first group, issued before
+// the barrier that precedes the step (see ntt_tw_fp; same layout).  HS_NTT_PRETW64: the same bit mask as
+// HS_NTT_PRETW for the 64-bit path.
+#ifndef HS_NTT_PRETW64
+#define HS_NTT_PRETW64 3
+#endif
+template <bool INV, bool ROWS, int LOGN, int RB, int DONE>
+__device__ __forceinline__ void ntt_tw_u64(uint64_t (&wpre)[8], uint64_t (&wppre)[8], const uint64_t* __restrict__ psi,
+                                           const uint64_t* __restrict__ psip, uint32_t tile0) {
+  using G = NttGeom<LOGN, ROWS>;
+  constexpr uint32_t logR = G::logR, logTPB = G::logTPB;
+  constexpr uint32_t logG = logR - RB;
+  constexpr uint32_t logs = INV ? DONE : logR - 1 - DONE - (RB - 1);
+  const uint32_t idx = threadIdx.x;
+  const uint32_t g = ROWS ? idx & ((1u << logG) - 1) : idx >> logTPB;
+  const uint32_t tr = ROWS ? idx >> logG : idx & ((1u << logTPB) - 1);
+  const uint32_t blk0 = g >> logs;
+  const uint32_t S = ROWS ? G::R1 + tile0 + tr : 1u;
+#pragma unroll
+  for (int st = 0; st < RB; ++st) {
+    uint64_t wv[8], wpv[8];
+    if (!INV) {
+      const uint32_t wi0 = ((1u << (DONE + st)) * S) + (blk0 << st);
+      ldg_tw(wv, psi + wi0, 1 << st);
+      ldg_tw(wpv, psip + wi0, 1 << st);
+#pragma unroll
+      for (int b = 0; b < (1 << st); ++b) {
+        wpre[(1 << st) - 1 + b] = wv[b];
+        wppre[(1 << st) - 1 + b] = wpv[b];
+      }
+    } else {
+      constexpr uint32_t logh0 = logR - 1 - DONE;
+      const uint32_t wi0 = ((1u << (logh0 - st)) * S) + (blk0 << (RB - 1 - st));
+      ldg_tw(wv, psi + wi0, 1 << (RB - 1 - st));
+      ldg_tw(wpv, psip + wi0, 1 << (RB - 1 - st));
+#pragma unroll
+      for (int b = 0; b < (1 << (RB - 1 - st)); ++b) {
+        wpre[(1 << RB) - (2 << (RB - 1 - st)) + b] = wv[b];
+        wppre[(1 << RB) - (2 << (RB - 1 - st)) + b] = wpv[b];
+      }
+    }
+  }
+}
+
 template <bool INV, bool ROWS, int LOGN, int DONE, class LD, class ST, class PF = NoPf>
 __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_t* sm, const uint64_t* psi,
                                           const uint64_t* psip, uint64_t q, uint32_t tile0, uint64_t ninv,
@@ -412,10 +473,13 @@ __device__ __forceinline__ void ntt_steps(const LD& gin, const ST& gout, uint64_
   if constexpr (DONE < logR) {
     constexpr int rem = logR - DONE;
     constexpr int RB = pick_rb(rem);
+    constexpr bool pre = ((HS_NTT_PRETW64 >> ((INV ? 2 : 0) + (ROWS ? 0 : 1))) & 1) != 0 && DONE > 0 && RB <= 3;
+    uint64_t wpre[8], wppre[8];
+    if constexpr (pre) ntt_tw_u64<INV, ROWS, LOGN, RB, DONE>(wpre, wppre, psi, psip, tile0);
     if constexpr (DONE > 0) __syncthreads();
     if constexpr (DONE > 0 && DONE == pick_rb(logR)) pf();
-    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(gin, gout, sm, psi, psip, q, tile0,
-                                                                              ninv, ninv_sh);
+    ntt_step<INV, ROWS, LOGN, RB, DONE, DONE == 0, DONE + RB == logR, LD, ST>(
+        gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh, pre ? wpre : nullptr, pre ? wppre : nullptr);
     ntt_steps<INV, ROWS, LOGN, DONE + RB, LD, ST, PF>(gin, gout, sm, psi, psip, q, tile0, ninv, ninv_sh, pf);
   } else if constexpr (DONE == pick_rb(logR) && !std::is_same_v<PF, NoPf>) {  // single-step pass
     __syncthreads();
