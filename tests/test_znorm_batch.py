@@ -76,3 +76,27 @@ def test_proven_exact_batch_is_capturable_and_matches():
     H.sync()
     for e, z in zip(eager, zg):
         assert np.array_equal(bits(e), bits(H.decode_column(ctx, z)))
+
+
+def test_constant_bank_tree_in_graph_replay_and_between_tables():
+    """One lane per slot (>= 1024 items per block): the degree-511 table is copied into the constant
+    bank before each launch.  A captured batch carries its own copy node, so replaying it after an
+    eager batch with a different table (another B) still gives the eager bits; HS_CONST_TREE-free
+    semantics are checked against the per-column calls."""
+    from paper_2508_12093_b200 import hestat as H
+    S = 4096
+    xs = _cols(S, 40)
+    ctx = H.EvalContext(H.CkksParams(slot_count=S))
+    cols = [H.encode_column(ctx, x) for x in xs]
+    eager100 = [H.decode_column(ctx, z) for z in H.znorm_batch(ctx, cols, 100.0)]
+    with H.Graph() as g:
+        zg = H.znorm_batch(ctx, cols, 100.0)
+    other = [H.decode_column(ctx, z) for z in H.znorm_batch(ctx, cols, 60.0)]  # another table in the bank
+    g.launch()
+    H.sync()
+    for k in (0, 17, 39):
+        assert np.array_equal(bits(eager100[k]), bits(H.decode_column(ctx, zg[k])))
+        assert np.array_equal(bits(eager100[k]), bits(H.decode_column(ctx, H.znorm(ctx, cols[k], 100.0))))
+        assert np.array_equal(bits(other[k]), bits(H.decode_column(ctx, H.znorm(ctx, cols[k], 60.0))))
+    again = H.znorm_batch(ctx, cols, 60.0)  # eager after the replay: uploads its own table again
+    assert np.array_equal(bits(other[5]), bits(H.decode_column(ctx, again[5])))
