@@ -748,6 +748,7 @@ int hs_decode_column(const hs_ctx* c, const hs_column* col, double* out) {
 struct hs_pending {
   std::shared_ptr<ReadyEv> done;      // fires when the enqueued work has completed (null: nothing to wait for)
   std::unique_ptr<EncodePending> enc;  // encode: deferred finiteness verdict + staging buffer
+  std::vector<Ct> reading;             // decode: the chunks being copied stay alive until the copy has completed
   bool settled = false;
   int rc = HS_OK;
   std::string err;
@@ -796,11 +797,14 @@ int hs_decode_column_async(const hs_ctx* c, const hs_column* col, double* out, h
     const size_t S = ctxp(c)->p.S;
     if (col->n_valid > col->n_chunks * S) fail(HS_E_LENGTH_MISMATCH, "decode_column: n_valid exceeds packed capacity");
     if (col->n_valid) need(out, "out");
+    for (uint64_t i = 0; i < col->n_chunks; ++i) p->reading.push_back(get(col->chunks[i]));
     cudaStream_t st = decode_enqueue(S, col, out, col->n_valid, false);
-    if (st)
+    if (st) {
       p->done = Runtime::get().mark_on(st);
-    else
+    } else {
       p->settled = true;
+      p->reading.clear();
+    }
     *pending = p.release();
   });
 }
@@ -819,6 +823,7 @@ int hs_pending_wait(hs_pending* p) {
       }
     }
     p->rc = guard([&] {
+      p->reading.clear();  // buffer frees are stream-ordered: under the API lock
       if (p->enc) p->enc->finish();
     });
     if (p->rc != HS_OK) p->err = g_err;

@@ -68,6 +68,7 @@ void EncodePending::finish() {
   if (bad) give_flag(bad);
   bad = nullptr;
   stage.reset();
+  block.reset();
   if (nf) fail(HS_E_NON_FINITE_VALUE, "encode_column: non-finite value in column");
 }
 EncodePending::~EncodePending() {
@@ -139,6 +140,7 @@ std::vector<Ct> DevB::encrypt_column(const double* v, size_t n, EncodePending* p
     pend->done = rt.mark_on(s);
     pend->bad = bad;
     pend->stage = std::move(stage);
+    pend->block = block;
     for (const Ct& c : out) c->filling = pend->done;
     return out;
   }

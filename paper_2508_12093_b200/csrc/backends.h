@@ -125,6 +125,8 @@ struct EncodePending {
   std::shared_ptr<ReadyEv> done;
   int* bad = nullptr;
   DevBuf stage;
+  DevBuf block;  // the column's output allocation: kept until the upload has completed, whatever the
+                 // caller does with the chunk handles meanwhile (its free is compute-stream ordered)
   void finish();  // after `done` has fired: returns the flag, frees the stage; throws non_finite_value
   ~EncodePending();
 };

@@ -82,6 +82,25 @@ int main(int argc, char** argv) {
       return 1;
     }
   }
+  // handles dropped before their transfer has settled: the library keeps the buffers alive
+  {
+    Pending pe;
+    { const EncryptedColumn gone = encode_column_async(ctx, std::span<const double>(hx[0], 2 * S), pe); }
+    pe.wait();
+    const EncryptedColumn c = encode_column(ctx, std::span<const double>(hx[0], S));
+    std::vector<double> got(S, 0.0);
+    Pending pd;
+    {
+      const EncryptedColumn z = znorm(ctx, c, B);
+      pd = decode_column_async(ctx, z, got);
+    }
+    for (int i = 0; i < 4; ++i) (void)znorm(ctx, c, B);  // pool churn while the copy may be in flight
+    pd.wait();
+    if (!same_bits(got.data(), want[0].data(), S)) {
+      std::fprintf(stderr, "decode_column_async of a released column differs\n");
+      return 1;
+    }
+  }
   // the pipeline
   auto run = [&](int n) {
     Pending pe;
