@@ -200,8 +200,8 @@ int hs_decode_column(const hs_ctx* ctx, const hs_column* col, double* out);     
  * passed to any op at once: the library orders its streams behind the upload.  A host loop
  * "encode k+1, compute k, decode k, wait k-1" keeps the copy engines and the SMs busy together.
  * The library keeps the buffers a pending transfer uses alive until it has settled, so the
- * chunk handles may be released earlier.  One thread owns an hs_pending (wait / release are not
- * synchronised against each other).  Every hs_pending is released with hs_pending_release (which
+ * chunk handles may be released earlier.  One thread owns a pending transfer: wait and release are not
+ * synchronised against each other.  Every hs_pending is released with hs_pending_release (which
  * waits first if needed). */
 typedef struct hs_pending hs_pending;
 int hs_encode_column_async(hs_ctx* ctx, const double* v, uint64_t n, hs_ct** chunks_out,
